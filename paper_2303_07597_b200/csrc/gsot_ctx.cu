@@ -1,0 +1,1347 @@
+// gsot_ctx.cu — resident instance, evaluation pipeline, device-vector
+// L-BFGS driver and the C ABI of include/gsot.h.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "gsot_internal.cuh"
+
+namespace gsot {
+int config_features(int cfg, uint64_t seed, double* src, double* tgt, int32_t* sizes, double* a,
+                    double* b);
+int config_shape(int cfg, int64_t* m, int64_t* n, int32_t* L, int64_t* d);
+}  // namespace gsot
+
+using gsot::Error;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local gsot_error_detail g_detail{};
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    g_detail = gsot_error_detail{};
+    return GSOT_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_detail = e.detail;
+    g_detail.status = e.status;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    g_detail = gsot_error_detail{};
+    g_detail.status = GSOT_ERR_OUT_OF_MEMORY;
+    return GSOT_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_detail = gsot_error_detail{};
+    g_detail.status = GSOT_ERR_CUDA;
+    return GSOT_ERR_CUDA;
+  }
+}
+
+template <typename T>
+T* dalloc(size_t count, size_t* tally) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  GSOT_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * count));
+  if (tally) *tally += sizeof(T) * count;
+  return p;
+}
+
+void check_params(double gamma, double mu) {  // core.hpp:61-66
+  if (!(gamma > 0.0) || !std::isfinite(gamma))
+    throw Error(GSOT_ERR_INVALID_ARGUMENT, "gamma must be positive, got " + std::to_string(gamma));
+  if (!(mu > 0.0) || !std::isfinite(mu))
+    throw Error(GSOT_ERR_INVALID_ARGUMENT, "mu must be positive, got " + std::to_string(mu));
+}
+
+double compensated_sum(const double* v, int64_t n) {  // core.hpp:85-98
+  double sum = 0.0, comp = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double x = v[i];
+    const double t = sum + x;
+    if (std::abs(sum) >= std::abs(x))
+      comp += (sum - t) + x;
+    else
+      comp += (x - t) + sum;
+    sum = t;
+  }
+  return sum + comp;
+}
+
+void check_marginal(const double* v, int64_t n, char which) {  // core.hpp:100-112
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(v[i] >= 0.0) || !std::isfinite(v[i])) {
+      Error e(GSOT_ERR_MARGINAL_NOT_NORMALIZED,
+              std::string("marginal ") + which + ": entry " + std::to_string(i) + " = " +
+                  std::to_string(v[i]) + " is negative or non-finite");
+      e.detail.which = which;
+      e.detail.index = i;
+      throw e;
+    }
+  }
+  const double sum = compensated_sum(v, n);
+  if (std::abs(sum - 1.0) > 1e-12) {
+    Error e(GSOT_ERR_MARGINAL_NOT_NORMALIZED,
+            std::string("marginal ") + which + ": sum = " + std::to_string(sum) +
+                " differs from 1");
+    e.detail.which = which;
+    e.detail.index = -1;
+    throw e;
+  }
+}
+
+}  // namespace
+
+struct gsot_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t m = 0, n = 0, ldc = 0;
+  int32_t L = 0, nw = 0;
+  double gamma = 1.0, mu = 1.0;
+  std::vector<int32_t> sizes, off, poff;
+  size_t bytes = 0;
+
+  // resident instance
+  double* C = nullptr;
+  int32_t *d_off = nullptr, *d_poff = nullptr, *d_row_group = nullptr, *d_row_to_prow = nullptr;
+  double *d_sqrt_g = nullptr, *d_a = nullptr, *d_b = nullptr;
+  // evaluation buffers
+  double *x_eval = nullptr, *g_eval = nullptr;
+  double *rowpart = nullptr, *colpart = nullptr, *psi = nullptr, *psicol = nullptr;
+  double* partials = nullptr;
+  uint32_t *words = nullptr, *dense_words = nullptr;
+  int2 *tasks = nullptr, *dense_tasks = nullptr;
+  // screening state
+  double *snap_x = nullptr, *zs = nullptr, *ks = nullptr, *os = nullptr;
+  double *dpos = nullptr, *dfull = nullptr, *dneg = nullptr, *dbeta = nullptr;
+  uint32_t* active_words = nullptr;
+  int64_t active_count = 0;
+  bool have_snapshot = false;
+  // scalars
+  gsot::EvalScalars* sc = nullptr;
+  gsot::EvalScalars* h_sc = nullptr;  // pinned
+  int eval_grid = 148 * 4;
+  int red_blocks = 148 * 2;
+  // measurement
+  bool profile = false;
+  struct Mark {
+    cudaEvent_t a, b;
+    int kind;
+    double bytes;
+  };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  double prof_ms[gsot::K_NKINDS] = {};
+  double prof_bytes[gsot::K_NKINDS] = {};
+  int64_t prof_launches[gsot::K_NKINDS] = {};
+  int64_t launches = 0;
+
+  gsot::DevProblem problem() const {
+    gsot::DevProblem P;
+    P.C = C;
+    P.ldc = ldc;
+    P.m = m;
+    P.n = n;
+    P.L = L;
+    P.nw = nw;
+    P.off = d_off;
+    P.poff = d_poff;
+    P.row_group = d_row_group;
+    P.sqrt_g = d_sqrt_g;
+    P.a = d_a;
+    P.b = d_b;
+    P.gamma = gamma;
+    P.mu = mu;
+    P.tau = mu * gamma;
+    return P;
+  }
+
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    GSOT_CUDA_CHECK(cudaEventCreate(&e));
+    return e;
+  }
+  // Bracket a launch with events when profiling; always count launches.
+  template <typename F>
+  void launch(int kind, double bytes_alg, F&& f) {
+    ++launches;
+    if (!profile) {
+      f();
+      GSOT_CUDA_CHECK(cudaGetLastError());
+      return;
+    }
+    Mark mk{take_event(), take_event(), kind, bytes_alg};
+    GSOT_CUDA_CHECK(cudaEventRecord(mk.a, stream));
+    f();
+    GSOT_CUDA_CHECK(cudaGetLastError());
+    GSOT_CUDA_CHECK(cudaEventRecord(mk.b, stream));
+    marks.push_back(mk);
+  }
+  void collect_marks() {
+    if (marks.empty()) return;
+    GSOT_CUDA_CHECK(cudaStreamSynchronize(stream));
+    for (auto& mk : marks) {
+      float ms = 0.f;
+      GSOT_CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
+      prof_ms[mk.kind] += ms;
+      prof_bytes[mk.kind] += mk.bytes;
+      prof_launches[mk.kind] += 1;
+      event_pool.push_back(mk.a);
+      event_pool.push_back(mk.b);
+    }
+    marks.clear();
+  }
+
+  void sync() { GSOT_CUDA_CHECK(cudaStreamSynchronize(stream)); }
+  void fetch_scalars() {
+    GSOT_CUDA_CHECK(
+        cudaMemcpyAsync(h_sc, sc, sizeof(gsot::EvalScalars), cudaMemcpyDeviceToHost, stream));
+    sync();
+  }
+  void reset_scalars() {
+    GSOT_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(gsot::EvalScalars), stream));
+  }
+
+  ~gsot_ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& mk : marks) {
+      cudaEventDestroy(mk.a);
+      cudaEventDestroy(mk.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    void* ptrs[] = {C,        d_off,        d_poff,     d_row_group, d_row_to_prow, d_sqrt_g,
+                    d_a,      d_b,          x_eval,     g_eval,      rowpart,       colpart,
+                    psi,      psicol,       partials,   words,       dense_words,   tasks,
+                    dense_tasks, snap_x,    zs,         ks,          os,            dpos,
+                    dfull,    dneg,         dbeta,      active_words, sc};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (h_sc) cudaFreeHost(h_sc);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// Partition + RegParams checks in the reference's constructor order
+// (GroupPartition core.hpp:19-30, then RegParams :61-66), then layout.
+void setup_shape(gsot_ctx* c, int64_t m, int64_t n, const int32_t* sizes, int32_t L, double gamma,
+                 double mu) {
+  if (L < 1 || sizes == nullptr) throw Error(GSOT_ERR_PARTITION_MISMATCH, "group partition: at least one group required");
+  for (int32_t l = 0; l < L; ++l)
+    if (sizes[l] < 1)
+      throw Error(GSOT_ERR_PARTITION_MISMATCH,
+                  "group partition: group " + std::to_string(l) + " has non-positive size " +
+                      std::to_string(sizes[l]));
+  check_params(gamma, mu);
+  if (m < 1 || n < 1)
+    throw Error(GSOT_ERR_DIMENSION_MISMATCH, "dimension mismatch: empty cost matrix");
+  c->m = m;
+  c->n = n;
+  c->L = L;
+  c->gamma = gamma;
+  c->mu = mu;
+  c->nw = static_cast<int32_t>((n + 31) / 32);
+  c->sizes.assign(sizes, sizes + L);
+  c->off.assign(static_cast<size_t>(L) + 1, 0);
+  c->poff.assign(static_cast<size_t>(L) + 1, 0);
+  for (int32_t l = 0; l < L; ++l) {
+    c->off[l + 1] = c->off[l] + sizes[l];
+    c->poff[l + 1] = c->poff[l] + ((sizes[l] + 3) / 4) * 4;
+  }
+  c->ldc = c->poff[L];
+}
+
+void init_device(gsot_ctx* c) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    throw Error(GSOT_ERR_CUDA, "no CUDA device available (libgsot has no CPU fallback)");
+  GSOT_CUDA_CHECK(cudaGetDevice(&c->device));
+  GSOT_CUDA_CHECK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  GSOT_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->red_blocks = c->num_sms * 2;
+}
+
+void alloc_buffers(gsot_ctx* c) {
+  size_t* t = &c->bytes;
+  const int64_t m = c->m, n = c->n, L = c->L, nw = c->nw, dim = m + n;
+  c->C = dalloc<double>(static_cast<size_t>(c->ldc) * n, t);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->C, 0, sizeof(double) * static_cast<size_t>(c->ldc) * n, c->stream));
+  c->d_off = dalloc<int32_t>(L + 1, t);
+  c->d_poff = dalloc<int32_t>(L + 1, t);
+  c->d_row_group = dalloc<int32_t>(m, t);
+  c->d_row_to_prow = dalloc<int32_t>(m, t);
+  c->d_sqrt_g = dalloc<double>(L, t);
+  c->d_a = dalloc<double>(m, t);
+  c->d_b = dalloc<double>(n, t);
+  c->x_eval = dalloc<double>(dim + 8, t);
+  c->g_eval = dalloc<double>(dim + 8, t);
+  c->rowpart = dalloc<double>(static_cast<size_t>(nw) * m, t);
+  c->colpart = dalloc<double>(static_cast<size_t>(L) * n, t);
+  c->psi = dalloc<double>(static_cast<size_t>(L) * n, t);
+  c->psicol = dalloc<double>(n, t);
+  c->partials = dalloc<double>(static_cast<size_t>(c->red_blocks) * 4 + 64, t);
+  c->words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
+  c->dense_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
+  c->tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
+  c->dense_tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
+  c->snap_x = dalloc<double>(dim + 8, t);
+  c->zs = dalloc<double>(static_cast<size_t>(L) * n, t);
+  c->ks = dalloc<double>(static_cast<size_t>(L) * n, t);
+  c->os = dalloc<double>(static_cast<size_t>(L) * n, t);
+  c->dpos = dalloc<double>(L, t);
+  c->dfull = dalloc<double>(L, t);
+  c->dneg = dalloc<double>(L, t);
+  c->dbeta = dalloc<double>(n, t);
+  c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
+  c->sc = dalloc<gsot::EvalScalars>(1, t);
+  GSOT_CUDA_CHECK(cudaMallocHost(&c->h_sc, sizeof(gsot::EvalScalars)));
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->sc, 0, sizeof(gsot::EvalScalars), c->stream));
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->x_eval, 0, sizeof(double) * (dim + 8), c->stream));
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_x, 0, sizeof(double) * (dim + 8), c->stream));
+
+  std::vector<int32_t> row_group(static_cast<size_t>(m)), row_to_prow(static_cast<size_t>(m));
+  std::vector<double> sqrt_g(static_cast<size_t>(L));
+  for (int32_t l = 0; l < L; ++l) {
+    sqrt_g[l] = std::sqrt(static_cast<double>(c->sizes[l]));  // screening.hpp:79
+    for (int32_t r = 0; r < c->sizes[l]; ++r) {
+      row_group[c->off[l] + r] = l;
+      row_to_prow[c->off[l] + r] = c->poff[l] + r;
+    }
+  }
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_off, c->off.data(), sizeof(int32_t) * (L + 1),
+                                  cudaMemcpyHostToDevice, c->stream));
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_poff, c->poff.data(), sizeof(int32_t) * (L + 1),
+                                  cudaMemcpyHostToDevice, c->stream));
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_row_group, row_group.data(), sizeof(int32_t) * m,
+                                  cudaMemcpyHostToDevice, c->stream));
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_row_to_prow, row_to_prow.data(), sizeof(int32_t) * m,
+                                  cudaMemcpyHostToDevice, c->stream));
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_sqrt_g, sqrt_g.data(), sizeof(double) * L,
+                                  cudaMemcpyHostToDevice, c->stream));
+  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_words(c->dense_words, c->L, c->nw, c->n, c->stream); });
+  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->dense_tasks, c->L, c->nw, c->stream); });
+  // Persistent eval grid: every SM filled to the kernel's occupancy.
+  c->eval_grid = c->num_sms * std::max(1, gsot::eval_blocks_per_sm());
+  c->sync();
+}
+
+void set_marginals(gsot_ctx* c, const double* a, const double* b) {
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_a, a, sizeof(double) * c->m, cudaMemcpyHostToDevice, c->stream));
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_b, b, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+}
+
+// validate_instance (core.hpp:117-139) order: cost scan (first offender in
+// j-major order, computed on device during the upload), a, b, partition.
+void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const double* a,
+                       const double* b, const double* d_src_for_value) {
+  unsigned long long first_bad = 0;
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(&first_bad, d_first_bad, sizeof(first_bad),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (first_bad != ~0ull) {
+    const int64_t row = static_cast<int64_t>(first_bad % static_cast<unsigned long long>(c->m));
+    const int64_t col = static_cast<int64_t>(first_bad / static_cast<unsigned long long>(c->m));
+    double value = 0.0;
+    const int64_t prow = c->poff[0];
+    (void)prow;
+    int32_t l = 0;
+    while (c->off[l + 1] <= row) ++l;
+    GSOT_CUDA_CHECK(cudaMemcpy(&value, c->C + col * c->ldc + c->poff[l] + (row - c->off[l]),
+                               sizeof(double), cudaMemcpyDeviceToHost));
+    (void)d_src_for_value;
+    Error e(GSOT_ERR_NEGATIVE_COST, "cost(" + std::to_string(row) + "," + std::to_string(col) +
+                                        ") = " + std::to_string(value) +
+                                        " is negative or non-finite");
+    e.detail.row = row;
+    e.detail.col = col;
+    e.detail.value = value;
+    throw e;
+  }
+  check_marginal(a, c->m, 'a');
+  check_marginal(b, c->n, 'b');
+  if (c->off[c->L] != c->m)
+    throw Error(GSOT_ERR_PARTITION_MISMATCH,
+                "group partition: partition covers " + std::to_string(c->off[c->L]) +
+                    " indices, cost has " + std::to_string(c->m) + " rows");
+}
+
+gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int64_t n,
+                        const int32_t* sizes, int32_t L, const double* a, const double* b,
+                        double gamma, double mu) {
+  auto* c = new gsot_ctx();
+  try {
+    setup_shape(c, m, n, sizes, L, gamma, mu);
+    if (c->off[L] != m) {
+      // The reference checks the cover last (core.hpp:134-138) but the
+      // layout needs it; the scan order of the remaining checks is kept.
+      if (!cost_on_device && cost) {
+        for (int64_t j = 0; j < n; ++j)
+          for (int64_t i = 0; i < m; ++i) {
+            const double v = cost[i + j * m];
+            if (!(v >= 0.0) || !std::isfinite(v)) {
+              Error e(GSOT_ERR_NEGATIVE_COST, "cost(" + std::to_string(i) + "," +
+                                                  std::to_string(j) + ") = " +
+                                                  std::to_string(v) + " is negative or non-finite");
+              e.detail.row = i;
+              e.detail.col = j;
+              e.detail.value = v;
+              throw e;
+            }
+          }
+      }
+      check_marginal(a, m, 'a');
+      check_marginal(b, n, 'b');
+      throw Error(GSOT_ERR_PARTITION_MISMATCH,
+                  "group partition: partition covers " + std::to_string(c->off[L]) +
+                      " indices, cost has " + std::to_string(m) + " rows");
+    }
+    init_device(c);
+    alloc_buffers(c);
+    set_marginals(c, a, b);
+    unsigned long long* d_bad = nullptr;
+    GSOT_CUDA_CHECK(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    GSOT_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), c->stream));
+    // Upload in column chunks through a staging buffer (bounded extra HBM).
+    const int64_t chunk_cols =
+        std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(256) << 20) / (8 * m)));
+    double* staging = nullptr;
+    if (!cost_on_device) GSOT_CUDA_CHECK(cudaMalloc(&staging, sizeof(double) * m * chunk_cols));
+    for (int64_t j0 = 0; j0 < n; j0 += chunk_cols) {
+      const int64_t nc = std::min(chunk_cols, n - j0);
+      const double* src = nullptr;
+      if (cost_on_device) {
+        src = cost + j0 * m;
+      } else {
+        GSOT_CUDA_CHECK(cudaMemcpyAsync(staging, cost + j0 * m, sizeof(double) * m * nc,
+                                        cudaMemcpyHostToDevice, c->stream));
+        src = staging;
+      }
+      c->launch(gsot::K_MISC, 16.0 * m * nc, [&] {
+        gsot::launch_relayout(src, m, j0, nc, c->d_row_to_prow, c->ldc, c->C, d_bad, c->stream);
+      });
+    }
+    finish_validation(c, d_bad, a, b, nullptr);
+    if (staging) cudaFree(staging);
+    cudaFree(d_bad);
+    return c;
+  } catch (...) {
+    delete c;
+    throw;
+  }
+}
+
+// ------------------------------------------------------------------ eval
+
+struct EvalOut {
+  double objective = 0.0;
+  double slope = 0.0;
+  gsot_call_stats stats{};
+};
+
+// Fused evaluation at device state d_x (length m+n): writes d_grad,
+// returns objective, slope against d_dir (if non-null) and the per-call
+// counters. mode: GSOT_EVAL_DENSE / GSOT_EVAL_SCREENED.
+EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
+                    const double* d_dir, double ub_offset, bool use_active) {
+  if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
+    throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
+  const gsot::DevProblem P = c->problem();
+  c->reset_scalars();
+  const uint32_t* words = c->dense_words;
+  const int2* tasks = c->dense_tasks;
+  int max_tasks = c->L * c->nw;
+  const double Ln = static_cast<double>(c->L) * c->n;
+  if (mode == GSOT_EVAL_SCREENED) {
+    c->launch(gsot::K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
+      gsot::launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
+    });
+    c->launch(gsot::K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
+      gsot::launch_bounds(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
+                          ub_offset, c->words, c->tasks, c->sc, c->stream);
+    });
+    words = c->words;
+    tasks = c->tasks;
+  }
+  const double dense_bytes = 8.0 * c->m * c->n + 8.0 * c->m * c->nw + 16.0 * Ln;
+  c->launch(gsot::K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : 0.0, [&] {
+    gsot::launch_eval(P, d_x, tasks, mode == GSOT_EVAL_DENSE ? max_tasks : -1, words,
+                      c->rowpart, c->colpart, c->psi, c->sc, c->eval_grid, c->stream);
+  });
+  c->launch(gsot::K_FINALIZE, 0.0, [&] {
+    gsot::launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, c->psicol,
+                          c->stream);
+  });
+  c->launch(gsot::K_FINALIZE, 16.0 * (c->m + c->n), [&] {
+    gsot::launch_objective(P, d_x, c->psicol, d_grad, d_dir, c->partials, c->red_blocks, c->sc,
+                           c->stream);
+  });
+  c->fetch_scalars();
+  EvalOut o;
+  o.objective = c->h_sc->objective;
+  o.slope = c->h_sc->slope;
+  if (mode == GSOT_EVAL_SCREENED) {
+    o.stats.in_active = static_cast<int64_t>(c->h_sc->counters[0]);
+    o.stats.skipped = static_cast<int64_t>(c->h_sc->counters[1]);
+    o.stats.unskipped = static_cast<int64_t>(c->h_sc->counters[2]);
+    o.stats.upper_bounds = static_cast<int64_t>(c->h_sc->counters[3]);
+  } else {
+    o.stats.unskipped = static_cast<int64_t>(c->L) * c->n;  // solver.hpp:117-119
+  }
+  return o;
+}
+
+void snapshot_at(gsot_ctx* c, const double* d_x) {  // take_snapshot at device state
+  const gsot::DevProblem P = c->problem();
+  const double Ln = static_cast<double>(c->L) * c->n;
+  c->launch(gsot::K_SNAPSHOT, 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n), [&] {
+    gsot::launch_snapshot(P, d_x, c->zs, c->ks, c->os, c->stream);
+  });
+  if (d_x != c->snap_x)
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(c->snap_x, d_x, sizeof(double) * (c->m + c->n),
+                                    cudaMemcpyDeviceToDevice, c->stream));
+  c->have_snapshot = true;
+}
+
+void init_snapshot_device(gsot_ctx* c, const double* d_x) {  // screening.hpp:220-227
+  snapshot_at(c, d_x);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->active_words, 0,
+                                  sizeof(uint32_t) * static_cast<size_t>(c->L) * c->nw, c->stream));
+  c->active_count = 0;
+}
+
+void refresh_device(gsot_ctx* c, const double* d_x, bool use_active) {  // screening.hpp:231-235
+  if (!c->have_snapshot) throw Error(GSOT_ERR_STATE, "refresh requires a snapshot");
+  const gsot::DevProblem P = c->problem();
+  if (use_active) {
+    c->reset_scalars();
+    c->launch(gsot::K_DELTA, 16.0 * (c->m + c->n), [&] {
+      gsot::launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
+    });
+    c->launch(gsot::K_ACTIVE, 16.0 * c->L * c->n + 4.0 * c->L * c->nw, [&] {
+      gsot::launch_active(P, c->ks, c->os, c->dfull, c->dneg, c->dbeta, c->active_words, c->sc,
+                          c->stream);
+    });
+    c->fetch_scalars();
+    c->active_count = static_cast<int64_t>(c->h_sc->counters[0]);
+  }
+  snapshot_at(c, d_x);
+}
+
+// ------------------------------------------------------------------ L-BFGS
+
+struct Pt {  // lbfgs.hpp:40-46 with the vectors held by reference
+  double t = 0.0, value = 0.0, slope = 0.0;
+  int buf = -1;
+};
+
+class DeviceMaximizer {
+ public:
+  DeviceMaximizer(gsot_ctx* c, const gsot_solver_options& o, gsot_solve_result* res,
+                  int64_t* history, int64_t history_cap)
+      : c_(c), o_(o), res_(res), hist_(history), hist_cap_(history_cap) {
+    dim_ = c->m + c->n;
+    mem_ = std::max(1, std::min<int>(o.lbfgs_memory, gsot::kMaxMemory));
+    for (int i = 0; i < 6; ++i) {
+      Buf b;
+      b.x = dalloc<double>(dim_ + 8, &extra_);
+      b.g = dalloc<double>(dim_ + 8, &extra_);
+      pool_.push_back(b);
+    }
+    d_ = dalloc<double>(dim_ + 8, &extra_);
+    for (int i = 0; i <= mem_; ++i) {
+      S_.push_back(dalloc<double>(dim_, &extra_));
+      Y_.push_back(dalloc<double>(dim_, &extra_));
+      free_slots_.push_back(i);
+    }
+    tl_out_ = dalloc<double>(4, &extra_);
+    GSOT_CUDA_CHECK(cudaMallocHost(&h_tl_, sizeof(double) * 4));
+  }
+  ~DeviceMaximizer() {
+    for (auto& b : pool_) {
+      cudaFree(b.x);
+      cudaFree(b.g);
+    }
+    cudaFree(d_);
+    for (auto p : S_) cudaFree(p);
+    for (auto p : Y_) cudaFree(p);
+    cudaFree(tl_out_);
+    cudaFreeHost(h_tl_);
+  }
+
+  // Returns the final iterate buffer index.
+  void run(double* x_out) {
+    const bool screened = o_.mode != GSOT_MODE_BASELINE;
+    const bool use_active = o_.mode == GSOT_MODE_FAST || o_.mode == GSOT_MODE_AUDIT;
+    audit_ = o_.mode == GSOT_MODE_AUDIT;
+    use_active_ = use_active;
+    screened_ = screened;
+    // x0 = 0 (solver.hpp:123, :244)
+    res_buf_ = acquire();
+    GSOT_CUDA_CHECK(cudaMemsetAsync(pool_[res_buf_].x, 0, sizeof(double) * dim_, c_->stream));
+    if (screened) init_snapshot_device(c_, pool_[res_buf_].x);  // solver.hpp:143-144
+
+    const auto t0 = std::chrono::steady_clock::now();
+    maximize();
+    const auto t1 = std::chrono::steady_clock::now();
+    res_->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (x_out)
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(x_out, pool_[res_buf_].x, sizeof(double) * dim_,
+                                      cudaMemcpyDeviceToHost, c_->stream));
+    c_->sync();
+    res_->objective = res_value_;  // == dual_objective(x*) (screened == dense bitwise)
+    res_->outer_loops = res_->chunks;
+  }
+
+ private:
+  struct Buf {
+    double* x;
+    double* g;
+    int refs = 0;
+  };
+
+  int acquire() {
+    for (size_t i = 0; i < pool_.size(); ++i)
+      if (pool_[i].refs == 0) {
+        pool_[i].refs = 1;
+        return static_cast<int>(i);
+      }
+    Buf b;
+    b.x = dalloc<double>(dim_ + 8, &extra_);
+    b.g = dalloc<double>(dim_ + 8, &extra_);
+    b.refs = 1;
+    pool_.push_back(b);
+    return static_cast<int>(pool_.size() - 1);
+  }
+  void release(int b) {
+    if (b >= 0) --pool_[b].refs;
+  }
+  void assign(Pt& dst, const Pt& src) {
+    if (&dst == &src) return;
+    if (src.buf >= 0) ++pool_[src.buf].refs;
+    release(dst.buf);
+    dst = src;
+  }
+
+  // One objective+gradient evaluation (the fused pair of ObjectiveFn and
+  // GradientFn, solver.hpp:161-210), with the GradStats bookkeeping.
+  gsot::EvalScalars dummy_{};
+  EvalOut evaluate(const double* d_x, double* d_g, const double* d_dir) {
+    const int mode = screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE;
+    EvalOut e = eval_device(c_, d_x, mode, d_g, d_dir, o_.upper_bound_offset, use_active_);
+    if (audit_) audit_call(d_x, d_g, e);
+    const int64_t row = res_->grad_calls;
+    if (hist_ && row < hist_cap_) {
+      hist_[row * 4 + 0] = e.stats.in_active;
+      hist_[row * 4 + 1] = e.stats.skipped;
+      hist_[row * 4 + 2] = e.stats.unskipped;
+      hist_[row * 4 + 3] = e.stats.upper_bounds;
+    }
+    res_->blocks_in_active_set += e.stats.in_active;
+    res_->blocks_skipped += e.stats.skipped;
+    res_->blocks_unskipped += e.stats.unskipped;
+    res_->upper_bounds_evaluated += e.stats.upper_bounds;
+    ++res_->grad_calls;
+    return e;
+  }
+
+  // audit_solve per gradient call (solver.hpp:172-201): every skipped block
+  // is recomputed and must be zero; the screened gradient and objective
+  // must equal the unscreened ones bitwise.
+  void audit_call(const double* d_x, const double* d_g, const EvalOut& e) {
+    const gsot::DevProblem P = c_->problem();
+    const uint32_t* words = c_->words;
+    c_->reset_scalars();
+    c_->launch(gsot::K_MISC, 0.0, [&] {
+      gsot::launch_audit_skips(P, d_x, words, c_->active_words, c_->sc, c_->stream);
+    });
+    c_->fetch_scalars();
+    res_->audit_skip_checks += static_cast<int64_t>(c_->h_sc->counters[0]);
+    if (c_->h_sc->audit_violation) {
+      const long long w = c_->h_sc->audit_where;
+      throw Error(GSOT_ERR_AUDIT_VIOLATION,
+                  "audit violation: skipped block (l=" + std::to_string(w / c_->n) +
+                      ", j=" + std::to_string(w % c_->n) + ") has nonzero exact gradient at call " +
+                      std::to_string(res_->grad_calls));
+    }
+    // Recompute the whole gradient unscreened and compare bitwise. The
+    // screen must not change the words/tasks used by the screened call, so
+    // the comparison runs after the skip check.
+    if (!audit_g_) audit_g_ = dalloc<double>(dim_ + 8, &extra_);
+    EvalOut d = eval_device(c_, d_x, GSOT_EVAL_DENSE, audit_g_, nullptr, 0.0, false);
+    std::vector<double> a(static_cast<size_t>(dim_)), b(static_cast<size_t>(dim_));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(a.data(), d_g, sizeof(double) * dim_, cudaMemcpyDeviceToHost, c_->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(b.data(), audit_g_, sizeof(double) * dim_, cudaMemcpyDeviceToHost, c_->stream));
+    c_->sync();
+    res_->audit_column_compares += c_->n;
+    if (memcmp(a.data(), b.data(), sizeof(double) * dim_) != 0 || d.objective != e.objective) {
+      throw Error(GSOT_ERR_AUDIT_VIOLATION,
+                  "audit violation: screened gradient differs from plain gradient at call " +
+                      std::to_string(res_->grad_calls));
+    }
+    ++res_->audit_gradient_calls;
+  }
+
+  void hook(const double* d_x) {  // solver.hpp:212-241
+    if (!screened_) return;
+    refresh_device(c_, d_x, use_active_);
+    if (audit_ && use_active_) {
+      const gsot::DevProblem P = c_->problem();
+      c_->reset_scalars();
+      c_->launch(gsot::K_MISC, 0.0, [&] {
+        gsot::launch_audit_active(P, d_x, c_->active_words, c_->sc, c_->stream);
+      });
+      c_->fetch_scalars();
+      res_->audit_active_checks += static_cast<int64_t>(c_->h_sc->counters[1]);
+      if (c_->h_sc->audit_violation) {
+        const long long w = c_->h_sc->audit_where;
+        throw Error(GSOT_ERR_AUDIT_VIOLATION,
+                    "audit violation: active-set block (l=" + std::to_string(w / c_->n) +
+                        ", j=" + std::to_string(w % c_->n) + ") has zero exact gradient at build time");
+      }
+    }
+  }
+
+  void eval_at(double t, Pt& p) {  // lbfgs.hpp:84-90
+    if (p.buf < 0 || pool_[p.buf].refs > 1) {
+      release(p.buf);
+      p.buf = acquire();
+    }
+    p.t = t;
+    double* xt = pool_[p.buf].x;
+    c_->launch(gsot::K_LBFGS, 24.0 * dim_, [&] {
+      gsot::launch_axpy_point(pool_[res_buf_].x, t, d_, xt, dim_, c_->stream);
+    });
+    EvalOut e = evaluate(xt, pool_[p.buf].g, d_);
+    p.value = e.objective;
+    p.slope = e.slope;
+  }
+
+  double norm_inf(const double* v) {  // lpNorm<Infinity> (lbfgs.hpp:264): exact in any order
+    c_->reset_scalars();
+    c_->launch(gsot::K_LBFGS, 8.0 * dim_, [&] {
+      gsot::launch_absmax(v, dim_, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
+    });
+    c_->fetch_scalars();
+    return c_->h_sc->extra[0];
+  }
+
+  double dot_host(const double* a, const double* b) {
+    c_->reset_scalars();
+    c_->launch(gsot::K_LBFGS, 16.0 * dim_, [&] {
+      gsot::launch_dot(a, b, dim_, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
+    });
+    c_->fetch_scalars();
+    return c_->h_sc->extra[0];
+  }
+
+  void clear_history() {
+    for (int s : order_) free_slots_.push_back(s);
+    order_.clear();
+    rho_.clear();
+    sy_.clear();
+    yy_.clear();
+  }
+
+  void maximize() {  // lbfgs.hpp:61-274
+    const double c1 = 1e-4, c2 = 0.9;  // MaximizeOptions defaults (lbfgs.hpp:16-17)
+    const int max_bracket = 40, max_zoom = 12;
+    // initial gradient + objective (lbfgs.hpp:70-71), one fused evaluation
+    {
+      EvalOut e = evaluate(pool_[res_buf_].x, pool_[res_buf_].g, nullptr);
+      res_value_ = e.objective;
+    }
+    bool stalled = false, zero_gradient = false;
+    Pt trial, lo, prev;
+    for (int chunk = 0; chunk < o_.max_outer_loops && !stalled && !zero_gradient; ++chunk) {
+      ++res_->chunks;
+      for (int it = 0; it < o_.snapshot_interval; ++it) {
+        bool accepted = false;
+        for (int attempt = 0; attempt < 2 && !accepted; ++attempt) {
+          if (attempt == 1) {
+            if (order_.empty()) break;
+            clear_history();
+          }
+          // two-loop recursion (lbfgs.hpp:109-124) in one cluster launch
+          gsot::TwoLoopArgs A{};
+          const int k = static_cast<int>(order_.size());
+          for (int i = 0; i < k; ++i) {
+            A.s[i] = S_[order_[i]];
+            A.y[i] = Y_[order_[i]];
+            A.rho[i] = rho_[i];
+          }
+          A.k = k;
+          A.apply_scale = 0;
+          A.gamma_scale = 1.0;
+          if (k > 0 && yy_.back() > 0.0) {
+            A.apply_scale = 1;
+            A.gamma_scale = sy_.back() / yy_.back();
+          }
+          A.g = pool_[res_buf_].g;
+          A.d = d_;
+          A.dim = dim_;
+          A.out = tl_out_;
+          c_->launch(gsot::K_LBFGS, 8.0 * dim_ * (4.0 * k + 4.0), [&] {
+            gsot::launch_two_loop(A, c_->stream);
+          });
+          GSOT_CUDA_CHECK(cudaMemcpyAsync(h_tl_, tl_out_, sizeof(double) * 2,
+                                          cudaMemcpyDeviceToHost, c_->stream));
+          c_->sync();
+          double dir_slope = h_tl_[0];
+          double dd = h_tl_[1];
+          if (!(dir_slope > 0.0)) {  // lbfgs.hpp:127-137
+            clear_history();
+            GSOT_CUDA_CHECK(cudaMemcpyAsync(d_, pool_[res_buf_].g, sizeof(double) * dim_,
+                                            cudaMemcpyDeviceToDevice, c_->stream));
+            dir_slope = dot_host(pool_[res_buf_].g, pool_[res_buf_].g);
+            dd = dir_slope;
+            if (dir_slope == 0.0) {
+              zero_gradient = true;
+              break;
+            }
+          }
+          const double f0 = res_value_;
+          const double armijo = c1 * dir_slope;
+          auto sufficient = [&](const Pt& p) { return p.value >= f0 + armijo * p.t; };
+          auto curvature_ok = [&](const Pt& p) { return std::abs(p.slope) <= c2 * dir_slope; };
+
+          double t_init = 1.0;  // lbfgs.hpp:150-154
+          if (res_->iterations == 0) {
+            const double dnorm = std::sqrt(dd);
+            if (dnorm > 0.0) t_init = 1.0 / dnorm;
+          }
+          bool have_bracket = false;
+          Pt lo0;
+          lo0.t = 0.0;
+          lo0.value = f0;
+          lo0.slope = dir_slope;
+          assign(lo, lo0);
+          double hi_t = 0.0;
+          double t = t_init;
+          assign(prev, lo);
+          for (int i = 0; i < max_bracket; ++i) {  // lbfgs.hpp:165-187
+            eval_at(t, trial);
+            if (!sufficient(trial) || (i > 0 && trial.value <= prev.value)) {
+              assign(lo, prev);
+              hi_t = trial.t;
+              have_bracket = true;
+              break;
+            }
+            if (curvature_ok(trial)) {
+              accepted = true;
+              break;
+            }
+            if (trial.slope <= 0.0) {
+              assign(lo, trial);
+              hi_t = prev.t;
+              have_bracket = true;
+              break;
+            }
+            assign(prev, trial);
+            t *= 2.0;
+          }
+          if (!accepted && have_bracket) {  // lbfgs.hpp:189-231
+            double hi_value = std::numeric_limits<double>::quiet_NaN();
+            for (int i = 0; i < max_zoom; ++i) {
+              double cand = 0.5 * (lo.t + hi_t);
+              if (std::isfinite(hi_value)) {
+                const double dt = hi_t - lo.t;
+                const double denom = 2.0 * (lo.value + lo.slope * dt - hi_value);
+                if (denom != 0.0) {
+                  const double interp = lo.t + lo.slope * dt * dt / denom;
+                  const double lo_guard = lo.t + 0.1 * dt;
+                  const double hi_guard = hi_t - 0.1 * dt;
+                  const double lim_min = std::min(lo_guard, hi_guard);
+                  const double lim_max = std::max(lo_guard, hi_guard);
+                  if (interp >= lim_min && interp <= lim_max) cand = interp;
+                }
+              }
+              if (cand == lo.t || cand == hi_t) break;
+              eval_at(cand, trial);
+              if (!sufficient(trial) || trial.value <= lo.value) {
+                hi_t = cand;
+                hi_value = trial.value;
+                continue;
+              }
+              if (curvature_ok(trial)) {
+                accepted = true;
+                break;
+              }
+              if (trial.slope * (hi_t - lo.t) <= 0.0) {
+                hi_t = lo.t;
+                hi_value = lo.value;
+              }
+              assign(lo, trial);
+            }
+            if (!accepted && lo.t > 0.0) {
+              assign(trial, lo);
+              accepted = true;
+            }
+          }
+          if (!accepted && !have_bracket && prev.t > 0.0) {
+            assign(trial, prev);
+            accepted = true;
+          }
+        }
+        if (zero_gradient) break;
+        if (!accepted) {
+          stalled = true;
+          break;
+        }
+        // curvature pair (lbfgs.hpp:243-255)
+        const int slot = free_slots_.back();
+        c_->reset_scalars();
+        c_->launch(gsot::K_LBFGS, 8.0 * dim_ * 6.0, [&] {
+          gsot::launch_pair(pool_[trial.buf].x, pool_[res_buf_].x, pool_[res_buf_].g,
+                            pool_[trial.buf].g, S_[slot], Y_[slot], dim_, c_->partials,
+                            c_->red_blocks, c_->sc, c_->stream);
+        });
+        c_->fetch_scalars();
+        const double sy = c_->h_sc->extra[0];
+        const double ss = c_->h_sc->extra[1];
+        const double yy = c_->h_sc->extra[2];
+        if (sy > 1e-10 * std::sqrt(ss) * std::sqrt(yy)) {
+          free_slots_.pop_back();
+          if (static_cast<int>(order_.size()) == mem_) {
+            free_slots_.push_back(order_.front());
+            order_.pop_front();
+            rho_.pop_front();
+            sy_.pop_front();
+            yy_.pop_front();
+          }
+          order_.push_back(slot);
+          rho_.push_back(1.0 / sy);
+          sy_.push_back(sy);
+          yy_.push_back(yy);
+        }
+        // res.x = trial.x; res.gradient = trial.grad (share the buffer)
+        ++pool_[trial.buf].refs;
+        release(res_buf_);
+        res_buf_ = trial.buf;
+        res_value_ = trial.value;
+        ++res_->iterations;
+      }
+      if (stalled) break;
+      hook(pool_[res_buf_].x);
+      if (norm_inf(pool_[res_buf_].g) <= o_.grad_tol) {
+        res_->converged = 1;
+        break;
+      }
+    }
+    if (!res_->converged) res_->converged = norm_inf(pool_[res_buf_].g) <= o_.grad_tol;
+    res_->line_search_failed = stalled && !res_->converged;
+    release(trial.buf);
+    release(lo.buf);
+    release(prev.buf);
+  }
+
+  gsot_ctx* c_;
+  gsot_solver_options o_;
+  gsot_solve_result* res_;
+  int64_t* hist_;
+  int64_t hist_cap_;
+  int64_t dim_ = 0;
+  int mem_ = 10;
+  size_t extra_ = 0;
+  std::vector<Buf> pool_;
+  double* d_ = nullptr;
+  std::vector<double*> S_, Y_;
+  std::deque<int> order_;
+  std::vector<int> free_slots_;
+  std::deque<double> rho_, sy_, yy_;
+  double* tl_out_ = nullptr;
+  double* h_tl_ = nullptr;
+  double* audit_g_ = nullptr;
+  int res_buf_ = -1;
+  double res_value_ = 0.0;
+  bool audit_ = false, use_active_ = false, screened_ = false;
+};
+
+gsot_ctx* checked(gsot_ctx* c) {
+  if (!c) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null context");
+  return c;
+}
+
+void upload_x(gsot_ctx* c, const double* x) {
+  if (!x) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null state");
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->x_eval, x, sizeof(double) * (c->m + c->n),
+                                  cudaMemcpyHostToDevice, c->stream));
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+GSOT_API const char* gsot_last_error(void) { return g_err.c_str(); }
+
+GSOT_API int gsot_last_error_detail(gsot_error_detail* out) {
+  if (out) *out = g_detail;
+  return GSOT_OK;
+}
+
+GSOT_API const char* gsot_version(void) { return "gsot-b200 0.1 (sm_100a)"; }
+
+GSOT_API int gsot_params_from_rho(double gamma, double rho, double* gamma_eff, double* mu_eff) {
+  return guard([&] {
+    if (!(rho > 0.0) || !(rho < 1.0))  // core.hpp:148-151
+      throw Error(GSOT_ERR_RHO_OUT_OF_RANGE,
+                  "rho = " + std::to_string(rho) + " is outside the open interval (0,1)");
+    const double g = gamma * (1.0 - rho), mu = rho / (1.0 - rho);
+    check_params(g, mu);
+    if (gamma_eff) *gamma_eff = g;
+    if (mu_eff) *mu_eff = mu;
+  });
+}
+
+GSOT_API int gsot_create(const double* cost, int64_t m, int64_t n, const int32_t* group_sizes,
+                         int32_t L, const double* a, const double* b, double gamma, double mu,
+                         gsot_ctx** out) {
+  return guard([&] {
+    if (!out || !cost || !a || !b) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    *out = create_common(cost, false, m, n, group_sizes, L, a, b, gamma, mu);
+  });
+}
+
+GSOT_API int gsot_create_device(const double* d_cost, int64_t m, int64_t n,
+                                const int32_t* group_sizes, int32_t L, const double* a,
+                                const double* b, double gamma, double mu, gsot_ctx** out) {
+  return guard([&] {
+    if (!out || !d_cost || !a || !b) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    *out = create_common(d_cost, true, m, n, group_sizes, L, a, b, gamma, mu);
+  });
+}
+
+GSOT_API void gsot_destroy(gsot_ctx* ctx) { delete ctx; }
+
+GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu) {
+  return guard([&] {
+    checked(ctx);
+    check_params(gamma, mu);
+    ctx->gamma = gamma;
+    ctx->mu = mu;
+  });
+}
+
+GSOT_API int gsot_shape(const gsot_ctx* ctx, int64_t* m, int64_t* n, int32_t* L,
+                        int64_t* device_bytes) {
+  return guard([&] {
+    if (!ctx) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null context");
+    if (m) *m = ctx->m;
+    if (n) *n = ctx->n;
+    if (L) *L = ctx->L;
+    if (device_bytes) *device_bytes = static_cast<int64_t>(ctx->bytes);
+  });
+}
+
+GSOT_API int gsot_eval(gsot_ctx* ctx, const double* x, int mode, double* objective, double* grad,
+                       gsot_call_stats* stats) {
+  return guard([&] {
+    checked(ctx);
+    if (mode != GSOT_EVAL_DENSE && mode != GSOT_EVAL_SCREENED)
+      throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
+    upload_x(ctx, x);
+    EvalOut e = eval_device(ctx, ctx->x_eval, mode, ctx->g_eval, nullptr, 0.0, true);
+    if (grad) {
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(grad, ctx->g_eval, sizeof(double) * (ctx->m + ctx->n),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+    }
+    if (objective) *objective = e.objective;
+    if (stats) *stats = e.stats;
+  });
+}
+
+GSOT_API int gsot_eval_device(gsot_ctx* ctx, const double* d_x, int mode, double* objective,
+                              double* d_grad, gsot_call_stats* stats) {
+  return guard([&] {
+    checked(ctx);
+    if (!d_x || !d_grad) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null device pointer");
+    if (mode != GSOT_EVAL_DENSE && mode != GSOT_EVAL_SCREENED)
+      throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(ctx->x_eval, d_x, sizeof(double) * (ctx->m + ctx->n),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+    EvalOut e = eval_device(ctx, ctx->x_eval, mode, d_grad, nullptr, 0.0, true);
+    if (objective) *objective = e.objective;
+    if (stats) *stats = e.stats;
+  });
+}
+
+GSOT_API int gsot_init_snapshot(gsot_ctx* ctx, const double* x) {
+  return guard([&] {
+    checked(ctx);
+    upload_x(ctx, x);
+    init_snapshot_device(ctx, ctx->x_eval);
+    ctx->sync();
+  });
+}
+
+GSOT_API int gsot_refresh(gsot_ctx* ctx, const double* x, int use_active_set) {
+  return guard([&] {
+    checked(ctx);
+    upload_x(ctx, x);
+    refresh_device(ctx, ctx->x_eval, use_active_set != 0);
+    ctx->sync();
+  });
+}
+
+GSOT_API int gsot_snapshot_norms(gsot_ctx* ctx, double* z, double* k, double* o) {
+  return guard([&] {
+    checked(ctx);
+    if (!ctx->have_snapshot) throw Error(GSOT_ERR_STATE, "no snapshot taken");
+    const int64_t Ln = static_cast<int64_t>(ctx->L) * ctx->n;
+    std::vector<double> tmp(static_cast<size_t>(Ln));
+    double* srcs[3] = {ctx->zs, ctx->ks, ctx->os};
+    double* dsts[3] = {z, k, o};
+    for (int q = 0; q < 3; ++q) {
+      if (!dsts[q]) continue;
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), srcs[q], sizeof(double) * Ln,
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      for (int32_t l = 0; l < ctx->L; ++l)
+        for (int64_t j = 0; j < ctx->n; ++j) dsts[q][l + j * ctx->L] = tmp[l * ctx->n + j];
+    }
+  });
+}
+
+GSOT_API int gsot_active_set(gsot_ctx* ctx, uint8_t* member, int64_t* count) {
+  return guard([&] {
+    checked(ctx);
+    if (count) *count = ctx->active_count;
+    if (!member) return;
+    const int64_t nwords = static_cast<int64_t>(ctx->L) * ctx->nw;
+    std::vector<uint32_t> w(static_cast<size_t>(nwords));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(w.data(), ctx->active_words, sizeof(uint32_t) * nwords,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int32_t l = 0; l < ctx->L; ++l)
+      for (int64_t j = 0; j < ctx->n; ++j)
+        member[l + j * ctx->L] = (w[l * ctx->nw + (j >> 5)] >> (j & 31)) & 1u;
+  });
+}
+
+GSOT_API int gsot_block_mask(gsot_ctx* ctx, const double* x, uint8_t* nonzero) {
+  return guard([&] {
+    checked(ctx);
+    if (!nonzero) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null output");
+    upload_x(ctx, x);
+    const gsot::DevProblem P = ctx->problem();
+    // reuse colpart as scratch for the per-block z
+    ctx->launch(gsot::K_MISC, 8.0 * ctx->m * ctx->n,
+                [&] { gsot::launch_block_z(P, ctx->x_eval, ctx->colpart, ctx->stream); });
+    const int64_t Ln = static_cast<int64_t>(ctx->L) * ctx->n;
+    std::vector<double> z(static_cast<size_t>(Ln));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(z.data(), ctx->colpart, sizeof(double) * Ln,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    const double tau = ctx->mu * ctx->gamma;
+    for (int32_t l = 0; l < ctx->L; ++l)
+      for (int64_t j = 0; j < ctx->n; ++j) nonzero[l + j * ctx->L] = z[l * ctx->n + j] > tau;
+  });
+}
+
+GSOT_API int gsot_plan_columns(gsot_ctx* ctx, const double* x, int64_t j0, int64_t j1,
+                               double* out) {
+  return guard([&] {
+    checked(ctx);
+    if (j0 < 0 || j1 > ctx->n || j0 > j1)
+      throw Error(GSOT_ERR_DIMENSION_MISMATCH, "dimension mismatch: column range");
+    if (!out) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null output");
+    upload_x(ctx, x);
+    const gsot::DevProblem P = ctx->problem();
+    // Stream through rowpart (nw * m doubles) as scratch: nw columns a step.
+    const int64_t step = std::max<int64_t>(1, ctx->nw);
+    for (int64_t a = j0; a < j1; a += step) {
+      const int64_t nc = std::min(step, j1 - a);
+      ctx->launch(gsot::K_MISC, 16.0 * ctx->m * nc, [&] {
+        gsot::launch_plan_columns(P, ctx->x_eval, a, nc, ctx->rowpart, ctx->stream);
+      });
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(out + (a - j0) * ctx->m, ctx->rowpart,
+                                      sizeof(double) * ctx->m * nc, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+    }
+    ctx->sync();
+  });
+}
+
+GSOT_API void gsot_default_solver_options(gsot_solver_options* o) {
+  if (!o) return;
+  o->snapshot_interval = 10;  // solver.hpp:26-30
+  o->grad_tol = 1e-6;
+  o->max_outer_loops = 200;
+  o->lbfgs_memory = 10;
+  o->mode = GSOT_MODE_FAST;
+  o->upper_bound_offset = 0.0;
+}
+
+GSOT_API int gsot_solve(gsot_ctx* ctx, const gsot_solver_options* opts, double* x_out,
+                        gsot_solve_result* result, int64_t* history, int64_t history_cap) {
+  return guard([&] {
+    checked(ctx);
+    gsot_solver_options o;
+    gsot_default_solver_options(&o);
+    if (opts) o = *opts;
+    if (o.mode < 0 || o.mode > 3) throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown solver mode");
+    if (o.lbfgs_memory > gsot::kMaxMemory)
+      throw Error(GSOT_ERR_INVALID_ARGUMENT, "lbfgs_memory above the supported maximum");
+    gsot_solve_result r{};
+    DeviceMaximizer dm(ctx, o, &r, history, history_cap);
+    dm.run(x_out);
+    if (result) *result = r;
+  });
+}
+
+GSOT_API int gsot_config_shape(int32_t cfg, int64_t* m, int64_t* n, int32_t* L, int64_t* d) {
+  return guard([&] { gsot::config_shape(cfg, m, n, L, d); });
+}
+
+GSOT_API int gsot_config_features(int32_t cfg, uint64_t seed, double* src, double* tgt,
+                                  int32_t* sizes, double* a, double* b) {
+  return guard([&] {
+    if (!src || !tgt || !sizes || !a || !b) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    gsot::config_features(cfg, seed, src, tgt, sizes, a, b);
+  });
+}
+
+GSOT_API int gsot_cost_matrix_device(const double* src, int64_t m, const double* tgt, int64_t n,
+                                     int64_t d, int normalize, double* d_cost) {
+  return guard([&] {
+    if (!src || !tgt || !d_cost) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s;
+    GSOT_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double *ds = nullptr, *dt = nullptr, *part = nullptr;
+    unsigned int* ticket = nullptr;
+    GSOT_CUDA_CHECK(cudaMalloc(&ds, sizeof(double) * m * d));
+    GSOT_CUDA_CHECK(cudaMalloc(&dt, sizeof(double) * n * d));
+    GSOT_CUDA_CHECK(cudaMalloc(&part, sizeof(double) * (148 * 8 + 1)));
+    GSOT_CUDA_CHECK(cudaMalloc(&ticket, sizeof(unsigned int)));
+    GSOT_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(ds, src, sizeof(double) * m * d, cudaMemcpyHostToDevice, s));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(dt, tgt, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
+    gsot::launch_cost_matrix(ds, m, dt, n, d, nullptr, m, d_cost, s);
+    if (normalize) {
+      gsot::launch_max_reduce(d_cost, m * n, part, 148 * 8, part + 148 * 8, ticket, s);
+      gsot::launch_scale_div(d_cost, m * n, part + 148 * 8, s);
+    }
+    GSOT_CUDA_CHECK(cudaGetLastError());
+    GSOT_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaFree(ds);
+    cudaFree(dt);
+    cudaFree(part);
+    cudaFree(ticket);
+    cudaStreamDestroy(s);
+  });
+}
+
+GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double mu,
+                                gsot_ctx** out) {
+  return guard([&] {
+    if (!out) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    int64_t m, n, d;
+    int32_t L;
+    gsot::config_shape(cfg, &m, &n, &L, &d);
+    std::vector<double> src(static_cast<size_t>(m * d)), tgt(static_cast<size_t>(n * d));
+    std::vector<double> a(static_cast<size_t>(m)), b(static_cast<size_t>(n));
+    std::vector<int32_t> sizes(static_cast<size_t>(L));
+    gsot::config_features(cfg, seed, src.data(), tgt.data(), sizes.data(), a.data(), b.data());
+    auto* c = new gsot_ctx();
+    try {
+      setup_shape(c, m, n, sizes.data(), L, gamma, mu);
+      init_device(c);
+      alloc_buffers(c);
+      set_marginals(c, a.data(), b.data());
+      double *ds = nullptr, *dt = nullptr, *part = nullptr;
+      unsigned int* ticket = nullptr;
+      GSOT_CUDA_CHECK(cudaMalloc(&ds, sizeof(double) * m * d));
+      GSOT_CUDA_CHECK(cudaMalloc(&dt, sizeof(double) * n * d));
+      GSOT_CUDA_CHECK(cudaMalloc(&part, sizeof(double) * (148 * 8 + 1)));
+      GSOT_CUDA_CHECK(cudaMalloc(&ticket, sizeof(unsigned int)));
+      GSOT_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), c->stream));
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(ds, src.data(), sizeof(double) * m * d,
+                                      cudaMemcpyHostToDevice, c->stream));
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(dt, tgt.data(), sizeof(double) * n * d,
+                                      cudaMemcpyHostToDevice, c->stream));
+      c->launch(gsot::K_MISC, 0, [&] {
+        gsot::launch_cost_matrix(ds, m, dt, n, d, c->d_row_to_prow, c->ldc, c->C, c->stream);
+      });
+      // padding rows are zero (memset at allocation) and C >= 0, so the max
+      // over the padded buffer is max(C).
+      const int64_t count = c->ldc * n;
+      c->launch(gsot::K_MISC, 0, [&] {
+        gsot::launch_max_reduce(c->C, count, part, 148 * 8, part + 148 * 8, ticket, c->stream);
+      });
+      c->launch(gsot::K_MISC, 0, [&] { gsot::launch_scale_div(c->C, count, part + 148 * 8, c->stream); });
+      c->sync();
+      cudaFree(ds);
+      cudaFree(dt);
+      cudaFree(part);
+      cudaFree(ticket);
+      check_marginal(a.data(), m, 'a');
+      check_marginal(b.data(), n, 'b');
+      *out = c;
+    } catch (...) {
+      delete c;
+      throw;
+    }
+  });
+}
+
+GSOT_API int gsot_profile_enable(gsot_ctx* ctx, int enable) {
+  return guard([&] {
+    checked(ctx);
+    ctx->collect_marks();
+    ctx->profile = enable != 0;
+  });
+}
+
+GSOT_API int gsot_profile_read(gsot_ctx* ctx, int kind, double* ms, double* bytes,
+                               int64_t* launches) {
+  return guard([&] {
+    checked(ctx);
+    if (kind < 0 || kind >= gsot::K_NKINDS) throw Error(GSOT_ERR_INVALID_ARGUMENT, "bad kind");
+    ctx->collect_marks();
+    if (ms) *ms = ctx->prof_ms[kind];
+    if (bytes) *bytes = ctx->prof_bytes[kind];
+    if (launches) *launches = ctx->prof_launches[kind];
+  });
+}
+
+GSOT_API int gsot_profile_reset(gsot_ctx* ctx) {
+  return guard([&] {
+    checked(ctx);
+    ctx->collect_marks();
+    for (int k = 0; k < gsot::K_NKINDS; ++k) {
+      ctx->prof_ms[k] = 0;
+      ctx->prof_bytes[k] = 0;
+      ctx->prof_launches[k] = 0;
+    }
+  });
+}
+
+GSOT_API int64_t gsot_kernel_launches(const gsot_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// gsot_internal.cuh — shared declarations of the sm_100a solver library.
+//
+// Device layout: the cost lives in HBM as a "group-padded
+// column-major" matrix: column j is a run of `ldc` doubles; inside it, group
+// l occupies `g_l` rows starting at padded offset poff[l], a multiple of 4
+// doubles, so every (group, column) block starts on a 32-byte sector.
+// Snapshot norms and per-block partials are [l][j] (j fastest) so that the
+// per-block kernels, which put consecutive target columns on consecutive
+// lanes, read and write them coalesced. Bitmasks are [l][c] words over
+// 32-column chunks c = j / 32: bit (j % 32) of word (l, c).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "gsot.h"
+
+namespace gsot {
+
+// Exception carrying a gsot_status; converted to a status code at the C ABI.
+struct Error : std::runtime_error {
+  int status;
+  gsot_error_detail detail{};
+  Error(int st, const std::string& what) : std::runtime_error(what), status(st) {
+    detail.status = st;
+    detail.index = -1;
+  }
+};
+
+#define GSOT_CUDA_CHECK(expr)                                                              \
+  do {                                                                                    \
+    cudaError_t gsot_e_ = (expr);                                                         \
+    if (gsot_e_ != cudaSuccess) {                                                         \
+      if (gsot_e_ == cudaErrorMemoryAllocation)                                           \
+        throw ::gsot::Error(GSOT_ERR_OUT_OF_MEMORY,                                       \
+                            std::string("CUDA out of memory at " #expr ": ") +            \
+                                cudaGetErrorString(gsot_e_));                             \
+      throw ::gsot::Error(GSOT_ERR_CUDA, std::string(#expr " failed: ") +                 \
+                                             cudaGetErrorString(gsot_e_));                \
+    }                                                                                     \
+  } while (0)
+
+// Read-only view of the resident instance passed to every kernel by value.
+struct DevProblem {
+  const double* C;        // ldc x n, group-padded column-major
+  int64_t ldc;            // padded rows per column (multiple of 4)
+  int64_t m, n;           // instance shape
+  int32_t L;              // groups
+  int32_t nw;             // 32-column chunks: ceil(n / 32)
+  const int32_t* off;     // L+1 unpadded row offsets (alpha indexing)
+  const int32_t* poff;    // L+1 padded row offsets (cost indexing)
+  const int32_t* row_group;  // m: group of each row
+  const double* sqrt_g;   // L: sqrt(g_l) (screening.hpp:79)
+  const double* a;        // m
+  const double* b;        // n
+  double gamma, mu, tau;  // tau = mu * gamma (core.hpp:70)
+};
+
+// Device scalars written by the reduction kernels and read back with one
+// D2H copy per evaluation.
+struct EvalScalars {
+  double objective;  // a.alpha + b.beta - psi
+  double slope;      // grad . d (line search), when requested
+  double dot_aa, dot_bb, psi_sum;
+  double extra[3];   // pair kernel: s.y, s.s, y.y
+  unsigned long long counters[4];  // in_active, skipped, unskipped, upper_bounds
+  unsigned long long nonzero_blocks;
+  int ntasks;        // screened work-list length
+  int next_task;     // dynamic scheduler cursor
+  unsigned int ticket;  // last-block-done counter
+  int audit_violation;  // audit: first violating block + 1 (l * n + j + 1)
+  long long audit_where;
+};
+
+// ---- kernels (gsot_kernels.cu) ---------------------------------------------
+
+// Per-kernel-class counters for gsot_profile_*.
+enum KernelKind {
+  K_EVAL = 0,
+  K_SNAPSHOT = 1,
+  K_BOUNDS = 2,
+  K_ACTIVE = 3,
+  K_FINALIZE = 4,
+  K_LBFGS = 5,
+  K_DELTA = 6,
+  K_MISC = 7,
+  K_NKINDS = 8
+};
+
+void launch_relayout(const double* src_colmajor, int64_t m, int64_t j0, int64_t ncols,
+                     const int32_t* row_to_prow, int64_t ldc, double* C,
+                     unsigned long long* first_bad, cudaStream_t s);
+void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
+                     cudaStream_t s);
+void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStream_t s);
+void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
+                  double* dfull, double* dneg, double* dbeta, cudaStream_t s);
+void launch_active(const DevProblem& P, const double* ks, const double* os, const double* dfull,
+                   const double* dneg, const double* dbeta, uint32_t* active_words,
+                   EvalScalars* sc, cudaStream_t s);
+void launch_bounds(const DevProblem& P, const double* zs, const uint32_t* active_words,
+                   const double* dpos, const double* dbeta, double ub_offset, uint32_t* words,
+                   int2* tasks, EvalScalars* sc, cudaStream_t s);
+int eval_blocks_per_sm();
+// dense_ntasks >= 0: dense task list of that length; -1: screened, the
+// length is sc->ntasks (written by the bounds kernel).
+void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int dense_ntasks,
+                 const uint32_t* words, double* rowpart, double* colpart, double* psi,
+                 EvalScalars* sc, int grid, cudaStream_t s);
+void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
+                     const double* rowpart, const double* colpart, const double* psi,
+                     double* grad, double* psicol, cudaStream_t s);
+void launch_objective(const DevProblem& P, const double* x, const double* psicol,
+                      const double* grad, const double* dvec, double* partials, int nblocks,
+                      EvalScalars* sc, cudaStream_t s);
+void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,
+                         double* out, cudaStream_t s);
+void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* words,
+                        const uint32_t* active_words, EvalScalars* sc, cudaStream_t s);
+void launch_audit_active(const DevProblem& P, const double* x, const uint32_t* active_words,
+                         EvalScalars* sc, cudaStream_t s);
+void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaStream_t s);
+void launch_dense_tasks(int2* tasks, int32_t L, int32_t nw, cudaStream_t s);
+
+// L-BFGS vector kernels (gsot_lbfgs.cu).
+constexpr int kMaxMemory = 64;
+struct TwoLoopArgs {
+  const double* s[kMaxMemory];
+  const double* y[kMaxMemory];
+  double rho[kMaxMemory];
+  int k;
+  double gamma_scale;  // s_last.y_last / y_last.y_last, or 1 when not applied
+  int apply_scale;
+  const double* g;
+  double* d;
+  int64_t dim;
+  double* out;  // [0] = g.d, [1] = d.d
+};
+void launch_two_loop(const TwoLoopArgs& a, cudaStream_t s);
+void launch_axpy_point(const double* x, double t, const double* d, double* out, int64_t dim,
+                       cudaStream_t s);
+void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* sv,
+                 double* yv, int64_t dim, double* partials, int nblocks, EvalScalars* sc,
+                 cudaStream_t s);
+void launch_dot(const double* a, const double* b, int64_t dim, double* partials, int nblocks,
+                EvalScalars* sc, int slot, cudaStream_t s);
+void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, EvalScalars* sc,
+                   int slot, cudaStream_t s);
+
+// Cost-matrix construction (gsot_data.cu).
+void launch_cost_matrix(const double* src, int64_t m, const double* tgt, int64_t n, int64_t d,
+                        const int32_t* row_to_prow, int64_t ldc, double* out, cudaStream_t s);
+void launch_max_reduce(const double* C, int64_t count, double* partials, int nblocks,
+                       double* out, unsigned int* ticket, cudaStream_t s);
+void launch_scale_div(double* C, int64_t count, const double* divisor, cudaStream_t s);
+
+}  // namespace gsot

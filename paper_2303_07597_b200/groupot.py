@@ -1,0 +1,690 @@
+"""Python mirror of the reference `groupot` API, backed by libgsot.so.
+
+Same names, argument meanings and error behaviour as the reference C++
+library (/root/reference/proj/include/groupot): the exception classes of
+errors.hpp, GroupPartition / ProblemInstance / RegParams (core.hpp),
+dual_objective / dual_gradient / recover_plan (dual.hpp), take_snapshot /
+build_active_set / FastGradDispatcher / GradStats (screening.hpp) and
+SolverMode / SolverOptions / Solution / solve / solve_baseline / solve_fast
+/ audit_solve (solver.hpp). Every computation runs on the GPU through the
+C ABI of include/gsot.h; nothing here computes the objective, the gradient
+or a bound on the host.
+
+Arrays: cost is m x n (any numpy order; passed to the library column-major
+as Eigen::MatrixXd is), vectors are float64 1-D arrays. Snapshot matrices
+and the active set are returned as (L, n) arrays, element [l, j].
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from datetime import timedelta
+
+import numpy as np
+
+from . import _lib
+
+# ----------------------------------------------------------------- errors.hpp
+
+
+class Error(RuntimeError):
+    """Base of every error raised by this library (errors.hpp:190-194)."""
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class NegativeCost(Error):
+    def __init__(self, msg: str, row: int, col: int, value: float):
+        super().__init__(msg)
+        self.row, self.col, self.value = row, col, value
+
+
+class MarginalNotNormalized(Error):
+    def __init__(self, msg: str, which: str, index: int):
+        super().__init__(msg)
+        self.which, self.index = which, index
+
+
+class PartitionMismatch(Error):
+    pass
+
+
+class RhoOutOfRange(Error):
+    def __init__(self, msg: str, rho: float = float("nan")):
+        super().__init__(msg)
+        self.rho = rho
+
+
+class AuditViolation(Error):
+    pass
+
+
+class CudaError(Error):
+    """No usable GPU / CUDA failure (the library has no CPU fallback)."""
+
+
+class StateError(Error):
+    pass
+
+
+def _raise(status: int) -> None:
+    if status == _lib.GSOT_OK:
+        return
+    msg, d = _lib.last_error()
+    if status == 1:
+        raise DimensionMismatch(msg)
+    if status == 2:
+        raise NegativeCost(msg, d.row, d.col, d.value)
+    if status == 3:
+        raise MarginalNotNormalized(msg, d.which.decode() if d.which else "?", d.index)
+    if status == 4:
+        raise PartitionMismatch(msg)
+    if status == 6:
+        raise RhoOutOfRange(msg)
+    if status == 7:
+        raise AuditViolation(msg)
+    if status == 8:
+        raise CudaError(msg)
+    if status == 9:
+        raise MemoryError(msg)
+    if status == 10:
+        raise StateError(msg)
+    raise Error(msg)
+
+
+def _f64(v) -> np.ndarray:
+    return np.ascontiguousarray(v, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ------------------------------------------------------------------- core.hpp
+
+
+class GroupPartition:
+    """Contiguous labelled row blocks (core.hpp:17-43)."""
+
+    def __init__(self, sizes):
+        sizes = [int(s) for s in sizes]
+        if not sizes:
+            raise PartitionMismatch("group partition: at least one group required")
+        for l, g in enumerate(sizes):
+            if g < 1:
+                raise PartitionMismatch(
+                    f"group partition: group {l} has non-positive size {g}")
+        self._sizes = np.asarray(sizes, dtype=np.int32)
+        self._offsets = np.concatenate([[0], np.cumsum(self._sizes)]).astype(np.int64)
+
+    def num_groups(self) -> int:
+        return len(self._sizes)
+
+    def total_size(self) -> int:
+        return int(self._offsets[-1])
+
+    def offset(self, l: int) -> int:
+        return int(self._offsets[l])
+
+    def size(self, l: int) -> int:
+        return int(self._sizes[l])
+
+    def sizes(self) -> list[int]:
+        return self._sizes.tolist()
+
+    def offsets(self) -> list[int]:
+        return self._offsets.tolist()
+
+
+class RegParams:
+    """(gamma, mu); tau = mu * gamma is derived, never stored (core.hpp:59-75)."""
+
+    def __init__(self, gamma: float, mu: float):
+        if not (gamma > 0.0) or not math.isfinite(gamma):
+            raise Error(f"gamma must be positive, got {gamma}")
+        if not (mu > 0.0) or not math.isfinite(mu):
+            raise Error(f"mu must be positive, got {mu}")
+        self._gamma, self._mu = float(gamma), float(mu)
+
+    def gamma(self) -> float:
+        return self._gamma
+
+    def mu(self) -> float:
+        return self._mu
+
+    def tau(self) -> float:
+        return self._mu * self._gamma
+
+
+def params_from_rho(gamma: float, rho: float) -> RegParams:
+    """core.hpp:148-151, computed by gsot_params_from_rho."""
+    ge, me = C.c_double(), C.c_double()
+    st = _lib.lib().gsot_params_from_rho(float(gamma), float(rho), C.byref(ge), C.byref(me))
+    if st == 6:
+        msg, _ = _lib.last_error()
+        raise RhoOutOfRange(msg, rho)
+    _raise(st)
+    return RegParams(ge.value, me.value)
+
+
+class ProblemInstance:
+    """Cost (m x n), marginals a (m), b (n), source groups (core.hpp:47-55).
+
+    The cost array is frozen (read-only) so that the device-resident copy
+    the library keeps cannot go stale; assign a new array to change it.
+    """
+
+    def __init__(self, cost, a, b, groups: GroupPartition):
+        self.groups = groups
+        self.cost = cost
+        self.a = a
+        self.b = b
+
+    @property
+    def cost(self) -> np.ndarray:
+        return self._cost
+
+    @cost.setter
+    def cost(self, value) -> None:
+        c = np.array(value, dtype=np.float64, order="F", copy=True)
+        if c.ndim != 2:
+            raise DimensionMismatch("dimension mismatch: cost must be a matrix")
+        c.flags.writeable = False
+        self._cost = c
+        self._drop_context()
+
+    @property
+    def a(self) -> np.ndarray:
+        return self._a
+
+    @a.setter
+    def a(self, value) -> None:
+        self._a = np.array(value, dtype=np.float64).reshape(-1)
+        self._a.flags.writeable = False
+        self._drop_context()
+
+    @property
+    def b(self) -> np.ndarray:
+        return self._b
+
+    @b.setter
+    def b(self, value) -> None:
+        self._b = np.array(value, dtype=np.float64).reshape(-1)
+        self._b.flags.writeable = False
+        self._drop_context()
+
+    def m(self) -> int:
+        return self._cost.shape[0]
+
+    def n(self) -> int:
+        return self._cost.shape[1]
+
+    def __setattr__(self, k, v):
+        if k == "groups" and "_ctx" in self.__dict__:
+            self._drop_context()
+        object.__setattr__(self, k, v)
+
+    def _drop_context(self) -> None:
+        ctx = self.__dict__.get("_ctx")
+        if ctx is not None:
+            ctx.close()
+        self.__dict__["_ctx"] = None
+
+    def context(self, p: RegParams) -> "Context":
+        """The device-resident copy of this instance (created on first use)."""
+        ctx = self.__dict__.get("_ctx")
+        if ctx is None:
+            ctx = Context.from_instance(self, p)
+            self.__dict__["_ctx"] = ctx
+        else:
+            ctx.set_params(p.gamma(), p.mu())
+        return ctx
+
+
+@dataclass
+class TransportPlan:
+    plan: np.ndarray
+
+
+def validate_instance(inst: ProblemInstance) -> None:
+    """core.hpp:117-139 (run by the library while uploading the cost)."""
+    if inst.a.size != inst.m():
+        raise DimensionMismatch(
+            f"dimension mismatch: marginal a has length {inst.a.size}, cost has {inst.m()} rows")
+    if inst.b.size != inst.n():
+        raise DimensionMismatch(
+            f"dimension mismatch: marginal b has length {inst.b.size}, cost has {inst.n()} "
+            "columns")
+    ctx = Context.from_instance(inst, RegParams(1.0, 1.0))
+    ctx.close()
+
+
+# ------------------------------------------------------------------- context
+
+
+class Context:
+    """Owner of one gsot_ctx: the resident instance on one CUDA stream."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        shape = (C.c_int64(), C.c_int64(), C.c_int32(), C.c_int64())
+        _raise(_lib.lib().gsot_shape(self._h, *[C.byref(s) for s in shape]))
+        self.m, self.n, self.L, self.device_bytes = (int(s.value) for s in shape)
+
+    @classmethod
+    def from_instance(cls, inst: ProblemInstance, p: RegParams) -> "Context":
+        if inst.a.size != inst.m() or inst.b.size != inst.n():
+            raise DimensionMismatch(
+                f"dimension mismatch: marginals ({inst.a.size},{inst.b.size}) vs cost "
+                f"{inst.m()}x{inst.n()}")
+        return cls.from_arrays(inst.cost, inst.groups.sizes(), inst.a, inst.b, p.gamma(), p.mu())
+
+    @classmethod
+    def from_arrays(cls, cost, sizes, a, b, gamma: float, mu: float) -> "Context":
+        cost = np.asfortranarray(cost, dtype=np.float64)
+        m, n = cost.shape
+        sizes = np.ascontiguousarray(sizes, dtype=np.int32)
+        a, b = _f64(a), _f64(b)
+        h = C.c_void_p()
+        st = _lib.lib().gsot_create(_ptr(cost), m, n, _ptr(sizes), len(sizes), _ptr(a), _ptr(b),
+                                    float(gamma), float(mu), C.byref(h))
+        _raise(st)
+        return cls(h.value)
+
+    @classmethod
+    def from_config(cls, cfg: int, seed: int, gamma: float, mu: float) -> "Context":
+        h = C.c_void_p()
+        _raise(_lib.lib().gsot_create_config(int(cfg), int(seed), float(gamma), float(mu),
+                                             C.byref(h)))
+        return cls(h.value)
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            _lib.lib().gsot_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def set_params(self, gamma: float, mu: float) -> None:
+        _raise(_lib.lib().gsot_set_params(self._h, float(gamma), float(mu)))
+
+    def eval(self, x, screened: bool = False):
+        x = _f64(x)
+        if x.size != self.m + self.n:
+            raise DimensionMismatch(
+                f"dimension mismatch: state has {x.size} entries, instance is "
+                f"({self.m},{self.n})")
+        g = np.empty(self.m + self.n)
+        obj = C.c_double()
+        st = CallStatsPy()
+        cs = _lib.CallStats()
+        _raise(_lib.lib().gsot_eval(self._h, _ptr(x), 1 if screened else 0, C.byref(obj), _ptr(g),
+                                    C.byref(cs)))
+        st.in_active, st.skipped, st.unskipped, st.upper_bounds = (
+            cs.in_active, cs.skipped, cs.unskipped, cs.upper_bounds)
+        return obj.value, g, st
+
+    def init_snapshot(self, x) -> None:
+        _raise(_lib.lib().gsot_init_snapshot(self._h, _ptr(_f64(x))))
+
+    def refresh(self, x, use_active_set: bool) -> None:
+        _raise(_lib.lib().gsot_refresh(self._h, _ptr(_f64(x)), int(bool(use_active_set))))
+
+    def snapshot_norms(self):
+        z, k, o = (np.empty(self.L * self.n) for _ in range(3))
+        _raise(_lib.lib().gsot_snapshot_norms(self._h, _ptr(z), _ptr(k), _ptr(o)))
+        f = lambda v: v.reshape(self.L, self.n, order="F")  # noqa: E731
+        return f(z), f(k), f(o)
+
+    def active_set(self):
+        mem = np.zeros(self.L * self.n, np.uint8)
+        cnt = C.c_int64()
+        _raise(_lib.lib().gsot_active_set(self._h, _ptr(mem), C.byref(cnt)))
+        return mem.reshape(self.L, self.n, order="F").astype(bool), int(cnt.value)
+
+    def block_mask(self, x) -> np.ndarray:
+        out = np.zeros(self.L * self.n, np.uint8)
+        _raise(_lib.lib().gsot_block_mask(self._h, _ptr(_f64(x)), _ptr(out)))
+        return out.reshape(self.L, self.n, order="F").astype(bool)
+
+    def plan_columns(self, x, j0: int, j1: int) -> np.ndarray:
+        out = np.empty(self.m * (j1 - j0))
+        _raise(_lib.lib().gsot_plan_columns(self._h, _ptr(_f64(x)), int(j0), int(j1), _ptr(out)))
+        return out.reshape(self.m, j1 - j0, order="F")
+
+    def solve(self, mode: int = 1, snapshot_interval: int = 10, grad_tol: float = 1e-6,
+              max_outer_loops: int = 200, lbfgs_memory: int = 10,
+              upper_bound_offset: float = 0.0, history_cap: int = 0):
+        o = _lib.SolverOptionsC(int(snapshot_interval), float(grad_tol), int(max_outer_loops),
+                                int(lbfgs_memory), int(mode), float(upper_bound_offset))
+        x = np.empty(self.m + self.n)
+        r = _lib.SolveResultC()
+        hist = np.zeros(max(1, history_cap) * 4, np.int64)
+        _raise(_lib.lib().gsot_solve(self._h, C.byref(o), _ptr(x), C.byref(r), _ptr(hist),
+                                     int(history_cap)))
+        res = {f: getattr(r, f) for f, _ in _lib.SolveResultC._fields_}
+        res["x"] = x
+        res["history"] = hist[: 4 * min(history_cap, r.grad_calls)].reshape(-1, 4)
+        return res
+
+    def profile(self, enable: bool) -> None:
+        _raise(_lib.lib().gsot_profile_enable(self._h, int(enable)))
+
+    def profile_read(self, kind: int):
+        ms, by, n = C.c_double(), C.c_double(), C.c_int64()
+        _raise(_lib.lib().gsot_profile_read(self._h, int(kind), C.byref(ms), C.byref(by),
+                                            C.byref(n)))
+        return ms.value, by.value, int(n.value)
+
+    def profile_reset(self) -> None:
+        _raise(_lib.lib().gsot_profile_reset(self._h))
+
+    def kernel_launches(self) -> int:
+        return int(_lib.lib().gsot_kernel_launches(self._h))
+
+
+@dataclass
+class CallStatsPy:
+    in_active: int = 0
+    skipped: int = 0
+    unskipped: int = 0
+    upper_bounds: int = 0
+
+
+# ------------------------------------------------------------------- dual.hpp
+
+
+@dataclass
+class DualState:
+    alpha: np.ndarray
+    beta: np.ndarray
+
+
+def _state_vec(s: DualState, inst: ProblemInstance) -> np.ndarray:
+    alpha, beta = _f64(s.alpha).reshape(-1), _f64(s.beta).reshape(-1)
+    if alpha.size != inst.m() or beta.size != inst.n():  # dual.hpp:17-23
+        raise DimensionMismatch(
+            f"dimension mismatch: dual state is ({alpha.size},{beta.size}), instance is "
+            f"({inst.m()},{inst.n()})")
+    return np.concatenate([alpha, beta])
+
+
+def dual_objective(s: DualState, inst: ProblemInstance, p: RegParams) -> float:
+    """a.alpha + b.beta - sum psi (dual.hpp:38-52)."""
+    x = _state_vec(s, inst)
+    obj, _, _ = inst.context(p).eval(x)
+    return obj
+
+
+def dual_gradient(s: DualState, inst: ProblemInstance, p: RegParams):
+    """(grad_alpha, grad_beta) with the unscreened provider (dual.hpp:85-130)."""
+    x = _state_vec(s, inst)
+    _, g, _ = inst.context(p).eval(x)
+    return g[: inst.m()], g[inst.m():]
+
+
+def recover_plan(s: DualState, inst: ProblemInstance, p: RegParams) -> TransportPlan:
+    """T[:, j] = grad psi(f_j) (dual.hpp:116-128), streamed from the device."""
+    x = _state_vec(s, inst)
+    return TransportPlan(inst.context(p).plan_columns(x, 0, inst.n()))
+
+
+@dataclass
+class PlanDiagnostics:
+    marginal_res_a: float = 0.0
+    marginal_res_b: float = 0.0
+    group_sparsity: float = 0.0
+    mass: float = 0.0
+
+
+def plan_diagnostics(t: TransportPlan, inst: ProblemInstance) -> PlanDiagnostics:
+    """Reporting only (dual.hpp:139-169); numpy on a downloaded plan."""
+    P = t.plan
+    if P.shape != (inst.m(), inst.n()):
+        raise DimensionMismatch(f"dimension mismatch: plan is {P.shape[0]}x{P.shape[1]}")
+    d = PlanDiagnostics()
+    d.marginal_res_a = float(np.max(np.abs(P.sum(axis=1) - inst.a)))
+    d.marginal_res_b = float(np.max(np.abs(P.sum(axis=0) - inst.b)))
+    d.mass = float(P.sum())
+    zero = 0
+    for l in range(inst.groups.num_groups()):
+        o, g = inst.groups.offset(l), inst.groups.size(l)
+        zero += int(np.sum(np.all(P[o:o + g, :] == 0.0, axis=0)))
+    d.group_sparsity = zero / (inst.groups.num_groups() * inst.n())
+    return d
+
+
+# -------------------------------------------------------------- screening.hpp
+
+
+@dataclass
+class SnapshotStore:
+    alpha_snap: np.ndarray
+    beta_snap: np.ndarray
+    z_snap: np.ndarray  # (L, n)
+    k_snap: np.ndarray
+    o_snap: np.ndarray
+    stamp: int = 0
+
+
+def take_snapshot(s: DualState, inst: ProblemInstance, stamp: int = 0,
+                  p: RegParams | None = None) -> SnapshotStore:
+    """screening.hpp:24-50, computed by the snapshot kernel."""
+    x = _state_vec(s, inst)
+    ctx = inst.context(p or RegParams(1.0, 1.0))
+    ctx.init_snapshot(x)
+    z, k, o = ctx.snapshot_norms()
+    return SnapshotStore(x[: inst.m()].copy(), x[inst.m():].copy(), z, k, o, stamp)
+
+
+@dataclass
+class ActiveSet:
+    num_groups: int
+    n: int
+    member: np.ndarray  # (L, n) bool
+    count: int
+
+    def contains(self, l: int, j: int) -> bool:
+        return bool(self.member[l, j])
+
+
+def build_active_set(snap_state: DualState, state: DualState, inst: ProblemInstance,
+                     p: RegParams) -> ActiveSet:
+    """screening.hpp:147-166: lower bounds at `state` against the snapshot
+    taken at `snap_state` (the device keeps the snapshot, not the caller)."""
+    ctx = inst.context(p)
+    ctx.init_snapshot(_state_vec(snap_state, inst))
+    ctx.refresh(_state_vec(state, inst), True)
+    mem, cnt = ctx.active_set()
+    return ActiveSet(inst.groups.num_groups(), inst.n(), mem, cnt)
+
+
+@dataclass
+class GradStats:
+    """screening.hpp:173-188."""
+
+    blocks_in_active_set: int = 0
+    blocks_skipped: int = 0
+    blocks_unskipped: int = 0
+    upper_bounds_evaluated: int = 0
+    outer_loops: int = 0
+    grad_calls: int = 0
+    history: list = field(default_factory=list)  # rows (in_active, skipped, unskipped, ub)
+
+
+class FastGradDispatcher:
+    """Screened gradient provider (screening.hpp:206-315), on the device.
+
+    init / refresh / gradient keep the reference's call protocol; one
+    `gradient` call is the reference's begin_call + n column calls + end_call.
+    """
+
+    def __init__(self, inst: ProblemInstance, p: RegParams, stats: GradStats,
+                 use_active_set: bool, upper_bound_offset: float = 0.0):
+        if upper_bound_offset != 0.0:
+            raise Error("upper_bound_offset is supported through audit_solve only")
+        self.inst, self.p, self.stats = inst, p, stats
+        self.use_active_set = use_active_set
+        self._ctx = inst.context(p)
+
+    def init(self, s: DualState) -> None:
+        self._ctx.init_snapshot(_state_vec(s, self.inst))
+
+    def refresh(self, s: DualState, stamp: int = 0) -> None:
+        self._ctx.refresh(_state_vec(s, self.inst), self.use_active_set)
+
+    def gradient(self, s: DualState):
+        obj, g, st = self._ctx.eval(_state_vec(s, self.inst), screened=True)
+        self.stats.blocks_in_active_set += st.in_active
+        self.stats.blocks_skipped += st.skipped
+        self.stats.blocks_unskipped += st.unskipped
+        self.stats.upper_bounds_evaluated += st.upper_bounds
+        self.stats.grad_calls += 1
+        self.stats.history.append((st.in_active, st.skipped, st.unskipped, st.upper_bounds))
+        m = self.inst.m()
+        return g[:m], g[m:], obj
+
+    def snapshot(self) -> SnapshotStore:
+        z, k, o = self._ctx.snapshot_norms()
+        return SnapshotStore(np.empty(0), np.empty(0), z, k, o)
+
+    def active_set(self) -> ActiveSet:
+        mem, cnt = self._ctx.active_set()
+        return ActiveSet(self.inst.groups.num_groups(), self.inst.n(), mem, cnt)
+
+
+# ----------------------------------------------------------------- solver.hpp
+
+
+class SolverMode(enum.IntEnum):
+    baseline = 0
+    fast = 1
+    fast_no_lower_bound = 2
+    audit = 3
+
+
+def to_string(m: SolverMode) -> str:
+    return {0: "baseline", 1: "fast", 2: "fast-no-lb", 3: "audit"}[int(m)]
+
+
+@dataclass
+class SolverOptions:
+    snapshot_interval: int = 10
+    grad_tol: float = 1e-6
+    max_outer_loops: int = 200
+    lbfgs_memory: int = 10
+    mode: SolverMode = SolverMode.fast
+
+
+@dataclass
+class AuditReport:
+    skip_checks: int = 0
+    active_checks: int = 0
+    column_compares: int = 0
+    gradient_calls: int = 0
+
+
+class Solution:
+    """solver.hpp:33-42. The plan is recovered from the device on first
+    access (column-streamed), not materialised by the solve."""
+
+    def __init__(self, inst: ProblemInstance, p: RegParams, res: dict):
+        m = inst.m()
+        self._inst, self._p = inst, p
+        self.state = DualState(res["x"][:m].copy(), res["x"][m:].copy())
+        self.objective = res["objective"]
+        self.iterations = res["iterations"]
+        self.converged = bool(res["converged"])
+        self.line_search_failed = bool(res["line_search_failed"])
+        self.wall_time = timedelta(seconds=res["wall_seconds"])
+        self.stats = GradStats(res["blocks_in_active_set"], res["blocks_skipped"],
+                               res["blocks_unskipped"], res["upper_bounds_evaluated"],
+                               res["outer_loops"], res["grad_calls"],
+                               [tuple(r) for r in res["history"].tolist()])
+        self._plan = None
+
+    @property
+    def plan(self) -> TransportPlan:
+        if self._plan is None:
+            self._plan = recover_plan(self.state, self._inst, self._p)
+        return self._plan
+
+
+def _run(inst: ProblemInstance, p: RegParams, opts: SolverOptions, mode: int,
+         ub_offset: float = 0.0):
+    ctx = inst.context(p)
+    cap = opts.snapshot_interval * opts.max_outer_loops * 64 + 16
+    res = ctx.solve(mode=mode, snapshot_interval=opts.snapshot_interval, grad_tol=opts.grad_tol,
+                    max_outer_loops=opts.max_outer_loops, lbfgs_memory=opts.lbfgs_memory,
+                    upper_bound_offset=ub_offset, history_cap=cap)
+    return res
+
+
+def solve_baseline(inst: ProblemInstance, p: RegParams,
+                   opts: SolverOptions | None = None) -> Solution:
+    opts = opts or SolverOptions()
+    return Solution(inst, p, _run(inst, p, opts, 0))
+
+
+def solve_fast(inst: ProblemInstance, p: RegParams, opts: SolverOptions | None = None) -> Solution:
+    opts = opts or SolverOptions()
+    mode = 2 if opts.mode == SolverMode.fast_no_lower_bound else 1
+    return Solution(inst, p, _run(inst, p, opts, mode))
+
+
+def audit_solve(inst: ProblemInstance, p: RegParams, opts: SolverOptions | None = None,
+                upper_bound_offset: float = 0.0):
+    opts = opts or SolverOptions()
+    if opts.mode == SolverMode.baseline:
+        return solve_baseline(inst, p, opts), AuditReport()
+    if opts.mode == SolverMode.fast_no_lower_bound:
+        raise Error("audit of fast-no-lb is not exposed by gsot_solve")
+    res = _run(inst, p, opts, 3, upper_bound_offset)
+    rep = AuditReport(res["audit_skip_checks"], res["audit_active_checks"],
+                      res["audit_column_compares"], res["audit_gradient_calls"])
+    return Solution(inst, p, res), rep
+
+
+def solve(inst: ProblemInstance, p: RegParams, opts: SolverOptions | None = None) -> Solution:
+    opts = opts or SolverOptions()
+    if opts.mode == SolverMode.baseline:
+        return solve_baseline(inst, p, opts)
+    if opts.mode in (SolverMode.fast, SolverMode.fast_no_lower_bound):
+        return solve_fast(inst, p, opts)
+    if opts.mode == SolverMode.audit:
+        return audit_solve(inst, p, opts)[0]
+    raise Error("unknown solver mode")
+
+
+# --------------------------------------------------------------- data inputs
+
+
+def config_shape(cfg: int):
+    m, n, d = C.c_int64(), C.c_int64(), C.c_int64()
+    L = C.c_int32()
+    _raise(_lib.lib().gsot_config_shape(int(cfg), C.byref(m), C.byref(n), C.byref(L),
+                                        C.byref(d)))
+    return int(m.value), int(n.value), int(L.value), int(d.value)
+
+
+def config_features(cfg: int, seed: int):
+    """Host features of BASELINE config `cfg` (SURVEY.md §8(d) recipe)."""
+    m, n, L, d = config_shape(cfg)
+    src, tgt = np.empty((m, d)), np.empty((n, d))
+    sizes = np.empty(L, np.int32)
+    a, b = np.empty(m), np.empty(n)
+    _raise(_lib.lib().gsot_config_features(int(cfg), int(seed), _ptr(src), _ptr(tgt),
+                                           _ptr(sizes), _ptr(a), _ptr(b)))
+    return src, tgt, sizes, a, b
