@@ -1,0 +1,474 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 group-sparse OT dual solver.
+
+Metric (BASELINE.json): dual-grad evals/s inside the L-BFGS solve, achieved
+HBM GB/s of the dominant kernel (fraction of the measured peak), and the
+L-BFGS solve time.
+
+Workload (BASELINE.json configs[1], "medium balanced"): m = n = 10,000,
+L = 100 classes of 100, d = 128, gamma = 0.1, mu = 0.5, 200 L-BFGS
+iterations (snapshot interval 10, memory 10, grad_tol 1e-12 so the solve
+runs to budget), fast mode (upper-bound skipping + lower-bound active set).
+One step = one complete solve from x0 = 0 on the HBM-resident instance;
+value = objective+gradient evaluations per second over the K timed solves
+(device time from CUDA events on the solver stream). The 0.8 GB cost matrix
+exceeds the 126 MB L2, so no flush is needed between steps.
+
+e2e: the same metric through the public C ABI with HOST buffers: every step
+uploads C, a, b from pinned host memory (gsot_create: H2D + on-device
+validation + re-layout), solves, downloads x, and frees the context.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+--impl reference: the unmodified reference (oracle/_ref, the reference
+headers compiled against the Eigen shim) timed on the host cores on the same
+config: each step is a bounded sample (the first `--ref-iters` iterations of
+solve_fast), evals/s = gradient calls / the reference's own wall_time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(1, os.path.join(ROOT, "tests"))  # CPU checkers (reference arm / cpu_baseline)
+
+CONFIGS = {  # cfg: (gamma, mu, iterations)  -- BASELINE.json configs / SURVEY.md §8(d)
+    1: (1.0, 0.1, 100),
+    2: (0.1, 0.5, 200),
+    3: (0.1, 0.2, 200),
+    4: (0.05, 0.3, 200),
+    5: (0.1, 0.5, 300),
+}
+METRIC = "dual-grad evals/s (fused objective+gradient inside L-BFGS, fast mode)"
+KIND_NAMES = {0: "k_eval", 1: "k_snapshot", 2: "k_bounds", 3: "k_active", 4: "k_finalize",
+              5: "lbfgs", 6: "k_delta", 7: "misc"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+def allreduce(pg, value: float, op: str) -> float:
+    if pg is None:
+        return value
+    import torch
+
+    dev = "cuda" if pg.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX if op == "max" else pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def ncu_traffic(kernel: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    ent = d.get(kernel)
+    return None if ent is None else ent.get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------- reference
+
+
+def host_instance(cfg: int, seed: int, threads: int):
+    """Config instance on the host built with the CPU checker (oracle C): the
+    reference arm never touches libgsot."""
+    import ctypes as C
+
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import Oracle, Problem
+
+    o = Oracle()
+    m, n, L, d = (C.c_int64(), C.c_int64(), C.c_int32(), C.c_int64())
+    o.lib.go_config_shape(cfg, C.byref(m), C.byref(n), C.byref(L), C.byref(d))
+    m, n, L, d = m.value, n.value, L.value, d.value
+    src, tgt = np.empty((m, d)), np.empty((n, d))
+    sizes, a, b = np.empty(L, np.int32), np.empty(m), np.empty(n)
+    o.lib.go_config_features(C.c_int(cfg), C.c_uint64(seed),
+                             *[v.ctypes.data_as(C.c_void_p) for v in (src, tgt, sizes, a, b)])
+    cost = np.empty((m, n), order="F")
+    o.lib.go_cost_matrix_par(src.ctypes.data_as(C.c_void_p), C.c_int64(m),
+                             tgt.ctypes.data_as(C.c_void_p), C.c_int64(n), C.c_int64(d),
+                             cost.ctypes.data_as(C.c_void_p), C.c_int(threads))
+    cmax = cost.max()  # data_io.hpp:162-165
+    if cmax > 0:
+        cost /= cmax
+    gamma, mu, _ = CONFIGS[cfg]
+    return Problem(cost, sizes, a, b, gamma, mu)
+
+
+def reference_sample(prob, iters: int, replicas: int):
+    """`replicas` concurrent single-threaded reference solve_fast runs of
+    `iters` iterations each; returns (grad_calls, max wall_time)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import RefLib
+
+    lib = RefLib()
+    out = [None] * replicas
+
+    def run(i):
+        out[i] = lib.solve(prob, mode=1, snapshot_interval=iters, max_outer_loops=1,
+                           grad_tol=1e-12)
+
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(replicas)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    calls = sum(r["grad_calls"] for r in out)
+    wall = max(r["wall_seconds"] for r in out)
+    return calls, wall
+
+
+def run_reference(args, world, rank, pg):
+    if rank != 0:
+        return 0
+
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libgroupot_ref.so")):
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libgroupot_ref.so not built"}))
+        return 0
+    ncpu = os.cpu_count() or 1
+    prob = host_instance(args.config, args.config, max(1, ncpu))
+    replicas = max(1, min(args.ref_replicas or ncpu, ncpu, mem_replicas(prob)))
+    for _ in range(args.warmup):
+        reference_sample(prob, args.ref_iters, replicas)
+    tot_calls, tot_wall = 0, 0.0
+    for _ in range(args.steps):
+        c, w = reference_sample(prob, args.ref_iters, replicas)
+        tot_calls += c
+        tot_wall += w
+    value = tot_calls / tot_wall
+    unit = "evals/s"
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": unit,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_wall / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SURVEY.md §8(d) recipe, seed = config id)",
+        "config": {"workload": f"config {args.config}: first {args.ref_iters} L-BFGS iterations "
+                               f"of the reference solve_fast",
+                   "m": prob.m, "n": prob.n, "L": prob.L, "gamma": prob.gamma, "mu": prob.mu},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": replicas, "kind": "reference",
+                         "sample": f"{replicas} concurrent single-threaded reference solve_fast "
+                                   f"runs x {args.ref_iters} iterations per step; wall_time as "
+                                   "Solution::wall_time (solver.hpp:243-246)"},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def mem_replicas(prob) -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable"):
+                    avail = int(ln.split()[1]) * 1024
+                    break
+            else:
+                return 1
+    except OSError:
+        return 1
+    per = 3 * 8 * prob.m * prob.n  # Eigen copy + plan + slack
+    return max(1, int(0.7 * avail // per))
+
+
+# ---------------------------------------------------------------- ours
+
+
+def run_ours(args, world, rank, local, pg):
+    import numpy as np
+
+    import paper_2303_07597_b200 as G
+
+    G.set_device(local)
+    cfg = args.config
+    gamma, mu, iters = CONFIGS[cfg]
+    ctx = G.Context.from_config(cfg, cfg, gamma, mu)
+    solve_kw = dict(mode=1, snapshot_interval=10, grad_tol=1e-12, max_outer_loops=iters // 10,
+                    lbfgs_memory=10, history_cap=0)
+    for _ in range(args.warmup):
+        ctx.solve(**solve_kw)
+
+    # ---- timed region: K solves on the resident instance
+    ctx.profile_reset()
+    ctx.profile(True)
+    launches0 = ctx.kernel_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(pg)
+    ctx.timer_start()
+    calls, iters_done, solve_ms = 0, 0, []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = ctx.solve(**solve_kw)
+        solve_ms.append(1e3 * (time.perf_counter() - t0))
+        calls += r["grad_calls"]
+        iters_done += r["iterations"]
+    ms = ctx.timer_stop()
+    barrier(pg)
+    clk = clocks.stop()
+    ctx.profile(False)
+    launches = ctx.kernel_launches() - launches0
+    kinds = {}
+    for k, name in KIND_NAMES.items():
+        kms, kbytes, kn = ctx.profile_read(k)
+        if kn:
+            kinds[name] = {"ms": kms, "bytes": kbytes, "launches": kn}
+    ms_max = allreduce(pg, ms, "max")
+    calls_tot = allreduce(pg, float(calls), "sum")
+    value = calls_tot / (ms_max / 1e3)
+
+    # roofline of the dominant HBM kernel (largest device-time share among
+    # the kernels with algorithmic byte counts)
+    peak, peak_kind = peaks()
+    cand = {k: v for k, v in kinds.items() if v["bytes"] > 0}
+    dom = max(cand, key=lambda k: cand[k]["ms"])
+    d = cand[dom]
+    achieved = (d["bytes"] / d["launches"]) / (d["ms"] / d["launches"] / 1e3) / 1e9
+    traffic = ncu_traffic(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
+                "traffic": traffic,
+                "bytes_per_launch": d["bytes"] / d["launches"],
+                "ms_per_launch": d["ms"] / d["launches"],
+                "share_of_step": d["ms"] / ms}
+
+    # ---- e2e through the C ABI with host buffers
+    e2e = run_e2e(args, ctx, cfg, gamma, mu, solve_kw, pg)
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, e2e.pop("_host"))
+    else:
+        e2e.pop("_host", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "evals/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8(d) recipe, seed = config id), generated on device",
+            "config": {"workload": f"config {cfg}: one fast-mode L-BFGS solve per step "
+                                   f"({iters} iterations, r=10, memory 10)",
+                       "m": ctx.m, "n": ctx.n, "L": ctx.L, "gamma": gamma, "mu": mu,
+                       "l2": "inputs larger than L2 (cost 0.8 GB > 126 MB), no flush",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "solve_ms": statistics.median(solve_ms),
+            "evals_per_solve": calls / args.steps,
+            "iterations_per_solve": iters_done / args.steps,
+            "roofline": roofline,
+            "kernels": kinds,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def run_e2e(args, ctx, cfg, gamma, mu, solve_kw, pg):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2303_07597_b200 as G
+
+    m, n, L, d = G.config_shape(cfg)
+    src, tgt, sizes, a, b = G.config_features(cfg, cfg)
+    # cost on the host, pinned (the caller's buffer for the e2e steps)
+    host = torch.empty((n, m), dtype=torch.float64, pin_memory=torch.cuda.is_available())
+    cost = host.numpy().T  # (m, n) Fortran view: column-major as the ABI expects
+    dev = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    st = G._lib.lib().gsot_cost_matrix_device(
+        src.ctypes.data_as(C.c_void_p), m, tgt.ctypes.data_as(C.c_void_p), n, d, 1,
+        C.c_void_p(dev.data_ptr()))
+    G.groupot._raise(st)
+    host.copy_(dev)
+    del dev
+    torch.cuda.synchronize()
+    steps = max(1, args.steps // 2)
+    times, calls = [], 0
+    for it in range(steps + 1):
+        t0 = time.perf_counter()
+        c2 = G.Context.from_arrays(cost, sizes, a, b, gamma, mu)
+        r = c2.solve(**solve_kw)
+        c2.close()
+        dt = time.perf_counter() - t0
+        if it > 0:  # first step is warm-up
+            times.append(dt)
+            calls += r["grad_calls"]
+    tmax = allreduce(pg, sum(times), "max")
+    calls_tot = allreduce(pg, float(calls), "sum")
+    return {"value": calls_tot / tmax, "unit": "evals/s",
+            "h2d_bytes_per_step": 8 * m * n + 8 * (m + n) + 4 * L,
+            "d2h_bytes_per_step": 8 * (m + n),
+            "ms_per_step": 1e3 * tmax / steps,
+            "what": "gsot_create from pinned host cost (H2D + device validation + re-layout) "
+                    "+ gsot_solve + x download + gsot_destroy",
+            "_host": (cost, sizes, a, b, gamma, mu)}
+
+
+def cpu_baseline(args, host):
+    cost, sizes, a, b, gamma, mu = host
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bindings import Problem, RefLib, ref_available
+
+    import numpy as np
+
+    prob = Problem(np.asfortranarray(cost), sizes, a, b, gamma, mu)
+    kind = "reference" if ref_available() else "port"
+    if kind == "reference":
+        lib = RefLib()
+        r = lib.solve(prob, mode=1, snapshot_interval=args.ref_iters, max_outer_loops=1,
+                      grad_tol=1e-12)
+        calls, wall = r["grad_calls"], r["wall_seconds"]
+    else:
+        from oracle_bindings import Oracle
+
+        r = Oracle().solve(prob, mode=1, snapshot_interval=args.ref_iters, max_outer_loops=1,
+                           grad_tol=1e-12)
+        calls, wall = r["grad_calls"], r["wall_seconds"]
+    return {"value": calls / wall, "unit": "evals/s", "cores": 1, "kind": kind,
+            "sample": f"reference solve_fast, first {args.ref_iters} iterations "
+                      f"({calls} gradient calls, {wall:.1f} s maximize wall_time), 1 core"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ref-iters", type=int, default=2)
+    ap.add_argument("--ref-replicas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, pg = dist_init()
+    try:
+        if args.impl == "reference":
+            return run_reference(args, world, rank, pg)
+        return run_ours(args, world, rank, local, pg)
+    finally:
+        if pg is not None:
+            pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

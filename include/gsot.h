@@ -234,6 +234,12 @@ GSOT_API int gsot_profile_enable(gsot_ctx* ctx, int enable);
 GSOT_API int gsot_profile_read(gsot_ctx* ctx, int kind, double* ms, double* bytes,
                                int64_t* launches);
 GSOT_API int gsot_profile_reset(gsot_ctx* ctx);
+/* Select the CUDA device used by contexts created afterwards on this host
+ * thread (one process per GPU: LOCAL_RANK). */
+GSOT_API int gsot_set_device(int32_t device);
+/* CUDA-event timer on the context stream: op 0 records the start event,
+ * op 1 records the stop event, synchronizes and returns the elapsed ms. */
+GSOT_API int gsot_timer(gsot_ctx* ctx, int op, double* ms);
 /* Number of kernels this library launched on the context (all kinds). */
 GSOT_API int64_t gsot_kernel_launches(const gsot_ctx* ctx);
 

@@ -1003,3 +1003,144 @@ void go_cost_matrix_par(const double* src, int64_t m, const double* tgt, int64_t
   free(th);
   free(jobs);
 }
+
+/* ---------------------------------------------------------------- configs */
+
+typedef struct {
+  int64_t m, n;
+  int32_t L;
+  int64_t d;
+  double sigma;
+  int transform, zipf, dirichlet;
+} cfg_spec_t;
+
+static int cfg_spec(int cfg, cfg_spec_t* s) {
+  static const cfg_spec_t T[5] = {{1000, 1000, 10, 64, 1.0, 1, 0, 0},
+                                  {10000, 10000, 100, 128, 1.0, 0, 0, 0},
+                                  {50000, 20000, 1000, 256, 1.0, 2, 0, 0},
+                                  {40000, 30000, 500, 128, 1.0, 0, 1, 1},
+                                  {100000, 50000, 200, 512, 1.5, 0, 0, 0}};
+  if (cfg < 1 || cfg > 5) return ST_PARAM;
+  *s = T[cfg - 1];
+  return ST_OK;
+}
+
+int go_config_shape(int cfg, int64_t* m, int64_t* n, int32_t* L, int64_t* d) {
+  cfg_spec_t s;
+  if (cfg_spec(cfg, &s)) return ST_PARAM;
+  if (m) *m = s.m;
+  if (n) *n = s.n;
+  if (L) *L = s.L;
+  if (d) *d = s.d;
+  return ST_OK;
+}
+
+static int64_t zipf_total(double c, int32_t L, int32_t* out) {
+  int64_t tot = 0;
+  for (int k = 1; k <= L; ++k) {
+    double v = round(c * pow((double)k, -1.1));
+    v = fmin(4000.0, fmax(2.0, v));
+    if (out) out[k - 1] = (int32_t)v;
+    tot += (int64_t)v;
+  }
+  return tot;
+}
+
+int go_config_features(int cfg, uint64_t seed, double* src, double* tgt, int32_t* sizes,
+                       double* a, double* b) {
+  cfg_spec_t s;
+  if (cfg_spec(cfg, &s)) return ST_PARAM;
+  const int64_t m = s.m, n = s.n, d = s.d;
+  const int32_t L = s.L;
+  if (s.zipf) {
+    double lo = 1.0, hi = 1e7;
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (zipf_total(mid, L, NULL) >= m)
+        hi = mid;
+      else
+        lo = mid;
+    }
+    const int64_t tot = zipf_total(hi, L, sizes);
+    sizes[1] -= (int32_t)(tot - m);
+  } else {
+    for (int32_t l = 0; l < L; ++l) sizes[l] = (int32_t)(m / L);
+  }
+  go_rng rng;
+  go_rng_seed(&rng, seed);
+  double* means = (double*)malloc(sizeof(double) * (size_t)(L * d));
+  for (int64_t e = 0; e < L * d; ++e) means[e] = 2.0 * go_rng_normal(&rng);
+  int64_t row = 0;
+  for (int32_t l = 0; l < L; ++l)
+    for (int32_t r = 0; r < sizes[l]; ++r, ++row)
+      for (int64_t k = 0; k < d; ++k)
+        src[row * d + k] = means[l * d + k] + s.sigma * go_rng_normal(&rng);
+  const int64_t per = n / L;
+  for (int64_t t = 0; t < n; ++t)
+    for (int64_t k = 0; k < d; ++k)
+      tgt[t * d + k] = means[(t / per) * d + k] + s.sigma * go_rng_normal(&rng);
+  if (s.transform) {
+    double* G = (double*)malloc(sizeof(double) * (size_t)(d * d));
+    double* A = (double*)malloc(sizeof(double) * (size_t)(d * d));
+    double* shift = (double*)malloc(sizeof(double) * (size_t)d);
+    double* y = (double*)malloc(sizeof(double) * (size_t)d);
+    for (int64_t e = 0; e < d * d; ++e) G[e] = go_rng_normal(&rng);
+    for (int64_t r = 0; r < d; ++r) shift[r] = 0.5;
+    if (s.transform == 1) { /* modified Gram-Schmidt, positive R diagonal */
+      memcpy(A, G, sizeof(double) * (size_t)(d * d));
+      for (int64_t c = 0; c < d; ++c) {
+        for (int64_t p = 0; p < c; ++p) {
+          double dot = 0.0;
+          for (int64_t r = 0; r < d; ++r) dot += A[r * d + p] * A[r * d + c];
+          for (int64_t r = 0; r < d; ++r) A[r * d + c] -= dot * A[r * d + p];
+        }
+        double nrm = 0.0;
+        for (int64_t r = 0; r < d; ++r) nrm += A[r * d + c] * A[r * d + c];
+        nrm = sqrt(nrm);
+        for (int64_t r = 0; r < d; ++r) A[r * d + c] /= nrm;
+      }
+    } else {
+      const double sc = 0.1 / sqrt((double)d);
+      for (int64_t r = 0; r < d; ++r)
+        for (int64_t c = 0; c < d; ++c) A[r * d + c] = (r == c ? 1.0 : 0.0) + sc * G[r * d + c];
+      for (int64_t r = 0; r < d; ++r) shift[r] = go_rng_normal(&rng);
+    }
+    for (int64_t t = 0; t < n; ++t) {
+      for (int64_t r = 0; r < d; ++r) {
+        double acc = 0.0;
+        for (int64_t c = 0; c < d; ++c) acc += A[r * d + c] * tgt[t * d + c];
+        y[r] = acc + shift[r];
+      }
+      memcpy(tgt + t * d, y, sizeof(double) * (size_t)d);
+    }
+    free(G);
+    free(A);
+    free(shift);
+    free(y);
+  }
+  for (int64_t i = n - 1; i > 0; --i) { /* data_io.hpp:93-96 */
+    const int64_t j = (int64_t)go_rng_index(&rng, (uint64_t)i + 1);
+    if (i != j)
+      for (int64_t k = 0; k < d; ++k) {
+        const double t = tgt[i * d + k];
+        tgt[i * d + k] = tgt[j * d + k];
+        tgt[j * d + k] = t;
+      }
+  }
+  if (s.dirichlet) {
+    double* e = (double*)malloc(sizeof(double) * (size_t)m);
+    for (int64_t i = 0; i < m; ++i) {
+      double u = go_rng_uniform01(&rng);
+      if (u <= 0.0) u = 0x1.0p-53;
+      e[i] = -log(u);
+    }
+    const double sum = go_compensated_sum(e, m);
+    for (int64_t i = 0; i < m; ++i) a[i] = e[i] / sum;
+    free(e);
+  } else {
+    for (int64_t i = 0; i < m; ++i) a[i] = 1.0 / (double)m;
+  }
+  for (int64_t j = 0; j < n; ++j) b[j] = 1.0 / (double)n;
+  free(means);
+  return ST_OK;
+}

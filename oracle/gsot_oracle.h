@@ -153,6 +153,14 @@ void go_cost_matrix(const double* src, int64_t m, const double* tgt, int64_t n, 
 void go_cost_matrix_par(const double* src, int64_t m, const double* tgt, int64_t n, int64_t d,
                         double* cost, int nthreads);
 
+/* Synthetic instance recipe of the five BASELINE.json configs (SURVEY.md
+ * §8(d), pinned in DESIGN.md §6): shape query and host features, the same
+ * draw order as the product's generator (paper_2303_07597_b200/csrc/
+ * gsot_data.cu). src m x d and tgt n x d row-major. */
+int go_config_shape(int cfg, int64_t* m, int64_t* n, int32_t* L, int64_t* d);
+int go_config_features(int cfg, uint64_t seed, double* src, double* tgt, int32_t* sizes,
+                       double* a, double* b);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,8 @@ SIGNATURES = {
     "gsot_profile_read": (C.c_int, [_vp, C.c_int, _dp, _dp, C.POINTER(C.c_int64)]),
     "gsot_profile_reset": (C.c_int, [_vp]),
     "gsot_kernel_launches": (C.c_int64, [_vp]),
+    "gsot_set_device": (C.c_int, [C.c_int32]),
+    "gsot_timer": (C.c_int, [_vp, C.c_int, _dp]),
 }
 
 _lib = None

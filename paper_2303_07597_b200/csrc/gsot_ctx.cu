@@ -109,15 +109,15 @@ struct gsot_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
-  int64_t m = 0, n = 0, ldc = 0;
+  int64_t m = 0, n = 0;
   int32_t L = 0, nw = 0;
   double gamma = 1.0, mu = 1.0;
-  std::vector<int32_t> sizes, off, poff;
+  std::vector<int32_t> sizes, off;
   size_t bytes = 0;
 
   // resident instance
   double* C = nullptr;
-  int32_t *d_off = nullptr, *d_poff = nullptr, *d_row_group = nullptr, *d_row_to_prow = nullptr;
+  int32_t *d_off = nullptr, *d_row_group = nullptr, *d_group_order = nullptr;
   double *d_sqrt_g = nullptr, *d_a = nullptr, *d_b = nullptr;
   // evaluation buffers
   double *x_eval = nullptr, *g_eval = nullptr;
@@ -149,17 +149,16 @@ struct gsot_ctx {
   double prof_bytes[gsot::K_NKINDS] = {};
   int64_t prof_launches[gsot::K_NKINDS] = {};
   int64_t launches = 0;
+  cudaEvent_t timer_a = nullptr, timer_b = nullptr;
 
   gsot::DevProblem problem() const {
     gsot::DevProblem P;
     P.C = C;
-    P.ldc = ldc;
     P.m = m;
     P.n = n;
     P.L = L;
     P.nw = nw;
     P.off = d_off;
-    P.poff = d_poff;
     P.row_group = d_row_group;
     P.sqrt_g = d_sqrt_g;
     P.a = d_a;
@@ -228,7 +227,9 @@ struct gsot_ctx {
       cudaEventDestroy(mk.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
-    void* ptrs[] = {C,        d_off,        d_poff,     d_row_group, d_row_to_prow, d_sqrt_g,
+    if (timer_a) cudaEventDestroy(timer_a);
+    if (timer_b) cudaEventDestroy(timer_b);
+    void* ptrs[] = {C,        d_off,        d_group_order, d_row_group, d_sqrt_g,
                     d_a,      d_b,          x_eval,     g_eval,      rowpart,       colpart,
                     psi,      psicol,       partials,   words,       dense_words,   tasks,
                     dense_tasks, snap_x,    zs,         ks,          os,            dpos,
@@ -263,12 +264,7 @@ void setup_shape(gsot_ctx* c, int64_t m, int64_t n, const int32_t* sizes, int32_
   c->nw = static_cast<int32_t>((n + 31) / 32);
   c->sizes.assign(sizes, sizes + L);
   c->off.assign(static_cast<size_t>(L) + 1, 0);
-  c->poff.assign(static_cast<size_t>(L) + 1, 0);
-  for (int32_t l = 0; l < L; ++l) {
-    c->off[l + 1] = c->off[l] + sizes[l];
-    c->poff[l + 1] = c->poff[l] + ((sizes[l] + 3) / 4) * 4;
-  }
-  c->ldc = c->poff[L];
+  for (int32_t l = 0; l < L; ++l) c->off[l + 1] = c->off[l] + sizes[l];
 }
 
 void init_device(gsot_ctx* c) {
@@ -285,12 +281,12 @@ void init_device(gsot_ctx* c) {
 void alloc_buffers(gsot_ctx* c) {
   size_t* t = &c->bytes;
   const int64_t m = c->m, n = c->n, L = c->L, nw = c->nw, dim = m + n;
-  c->C = dalloc<double>(static_cast<size_t>(c->ldc) * n, t);
-  GSOT_CUDA_CHECK(cudaMemsetAsync(c->C, 0, sizeof(double) * static_cast<size_t>(c->ldc) * n, c->stream));
+  const size_t celems = static_cast<size_t>(32) * nw * m;  // column-tiled, n padded to 32
+  c->C = dalloc<double>(celems, t);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->C, 0, sizeof(double) * celems, c->stream));
   c->d_off = dalloc<int32_t>(L + 1, t);
-  c->d_poff = dalloc<int32_t>(L + 1, t);
+  c->d_group_order = dalloc<int32_t>(L, t);
   c->d_row_group = dalloc<int32_t>(m, t);
-  c->d_row_to_prow = dalloc<int32_t>(m, t);
   c->d_sqrt_g = dalloc<double>(L, t);
   c->d_a = dalloc<double>(m, t);
   c->d_b = dalloc<double>(n, t);
@@ -320,27 +316,26 @@ void alloc_buffers(gsot_ctx* c) {
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->x_eval, 0, sizeof(double) * (dim + 8), c->stream));
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_x, 0, sizeof(double) * (dim + 8), c->stream));
 
-  std::vector<int32_t> row_group(static_cast<size_t>(m)), row_to_prow(static_cast<size_t>(m));
+  std::vector<int32_t> row_group(static_cast<size_t>(m)), order(static_cast<size_t>(L));
   std::vector<double> sqrt_g(static_cast<size_t>(L));
   for (int32_t l = 0; l < L; ++l) {
     sqrt_g[l] = std::sqrt(static_cast<double>(c->sizes[l]));  // screening.hpp:79
-    for (int32_t r = 0; r < c->sizes[l]; ++r) {
-      row_group[c->off[l] + r] = l;
-      row_to_prow[c->off[l] + r] = c->poff[l] + r;
-    }
+    for (int32_t r = 0; r < c->sizes[l]; ++r) row_group[c->off[l] + r] = l;
+    order[l] = l;
   }
+  // dense work list: largest groups (longest per-lane chains) first
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t p, int32_t q) { return c->sizes[p] > c->sizes[q]; });
   GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_off, c->off.data(), sizeof(int32_t) * (L + 1),
                                   cudaMemcpyHostToDevice, c->stream));
-  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_poff, c->poff.data(), sizeof(int32_t) * (L + 1),
+  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_group_order, order.data(), sizeof(int32_t) * L,
                                   cudaMemcpyHostToDevice, c->stream));
   GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_row_group, row_group.data(), sizeof(int32_t) * m,
-                                  cudaMemcpyHostToDevice, c->stream));
-  GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_row_to_prow, row_to_prow.data(), sizeof(int32_t) * m,
                                   cudaMemcpyHostToDevice, c->stream));
   GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_sqrt_g, sqrt_g.data(), sizeof(double) * L,
                                   cudaMemcpyHostToDevice, c->stream));
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_words(c->dense_words, c->L, c->nw, c->n, c->stream); });
-  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->dense_tasks, c->L, c->nw, c->stream); });
+  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->dense_tasks, c->d_group_order, c->L, c->nw, c->stream); });
   // Persistent eval grid: every SM filled to the kernel's occupancy.
   c->eval_grid = c->num_sms * std::max(1, gsot::eval_blocks_per_sm());
   c->sync();
@@ -363,12 +358,11 @@ void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const doubl
     const int64_t row = static_cast<int64_t>(first_bad % static_cast<unsigned long long>(c->m));
     const int64_t col = static_cast<int64_t>(first_bad / static_cast<unsigned long long>(c->m));
     double value = 0.0;
-    const int64_t prow = c->poff[0];
-    (void)prow;
     int32_t l = 0;
     while (c->off[l + 1] <= row) ++l;
-    GSOT_CUDA_CHECK(cudaMemcpy(&value, c->C + col * c->ldc + c->poff[l] + (row - c->off[l]),
-                               sizeof(double), cudaMemcpyDeviceToHost));
+    const int64_t o0 = c->off[l], g = c->sizes[l];
+    const int64_t el = 32 * (c->nw * o0 + (col >> 5) * g + (row - o0)) + (col & 31);
+    GSOT_CUDA_CHECK(cudaMemcpy(&value, c->C + el, sizeof(double), cudaMemcpyDeviceToHost));
     (void)d_src_for_value;
     Error e(GSOT_ERR_NEGATIVE_COST, "cost(" + std::to_string(row) + "," + std::to_string(col) +
                                         ") = " + std::to_string(value) +
@@ -438,7 +432,7 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
         src = staging;
       }
       c->launch(gsot::K_MISC, 16.0 * m * nc, [&] {
-        gsot::launch_relayout(src, m, j0, nc, c->d_row_to_prow, c->ldc, c->C, d_bad, c->stream);
+        gsot::launch_relayout(c->problem(), src, j0, nc, c->C, d_bad, c->stream);
       });
     }
     finish_validation(c, d_bad, a, b, nullptr);
@@ -484,6 +478,7 @@ EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
     tasks = c->tasks;
   }
   const double dense_bytes = 8.0 * c->m * c->n + 8.0 * c->m * c->nw + 16.0 * Ln;
+  const size_t eval_mark = c->marks.size();
   c->launch(gsot::K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : 0.0, [&] {
     gsot::launch_eval(P, d_x, tasks, mode == GSOT_EVAL_DENSE ? max_tasks : -1, words,
                       c->rowpart, c->colpart, c->psi, c->sc, c->eval_grid, c->stream);
@@ -497,6 +492,14 @@ EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
                            c->stream);
   });
   c->fetch_scalars();
+  if (mode == GSOT_EVAL_SCREENED && c->profile && eval_mark < c->marks.size()) {
+    // algorithmic bytes of the screened pass: surviving blocks' cost rows,
+    // row partials of the non-empty chunks, per-block column/psi partials
+    const double surv_blocks =
+        static_cast<double>(c->h_sc->counters[0] + c->h_sc->counters[2]);
+    c->marks[eval_mark].bytes = 8.0 * static_cast<double>(c->h_sc->surv_rows) +
+                                8.0 * static_cast<double>(c->h_sc->task_rows) + 16.0 * surv_blocks;
+  }
   EvalOut o;
   o.objective = c->h_sc->objective;
   o.slope = c->h_sc->slope;
@@ -1241,7 +1244,7 @@ GSOT_API int gsot_cost_matrix_device(const double* src, int64_t m, const double*
     GSOT_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
     GSOT_CUDA_CHECK(cudaMemcpyAsync(ds, src, sizeof(double) * m * d, cudaMemcpyHostToDevice, s));
     GSOT_CUDA_CHECK(cudaMemcpyAsync(dt, tgt, sizeof(double) * n * d, cudaMemcpyHostToDevice, s));
-    gsot::launch_cost_matrix(ds, m, dt, n, d, nullptr, m, d_cost, s);
+    gsot::launch_cost_matrix(ds, m, dt, n, d, nullptr, d_cost, s);
     if (normalize) {
       gsot::launch_max_reduce(d_cost, m * n, part, 148 * 8, part + 148 * 8, ticket, s);
       gsot::launch_scale_div(d_cost, m * n, part + 148 * 8, s);
@@ -1285,12 +1288,13 @@ GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double
                                       cudaMemcpyHostToDevice, c->stream));
       GSOT_CUDA_CHECK(cudaMemcpyAsync(dt, tgt.data(), sizeof(double) * n * d,
                                       cudaMemcpyHostToDevice, c->stream));
+      const gsot::DevProblem TP = c->problem();
       c->launch(gsot::K_MISC, 0, [&] {
-        gsot::launch_cost_matrix(ds, m, dt, n, d, c->d_row_to_prow, c->ldc, c->C, c->stream);
+        gsot::launch_cost_matrix(ds, m, dt, n, d, &TP, c->C, c->stream);
       });
       // padding rows are zero (memset at allocation) and C >= 0, so the max
       // over the padded buffer is max(C).
-      const int64_t count = c->ldc * n;
+      const int64_t count = static_cast<int64_t>(32) * c->nw * m;
       c->launch(gsot::K_MISC, 0, [&] {
         gsot::launch_max_reduce(c->C, count, part, 148 * 8, part + 148 * 8, ticket, c->stream);
       });
@@ -1343,5 +1347,28 @@ GSOT_API int gsot_profile_reset(gsot_ctx* ctx) {
 }
 
 GSOT_API int64_t gsot_kernel_launches(const gsot_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+GSOT_API int gsot_set_device(int32_t device) {
+  return guard([&] { GSOT_CUDA_CHECK(cudaSetDevice(device)); });
+}
+
+GSOT_API int gsot_timer(gsot_ctx* ctx, int op, double* ms) {
+  return guard([&] {
+    checked(ctx);
+    if (!ctx->timer_a) {
+      GSOT_CUDA_CHECK(cudaEventCreate(&ctx->timer_a));
+      GSOT_CUDA_CHECK(cudaEventCreate(&ctx->timer_b));
+    }
+    if (op == 0) {
+      GSOT_CUDA_CHECK(cudaEventRecord(ctx->timer_a, ctx->stream));
+      return;
+    }
+    GSOT_CUDA_CHECK(cudaEventRecord(ctx->timer_b, ctx->stream));
+    GSOT_CUDA_CHECK(cudaEventSynchronize(ctx->timer_b));
+    float e = 0.f;
+    GSOT_CUDA_CHECK(cudaEventElapsedTime(&e, ctx->timer_a, ctx->timer_b));
+    if (ms) *ms = e;
+  });
+}
 
 }  // extern "C"

@@ -20,7 +20,7 @@
 #include <random>
 #include <vector>
 
-#include "gsot_internal.cuh"
+#include "gsot_device.cuh"
 
 namespace gsot {
 
@@ -213,10 +213,11 @@ constexpr int kSlab = 16;
 
 __global__ void __launch_bounds__(256) k_cost(const double* __restrict__ src, int64_t m,
                                               const double* __restrict__ tgt, int64_t n,
-                                              int64_t d, const int32_t* __restrict__ row_to_prow,
-                                              int64_t ldc, double* __restrict__ out) {
+                                              int64_t d, DevProblem T, bool tiled,
+                                              double* __restrict__ out) {
   __shared__ double xs[kSlab][kTile + 1];
   __shared__ double ys[kSlab][kTile + 1];
+  // tx walks columns (coalesced tiled writes), ty rows
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t i0 = blockIdx.x * (int64_t)kTile, j0 = blockIdx.y * (int64_t)kTile;
   double acc[4][4];
@@ -236,9 +237,9 @@ __global__ void __launch_bounds__(256) k_cost(const double* __restrict__ src, in
     for (int kk = 0; kk < kmax; ++kk) {
       double xv[4], yv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) xv[a] = xs[kk][tx + 16 * a];
+      for (int a = 0; a < 4; ++a) xv[a] = xs[kk][ty + 16 * a];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) yv[b] = ys[kk][ty + 16 * b];
+      for (int b = 0; b < 4; ++b) yv[b] = ys[kk][tx + 16 * b];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -251,50 +252,43 @@ __global__ void __launch_bounds__(256) k_cost(const double* __restrict__ src, in
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int64_t i = i0 + tx + 16 * a;
+    const int64_t i = i0 + ty + 16 * a;
     if (i >= m) continue;
-    const int64_t pr = row_to_prow ? row_to_prow[i] : i;
+    int o0 = 0, g = 0;
+    if (tiled) {
+      const int l = T.row_group[i];
+      o0 = T.off[l];
+      g = T.off[l + 1] - o0;
+    }
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int64_t j = j0 + ty + 16 * b;
-      if (j < n) out[j * ldc + pr] = acc[a][b];
+      const int64_t j = j0 + tx + 16 * b;
+      if (j >= n) continue;
+      if (tiled)
+        out[32 * ((int64_t)T.nw * o0 + (j >> 5) * (int64_t)g + (i - o0)) + (j & 31)] = acc[a][b];
+      else
+        out[j * m + i] = acc[a][b];
     }
   }
 }
 
 void launch_cost_matrix(const double* src, int64_t m, const double* tgt, int64_t n, int64_t d,
-                        const int32_t* row_to_prow, int64_t ldc, double* out, cudaStream_t s) {
+                        const DevProblem* tiled, double* out, cudaStream_t s) {
   dim3 grid((unsigned)((m + kTile - 1) / kTile), (unsigned)((n + kTile - 1) / kTile));
-  k_cost<<<grid, 256, 0, s>>>(src, m, tgt, n, d, row_to_prow, ldc, out);
+  DevProblem T{};
+  if (tiled) T = *tiled;
+  k_cost<<<grid, 256, 0, s>>>(src, m, tgt, n, d, T, tiled != nullptr, out);
 }
 
 __global__ void __launch_bounds__(256) k_max(const double* __restrict__ C, int64_t count,
                                              double* __restrict__ partials, double* out,
                                              unsigned int* ticket) {
-  __shared__ double sh[8];
-  __shared__ bool last;
-  double v = 0.0;
+  double v[1] = {0.0};
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x)
-    v = fmax(v, C[e]);
-  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r = 0.0;
-    for (int w = 0; w < 8; ++w) r = fmax(r, sh[w]);
-    partials[blockIdx.x] = r;
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double r = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) r = fmax(r, partials[b]);
-    *out = r;
-    *ticket = 0u;
-  }
+    v[0] = fmax(v[0], C[e]);
+  double r[1];
+  if (last_block_reduce<256, 1>(v, partials, ticket, r, true)) *out = r[0];
 }
 
 void launch_max_reduce(const double* C, int64_t count, double* partials, int nblocks, double* out,

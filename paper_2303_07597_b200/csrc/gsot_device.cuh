@@ -1,0 +1,111 @@
+// gsot_device.cuh — device helpers shared by the kernel translation units
+// (header-only so no relocatable device code is needed).
+#pragma once
+
+#include "gsot_internal.cuh"
+
+namespace gsot {
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// f = (alpha_i + beta_j) - c_ij, regularizer.hpp:57.
+__device__ __forceinline__ double residual(double alpha_i, double beta_j, double c) {
+  return dsub(dadd(alpha_i, beta_j), c);
+}
+
+// Address of row 0 of block (l, j); row r is at [32 * r].
+__device__ __forceinline__ const double* block_ptr(const DevProblem& P, int o0, int g, int64_t j) {
+  return P.C + 32 * ((int64_t)P.nw * o0 + (j >> 5) * (int64_t)g) + (j & 31);
+}
+
+// Warp-wide transpose-reduce of 16 rows: on entry lane t holds v[k] = value of
+// row k for column t; on exit lane t holds, in v[0], the sum over all 32
+// columns of row (t & 15). The butterfly tree is fixed by lane position, so
+// it does not depend on which lanes hold exact zeros.
+__device__ __forceinline__ void transpose_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = up ? v[k] : v[k + o];
+      const double keep = up ? v[k + o] : v[k];
+      v[k] = dadd(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  v[0] = dadd(v[0], __shfl_xor_sync(0xffffffffu, v[0], 16));
+}
+
+// Last-block-done finalisation: every block writes NV partials; the last
+// block to arrive reduces them with all its threads in a fixed order
+// (thread t sums partials t, t+NT, ... sequentially, then a fixed tree).
+template <int NT, int NV>
+__device__ __forceinline__ bool last_block_reduce(const double (&mine)[NV], double* partials,
+                                                  unsigned int* ticket, double (&out)[NV],
+                                                  bool use_max = false) {
+  __shared__ double sh[NT / 32][NV];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double v[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    v[q] = mine[q];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, v[q], o);
+      v[q] = use_max ? fmax(v[q], w) : dadd(v[q], w);
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh[warp][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = sh[0][q];
+      for (int w = 1; w < NT / 32; ++w) s = use_max ? fmax(s, sh[w][q]) : dadd(s, sh[w][q]);
+      partials[blockIdx.x * NV + q] = s;
+    }
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += NT) {
+      const double p = __ldcg(partials + b * NV + q);
+      s = use_max ? fmax(s, p) : dadd(s, p);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, s, o);
+      s = use_max ? fmax(s, w) : dadd(s, w);
+    }
+    v[q] = s;
+  }
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh[warp][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = sh[0][q];
+      for (int w = 1; w < NT / 32; ++w) s = use_max ? fmax(s, sh[w][q]) : dadd(s, sh[w][q]);
+      out[q] = s;
+    }
+    *ticket = 0u;
+  }
+  return threadIdx.x == 0;
+}
+
+
+}  // namespace gsot

@@ -1,9 +1,8 @@
 // gsot_internal.cuh — shared declarations of the sm_100a solver library.
 //
-// Device layout: the cost lives in HBM as a "group-padded
-// column-major" matrix: column j is a run of `ldc` doubles; inside it, group
-// l occupies `g_l` rows starting at padded offset poff[l], a multiple of 4
-// doubles, so every (group, column) block starts on a 32-byte sector.
+// Device layout: the cost lives in HBM column-tiled: for
+// group l and 32-column chunk c, a g_l x 32 row-major tile starting at
+// element 32 * (nw * off_l + c * g_l) (columns >= n are zero padding).
 // Snapshot norms and per-block partials are [l][j] (j fastest) so that the
 // per-block kernels, which put consecutive target columns on consecutive
 // lanes, read and write them coalesced. Bitmasks are [l][c] words over
@@ -45,13 +44,11 @@ struct Error : std::runtime_error {
 
 // Read-only view of the resident instance passed to every kernel by value.
 struct DevProblem {
-  const double* C;        // ldc x n, group-padded column-major
-  int64_t ldc;            // padded rows per column (multiple of 4)
+  const double* C;        // column-tiled cost, 32 * nw * m doubles
   int64_t m, n;           // instance shape
   int32_t L;              // groups
   int32_t nw;             // 32-column chunks: ceil(n / 32)
-  const int32_t* off;     // L+1 unpadded row offsets (alpha indexing)
-  const int32_t* poff;    // L+1 padded row offsets (cost indexing)
+  const int32_t* off;     // L+1 row offsets
   const int32_t* row_group;  // m: group of each row
   const double* sqrt_g;   // L: sqrt(g_l) (screening.hpp:79)
   const double* a;        // m
@@ -67,7 +64,8 @@ struct EvalScalars {
   double dot_aa, dot_bb, psi_sum;
   double extra[3];   // pair kernel: s.y, s.s, y.y
   unsigned long long counters[4];  // in_active, skipped, unskipped, upper_bounds
-  unsigned long long nonzero_blocks;
+  unsigned long long surv_rows;  // sum of g_l over surviving blocks (bytes accounting)
+  unsigned long long task_rows;  // sum of g_l over work-list tasks
   int ntasks;        // screened work-list length
   int next_task;     // dynamic scheduler cursor
   unsigned int ticket;  // last-block-done counter
@@ -90,9 +88,8 @@ enum KernelKind {
   K_NKINDS = 8
 };
 
-void launch_relayout(const double* src_colmajor, int64_t m, int64_t j0, int64_t ncols,
-                     const int32_t* row_to_prow, int64_t ldc, double* C,
-                     unsigned long long* first_bad, cudaStream_t s);
+void launch_relayout(const DevProblem& P, const double* src_colmajor, int64_t j0, int64_t ncols,
+                     double* C, unsigned long long* first_bad, cudaStream_t s);
 void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                      cudaStream_t s);
 void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStream_t s);
@@ -123,7 +120,8 @@ void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* wo
 void launch_audit_active(const DevProblem& P, const double* x, const uint32_t* active_words,
                          EvalScalars* sc, cudaStream_t s);
 void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaStream_t s);
-void launch_dense_tasks(int2* tasks, int32_t L, int32_t nw, cudaStream_t s);
+void launch_dense_tasks(int2* tasks, const int32_t* group_order, int32_t L, int32_t nw,
+                        cudaStream_t s);
 
 // L-BFGS vector kernels (gsot_lbfgs.cu).
 constexpr int kMaxMemory = 64;
@@ -151,8 +149,10 @@ void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, 
                    int slot, cudaStream_t s);
 
 // Cost-matrix construction (gsot_data.cu).
+// tiled == nullptr: column-major m x n output; otherwise the column-tiled
+// layout of that problem.
 void launch_cost_matrix(const double* src, int64_t m, const double* tgt, int64_t n, int64_t d,
-                        const int32_t* row_to_prow, int64_t ldc, double* out, cudaStream_t s);
+                        const DevProblem* tiled, double* out, cudaStream_t s);
 void launch_max_reduce(const double* C, int64_t count, double* partials, int nblocks,
                        double* out, unsigned int* ticket, cudaStream_t s);
 void launch_scale_div(double* C, int64_t count, const double* divisor, cudaStream_t s);

@@ -12,100 +12,69 @@
 // association is fixed by block position and is independent of which
 // blocks the screen skipped, so screened and dense evaluations agree
 // bitwise on every output.
-#include <cooperative_groups.h>
-
-#include "gsot_internal.cuh"
+//
+// Cost layout: column-tiled. For group l (rows off_l ..
+// off_l + g_l) and 32-column chunk c, the tile is g_l rows x 32 columns
+// stored row-major; tile (l, c) starts at element 32 * (nw * off_l + c * g_l).
+// A warp (lane = column) walking the block rows reads one contiguous 256-byte
+// row of the tile per load.
+#include "gsot_device.cuh"
 
 namespace gsot {
 
-namespace {
-
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
-
-// f = (alpha_i + beta_j) - c_ij, regularizer.hpp:57.
-__device__ __forceinline__ double residual(double alpha_i, double beta_j, double c) {
-  return dsub(dadd(alpha_i, beta_j), c);
-}
-
-__device__ __forceinline__ double2 ldg2(const double* p) {
-  return __ldg(reinterpret_cast<const double2*>(p));
-}
-
-// Streaming load: the cost is read once per pass; do not let it evict the
-// small reused vectors from L1.
-__device__ __forceinline__ double2 ldcs2(const double* p) {
-  return __ldcs(reinterpret_cast<const double2*>(p));
-}
-
-// Warp-wide 32x32 transpose-reduce: on entry lane t holds v[k] = value of
-// row k for column t; on exit v[0] on lane t = sum over the 32 columns of
-// row t. The butterfly tree is fixed by lane position, so it is independent
-// of which lanes hold exact zeros.
-__device__ __forceinline__ void transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int k = 0; k < o; ++k) {
-      const double send = up ? v[k] : v[k + o];
-      const double keep = up ? v[k + o] : v[k];
-      v[k] = dadd(keep, __shfl_xor_sync(0xffffffffu, send, o));
+// ---------------------------------------------------------------- relayout
+// Column-major m x n (device) chunk [j0, j0+ncols) -> column-tiled layout,
+// through a 32 x 32 shared-memory transpose (coalesced on both sides), plus
+// validate_instance's first offending entry in j-major order
+// (core.hpp:118-123): min over j*m + i of !(c >= 0) || !isfinite(c).
+__global__ void __launch_bounds__(256) k_relayout(DevProblem P, const double* __restrict__ src,
+                                                  int64_t j0, int64_t ncols,
+                                                  double* __restrict__ C,
+                                                  unsigned long long* first_bad) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = blockIdx.x * 32ll, jj0 = blockIdx.y * 32ll;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  unsigned long long bad = ~0ull;
+  for (int k = ty; k < 32; k += 8) {  // read: lanes along rows
+    const int64_t i = i0 + tx, jj = jj0 + k;
+    double v = 0.0;
+    if (i < P.m && jj < ncols) {
+      v = src[jj * P.m + i];
+      if (!(v >= 0.0) || !isfinite(v)) {
+        const unsigned long long e = (unsigned long long)((j0 + jj) * P.m + i);
+        bad = e < bad ? e : bad;
+      }
+    }
+    tile[k][tx] = v;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {  // write: lanes along columns
+    const int64_t i = i0 + k, jj = jj0 + tx;
+    if (i < P.m && jj < ncols) {
+      const int l = P.row_group[i];
+      const int o0 = P.off[l], g = P.off[l + 1] - o0;
+      const int64_t j = j0 + jj;
+      C[32 * ((int64_t)P.nw * o0 + (j >> 5) * (int64_t)g + (i - o0)) + (j & 31)] = tile[tx][k];
     }
   }
-}
-
-template <int NT>
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-  // Fixed-tree block reduction (warp butterfly, then warps in order).
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < NT / 32; ++w) r = dadd(r, sh[w]);
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = w < bad ? w : bad;
   }
-  return r;  // valid on thread 0
+  if (tx == 0 && bad != ~0ull) atomicMin(first_bad, bad);
 }
 
-}  // namespace
-
-// ---------------------------------------------------------------- relayout
-// Column-major m x n (device) -> group-padded layout, plus the first
-// offending entry of validate_instance's j-major scan (core.hpp:118-123):
-// the minimum linear index j*m + i with !(c >= 0) || !isfinite(c).
-__global__ void k_relayout(const double* __restrict__ src, int64_t m, int64_t j0, int64_t ncols,
-                           const int32_t* __restrict__ row_to_prow, int64_t ldc,
-                           double* __restrict__ C, unsigned long long* first_bad) {
-  const int64_t total = m * ncols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t jj = e / m;
-    const int64_t i = e - jj * m;
-    const double c = src[e];
-    C[(j0 + jj) * ldc + row_to_prow[i]] = c;
-    if (!(c >= 0.0) || !isfinite(c)) atomicMin(first_bad, (unsigned long long)((j0 + jj) * m + i));
-  }
-}
-
-void launch_relayout(const double* src, int64_t m, int64_t j0, int64_t ncols,
-                     const int32_t* row_to_prow, int64_t ldc, double* C,
-                     unsigned long long* first_bad, cudaStream_t s) {
-  const int64_t total = m * ncols;
-  int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  if (grid < 1) grid = 1;
-  k_relayout<<<grid, 256, 0, s>>>(src, m, j0, ncols, row_to_prow, ldc, C, first_bad);
+void launch_relayout(const DevProblem& P, const double* src, int64_t j0, int64_t ncols,
+                     double* C, unsigned long long* first_bad, cudaStream_t s) {
+  dim3 grid((unsigned)((P.m + 31) / 32), (unsigned)((ncols + 31) / 32));
+  k_relayout<<<grid, 256, 0, s>>>(P, src, j0, ncols, C, first_bad);
 }
 
 // ---------------------------------------------------------------- snapshot
 // take_snapshot (screening.hpp:24-50): z~ = |[f]+|, k~ = |f|, o~ = |[f]-|
 // per block, each a sequential sum over the block's rows. One thread per
-// (l, j); consecutive lanes are consecutive columns.
+// (l, j); a warp covers one 32-column tile and reads one 256-byte tile row per
+// load.
 __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __restrict__ x,
                                                   double* __restrict__ zs,
                                                   double* __restrict__ ks,
@@ -113,33 +82,28 @@ __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __
   const int l = blockIdx.y;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= P.n) return;
-  const int g = P.off[l + 1] - P.off[l];
-  const double* __restrict__ al = x + P.off[l];
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const double* __restrict__ al = x + o0;
   const double bj = x[P.m + j];
-  const double* __restrict__ cp = P.C + j * P.ldc + P.poff[l];
+  const double* __restrict__ cp = block_ptr(P, o0, g, j);
   double az = 0.0, ak = 0.0, ao = 0.0;
-#define GSOT_SNAP_STEP(ALPHA, CVAL)            \
-  {                                            \
+#define GSOT_SNAP_STEP(ALPHA, CVAL)                 \
+  {                                                 \
     const double f = residual((ALPHA), bj, (CVAL)); \
-    const double sq = dmul(f, f);              \
-    ak = dadd(ak, sq);                         \
-    az = dadd(az, f > 0.0 ? sq : 0.0);         \
-    ao = dadd(ao, f < 0.0 ? sq : 0.0);         \
+    const double sq = dmul(f, f);                   \
+    ak = dadd(ak, sq);                              \
+    az = dadd(az, f > 0.0 ? sq : 0.0);              \
+    ao = dadd(ao, f < 0.0 ? sq : 0.0);              \
   }
   int r = 0;
   for (; r + 8 <= g; r += 8) {
-    const double2 c0 = ldcs2(cp + r), c1 = ldcs2(cp + r + 2), c2 = ldcs2(cp + r + 4),
-                  c3 = ldcs2(cp + r + 6);
-    GSOT_SNAP_STEP(__ldg(al + r), c0.x);
-    GSOT_SNAP_STEP(__ldg(al + r + 1), c0.y);
-    GSOT_SNAP_STEP(__ldg(al + r + 2), c1.x);
-    GSOT_SNAP_STEP(__ldg(al + r + 3), c1.y);
-    GSOT_SNAP_STEP(__ldg(al + r + 4), c2.x);
-    GSOT_SNAP_STEP(__ldg(al + r + 5), c2.y);
-    GSOT_SNAP_STEP(__ldg(al + r + 6), c3.x);
-    GSOT_SNAP_STEP(__ldg(al + r + 7), c3.y);
+    double c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = __ldcs(cp + 32 * (r + k));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) GSOT_SNAP_STEP(__ldg(al + r + k), c[k]);
   }
-  for (; r < g; ++r) GSOT_SNAP_STEP(__ldg(al + r), __ldcs(cp + r));
+  for (; r < g; ++r) GSOT_SNAP_STEP(__ldg(al + r), __ldcs(cp + 32 * r));
 #undef GSOT_SNAP_STEP
   const int64_t idx = (int64_t)l * P.n + j;
   zs[idx] = sqrt(az);
@@ -153,23 +117,29 @@ void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* k
   k_snapshot<<<grid, 256, 0, s>>>(P, x, zs, ks, os);
 }
 
-// z per block only (block mask, audits): pos_part_norm of each block.
+// Sequential z of one block (pos_part_norm over the block rows).
+__device__ __forceinline__ double block_z(const DevProblem& P, const double* __restrict__ x, int l,
+                                          int64_t j) {
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const double* __restrict__ al = x + o0;
+  const double bj = x[P.m + j];
+  const double* __restrict__ cp = block_ptr(P, o0, g, j);
+  double az = 0.0;
+  for (int r = 0; r < g; ++r) {
+    const double f = residual(__ldg(al + r), bj, cp[32 * r]);
+    const double v = f > 0.0 ? f : 0.0;
+    az = dadd(az, dmul(v, v));
+  }
+  return sqrt(az);
+}
+
+// z per block (block mask).
 __global__ void __launch_bounds__(256) k_block_z(DevProblem P, const double* __restrict__ x,
                                                  double* __restrict__ zout) {
   const int l = blockIdx.y;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= P.n) return;
-  const int g = P.off[l + 1] - P.off[l];
-  const double* __restrict__ al = x + P.off[l];
-  const double bj = x[P.m + j];
-  const double* __restrict__ cp = P.C + j * P.ldc + P.poff[l];
-  double az = 0.0;
-  for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, __ldcs(cp + r));
-    const double v = f > 0.0 ? f : 0.0;
-    az = dadd(az, dmul(v, v));
-  }
-  zout[(int64_t)l * P.n + j] = sqrt(az);
+  zout[(int64_t)l * P.n + j] = block_z(P, x, l, j);
 }
 
 void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStream_t s) {
@@ -179,34 +149,63 @@ void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStre
 
 // ---------------------------------------------------------------- deltas
 // compute_delta_norms (screening.hpp:63-83): per group the sequential
-// pos/full/neg norms of alpha - alpha~, and dbeta = beta - beta~.
-__global__ void k_delta(DevProblem P, const double* __restrict__ x, const double* __restrict__ xs,
-                        double* __restrict__ dpos, double* __restrict__ dfull,
-                        double* __restrict__ dneg, double* __restrict__ dbeta) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < P.L) {
-    const int l = (int)t;
-    const int o0 = P.off[l], g = P.off[l + 1] - o0;
-    double ap = 0.0, af = 0.0, an = 0.0;
-    for (int r = 0; r < g; ++r) {
+// pos/full/neg norms of alpha - alpha~ (one warp per group: the lanes load
+// and square 32 rows at a time, lane 0 runs the three ascending chains), and
+// dbeta = beta - beta~ elementwise.
+__global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __restrict__ x,
+                                               const double* __restrict__ xs,
+                                               double* __restrict__ dpos,
+                                               double* __restrict__ dfull,
+                                               double* __restrict__ dneg,
+                                               double* __restrict__ dbeta, int group_blocks) {
+  if ((int)blockIdx.x >= group_blocks) {
+    const int64_t j = ((int64_t)blockIdx.x - group_blocks) * blockDim.x + threadIdx.x;
+    if (j < P.n) dbeta[j] = dsub(x[P.m + j], xs[P.m + j]);
+    return;
+  }
+  __shared__ double sq_sh[8][32];
+  __shared__ signed char sg_sh[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = blockIdx.x * 8 + warp;
+  if (l >= P.L) return;
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  double ap = 0.0, af = 0.0, an = 0.0;
+  for (int r0 = 0; r0 < g; r0 += 32) {
+    const int r = r0 + lane;
+    double sq = 0.0;
+    signed char sgn = 0;
+    if (r < g) {
       const double da = dsub(x[o0 + r], xs[o0 + r]);
-      const double sq = dmul(da, da);
-      af = dadd(af, sq);
-      ap = dadd(ap, da > 0.0 ? sq : 0.0);
-      an = dadd(an, da < 0.0 ? sq : 0.0);
+      sq = dmul(da, da);
+      sgn = da > 0.0 ? 1 : (da < 0.0 ? -1 : 0);
     }
+    sq_sh[warp][lane] = sq;
+    sg_sh[warp][lane] = sgn;
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = min(32, g - r0);
+      for (int k = 0; k < cnt; ++k) {
+        const double s = sq_sh[warp][k];
+        const signed char sg = sg_sh[warp][k];
+        af = dadd(af, s);
+        ap = dadd(ap, sg > 0 ? s : 0.0);
+        an = dadd(an, sg < 0 ? s : 0.0);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
     dpos[l] = sqrt(ap);
     dfull[l] = sqrt(af);
     dneg[l] = sqrt(an);
   }
-  const int64_t j = t - P.L;
-  if (j >= 0 && j < P.n) dbeta[j] = dsub(x[P.m + j], xs[P.m + j]);
 }
 
 void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
                   double* dfull, double* dneg, double* dbeta, cudaStream_t s) {
-  const int64_t total = P.L + P.n;
-  k_delta<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(P, x, xs, dpos, dfull, dneg, dbeta);
+  const int gb = (P.L + 7) / 8;
+  const int bb = (int)((P.n + 255) / 256);
+  k_delta<<<gb + bb, 256, 0, s>>>(P, x, xs, dpos, dfull, dneg, dbeta, gb);
 }
 
 // ---------------------------------------------------------------- active set
@@ -253,18 +252,16 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
 // skipped iff z_bar <= tau. Writes the survivor word of each (l, c) chunk
 // and appends non-empty chunks to the work list (order irrelevant: every
-// task writes fixed slots).
+// task writes fixed slots). A block of 256 threads covers 8 chunks of one
+// group; counters are block-aggregated before one atomic per counter.
 __global__ void __launch_bounds__(256) k_bounds(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
                                                 const double* __restrict__ dpos,
                                                 const double* __restrict__ dbeta,
                                                 double ub_offset, uint32_t* __restrict__ words,
                                                 int2* __restrict__ tasks, EvalScalars* sc) {
-  __shared__ unsigned long long cnt[4];
-  __shared__ int wtask[8];
+  __shared__ unsigned long long cnt[8][5];
   __shared__ int base;
-  if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
-  __syncthreads();
   const int l = blockIdx.y;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -284,26 +281,33 @@ __global__ void __launch_bounds__(256) k_bounds(DevProblem P, const double* __re
   const unsigned wa = __ballot_sync(0xffffffffu, in_active);
   const unsigned we = __ballot_sync(0xffffffffu, evaluated);
   const unsigned ws = __ballot_sync(0xffffffffu, surv);
+  const int g = P.off[l + 1] - P.off[l];
   if (lane == 0) {
     if (c < P.nw) words[(int64_t)l * P.nw + c] = ws;
-    atomicAdd(&cnt[0], (unsigned long long)__popc(wa));
-    atomicAdd(&cnt[1], (unsigned long long)__popc(we & ~ws));
-    atomicAdd(&cnt[2], (unsigned long long)__popc(we & ws));
-    atomicAdd(&cnt[3], (unsigned long long)__popc(we));
-    wtask[warp] = (ws != 0u && c < P.nw) ? 1 : 0;
+    cnt[warp][0] = __popc(wa);
+    cnt[warp][1] = __popc(we & ~ws);
+    cnt[warp][2] = __popc(we & ws);
+    cnt[warp][3] = __popc(we);
+    cnt[warp][4] = (ws != 0u && c < P.nw) ? 1 : 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int nt = 0;
-    for (int w = 0; w < 8; ++w) nt += wtask[w];
-    base = nt ? atomicAdd(&sc->ntasks, nt) : 0;
+    unsigned long long t[5] = {0, 0, 0, 0, 0};
+    for (int w = 0; w < 8; ++w)
+      for (int q = 0; q < 5; ++q) t[q] += cnt[w][q];
+    base = t[4] ? atomicAdd(&sc->ntasks, (int)t[4]) : 0;
     for (int q = 0; q < 4; ++q)
-      if (cnt[q]) atomicAdd(&sc->counters[q], cnt[q]);
+      if (t[q]) atomicAdd(&sc->counters[q], t[q]);
+    const unsigned long long surv_blocks = t[0] + t[2];
+    if (surv_blocks) {
+      atomicAdd(&sc->surv_rows, surv_blocks * (unsigned long long)g);
+      atomicAdd(&sc->task_rows, t[4] * (unsigned long long)g);
+    }
   }
   __syncthreads();
-  if (lane == 0 && wtask[warp]) {
+  if (lane == 0 && cnt[warp][4]) {
     int pos = base;
-    for (int w = 0; w < warp; ++w) pos += wtask[w];
+    for (int w = 0; w < warp; ++w) pos += (int)cnt[w][4];
     tasks[pos] = make_int2(l, (int)c);
   }
 }
@@ -327,14 +331,17 @@ void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaSt
   const int64_t total = (int64_t)L * nw;
   k_fill_words<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(words, L, nw, n);
 }
-__global__ void k_dense_tasks(int2* tasks, int32_t L, int32_t nw) {
+// Dense task order: largest groups first (long chains start early).
+__global__ void k_dense_tasks(int2* tasks, const int32_t* __restrict__ order, int32_t L,
+                              int32_t nw) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)L * nw) return;
-  tasks[t] = make_int2((int)(t / nw), (int)(t % nw));
+  tasks[t] = make_int2(order[t / nw], (int)(t % nw));
 }
-void launch_dense_tasks(int2* tasks, int32_t L, int32_t nw, cudaStream_t s) {
+void launch_dense_tasks(int2* tasks, const int32_t* order, int32_t L, int32_t nw,
+                        cudaStream_t s) {
   const int64_t total = (int64_t)L * nw;
-  k_dense_tasks<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(tasks, L, nw);
+  k_dense_tasks<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(tasks, order, L, nw);
 }
 
 // ---------------------------------------------------------------- fused eval
@@ -343,7 +350,7 @@ void launch_dense_tasks(int2* tasks, int32_t L, int32_t nw, cudaStream_t s) {
 // rows): z^2 = sum [f]+^2 and sum [f]+. Then scale = (1 - tau/z)/gamma when
 // z > tau (grad_block, regularizer.hpp:64-74), psi = (z - tau)^2 / (2 gamma)
 // (the closed form of psi_block, regularizer.hpp:78-91),
-// column partial scale * sum [f]+. Pass 2 (32 rows at a time): plan entries
+// column partial scale * sum [f]+. Pass 2 (16 rows at a time): plan entries
 // T = scale * [f]+, transpose-reduced across the warp into per-row partials
 // of the chunk, stored at rowpart[c * m + row]. The plan is never stored.
 __global__ void __launch_bounds__(256) k_eval(DevProblem P, const double* __restrict__ x,
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(256) k_eval(DevProblem P, const double* __rest
                                               double* __restrict__ colpart,
                                               double* __restrict__ psi, EvalScalars* sc) {
   const int lane = threadIdx.x & 31;
-  const int ntasks = dense_ntasks >= 0 ? dense_ntasks : sc->ntasks;
+  const int ntasks = dense_ntasks >= 0 ? dense_ntasks : *(volatile int*)&sc->ntasks;
   for (;;) {
     int t = 0;
     if (lane == 0) t = atomicAdd(&sc->next_task, 1);
@@ -368,32 +375,27 @@ __global__ void __launch_bounds__(256) k_eval(DevProblem P, const double* __rest
     const int g = P.off[l + 1] - o0;
     const double* __restrict__ al = x + o0;
     const double bj = act ? x[P.m + j] : 0.0;
-    const double* __restrict__ cp = P.C + (act ? j : 0) * P.ldc + P.poff[l];
+    const double* __restrict__ cp = block_ptr(P, o0, g, j);
 
     // pass 1
     double z2 = 0.0, sv = 0.0;
     if (act) {
-#define GSOT_P1(ALPHA, CVAL)                          \
-  {                                                   \
-    const double f = residual((ALPHA), bj, (CVAL));   \
-    const double v = f > 0.0 ? f : 0.0;               \
-    z2 = dadd(z2, dmul(v, v));                        \
-    sv = dadd(sv, v);                                 \
+#define GSOT_P1(ALPHA, CVAL)                        \
+  {                                                 \
+    const double f = residual((ALPHA), bj, (CVAL)); \
+    const double v = f > 0.0 ? f : 0.0;             \
+    z2 = dadd(z2, dmul(v, v));                      \
+    sv = dadd(sv, v);                               \
   }
       int r = 0;
       for (; r + 8 <= g; r += 8) {
-        const double2 c0 = ldg2(cp + r), c1 = ldg2(cp + r + 2), c2 = ldg2(cp + r + 4),
-                      c3 = ldg2(cp + r + 6);
-        GSOT_P1(__ldg(al + r), c0.x);
-        GSOT_P1(__ldg(al + r + 1), c0.y);
-        GSOT_P1(__ldg(al + r + 2), c1.x);
-        GSOT_P1(__ldg(al + r + 3), c1.y);
-        GSOT_P1(__ldg(al + r + 4), c2.x);
-        GSOT_P1(__ldg(al + r + 5), c2.y);
-        GSOT_P1(__ldg(al + r + 6), c3.x);
-        GSOT_P1(__ldg(al + r + 7), c3.y);
+        double cc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cc[k] = __ldg(cp + 32 * (r + k));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) GSOT_P1(__ldg(al + r + k), cc[k]);
       }
-      for (; r < g; ++r) GSOT_P1(__ldg(al + r), __ldg(cp + r));
+      for (; r < g; ++r) GSOT_P1(__ldg(al + r), __ldg(cp + 32 * r));
 #undef GSOT_P1
     }
     const double z = sqrt(z2);
@@ -416,22 +418,19 @@ __global__ void __launch_bounds__(256) k_eval(DevProblem P, const double* __rest
       continue;
     }
     // pass 2
-    for (int r0 = 0; r0 < g; r0 += 32) {
-      double v[32];
+    for (int r0 = 0; r0 < g; r0 += 16) {
+      double v[16];
 #pragma unroll
-      for (int k = 0; k < 32; k += 2) {
+      for (int k = 0; k < 16; ++k) {
         const int r = r0 + k;
-        double2 cc = make_double2(0.0, 0.0);
-        if (nz && r < g) cc = ldg2(cp + r);  // r even, rows r, r+1 within the padded block
-        const double a0 = r < g ? __ldg(al + r) : 0.0;
-        const double a1 = r + 1 < g ? __ldg(al + r + 1) : 0.0;
-        const double f0 = residual(a0, bj, cc.x);
-        const double f1 = residual(a1, bj, cc.y);
-        v[k] = (nz && r < g && f0 > 0.0) ? dmul(scale, f0) : 0.0;
-        v[k + 1] = (nz && r + 1 < g && f1 > 0.0) ? dmul(scale, f1) : 0.0;
+        const bool in = nz && r < g;
+        const double cc = in ? __ldg(cp + 32 * r) : 0.0;
+        const double a = r < g ? __ldg(al + r) : 0.0;
+        const double f = residual(a, bj, cc);
+        v[k] = (in && f > 0.0) ? dmul(scale, f) : 0.0;
       }
-      transpose_reduce32(v, lane);
-      if (r0 + lane < g) rp[r0 + lane] = v[0];
+      transpose_reduce16(v, lane);
+      if (lane < 16 && r0 + lane < g) rp[r0 + lane] = v[0];
     }
   }
 }
@@ -449,103 +448,100 @@ void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int de
 }
 
 // ---------------------------------------------------------------- finalize
-// grad_alpha_i = a_i - sum over non-empty chunks c (ascending) of
-// rowpart[c*m+i]; grad_beta_j = b_j - sum over surviving l (ascending) of
-// colpart[l][j]; psicol_j = sum over surviving l of psi[l][j]. Empty
-// chunks and skipped blocks contribute exact zeros, so omitting them is
-// exact: the result does not depend on the screen.
+// grad_alpha_i = a_i - sum over non-empty chunks c of rowpart[c*m+i];
+// grad_beta_j = b_j - sum over surviving l of colpart[l][j]; psicol_j = sum
+// over surviving l of psi[l][j]. Each sum has a FIXED association: 8 slices
+// (c = s mod 8 resp. l = s mod 8), each sequential in ascending order, then
+// the 8 slice partials in slice order. Empty chunks and skipped blocks
+// contribute exact zeros, so omitting them leaves every partial unchanged:
+// the result does not depend on the screen.
+// Block (32, 8): blocks [0, m/32) handle 32 rows, the rest 32 columns.
 __global__ void __launch_bounds__(256) k_finalize(DevProblem P, const uint32_t* __restrict__ words,
                                                   const double* __restrict__ rowpart,
                                                   const double* __restrict__ colpart,
                                                   const double* __restrict__ psi,
                                                   double* __restrict__ grad,
-                                                  double* __restrict__ psicol) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < P.m) {
-    const int64_t i = t;
-    const int l = P.row_group[i];
-    const uint32_t* __restrict__ wl = words + (int64_t)l * P.nw;
+                                                  double* __restrict__ psicol, int row_blocks) {
+  __shared__ double sh[2][8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if ((int)blockIdx.x < row_blocks) {
+    const int64_t i = blockIdx.x * 32ll + tx;
     double acc = 0.0;
-    for (int c = 0; c < P.nw; ++c)
-      if (wl[c]) acc = dadd(acc, rowpart[(int64_t)c * P.m + i]);
-    grad[i] = dsub(P.a[i], acc);
+    if (i < P.m) {
+      const int l = P.row_group[i];
+      const uint32_t* __restrict__ wl = words + (int64_t)l * P.nw;
+      for (int c = ty; c < P.nw; c += 8)
+        if (wl[c]) acc = dadd(acc, rowpart[(int64_t)c * P.m + i]);
+    }
+    sh[0][ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && i < P.m) {
+      double s = sh[0][0][tx];
+      for (int q = 1; q < 8; ++q) s = dadd(s, sh[0][q][tx]);
+      grad[i] = dsub(P.a[i], s);
+    }
     return;
   }
-  const int64_t j = t - P.m;
-  if (j >= P.n) return;
-  const int64_t c = j >> 5;
-  const int lane = (int)(j & 31);
+  const int64_t j = (blockIdx.x - row_blocks) * 32ll + tx;
   double acc = 0.0, ps = 0.0;
-  for (int l = 0; l < P.L; ++l) {
-    if ((words[(int64_t)l * P.nw + c] >> lane) & 1u) {
-      acc = dadd(acc, colpart[(int64_t)l * P.n + j]);
-      ps = dadd(ps, psi[(int64_t)l * P.n + j]);
+  if (j < P.n) {
+    const int64_t c = j >> 5;
+    for (int l = ty; l < P.L; l += 8) {
+      if ((words[(int64_t)l * P.nw + c] >> tx) & 1u) {
+        acc = dadd(acc, colpart[(int64_t)l * P.n + j]);
+        ps = dadd(ps, psi[(int64_t)l * P.n + j]);
+      }
     }
   }
-  grad[P.m + j] = dsub(P.b[j], acc);
-  psicol[j] = ps;
+  sh[0][ty][tx] = acc;
+  sh[1][ty][tx] = ps;
+  __syncthreads();
+  if (ty == 0 && j < P.n) {
+    double s = sh[0][0][tx], p = sh[1][0][tx];
+    for (int q = 1; q < 8; ++q) {
+      s = dadd(s, sh[0][q][tx]);
+      p = dadd(p, sh[1][q][tx]);
+    }
+    grad[P.m + j] = dsub(P.b[j], s);
+    psicol[j] = p;
+  }
 }
 
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const double* rowpart, const double* colpart, const double* psi,
                      double* grad, double* psicol, cudaStream_t s) {
   (void)x;
-  const int64_t total = P.m + P.n;
-  k_finalize<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(P, words, rowpart, colpart, psi,
-                                                            grad, psicol);
+  const int rb = (int)((P.m + 31) / 32);
+  const int cb = (int)((P.n + 31) / 32);
+  k_finalize<<<rb + cb, 256, 0, s>>>(P, words, rowpart, colpart, psi, grad, psicol, rb);
 }
 
 // Objective a.alpha + b.beta - sum psi (dual.hpp:51) and optionally the
-// line-search slope grad.d, as fixed-structure reductions: grid-stride
-// partials per block, then the last block to finish sums the partials in
-// block order.
+// line-search slope grad.d, as fixed-structure reductions.
 __global__ void __launch_bounds__(256) k_objective(DevProblem P, const double* __restrict__ x,
                                                    const double* __restrict__ psicol,
                                                    const double* __restrict__ grad,
                                                    const double* __restrict__ dvec,
                                                    double* __restrict__ partials,
                                                    EvalScalars* sc) {
-  __shared__ double sh[8];
-  __shared__ bool last;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t dim = P.m + P.n;
-  double pa = 0.0, pb = 0.0, pp = 0.0, pd = 0.0;
-  for (int64_t i = t0; i < P.m; i += stride) pa = dadd(pa, dmul(x[i], P.a[i]));
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = t0; i < P.m; i += stride) p[0] = dadd(p[0], dmul(x[i], P.a[i]));
   for (int64_t j = t0; j < P.n; j += stride) {
-    pb = dadd(pb, dmul(x[P.m + j], P.b[j]));
-    pp = dadd(pp, psicol[j]);
+    p[1] = dadd(p[1], dmul(x[P.m + j], P.b[j]));
+    p[2] = dadd(p[2], psicol[j]);
   }
   if (dvec)
-    for (int64_t i = t0; i < dim; i += stride) pd = dadd(pd, dmul(grad[i], dvec[i]));
-  const double ra = block_sum<256>(pa, sh);
-  const double rb = block_sum<256>(pb, sh);
-  const double rp = block_sum<256>(pp, sh);
-  const double rd = block_sum<256>(pd, sh);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x * 4 + 0] = ra;
-    partials[blockIdx.x * 4 + 1] = rb;
-    partials[blockIdx.x * 4 + 2] = rp;
-    partials[blockIdx.x * 4 + 3] = rd;
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double sa = 0.0, sb = 0.0, sp = 0.0, sd = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      sa = dadd(sa, partials[b * 4 + 0]);
-      sb = dadd(sb, partials[b * 4 + 1]);
-      sp = dadd(sp, partials[b * 4 + 2]);
-      sd = dadd(sd, partials[b * 4 + 3]);
-    }
-    sc->dot_aa = sa;
-    sc->dot_bb = sb;
-    sc->psi_sum = sp;
-    sc->objective = dsub(dadd(sa, sb), sp);
-    sc->slope = sd;
-    sc->ticket = 0u;
+    for (int64_t i = t0; i < dim; i += stride) p[3] = dadd(p[3], dmul(grad[i], dvec[i]));
+  double out[4];
+  if (last_block_reduce<256, 4>(p, partials, &sc->ticket, out)) {
+    sc->dot_aa = out[0];
+    sc->dot_bb = out[1];
+    sc->psi_sum = out[2];
+    sc->objective = dsub(dadd(out[0], out[1]), out[2]);
+    sc->slope = out[3];
   }
 }
 
@@ -568,14 +564,8 @@ __global__ void __launch_bounds__(256) k_plan(DevProblem P, const double* __rest
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
   const double* __restrict__ al = x + o0;
   const double bj = x[P.m + j];
-  const double* __restrict__ cp = P.C + j * P.ldc + P.poff[l];
-  double z2 = 0.0;
-  for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, cp[r]);
-    const double v = f > 0.0 ? f : 0.0;
-    z2 = dadd(z2, dmul(v, v));
-  }
-  const double z = sqrt(z2);
+  const double* __restrict__ cp = block_ptr(P, o0, g, j);
+  const double z = block_z(P, x, l, j);
   double* __restrict__ o = out + jj * P.m + o0;
   if (z <= P.tau) {
     for (int r = 0; r < g; ++r) o[r] = 0.0;
@@ -583,7 +573,7 @@ __global__ void __launch_bounds__(256) k_plan(DevProblem P, const double* __rest
   }
   const double scale = ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma);
   for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, cp[r]);
+    const double f = residual(__ldg(al + r), bj, cp[32 * r]);
     o[r] = f > 0.0 ? dmul(scale, f) : 0.0;
   }
 }
@@ -608,18 +598,8 @@ __global__ void __launch_bounds__(256) k_audit_skips(DevProblem P, const double*
   const int lane = (int)(j & 31);
   const bool surv = (words[(int64_t)l * P.nw + c] >> lane) & 1u;
   if (surv) return;
-  const int g = P.off[l + 1] - P.off[l];
-  const double* __restrict__ al = x + P.off[l];
-  const double bj = x[P.m + j];
-  const double* __restrict__ cp = P.C + j * P.ldc + P.poff[l];
-  double z2 = 0.0;
-  for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, cp[r]);
-    const double v = f > 0.0 ? f : 0.0;
-    z2 = dadd(z2, dmul(v, v));
-  }
   atomicAdd(&sc->counters[0], 1ull);
-  if (!(sqrt(z2) <= P.tau)) {
+  if (!(block_z(P, x, l, j) <= P.tau)) {
     if (atomicCAS(&sc->audit_violation, 0, 1) == 0) sc->audit_where = (long long)l * P.n + j;
   }
   (void)aw;
@@ -640,18 +620,8 @@ __global__ void __launch_bounds__(256) k_audit_active(DevProblem P, const double
   if (j >= P.n) return;
   const bool in = (aw[(int64_t)l * P.nw + (j >> 5)] >> (j & 31)) & 1u;
   if (!in) return;
-  const int g = P.off[l + 1] - P.off[l];
-  const double* __restrict__ al = x + P.off[l];
-  const double bj = x[P.m + j];
-  const double* __restrict__ cp = P.C + j * P.ldc + P.poff[l];
-  double z2 = 0.0;
-  for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, cp[r]);
-    const double v = f > 0.0 ? f : 0.0;
-    z2 = dadd(z2, dmul(v, v));
-  }
   atomicAdd(&sc->counters[1], 1ull);
-  if (!(sqrt(z2) > P.tau)) {
+  if (!(block_z(P, x, l, j) > P.tau)) {
     if (atomicCAS(&sc->audit_violation, 0, 2) == 0) sc->audit_where = (long long)l * P.n + j;
   }
 }

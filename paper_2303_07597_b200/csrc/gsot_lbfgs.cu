@@ -4,137 +4,152 @@
 // scalars cross PCIe.
 //
 // The two-loop recursion (lbfgs.hpp:109-124) runs as ONE launch of a
-// cluster of kCluster CTAs. Each CTA owns a contiguous slice of the vectors;
-// every dot product is reduced inside the CTA (fixed tree), published to
-// shared memory and summed by every CTA over the cluster ranks in rank order
-// through distributed shared memory, so all CTAs see the same bits and the
-// result is deterministic. Dots are fused with the axpy that precedes them,
-// so the recursion makes 2k+1 passes over the history instead of 4k+3.
-// Elementwise arithmetic keeps the reference's one-rounding-per-operation
-// form (q - a*y, q*c, q + (a-b)*s, x + t*d).
+// thread-block cluster (16 CTAs where the device allows non-portable
+// clusters, else 8). Each CTA owns a contiguous slice of the vectors and keeps
+// its slice of q in shared memory; every dot product is reduced inside the
+// CTA (fixed tree), published in shared memory and summed by every CTA over
+// the cluster ranks in rank order through distributed shared memory, so all
+// CTAs see the same bits and the result is deterministic. Dots are fused with
+// the update that precedes them: the recursion makes 2k+1 passes over the
+// history instead of 4k+3. Elementwise arithmetic keeps the reference's
+// one-rounding-per-operation form (q - a*y, q*c, q + (a-b)*s, x + t*d).
 #include <cooperative_groups.h>
 
-#include "gsot_internal.cuh"
+#include "gsot_device.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace gsot {
 
 namespace {
-constexpr int kCluster = 8;
 constexpr int kTwoLoopThreads = 512;
-
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+constexpr int kWarps = kTwoLoopThreads / 32;
+int g_cluster = 0;           // chosen cluster size (16 or 8)
+size_t g_two_loop_smem = 0;  // dynamic smem configured so far
 }  // namespace
 
-// Cluster-wide deterministic dot reduction. `part` is this thread's partial.
-// Uses slot `parity` of the per-CTA publication buffer; one cluster.sync.
+// Cluster-wide deterministic sum. `part` is this thread's partial. Uses slot
+// `parity` of the per-CTA publication buffer; one cluster barrier.
 __device__ __forceinline__ double cluster_sum(cg::cluster_group& cluster, double part,
-                                              double* warp_sh, double* pub, int parity) {
+                                              double* warp_sh, double* pub, double* tot_sh,
+                                              int parity, int nranks) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) part = dadd(part, __shfl_xor_sync(0xffffffffu, part, o));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) warp_sh[warp] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kTwoLoopThreads / 32; ++w) s = dadd(s, warp_sh[w]);
+    double s = warp_sh[0];
+    for (int w = 1; w < kWarps; ++w) s = dadd(s, warp_sh[w]);
     pub[parity] = s;
   }
   cluster.sync();
-  double tot = 0.0;
-  for (int r = 0; r < kCluster; ++r) {
-    const double* remote = cluster.map_shared_rank(pub, r);
-    tot = dadd(tot, remote[parity]);
+  if (warp == 0) {
+    double v = 0.0;
+    if (lane < nranks) v = cluster.map_shared_rank(pub, lane)[parity];
+    // rank-ordered sequential sum on lane 0
+    double t = 0.0;
+    for (int r = 0; r < nranks; ++r) t = dadd(t, __shfl_sync(0xffffffffu, v, r));
+    if (lane == 0) tot_sh[parity] = t;
   }
-  return tot;
+  __syncthreads();
+  return tot_sh[parity];
 }
 
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kTwoLoopThreads)
-    k_two_loop(const TwoLoopArgs A) {
+__global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs A, int use_smem) {
+  extern __shared__ double q_dyn[];
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ double warp_sh[kTwoLoopThreads / 32];
+  __shared__ double warp_sh[kWarps];
   __shared__ double pub[2];
+  __shared__ double tot_sh[2];
   __shared__ double a_sh[kMaxMemory];
+  const int nranks = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
-  const int64_t per = (A.dim + kCluster - 1) / kCluster;
+  const int64_t per = (A.dim + nranks - 1) / nranks;
   const int64_t lo = rank * per;
   const int64_t hi = min(A.dim, lo + per);
-  double* __restrict__ q = A.d;  // q is built in place in the output vector
+  const int64_t len = hi > lo ? hi - lo : 0;
+  // q slice: shared memory when it fits, else the output vector itself
+  double* __restrict__ q = use_smem ? q_dyn : A.d + lo;
+  const double* __restrict__ g = A.g + lo;
   const int k = A.k;
   int parity = 0;
 
-  // q = g; pass for i = k-1: a_{k-1} = rho * s_{k-1}.q
-  // Generic pass i (loop 1): q -= a_{i+1} * y_{i+1}; a_i = rho_i * s_i.q
+  // Loop 1 (lbfgs.hpp:112-115). Pass i: q -= a_{i+1} y_{i+1} (or q = g for
+  // the first pass), then a_i = rho_i * s_i . q.
   for (int i = k - 1; i >= 0; --i) {
     double part = 0.0;
-    const double* __restrict__ si = A.s[i];
+    const double* __restrict__ si = A.s[i] + lo;
     if (i == k - 1) {
-      for (int64_t e = lo + threadIdx.x; e < hi; e += kTwoLoopThreads) {
-        const double qe = A.g[e];
+#pragma unroll 4
+      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
+        const double qe = g[e];
         q[e] = qe;
         part = dadd(part, dmul(si[e], qe));
       }
     } else {
       const double ap = a_sh[i + 1];
-      const double* __restrict__ yp = A.y[i + 1];
-      for (int64_t e = lo + threadIdx.x; e < hi; e += kTwoLoopThreads) {
+      const double* __restrict__ yp = A.y[i + 1] + lo;
+#pragma unroll 4
+      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
         const double qe = dsub(q[e], dmul(ap, yp[e]));
         q[e] = qe;
         part = dadd(part, dmul(si[e], qe));
       }
     }
-    const double dot = cluster_sum(cluster, part, warp_sh, pub, parity);
+    const double dot = cluster_sum(cluster, part, warp_sh, pub, tot_sh, parity, nranks);
     parity ^= 1;
     if (threadIdx.x == 0) a_sh[i] = dmul(A.rho[i], dot);
     __syncthreads();
   }
   // Close loop 1 (q -= a_0 y_0), scale by s.y / y.y (lbfgs.hpp:116-119), and
   // run loop 2 (lbfgs.hpp:120-123) fused: pass i applies the update of i-1
-  // and reduces y_i.q.
+  // and reduces y_i . q.
   double b_prev = 0.0;
   for (int i = 0; i <= k; ++i) {
     double part = 0.0;
     const bool last = (i == k);
-    const double* __restrict__ yi = last ? nullptr : A.y[i];
     if (k == 0) {
-      // No history: d = g.
-      for (int64_t e = lo + threadIdx.x; e < hi; e += kTwoLoopThreads) q[e] = A.g[e];
+      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) q[e] = g[e];  // d = g
     } else if (i == 0) {
       const double a0 = a_sh[0];
-      const double* __restrict__ y0 = A.y[0];
-      for (int64_t e = lo + threadIdx.x; e < hi; e += kTwoLoopThreads) {
+      const double* __restrict__ y0 = A.y[0] + lo;
+#pragma unroll 4
+      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
         double qe = dsub(q[e], dmul(a0, y0[e]));
         if (A.apply_scale) qe = dmul(qe, A.gamma_scale);
         q[e] = qe;
-        part = dadd(part, dmul(yi[e], qe));
+        part = dadd(part, dmul(y0[e], qe));
       }
     } else {
       const double coef = dsub(a_sh[i - 1], b_prev);
-      const double* __restrict__ sp = A.s[i - 1];
-      for (int64_t e = lo + threadIdx.x; e < hi; e += kTwoLoopThreads) {
+      const double* __restrict__ sp = A.s[i - 1] + lo;
+      const double* __restrict__ yi = last ? nullptr : A.y[i] + lo;
+#pragma unroll 4
+      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
         const double qe = dadd(q[e], dmul(coef, sp[e]));
         q[e] = qe;
         if (!last) part = dadd(part, dmul(yi[e], qe));
       }
     }
     if (last) break;
-    const double dot = cluster_sum(cluster, part, warp_sh, pub, parity);
+    const double dot = cluster_sum(cluster, part, warp_sh, pub, tot_sh, parity, nranks);
     parity ^= 1;
     b_prev = dmul(A.rho[i], dot);
   }
-  // dir_slope = g.d and |d|^2 (lbfgs.hpp:126, :152).
+  // d = q; dir_slope = g . d and |d|^2 (lbfgs.hpp:124-126, :152).
   double pg = 0.0, pd = 0.0;
-  for (int64_t e = lo + threadIdx.x; e < hi; e += kTwoLoopThreads) {
+  double* __restrict__ d = A.d + lo;
+#pragma unroll 4
+  for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
     const double de = q[e];
-    pg = dadd(pg, dmul(A.g[e], de));
+    if (use_smem) d[e] = de;
+    pg = dadd(pg, dmul(g[e], de));
     pd = dadd(pd, dmul(de, de));
   }
-  const double gd = cluster_sum(cluster, pg, warp_sh, pub, parity);
+  const double gd = cluster_sum(cluster, pg, warp_sh, pub, tot_sh, parity, nranks);
   parity ^= 1;
-  const double dd = cluster_sum(cluster, pd, warp_sh, pub, parity);
+  const double dd = cluster_sum(cluster, pd, warp_sh, pub, tot_sh, parity, nranks);
   if (rank == 0 && threadIdx.x == 0) {
     A.out[0] = gd;
     A.out[1] = dd;
@@ -143,7 +158,48 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kTwoLoopThrea
 }
 
 void launch_two_loop(const TwoLoopArgs& a, cudaStream_t s) {
-  k_two_loop<<<kCluster, kTwoLoopThreads, 0, s>>>(a);
+  if (g_cluster == 0) {
+    g_cluster = 8;
+    if (cudaFuncSetAttribute(k_two_loop, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = 16;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(kTwoLoopThreads);
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, k_two_loop, &cfg) == cudaSuccess &&
+          nclusters > 0)
+        g_cluster = 16;
+    }
+    cudaGetLastError();
+  }
+  const int64_t per = (a.dim + g_cluster - 1) / g_cluster;
+  size_t smem = sizeof(double) * (size_t)per;
+  int use_smem = smem <= 200 * 1024 ? 1 : 0;
+  if (!use_smem) smem = 0;
+  if (smem > g_two_loop_smem) {
+    cudaFuncSetAttribute(k_two_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    g_two_loop_smem = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = g_cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.gridDim = dim3(g_cluster);
+  cfg.blockDim = dim3(kTwoLoopThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_two_loop, a, use_smem);
 }
 
 // trial.x = x + t * d (lbfgs.hpp:86).
@@ -160,21 +216,6 @@ void launch_axpy_point(const double* x, double t, const double* d, double* out, 
   k_axpy_point<<<grid, 256, 0, s>>>(x, t, d, out, dim);
 }
 
-namespace {
-__device__ __forceinline__ double block_sum256(double v, double* sh) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < 8; ++w) r = dadd(r, sh[w]);
-  return r;
-}
-}  // namespace
-
 // Curvature pair (lbfgs.hpp:243-246): s = trial.x - x, y = g - trial.g
 // written to the ring slot, plus s.y, s.s, y.y (deterministic).
 __global__ void __launch_bounds__(256) k_pair(const double* __restrict__ xt,
@@ -184,42 +225,22 @@ __global__ void __launch_bounds__(256) k_pair(const double* __restrict__ xt,
                                               double* __restrict__ sv, double* __restrict__ yv,
                                               int64_t dim, double* __restrict__ partials,
                                               EvalScalars* sc) {
-  __shared__ double sh[8];
-  __shared__ bool last;
-  double psy = 0.0, pss = 0.0, pyy = 0.0;
+  double p[3] = {0.0, 0.0, 0.0};
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
        e += (int64_t)gridDim.x * blockDim.x) {
     const double s = dsub(xt[e], x[e]);
     const double y = dsub(g[e], gt[e]);
     sv[e] = s;
     yv[e] = y;
-    psy = dadd(psy, dmul(s, y));
-    pss = dadd(pss, dmul(s, s));
-    pyy = dadd(pyy, dmul(y, y));
+    p[0] = dadd(p[0], dmul(s, y));
+    p[1] = dadd(p[1], dmul(s, s));
+    p[2] = dadd(p[2], dmul(y, y));
   }
-  const double a = block_sum256(psy, sh);
-  const double b = block_sum256(pss, sh);
-  const double c = block_sum256(pyy, sh);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x * 3 + 0] = a;
-    partials[blockIdx.x * 3 + 1] = b;
-    partials[blockIdx.x * 3 + 2] = c;
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double ta = 0.0, tb = 0.0, tc = 0.0;
-    for (unsigned q = 0; q < gridDim.x; ++q) {
-      ta = dadd(ta, partials[q * 3 + 0]);
-      tb = dadd(tb, partials[q * 3 + 1]);
-      tc = dadd(tc, partials[q * 3 + 2]);
-    }
-    sc->extra[0] = ta;
-    sc->extra[1] = tb;
-    sc->extra[2] = tc;
-    sc->ticket = 0u;
+  double out[3];
+  if (last_block_reduce<256, 3>(p, partials, &sc->ticket, out)) {
+    sc->extra[0] = out[0];
+    sc->extra[1] = out[1];
+    sc->extra[2] = out[2];
   }
 }
 
@@ -234,26 +255,12 @@ __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ a,
                                              const double* __restrict__ b, int64_t dim,
                                              double* __restrict__ partials, EvalScalars* sc,
                                              int slot) {
-  __shared__ double sh[8];
-  __shared__ bool last;
-  double p = 0.0;
+  double p[1] = {0.0};
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
        e += (int64_t)gridDim.x * blockDim.x)
-    p = dadd(p, dmul(a[e], b[e]));
-  const double r = block_sum256(p, sh);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x] = r;
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double t = 0.0;
-    for (unsigned q = 0; q < gridDim.x; ++q) t = dadd(t, partials[q]);
-    sc->extra[slot] = t;
-    sc->ticket = 0u;
-  }
+    p[0] = dadd(p[0], dmul(a[e], b[e]));
+  double out[1];
+  if (last_block_reduce<256, 1>(p, partials, &sc->ticket, out)) sc->extra[slot] = out[0];
 }
 
 void launch_dot(const double* a, const double* b, int64_t dim, double* partials, int nblocks,
@@ -261,34 +268,16 @@ void launch_dot(const double* a, const double* b, int64_t dim, double* partials,
   k_dot<<<nblocks, 256, 0, s>>>(a, b, dim, partials, sc, slot);
 }
 
-// max |a_e| into sc->extra[slot] (order-independent, exact).
+// max |a_e| into sc->extra[slot] (lpNorm<Infinity>; exact in any order).
 __global__ void __launch_bounds__(256) k_absmax(const double* __restrict__ a, int64_t dim,
                                                 double* __restrict__ partials, EvalScalars* sc,
                                                 int slot) {
-  __shared__ double sh[8];
-  __shared__ bool last;
-  double p = 0.0;
+  double p[1] = {0.0};
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
        e += (int64_t)gridDim.x * blockDim.x)
-    p = fmax(p, fabs(a[e]));
-  for (int o = 16; o >= 1; o >>= 1) p = fmax(p, __shfl_xor_sync(0xffffffffu, p, o));
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = p;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r = 0.0;
-    for (int w = 0; w < 8; ++w) r = fmax(r, sh[w]);
-    partials[blockIdx.x] = r;
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double t = 0.0;
-    for (unsigned q = 0; q < gridDim.x; ++q) t = fmax(t, partials[q]);
-    sc->extra[slot] = t;
-    sc->ticket = 0u;
-  }
+    p[0] = fmax(p[0], fabs(a[e]));
+  double out[1];
+  if (last_block_reduce<256, 1>(p, partials, &sc->ticket, out, true)) sc->extra[slot] = out[0];
 }
 
 void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, EvalScalars* sc,

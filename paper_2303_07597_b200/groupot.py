@@ -394,6 +394,19 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.lib().gsot_kernel_launches(self._h))
 
+    def timer_start(self) -> None:
+        _raise(_lib.lib().gsot_timer(self._h, 0, None))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        _raise(_lib.lib().gsot_timer(self._h, 1, C.byref(ms)))
+        return ms.value
+
+
+def set_device(device: int) -> None:
+    """CUDA device for contexts created afterwards on this thread."""
+    _raise(_lib.lib().gsot_set_device(int(device)))
+
 
 @dataclass
 class CallStatsPy:

@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden fixtures.
+
+Tolerances (BASELINE.json north_star):
+* per-block values -- plan entries, snapshot norms z~/k~/o~, the nonzero
+  block set, active set, screening counters -- BITWISE (the kernels compute
+  each block in the reference's order of operations);
+* objective within 1e-9 relative;
+* gradient within 1e-9 scale-aware: |g - g_ref| <= 1e-9 * (a_i + sum_j T_ij)
+  for grad_alpha and 1e-9 * (b_j + sum_i T_ij) for grad_beta (the sums cancel
+  near the optimum);
+* final plan within 1e-6 after the solve.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2303_07597_b200 as G
+from oracle_bindings import Oracle, Problem
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
+OBJ_RTOL = 1e-9
+GRAD_STOL = 1e-9
+PLAN_ATOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def o():
+    return Oracle()
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+def ctx_of(p: Problem) -> G.Context:
+    return G.Context.from_arrays(p.cost, p.sizes, p.a, p.b, p.gamma, p.mu)
+
+
+def grad_scale(o, p, x):
+    plan = o.plan(p, x[: p.m], x[p.m:])
+    return np.concatenate([p.a + plan.sum(axis=1), p.b + plan.sum(axis=0)])
+
+
+def assert_eval_close(o, p, x, obj, g, obj_ref=None, g_ref=None):
+    if obj_ref is None:
+        obj_ref = o.objective(p, x[: p.m], x[p.m:])
+    if g_ref is None:
+        ga, gb = o.gradient(p, x[: p.m], x[p.m:])
+        g_ref = np.concatenate([ga, gb])
+    assert abs(obj - obj_ref) <= OBJ_RTOL * max(abs(obj_ref), 1e-300), (obj, obj_ref)
+    scale = grad_scale(o, p, x)
+    err = np.abs(g - g_ref)
+    assert np.all(err <= GRAD_STOL * scale), float(np.max(err / scale))
+
+
+def gold_problem(g, name, pi):
+    gamma, mu = g[f"{name}/p{pi}/params"]
+    return Problem(g[f"{name}/cost"], g[f"{name}/sizes"], g[f"{name}/a"], g[f"{name}/b"],
+                   float(gamma), float(mu))
+
+
+# ------------------------------------------------------------ golden fixtures
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_golden_eval_plan_snapshot_active(o, gold, name, pi):
+    p = gold_problem(gold, name, pi)
+    key = f"{name}/p{pi}"
+    ctx = ctx_of(p)
+    for si in range(3):
+        x = gold[f"{key}/s{si}/x"]
+        obj, g, st = ctx.eval(x)
+        assert_eval_close(o, p, x, obj, g, gold[f"{key}/s{si}/objective"][0],
+                          gold[f"{key}/s{si}/grad"])
+        assert (st.in_active, st.skipped, st.unskipped, st.upper_bounds) == (0, 0, p.L * p.n, 0)
+    x2 = gold[f"{key}/s2/x"]
+    assert np.array_equal(ctx.plan_columns(x2, 0, p.n), gold[f"{key}/plan"])
+    x0, x1 = gold[f"{key}/s0/x"], gold[f"{key}/s1/x"]
+    ctx.init_snapshot(x1)
+    z, k, oo = ctx.snapshot_norms()
+    assert np.array_equal(z, gold[f"{key}/snap_z"])
+    assert np.array_equal(k, gold[f"{key}/snap_k"])
+    assert np.array_equal(oo, gold[f"{key}/snap_o"])
+    for ua in (0, 1):
+        ctx.init_snapshot(x0)
+        ctx.refresh(x1, bool(ua))
+        mem, cnt = ctx.active_set()
+        if ua:
+            assert np.array_equal(mem, gold[f"{key}/fast1/member"].astype(bool))
+            assert cnt == int(gold[f"{key}/fast1/member"].sum())
+        else:
+            assert cnt == 0 and not mem.any()
+        x = gold[f"{key}/fast{ua}/x"]
+        obj_s, g_s, st = ctx.eval(x, screened=True)
+        assert [st.in_active, st.skipped, st.unskipped, st.upper_bounds] == \
+            gold[f"{key}/fast{ua}/counters"].tolist()
+        assert_eval_close(o, p, x, obj_s, g_s, None, gold[f"{key}/fast{ua}/grad"])
+        obj_d, g_d, _ = ctx.eval(x)
+        assert obj_d == obj_s and np.array_equal(g_d, g_s)  # screen changes no bit
+    ctx.close()
+
+
+def test_golden_hand_examples(gold):
+    h = Problem(np.zeros((1, 1)), np.array([1], np.int32), np.ones(1), np.ones(1), 1.0, 0.5)
+    ctx = ctx_of(h)
+    obj, g, _ = ctx.eval(np.array([1.0, 0.0]))
+    assert abs(obj - 0.875) <= 1e-15 and abs(obj - gold["hand/1x1/objective"][0]) <= 1e-15
+    assert np.allclose(g, gold["hand/1x1/grad"], atol=1e-15, rtol=0)
+    h2 = Problem(np.zeros((2, 1)), np.array([2], np.int32), np.full(2, .5), np.ones(1), 1.0, 1.0)
+    pl = ctx_of(h2).plan_columns(np.array([3.0, 4.0, 0.0]), 0, 1)
+    assert np.array_equal(pl, gold["hand/plan34"])
+    # test_dual.cpp:73-81: C = 1e6 thresholds everything: grad == (a, b) bitwise
+    q = Problem(np.full((4, 3), 1e6), np.array([2, 2], np.int32), np.full(4, .25),
+                np.full(3, 1 / 3), 1.0, 1.0)
+    obj, g, _ = ctx_of(q).eval(np.zeros(7))
+    assert np.array_equal(g, np.concatenate([q.a, q.b])) and obj == 0.0
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_golden_solve(o, gold, name, pi):
+    p = gold_problem(gold, name, pi)
+    key = f"{name}/p{pi}"
+    ctx = ctx_of(p)
+    ref_plan = gold[f"{key}/solve_plan"]
+    for mode in (0, 1, 2, 3):
+        r = ctx.solve(mode=mode, max_outer_loops=20, grad_tol=1e-7, history_cap=100000)
+        ints = gold[f"{key}/solve{mode}/ints"]
+        obj_ref = gold[f"{key}/solve{mode}/objective"][0]
+        assert abs(r["objective"] - obj_ref) <= OBJ_RTOL * abs(obj_ref)
+        assert r["converged"] == ints[1] and not r["line_search_failed"]
+        plan = ctx.plan_columns(r["x"], 0, p.n)
+        assert np.max(np.abs(plan - ref_plan)) <= PLAN_ATOL
+        # counter identity of GradStats (screening.hpp:168-172)
+        h = r["history"]
+        assert np.all(h[:, 0] + h[:, 1] + h[:, 2] == p.L * p.n)
+        if mode != 0:  # the baseline books every block unskipped, no bounds
+            assert np.all(h[:, 3] == h[:, 1] + h[:, 2])
+        if r["iterations"] == ints[0] and r["grad_calls"] == ints[4]:
+            ref_h = gold[f"{key}/solve{mode}/history"]
+            # same trajectory length: the screening decisions agree call by call
+            assert np.abs(h - ref_h).sum() <= 0.01 * ref_h.sum()
+    ctx.close()
+
+
+# ------------------------------------------------------------ random structures
+
+STRUCTURES = {
+    "one_group": ([57], 40),
+    "singletons": ([1] * 23, 37),
+    "large_groups": ([300, 5, 41], 70),
+    "odd_ragged": ([3, 33, 1, 7, 64, 65, 2], 97),
+    "n_one": ([4, 5], 1),
+    "n_33": ([9, 9, 9], 33),
+}
+
+
+def random_problem(sizes, n, gamma, mu, seed, weighted=False):
+    rng = np.random.default_rng(seed)
+    sizes = np.array(sizes, np.int32)
+    m = int(sizes.sum())
+    cost = rng.uniform(0, 2, (m, n))
+    a = rng.uniform(0.5, 1.5, m) if weighted else np.ones(m)
+    a = a / a.sum()
+    return Problem(cost, sizes, a, np.full(n, 1 / n), gamma, mu), rng
+
+
+@pytest.mark.parametrize("struct", sorted(STRUCTURES))
+@pytest.mark.parametrize("gamma,mu", [(1.0, 0.1), (0.3, 0.9)])
+def test_structures_eval_and_screen(o, struct, gamma, mu):
+    sizes, n = STRUCTURES[struct]
+    p, rng = random_problem(sizes, n, gamma, mu, sum(map(ord, struct)), weighted=True)
+    ctx = ctx_of(p)
+    x0 = np.zeros(p.m + p.n)
+    x1 = np.concatenate([rng.uniform(-0.2, 1.6, p.m), rng.uniform(-0.2, 1.6, p.n)])
+    x2 = x1 + 0.05 * rng.normal(size=x1.size)
+    obj, g, _ = ctx.eval(x1)
+    assert_eval_close(o, p, x1, obj, g)
+    assert np.array_equal(ctx.plan_columns(x1, 0, p.n), o.plan(p, x1[: p.m], x1[p.m:]))
+    if p.n > 3:
+        assert np.array_equal(ctx.plan_columns(x1, 1, p.n - 1),
+                              o.plan(p, x1[: p.m], x1[p.m:])[:, 1: p.n - 1])
+    z_o, k_o, oo_o = o.snapshot(p, x1[: p.m], x1[p.m:])
+    assert np.array_equal(ctx.block_mask(x1), z_o > p.mu * p.gamma)
+    ctx.init_snapshot(x0)
+    ctx.refresh(x1, True)
+    z, k, oo = ctx.snapshot_norms()
+    assert np.array_equal(z, z_o) and np.array_equal(k, k_o) and np.array_equal(oo, oo_o)
+    mem, cnt = ctx.active_set()
+    mem_o, cnt_o = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+    assert cnt == cnt_o and np.array_equal(mem, mem_o.astype(bool))
+    obj_s, g_s, st = ctx.eval(x2, screened=True)
+    ga, gb, c_o, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem_o, x2[: p.m], x2[p.m:])
+    assert [st.in_active, st.skipped, st.unskipped, st.upper_bounds] == c_o.tolist()
+    assert_eval_close(o, p, x2, obj_s, g_s, None, np.concatenate([ga, gb]))
+    obj_d, g_d, _ = ctx.eval(x2)
+    assert obj_d == obj_s and np.array_equal(g_d, g_s)
+    ctx.close()
+
+
+def test_fast_equals_baseline_bitwise_on_device(o):
+    # SPEC.md:315/:320 (Theorem 2): the screened solve follows the unscreened
+    # trajectory exactly.
+    p, _ = random_problem([12, 7, 30, 1, 9], 50, 0.4, 0.7, 3)
+    ctx = ctx_of(p)
+    rb = ctx.solve(mode=0, max_outer_loops=15, grad_tol=1e-12)
+    for mode in (1, 2, 3):
+        rf = ctx.solve(mode=mode, max_outer_loops=15, grad_tol=1e-12)
+        assert np.array_equal(rf["x"], rb["x"])
+        assert rf["objective"] == rb["objective"]
+        assert rf["iterations"] == rb["iterations"] and rf["grad_calls"] == rb["grad_calls"]
+    ctx.close()
+
+
+def test_audit_mode_and_fault_injection(o):
+    p, _ = random_problem([10, 10, 10], 40, 0.5, 0.8, 4)
+    ctx = ctx_of(p)
+    r = ctx.solve(mode=3, max_outer_loops=10)
+    assert r["audit_gradient_calls"] == r["grad_calls"]
+    assert r["audit_column_compares"] == r["grad_calls"] * p.n
+    assert r["audit_skip_checks"] == r["blocks_skipped"]
+    with pytest.raises(G.AuditViolation):
+        ctx.solve(mode=3, max_outer_loops=10, upper_bound_offset=-1e3)
+    ctx.close()
+
+
+def test_validation_matches_reference_semantics(o):
+    cost = np.zeros((3, 4))
+    cost[2, 1] = -1.0
+    cost[0, 3] = np.nan
+    sizes, a, b = [2, 1], np.full(3, 1 / 3), np.full(4, 0.25)
+    with pytest.raises(G.NegativeCost) as e:
+        G.Context.from_arrays(cost, sizes, a, b, 1.0, 1.0)
+    assert (e.value.row, e.value.col, e.value.value) == (2, 1, -1.0)
+    p = Problem(cost, np.array(sizes, np.int32), a, b, 1.0, 1.0)
+    st, d = o.validate(p)
+    assert st == 2 and (d["row"], d["col"]) == (2, 1)
+    cost[2, 1] = 0.0
+    with pytest.raises(G.NegativeCost) as e:  # NaN is rejected too
+        G.Context.from_arrays(cost, sizes, a, b, 1.0, 1.0)
+    assert (e.value.row, e.value.col) == (0, 3)
+    with pytest.raises(G.MarginalNotNormalized) as e:
+        G.Context.from_arrays(np.zeros((3, 4)), sizes, [0.6, 0.6, -0.2], b, 1.0, 1.0)
+    assert e.value.which == "a" and e.value.index == 2
+    with pytest.raises(G.MarginalNotNormalized) as e:
+        G.Context.from_arrays(np.zeros((3, 4)), sizes, a, [0.3, 0.3, 0.3, 0.3], 1.0, 1.0)
+    assert e.value.which == "b" and e.value.index == -1
+    with pytest.raises(G.PartitionMismatch):
+        G.Context.from_arrays(np.zeros((3, 4)), [2, 2], a, b, 1.0, 1.0)
+    # compensated sum: 12800 x 1/12800 (test_core.cpp:60-67)
+    m = 12800
+    G.Context.from_arrays(np.zeros((m, 2)), [10] * 1280, np.full(m, 1 / m), [.5, .5], 1., 1.)
+
+
+def test_python_mirror_api(o):
+    p, _ = random_problem([5, 6, 7], 20, 0.5, 0.5, 9)
+    inst = G.ProblemInstance(p.cost, p.a, p.b, G.GroupPartition(p.sizes))
+    prm = G.RegParams(p.gamma, p.mu)
+    s = G.DualState(np.full(p.m, 0.3), np.full(p.n, 0.2))
+    assert abs(G.dual_objective(s, inst, prm) - o.objective(p, s.alpha, s.beta)) <= 1e-12
+    ga, gb = G.dual_gradient(s, inst, prm)
+    oa, ob = o.gradient(p, s.alpha, s.beta)
+    assert np.allclose(ga, oa, atol=1e-14) and np.allclose(gb, ob, atol=1e-14)
+    assert np.array_equal(G.recover_plan(s, inst, prm).plan, o.plan(p, s.alpha, s.beta))
+    for mode in G.SolverMode:
+        sol = G.solve(inst, prm, G.SolverOptions(max_outer_loops=5, mode=mode))
+        assert sol.iterations > 0 and sol.stats.grad_calls == len(sol.stats.history)
+    sol, rep = G.audit_solve(inst, prm, G.SolverOptions(max_outer_loops=5))
+    assert rep.gradient_calls == sol.stats.grad_calls
+    d = G.plan_diagnostics(sol.plan, inst)
+    assert 0.0 <= d.group_sparsity <= 1.0 and d.mass > 0
+
+
+# ------------------------------------------------------------ configs
+
+
+def config_problem(o, cfg):
+    import ctypes as C
+
+    gamma, mu = {1: (1.0, 0.1), 2: (0.1, 0.5)}[cfg]
+    src, tgt, sizes, a, b = G.config_features(cfg, cfg)
+    cost = o.cost_matrix(src, tgt)
+    cost /= cost.max()
+    return Problem(cost, sizes, a, b, gamma, mu), src, tgt
+
+
+def test_cost_matrix_device_matches_reference_definition(o):
+    import ctypes as C
+
+    import torch
+
+    src, tgt, sizes, a, b = G.config_features(1, 1)
+    m, n, d = src.shape[0], tgt.shape[0], src.shape[1]
+    dev = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    G.groupot._raise(G._lib.lib().gsot_cost_matrix_device(
+        src.ctypes.data_as(C.c_void_p), m, tgt.ctypes.data_as(C.c_void_p), n, d, 0,
+        C.c_void_p(dev.data_ptr())))
+    torch.cuda.synchronize()
+    got = dev.cpu().numpy().T
+    assert np.array_equal(got, o.cost_matrix(src, tgt))  # data_io.hpp:101-123, bitwise
+
+
+def test_config1_solve_vs_oracle(o):
+    p, _, _ = config_problem(o, 1)
+    ctx = G.Context.from_config(1, 1, p.gamma, p.mu)
+    r = ctx.solve(mode=1, max_outer_loops=10, grad_tol=1e-12)
+    ro = o.solve(p, mode=1, max_outer_loops=10, grad_tol=1e-12)
+    assert r["iterations"] == ro["iterations"] == 100
+    assert abs(r["objective"] - ro["objective"]) <= OBJ_RTOL * abs(ro["objective"])
+    plan = ctx.plan_columns(r["x"], 0, p.n)
+    plan_o = o.plan(p, ro["x"][: p.m], ro["x"][p.m:])
+    assert np.max(np.abs(plan - plan_o)) <= PLAN_ATOL
+    # the device context built from features equals one built from the
+    # oracle's cost matrix
+    ctx2 = ctx_of(p)
+    x = r["x"]
+    o1, g1, _ = ctx.eval(x)
+    o2, g2, _ = ctx2.eval(x)
+    assert o1 == o2 and np.array_equal(g1, g2)
+    assert_eval_close(o, p, x, o1, g1)
+
+
+def test_config2_full_size_properties(o):
+    # Full BASELINE size: properties the oracle need not recompute, plus one
+    # oracle evaluation at a mid-solve state.
+    p, _, _ = config_problem(o, 2)
+    ctx = G.Context.from_config(2, 2, p.gamma, p.mu)
+    r = ctx.solve(mode=1, max_outer_loops=3, grad_tol=1e-12)
+    x = r["x"]
+    obj, g, _ = ctx.eval(x)
+    ctx.init_snapshot(x * 0.9)
+    ctx.refresh(x * 0.95, True)
+    obj_s, g_s, st = ctx.eval(x, screened=True)
+    assert obj_s == obj and np.array_equal(g_s, g)
+    assert st.in_active + st.skipped + st.unskipped == p.L * p.n
+    # sum(grad_alpha) = 1 - mass = sum(grad_beta)
+    assert abs(g[: p.m].sum() - g[p.m:].sum()) <= 1e-12
+    assert_eval_close(o, p, x, obj, g)
+    ctx.close()

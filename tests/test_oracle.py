@@ -1,0 +1,264 @@
+"""CPU: pin the oracle (oracle/gsot_oracle.c) before trusting it.
+
+1. Against the hand-derived known answers of the reference tests
+   (test_regularizer.cpp, test_dual.cpp, test_core.cpp) and the SPEC's
+   screened-path examples (ref/SPEC.md:279-309), which the reference itself
+   never executes.
+2. Against tests/golden/reference_golden.npz, produced by the real
+   reference (oracle/_ref) -- bitwise.
+3. Against the real reference library directly (when oracle/_ref is built
+   here): random instances, every solver mode, bitwise trajectories.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle_bindings import Oracle, Problem, RefLib, ref_available
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def o():
+    return Oracle()
+
+
+def vec(*v):
+    return np.array(v, dtype=np.float64)
+
+
+# ------------------------------------------------------------ block math
+
+
+def test_block_map_hand_values(o):
+    # test_regularizer.cpp:51-64: [3,4], gamma=mu=1 -> [2.4, 3.2], z = 5
+    out = np.empty(2)
+    z = o.lib.go_grad_block(vec(3, 4).ctypes.data_as(__import__("ctypes").c_void_p), 2,
+                            __import__("ctypes").c_double(1.0), __import__("ctypes").c_double(1.0),
+                            out.ctypes.data_as(__import__("ctypes").c_void_p))
+    assert z == 0 or True  # restype int by default; check the output instead
+    assert abs(out[0] - 2.4) <= 1e-14 and abs(out[1] - 3.2) <= 1e-14
+    assert o.lib.go_pos_part_norm(vec(3, 4), 2) == 5.0
+
+
+def _problem(cost, sizes, a, b, gamma, mu):
+    return Problem(np.asarray(cost, float), np.asarray(sizes, np.int32), a, b, gamma, mu)
+
+
+def test_all_negative_and_threshold_ties_are_exact_zero(o):
+    # test_regularizer.cpp:42-49, :83-99 through the plan recovery
+    p = _problem(np.zeros((2, 1)), [2], vec(0.5, 0.5), vec(1.0), 1.0, 1.0)
+    assert np.all(o.plan(p, vec(-1, -2), vec(0)) == 0.0)
+    assert np.all(o.plan(p, vec(0.6, 0.8), vec(0)) == 0.0)  # z = tau = 1
+    p5 = _problem(np.zeros((2, 1)), [2], vec(0.5, 0.5), vec(1.0), 1.0, 5.0)
+    assert np.all(o.plan(p5, vec(3, 4), vec(0)) == 0.0)  # z = 5 = tau
+
+
+def test_psi_hand_values(o):
+    # test_regularizer.cpp:101-115 via the dual objective of 1-column instances
+    import ctypes as C
+
+    f = o.lib.go_psi_block
+    f.restype = C.c_double
+    f.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double]
+    assert f(vec(-5, -5).ctypes.data, 2, 1.0, 1.0, 1.0) == 0.0
+    assert abs(f(vec(3, 4).ctypes.data, 2, 1.0, 1.0, 1.0) - 8.0) <= 1e-13
+    assert abs(f(vec(6, 8).ctypes.data, 2, 2.0, 1.0, 2.0) - 16.0) <= 1e-13
+
+
+def test_dual_hand_examples(o):
+    # test_dual.cpp:28-35 and :83-91
+    p = _problem(np.zeros((1, 1)), [1], vec(1.0), vec(1.0), 1.0, 0.5)
+    assert abs(o.objective(p, vec(1.0), vec(0.0)) - 0.875) <= 1e-15
+    ga, gb = o.gradient(p, vec(1.0), vec(0.0))
+    assert abs(ga[0] - 0.5) <= 1e-15 and abs(gb[0] - 0.5) <= 1e-15
+    # test_dual.cpp:73-81: fully thresholded gradient == marginals bitwise
+    q = _problem(np.full((4, 3), 1e6), [2, 2], np.full(4, 0.25), np.full(3, 1 / 3), 1.0, 1.0)
+    ga, gb = o.gradient(q, np.zeros(4), np.zeros(3))
+    assert np.array_equal(ga, q.a) and np.array_equal(gb, q.b)
+    # test_dual.cpp:172-181: plan of alpha = [3, 4], C = 0
+    r = _problem(np.zeros((2, 1)), [2], vec(0.5, 0.5), vec(1.0), 1.0, 1.0)
+    pl = o.plan(r, vec(3, 4), vec(0))
+    assert abs(pl[0, 0] - 2.4) <= 1e-14 and abs(pl[1, 0] - 3.2) <= 1e-14
+
+
+def test_spec_snapshot_and_bounds_examples(o):
+    # f = [3, -4] -> z~ = 3, o~ = 4, k~ = 5
+    p = _problem(np.zeros((2, 1)), [2], vec(0.5, 0.5), vec(1.0), 1.0, 1.0)
+    z, k, oo = o.snapshot(p, vec(3, -4), vec(0))
+    assert (z[0, 0], k[0, 0], oo[0, 0]) == (3.0, 5.0, 4.0)
+    # z~=2, dalpha=[1,-1], dbeta=-2, g=2 -> z_bar = 3 (via the
+    # dispatcher: snapshot at 0 with z~ = 2 needs f = [2, 0] at x_s)
+    dpos, dfull, dneg, sg, db = o.delta_norms(p, vec(1, -1), vec(-2), vec(0, 0), vec(0))
+    assert dpos[0] == 1.0 and sg[0] == math.sqrt(2.0) and db[0] == -2.0
+    assert 2.0 + dpos[0] + sg[0] * max(db[0], 0.0) == 3.0
+    # z~=0, dalpha=[-1]*4, dbeta=0.5, g=4 -> 0 + 0 + 2*0.5 = 1
+    p4 = _problem(np.zeros((4, 1)), [4], np.full(4, 0.25), vec(1.0), 1.0, 1.0)
+    dpos, dfull, dneg, sg, db = o.delta_norms(p4, -np.ones(4), vec(0.5), np.zeros(4), vec(0))
+    assert 0.0 + dpos[0] + sg[0] * max(db[0], 0.0) == 1.0
+    # SPEC.md:298-300 lower bounds: Delta = 0, f=[3,4] -> 5; f=[3,-4] -> 1
+    z, k, oo = o.snapshot(p, vec(3, 4), vec(0))
+    assert k[0, 0] - oo[0, 0] == 5.0
+    z, k, oo = o.snapshot(p, vec(3, -4), vec(0))
+    assert k[0, 0] - oo[0, 0] == 1.0
+    # k~=5, o~=0, dalpha=[0.3,-0.4], dbeta=-1, g=2 -> 4.1 - 2 sqrt 2
+    dpos, dfull, dneg, sg, db = o.delta_norms(p, vec(0.3, -0.4), vec(-1), vec(0, 0), vec(0))
+    lb = 5.0 - dfull[0] - sg[0] * abs(db[0]) - 0.0 - dneg[0] - sg[0] * max(-db[0], 0.0)
+    assert abs(lb - (4.1 - 2 * math.sqrt(2))) <= 1e-12
+
+
+def test_spec_active_set_examples(o):
+    rng = np.random.default_rng(3)
+    cost = rng.uniform(0, 1, (6, 4))
+    # tau -> infinity: empty
+    p = _problem(cost, [3, 3], np.full(6, 1 / 6), np.full(4, 0.25), 1.0, 1e9)
+    x = (np.full(6, 5.0), np.zeros(4))
+    mem, cnt = o.active_set(p, *x, *x)
+    assert cnt == 0 and not mem.any()
+    # Delta = 0 with all-positive blocks and k~ > tau: everything
+    q = _problem(cost, [3, 3], np.full(6, 1 / 6), np.full(4, 0.25), 1.0, 0.1)
+    mem, cnt = o.active_set(q, *x, *x)
+    assert cnt == 8 and mem.all()  # L * n
+
+
+def test_params_from_rho_and_validation(o):
+    # test_core.cpp:83-93 conversions: (1, .5) -> gamma .5, mu 1, tau .5
+    assert 1.0 * (1 - 0.5) == 0.5 and 0.5 / (1 - 0.5) == 1.0
+    # validate: NegativeCost names the first offender in j-major order
+    cost = np.zeros((2, 3))
+    cost[1, 0] = -1.0
+    cost[0, 2] = -2.0
+    p = _problem(cost, [1, 1], vec(0.5, 0.5), np.full(3, 1 / 3), 1.0, 1.0)
+    st, d = o.validate(p)
+    assert st == 2 and (d["row"], d["col"]) == (1, 0)
+    p = _problem(np.zeros((2, 2)), [2], vec(-0.5, 1.5), vec(0.5, 0.5), 1.0, 1.0)
+    st, d = o.validate(p)
+    assert st == 3 and d["which"] == "a" and d["index"] == 0
+    # compensated marginal sum: 12800 x 1/12800 passes (test_core.cpp:60-67)
+    m = 12800
+    p = _problem(np.zeros((m, 2)), [10] * 1280, np.full(m, 1 / m), vec(0.5, 0.5), 1.0, 1.0)
+    assert o.validate(p)[0] == 0
+
+
+# ------------------------------------------------------------ golden fixtures
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+def _gold_problem(g, name, pi):
+    gamma, mu = g[f"{name}/p{pi}/params"]
+    return Problem(g[f"{name}/cost"], g[f"{name}/sizes"], g[f"{name}/a"], g[f"{name}/b"],
+                   float(gamma), float(mu))
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_oracle_reproduces_reference_golden_bitwise(o, gold, name, pi):
+    p = _gold_problem(gold, name, pi)
+    key = f"{name}/p{pi}"
+    for si in range(3):
+        x = gold[f"{key}/s{si}/x"]
+        assert o.objective(p, x[: p.m], x[p.m:]) == gold[f"{key}/s{si}/objective"][0]
+        ga, gb = o.gradient(p, x[: p.m], x[p.m:])
+        assert np.array_equal(np.concatenate([ga, gb]), gold[f"{key}/s{si}/grad"])
+    x = gold[f"{key}/s2/x"]
+    assert np.array_equal(o.plan(p, x[: p.m], x[p.m:]), gold[f"{key}/plan"])
+    x1 = gold[f"{key}/s1/x"]
+    z, k, oo = o.snapshot(p, x1[: p.m], x1[p.m:])
+    assert np.array_equal(z, gold[f"{key}/snap_z"])
+    assert np.array_equal(k, gold[f"{key}/snap_k"])
+    assert np.array_equal(oo, gold[f"{key}/snap_o"])
+    x0 = gold[f"{key}/s0/x"]
+    for ua in (0, 1):
+        x = gold[f"{key}/fast{ua}/x"]
+        mem, cnt = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+        if ua:
+            assert np.array_equal(mem, gold[f"{key}/fast1/member"])
+        ga, gb, c, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem if ua else None, x[: p.m],
+                                       x[p.m:])
+        assert np.array_equal(np.concatenate([ga, gb]), gold[f"{key}/fast{ua}/grad"])
+        assert np.array_equal(c, gold[f"{key}/fast{ua}/counters"])
+    for mode in (0, 1, 2, 3):
+        r = o.solve(p, mode=mode, max_outer_loops=20, grad_tol=1e-7)
+        sk = f"{key}/solve{mode}"
+        assert np.array_equal(r["x"], gold[f"{sk}/x"])
+        assert r["objective"] == gold[f"{sk}/objective"][0]
+        ints = [r["iterations"], r["converged"], r["line_search_failed"], r["outer_loops"],
+                r["grad_calls"], r["blocks_in_active_set"], r["blocks_skipped"],
+                r["blocks_unskipped"], r["upper_bounds_evaluated"]]
+        assert ints == gold[f"{sk}/ints"].tolist()
+        assert np.array_equal(r["history"], gold[f"{sk}/history"])
+
+
+def test_oracle_hand_golden(o, gold):
+    p = _problem(np.zeros((1, 1)), [1], vec(1.0), vec(1.0), 1.0, 0.5)
+    assert o.objective(p, vec(1.0), vec(0.0)) == gold["hand/1x1/objective"][0]
+
+
+# ------------------------------------------------------------ vs the reference
+
+
+needs_ref = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+
+
+@needs_ref
+def test_reference_catch2_suite_passes_against_shim():
+    import subprocess
+
+    d = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref")
+    ran = 0
+    for t in ("core", "regularizer", "dual", "lbfgs"):
+        exe = os.path.join(d, f"test_{t}")
+        if not os.path.exists(exe):
+            pytest.skip("reference tests not built")
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        ran += int(r.stdout.split()[0])
+    assert ran == 44  # the reference's 44 real TEST_CASEs
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_oracle_equals_reference_random(o, seed):
+    ref = RefLib()
+    rng = np.random.default_rng(100 + seed)
+    sizes = rng.integers(1, 9, size=6).astype(np.int32)
+    m, n = int(sizes.sum()), int(rng.integers(3, 40))
+    cost = rng.uniform(0, 2, (m, n))
+    for gamma, mu in [(0.7, 0.3), (0.2, 1.5)]:
+        p = Problem(cost, sizes, np.full(m, 1 / m), np.full(n, 1 / n), gamma, mu)
+        x = (rng.uniform(-0.5, 1.5, m), rng.uniform(-0.5, 1.5, n))
+        obj, ga, gb = ref.eval(p, *x)
+        assert obj == o.objective(p, *x)
+        g2 = o.gradient(p, *x)
+        assert np.array_equal(ga, g2[0]) and np.array_equal(gb, g2[1])
+        for mode in (0, 1, 2, 3):
+            R = ref.solve(p, mode=mode, max_outer_loops=10)
+            O = o.solve(p, mode=mode, max_outer_loops=10)
+            assert np.array_equal(R["x"], O["x"]) and R["objective"] == O["objective"]
+            assert np.array_equal(R["history"], O["history"])
+
+
+@needs_ref
+def test_oracle_rng_and_cost_match_reference(o):
+    ref = RefLib()
+    for kind in (0, 1, 2):
+        assert np.array_equal(ref.rng_stream(7, kind, 2000), o.rng_stream(7, kind, 2000))
+    assert np.array_equal(ref.rng_stream(9, 3, 500, bound=37), o.rng_stream(9, 3, 500, bound=37))
+    cost, a, b, sizes, sf, tf = ref.gen_synthetic(4, 10, 5, False)
+    assert np.array_equal(o.cost_matrix(sf, tf), cost)
+
+
+@needs_ref
+def test_audit_fault_injection_matches_reference(o):
+    ref = RefLib()
+    cost, a, b, sizes, _, _ = ref.gen_synthetic(3, 10, 2, True)
+    p = Problem(cost, sizes, a, b, 0.5, 0.8)
+    R = ref.solve(p, mode=3, max_outer_loops=5, ub_offset=-1e3)
+    O = o.solve(p, mode=3, max_outer_loops=5, ub_offset=-1e3)
+    assert R["status"] == 7 and O["status"] == 7  # AuditViolation
