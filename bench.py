@@ -292,10 +292,14 @@ def run_ours(args, world, rank, local, pg):
                     lbfgs_memory=10, history_cap=0)
     for _ in range(args.warmup):
         ctx.solve(**solve_kw)
+    ctx.profile((1 << 0) | (1 << 1))  # capture the profiled graphs outside the timed region
+    ctx.solve(**solve_kw)
 
     # ---- timed region: K solves on the resident instance
     ctx.profile_reset()
-    ctx.profile(True)
+    # CUDA events only around the two HBM-streaming kernels (eval, snapshot):
+    # event nodes around every kernel would perturb the step
+    ctx.profile((1 << 0) | (1 << 1))
     launches0 = ctx.kernel_launches()
     clocks = ClockSampler(local)
     clocks.start()

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libgsot.so")
-SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu"]
+SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu", "gsot_solver.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -29,7 +29,7 @@ FLAGS = [
 
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "gsot_internal.cuh"), os.path.join(ROOT, "include", "gsot.h")]
+    deps = srcs + [os.path.join(CSRC, h) for h in ("gsot_internal.cuh", "gsot_device.cuh", "gsot_ctx.cuh")] + [os.path.join(ROOT, "include", "gsot.h")]
     if (not force and os.path.exists(LIB)
             and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps)):
         return LIB

@@ -1,5 +1,5 @@
-// gsot_ctx.cu — resident instance, evaluation pipeline, device-vector
-// L-BFGS driver and the C ABI of include/gsot.h.
+// gsot_ctx.cu — resident instance, evaluation pipeline, screening state and
+// the C ABI of include/gsot.h (the solver lives in gsot_solver.cu).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <string.h>
@@ -11,7 +11,7 @@
 #include <string>
 #include <vector>
 
-#include "gsot_internal.cuh"
+#include "gsot_ctx.cuh"
 
 namespace gsot {
 int config_features(int cfg, uint64_t seed, double* src, double* tgt, int32_t* sizes, double* a,
@@ -20,6 +20,8 @@ int config_shape(int cfg, int64_t* m, int64_t* n, int32_t* L, int64_t* d);
 }  // namespace gsot
 
 using gsot::Error;
+
+using gsot::dalloc;
 
 namespace {
 
@@ -51,14 +53,6 @@ int guard(F&& f) {
   }
 }
 
-template <typename T>
-T* dalloc(size_t count, size_t* tally) {
-  T* p = nullptr;
-  if (count == 0) count = 1;
-  GSOT_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * count));
-  if (tally) *tally += sizeof(T) * count;
-  return p;
-}
 
 void check_params(double gamma, double mu) {  // core.hpp:61-66
   if (!(gamma > 0.0) || !std::isfinite(gamma))
@@ -105,141 +99,33 @@ void check_marginal(const double* v, int64_t n, char which) {  // core.hpp:100-1
 
 }  // namespace
 
-struct gsot_ctx {
-  int device = 0;
-  int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  int64_t m = 0, n = 0;
-  int32_t L = 0, nw = 0;
-  double gamma = 1.0, mu = 1.0;
-  std::vector<int32_t> sizes, off;
-  size_t bytes = 0;
 
-  // resident instance
-  double* C = nullptr;
-  int32_t *d_off = nullptr, *d_row_group = nullptr, *d_group_order = nullptr;
-  double *d_sqrt_g = nullptr, *d_a = nullptr, *d_b = nullptr;
-  // evaluation buffers
-  double *x_eval = nullptr, *g_eval = nullptr;
-  double *rowpart = nullptr, *colpart = nullptr, *psi = nullptr, *psicol = nullptr;
-  double* partials = nullptr;
-  uint32_t *words = nullptr, *dense_words = nullptr;
-  int2 *tasks = nullptr, *dense_tasks = nullptr;
-  // screening state
-  double *snap_x = nullptr, *zs = nullptr, *ks = nullptr, *os = nullptr;
-  double *dpos = nullptr, *dfull = nullptr, *dneg = nullptr, *dbeta = nullptr;
-  uint32_t* active_words = nullptr;
-  int64_t active_count = 0;
-  bool have_snapshot = false;
-  // scalars
-  gsot::EvalScalars* sc = nullptr;
-  gsot::EvalScalars* h_sc = nullptr;  // pinned
-  int eval_grid = 148 * 4;
-  int red_blocks = 148 * 2;
-  // measurement
-  bool profile = false;
-  struct Mark {
-    cudaEvent_t a, b;
-    int kind;
-    double bytes;
-  };
-  std::vector<Mark> marks;
-  std::vector<cudaEvent_t> event_pool;
-  double prof_ms[gsot::K_NKINDS] = {};
-  double prof_bytes[gsot::K_NKINDS] = {};
-  int64_t prof_launches[gsot::K_NKINDS] = {};
-  int64_t launches = 0;
-  cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+gsot_ctx::~gsot_ctx() {
+  if (stream) cudaStreamSynchronize(stream);
+  ws.reset();
+  for (auto& mk : marks) {
+    cudaEventDestroy(mk.a);
+    cudaEventDestroy(mk.b);
+  }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  if (timer_a) cudaEventDestroy(timer_a);
+  if (timer_b) cudaEventDestroy(timer_b);
+  void* ptrs[] = {C,        d_off,   d_group_order, d_row_group, d_sqrt_g, d_a,     d_b,
+                  x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
+                  words,    dense_words, tasks,     dense_tasks, snap_x,   zs,      ks,
+                  os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h_sync) cudaFreeHost(h_sync);
+  if (stream) cudaStreamDestroy(stream);
+}
 
-  gsot::DevProblem problem() const {
-    gsot::DevProblem P;
-    P.C = C;
-    P.m = m;
-    P.n = n;
-    P.L = L;
-    P.nw = nw;
-    P.off = d_off;
-    P.row_group = d_row_group;
-    P.sqrt_g = d_sqrt_g;
-    P.a = d_a;
-    P.b = d_b;
-    P.gamma = gamma;
-    P.mu = mu;
-    P.tau = mu * gamma;
-    return P;
-  }
-
-  cudaEvent_t take_event() {
-    if (!event_pool.empty()) {
-      cudaEvent_t e = event_pool.back();
-      event_pool.pop_back();
-      return e;
-    }
-    cudaEvent_t e;
-    GSOT_CUDA_CHECK(cudaEventCreate(&e));
-    return e;
-  }
-  // Bracket a launch with events when profiling; always count launches.
-  template <typename F>
-  void launch(int kind, double bytes_alg, F&& f) {
-    ++launches;
-    if (!profile) {
-      f();
-      GSOT_CUDA_CHECK(cudaGetLastError());
-      return;
-    }
-    Mark mk{take_event(), take_event(), kind, bytes_alg};
-    GSOT_CUDA_CHECK(cudaEventRecord(mk.a, stream));
-    f();
-    GSOT_CUDA_CHECK(cudaGetLastError());
-    GSOT_CUDA_CHECK(cudaEventRecord(mk.b, stream));
-    marks.push_back(mk);
-  }
-  void collect_marks() {
-    if (marks.empty()) return;
-    GSOT_CUDA_CHECK(cudaStreamSynchronize(stream));
-    for (auto& mk : marks) {
-      float ms = 0.f;
-      GSOT_CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
-      prof_ms[mk.kind] += ms;
-      prof_bytes[mk.kind] += mk.bytes;
-      prof_launches[mk.kind] += 1;
-      event_pool.push_back(mk.a);
-      event_pool.push_back(mk.b);
-    }
-    marks.clear();
-  }
-
-  void sync() { GSOT_CUDA_CHECK(cudaStreamSynchronize(stream)); }
-  void fetch_scalars() {
-    GSOT_CUDA_CHECK(
-        cudaMemcpyAsync(h_sc, sc, sizeof(gsot::EvalScalars), cudaMemcpyDeviceToHost, stream));
-    sync();
-  }
-  void reset_scalars() {
-    GSOT_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(gsot::EvalScalars), stream));
-  }
-
-  ~gsot_ctx() {
-    if (stream) cudaStreamSynchronize(stream);
-    for (auto& mk : marks) {
-      cudaEventDestroy(mk.a);
-      cudaEventDestroy(mk.b);
-    }
-    for (auto e : event_pool) cudaEventDestroy(e);
-    if (timer_a) cudaEventDestroy(timer_a);
-    if (timer_b) cudaEventDestroy(timer_b);
-    void* ptrs[] = {C,        d_off,        d_group_order, d_row_group, d_sqrt_g,
-                    d_a,      d_b,          x_eval,     g_eval,      rowpart,       colpart,
-                    psi,      psicol,       partials,   words,       dense_words,   tasks,
-                    dense_tasks, snap_x,    zs,         ks,          os,            dpos,
-                    dfull,    dneg,         dbeta,      active_words, sc};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
-    if (h_sc) cudaFreeHost(h_sc);
-    if (stream) cudaStreamDestroy(stream);
-  }
-};
+gsot::SolverWorkspace::~SolverWorkspace() {
+  graphs.clear();
+  void* ptrs[] = {X[0], X[1], G[0], G[1], lo_x, lo_g, prev_x, prev_g, d, S, Y, audit_g};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
 
 namespace {
 
@@ -310,9 +196,12 @@ void alloc_buffers(gsot_ctx* c) {
   c->dneg = dalloc<double>(L, t);
   c->dbeta = dalloc<double>(n, t);
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
-  c->sc = dalloc<gsot::EvalScalars>(1, t);
-  GSOT_CUDA_CHECK(cudaMallocHost(&c->h_sc, sizeof(gsot::EvalScalars)));
-  GSOT_CUDA_CHECK(cudaMemsetAsync(c->sc, 0, sizeof(gsot::EvalScalars), c->stream));
+  c->dsync = dalloc<gsot::DevSync>(1, t);
+  GSOT_CUDA_CHECK(cudaMallocHost(&c->h_sync, sizeof(gsot::DevSync)));
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->dsync, 0, sizeof(gsot::DevSync), c->stream));
+  memset(c->h_sync, 0, sizeof(gsot::DevSync));
+  c->sc = &c->dsync->sc;
+  c->h_sc = &c->h_sync->sc;
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->x_eval, 0, sizeof(double) * (dim + 8), c->stream));
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_x, 0, sizeof(double) * (dim + 8), c->stream));
 
@@ -447,59 +336,46 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
 
 // ------------------------------------------------------------------ eval
 
-struct EvalOut {
-  double objective = 0.0;
-  double slope = 0.0;
-  gsot_call_stats stats{};
-};
+}  // namespace
 
-// Fused evaluation at device state d_x (length m+n): writes d_grad,
-// returns objective, slope against d_dir (if non-null) and the per-call
-// counters. mode: GSOT_EVAL_DENSE / GSOT_EVAL_SCREENED.
-EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
-                    const double* d_dir, double ub_offset, bool use_active) {
+namespace gsot {
+
+void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, const double* d_dir,
+                  double ub_offset, bool use_active) {
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
-  const gsot::DevProblem P = c->problem();
+  const DevProblem P = c->problem();
   c->reset_scalars();
   const uint32_t* words = c->dense_words;
   const int2* tasks = c->dense_tasks;
-  int max_tasks = c->L * c->nw;
+  const int max_tasks = c->L * c->nw;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
-    c->launch(gsot::K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
-      gsot::launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
+    c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
     });
-    c->launch(gsot::K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
-      gsot::launch_bounds(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
-                          ub_offset, c->words, c->tasks, c->sc, c->stream);
+    c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
+      launch_bounds(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
+                    ub_offset, c->words, c->tasks, c->sc, c->stream);
     });
     words = c->words;
     tasks = c->tasks;
   }
   const double dense_bytes = 8.0 * c->m * c->n + 8.0 * c->m * c->nw + 16.0 * Ln;
-  const size_t eval_mark = c->marks.size();
-  c->launch(gsot::K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : 0.0, [&] {
-    gsot::launch_eval(P, d_x, tasks, mode == GSOT_EVAL_DENSE ? max_tasks : -1, words,
-                      c->rowpart, c->colpart, c->psi, c->sc, c->eval_grid, c->stream);
+  c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
+    launch_eval(P, d_x, tasks, mode == GSOT_EVAL_DENSE ? max_tasks : -1, words, c->rowpart,
+                c->colpart, c->psi, c->sc, c->eval_grid, c->stream);
   });
-  c->launch(gsot::K_FINALIZE, 0.0, [&] {
-    gsot::launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, c->psicol,
-                          c->stream);
+  c->launch(K_FINALIZE, 0.0, [&] {
+    launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, c->psicol, c->stream);
   });
-  c->launch(gsot::K_FINALIZE, 16.0 * (c->m + c->n), [&] {
-    gsot::launch_objective(P, d_x, c->psicol, d_grad, d_dir, c->partials, c->red_blocks, c->sc,
-                           c->stream);
+  c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
+    launch_objective(P, d_x, c->psicol, d_grad, d_dir, c->partials, c->red_blocks, c->sc,
+                     c->stream);
   });
-  c->fetch_scalars();
-  if (mode == GSOT_EVAL_SCREENED && c->profile && eval_mark < c->marks.size()) {
-    // algorithmic bytes of the screened pass: surviving blocks' cost rows,
-    // row partials of the non-empty chunks, per-block column/psi partials
-    const double surv_blocks =
-        static_cast<double>(c->h_sc->counters[0] + c->h_sc->counters[2]);
-    c->marks[eval_mark].bytes = 8.0 * static_cast<double>(c->h_sc->surv_rows) +
-                                8.0 * static_cast<double>(c->h_sc->task_rows) + 16.0 * surv_blocks;
-  }
+}
+
+EvalOut eval_result(gsot_ctx* c, int mode) {
   EvalOut o;
   o.objective = c->h_sc->objective;
   o.slope = c->h_sc->slope;
@@ -514,12 +390,18 @@ EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
   return o;
 }
 
-void snapshot_at(gsot_ctx* c, const double* d_x) {  // take_snapshot at device state
-  const gsot::DevProblem P = c->problem();
+EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
+                    const double* d_dir, double ub_offset, bool use_active) {
+  enqueue_eval(c, d_x, mode, d_grad, d_dir, ub_offset, use_active);
+  c->fetch_scalars();
+  return eval_result(c, mode);
+}
+
+void enqueue_snapshot(gsot_ctx* c, const double* d_x) {  // take_snapshot (screening.hpp:24-50)
+  const DevProblem P = c->problem();
   const double Ln = static_cast<double>(c->L) * c->n;
-  c->launch(gsot::K_SNAPSHOT, 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n), [&] {
-    gsot::launch_snapshot(P, d_x, c->zs, c->ks, c->os, c->stream);
-  });
+  c->launch(K_SNAPSHOT, 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n),
+            [&] { launch_snapshot(P, d_x, c->zs, c->ks, c->os, c->stream); });
   if (d_x != c->snap_x)
     GSOT_CUDA_CHECK(cudaMemcpyAsync(c->snap_x, d_x, sizeof(double) * (c->m + c->n),
                                     cudaMemcpyDeviceToDevice, c->stream));
@@ -527,458 +409,45 @@ void snapshot_at(gsot_ctx* c, const double* d_x) {  // take_snapshot at device s
 }
 
 void init_snapshot_device(gsot_ctx* c, const double* d_x) {  // screening.hpp:220-227
-  snapshot_at(c, d_x);
+  enqueue_snapshot(c, d_x);
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->active_words, 0,
                                   sizeof(uint32_t) * static_cast<size_t>(c->L) * c->nw, c->stream));
   c->active_count = 0;
 }
 
-void refresh_device(gsot_ctx* c, const double* d_x, bool use_active) {  // screening.hpp:231-235
+// FastGradDispatcher::refresh (screening.hpp:231-235): active set from the
+// lower bounds against the current snapshot, then the new snapshot. The
+// active-set size lands in sc->counters[0] (reset first).
+void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active) {
   if (!c->have_snapshot) throw Error(GSOT_ERR_STATE, "refresh requires a snapshot");
-  const gsot::DevProblem P = c->problem();
+  const DevProblem P = c->problem();
+  c->reset_scalars();
   if (use_active) {
-    c->reset_scalars();
-    c->launch(gsot::K_DELTA, 16.0 * (c->m + c->n), [&] {
-      gsot::launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
+    c->launch(K_DELTA, 16.0 * (c->m + c->n), [&] {
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
     });
-    c->launch(gsot::K_ACTIVE, 16.0 * c->L * c->n + 4.0 * c->L * c->nw, [&] {
-      gsot::launch_active(P, c->ks, c->os, c->dfull, c->dneg, c->dbeta, c->active_words, c->sc,
-                          c->stream);
+    c->launch(K_ACTIVE, 16.0 * c->L * c->n + 4.0 * c->L * c->nw, [&] {
+      launch_active(P, c->ks, c->os, c->dfull, c->dneg, c->dbeta, c->active_words, c->sc,
+                    c->stream);
     });
-    c->fetch_scalars();
-    c->active_count = static_cast<int64_t>(c->h_sc->counters[0]);
   }
-  snapshot_at(c, d_x);
+  enqueue_snapshot(c, d_x);
 }
 
-// ------------------------------------------------------------------ L-BFGS
+void refresh_device(gsot_ctx* c, const double* d_x, bool use_active) {
+  enqueue_refresh(c, d_x, use_active);
+  c->fetch_scalars();
+  if (use_active) c->active_count = static_cast<int64_t>(c->h_sc->counters[0]);
+}
 
-struct Pt {  // lbfgs.hpp:40-46 with the vectors held by reference
-  double t = 0.0, value = 0.0, slope = 0.0;
-  int buf = -1;
-};
+}  // namespace gsot
 
-class DeviceMaximizer {
- public:
-  DeviceMaximizer(gsot_ctx* c, const gsot_solver_options& o, gsot_solve_result* res,
-                  int64_t* history, int64_t history_cap)
-      : c_(c), o_(o), res_(res), hist_(history), hist_cap_(history_cap) {
-    dim_ = c->m + c->n;
-    mem_ = std::max(1, std::min<int>(o.lbfgs_memory, gsot::kMaxMemory));
-    for (int i = 0; i < 6; ++i) {
-      Buf b;
-      b.x = dalloc<double>(dim_ + 8, &extra_);
-      b.g = dalloc<double>(dim_ + 8, &extra_);
-      pool_.push_back(b);
-    }
-    d_ = dalloc<double>(dim_ + 8, &extra_);
-    for (int i = 0; i <= mem_; ++i) {
-      S_.push_back(dalloc<double>(dim_, &extra_));
-      Y_.push_back(dalloc<double>(dim_, &extra_));
-      free_slots_.push_back(i);
-    }
-    tl_out_ = dalloc<double>(4, &extra_);
-    GSOT_CUDA_CHECK(cudaMallocHost(&h_tl_, sizeof(double) * 4));
-  }
-  ~DeviceMaximizer() {
-    for (auto& b : pool_) {
-      cudaFree(b.x);
-      cudaFree(b.g);
-    }
-    cudaFree(d_);
-    for (auto p : S_) cudaFree(p);
-    for (auto p : Y_) cudaFree(p);
-    cudaFree(tl_out_);
-    cudaFreeHost(h_tl_);
-  }
+using gsot::EvalOut;
+using gsot::eval_device;
+using gsot::init_snapshot_device;
+using gsot::refresh_device;
 
-  // Returns the final iterate buffer index.
-  void run(double* x_out) {
-    const bool screened = o_.mode != GSOT_MODE_BASELINE;
-    const bool use_active = o_.mode == GSOT_MODE_FAST || o_.mode == GSOT_MODE_AUDIT;
-    audit_ = o_.mode == GSOT_MODE_AUDIT;
-    use_active_ = use_active;
-    screened_ = screened;
-    // x0 = 0 (solver.hpp:123, :244)
-    res_buf_ = acquire();
-    GSOT_CUDA_CHECK(cudaMemsetAsync(pool_[res_buf_].x, 0, sizeof(double) * dim_, c_->stream));
-    if (screened) init_snapshot_device(c_, pool_[res_buf_].x);  // solver.hpp:143-144
-
-    const auto t0 = std::chrono::steady_clock::now();
-    maximize();
-    const auto t1 = std::chrono::steady_clock::now();
-    res_->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
-    if (x_out)
-      GSOT_CUDA_CHECK(cudaMemcpyAsync(x_out, pool_[res_buf_].x, sizeof(double) * dim_,
-                                      cudaMemcpyDeviceToHost, c_->stream));
-    c_->sync();
-    res_->objective = res_value_;  // == dual_objective(x*) (screened == dense bitwise)
-    res_->outer_loops = res_->chunks;
-  }
-
- private:
-  struct Buf {
-    double* x;
-    double* g;
-    int refs = 0;
-  };
-
-  int acquire() {
-    for (size_t i = 0; i < pool_.size(); ++i)
-      if (pool_[i].refs == 0) {
-        pool_[i].refs = 1;
-        return static_cast<int>(i);
-      }
-    Buf b;
-    b.x = dalloc<double>(dim_ + 8, &extra_);
-    b.g = dalloc<double>(dim_ + 8, &extra_);
-    b.refs = 1;
-    pool_.push_back(b);
-    return static_cast<int>(pool_.size() - 1);
-  }
-  void release(int b) {
-    if (b >= 0) --pool_[b].refs;
-  }
-  void assign(Pt& dst, const Pt& src) {
-    if (&dst == &src) return;
-    if (src.buf >= 0) ++pool_[src.buf].refs;
-    release(dst.buf);
-    dst = src;
-  }
-
-  // One objective+gradient evaluation (the fused pair of ObjectiveFn and
-  // GradientFn, solver.hpp:161-210), with the GradStats bookkeeping.
-  gsot::EvalScalars dummy_{};
-  EvalOut evaluate(const double* d_x, double* d_g, const double* d_dir) {
-    const int mode = screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE;
-    EvalOut e = eval_device(c_, d_x, mode, d_g, d_dir, o_.upper_bound_offset, use_active_);
-    if (audit_) audit_call(d_x, d_g, e);
-    const int64_t row = res_->grad_calls;
-    if (hist_ && row < hist_cap_) {
-      hist_[row * 4 + 0] = e.stats.in_active;
-      hist_[row * 4 + 1] = e.stats.skipped;
-      hist_[row * 4 + 2] = e.stats.unskipped;
-      hist_[row * 4 + 3] = e.stats.upper_bounds;
-    }
-    res_->blocks_in_active_set += e.stats.in_active;
-    res_->blocks_skipped += e.stats.skipped;
-    res_->blocks_unskipped += e.stats.unskipped;
-    res_->upper_bounds_evaluated += e.stats.upper_bounds;
-    ++res_->grad_calls;
-    return e;
-  }
-
-  // audit_solve per gradient call (solver.hpp:172-201): every skipped block
-  // is recomputed and must be zero; the screened gradient and objective
-  // must equal the unscreened ones bitwise.
-  void audit_call(const double* d_x, const double* d_g, const EvalOut& e) {
-    const gsot::DevProblem P = c_->problem();
-    const uint32_t* words = c_->words;
-    c_->reset_scalars();
-    c_->launch(gsot::K_MISC, 0.0, [&] {
-      gsot::launch_audit_skips(P, d_x, words, c_->active_words, c_->sc, c_->stream);
-    });
-    c_->fetch_scalars();
-    res_->audit_skip_checks += static_cast<int64_t>(c_->h_sc->counters[0]);
-    if (c_->h_sc->audit_violation) {
-      const long long w = c_->h_sc->audit_where;
-      throw Error(GSOT_ERR_AUDIT_VIOLATION,
-                  "audit violation: skipped block (l=" + std::to_string(w / c_->n) +
-                      ", j=" + std::to_string(w % c_->n) + ") has nonzero exact gradient at call " +
-                      std::to_string(res_->grad_calls));
-    }
-    // Recompute the whole gradient unscreened and compare bitwise. The
-    // screen must not change the words/tasks used by the screened call, so
-    // the comparison runs after the skip check.
-    if (!audit_g_) audit_g_ = dalloc<double>(dim_ + 8, &extra_);
-    EvalOut d = eval_device(c_, d_x, GSOT_EVAL_DENSE, audit_g_, nullptr, 0.0, false);
-    std::vector<double> a(static_cast<size_t>(dim_)), b(static_cast<size_t>(dim_));
-    GSOT_CUDA_CHECK(cudaMemcpyAsync(a.data(), d_g, sizeof(double) * dim_, cudaMemcpyDeviceToHost, c_->stream));
-    GSOT_CUDA_CHECK(cudaMemcpyAsync(b.data(), audit_g_, sizeof(double) * dim_, cudaMemcpyDeviceToHost, c_->stream));
-    c_->sync();
-    res_->audit_column_compares += c_->n;
-    if (memcmp(a.data(), b.data(), sizeof(double) * dim_) != 0 || d.objective != e.objective) {
-      throw Error(GSOT_ERR_AUDIT_VIOLATION,
-                  "audit violation: screened gradient differs from plain gradient at call " +
-                      std::to_string(res_->grad_calls));
-    }
-    ++res_->audit_gradient_calls;
-  }
-
-  void hook(const double* d_x) {  // solver.hpp:212-241
-    if (!screened_) return;
-    refresh_device(c_, d_x, use_active_);
-    if (audit_ && use_active_) {
-      const gsot::DevProblem P = c_->problem();
-      c_->reset_scalars();
-      c_->launch(gsot::K_MISC, 0.0, [&] {
-        gsot::launch_audit_active(P, d_x, c_->active_words, c_->sc, c_->stream);
-      });
-      c_->fetch_scalars();
-      res_->audit_active_checks += static_cast<int64_t>(c_->h_sc->counters[1]);
-      if (c_->h_sc->audit_violation) {
-        const long long w = c_->h_sc->audit_where;
-        throw Error(GSOT_ERR_AUDIT_VIOLATION,
-                    "audit violation: active-set block (l=" + std::to_string(w / c_->n) +
-                        ", j=" + std::to_string(w % c_->n) + ") has zero exact gradient at build time");
-      }
-    }
-  }
-
-  void eval_at(double t, Pt& p) {  // lbfgs.hpp:84-90
-    if (p.buf < 0 || pool_[p.buf].refs > 1) {
-      release(p.buf);
-      p.buf = acquire();
-    }
-    p.t = t;
-    double* xt = pool_[p.buf].x;
-    c_->launch(gsot::K_LBFGS, 24.0 * dim_, [&] {
-      gsot::launch_axpy_point(pool_[res_buf_].x, t, d_, xt, dim_, c_->stream);
-    });
-    EvalOut e = evaluate(xt, pool_[p.buf].g, d_);
-    p.value = e.objective;
-    p.slope = e.slope;
-  }
-
-  double norm_inf(const double* v) {  // lpNorm<Infinity> (lbfgs.hpp:264): exact in any order
-    c_->reset_scalars();
-    c_->launch(gsot::K_LBFGS, 8.0 * dim_, [&] {
-      gsot::launch_absmax(v, dim_, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
-    });
-    c_->fetch_scalars();
-    return c_->h_sc->extra[0];
-  }
-
-  double dot_host(const double* a, const double* b) {
-    c_->reset_scalars();
-    c_->launch(gsot::K_LBFGS, 16.0 * dim_, [&] {
-      gsot::launch_dot(a, b, dim_, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
-    });
-    c_->fetch_scalars();
-    return c_->h_sc->extra[0];
-  }
-
-  void clear_history() {
-    for (int s : order_) free_slots_.push_back(s);
-    order_.clear();
-    rho_.clear();
-    sy_.clear();
-    yy_.clear();
-  }
-
-  void maximize() {  // lbfgs.hpp:61-274
-    const double c1 = 1e-4, c2 = 0.9;  // MaximizeOptions defaults (lbfgs.hpp:16-17)
-    const int max_bracket = 40, max_zoom = 12;
-    // initial gradient + objective (lbfgs.hpp:70-71), one fused evaluation
-    {
-      EvalOut e = evaluate(pool_[res_buf_].x, pool_[res_buf_].g, nullptr);
-      res_value_ = e.objective;
-    }
-    bool stalled = false, zero_gradient = false;
-    Pt trial, lo, prev;
-    for (int chunk = 0; chunk < o_.max_outer_loops && !stalled && !zero_gradient; ++chunk) {
-      ++res_->chunks;
-      for (int it = 0; it < o_.snapshot_interval; ++it) {
-        bool accepted = false;
-        for (int attempt = 0; attempt < 2 && !accepted; ++attempt) {
-          if (attempt == 1) {
-            if (order_.empty()) break;
-            clear_history();
-          }
-          // two-loop recursion (lbfgs.hpp:109-124) in one cluster launch
-          gsot::TwoLoopArgs A{};
-          const int k = static_cast<int>(order_.size());
-          for (int i = 0; i < k; ++i) {
-            A.s[i] = S_[order_[i]];
-            A.y[i] = Y_[order_[i]];
-            A.rho[i] = rho_[i];
-          }
-          A.k = k;
-          A.apply_scale = 0;
-          A.gamma_scale = 1.0;
-          if (k > 0 && yy_.back() > 0.0) {
-            A.apply_scale = 1;
-            A.gamma_scale = sy_.back() / yy_.back();
-          }
-          A.g = pool_[res_buf_].g;
-          A.d = d_;
-          A.dim = dim_;
-          A.out = tl_out_;
-          c_->launch(gsot::K_LBFGS, 8.0 * dim_ * (4.0 * k + 4.0), [&] {
-            gsot::launch_two_loop(A, c_->stream);
-          });
-          GSOT_CUDA_CHECK(cudaMemcpyAsync(h_tl_, tl_out_, sizeof(double) * 2,
-                                          cudaMemcpyDeviceToHost, c_->stream));
-          c_->sync();
-          double dir_slope = h_tl_[0];
-          double dd = h_tl_[1];
-          if (!(dir_slope > 0.0)) {  // lbfgs.hpp:127-137
-            clear_history();
-            GSOT_CUDA_CHECK(cudaMemcpyAsync(d_, pool_[res_buf_].g, sizeof(double) * dim_,
-                                            cudaMemcpyDeviceToDevice, c_->stream));
-            dir_slope = dot_host(pool_[res_buf_].g, pool_[res_buf_].g);
-            dd = dir_slope;
-            if (dir_slope == 0.0) {
-              zero_gradient = true;
-              break;
-            }
-          }
-          const double f0 = res_value_;
-          const double armijo = c1 * dir_slope;
-          auto sufficient = [&](const Pt& p) { return p.value >= f0 + armijo * p.t; };
-          auto curvature_ok = [&](const Pt& p) { return std::abs(p.slope) <= c2 * dir_slope; };
-
-          double t_init = 1.0;  // lbfgs.hpp:150-154
-          if (res_->iterations == 0) {
-            const double dnorm = std::sqrt(dd);
-            if (dnorm > 0.0) t_init = 1.0 / dnorm;
-          }
-          bool have_bracket = false;
-          Pt lo0;
-          lo0.t = 0.0;
-          lo0.value = f0;
-          lo0.slope = dir_slope;
-          assign(lo, lo0);
-          double hi_t = 0.0;
-          double t = t_init;
-          assign(prev, lo);
-          for (int i = 0; i < max_bracket; ++i) {  // lbfgs.hpp:165-187
-            eval_at(t, trial);
-            if (!sufficient(trial) || (i > 0 && trial.value <= prev.value)) {
-              assign(lo, prev);
-              hi_t = trial.t;
-              have_bracket = true;
-              break;
-            }
-            if (curvature_ok(trial)) {
-              accepted = true;
-              break;
-            }
-            if (trial.slope <= 0.0) {
-              assign(lo, trial);
-              hi_t = prev.t;
-              have_bracket = true;
-              break;
-            }
-            assign(prev, trial);
-            t *= 2.0;
-          }
-          if (!accepted && have_bracket) {  // lbfgs.hpp:189-231
-            double hi_value = std::numeric_limits<double>::quiet_NaN();
-            for (int i = 0; i < max_zoom; ++i) {
-              double cand = 0.5 * (lo.t + hi_t);
-              if (std::isfinite(hi_value)) {
-                const double dt = hi_t - lo.t;
-                const double denom = 2.0 * (lo.value + lo.slope * dt - hi_value);
-                if (denom != 0.0) {
-                  const double interp = lo.t + lo.slope * dt * dt / denom;
-                  const double lo_guard = lo.t + 0.1 * dt;
-                  const double hi_guard = hi_t - 0.1 * dt;
-                  const double lim_min = std::min(lo_guard, hi_guard);
-                  const double lim_max = std::max(lo_guard, hi_guard);
-                  if (interp >= lim_min && interp <= lim_max) cand = interp;
-                }
-              }
-              if (cand == lo.t || cand == hi_t) break;
-              eval_at(cand, trial);
-              if (!sufficient(trial) || trial.value <= lo.value) {
-                hi_t = cand;
-                hi_value = trial.value;
-                continue;
-              }
-              if (curvature_ok(trial)) {
-                accepted = true;
-                break;
-              }
-              if (trial.slope * (hi_t - lo.t) <= 0.0) {
-                hi_t = lo.t;
-                hi_value = lo.value;
-              }
-              assign(lo, trial);
-            }
-            if (!accepted && lo.t > 0.0) {
-              assign(trial, lo);
-              accepted = true;
-            }
-          }
-          if (!accepted && !have_bracket && prev.t > 0.0) {
-            assign(trial, prev);
-            accepted = true;
-          }
-        }
-        if (zero_gradient) break;
-        if (!accepted) {
-          stalled = true;
-          break;
-        }
-        // curvature pair (lbfgs.hpp:243-255)
-        const int slot = free_slots_.back();
-        c_->reset_scalars();
-        c_->launch(gsot::K_LBFGS, 8.0 * dim_ * 6.0, [&] {
-          gsot::launch_pair(pool_[trial.buf].x, pool_[res_buf_].x, pool_[res_buf_].g,
-                            pool_[trial.buf].g, S_[slot], Y_[slot], dim_, c_->partials,
-                            c_->red_blocks, c_->sc, c_->stream);
-        });
-        c_->fetch_scalars();
-        const double sy = c_->h_sc->extra[0];
-        const double ss = c_->h_sc->extra[1];
-        const double yy = c_->h_sc->extra[2];
-        if (sy > 1e-10 * std::sqrt(ss) * std::sqrt(yy)) {
-          free_slots_.pop_back();
-          if (static_cast<int>(order_.size()) == mem_) {
-            free_slots_.push_back(order_.front());
-            order_.pop_front();
-            rho_.pop_front();
-            sy_.pop_front();
-            yy_.pop_front();
-          }
-          order_.push_back(slot);
-          rho_.push_back(1.0 / sy);
-          sy_.push_back(sy);
-          yy_.push_back(yy);
-        }
-        // res.x = trial.x; res.gradient = trial.grad (share the buffer)
-        ++pool_[trial.buf].refs;
-        release(res_buf_);
-        res_buf_ = trial.buf;
-        res_value_ = trial.value;
-        ++res_->iterations;
-      }
-      if (stalled) break;
-      hook(pool_[res_buf_].x);
-      if (norm_inf(pool_[res_buf_].g) <= o_.grad_tol) {
-        res_->converged = 1;
-        break;
-      }
-    }
-    if (!res_->converged) res_->converged = norm_inf(pool_[res_buf_].g) <= o_.grad_tol;
-    res_->line_search_failed = stalled && !res_->converged;
-    release(trial.buf);
-    release(lo.buf);
-    release(prev.buf);
-  }
-
-  gsot_ctx* c_;
-  gsot_solver_options o_;
-  gsot_solve_result* res_;
-  int64_t* hist_;
-  int64_t hist_cap_;
-  int64_t dim_ = 0;
-  int mem_ = 10;
-  size_t extra_ = 0;
-  std::vector<Buf> pool_;
-  double* d_ = nullptr;
-  std::vector<double*> S_, Y_;
-  std::deque<int> order_;
-  std::vector<int> free_slots_;
-  std::deque<double> rho_, sy_, yy_;
-  double* tl_out_ = nullptr;
-  double* h_tl_ = nullptr;
-  double* audit_g_ = nullptr;
-  int res_buf_ = -1;
-  double res_value_ = 0.0;
-  bool audit_ = false, use_active_ = false, screened_ = false;
-};
+namespace {
 
 gsot_ctx* checked(gsot_ctx* c) {
   if (!c) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null context");
@@ -1044,8 +513,11 @@ GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu) {
   return guard([&] {
     checked(ctx);
     check_params(gamma, mu);
-    ctx->gamma = gamma;
-    ctx->mu = mu;
+    if (gamma != ctx->gamma || mu != ctx->mu) {
+      ctx->gamma = gamma;
+      ctx->mu = mu;
+      if (ctx->ws) ctx->ws->graphs.clear();  // graphs bake (gamma, mu) into kernel parameters
+    }
   });
 }
 
@@ -1211,8 +683,7 @@ GSOT_API int gsot_solve(gsot_ctx* ctx, const gsot_solver_options* opts, double* 
     if (o.lbfgs_memory > gsot::kMaxMemory)
       throw Error(GSOT_ERR_INVALID_ARGUMENT, "lbfgs_memory above the supported maximum");
     gsot_solve_result r{};
-    DeviceMaximizer dm(ctx, o, &r, history, history_cap);
-    dm.run(x_out);
+    gsot::run_solve(ctx, o, x_out, &r, history, history_cap);
     if (result) *result = r;
   });
 }
@@ -1319,6 +790,9 @@ GSOT_API int gsot_profile_enable(gsot_ctx* ctx, int enable) {
     checked(ctx);
     ctx->collect_marks();
     ctx->profile = enable != 0;
+    // negative = every kernel class, positive = bit mask (1 << kind)
+    ctx->profile_mask = enable < 0 ? 0xffffffffu : static_cast<unsigned>(enable);
+    if (ctx->ws) ctx->ws->graphs.clear();  // graphs carry their event nodes
   });
 }
 

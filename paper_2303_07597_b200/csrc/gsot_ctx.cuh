@@ -1,0 +1,251 @@
+// gsot_ctx.cuh — the resident-instance context shared by the context/eval
+// code (gsot_ctx.cu) and the solver (gsot_solver.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gsot_internal.cuh"
+
+namespace gsot {
+
+// One captured device sequence (CUDA graph) plus the timing marks it records
+// through external event nodes when profiling.
+struct Mark {
+  cudaEvent_t a, b;
+  int kind;
+  double bytes;  // < 0: screened eval, bytes from the synced counters
+};
+
+struct Sequence {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Mark> marks;
+  int kernels = 0;
+  ~Sequence() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto& m : marks) {
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
+  }
+};
+
+// Persistent solver workspace (lives as long as the context so captured
+// graphs stay valid across solves).
+struct SolverWorkspace {
+  int64_t dim = 0;
+  int mem = 0;
+  double* X[2] = {nullptr, nullptr};  // iterate / trial, alternating roles
+  double* G[2] = {nullptr, nullptr};
+  double* lo_x = nullptr;  // line-search points kept by value (lbfgs.hpp:157, :166)
+  double* lo_g = nullptr;
+  double* prev_x = nullptr;
+  double* prev_g = nullptr;
+  double* d = nullptr;     // direction
+  double* S = nullptr;     // (mem + 1) pair slots of dim doubles
+  double* Y = nullptr;
+  double* audit_g = nullptr;
+  std::map<std::string, std::unique_ptr<Sequence>> graphs;
+  ~SolverWorkspace();
+};
+
+}  // namespace gsot
+
+struct gsot_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t m = 0, n = 0;
+  int32_t L = 0, nw = 0;
+  double gamma = 1.0, mu = 1.0;
+  std::vector<int32_t> sizes, off;
+  size_t bytes = 0;
+
+  // resident instance
+  double* C = nullptr;
+  int32_t *d_off = nullptr, *d_row_group = nullptr, *d_group_order = nullptr;
+  double *d_sqrt_g = nullptr, *d_a = nullptr, *d_b = nullptr;
+  // evaluation buffers
+  double *x_eval = nullptr, *g_eval = nullptr;
+  double *rowpart = nullptr, *colpart = nullptr, *psi = nullptr, *psicol = nullptr;
+  double* partials = nullptr;
+  uint32_t *words = nullptr, *dense_words = nullptr;
+  int2 *tasks = nullptr, *dense_tasks = nullptr;
+  // screening state
+  double *snap_x = nullptr, *zs = nullptr, *ks = nullptr, *os = nullptr;
+  double *dpos = nullptr, *dfull = nullptr, *dneg = nullptr, *dbeta = nullptr;
+  uint32_t* active_words = nullptr;
+  int64_t active_count = 0;
+  bool have_snapshot = false;
+  // scalars: one device block, one pinned mirror
+  gsot::DevSync* dsync = nullptr;
+  gsot::DevSync* h_sync = nullptr;
+  gsot::EvalScalars* sc = nullptr;    // &dsync->sc
+  gsot::EvalScalars* h_sc = nullptr;  // &h_sync->sc
+  int eval_grid = 148 * 4;
+  int red_blocks = 148 * 2;
+  // solver
+  std::unique_ptr<gsot::SolverWorkspace> ws;
+  uint64_t graph_epoch = 0;  // bumped when baked-in parameters change
+  // measurement
+  bool profile = false;
+  unsigned profile_mask = 0;  // kinds bracketed with events (bit per KernelKind)
+  std::vector<gsot::Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  double prof_ms[gsot::K_NKINDS] = {};
+  double prof_bytes[gsot::K_NKINDS] = {};
+  int64_t prof_launches[gsot::K_NKINDS] = {};
+  int64_t launches = 0;
+  cudaEvent_t timer_a = nullptr, timer_b = nullptr;
+  // stream capture in progress: marks/kernels go to the sequence
+  gsot::Sequence* capturing = nullptr;
+
+  gsot::DevProblem problem() const {
+    gsot::DevProblem P;
+    P.C = C;
+    P.m = m;
+    P.n = n;
+    P.L = L;
+    P.nw = nw;
+    P.off = d_off;
+    P.row_group = d_row_group;
+    P.sqrt_g = d_sqrt_g;
+    P.a = d_a;
+    P.b = d_b;
+    P.gamma = gamma;
+    P.mu = mu;
+    P.tau = mu * gamma;
+    return P;
+  }
+
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    GSOT_CUDA_CHECK(cudaEventCreate(&e));
+    return e;
+  }
+
+  // Enqueue one kernel launch; bracket it with events when profiling (event
+  // record nodes when capturing); count launches.
+  template <typename F>
+  void launch(int kind, double bytes_alg, F&& f) {
+    const bool timed = profile && ((profile_mask >> kind) & 1u);
+    if (capturing) {
+      ++capturing->kernels;
+      if (timed) {
+        gsot::Mark mk{nullptr, nullptr, kind, bytes_alg};
+        GSOT_CUDA_CHECK(cudaEventCreate(&mk.a));
+        GSOT_CUDA_CHECK(cudaEventCreate(&mk.b));
+        GSOT_CUDA_CHECK(cudaEventRecordWithFlags(mk.a, stream, cudaEventRecordExternal));
+        f();
+        GSOT_CUDA_CHECK(cudaGetLastError());
+        GSOT_CUDA_CHECK(cudaEventRecordWithFlags(mk.b, stream, cudaEventRecordExternal));
+        capturing->marks.push_back(mk);
+      } else {
+        f();
+        GSOT_CUDA_CHECK(cudaGetLastError());
+      }
+      return;
+    }
+    ++launches;
+    if (!timed) {
+      f();
+      GSOT_CUDA_CHECK(cudaGetLastError());
+      return;
+    }
+    gsot::Mark mk{take_event(), take_event(), kind, bytes_alg};
+    GSOT_CUDA_CHECK(cudaEventRecord(mk.a, stream));
+    f();
+    GSOT_CUDA_CHECK(cudaGetLastError());
+    GSOT_CUDA_CHECK(cudaEventRecord(mk.b, stream));
+    marks.push_back(mk);
+  }
+
+  double screened_eval_bytes() const {
+    const double surv_blocks = static_cast<double>(h_sc->counters[0] + h_sc->counters[2]);
+    return 8.0 * static_cast<double>(h_sc->surv_rows) +
+           8.0 * static_cast<double>(h_sc->task_rows) + 16.0 * surv_blocks;
+  }
+
+  void account(const gsot::Mark& mk) {
+    float ms = 0.f;
+    GSOT_CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
+    prof_ms[mk.kind] += ms;
+    prof_bytes[mk.kind] += mk.bytes < 0 ? screened_eval_bytes() : mk.bytes;
+    prof_launches[mk.kind] += 1;
+  }
+
+  // After a synchronisation: fold eager marks into the counters.
+  void collect_marks() {
+    if (marks.empty()) return;
+    GSOT_CUDA_CHECK(cudaStreamSynchronize(stream));
+    for (auto& mk : marks) {
+      account(mk);
+      event_pool.push_back(mk.a);
+      event_pool.push_back(mk.b);
+    }
+    marks.clear();
+  }
+
+  void sync() { GSOT_CUDA_CHECK(cudaStreamSynchronize(stream)); }
+  void fetch_scalars() {
+    GSOT_CUDA_CHECK(
+        cudaMemcpyAsync(h_sync, dsync, sizeof(gsot::DevSync), cudaMemcpyDeviceToHost, stream));
+    sync();
+    collect_marks();
+  }
+  void enqueue_fetch() {
+    GSOT_CUDA_CHECK(
+        cudaMemcpyAsync(h_sync, dsync, sizeof(gsot::DevSync), cudaMemcpyDeviceToHost, stream));
+  }
+  void reset_scalars() {
+    GSOT_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(gsot::EvalScalars), stream));
+  }
+
+  ~gsot_ctx();
+};
+
+namespace gsot {
+
+struct EvalOut {
+  double objective = 0.0;
+  double slope = 0.0;
+  gsot_call_stats stats{};
+};
+
+// Enqueue the fused evaluation at device state d_x (length m+n) into d_grad,
+// with the line-search slope against d_dir when non-null. No sync; the
+// scalars land in c->dsync->sc.
+void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, const double* d_dir,
+                  double ub_offset, bool use_active);
+// Read back the result of the last enqueue_eval after c->fetch_scalars().
+EvalOut eval_result(gsot_ctx* c, int mode);
+EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
+                    const double* d_dir, double ub_offset, bool use_active);
+void enqueue_snapshot(gsot_ctx* c, const double* d_x);
+void init_snapshot_device(gsot_ctx* c, const double* d_x);
+void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active);
+void refresh_device(gsot_ctx* c, const double* d_x, bool use_active);
+
+template <typename T>
+T* dalloc(size_t count, size_t* tally) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  GSOT_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * count));
+  if (tally) *tally += sizeof(T) * count;
+  return p;
+}
+
+void run_solve(gsot_ctx* c, const gsot_solver_options& o, double* x_out, gsot_solve_result* res,
+               int64_t* history, int64_t history_cap);
+
+}  // namespace gsot

@@ -125,24 +125,52 @@ void launch_dense_tasks(int2* tasks, const int32_t* group_order, int32_t L, int3
 
 // L-BFGS vector kernels (gsot_lbfgs.cu).
 constexpr int kMaxMemory = 64;
-struct TwoLoopArgs {
-  const double* s[kMaxMemory];
-  const double* y[kMaxMemory];
-  double rho[kMaxMemory];
+
+// Device-resident curvature-pair history (lbfgs.hpp:73-74, :243-255): a ring
+// of mem+1 vector slots, `order` lists the k live pairs oldest first and
+// `scratch` is the slot the next pair is written to before the acceptance
+// test. The pair kernel decides acceptance and evicts on the device, so the
+// per-iteration graph needs no host round trip.
+struct HistState {
   int k;
-  double gamma_scale;  // s_last.y_last / y_last.y_last, or 1 when not applied
-  int apply_scale;
+  int mem;
+  int scratch;
+  int accepted;  // last pair: 1 pushed, 0 rejected by the s.y test
+  int order[kMaxMemory + 1];
+  double rho[kMaxMemory + 1];  // 1 / s.y, by logical position
+  double sy[kMaxMemory + 1];   // s.y, by logical position
+  double yy[kMaxMemory + 1];   // y.y, by logical position
+  double last_sy, last_ss, last_yy;
+};
+
+// Everything the host reads after one device sequence, in one D2H copy.
+struct DevSync {
+  EvalScalars sc;
+  HistState h;
+  double tl[2];  // two-loop: g.d, d.d
+  double t;      // line-search step read by the axpy kernel
+};
+
+struct TwoLoopArgs {
+  const double* S;  // pair slots: slot s at S + s * stride
+  const double* Y;
+  int64_t stride;
+  const HistState* h;
   const double* g;
   double* d;
   int64_t dim;
   double* out;  // [0] = g.d, [1] = d.d
 };
 void launch_two_loop(const TwoLoopArgs& a, cudaStream_t s);
-void launch_axpy_point(const double* x, double t, const double* d, double* out, int64_t dim,
-                       cudaStream_t s);
-void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* sv,
-                 double* yv, int64_t dim, double* partials, int nblocks, EvalScalars* sc,
-                 cudaStream_t s);
+// trial.x = x + t * d with t read from device memory.
+void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
+                       int64_t dim, cudaStream_t s);
+// s = trial.x - x, y = g - trial.g into slot h->scratch, then the acceptance
+// test s.y > 1e-10 |s| |y| and the ring update (lbfgs.hpp:243-255).
+void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* S,
+                 double* Y, int64_t stride, HistState* h, int64_t dim, double* partials,
+                 int nblocks, EvalScalars* sc, cudaStream_t s);
+void launch_hist_reset(HistState* h, int mem, cudaStream_t s);
 void launch_dot(const double* a, const double* b, int64_t dim, double* partials, int nblocks,
                 EvalScalars* sc, int slot, cudaStream_t s);
 void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, EvalScalars* sc,

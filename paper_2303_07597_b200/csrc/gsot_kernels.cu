@@ -252,71 +252,88 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
 // skipped iff z_bar <= tau. Writes the survivor word of each (l, c) chunk
 // and appends non-empty chunks to the work list (order irrelevant: every
-// task writes fixed slots). A block of 256 threads covers 8 chunks of one
-// group; counters are block-aggregated before one atomic per counter.
+// task writes fixed slots). Persistent blocks walk units of 8 chunks of one
+// group (one chunk per warp), buffer their tasks in shared memory and flush
+// them, and their counters, with one global atomic each at the end.
 __global__ void __launch_bounds__(256) k_bounds(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
                                                 const double* __restrict__ dpos,
                                                 const double* __restrict__ dbeta,
                                                 double ub_offset, uint32_t* __restrict__ words,
                                                 int2* __restrict__ tasks, EvalScalars* sc) {
-  __shared__ unsigned long long cnt[8][5];
-  __shared__ int base;
-  const int l = blockIdx.y;
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  extern __shared__ int2 tbuf[];
+  __shared__ unsigned long long cnt[6];
+  __shared__ int ntb, base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c = j >> 5;
-  const bool valid = j < P.n;
-  bool in_active = false;
-  if (valid && aw != nullptr) in_active = (aw[(int64_t)l * P.nw + c] >> lane) & 1u;
-  const bool evaluated = valid && !in_active;
-  bool surv = in_active;
-  if (evaluated) {
-    const double db = dbeta[j];
-    const double db_pos = db > 0.0 ? db : 0.0;
-    const double zbar =
-        dadd(dadd(dadd(zs[(int64_t)l * P.n + j], dpos[l]), dmul(P.sqrt_g[l], db_pos)), ub_offset);
-    surv = !(zbar <= P.tau);
-  }
-  const unsigned wa = __ballot_sync(0xffffffffu, in_active);
-  const unsigned we = __ballot_sync(0xffffffffu, evaluated);
-  const unsigned ws = __ballot_sync(0xffffffffu, surv);
-  const int g = P.off[l + 1] - P.off[l];
-  if (lane == 0) {
-    if (c < P.nw) words[(int64_t)l * P.nw + c] = ws;
-    cnt[warp][0] = __popc(wa);
-    cnt[warp][1] = __popc(we & ~ws);
-    cnt[warp][2] = __popc(we & ws);
-    cnt[warp][3] = __popc(we);
-    cnt[warp][4] = (ws != 0u && c < P.nw) ? 1 : 0;
-  }
+  if (threadIdx.x < 6) cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) ntb = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t[5] = {0, 0, 0, 0, 0};
-    for (int w = 0; w < 8; ++w)
-      for (int q = 0; q < 5; ++q) t[q] += cnt[w][q];
-    base = t[4] ? atomicAdd(&sc->ntasks, (int)t[4]) : 0;
-    for (int q = 0; q < 4; ++q)
-      if (t[q]) atomicAdd(&sc->counters[q], t[q]);
-    const unsigned long long surv_blocks = t[0] + t[2];
-    if (surv_blocks) {
-      atomicAdd(&sc->surv_rows, surv_blocks * (unsigned long long)g);
-      atomicAdd(&sc->task_rows, t[4] * (unsigned long long)g);
+  const int nunit8 = (P.nw + 7) / 8;
+  const int64_t nunits = (int64_t)P.L * nunit8;
+  unsigned long long my[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int l = (int)(u / nunit8);
+    const int c = (int)(u % nunit8) * 8 + warp;
+    const int64_t j = (int64_t)c * 32 + lane;
+    const bool valid = c < P.nw && j < P.n;
+    bool in_active = false;
+    if (valid && aw != nullptr) in_active = (aw[(int64_t)l * P.nw + c] >> lane) & 1u;
+    const bool evaluated = valid && !in_active;
+    bool surv = in_active;
+    if (evaluated) {
+      const double db = dbeta[j];
+      const double db_pos = db > 0.0 ? db : 0.0;
+      const double zbar = dadd(
+          dadd(dadd(zs[(int64_t)l * P.n + j], dpos[l]), dmul(P.sqrt_g[l], db_pos)), ub_offset);
+      surv = !(zbar <= P.tau);
+    }
+    const unsigned wa = __ballot_sync(0xffffffffu, in_active);
+    const unsigned we = __ballot_sync(0xffffffffu, evaluated);
+    const unsigned ws = __ballot_sync(0xffffffffu, surv);
+    if (lane == 0 && c < P.nw) {
+      words[(int64_t)l * P.nw + c] = ws;
+      const unsigned long long g = (unsigned long long)(P.off[l + 1] - P.off[l]);
+      my[0] += __popc(wa);
+      my[1] += __popc(we & ~ws);
+      my[2] += __popc(we & ws);
+      my[3] += __popc(we);
+      my[4] += (unsigned long long)__popc(ws) * g;  // survivors' rows
+      if (ws) {
+        my[5] += g;  // task rows
+        tbuf[atomicAdd(&ntb, 1)] = make_int2(l, c);
+      }
     }
   }
+  if (lane == 0)
+    for (int q = 0; q < 6; ++q)
+      if (my[q]) atomicAdd(&cnt[q], my[q]);
   __syncthreads();
-  if (lane == 0 && cnt[warp][4]) {
-    int pos = base;
-    for (int w = 0; w < warp; ++w) pos += (int)cnt[w][4];
-    tasks[pos] = make_int2(l, (int)c);
+  if (threadIdx.x == 0) {
+    base = ntb ? atomicAdd(&sc->ntasks, ntb) : 0;
+    for (int q = 0; q < 4; ++q)
+      if (cnt[q]) atomicAdd(&sc->counters[q], cnt[q]);
+    if (cnt[4]) atomicAdd(&sc->surv_rows, cnt[4]);
+    if (cnt[5]) atomicAdd(&sc->task_rows, cnt[5]);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ntb; i += blockDim.x) tasks[base + i] = tbuf[i];
 }
 
 void launch_bounds(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, int2* tasks,
                    EvalScalars* sc, cudaStream_t s) {
-  dim3 grid((unsigned)((P.nw * 32 + 255) / 256), (unsigned)P.L);
-  k_bounds<<<grid, 256, 0, s>>>(P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc);
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  }
+  const int64_t nunits = (int64_t)P.L * ((P.nw + 7) / 8);
+  const int grid = (int)std::min<int64_t>(nunits, (int64_t)nsm * 4);
+  const int64_t per = (nunits + grid - 1) / grid;
+  const size_t smem = sizeof(int2) * (size_t)(per * 8);
+  k_bounds<<<grid, 256, smem, s>>>(P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.

@@ -72,14 +72,38 @@ __global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs 
   // q slice: shared memory when it fits, else the output vector itself
   double* __restrict__ q = use_smem ? q_dyn : A.d + lo;
   const double* __restrict__ g = A.g + lo;
-  const int k = A.k;
+  // history snapshot (no CTA writes it during this kernel)
+  __shared__ const double* s_ptr[kMaxMemory];
+  __shared__ const double* y_ptr[kMaxMemory];
+  __shared__ double rho_sh[kMaxMemory];
+  __shared__ double scale_sh;
+  __shared__ int k_sh, apply_sh;
+  if (threadIdx.x == 0) {
+    const int kk = A.h->k;
+    k_sh = kk;
+    for (int i = 0; i < kk; ++i) {
+      const int slot = A.h->order[i];
+      s_ptr[i] = A.S + slot * A.stride;
+      y_ptr[i] = A.Y + slot * A.stride;
+      rho_sh[i] = A.h->rho[i];
+    }
+    // lbfgs.hpp:116-119: q *= s.y / y.y of the newest pair when y.y > 0
+    apply_sh = 0;
+    scale_sh = 1.0;
+    if (kk > 0 && A.h->yy[kk - 1] > 0.0) {
+      apply_sh = 1;
+      scale_sh = A.h->sy[kk - 1] / A.h->yy[kk - 1];
+    }
+  }
+  __syncthreads();
+  const int k = k_sh;
   int parity = 0;
 
   // Loop 1 (lbfgs.hpp:112-115). Pass i: q -= a_{i+1} y_{i+1} (or q = g for
   // the first pass), then a_i = rho_i * s_i . q.
   for (int i = k - 1; i >= 0; --i) {
     double part = 0.0;
-    const double* __restrict__ si = A.s[i] + lo;
+    const double* __restrict__ si = s_ptr[i] + lo;
     if (i == k - 1) {
 #pragma unroll 4
       for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
@@ -89,7 +113,7 @@ __global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs 
       }
     } else {
       const double ap = a_sh[i + 1];
-      const double* __restrict__ yp = A.y[i + 1] + lo;
+      const double* __restrict__ yp = y_ptr[i + 1] + lo;
 #pragma unroll 4
       for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
         const double qe = dsub(q[e], dmul(ap, yp[e]));
@@ -99,7 +123,7 @@ __global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs 
     }
     const double dot = cluster_sum(cluster, part, warp_sh, pub, tot_sh, parity, nranks);
     parity ^= 1;
-    if (threadIdx.x == 0) a_sh[i] = dmul(A.rho[i], dot);
+    if (threadIdx.x == 0) a_sh[i] = dmul(rho_sh[i], dot);
     __syncthreads();
   }
   // Close loop 1 (q -= a_0 y_0), scale by s.y / y.y (lbfgs.hpp:116-119), and
@@ -113,18 +137,18 @@ __global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs 
       for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) q[e] = g[e];  // d = g
     } else if (i == 0) {
       const double a0 = a_sh[0];
-      const double* __restrict__ y0 = A.y[0] + lo;
+      const double* __restrict__ y0 = y_ptr[0] + lo;
 #pragma unroll 4
       for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
         double qe = dsub(q[e], dmul(a0, y0[e]));
-        if (A.apply_scale) qe = dmul(qe, A.gamma_scale);
+        if (apply_sh) qe = dmul(qe, scale_sh);
         q[e] = qe;
         part = dadd(part, dmul(y0[e], qe));
       }
     } else {
       const double coef = dsub(a_sh[i - 1], b_prev);
-      const double* __restrict__ sp = A.s[i - 1] + lo;
-      const double* __restrict__ yi = last ? nullptr : A.y[i] + lo;
+      const double* __restrict__ sp = s_ptr[i - 1] + lo;
+      const double* __restrict__ yi = last ? nullptr : y_ptr[i] + lo;
 #pragma unroll 4
       for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
         const double qe = dadd(q[e], dmul(coef, sp[e]));
@@ -135,7 +159,7 @@ __global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs 
     if (last) break;
     const double dot = cluster_sum(cluster, part, warp_sh, pub, tot_sh, parity, nranks);
     parity ^= 1;
-    b_prev = dmul(A.rho[i], dot);
+    b_prev = dmul(rho_sh[i], dot);
   }
   // d = q; dir_slope = g . d and |d|^2 (lbfgs.hpp:124-126, :152).
   double pg = 0.0, pd = 0.0;
@@ -203,28 +227,34 @@ void launch_two_loop(const TwoLoopArgs& a, cudaStream_t s) {
 }
 
 // trial.x = x + t * d (lbfgs.hpp:86).
-__global__ void k_axpy_point(const double* __restrict__ x, double t, const double* __restrict__ d,
-                             double* __restrict__ out, int64_t dim) {
+__global__ void k_axpy_point(const double* __restrict__ x, const double* __restrict__ tp,
+                             const double* __restrict__ d, double* __restrict__ out, int64_t dim) {
+  const double t = *tp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
        e += (int64_t)gridDim.x * blockDim.x)
     out[e] = dadd(x[e], dmul(t, d[e]));
 }
 
-void launch_axpy_point(const double* x, double t, const double* d, double* out, int64_t dim,
-                       cudaStream_t s) {
+void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
+                       int64_t dim, cudaStream_t s) {
   const int grid = (int)std::min<int64_t>((dim + 255) / 256, 148 * 4);
   k_axpy_point<<<grid, 256, 0, s>>>(x, t, d, out, dim);
 }
 
-// Curvature pair (lbfgs.hpp:243-246): s = trial.x - x, y = g - trial.g
-// written to the ring slot, plus s.y, s.s, y.y (deterministic).
+// Curvature pair (lbfgs.hpp:243-255): s = trial.x - x, y = g - trial.g
+// written to the scratch slot, s.y, s.s, y.y (deterministic), then -- in
+// the last block -- the acceptance test sy > 1e-10 |s| |y| and the ring
+// update: evict the oldest pair when full, append the scratch slot.
 __global__ void __launch_bounds__(256) k_pair(const double* __restrict__ xt,
                                               const double* __restrict__ x,
                                               const double* __restrict__ g,
                                               const double* __restrict__ gt,
-                                              double* __restrict__ sv, double* __restrict__ yv,
-                                              int64_t dim, double* __restrict__ partials,
-                                              EvalScalars* sc) {
+                                              double* __restrict__ S, double* __restrict__ Y,
+                                              int64_t stride, HistState* h, int64_t dim,
+                                              double* __restrict__ partials, EvalScalars* sc) {
+  const int scratch = h->scratch;  // read by every block before the last one updates h
+  double* __restrict__ sv = S + scratch * stride;
+  double* __restrict__ yv = Y + scratch * stride;
   double p[3] = {0.0, 0.0, 0.0};
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -238,17 +268,62 @@ __global__ void __launch_bounds__(256) k_pair(const double* __restrict__ xt,
   }
   double out[3];
   if (last_block_reduce<256, 3>(p, partials, &sc->ticket, out)) {
-    sc->extra[0] = out[0];
-    sc->extra[1] = out[1];
-    sc->extra[2] = out[2];
+    const double sy = out[0], ss = out[1], yy = out[2];
+    sc->extra[0] = sy;
+    sc->extra[1] = ss;
+    sc->extra[2] = yy;
+    h->last_sy = sy;
+    h->last_ss = ss;
+    h->last_yy = yy;
+    const bool accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);
+    h->accepted = accept ? 1 : 0;
+    if (accept) {
+      int k = h->k;
+      if (k == h->mem) {  // erase the oldest (lbfgs.hpp:247-251)
+        const int ev = h->order[0];
+        for (int i = 1; i < k; ++i) {
+          h->order[i - 1] = h->order[i];
+          h->rho[i - 1] = h->rho[i];
+          h->sy[i - 1] = h->sy[i];
+          h->yy[i - 1] = h->yy[i];
+        }
+        --k;
+        h->order[k] = scratch;
+        h->scratch = ev;
+      } else {
+        h->order[k] = scratch;
+        // next scratch: the lowest slot not in use
+        int next = 0;
+        for (;; ++next) {
+          bool used = false;
+          for (int i = 0; i <= k; ++i) used |= h->order[i] == next;
+          if (!used) break;
+        }
+        h->scratch = next;
+      }
+      h->rho[k] = 1.0 / sy;
+      h->sy[k] = sy;
+      h->yy[k] = yy;
+      h->k = k + 1;
+    }
   }
 }
 
-void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* sv,
-                 double* yv, int64_t dim, double* partials, int nblocks, EvalScalars* sc,
-                 cudaStream_t s) {
-  k_pair<<<nblocks, 256, 0, s>>>(xt, x, g, gt, sv, yv, dim, partials, sc);
+void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* S,
+                 double* Y, int64_t stride, HistState* h, int64_t dim, double* partials,
+                 int nblocks, EvalScalars* sc, cudaStream_t s) {
+  k_pair<<<nblocks, 256, 0, s>>>(xt, x, g, gt, S, Y, stride, h, dim, partials, sc);
 }
+
+// Clear the history (lbfgs.hpp:102-104, :128-130).
+__global__ void k_hist_reset(HistState* h, int mem) {
+  h->k = 0;
+  h->mem = mem;
+  h->scratch = 0;
+  h->accepted = 0;
+}
+
+void launch_hist_reset(HistState* h, int mem, cudaStream_t s) { k_hist_reset<<<1, 1, 0, s>>>(h, mem); }
 
 // Plain deterministic dot into sc->extra[slot].
 __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ a,

@@ -1,0 +1,508 @@
+// gsot_solver.cu — solve() on the device (solver.hpp:92-293).
+//
+// The host runs the scalar control flow of the reference's L-BFGS ascent
+// (lbfgs.hpp:61-274) verbatim: two-loop direction, strong-Wolfe bracketing
+// and zoom, retry from steepest ascent, the curvature-pair test, chunk hooks
+// and the infinity-norm stop test. Every vector operation and every
+// evaluation runs on the device. Each host decision point needs exactly one
+// device round trip: the work between two decisions is one CUDA graph
+//   DT   two-loop -> trial point -> fused evaluation -> scalars to host
+//   PDT  curvature pair + ring update -> DT            (after an acceptance)
+//   T    trial point -> fused evaluation -> scalars    (further line-search steps)
+//   RF   active set + snapshot (chunk hook) -> |g|_inf -> scalars
+// captured once per context and replayed (the line-search step t and the
+// pair history live in device memory, so the graphs never change). Audit
+// mode runs the same sequences eagerly and re-verifies every evaluation.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <functional>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "gsot_ctx.cuh"
+
+namespace gsot {
+
+namespace {
+
+struct Pt {  // lbfgs.hpp:40-46
+  double t = 0.0, value = 0.0, slope = 0.0;
+  bool vec = false;  // vectors valid in this point's buffer
+};
+
+class Solver {
+ public:
+  Solver(gsot_ctx* c, const gsot_solver_options& o, gsot_solve_result* res, int64_t* hist,
+         int64_t hist_cap)
+      : c_(c), o_(o), res_(res), hist_(hist), hist_cap_(hist_cap) {
+    screened_ = o.mode != GSOT_MODE_BASELINE;
+    use_active_ = o.mode == GSOT_MODE_FAST || o.mode == GSOT_MODE_AUDIT;
+    audit_ = o.mode == GSOT_MODE_AUDIT;
+    graphs_ = !audit_;
+    mode_eval_ = screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE;
+    mem_ = std::max(1, o.lbfgs_memory);
+    ensure_workspace();
+    w_ = c_->ws.get();
+    key_ = std::to_string(o.mode) + "/" + std::to_string(o.lbfgs_memory) + "/" +
+           std::to_string(o.upper_bound_offset) + "/" + std::to_string(c_->profile ? c_->profile_mask : 0u);
+  }
+
+  void run(double* x_out) {
+    const int64_t dim = w_->dim;
+    r_ = 0;
+    GSOT_CUDA_CHECK(cudaMemsetAsync(w_->X[0], 0, sizeof(double) * dim, c_->stream));
+    c_->launch(K_LBFGS, 0.0, [&] { launch_hist_reset(&c_->dsync->h, mem_, c_->stream); });
+    if (screened_) init_snapshot_device(c_, w_->X[0]);  // solver.hpp:141-144
+    // initial gradient + objective (lbfgs.hpp:70-71): one fused evaluation
+    enqueue_eval(c_, w_->X[0], mode_eval_, w_->G[0], nullptr, o_.upper_bound_offset, use_active_);
+    c_->fetch_scalars();
+    EvalOut e0 = eval_result(c_, mode_eval_);
+    record(e0);
+    if (audit_) audit_call(w_->X[0], w_->G[0], e0);
+    res_value_ = e0.objective;
+
+    const auto t0 = std::chrono::steady_clock::now();
+    maximize();
+    const auto t1 = std::chrono::steady_clock::now();
+    res_->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (x_out)
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(x_out, w_->X[r_], sizeof(double) * dim,
+                                      cudaMemcpyDeviceToHost, c_->stream));
+    c_->sync();
+    // finish_solution's dual_objective(x*) (solver.hpp:78) equals the
+    // accepted point's value: screened and dense evaluations agree bitwise.
+    res_->objective = res_value_;
+    res_->outer_loops = res_->chunks;
+  }
+
+ private:
+  void ensure_workspace() {
+    const int64_t dim = c_->m + c_->n;
+    const int mem = std::max(1, o_.lbfgs_memory);
+    auto& ws = c_->ws;
+    if (ws && ws->dim == dim && ws->mem >= mem) return;
+    ws.reset(new SolverWorkspace());
+    ws->dim = dim;
+    ws->mem = mem;
+    size_t* t = &c_->bytes;
+    for (int q = 0; q < 2; ++q) {
+      ws->X[q] = dalloc<double>(dim + 8, t);
+      ws->G[q] = dalloc<double>(dim + 8, t);
+    }
+    ws->lo_x = dalloc<double>(dim, t);
+    ws->lo_g = dalloc<double>(dim, t);
+    ws->prev_x = dalloc<double>(dim, t);
+    ws->prev_g = dalloc<double>(dim, t);
+    ws->d = dalloc<double>(dim + 8, t);
+    ws->S = dalloc<double>(static_cast<size_t>(mem + 1) * dim, t);
+    ws->Y = dalloc<double>(static_cast<size_t>(mem + 1) * dim, t);
+  }
+
+  // ---- device sequences ----------------------------------------------------
+
+  // Run `body` (which enqueues work ending with enqueue_fetch) as a captured
+  // graph keyed by name and iterate parity, or eagerly in audit mode; then
+  // synchronise and account the timing marks.
+  void run_seq(const char* name, const std::function<void()>& body) {
+    if (!graphs_) {
+      body();
+      c_->sync();
+      c_->collect_marks();
+      return;
+    }
+    const std::string key =
+        std::string(name) + "/" + std::to_string(r_) + "/" + key_ + "/" + std::to_string(c_->graph_epoch);
+    auto it = w_->graphs.find(key);
+    if (it == w_->graphs.end()) {
+      std::unique_ptr<Sequence> sq(new Sequence());
+      GSOT_CUDA_CHECK(cudaStreamBeginCapture(c_->stream, cudaStreamCaptureModeThreadLocal));
+      c_->capturing = sq.get();
+      try {
+        body();
+      } catch (...) {
+        c_->capturing = nullptr;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(c_->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      c_->capturing = nullptr;
+      cudaGraph_t g = nullptr;
+      GSOT_CUDA_CHECK(cudaStreamEndCapture(c_->stream, &g));
+      GSOT_CUDA_CHECK(cudaGraphInstantiate(&sq->exec, g, 0));
+      GSOT_CUDA_CHECK(cudaGraphDestroy(g));
+      it = w_->graphs.emplace(key, std::move(sq)).first;
+    }
+    Sequence& sq = *it->second;
+    GSOT_CUDA_CHECK(cudaGraphLaunch(sq.exec, c_->stream));
+    c_->launches += sq.kernels;
+    c_->sync();
+    for (const auto& mk : sq.marks) c_->account(mk);
+  }
+
+  void enqueue_t() {  // the line-search step, read by the axpy kernel
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(&c_->dsync->t, &c_->h_sync->t, sizeof(double),
+                                    cudaMemcpyHostToDevice, c_->stream));
+  }
+  void enqueue_two_loop() {  // lbfgs.hpp:109-126
+    TwoLoopArgs A;
+    A.S = w_->S;
+    A.Y = w_->Y;
+    A.stride = w_->dim;
+    A.h = &c_->dsync->h;
+    A.g = w_->G[r_];
+    A.d = w_->d;
+    A.dim = w_->dim;
+    A.out = c_->dsync->tl;
+    c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 4.0),
+               [&] { launch_two_loop(A, c_->stream); });
+  }
+  void enqueue_pair() {  // res = X[r] (just accepted), previous res = X[1-r]
+    const int q = 1 - r_;
+    c_->launch(K_LBFGS, 8.0 * w_->dim * 6.0, [&] {
+      launch_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim, &c_->dsync->h,
+                  w_->dim, c_->partials, c_->red_blocks, c_->sc, c_->stream);
+    });
+  }
+  void enqueue_trial() {  // trial = X[r] + t d into X[1-r], evaluated into G[1-r]
+    const int q = 1 - r_;
+    enqueue_t();
+    c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
+      launch_axpy_point(w_->X[r_], &c_->dsync->t, w_->d, w_->X[q], w_->dim, c_->stream);
+    });
+    enqueue_eval(c_, w_->X[q], mode_eval_, w_->G[q], w_->d, o_.upper_bound_offset, use_active_);
+  }
+
+  // ---- bookkeeping ---------------------------------------------------------
+
+  void record(const EvalOut& e) {  // GradStats (screening.hpp:280-287, solver.hpp:117-119)
+    const int64_t row = res_->grad_calls;
+    if (hist_ && row < hist_cap_) {
+      hist_[row * 4 + 0] = e.stats.in_active;
+      hist_[row * 4 + 1] = e.stats.skipped;
+      hist_[row * 4 + 2] = e.stats.unskipped;
+      hist_[row * 4 + 3] = e.stats.upper_bounds;
+    }
+    res_->blocks_in_active_set += e.stats.in_active;
+    res_->blocks_skipped += e.stats.skipped;
+    res_->blocks_unskipped += e.stats.unskipped;
+    res_->upper_bounds_evaluated += e.stats.upper_bounds;
+    ++res_->grad_calls;
+  }
+
+  double* px(int which) { return which == 0 ? w_->X[1 - r_] : which == 1 ? w_->lo_x : w_->prev_x; }
+  double* pg(int which) { return which == 0 ? w_->G[1 - r_] : which == 1 ? w_->lo_g : w_->prev_g; }
+  // dst = src for line-search points 0 trial, 1 lo, 2 prev (value copy).
+  void assign(Pt* pts, int dst, int src) {
+    if (dst == src) return;
+    pts[dst] = pts[src];
+    if (pts[src].vec) {
+      const size_t b = sizeof(double) * w_->dim;
+      GSOT_CUDA_CHECK(
+          cudaMemcpyAsync(px(dst), px(src), b, cudaMemcpyDeviceToDevice, c_->stream));
+      GSOT_CUDA_CHECK(
+          cudaMemcpyAsync(pg(dst), pg(src), b, cudaMemcpyDeviceToDevice, c_->stream));
+    }
+  }
+
+  // eval_at (lbfgs.hpp:84-90) for a further step of the current search.
+  void eval_trial(double t, Pt& trial) {
+    c_->h_sync->t = t;
+    run_seq("T", [&] {
+      enqueue_trial();
+      c_->enqueue_fetch();
+    });
+    take_trial(t, trial);
+  }
+  void take_trial(double t, Pt& trial) {
+    EvalOut e = eval_result(c_, mode_eval_);
+    trial.t = t;
+    trial.value = e.objective;
+    trial.slope = e.slope;
+    trial.vec = true;
+    record(e);
+    if (audit_) audit_call(w_->X[1 - r_], w_->G[1 - r_], e);
+  }
+
+  double norm_inf_now() {  // lpNorm<Infinity> of the iterate's gradient
+    run_seq("N", [&] {
+      c_->reset_scalars();
+      c_->launch(K_LBFGS, 8.0 * w_->dim, [&] {
+        launch_absmax(w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
+      });
+      c_->enqueue_fetch();
+    });
+    return c_->h_sc->extra[0];
+  }
+
+  // chunk hook (solver.hpp:212-241) + the stop test (lbfgs.hpp:263-267)
+  double hook_and_norm() {
+    if (!screened_) return norm_inf_now();
+    run_seq("RF", [&] {
+      enqueue_refresh(c_, w_->X[r_], use_active_);
+      c_->launch(K_LBFGS, 8.0 * w_->dim, [&] {
+        launch_absmax(w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
+      });
+      c_->enqueue_fetch();
+    });
+    const double nrm = c_->h_sc->extra[0];
+    if (use_active_) c_->active_count = static_cast<int64_t>(c_->h_sc->counters[0]);
+    if (audit_ && use_active_) audit_active(w_->X[r_]);
+    return nrm;
+  }
+
+  void clear_history() {
+    c_->launch(K_LBFGS, 0.0, [&] { launch_hist_reset(&c_->dsync->h, mem_, c_->stream); });
+    hk_ = 0;
+  }
+
+  // ---- audit (solver.hpp:172-201, :215-240) ---------------------------------
+
+  void audit_call(const double* d_x, const double* d_g, const EvalOut& e) {
+    const DevProblem P = c_->problem();
+    const gsot::DevSync saved = *c_->h_sync;
+    c_->reset_scalars();
+    c_->launch(K_MISC, 0.0, [&] {
+      launch_audit_skips(P, d_x, c_->words, c_->active_words, c_->sc, c_->stream);
+    });
+    c_->fetch_scalars();
+    res_->audit_skip_checks += static_cast<int64_t>(c_->h_sc->counters[0]);
+    if (c_->h_sc->audit_violation) {
+      const long long wv = c_->h_sc->audit_where;
+      throw Error(GSOT_ERR_AUDIT_VIOLATION,
+                  "audit violation: skipped block (l=" + std::to_string(wv / c_->n) +
+                      ", j=" + std::to_string(wv % c_->n) +
+                      ") has nonzero exact gradient at call " + std::to_string(res_->grad_calls));
+    }
+    if (!w_->audit_g) w_->audit_g = dalloc<double>(w_->dim + 8, &c_->bytes);
+    EvalOut d = eval_device(c_, d_x, GSOT_EVAL_DENSE, w_->audit_g, nullptr, 0.0, false);
+    std::vector<double> a(static_cast<size_t>(w_->dim)), b(static_cast<size_t>(w_->dim));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(a.data(), d_g, sizeof(double) * w_->dim,
+                                    cudaMemcpyDeviceToHost, c_->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(b.data(), w_->audit_g, sizeof(double) * w_->dim,
+                                    cudaMemcpyDeviceToHost, c_->stream));
+    c_->sync();
+    res_->audit_column_compares += c_->n;
+    if (memcmp(a.data(), b.data(), sizeof(double) * w_->dim) != 0 || d.objective != e.objective)
+      throw Error(GSOT_ERR_AUDIT_VIOLATION,
+                  "audit violation: screened gradient differs from plain gradient at call " +
+                      std::to_string(res_->grad_calls));
+    ++res_->audit_gradient_calls;
+    *c_->h_sync = saved;
+  }
+
+  void audit_active(const double* d_x) {
+    const DevProblem P = c_->problem();
+    c_->reset_scalars();
+    c_->launch(K_MISC, 0.0, [&] {
+      launch_audit_active(P, d_x, c_->active_words, c_->sc, c_->stream);
+    });
+    c_->fetch_scalars();
+    res_->audit_active_checks += static_cast<int64_t>(c_->h_sc->counters[1]);
+    if (c_->h_sc->audit_violation) {
+      const long long wv = c_->h_sc->audit_where;
+      throw Error(GSOT_ERR_AUDIT_VIOLATION,
+                  "audit violation: active-set block (l=" + std::to_string(wv / c_->n) + ", j=" +
+                      std::to_string(wv % c_->n) + ") has zero exact gradient at build time");
+    }
+  }
+
+  // ---- lbfgs.hpp:61-274 ------------------------------------------------------
+
+  void maximize() {
+    const double c1 = 1e-4, c2 = 0.9;  // MaximizeOptions (lbfgs.hpp:16-19)
+    const int max_bracket = 40, max_zoom = 12;
+    bool stalled = false, zero_gradient = false;
+    bool pending_pair = false;
+    Pt pts[3];  // 0 trial, 1 lo, 2 prev
+    Pt& trial = pts[0];
+    Pt& lo = pts[1];
+    Pt& prev = pts[2];
+    for (int chunk = 0; chunk < o_.max_outer_loops && !stalled && !zero_gradient; ++chunk) {
+      ++res_->chunks;
+      for (int it = 0; it < o_.snapshot_interval; ++it) {
+        bool accepted = false;
+        for (int attempt = 0; attempt < 2 && !accepted; ++attempt) {
+          if (attempt == 1) {  // lbfgs.hpp:100-105
+            if (hk_ == 0) break;
+            clear_history();
+          }
+          // direction (two-loop) and, once the first step is known, the first
+          // trial of the search in the same device sequence
+          double dir_slope, dd;
+          bool have_first = false;
+          if (res_->iterations == 0) {
+            run_seq(pending_pair ? "PD" : "D", [&] {
+              if (pending_pair) enqueue_pair();
+              enqueue_two_loop();
+              c_->enqueue_fetch();
+            });
+          } else {
+            c_->h_sync->t = 1.0;  // t_init (lbfgs.hpp:150)
+            run_seq(pending_pair ? "PDT" : "DT", [&] {
+              if (pending_pair) enqueue_pair();
+              enqueue_two_loop();
+              enqueue_trial();
+              c_->enqueue_fetch();
+            });
+            have_first = true;
+          }
+          pending_pair = false;
+          hk_ = c_->h_sync->h.k;
+          dir_slope = c_->h_sync->tl[0];
+          dd = c_->h_sync->tl[1];
+          if (!(dir_slope > 0.0)) {  // lbfgs.hpp:127-137
+            have_first = false;      // that trial used the rejected direction
+            clear_history();
+            GSOT_CUDA_CHECK(cudaMemcpyAsync(w_->d, w_->G[r_], sizeof(double) * w_->dim,
+                                            cudaMemcpyDeviceToDevice, c_->stream));
+            c_->reset_scalars();
+            c_->launch(K_LBFGS, 16.0 * w_->dim, [&] {
+              launch_dot(w_->G[r_], w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0,
+                         c_->stream);
+            });
+            c_->fetch_scalars();
+            dir_slope = c_->h_sc->extra[0];
+            dd = dir_slope;
+            if (dir_slope == 0.0) {
+              zero_gradient = true;
+              break;
+            }
+          }
+          if (have_first) take_trial(1.0, trial);
+
+          const double f0 = res_value_;  // lbfgs.hpp:141-148
+          const double armijo = c1 * dir_slope;
+          auto sufficient = [&](const Pt& p) { return p.value >= f0 + armijo * p.t; };
+          auto curvature_ok = [&](const Pt& p) { return std::abs(p.slope) <= c2 * dir_slope; };
+
+          double t_init = 1.0;  // lbfgs.hpp:150-154
+          if (res_->iterations == 0) {
+            const double dnorm = std::sqrt(dd);
+            if (dnorm > 0.0) t_init = 1.0 / dnorm;
+          }
+          bool have_bracket = false;
+          lo = Pt{0.0, f0, dir_slope, false};
+          double hi_t = 0.0;
+          double t = t_init;
+          assign(pts, 2, 1);
+          for (int i = 0; i < max_bracket; ++i) {  // lbfgs.hpp:165-187
+            if (i == 0 && have_first && t == 1.0) {
+              // the first trial already ran inside the direction sequence
+            } else {
+              eval_trial(t, trial);
+            }
+            if (!sufficient(trial) || (i > 0 && trial.value <= prev.value)) {
+              assign(pts, 1, 2);
+              hi_t = trial.t;
+              have_bracket = true;
+              break;
+            }
+            if (curvature_ok(trial)) {
+              accepted = true;
+              break;
+            }
+            if (trial.slope <= 0.0) {
+              assign(pts, 1, 0);
+              hi_t = prev.t;
+              have_bracket = true;
+              break;
+            }
+            assign(pts, 2, 0);
+            t *= 2.0;
+          }
+          if (!accepted && have_bracket) {  // lbfgs.hpp:189-231
+            double hi_value = std::numeric_limits<double>::quiet_NaN();
+            for (int i = 0; i < max_zoom; ++i) {
+              double cand = 0.5 * (lo.t + hi_t);
+              if (std::isfinite(hi_value)) {
+                const double dt = hi_t - lo.t;
+                const double denom = 2.0 * (lo.value + lo.slope * dt - hi_value);
+                if (denom != 0.0) {
+                  const double interp = lo.t + lo.slope * dt * dt / denom;
+                  const double lo_guard = lo.t + 0.1 * dt;
+                  const double hi_guard = hi_t - 0.1 * dt;
+                  const double lim_min = std::min(lo_guard, hi_guard);
+                  const double lim_max = std::max(lo_guard, hi_guard);
+                  if (interp >= lim_min && interp <= lim_max) cand = interp;
+                }
+              }
+              if (cand == lo.t || cand == hi_t) break;
+              eval_trial(cand, trial);
+              if (!sufficient(trial) || trial.value <= lo.value) {
+                hi_t = cand;
+                hi_value = trial.value;
+                continue;
+              }
+              if (curvature_ok(trial)) {
+                accepted = true;
+                break;
+              }
+              if (trial.slope * (hi_t - lo.t) <= 0.0) {
+                hi_t = lo.t;
+                hi_value = lo.value;
+              }
+              assign(pts, 1, 0);
+            }
+            if (!accepted && lo.t > 0.0) {
+              assign(pts, 0, 1);
+              accepted = true;
+            }
+          }
+          if (!accepted && !have_bracket && prev.t > 0.0) {
+            assign(pts, 0, 2);
+            accepted = true;
+          }
+        }
+        if (zero_gradient) break;
+        if (!accepted) {
+          stalled = true;
+          break;
+        }
+        // accept: the trial buffer becomes the iterate; the curvature pair
+        // (lbfgs.hpp:243-255) is formed at the start of the next sequence,
+        // before the old iterate's buffer is reused.
+        r_ = 1 - r_;
+        res_value_ = trial.value;
+        ++res_->iterations;
+        pending_pair = true;
+        trial.vec = lo.vec = prev.vec = false;
+      }
+      if (stalled) break;
+      if (hook_and_norm() <= o_.grad_tol) {
+        res_->converged = 1;
+        break;
+      }
+    }
+    if (!res_->converged) res_->converged = norm_inf_now() <= o_.grad_tol;
+    res_->line_search_failed = stalled && !res_->converged;
+  }
+
+  gsot_ctx* c_;
+  gsot_solver_options o_;
+  gsot_solve_result* res_;
+  int64_t* hist_;
+  int64_t hist_cap_;
+  SolverWorkspace* w_ = nullptr;
+  std::string key_;
+  int mem_ = 10;  // history capacity (lbfgs_memory)
+  int r_ = 0;    // iterate buffer index
+  int hk_ = 0;  // history length mirrored from the device
+  double res_value_ = 0.0;
+  bool screened_ = false, use_active_ = false, audit_ = false, graphs_ = true;
+  int mode_eval_ = GSOT_EVAL_DENSE;
+};
+
+}  // namespace
+
+void run_solve(gsot_ctx* c, const gsot_solver_options& o, double* x_out, gsot_solve_result* res,
+               int64_t* history, int64_t history_cap) {
+  Solver s(c, o, res, history, history_cap);
+  s.run(x_out);
+}
+
+}  // namespace gsot

@@ -379,7 +379,10 @@ class Context:
         res["history"] = hist[: 4 * min(history_cap, r.grad_calls)].reshape(-1, 4)
         return res
 
-    def profile(self, enable: bool) -> None:
+    def profile(self, enable) -> None:
+        """False: off; True: time every kernel class; int: bit mask (1 << kind)."""
+        if enable is True:
+            enable = -1
         _raise(_lib.lib().gsot_profile_enable(self._h, int(enable)))
 
     def profile_read(self, kind: int):
