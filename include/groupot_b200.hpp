@@ -1,0 +1,223 @@
+// groupot_b200.hpp — drop-in adapter: the reference `groupot` C++ API on
+// top of the B200 C ABI (gsot.h).
+//
+// Include AFTER the reference headers ("groupot/solver.hpp"). It adds the
+// namespace groupot::b200 with the same entry points and types as the
+// reference's solver.hpp / dual.hpp / screening.hpp, backed by libgsot.so:
+//
+//   reference                                  drop-in
+//   groupot::solve(inst, p, opts)              groupot::b200::solve(inst, p, opts)
+//   groupot::solve_baseline / solve_fast       groupot::b200::solve_baseline / solve_fast
+//   groupot::audit_solve(inst, p, opts, off)   groupot::b200::audit_solve(...)
+//   groupot::dual_objective(s, inst, p)        groupot::b200::Device::objective(s)
+//   groupot::dual_gradient(s, inst, p, ga, gb) groupot::b200::Device::gradient(s, ga, gb)
+//   groupot::recover_plan(s, inst, p)          groupot::b200::Device::plan(s)
+//   ObjectiveFn / GradientFn closures          groupot::b200::Device::callbacks()
+//
+// Inputs are read straight from the Eigen storage (column-major cost, as
+// ProblemInstance holds it, solver.hpp:47-55); status codes are rethrown as
+// the reference's exception classes (errors.hpp) with their fields.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gsot.h"
+
+namespace groupot {
+namespace b200 {
+
+// Status -> the reference's exception types (errors.hpp:190-271).
+inline void check(int st) {
+  if (st == GSOT_OK) return;
+  gsot_error_detail d;
+  gsot_last_error_detail(&d);
+  std::string msg = gsot_last_error();
+  auto strip = [&](const char* prefix) {
+    const std::string p(prefix);
+    if (msg.compare(0, p.size(), p) == 0) msg = msg.substr(p.size());
+  };
+  switch (st) {
+    case GSOT_ERR_DIMENSION_MISMATCH: strip("dimension mismatch: "); throw DimensionMismatch(msg);
+    case GSOT_ERR_NEGATIVE_COST: throw NegativeCost(d.row, d.col, d.value);
+    case GSOT_ERR_MARGINAL_NOT_NORMALIZED:
+      strip(std::string("marginal ").append(1, d.which).append(": ").c_str());
+      throw MarginalNotNormalized(d.which, d.index, msg);
+    case GSOT_ERR_PARTITION_MISMATCH: strip("group partition: "); throw PartitionMismatch(msg);
+    case GSOT_ERR_RHO_OUT_OF_RANGE: throw Error(msg);
+    case GSOT_ERR_AUDIT_VIOLATION: strip("audit violation: "); throw AuditViolation(msg);
+    default: throw Error(msg);
+  }
+}
+
+// The resident instance on the GPU (one gsot_ctx).
+class Device {
+ public:
+  Device(const ProblemInstance& inst, const RegParams& p) : m_(inst.m()), n_(inst.n()) {
+    std::vector<int32_t> sizes(inst.groups.sizes().begin(), inst.groups.sizes().end());
+    if (inst.a.size() != m_ || inst.b.size() != n_)
+      throw DimensionMismatch("marginals do not match the cost matrix");
+    check(gsot_create(inst.cost.data(), m_, n_, sizes.data(), static_cast<int32_t>(sizes.size()),
+                      inst.a.data(), inst.b.data(), p.gamma(), p.mu(), &ctx_));
+  }
+  ~Device() { gsot_destroy(ctx_); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+
+  gsot_ctx* handle() const { return ctx_; }
+
+  // dual_objective (dual.hpp:38-52)
+  double objective(const DualState& s) {
+    double obj = 0.0;
+    pack(s);
+    check(gsot_eval(ctx_, x_.data(), GSOT_EVAL_DENSE, &obj, nullptr, nullptr));
+    return obj;
+  }
+  // dual_gradient (dual.hpp:85-100)
+  void gradient(const DualState& s, Eigen::VectorXd& ga, Eigen::VectorXd& gb) {
+    pack(s);
+    g_.resize(static_cast<size_t>(m_ + n_));
+    check(gsot_eval(ctx_, x_.data(), GSOT_EVAL_DENSE, nullptr, g_.data(), nullptr));
+    ga.resize(m_);
+    gb.resize(n_);
+    std::memcpy(ga.data(), g_.data(), sizeof(double) * static_cast<size_t>(m_));
+    std::memcpy(gb.data(), g_.data() + m_, sizeof(double) * static_cast<size_t>(n_));
+  }
+  // recover_plan (dual.hpp:116-128)
+  TransportPlan plan(const DualState& s) {
+    pack(s);
+    TransportPlan t;
+    t.plan.resize(m_, n_);
+    check(gsot_plan_columns(ctx_, x_.data(), 0, n_, t.plan.data()));
+    return t;
+  }
+  // ObjectiveFn / GradientFn for the reference's maximize (lbfgs.hpp:32-33):
+  // one fused device evaluation serves both calls at the same x.
+  std::pair<ObjectiveFn, GradientFn> callbacks() {
+    ObjectiveFn f = [this](const Eigen::VectorXd& x) {
+      eval_cached(x);
+      return cache_obj_;
+    };
+    GradientFn g = [this](const Eigen::VectorXd& x, Eigen::VectorXd& out) {
+      eval_cached(x);
+      out.resize(m_ + n_);
+      std::memcpy(out.data(), g_.data(), sizeof(double) * static_cast<size_t>(m_ + n_));
+    };
+    return {f, g};
+  }
+
+ private:
+  void pack(const DualState& s) {
+    if (s.alpha.size() != m_ || s.beta.size() != n_)
+      throw DimensionMismatch("dual state does not match the instance");
+    x_.resize(static_cast<size_t>(m_ + n_));
+    std::memcpy(x_.data(), s.alpha.data(), sizeof(double) * static_cast<size_t>(m_));
+    std::memcpy(x_.data() + m_, s.beta.data(), sizeof(double) * static_cast<size_t>(n_));
+  }
+  void eval_cached(const Eigen::VectorXd& x) {
+    const size_t dim = static_cast<size_t>(m_ + n_);
+    if (have_cache_ && cache_x_.size() == dim &&
+        std::memcmp(cache_x_.data(), x.data(), sizeof(double) * dim) == 0)
+      return;
+    cache_x_.assign(x.data(), x.data() + dim);
+    g_.resize(dim);
+    check(gsot_eval(ctx_, cache_x_.data(), GSOT_EVAL_DENSE, &cache_obj_, g_.data(), nullptr));
+    have_cache_ = true;
+  }
+
+  gsot_ctx* ctx_ = nullptr;
+  Eigen::Index m_, n_;
+  std::vector<double> x_, g_, cache_x_;
+  double cache_obj_ = 0.0;
+  bool have_cache_ = false;
+};
+
+namespace detail {
+
+inline Solution run(const ProblemInstance& inst, const RegParams& p, const SolverOptions& opts,
+                    int mode, double ub_offset, AuditReport* report) {
+  Device dev(inst, p);
+  gsot_solver_options o;
+  gsot_default_solver_options(&o);
+  o.snapshot_interval = opts.snapshot_interval;
+  o.grad_tol = opts.grad_tol;
+  o.max_outer_loops = opts.max_outer_loops;
+  o.lbfgs_memory = opts.lbfgs_memory;
+  o.mode = mode;
+  o.upper_bound_offset = ub_offset;
+  const Eigen::Index m = inst.m(), n = inst.n();
+  std::vector<double> x(static_cast<size_t>(m + n));
+  const int64_t cap = static_cast<int64_t>(opts.snapshot_interval) * opts.max_outer_loops * 64 + 16;
+  std::vector<int64_t> hist(static_cast<size_t>(cap) * 4);
+  gsot_solve_result r;
+  check(gsot_solve(dev.handle(), &o, x.data(), &r, hist.data(), cap));
+  Solution sol;  // solver.hpp:33-42, finish_solution (:72-87)
+  sol.state.alpha.resize(m);
+  sol.state.beta.resize(n);
+  std::memcpy(sol.state.alpha.data(), x.data(), sizeof(double) * static_cast<size_t>(m));
+  std::memcpy(sol.state.beta.data(), x.data() + m, sizeof(double) * static_cast<size_t>(n));
+  sol.objective = r.objective;
+  sol.plan = dev.plan(sol.state);
+  sol.stats.blocks_in_active_set = r.blocks_in_active_set;
+  sol.stats.blocks_skipped = r.blocks_skipped;
+  sol.stats.blocks_unskipped = r.blocks_unskipped;
+  sol.stats.upper_bounds_evaluated = r.upper_bounds_evaluated;
+  sol.stats.outer_loops = r.outer_loops;
+  sol.stats.grad_calls = r.grad_calls;
+  const int64_t rows = std::min<int64_t>(r.grad_calls, cap);
+  for (int64_t i = 0; i < rows; ++i)
+    sol.stats.history.push_back({hist[i * 4], hist[i * 4 + 1], hist[i * 4 + 2], hist[i * 4 + 3]});
+  sol.iterations = r.iterations;
+  sol.wall_time = std::chrono::nanoseconds(static_cast<int64_t>(r.wall_seconds * 1e9));
+  sol.converged = r.converged != 0;
+  sol.line_search_failed = r.line_search_failed != 0;
+  if (report) {
+    report->skip_checks = r.audit_skip_checks;
+    report->active_checks = r.audit_active_checks;
+    report->column_compares = r.audit_column_compares;
+    report->gradient_calls = r.audit_gradient_calls;
+  }
+  return sol;
+}
+
+}  // namespace detail
+
+// solver.hpp:92-127
+inline Solution solve_baseline(const ProblemInstance& inst, const RegParams& p,
+                               const SolverOptions& opts = {}) {
+  return detail::run(inst, p, opts, GSOT_MODE_BASELINE, 0.0, nullptr);
+}
+// solver.hpp:254-258
+inline Solution solve_fast(const ProblemInstance& inst, const RegParams& p,
+                           const SolverOptions& opts = {}) {
+  const int mode = opts.mode == SolverMode::fast_no_lower_bound ? GSOT_MODE_FAST_NO_LOWER_BOUND
+                                                                : GSOT_MODE_FAST;
+  return detail::run(inst, p, opts, mode, 0.0, nullptr);
+}
+// solver.hpp:268-281
+inline std::pair<Solution, AuditReport> audit_solve(const ProblemInstance& inst,
+                                                    const RegParams& p,
+                                                    const SolverOptions& opts = {},
+                                                    double upper_bound_offset = 0.0) {
+  AuditReport report;
+  if (opts.mode == SolverMode::baseline) return {b200::solve_baseline(inst, p, opts), report};
+  Solution sol = detail::run(inst, p, opts, GSOT_MODE_AUDIT, upper_bound_offset, &report);
+  return {std::move(sol), report};
+}
+// solver.hpp:284-293
+inline Solution solve(const ProblemInstance& inst, const RegParams& p,
+                      const SolverOptions& opts = {}) {
+  switch (opts.mode) {
+    case SolverMode::baseline: return b200::solve_baseline(inst, p, opts);
+    case SolverMode::fast:
+    case SolverMode::fast_no_lower_bound: return b200::solve_fast(inst, p, opts);
+    case SolverMode::audit: return b200::audit_solve(inst, p, opts).first;
+  }
+  throw Error("unknown solver mode");
+}
+
+}  // namespace b200
+}  // namespace groupot

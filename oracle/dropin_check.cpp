@@ -1,0 +1,107 @@
+// dropin_check.cpp — TEST INFRASTRUCTURE: the reference C++ API, unchanged,
+// next to the drop-in groupot::b200 adapter (include/groupot_b200.hpp) on
+// the same ProblemInstance. Built by oracle/Makefile into oracle/_ref/ (it
+// needs the reference headers, present in the build container only) and run
+// on the GPU box by tests/test_gpu_dropin.py. Prints one JSON object.
+#include <cmath>
+#include <cstdio>
+#include <exception>
+
+#include "groupot/data_io.hpp"
+#include "groupot/solver.hpp"
+#include "groupot_b200.hpp"
+
+using namespace groupot;
+
+static double max_abs_diff(const Eigen::MatrixXd& a, const Eigen::MatrixXd& b) {
+  double m = 0.0;
+  for (Eigen::Index j = 0; j < a.cols(); ++j)
+    for (Eigen::Index i = 0; i < a.rows(); ++i) m = std::max(m, std::abs(a(i, j) - b(i, j)));
+  return m;
+}
+
+int main() {
+  // the reference's own generator and instance builder (data_io.hpp:67-98, :157-181)
+  auto [src, tgt] = gen_synthetic(4, 25, 7);
+  ProblemInstance inst = make_instance(src, tgt, true);
+  const RegParams p(1.0, 0.1);
+  std::printf("{");
+  // evaluation through the adapter vs the reference
+  DualState s{Eigen::VectorXd::Constant(inst.m(), 0.02), Eigen::VectorXd::Constant(inst.n(), 0.01)};
+  b200::Device dev(inst, p);
+  const double obj_ref = dual_objective(s, inst, p);
+  const double obj_dev = dev.objective(s);
+  Eigen::VectorXd ga, gb, ga2, gb2;
+  dual_gradient(s, inst, p, ga, gb);
+  dev.gradient(s, ga2, gb2);
+  double gerr = 0.0;
+  for (Eigen::Index i = 0; i < ga.size(); ++i) gerr = std::max(gerr, std::abs(ga[i] - ga2[i]));
+  for (Eigen::Index j = 0; j < gb.size(); ++j) gerr = std::max(gerr, std::abs(gb[j] - gb2[j]));
+  const double plan_err = max_abs_diff(recover_plan(s, inst, p).plan, dev.plan(s).plan);
+  std::printf("\"obj_rel\": %.3e, \"grad_abs\": %.3e, \"plan_eval_abs\": %.3e",
+              std::abs(obj_dev - obj_ref) / std::abs(obj_ref), gerr, plan_err);
+  // the reference's own maximize() driving device evaluations
+  {
+    auto [f, g] = dev.callbacks();
+    MaximizeOptions mo;
+    mo.max_chunks = 3;
+    mo.grad_tol = 1e-12;
+    const MaximizeResult rd = maximize(f, g, Eigen::VectorXd::Zero(inst.m() + inst.n()), mo);
+    SolverOptions so;
+    so.max_outer_loops = 3;
+    so.grad_tol = 1e-12;
+    so.mode = SolverMode::baseline;
+    const Solution rr = groupot::solve(inst, p, so);
+    double xd = 0.0;
+    for (Eigen::Index i = 0; i < inst.m(); ++i) xd = std::max(xd, std::abs(rd.x[i] - rr.state.alpha[i]));
+    std::printf(", \"maximize_iters\": [%d, %d], \"maximize_x_abs\": %.3e", rd.iterations,
+                rr.iterations, xd);
+  }
+  // solve() in every mode: reference vs drop-in
+  const SolverMode modes[] = {SolverMode::baseline, SolverMode::fast,
+                              SolverMode::fast_no_lower_bound, SolverMode::audit};
+  for (SolverMode mode : modes) {
+    SolverOptions o;
+    o.mode = mode;
+    o.max_outer_loops = 30;
+    const Solution r = groupot::solve(inst, p, o);
+    const Solution d = b200::solve(inst, p, o);
+    std::printf(", \"%s\": {\"iters\": [%d, %d], \"converged\": [%d, %d], \"obj_rel\": %.3e, "
+                "\"plan_abs\": %.3e, \"grad_calls\": [%ld, %ld]}",
+                to_string(mode), r.iterations, d.iterations, (int)r.converged, (int)d.converged,
+                std::abs(d.objective - r.objective) / std::abs(r.objective),
+                max_abs_diff(r.plan.plan, d.plan.plan), (long)r.stats.grad_calls,
+                (long)d.stats.grad_calls);
+  }
+  // error behaviour: the same exception type and fields
+  {
+    ProblemInstance bad = inst;
+    bad.cost(3, 2) = -1.0;
+    int ok = 0;
+    try {
+      b200::solve(bad, p);
+    } catch (const NegativeCost& e) {
+      ok = e.row == 3 && e.col == 2 && e.value == -1.0;
+    }
+    ProblemInstance bad2 = inst;
+    bad2.a[0] = -0.5;
+    int ok2 = 0;
+    try {
+      b200::solve(bad2, p);
+    } catch (const MarginalNotNormalized& e) {
+      ok2 = e.which == 'a' && e.index == 0;
+    }
+    int ok3 = 0;
+    try {
+      SolverOptions o;
+      o.mode = SolverMode::audit;
+      b200::audit_solve(inst, p, o, -1e3);
+    } catch (const AuditViolation&) {
+      ok3 = 1;
+    }
+    std::printf(", \"negative_cost_fields\": %d, \"marginal_fields\": %d, \"audit_violation\": %d",
+                ok, ok2, ok3);
+  }
+  std::printf("}\n");
+  return 0;
+}

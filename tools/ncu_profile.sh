@@ -1,5 +1,11 @@
+#!/bin/bash
+# ncu evidence for profiles/: launch list (device time per kernel, cold-cache,
+# serialised) and one --set full capture of the hot kernels. Run on the GPU box
+# only after the same bench command exited 0 without ncu.
 set -x
-python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain1.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches1.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_l.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_snapshot|k_eval|k_finalize|k_two_loop|k_delta|k_bounds|k_objective" -s 40 -c 14 -o gpurun_out/prof1 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_f.log 2>&1
+TAG=${1:-r1}
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
+$CMD > gpurun_out/plain_$TAG.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_l_$TAG.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_snapshot|k_eval|k_finalize|k_two_loop|k_bounds|k_objective|k_pair" -s 300 -c 14 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_f_$TAG.log 2>&1
 echo DONE $?
