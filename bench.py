@@ -306,12 +306,15 @@ def run_ours(args, world, rank, local, pg):
     barrier(pg)
     ctx.timer_start()
     calls, iters_done, solve_ms = 0, 0, []
+    blocks, tasks = 0, 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
         r = ctx.solve(**solve_kw)
         solve_ms.append(1e3 * (time.perf_counter() - t0))
         calls += r["grad_calls"]
         iters_done += r["iterations"]
+        blocks += r["eval_blocks"]
+        tasks += r["eval_tasks"]
     ms = ctx.timer_stop()
     barrier(pg)
     clk = clocks.stop()
@@ -373,6 +376,8 @@ def run_ours(args, world, rank, local, pg):
             "solve_ms": statistics.median(solve_ms),
             "evals_per_solve": calls / args.steps,
             "iterations_per_solve": iters_done / args.steps,
+            "screening": {"blocks_computed_frac": blocks / (calls * ctx.L * ctx.n),
+                          "active_lanes_per_task": blocks / max(tasks, 1)},
             "roofline": roofline,
             "kernels": kinds,
             "gpu_launches": launches,

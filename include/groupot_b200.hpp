@@ -135,6 +135,12 @@ class Device {
   bool have_cache_ = false;
 };
 
+// Exact-order solves (bitwise the reference's trajectory; verification mode).
+inline bool& exact_order() {
+  static bool on = false;
+  return on;
+}
+
 namespace detail {
 
 inline Solution run(const ProblemInstance& inst, const RegParams& p, const SolverOptions& opts,
@@ -148,6 +154,7 @@ inline Solution run(const ProblemInstance& inst, const RegParams& p, const Solve
   o.lbfgs_memory = opts.lbfgs_memory;
   o.mode = mode;
   o.upper_bound_offset = ub_offset;
+  o.flags = exact_order() ? GSOT_SOLVE_EXACT : 0;
   const Eigen::Index m = inst.m(), n = inst.n();
   std::vector<double> x(static_cast<size_t>(m + n));
   const int64_t cap = static_cast<int64_t>(opts.snapshot_interval) * opts.max_outer_loops * 64 + 16;

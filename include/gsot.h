@@ -111,7 +111,13 @@ GSOT_API int gsot_shape(const gsot_ctx* ctx, int64_t* m, int64_t* n, int32_t* L,
 
 /* ---- Stage 1: fused evaluation (ObjectiveFn + GradientFn) ---------------- */
 
-enum { GSOT_EVAL_DENSE = 0, GSOT_EVAL_SCREENED = 1 };
+enum {
+  GSOT_EVAL_DENSE = 0,
+  GSOT_EVAL_SCREENED = 1,
+  /* | GSOT_EVAL_EXACT: cross-block sums in the reference's own order
+   * (sequential; verification mode) */
+  GSOT_EVAL_EXACT = 2
+};
 
 /* GradStats::PerCall (screening.hpp:181-186). */
 typedef struct gsot_call_stats {
@@ -173,7 +179,10 @@ typedef struct gsot_solver_options {
   int32_t lbfgs_memory;      /* 10 */
   int32_t mode;              /* GSOT_MODE_FAST */
   double upper_bound_offset; /* 0.0; fault injection (solver.hpp:266-270) */
+  int32_t flags;             /* GSOT_SOLVE_EXACT: reference-order sums and dots */
 } gsot_solver_options;
+
+enum { GSOT_SOLVE_EXACT = 1 };
 
 /* Solution (solver.hpp:33-42) minus the dense state/plan (returned through
  * x_out and gsot_plan_columns), GradStats totals (screening.hpp:173-180)
@@ -195,6 +204,10 @@ typedef struct gsot_solve_result {
   int64_t audit_active_checks;
   int64_t audit_column_compares;
   int64_t audit_gradient_calls;
+  /* work of the screened evaluations: blocks computed (|W| = active set +
+   * unskipped) and (group, 32-column) tasks launched, summed over calls */
+  int64_t eval_blocks;
+  int64_t eval_tasks;
 } gsot_solve_result;
 
 GSOT_API void gsot_default_solver_options(gsot_solver_options* o);

@@ -41,7 +41,7 @@ class CallStats(C.Structure):
 class SolverOptionsC(C.Structure):
     _fields_ = [("snapshot_interval", C.c_int32), ("grad_tol", C.c_double),
                 ("max_outer_loops", C.c_int32), ("lbfgs_memory", C.c_int32),
-                ("mode", C.c_int32), ("upper_bound_offset", C.c_double)]
+                ("mode", C.c_int32), ("upper_bound_offset", C.c_double), ("flags", C.c_int32)]
 
 
 class SolveResultC(C.Structure):
@@ -52,7 +52,8 @@ class SolveResultC(C.Structure):
                 ("outer_loops", C.c_int64), ("grad_calls", C.c_int64),
                 ("wall_seconds", C.c_double), ("audit_skip_checks", C.c_int64),
                 ("audit_active_checks", C.c_int64), ("audit_column_compares", C.c_int64),
-                ("audit_gradient_calls", C.c_int64)]
+                ("audit_gradient_calls", C.c_int64), ("eval_blocks", C.c_int64),
+                ("eval_tasks", C.c_int64)]
 
 
 # Every entry point of include/gsot.h with its C signature.

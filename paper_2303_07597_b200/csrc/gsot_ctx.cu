@@ -340,8 +340,10 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
 
 namespace gsot {
 
-void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, const double* d_dir,
-                  double ub_offset, bool use_active) {
+void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad,
+                  const double* d_dir, double ub_offset, bool use_active) {
+  const bool exact = (mode_flags & GSOT_EVAL_EXACT) != 0;
+  const int mode = mode_flags & 1;
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
   const DevProblem P = c->problem();
@@ -361,6 +363,12 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, cons
     words = c->words;
     tasks = c->tasks;
   }
+  if (exact) {  // reference-order sums (gsot_exact.cu); the screen only counts
+    c->launch(K_EVAL, 0.0, [&] {
+      launch_exact_eval(P, d_x, c->colpart, c->psi, d_grad, d_dir, c->sc, c->stream);
+    });
+    return;
+  }
   const double dense_bytes = 8.0 * c->m * c->n + 8.0 * c->m * c->nw + 16.0 * Ln;
   c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
     launch_eval(P, d_x, tasks, mode == GSOT_EVAL_DENSE ? max_tasks : -1, words, c->rowpart,
@@ -375,7 +383,8 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, cons
   });
 }
 
-EvalOut eval_result(gsot_ctx* c, int mode) {
+EvalOut eval_result(gsot_ctx* c, int mode_flags) {
+  const int mode = mode_flags & 1;
   EvalOut o;
   o.objective = c->h_sc->objective;
   o.slope = c->h_sc->slope;
@@ -536,8 +545,7 @@ GSOT_API int gsot_eval(gsot_ctx* ctx, const double* x, int mode, double* objecti
                        gsot_call_stats* stats) {
   return guard([&] {
     checked(ctx);
-    if (mode != GSOT_EVAL_DENSE && mode != GSOT_EVAL_SCREENED)
-      throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
+    if (mode < 0 || mode > 3) throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
     upload_x(ctx, x);
     EvalOut e = eval_device(ctx, ctx->x_eval, mode, ctx->g_eval, nullptr, 0.0, true);
     if (grad) {
@@ -555,8 +563,7 @@ GSOT_API int gsot_eval_device(gsot_ctx* ctx, const double* d_x, int mode, double
   return guard([&] {
     checked(ctx);
     if (!d_x || !d_grad) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null device pointer");
-    if (mode != GSOT_EVAL_DENSE && mode != GSOT_EVAL_SCREENED)
-      throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
+    if (mode < 0 || mode > 3) throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
     GSOT_CUDA_CHECK(cudaMemcpyAsync(ctx->x_eval, d_x, sizeof(double) * (ctx->m + ctx->n),
                                     cudaMemcpyDeviceToDevice, ctx->stream));
     EvalOut e = eval_device(ctx, ctx->x_eval, mode, d_grad, nullptr, 0.0, true);
@@ -670,6 +677,7 @@ GSOT_API void gsot_default_solver_options(gsot_solver_options* o) {
   o->lbfgs_memory = 10;
   o->mode = GSOT_MODE_FAST;
   o->upper_bound_offset = 0.0;
+  o->flags = 0;
 }
 
 GSOT_API int gsot_solve(gsot_ctx* ctx, const gsot_solver_options* opts, double* x_out,

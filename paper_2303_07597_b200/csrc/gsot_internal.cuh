@@ -176,6 +176,16 @@ void launch_dot(const double* a, const double* b, int64_t dim, double* partials,
 void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, EvalScalars* sc,
                    int slot, cudaStream_t s);
 
+// Exact-order mode (gsot_exact.cu).
+void launch_exact_eval(const DevProblem& P, const double* x, double* scale, double* psi,
+                       double* grad, const double* dvec, EvalScalars* sc, cudaStream_t s);
+void launch_exact_two_loop(const TwoLoopArgs& a, cudaStream_t s);
+void launch_exact_pair(const double* xt, const double* x, const double* g, const double* gt,
+                       double* S, double* Y, int64_t stride, HistState* h, int64_t dim,
+                       EvalScalars* sc, cudaStream_t s);
+void launch_exact_dot(const double* a, const double* b, int64_t dim, EvalScalars* sc, int slot,
+                      cudaStream_t s);
+
 // Cost-matrix construction (gsot_data.cu).
 // tiled == nullptr: column-major m x n output; otherwise the column-tiled
 // layout of that problem.

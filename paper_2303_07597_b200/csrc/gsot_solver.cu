@@ -43,12 +43,14 @@ class Solver {
     use_active_ = o.mode == GSOT_MODE_FAST || o.mode == GSOT_MODE_AUDIT;
     audit_ = o.mode == GSOT_MODE_AUDIT;
     graphs_ = !audit_;
-    mode_eval_ = screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE;
+    exact_ = (o.flags & GSOT_SOLVE_EXACT) != 0;
+    mode_eval_ = (screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE) | (exact_ ? GSOT_EVAL_EXACT : 0);
     mem_ = std::max(1, o.lbfgs_memory);
     ensure_workspace();
     w_ = c_->ws.get();
     key_ = std::to_string(o.mode) + "/" + std::to_string(o.lbfgs_memory) + "/" +
-           std::to_string(o.upper_bound_offset) + "/" + std::to_string(c_->profile ? c_->profile_mask : 0u);
+           std::to_string(o.upper_bound_offset) + "/" + std::to_string(c_->profile ? c_->profile_mask : 0u) +
+           (exact_ ? "/exact" : "");
   }
 
   void run(double* x_out) {
@@ -158,14 +160,22 @@ class Solver {
     A.d = w_->d;
     A.dim = w_->dim;
     A.out = c_->dsync->tl;
-    c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 4.0),
-               [&] { launch_two_loop(A, c_->stream); });
+    c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 4.0), [&] {
+      if (exact_)
+        launch_exact_two_loop(A, c_->stream);
+      else
+        launch_two_loop(A, c_->stream);
+    });
   }
   void enqueue_pair() {  // res = X[r] (just accepted), previous res = X[1-r]
     const int q = 1 - r_;
     c_->launch(K_LBFGS, 8.0 * w_->dim * 6.0, [&] {
-      launch_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim, &c_->dsync->h,
-                  w_->dim, c_->partials, c_->red_blocks, c_->sc, c_->stream);
+      if (exact_)
+        launch_exact_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim,
+                          &c_->dsync->h, w_->dim, c_->sc, c_->stream);
+      else
+        launch_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim,
+                    &c_->dsync->h, w_->dim, c_->partials, c_->red_blocks, c_->sc, c_->stream);
     });
   }
   void enqueue_trial() {  // trial = X[r] + t d into X[1-r], evaluated into G[1-r]
@@ -192,6 +202,13 @@ class Solver {
     res_->blocks_unskipped += e.stats.unskipped;
     res_->upper_bounds_evaluated += e.stats.upper_bounds;
     ++res_->grad_calls;
+    if ((mode_eval_ & 1) == GSOT_EVAL_SCREENED) {
+      res_->eval_blocks += e.stats.in_active + e.stats.unskipped;
+      res_->eval_tasks += c_->h_sc->ntasks;
+    } else {
+      res_->eval_blocks += static_cast<int64_t>(c_->L) * c_->n;
+      res_->eval_tasks += static_cast<int64_t>(c_->L) * c_->nw;
+    }
   }
 
   double* px(int which) { return which == 0 ? w_->X[1 - r_] : which == 1 ? w_->lo_x : w_->prev_x; }
@@ -362,8 +379,11 @@ class Solver {
                                             cudaMemcpyDeviceToDevice, c_->stream));
             c_->reset_scalars();
             c_->launch(K_LBFGS, 16.0 * w_->dim, [&] {
-              launch_dot(w_->G[r_], w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0,
-                         c_->stream);
+              if (exact_)
+                launch_exact_dot(w_->G[r_], w_->G[r_], w_->dim, c_->sc, 0, c_->stream);
+              else
+                launch_dot(w_->G[r_], w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0,
+                           c_->stream);
             });
             c_->fetch_scalars();
             dir_slope = c_->h_sc->extra[0];
@@ -493,7 +513,7 @@ class Solver {
   int r_ = 0;    // iterate buffer index
   int hk_ = 0;  // history length mirrored from the device
   double res_value_ = 0.0;
-  bool screened_ = false, use_active_ = false, audit_ = false, graphs_ = true;
+  bool screened_ = false, use_active_ = false, audit_ = false, graphs_ = true, exact_ = false;
   int mode_eval_ = GSOT_EVAL_DENSE;
 };
 

@@ -320,7 +320,7 @@ class Context:
     def set_params(self, gamma: float, mu: float) -> None:
         _raise(_lib.lib().gsot_set_params(self._h, float(gamma), float(mu)))
 
-    def eval(self, x, screened: bool = False):
+    def eval(self, x, screened: bool = False, exact: bool = False):
         x = _f64(x)
         if x.size != self.m + self.n:
             raise DimensionMismatch(
@@ -330,8 +330,8 @@ class Context:
         obj = C.c_double()
         st = CallStatsPy()
         cs = _lib.CallStats()
-        _raise(_lib.lib().gsot_eval(self._h, _ptr(x), 1 if screened else 0, C.byref(obj), _ptr(g),
-                                    C.byref(cs)))
+        mode = (1 if screened else 0) | (2 if exact else 0)
+        _raise(_lib.lib().gsot_eval(self._h, _ptr(x), mode, C.byref(obj), _ptr(g), C.byref(cs)))
         st.in_active, st.skipped, st.unskipped, st.upper_bounds = (
             cs.in_active, cs.skipped, cs.unskipped, cs.upper_bounds)
         return obj.value, g, st
@@ -366,9 +366,11 @@ class Context:
 
     def solve(self, mode: int = 1, snapshot_interval: int = 10, grad_tol: float = 1e-6,
               max_outer_loops: int = 200, lbfgs_memory: int = 10,
-              upper_bound_offset: float = 0.0, history_cap: int = 0):
+              upper_bound_offset: float = 0.0, history_cap: int = 0, exact: bool = False):
+        """gsot_solve; exact=True runs the reference-order sums (bitwise trajectory)."""
         o = _lib.SolverOptionsC(int(snapshot_interval), float(grad_tol), int(max_outer_loops),
-                                int(lbfgs_memory), int(mode), float(upper_bound_offset))
+                                int(lbfgs_memory), int(mode), float(upper_bound_offset),
+                                1 if exact else 0)
         x = np.empty(self.m + self.n)
         r = _lib.SolveResultC()
         hist = np.zeros(max(1, history_cap) * 4, np.int64)
