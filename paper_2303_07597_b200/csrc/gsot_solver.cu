@@ -296,7 +296,8 @@ class Solver {
                       ") has nonzero exact gradient at call " + std::to_string(res_->grad_calls));
     }
     if (!w_->audit_g) w_->audit_g = dalloc<double>(w_->dim + 8, &c_->bytes);
-    EvalOut d = eval_device(c_, d_x, GSOT_EVAL_DENSE, w_->audit_g, nullptr, 0.0, false);
+    EvalOut d = eval_device(c_, d_x, GSOT_EVAL_DENSE | (exact_ ? GSOT_EVAL_EXACT : 0), w_->audit_g,
+                            nullptr, 0.0, false);
     std::vector<double> a(static_cast<size_t>(w_->dim)), b(static_cast<size_t>(w_->dim));
     GSOT_CUDA_CHECK(cudaMemcpyAsync(a.data(), d_g, sizeof(double) * w_->dim,
                                     cudaMemcpyDeviceToHost, c_->stream));

@@ -1,0 +1,84 @@
+"""GPU, exact-order mode: with the reference's own association for every
+cross-block sum and every L-BFGS dot (gsot_exact.cu), the device evaluation
+and the whole device solve are BITWISE the reference's (the oracle is
+bitwise the reference compiled against the sequential Eigen shim,
+tests/test_oracle.py): same iterates, objective, gradient calls, per-call
+screening counters and plan, in every solver mode."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2303_07597_b200 as G
+from oracle_bindings import Oracle, Problem
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def o():
+    return Oracle()
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+def gold_problem(g, name, pi):
+    gamma, mu = g[f"{name}/p{pi}/params"]
+    return Problem(g[f"{name}/cost"], g[f"{name}/sizes"], g[f"{name}/a"], g[f"{name}/b"],
+                   float(gamma), float(mu))
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_exact_eval_bitwise(gold, name, pi):
+    p = gold_problem(gold, name, pi)
+    ctx = G.Context.from_arrays(p.cost, p.sizes, p.a, p.b, p.gamma, p.mu)
+    for si in range(3):
+        x = gold[f"{name}/p{pi}/s{si}/x"]
+        obj, g, _ = ctx.eval(x, exact=True)
+        assert obj == gold[f"{name}/p{pi}/s{si}/objective"][0]
+        assert np.array_equal(g, gold[f"{name}/p{pi}/s{si}/grad"])
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_exact_solve_matches_reference_golden_bitwise(gold, name, pi):
+    p = gold_problem(gold, name, pi)
+    ctx = G.Context.from_arrays(p.cost, p.sizes, p.a, p.b, p.gamma, p.mu)
+    for mode in (0, 1, 2, 3):
+        r = ctx.solve(mode=mode, max_outer_loops=20, grad_tol=1e-7, history_cap=100000,
+                      exact=True)
+        sk = f"{name}/p{pi}/solve{mode}"
+        ints = gold[f"{sk}/ints"]
+        assert [r["iterations"], r["converged"], r["line_search_failed"], r["outer_loops"],
+                r["grad_calls"], r["blocks_in_active_set"], r["blocks_skipped"],
+                r["blocks_unskipped"], r["upper_bounds_evaluated"]] == ints.tolist()
+        assert np.array_equal(r["x"], gold[f"{sk}/x"])
+        assert r["objective"] == gold[f"{sk}/objective"][0]
+        assert np.array_equal(r["history"], gold[f"{sk}/history"])
+        if mode == 1:
+            assert np.array_equal(ctx.plan_columns(r["x"], 0, p.n), gold[f"{name}/p{pi}/solve_plan"])
+    ctx.close()
+
+
+def test_exact_solve_config1_bitwise(o):
+    # BASELINE config 1 (m = n = 1000, 100 iterations) against the oracle
+    src, tgt, sizes, a, b = G.config_features(1, 1)
+    cost = o.cost_matrix(src, tgt)
+    cost /= cost.max()
+    p = Problem(cost, sizes, a, b, 1.0, 0.1)
+    ctx = G.Context.from_config(1, 1, 1.0, 0.1)
+    r = ctx.solve(mode=1, max_outer_loops=10, grad_tol=1e-12, history_cap=100000, exact=True)
+    ro = o.solve(p, mode=1, max_outer_loops=10, grad_tol=1e-12, plan=True)
+    assert r["iterations"] == ro["iterations"] == 100
+    assert r["grad_calls"] == ro["grad_calls"]
+    assert np.array_equal(r["history"], ro["history"])
+    assert np.array_equal(r["x"], ro["x"])
+    assert r["objective"] == ro["objective"]
+    assert np.array_equal(ctx.plan_columns(r["x"], 0, p.n), ro["plan"])  # final plan bitwise
+    ctx.close()
