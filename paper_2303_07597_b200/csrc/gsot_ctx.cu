@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cstdio>
 #include <deque>
@@ -112,8 +113,9 @@ gsot_ctx::~gsot_ctx() {
   if (timer_b) cudaEventDestroy(timer_b);
   void* ptrs[] = {C,        d_off,   d_group_order, d_row_group, d_sqrt_g, d_a,     d_b,
                   x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
-                  words,    dense_words, tasks,     dense_tasks, snap_x,   zs,      ks,
-                  os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync};
+                  words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
+                  os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
+                  cnt_partials, cnt_slots};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -122,7 +124,7 @@ gsot_ctx::~gsot_ctx() {
 
 gsot::SolverWorkspace::~SolverWorkspace() {
   graphs.clear();
-  void* ptrs[] = {X[0], X[1], G[0], G[1], lo_x, lo_g, prev_x, prev_g, d, S, Y, audit_g};
+  void* ptrs[] = {X[0], X[1], G[0], G[1], lo_x, lo_g, prev_x, prev_g, d, S, Y, audit_g, cs, cpart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -183,10 +185,14 @@ void alloc_buffers(gsot_ctx* c) {
   c->psi = dalloc<double>(static_cast<size_t>(L) * n, t);
   c->psicol = dalloc<double>(n, t);
   c->partials = dalloc<double>(static_cast<size_t>(c->red_blocks) * 4 + 64, t);
+  c->cnt_slots = dalloc<unsigned long long>(64 * 8, t);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->cnt_slots, 0, sizeof(unsigned long long) * 64 * 8, c->stream));
+  c->cnt_partials = dalloc<unsigned long long>(
+      static_cast<size_t>(std::max<int64_t>(c->num_sms * 64, L * ((nw + 7) / 8))) * 8, t);
   c->words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dense_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
-  c->tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
   c->dense_tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
+  c->tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
   c->snap_x = dalloc<double>(dim + 8, t);
   c->zs = dalloc<double>(static_cast<size_t>(L) * n, t);
   c->ks = dalloc<double>(static_cast<size_t>(L) * n, t);
@@ -225,8 +231,38 @@ void alloc_buffers(gsot_ctx* c) {
                                   cudaMemcpyHostToDevice, c->stream));
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_words(c->dense_words, c->L, c->nw, c->n, c->stream); });
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->dense_tasks, c->d_group_order, c->L, c->nw, c->stream); });
-  // Persistent eval grid: every SM filled to the kernel's occupancy.
-  c->eval_grid = c->num_sms * std::max(1, gsot::eval_blocks_per_sm());
+  // Persistent eval grid: staging buffers sized to the tallest group (whole
+  // tile per warp when it fits), then as many blocks per SM as shared
+  // memory allows (the per-block task list shrinks as the grid grows).
+  {
+    const int gmax = *std::max_element(c->sizes.begin(), c->sizes.end());
+    const int64_t nchunks = static_cast<int64_t>(c->L) * c->nw;
+    std::vector<int> cands;
+    const char* ev = std::getenv("GSOT_EVAL_BUF");  // tuning override (rows; 0 = streaming)
+    if (ev) {
+      cands.push_back(std::atoi(ev));
+    } else {
+      cands.push_back(0);  // register streaming, highest occupancy
+    }
+    if (gmax <= 104) cands.push_back(std::max(16, gmax));  // whole tile per warp (TMA)
+    for (int b : {96, 64, 32}) cands.push_back(b);         // streamed in two halves
+    c->eval_buf = 32;
+    c->eval_grid = c->num_sms;
+    bool done = false;
+    for (int buf : cands) {
+      for (int bps = 4; bps >= 1 && !done; --bps) {
+        const int64_t grid = static_cast<int64_t>(c->num_sms) * bps;
+        const int cap = static_cast<int>((nchunks + grid - 1) / grid);
+        const size_t smem = gsot::eval_smem_bytes(buf, cap);
+        if (static_cast<size_t>(bps) * (smem + 2048) > 228 * 1024) continue;
+        if (gsot::eval_blocks_per_sm(smem) < bps) continue;
+        c->eval_buf = buf;
+        c->eval_grid = static_cast<int>(grid);
+        done = true;
+      }
+      if (done) break;
+    }
+  }
   c->sync();
 }
 
@@ -349,37 +385,39 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   const DevProblem P = c->problem();
   c->reset_scalars();
   const uint32_t* words = c->dense_words;
-  const int2* tasks = c->dense_tasks;
-  const int max_tasks = c->L * c->nw;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
     c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
       launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
     });
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
-      launch_bounds(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
-                    ub_offset, c->words, c->tasks, c->sc, c->stream);
+      launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
+                    ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->stream);
     });
     words = c->words;
-    tasks = c->tasks;
   }
   if (exact) {  // reference-order sums (gsot_exact.cu); the screen only counts
     c->launch(K_EVAL, 0.0, [&] {
-      launch_exact_eval(P, d_x, c->colpart, c->psi, d_grad, d_dir, c->sc, c->stream);
+      launch_exact_eval(P, d_x, c->colpart, c->psi, d_grad, d_dir, c->sc,
+                        mode == GSOT_EVAL_SCREENED ? c->cnt_slots : nullptr, c->stream);
     });
     return;
   }
   const double dense_bytes = 8.0 * c->m * c->n + 8.0 * c->m * c->nw + 16.0 * Ln;
   c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
-    launch_eval(P, d_x, tasks, mode == GSOT_EVAL_DENSE ? max_tasks : -1, words, c->rowpart,
-                c->colpart, c->psi, c->sc, c->eval_grid, c->stream);
+    if (mode == GSOT_EVAL_SCREENED)
+      launch_eval(P, d_x, c->tasks, -1, &c->sc->ntasks, words, c->rowpart, c->colpart, c->psi,
+                  c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
+    else
+      launch_eval(P, d_x, c->dense_tasks, c->L * c->nw, nullptr, words, c->rowpart, c->colpart,
+                  c->psi, c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
   });
   c->launch(K_FINALIZE, 0.0, [&] {
     launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, c->psicol, c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
     launch_objective(P, d_x, c->psicol, d_grad, d_dir, c->partials, c->red_blocks, c->sc,
-                     c->stream);
+                     mode == GSOT_EVAL_SCREENED ? c->cnt_slots : nullptr, c->stream);
   });
 }
 

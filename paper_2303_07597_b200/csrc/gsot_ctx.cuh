@@ -50,6 +50,8 @@ struct SolverWorkspace {
   double* S = nullptr;     // (mem + 1) pair slots of dim doubles
   double* Y = nullptr;
   double* audit_g = nullptr;
+  CompactState* cs = nullptr;   // compact L-BFGS state (fast mode)
+  double* cpart = nullptr;      // prepare-pass partials: (mem + 1) x 64 x 5
   std::map<std::string, std::unique_ptr<Sequence>> graphs;
   ~SolverWorkspace();
 };
@@ -74,8 +76,11 @@ struct gsot_ctx {
   double *x_eval = nullptr, *g_eval = nullptr;
   double *rowpart = nullptr, *colpart = nullptr, *psi = nullptr, *psicol = nullptr;
   double* partials = nullptr;
+  unsigned long long* cnt_partials = nullptr;  // spare counter partials
+  unsigned long long* cnt_slots = nullptr;     // screen counters, 64 x 8
   uint32_t *words = nullptr, *dense_words = nullptr;
-  int2 *tasks = nullptr, *dense_tasks = nullptr;
+  int2* dense_tasks = nullptr;  // canonical chunk order (largest groups first)
+  int2* tasks = nullptr;        // screened work list (non-empty chunks)
   // screening state
   double *snap_x = nullptr, *zs = nullptr, *ks = nullptr, *os = nullptr;
   double *dpos = nullptr, *dfull = nullptr, *dneg = nullptr, *dbeta = nullptr;
@@ -88,6 +93,7 @@ struct gsot_ctx {
   gsot::EvalScalars* sc = nullptr;    // &dsync->sc
   gsot::EvalScalars* h_sc = nullptr;  // &h_sync->sc
   int eval_grid = 148 * 4;
+  int eval_buf = 96;  // rows per warp staging buffer in k_eval
   int red_blocks = 148 * 2;
   // solver
   std::unique_ptr<gsot::SolverWorkspace> ws;
@@ -171,8 +177,12 @@ struct gsot_ctx {
   }
 
   double screened_eval_bytes() const {
+    // screen: z~ of every bound-checked block + the survivor words; then the
+    // surviving blocks' cost rows, the non-empty chunks' row partials and
+    // the per-block column / psi partials
     const double surv_blocks = static_cast<double>(h_sc->counters[0] + h_sc->counters[2]);
-    return 8.0 * static_cast<double>(h_sc->surv_rows) +
+    return 8.0 * static_cast<double>(h_sc->counters[3]) + 4.0 * static_cast<double>(L) * nw +
+           8.0 * static_cast<double>(h_sc->surv_rows) +
            8.0 * static_cast<double>(h_sc->task_rows) + 16.0 * surv_blocks;
   }
 

@@ -109,3 +109,75 @@ __device__ __forceinline__ bool last_block_reduce(const double (&mine)[NV], doub
 
 
 }  // namespace gsot
+
+namespace gsot {
+
+// ---- TMA bulk copies (cp.async.bulk) with mbarrier completion --------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned.
+// The proxy fence orders the warp's earlier generic reads of the buffer
+// before the async-proxy write.
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace gsot
+
+namespace gsot {
+
+// Fold the 64 counter slots into sc->counters etc. and zero them (one warp).
+__device__ __forceinline__ void fold_counter_slots(unsigned long long* slots, EvalScalars* sc) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  unsigned long long v[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    v[k] = slots[lane * 8 + k] + slots[(lane + 32) * 8 + k];
+    slots[lane * 8 + k] = 0ull;
+    slots[(lane + 32) * 8 + k] = 0ull;
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k)
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  if (lane == 0) {
+    sc->counters[0] = v[0];
+    sc->counters[1] = v[1];
+    sc->counters[2] = v[2];
+    sc->counters[3] = v[3];
+    sc->surv_rows = v[4];
+    sc->task_rows = v[5];
+  }
+}
+
+}  // namespace gsot

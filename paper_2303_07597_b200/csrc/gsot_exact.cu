@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(256) k_exact_grad_beta(DevProblem P, const dou
 // association, and the slope grad.d, all sequential on one thread.
 __global__ void k_exact_objective(DevProblem P, const double* __restrict__ x,
                                   const double* __restrict__ psi, const double* __restrict__ grad,
-                                  const double* __restrict__ dvec, EvalScalars* sc) {
+                                  const double* __restrict__ dvec, EvalScalars* sc,
+                                  unsigned long long* cnt_slots) {
+  if (cnt_slots) fold_counter_slots(cnt_slots, sc);  // screen counters (one warp)
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double psi_sum = 0.0;
   for (int64_t j = 0; j < P.n; ++j)
@@ -127,12 +129,13 @@ __global__ void k_exact_objective(DevProblem P, const double* __restrict__ x,
 }
 
 void launch_exact_eval(const DevProblem& P, const double* x, double* scale, double* psi,
-                       double* grad, const double* dvec, EvalScalars* sc, cudaStream_t s) {
+                       double* grad, const double* dvec, EvalScalars* sc,
+                       unsigned long long* cnt_slots, cudaStream_t s) {
   dim3 g1((unsigned)((P.n + 255) / 256), (unsigned)P.L);
   k_exact_blocks<<<g1, 256, 0, s>>>(P, x, scale, psi);
   k_exact_grad_alpha<<<(unsigned)((P.m + 127) / 128), 128, 0, s>>>(P, x, scale, grad);
   k_exact_grad_beta<<<(unsigned)((P.n + 255) / 256), 256, 0, s>>>(P, x, scale, grad);
-  k_exact_objective<<<1, 32, 0, s>>>(P, x, psi, grad, dvec, sc);
+  k_exact_objective<<<1, 32, 0, s>>>(P, x, psi, grad, dvec, sc, cnt_slots);
 }
 
 // ---------------------------------------------------------------- L-BFGS

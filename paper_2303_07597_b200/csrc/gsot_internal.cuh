@@ -98,21 +98,27 @@ void launch_delta(const DevProblem& P, const double* x, const double* xs, double
 void launch_active(const DevProblem& P, const double* ks, const double* os, const double* dfull,
                    const double* dneg, const double* dbeta, uint32_t* active_words,
                    EvalScalars* sc, cudaStream_t s);
-void launch_bounds(const DevProblem& P, const double* zs, const uint32_t* active_words,
-                   const double* dpos, const double* dbeta, double ub_offset, uint32_t* words,
-                   int2* tasks, EvalScalars* sc, cudaStream_t s);
-int eval_blocks_per_sm();
-// dense_ntasks >= 0: dense task list of that length; -1: screened, the
-// length is sc->ntasks (written by the bounds kernel).
-void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int dense_ntasks,
-                 const uint32_t* words, double* rowpart, double* colpart, double* psi,
-                 EvalScalars* sc, int grid, cudaStream_t s);
+// Upper-bound screen (screening.hpp:252-275): survivor words + counters.
+// Counters accumulate into 64 slots x 8 (cnt_slots); the objective kernel
+// folds them into EvalScalars and zeroes the slots.
+void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
+                   const double* dbeta, double ub_offset, uint32_t* words, int2* tasks,
+                   EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s);
+// Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
+int eval_buf_rows(int gmax);
+size_t eval_smem_bytes(int buf_rows, int cap);
+int eval_blocks_per_sm(size_t smem);
+// ntasks >= 0: `tasks` holds that many entries (dense list); -1: the
+// screened list, length *ntasks_dev (written by the screen kernel).
+void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int ntasks,
+                 const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
+                 double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s);
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const double* rowpart, const double* colpart, const double* psi,
                      double* grad, double* psicol, cudaStream_t s);
 void launch_objective(const DevProblem& P, const double* x, const double* psicol,
                       const double* grad, const double* dvec, double* partials, int nblocks,
-                      EvalScalars* sc, cudaStream_t s);
+                      EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s);
 void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,
                          double* out, cudaStream_t s);
 void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* words,
@@ -178,7 +184,8 @@ void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, 
 
 // Exact-order mode (gsot_exact.cu).
 void launch_exact_eval(const DevProblem& P, const double* x, double* scale, double* psi,
-                       double* grad, const double* dvec, EvalScalars* sc, cudaStream_t s);
+                       double* grad, const double* dvec, EvalScalars* sc,
+                       unsigned long long* cnt_slots, cudaStream_t s);
 void launch_exact_two_loop(const TwoLoopArgs& a, cudaStream_t s);
 void launch_exact_pair(const double* xt, const double* x, const double* g, const double* gt,
                        double* S, double* Y, int64_t stride, HistState* h, int64_t dim,
@@ -194,5 +201,39 @@ void launch_cost_matrix(const double* src, int64_t m, const double* tgt, int64_t
 void launch_max_reduce(const double* C, int64_t count, double* partials, int nblocks,
                        double* out, unsigned int* ticket, cudaStream_t s);
 void launch_scale_div(double* C, int64_t count, const double* divisor, cudaStream_t s);
+
+}  // namespace gsot
+
+namespace gsot {
+
+// Compact (Byrd-Nocedal-Schnabel) representation of the same L-BFGS
+// operator the two-loop recursion applies (fast mode): R = upper triangle of
+// S^T Y, D = diag(R), YY = Y^T Y, kept by logical pair position on the
+// device, plus the current u = S^T g, v = Y^T g and the direction
+// coefficients d = gam * g + S p - Y w (w already scaled by gam).
+struct CompactState {
+  double R[kMaxMemory * kMaxMemory];   // R[i * kMaxMemory + j] = s_i . y_j, i <= j
+  double YY[kMaxMemory * kMaxMemory];  // y_i . y_j
+  double u[kMaxMemory + 1], v[kMaxMemory + 1];
+  double p[kMaxMemory], w[kMaxMemory];
+  double gam;
+  int k;
+};
+
+// One multi-dot pass + last-block solve. pair != 0: first form the
+// curvature pair of (xt, x, gt, g) into the scratch slot (lbfgs.hpp:243-255),
+// test it, update the ring and R / YY; then u, v for the gradient gn (= gt
+// when pair != 0) and the direction coefficients.
+void launch_compact_prepare(int pair, const double* xt, const double* x, const double* gt,
+                            const double* g, const double* gn, double* S, double* Y,
+                            int64_t stride, HistState* h, CompactState* cs, int mem, int64_t dim,
+                            double* partials, EvalScalars* sc, cudaStream_t s);
+// d = gam g + S p - Y w; out[0] = g.d, out[1] = d.d; xt_out = x + t d when
+// xt_out != null (the first trial point of the line search).
+void launch_compact_direction(const double* g, const double* S, const double* Y, int64_t stride,
+                              const HistState* h, const CompactState* cs, double* d,
+                              const double* x, const double* t, double* xt_out, int64_t dim,
+                              double* partials, EvalScalars* sc, double* out, int nblocks,
+                              cudaStream_t s);
 
 }  // namespace gsot

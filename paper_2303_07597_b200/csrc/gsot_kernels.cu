@@ -246,95 +246,83 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
   k_active<<<grid, 256, 0, s>>>(P, ks, os, dfull, dneg, dbeta, aw, sc);
 }
 
-// ---------------------------------------------------------------- bounds
+// ---------------------------------------------------------------- screen
 // FastGradDispatcher::column's per-block decision (screening.hpp:252-275):
 // active-set members are computed without a bound; every other block gets
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
-// skipped iff z_bar <= tau. Writes the survivor word of each (l, c) chunk
-// and appends non-empty chunks to the work list (order irrelevant: every
-// task writes fixed slots). Persistent blocks walk units of 8 chunks of one
-// group (one chunk per warp), buffer their tasks in shared memory and flush
-// them, and their counters, with one global atomic each at the end.
-__global__ void __launch_bounds__(256) k_bounds(DevProblem P, const double* __restrict__ zs,
+// skipped iff z_bar <= tau. One warp per (group, 32-column) chunk writes the
+// survivor word; GradStats::PerCall counters go through per-block partials
+// and a last-block sum (integer, order-independent; no contended atomics).
+__global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
                                                 const double* __restrict__ dpos,
                                                 const double* __restrict__ dbeta,
                                                 double ub_offset, uint32_t* __restrict__ words,
-                                                int2* __restrict__ tasks, EvalScalars* sc) {
-  extern __shared__ int2 tbuf[];
-  __shared__ unsigned long long cnt[6];
-  __shared__ int ntb, base;
+                                                int2* __restrict__ tasks, EvalScalars* sc,
+                                                unsigned long long* __restrict__ cnt_slots) {
+  __shared__ unsigned long long cnt[8][7];
+  __shared__ int base;
+  const int l = blockIdx.y;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < 6) cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) ntb = 0;
-  __syncthreads();
-  const int nunit8 = (P.nw + 7) / 8;
-  const int64_t nunits = (int64_t)P.L * nunit8;
-  unsigned long long my[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const int l = (int)(u / nunit8);
-    const int c = (int)(u % nunit8) * 8 + warp;
-    const int64_t j = (int64_t)c * 32 + lane;
-    const bool valid = c < P.nw && j < P.n;
-    bool in_active = false;
-    if (valid && aw != nullptr) in_active = (aw[(int64_t)l * P.nw + c] >> lane) & 1u;
-    const bool evaluated = valid && !in_active;
-    bool surv = in_active;
-    if (evaluated) {
-      const double db = dbeta[j];
-      const double db_pos = db > 0.0 ? db : 0.0;
-      const double zbar = dadd(
-          dadd(dadd(zs[(int64_t)l * P.n + j], dpos[l]), dmul(P.sqrt_g[l], db_pos)), ub_offset);
-      surv = !(zbar <= P.tau);
-    }
-    const unsigned wa = __ballot_sync(0xffffffffu, in_active);
-    const unsigned we = __ballot_sync(0xffffffffu, evaluated);
-    const unsigned ws = __ballot_sync(0xffffffffu, surv);
-    if (lane == 0 && c < P.nw) {
-      words[(int64_t)l * P.nw + c] = ws;
-      const unsigned long long g = (unsigned long long)(P.off[l + 1] - P.off[l]);
-      my[0] += __popc(wa);
-      my[1] += __popc(we & ~ws);
-      my[2] += __popc(we & ws);
-      my[3] += __popc(we);
-      my[4] += (unsigned long long)__popc(ws) * g;  // survivors' rows
-      if (ws) {
-        my[5] += g;  // task rows
-        tbuf[atomicAdd(&ntb, 1)] = make_int2(l, c);
-      }
-    }
+  const int64_t c = j >> 5;
+  const bool valid = j < P.n;
+  bool in_active = false;
+  if (valid && aw != nullptr) in_active = (aw[(int64_t)l * P.nw + c] >> lane) & 1u;
+  const bool evaluated = valid && !in_active;
+  bool surv = in_active;
+  if (evaluated) {
+    const double db = dbeta[j];
+    const double db_pos = db > 0.0 ? db : 0.0;
+    const double zbar =
+        dadd(dadd(dadd(zs[(int64_t)l * P.n + j], dpos[l]), dmul(P.sqrt_g[l], db_pos)), ub_offset);
+    surv = !(zbar <= P.tau);
   }
-  if (lane == 0)
-    for (int q = 0; q < 6; ++q)
-      if (my[q]) atomicAdd(&cnt[q], my[q]);
+  const unsigned wa = __ballot_sync(0xffffffffu, in_active);
+  const unsigned we = __ballot_sync(0xffffffffu, evaluated);
+  const unsigned ws = __ballot_sync(0xffffffffu, surv);
+  if (lane == 0) {
+    const unsigned long long g = (unsigned long long)(P.off[l + 1] - P.off[l]);
+    if (c < P.nw) words[(int64_t)l * P.nw + c] = ws;
+    cnt[warp][0] = __popc(wa);
+    cnt[warp][1] = __popc(we & ~ws);
+    cnt[warp][2] = __popc(we & ws);
+    cnt[warp][3] = __popc(we);
+    cnt[warp][4] = (unsigned long long)__popc(ws) * g;  // survivors' rows
+    cnt[warp][5] = ws ? g : 0;                          // task rows
+    cnt[warp][6] = ws ? 1 : 0;                          // tasks
+  }
   __syncthreads();
+  // work list: one atomic per block reserves its non-empty chunks' slots
   if (threadIdx.x == 0) {
-    base = ntb ? atomicAdd(&sc->ntasks, ntb) : 0;
-    for (int q = 0; q < 4; ++q)
-      if (cnt[q]) atomicAdd(&sc->counters[q], cnt[q]);
-    if (cnt[4]) atomicAdd(&sc->surv_rows, cnt[4]);
-    if (cnt[5]) atomicAdd(&sc->task_rows, cnt[5]);
+    int nt = 0;
+    for (int w = 0; w < 8; ++w) nt += (int)cnt[w][6];
+    base = nt ? atomicAdd(&sc->ntasks, nt) : 0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < ntb; i += blockDim.x) tasks[base + i] = tbuf[i];
+  if (lane == 0 && ws != 0u && c < P.nw) {
+    int pos = base;
+    for (int w = 0; w < warp; ++w) pos += (int)cnt[w][6];
+    tasks[pos] = make_int2(l, (int)c);
+  }
+  // block totals into one of 64 counter slots (spread, no fences); the
+  // objective kernel's last block folds the slots into sc->counters
+  if (threadIdx.x < 6) {
+    unsigned long long t = 0;
+    for (int w = 0; w < 8; ++w) t += cnt[w][threadIdx.x];
+    const unsigned slot = (blockIdx.y * gridDim.x + blockIdx.x) & 63u;
+    if (t) atomicAdd(cnt_slots + slot * 8 + threadIdx.x, t);
+  }
 }
 
-void launch_bounds(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
+void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, int2* tasks,
-                   EvalScalars* sc, cudaStream_t s) {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-  }
-  const int64_t nunits = (int64_t)P.L * ((P.nw + 7) / 8);
-  const int grid = (int)std::min<int64_t>(nunits, (int64_t)nsm * 4);
-  const int64_t per = (nunits + grid - 1) / grid;
-  const size_t smem = sizeof(int2) * (size_t)(per * 8);
-  k_bounds<<<grid, 256, smem, s>>>(P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc);
+                   EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s) {
+  dim3 grid((unsigned)((P.nw * 32 + 255) / 256), (unsigned)P.L);
+  k_screen<<<grid, 256, 0, s>>>(P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc, cnt_slots);
 }
+
+
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
 __global__ void k_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n) {
@@ -362,106 +350,265 @@ void launch_dense_tasks(int2* tasks, const int32_t* order, int32_t L, int32_t nw
 }
 
 // ---------------------------------------------------------------- fused eval
-// One warp per (group l, 32-column chunk c) task; lane = column j = 32c+lane,
-// active iff its survivor bit is set. Pass 1 (sequential over the block's
-// rows): z^2 = sum [f]+^2 and sum [f]+. Then scale = (1 - tau/z)/gamma when
-// z > tau (grad_block, regularizer.hpp:64-74), psi = (z - tau)^2 / (2 gamma)
-// (the closed form of psi_block, regularizer.hpp:78-91),
-// column partial scale * sum [f]+. Pass 2 (16 rows at a time): plan entries
-// T = scale * [f]+, transpose-reduced across the warp into per-row partials
-// of the chunk, stored at rowpart[c * m + row]. The plan is never stored.
-__global__ void __launch_bounds__(256) k_eval(DevProblem P, const double* __restrict__ x,
-                                              const int2* __restrict__ tasks, int dense_ntasks,
-                                              const uint32_t* __restrict__ words,
-                                              double* __restrict__ rowpart,
-                                              double* __restrict__ colpart,
-                                              double* __restrict__ psi, EvalScalars* sc) {
-  const int lane = threadIdx.x & 31;
-  const int ntasks = dense_ntasks >= 0 ? dense_ntasks : *(volatile int*)&sc->ntasks;
+// Persistent blocks; block b owns the chunks t = b + G*q of the canonical
+// chunk order (largest groups first, interleaved so every block samples
+// every group). Phase 0: the block collects its non-empty chunks (survivor
+// word != 0) into a shared-memory task list. Phase 1: its warps drain the
+// list through a shared counter. One warp per (group l, 32-column chunk c)
+// task: the g_l x 32 tile is contiguous, so lane 0 stages it into the warp's
+// shared buffer with ONE TMA bulk copy (cp.async.bulk + mbarrier); groups
+// taller than the buffer stream through its two halves (copy of segment s+1
+// in flight while segment s is computed). Lane = column j = 32c + lane,
+// active iff its survivor bit is set.
+//   pass 1, sequential over the block's rows: z^2 = sum [f]+^2, sum [f]+;
+//   scale = (1 - tau/z)/gamma when z > tau (grad_block, regularizer.hpp:
+//   64-74); psi = (z - tau)^2 / (2 gamma) (closed form of psi_block,
+//   regularizer.hpp:78-91); column partial scale * sum [f]+;
+//   pass 2, 16 rows at a time: T = scale * [f]+ transpose-reduced across the
+//   warp into per-row partials of the chunk, stored at rowpart[c*m + row].
+// The plan is never stored.
+struct EvalArgs {
+  DevProblem P;
+  const double* x;
+  const int2* order;  // canonical chunk order
+  int nchunks;
+  const uint32_t* words;  // survivor words (dense: all valid columns)
+  double* rowpart;
+  double* colpart;
+  double* psi;
+  int buf_rows;  // rows per warp buffer (whole tile when g <= buf_rows)
+  int* next_chunk;  // global claim cursor (zeroed per evaluation)
+  int ntasks;       // >= 0: list length; -1: read *ntasks_dev (screened)
+  const int* ntasks_dev;
+  int batch;        // tasks claimed per atomic
+};
+
+constexpr int kEvalWarps = 8;
+
+__global__ void __launch_bounds__(256) k_eval(const EvalArgs A) {
+  extern __shared__ __align__(128) unsigned char eval_smem[];
+  const DevProblem& P = A.P;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int B = A.buf_rows, H = A.buf_rows / 2;  // whole buffer / half (B = 0: streaming)
+  double* buf = reinterpret_cast<double*>(eval_smem) + (size_t)warp * B * 32;
+  __shared__ uint64_t bars[kEvalWarps][2];
+  if (B > 0 && lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+  }
+  mbar_fence_init();
+  __syncwarp();
+  uint32_t ph[2] = {0u, 0u};
+  // Dynamic scheduling over the compact work list: a warp claims `batch`
+  // consecutive tasks per atomic (1 for the sparse screened list, a few for
+  // the dense list).
+  const int ntasks = A.ntasks >= 0 ? A.ntasks : *(volatile const int*)A.ntasks_dev;
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(&sc->next_task, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= ntasks) break;
-    const int2 tk = tasks[t];
+    int base = 0;
+    if (lane == 0) base = atomicAdd(A.next_chunk, A.batch);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= ntasks) break;
+   const int bend = min(ntasks, base + A.batch);
+   for (int t = base; t < bend; ++t) {
+    const int2 tk = A.order[t];
+    const uint32_t word = A.words[(int64_t)tk.x * P.nw + tk.y];
     const int l = tk.x, c = tk.y;
-    const uint32_t word = words[(int64_t)l * P.nw + c];
     const int64_t j = (int64_t)c * 32 + lane;
     const bool act = (word >> lane) & 1u;
     const int o0 = P.off[l];
     const int g = P.off[l + 1] - o0;
-    const double* __restrict__ al = x + o0;
-    const double bj = act ? x[P.m + j] : 0.0;
-    const double* __restrict__ cp = block_ptr(P, o0, g, j);
+    const double* __restrict__ al = A.x + o0;
+    const double bj = act ? A.x[P.m + j] : 0.0;
+    const double* tile = P.C + 32 * ((int64_t)P.nw * o0 + (int64_t)c * g);
+    if (B == 0) {  // register-streaming path: no staging, loads batched per lane
+      const double* __restrict__ cp = tile + lane;
+      double z2 = 0.0, sv = 0.0;
+      if (act) {
+        int r = 0;
+        for (; r + 8 <= g; r += 8) {
+          double cc[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cc[k] = __ldg(cp + 32 * (r + k));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double f = residual(__ldg(al + r + k), bj, cc[k]);
+            const double v = f > 0.0 ? f : 0.0;
+            z2 = dadd(z2, dmul(v, v));
+            sv = dadd(sv, v);
+          }
+        }
+        for (; r < g; ++r) {
+          const double f = residual(__ldg(al + r), bj, __ldg(cp + 32 * r));
+          const double v = f > 0.0 ? f : 0.0;
+          z2 = dadd(z2, dmul(v, v));
+          sv = dadd(sv, v);
+        }
+      }
+      const double z = sqrt(z2);
+      const bool nz = act && z > P.tau;
+      const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
+      if (act) {
+        const int64_t idx = (int64_t)l * P.n + j;
+        A.colpart[idx] = dmul(scale, sv);
+        double ps = 0.0;
+        if (nz) {
+          const double e = dsub(z, P.tau);
+          ps = ddiv(dmul(e, e), dmul(2.0, P.gamma));
+        }
+        A.psi[idx] = ps;
+      }
+      double* __restrict__ rp = A.rowpart + (int64_t)c * P.m + o0;
+      if (__ballot_sync(0xffffffffu, nz) == 0u) {
+        for (int r = lane; r < g; r += 32) rp[r] = 0.0;
+        continue;
+      }
+      for (int r0 = 0; r0 < g; r0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int r = r0 + k;
+          const bool in = nz && r < g;
+          const double cc = in ? __ldg(cp + 32 * r) : 0.0;
+          const double a = r < g ? __ldg(al + r) : 0.0;
+          const double f = residual(a, bj, cc);
+          v[k] = (in && f > 0.0) ? dmul(scale, f) : 0.0;
+        }
+        transpose_reduce16(v, lane);
+        if (lane < 16 && r0 + lane < g) rp[r0 + lane] = v[0];
+      }
+      continue;
+    }
+    const bool whole = g <= B;
+    // segment s: rows [s*H, min(g, (s+1)*H)) in half (s & 1) of the buffer
+    const int nseg = whole ? 1 : (g + H - 1) / H;
+    auto issue = [&](int sgm) {  // lane 0 only
+      if (whole) {
+        mbar_expect_tx(&bars[warp][0], (uint32_t)g * 256u);
+        tma_load_1d(buf, tile, (uint32_t)g * 256u, &bars[warp][0]);
+      } else {
+        const int r0 = sgm * H, rows = min(H, g - r0), hb = sgm & 1;
+        mbar_expect_tx(&bars[warp][hb], (uint32_t)rows * 256u);
+        tma_load_1d(buf + (size_t)hb * H * 32, tile + (int64_t)r0 * 32, (uint32_t)rows * 256u,
+                    &bars[warp][hb]);
+      }
+    };
+    auto wait_seg = [&](int sgm) {
+      const int hb = whole ? 0 : (sgm & 1);
+      mbar_wait(&bars[warp][hb], ph[hb]);
+      ph[hb] ^= 1u;
+    };
+    auto row_ptr = [&](int r) -> const double* {  // row r of the current residency
+      return whole ? buf + (size_t)r * 32 : buf + (size_t)(((r / H) & 1) * H + (r % H)) * 32;
+    };
 
     // pass 1
+    if (lane == 0) {
+      issue(0);
+      if (!whole && nseg > 1) issue(1);
+    }
     double z2 = 0.0, sv = 0.0;
-    if (act) {
-#define GSOT_P1(ALPHA, CVAL)                        \
-  {                                                 \
-    const double f = residual((ALPHA), bj, (CVAL)); \
-    const double v = f > 0.0 ? f : 0.0;             \
-    z2 = dadd(z2, dmul(v, v));                      \
-    sv = dadd(sv, v);                               \
-  }
-      int r = 0;
-      for (; r + 8 <= g; r += 8) {
-        double cc[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) cc[k] = __ldg(cp + 32 * (r + k));
-#pragma unroll
-        for (int k = 0; k < 8; ++k) GSOT_P1(__ldg(al + r + k), cc[k]);
+    for (int sgm = 0; sgm < nseg; ++sgm) {
+      wait_seg(sgm);
+      const int r0 = whole ? 0 : sgm * H, r1 = whole ? g : min(g, r0 + H);
+      if (act) {
+        for (int r = r0; r < r1; ++r) {
+          const double f = residual(__ldg(al + r), bj, row_ptr(r)[lane]);
+          const double v = f > 0.0 ? f : 0.0;
+          z2 = dadd(z2, dmul(v, v));
+          sv = dadd(sv, v);
+        }
       }
-      for (; r < g; ++r) GSOT_P1(__ldg(al + r), __ldg(cp + 32 * r));
-#undef GSOT_P1
+      __syncwarp();
+      if (!whole && lane == 0 && sgm + 2 < nseg) issue(sgm + 2);
     }
     const double z = sqrt(z2);
     const bool nz = act && z > P.tau;
     const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
     if (act) {
       const int64_t idx = (int64_t)l * P.n + j;
-      colpart[idx] = dmul(scale, sv);
+      A.colpart[idx] = dmul(scale, sv);
       double ps = 0.0;
       if (nz) {
         const double e = dsub(z, P.tau);
         ps = ddiv(dmul(e, e), dmul(2.0, P.gamma));
       }
-      psi[idx] = ps;
+      A.psi[idx] = ps;
     }
-    double* __restrict__ rp = rowpart + (int64_t)c * P.m + o0;
+    double* __restrict__ rp = A.rowpart + (int64_t)c * P.m + o0;
     const unsigned nzm = __ballot_sync(0xffffffffu, nz);
     if (nzm == 0u) {
       for (int r = lane; r < g; r += 32) rp[r] = 0.0;
+      __syncwarp();
       continue;
     }
-    // pass 2
-    for (int r0 = 0; r0 < g; r0 += 16) {
-      double v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int r = r0 + k;
-        const bool in = nz && r < g;
-        const double cc = in ? __ldg(cp + 32 * r) : 0.0;
-        const double a = r < g ? __ldg(al + r) : 0.0;
-        const double f = residual(a, bj, cc);
-        v[k] = (in && f > 0.0) ? dmul(scale, f) : 0.0;
-      }
-      transpose_reduce16(v, lane);
-      if (lane < 16 && r0 + lane < g) rp[r0 + lane] = v[0];
+    // pass 2 (the whole tile is still resident; a streamed one is re-read)
+    if (!whole && lane == 0) {
+      issue(0);
+      if (nseg > 1) issue(1);
     }
+    for (int sgm = 0; sgm < nseg; ++sgm) {
+      if (!whole) wait_seg(sgm);
+      const int r0s = whole ? 0 : sgm * H, r1s = whole ? g : min(g, r0s + H);
+      for (int r0 = r0s; r0 < r1s; r0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int r = r0 + k;
+          const bool in = nz && r < r1s;
+          const double cc = in ? row_ptr(r)[lane] : 0.0;
+          const double a = r < r1s ? __ldg(al + r) : 0.0;
+          const double f = residual(a, bj, cc);
+          v[k] = (in && f > 0.0) ? dmul(scale, f) : 0.0;
+        }
+        transpose_reduce16(v, lane);
+        if (lane < 16 && r0 + lane < r1s) rp[r0 + lane] = v[0];
+      }
+      __syncwarp();
+      if (!whole && lane == 0 && sgm + 2 < nseg) issue(sgm + 2);
+    }
+   }
   }
 }
 
-int eval_blocks_per_sm() {
+namespace {
+int g_eval_per_sm = 0;
+int g_eval_smem_attr = 0;
+}
+
+int eval_buf_rows(int gmax) {
+  // whole tile per warp when it fits 8 warps x rows x 256 B in ~200 KB,
+  // else 96-row buffers streamed as two 48-row halves
+  return gmax <= 96 ? std::max(16, gmax) : 96;
+}
+
+size_t eval_smem_bytes(int buf_rows, int cap) {
+  (void)cap;
+  return sizeof(double) * (size_t)kEvalWarps * buf_rows * 32;
+}
+
+int eval_blocks_per_sm(size_t smem) {
+  if ((int)smem > g_eval_smem_attr) {
+    cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    g_eval_smem_attr = (int)smem;
+  }
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval, 256, 0) != cudaSuccess) return 2;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval, 256, smem) != cudaSuccess || n < 1)
+    n = 1;
+  g_eval_per_sm = n;
   return n;
 }
 
-void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int dense_ntasks,
-                 const uint32_t* words, double* rowpart, double* colpart, double* psi,
-                 EvalScalars* sc, int grid, cudaStream_t s) {
-  k_eval<<<grid, 256, 0, s>>>(P, x, tasks, dense_ntasks, words, rowpart, colpart, psi, sc);
+void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int ntasks,
+                 const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
+                 double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s) {
+  EvalArgs A{P, x, tasks, P.L * P.nw, words, rowpart, colpart, psi, buf_rows, next_chunk,
+             ntasks, ntasks_dev, ntasks >= 0 ? 4 : 1};
+  const size_t smem = eval_smem_bytes(buf_rows, 0);
+  if ((int)smem > g_eval_smem_attr) {
+    cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    g_eval_smem_attr = (int)smem;
+  }
+  k_eval<<<grid, 256, smem, s>>>(A);
 }
 
 // ---------------------------------------------------------------- finalize
@@ -487,8 +634,21 @@ __global__ void __launch_bounds__(256) k_finalize(DevProblem P, const uint32_t* 
     if (i < P.m) {
       const int l = P.row_group[i];
       const uint32_t* __restrict__ wl = words + (int64_t)l * P.nw;
-      for (int c = ty; c < P.nw; c += 8)
-        if (wl[c]) acc = dadd(acc, rowpart[(int64_t)c * P.m + i]);
+      // slice ty: chunks c = ty + 8q, ascending; loads batched 8 at a time
+      for (int c0 = ty; c0 < P.nw; c0 += 64) {
+        uint32_t w[8];
+        double r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + 8 * u;
+          w[u] = c < P.nw ? wl[c] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = w[u] ? rowpart[(int64_t)(c0 + 8 * u) * P.m + i] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (w[u]) acc = dadd(acc, r[u]);
+      }
     }
     sh[0][ty][tx] = acc;
     __syncthreads();
@@ -503,11 +663,26 @@ __global__ void __launch_bounds__(256) k_finalize(DevProblem P, const uint32_t* 
   double acc = 0.0, ps = 0.0;
   if (j < P.n) {
     const int64_t c = j >> 5;
-    for (int l = ty; l < P.L; l += 8) {
-      if ((words[(int64_t)l * P.nw + c] >> tx) & 1u) {
-        acc = dadd(acc, colpart[(int64_t)l * P.n + j]);
-        ps = dadd(ps, psi[(int64_t)l * P.n + j]);
+    for (int l0 = ty; l0 < P.L; l0 += 64) {
+      bool on[8];
+      double cp[8], pp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int l = l0 + 8 * u;
+        on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t idx = (int64_t)(l0 + 8 * u) * P.n + j;
+        cp[u] = on[u] ? colpart[idx] : 0.0;
+        pp[u] = on[u] ? psi[idx] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (on[u]) {
+          acc = dadd(acc, cp[u]);
+          ps = dadd(ps, pp[u]);
+        }
     }
   }
   sh[0][ty][tx] = acc;
@@ -540,7 +715,8 @@ __global__ void __launch_bounds__(256) k_objective(DevProblem P, const double* _
                                                    const double* __restrict__ grad,
                                                    const double* __restrict__ dvec,
                                                    double* __restrict__ partials,
-                                                   EvalScalars* sc) {
+                                                   EvalScalars* sc,
+                                                   unsigned long long* cnt_slots) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t dim = P.m + P.n;
@@ -553,7 +729,9 @@ __global__ void __launch_bounds__(256) k_objective(DevProblem P, const double* _
   if (dvec)
     for (int64_t i = t0; i < dim; i += stride) p[3] = dadd(p[3], dmul(grad[i], dvec[i]));
   double out[4];
-  if (last_block_reduce<256, 4>(p, partials, &sc->ticket, out)) {
+  const bool lastb = last_block_reduce<256, 4>(p, partials, &sc->ticket, out);
+  if (cnt_slots != nullptr && __syncthreads_or(lastb)) fold_counter_slots(cnt_slots, sc);
+  if (lastb) {
     sc->dot_aa = out[0];
     sc->dot_bb = out[1];
     sc->psi_sum = out[2];
@@ -564,8 +742,8 @@ __global__ void __launch_bounds__(256) k_objective(DevProblem P, const double* _
 
 void launch_objective(const DevProblem& P, const double* x, const double* psicol,
                       const double* grad, const double* dvec, double* partials, int nblocks,
-                      EvalScalars* sc, cudaStream_t s) {
-  k_objective<<<nblocks, 256, 0, s>>>(P, x, psicol, grad, dvec, partials, sc);
+                      EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s) {
+  k_objective<<<nblocks, 256, 0, s>>>(P, x, psicol, grad, dvec, partials, sc, cnt_slots);
 }
 
 // ---------------------------------------------------------------- plan

@@ -361,3 +361,259 @@ void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, 
 }
 
 }  // namespace gsot
+
+// ============================================================ compact L-BFGS
+namespace gsot {
+
+namespace {
+constexpr int kSlices = 16;  // dim slices per history row in the prepare pass
+}
+
+// Multi-dot pass. Row i < k: history pair i (logical) against the new pair
+// and the new gradient: s_i.y, y_i.y, s_i.gn, y_i.gn. Row k (pair != 0):
+// the new pair itself, written to the scratch slot: s.y, s.s, y.y, s.gn,
+// y.gn. Rows beyond are idle (the grid is sized for mem + 1 rows so that a
+// captured graph never changes). The last block reduces the partials in
+// slice order, applies the acceptance test and ring update, maintains R and
+// YY by logical position, and solves for the direction coefficients.
+__global__ void __launch_bounds__(256) k_compact_prepare(
+    int pair, const double* __restrict__ xt, const double* __restrict__ x,
+    const double* __restrict__ gt, const double* __restrict__ g, const double* __restrict__ gn,
+    double* __restrict__ S, double* __restrict__ Y, int64_t stride, HistState* h,
+    CompactState* cs, int64_t dim, double* __restrict__ partials, EvalScalars* sc) {
+  __shared__ double sh[8][5];
+  __shared__ bool last;
+  const int k = h->k;  // every block reads before the last block updates
+  const int scratch = h->scratch;
+  const int row = blockIdx.y;
+  const int nrows = gridDim.y;
+  const int64_t per = (dim + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(dim, lo + per);
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (row < k) {
+    const double* __restrict__ si = S + h->order[row] * stride;
+    const double* __restrict__ yi = Y + h->order[row] * stride;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+      const double s = si[e], y = yi[e], gg = gn[e];
+      if (pair) {
+        const double yn = dsub(g[e], gt[e]);
+        acc[0] = dadd(acc[0], dmul(s, yn));
+        acc[1] = dadd(acc[1], dmul(y, yn));
+      }
+      acc[2] = dadd(acc[2], dmul(s, gg));
+      acc[3] = dadd(acc[3], dmul(y, gg));
+    }
+  } else if (row == k && pair) {
+    double* __restrict__ sv = S + scratch * stride;
+    double* __restrict__ yv = Y + scratch * stride;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+      const double s = dsub(xt[e], x[e]);
+      const double y = dsub(g[e], gt[e]);
+      sv[e] = s;
+      yv[e] = y;
+      const double gg = gn[e];
+      acc[0] = dadd(acc[0], dmul(s, y));
+      acc[1] = dadd(acc[1], dmul(s, s));
+      acc[2] = dadd(acc[2], dmul(y, y));
+      acc[3] = dadd(acc[3], dmul(s, gg));
+      acc[4] = dadd(acc[4], dmul(y, gg));
+    }
+  }
+  // fixed-tree block reduction of the 5 accumulators
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t base = ((int64_t)row * gridDim.x + blockIdx.x) * 5;
+    for (int q = 0; q < 5; ++q) {
+      double v = sh[0][q];
+      for (int w = 1; w < 8; ++w) v = dadd(v, sh[w][q]);
+      partials[base + q] = v;
+    }
+    __threadfence();
+    last = atomicAdd(&sc->ticket, 1u) == gridDim.x * gridDim.y - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // reduce each (row, q) over the slices in slice order (one thread each)
+  __shared__ double red[(kMaxMemory + 1) * 5];
+  for (int t = threadIdx.x; t < nrows * 5; t += blockDim.x) {
+    const int r = t / 5, q = t % 5;
+    double pv[kSlices];  // all loads first, then the slice-ordered sum
+#pragma unroll
+    for (int b = 0; b < kSlices; ++b) pv[b] = __ldcg(partials + ((int64_t)r * kSlices + b) * 5 + q);
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < kSlices; ++b) v = dadd(v, pv[b]);
+    red[t] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  sc->ticket = 0u;
+  int kk = k;
+  double u[kMaxMemory + 1], vv[kMaxMemory + 1];
+  for (int i = 0; i < k; ++i) {
+    u[i] = red[i * 5 + 2];
+    vv[i] = red[i * 5 + 3];
+  }
+  if (pair) {
+    const double sy = red[k * 5 + 0], ss = red[k * 5 + 1], yy = red[k * 5 + 2];
+    sc->extra[0] = sy;
+    sc->extra[1] = ss;
+    sc->extra[2] = yy;
+    h->last_sy = sy;
+    h->last_ss = ss;
+    h->last_yy = yy;
+    const bool accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);  // lbfgs.hpp:246
+    h->accepted = accept ? 1 : 0;
+    if (accept) {
+      double sy_new[kMaxMemory], yy_new[kMaxMemory];
+      for (int i = 0; i < k; ++i) {
+        sy_new[i] = red[i * 5 + 0];  // s_i . y_new
+        yy_new[i] = red[i * 5 + 1];  // y_i . y_new
+      }
+      int first = 0;
+      if (k == h->mem) {  // evict the oldest (lbfgs.hpp:247-251)
+        first = 1;
+        const int ev = h->order[0];
+        for (int i = 1; i < k; ++i) {
+          h->order[i - 1] = h->order[i];
+          h->rho[i - 1] = h->rho[i];
+          h->sy[i - 1] = h->sy[i];
+          h->yy[i - 1] = h->yy[i];
+          for (int j = 1; j < k; ++j) {
+            cs->R[(i - 1) * kMaxMemory + (j - 1)] = cs->R[i * kMaxMemory + j];
+            cs->YY[(i - 1) * kMaxMemory + (j - 1)] = cs->YY[i * kMaxMemory + j];
+          }
+        }
+        kk = k - 1;
+        h->order[kk] = scratch;
+        h->scratch = ev;
+      } else {
+        h->order[k] = scratch;
+        int next = 0;
+        for (;; ++next) {
+          bool used = false;
+          for (int i = 0; i <= k; ++i) used |= h->order[i] == next;
+          if (!used) break;
+        }
+        h->scratch = next;
+      }
+      for (int i = 0; i < kk; ++i) {  // shift u, v and the new column
+        u[i] = u[i + first];
+        vv[i] = vv[i + first];
+        cs->R[i * kMaxMemory + kk] = sy_new[i + first];
+        cs->YY[i * kMaxMemory + kk] = yy_new[i + first];
+        cs->YY[kk * kMaxMemory + i] = yy_new[i + first];
+      }
+      cs->R[kk * kMaxMemory + kk] = sy;
+      cs->YY[kk * kMaxMemory + kk] = yy;
+      u[kk] = red[k * 5 + 3];
+      vv[kk] = red[k * 5 + 4];
+      h->rho[kk] = 1.0 / sy;
+      h->sy[kk] = sy;
+      h->yy[kk] = yy;
+      kk += 1;
+      h->k = kk;
+    }
+  }
+  // gam (lbfgs.hpp:116-119), then w = R^-1 u, z = (D + gam YY) w - gam v,
+  // p = R^-T z; d = gam g + S p - gam Y w.
+  double gam = 1.0;
+  if (kk > 0 && h->yy[kk - 1] > 0.0) gam = h->sy[kk - 1] / h->yy[kk - 1];
+  double w[kMaxMemory], p[kMaxMemory];
+  for (int i = kk - 1; i >= 0; --i) {
+    double t = u[i];
+    for (int j = i + 1; j < kk; ++j) t -= cs->R[i * kMaxMemory + j] * w[j];
+    w[i] = t / cs->R[i * kMaxMemory + i];
+  }
+  for (int i = 0; i < kk; ++i) {
+    double t = cs->R[i * kMaxMemory + i] * w[i] - gam * vv[i];
+    for (int j = 0; j < kk; ++j) t += gam * cs->YY[i * kMaxMemory + j] * w[j];
+    for (int j = 0; j < i; ++j) t -= cs->R[j * kMaxMemory + i] * p[j];
+    p[i] = t / cs->R[i * kMaxMemory + i];
+  }
+  for (int i = 0; i < kk; ++i) {
+    cs->p[i] = p[i];
+    cs->w[i] = gam * w[i];
+    cs->u[i] = u[i];
+    cs->v[i] = vv[i];
+  }
+  cs->gam = gam;
+  cs->k = kk;
+}
+
+void launch_compact_prepare(int pair, const double* xt, const double* x, const double* gt,
+                            const double* g, const double* gn, double* S, double* Y,
+                            int64_t stride, HistState* h, CompactState* cs, int mem, int64_t dim,
+                            double* partials, EvalScalars* sc, cudaStream_t s) {
+  // rows: the history capacity + 1, static so that captured graphs never change
+  dim3 grid(kSlices, (unsigned)(mem + 1));
+  k_compact_prepare<<<grid, 256, 0, s>>>(pair, xt, x, gt, g, gn, S, Y, stride, h, cs, dim,
+                                         partials, sc);
+}
+
+// d = gam g + sum_i p_i s_i - sum_i w_i y_i (per element, i ascending), the
+// slopes g.d and d.d, and the first trial point x + t d.
+__global__ void __launch_bounds__(256) k_compact_direction(
+    const double* __restrict__ g, const double* __restrict__ S, const double* __restrict__ Y,
+    int64_t stride, const HistState* __restrict__ h, const CompactState* __restrict__ cs,
+    double* __restrict__ d, const double* __restrict__ x, const double* __restrict__ tp,
+    double* __restrict__ xt, int64_t dim, double* __restrict__ partials, EvalScalars* sc,
+    double* __restrict__ out) {
+  __shared__ const double* sp[kMaxMemory];
+  __shared__ const double* yp[kMaxMemory];
+  __shared__ double pc[kMaxMemory], wc[kMaxMemory];
+  __shared__ int ks;
+  __shared__ double gs;
+  if (threadIdx.x == 0) {
+    ks = cs->k;
+    gs = cs->gam;
+  }
+  __syncthreads();
+  const int k = ks;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    sp[i] = S + h->order[i] * stride;
+    yp[i] = Y + h->order[i] * stride;
+    pc[i] = cs->p[i];
+    wc[i] = cs->w[i];
+  }
+  __syncthreads();
+  const double gam = gs;
+  const double t = xt ? *tp : 0.0;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double ge = g[e];
+    double de = dmul(gam, ge);
+    for (int i = 0; i < k; ++i) de = dadd(de, dmul(pc[i], sp[i][e]));
+    for (int i = 0; i < k; ++i) de = dsub(de, dmul(wc[i], yp[i][e]));
+    d[e] = de;
+    if (xt) xt[e] = dadd(x[e], dmul(t, de));  // lbfgs.hpp:86
+    acc[0] = dadd(acc[0], dmul(ge, de));
+    acc[1] = dadd(acc[1], dmul(de, de));
+  }
+  double r[2];
+  if (last_block_reduce<256, 2>(acc, partials, &sc->ticket, r)) {
+    out[0] = r[0];
+    out[1] = r[1];
+  }
+}
+
+void launch_compact_direction(const double* g, const double* S, const double* Y, int64_t stride,
+                              const HistState* h, const CompactState* cs, double* d,
+                              const double* x, const double* t, double* xt_out, int64_t dim,
+                              double* partials, EvalScalars* sc, double* out, int nblocks,
+                              cudaStream_t s) {
+  k_compact_direction<<<nblocks, 256, 0, s>>>(g, S, Y, stride, h, cs, d, x, t, xt_out, dim,
+                                              partials, sc, out);
+}
+
+}  // namespace gsot

@@ -102,6 +102,8 @@ class Solver {
     ws->d = dalloc<double>(dim + 8, t);
     ws->S = dalloc<double>(static_cast<size_t>(mem + 1) * dim, t);
     ws->Y = dalloc<double>(static_cast<size_t>(mem + 1) * dim, t);
+    ws->cs = dalloc<CompactState>(1, t);
+    ws->cpart = dalloc<double>(static_cast<size_t>(mem + 2) * 64 * 5, t);
   }
 
   // ---- device sequences ----------------------------------------------------
@@ -185,6 +187,35 @@ class Solver {
       launch_axpy_point(w_->X[r_], &c_->dsync->t, w_->d, w_->X[q], w_->dim, c_->stream);
     });
     enqueue_eval(c_, w_->X[q], mode_eval_, w_->G[q], w_->d, o_.upper_bound_offset, use_active_);
+  }
+
+  // The search direction (lbfgs.hpp:109-126), optionally preceded by the
+  // pending curvature pair of the last acceptance (lbfgs.hpp:243-255) and
+  // followed by the first trial point x + t d into the trial buffer.
+  // Exact mode: the reference's two-loop with sequential dots. Fast mode:
+  // the compact representation (one multi-dot pass with a last-block solve,
+  // one combine pass that also forms the trial point).
+  void enqueue_direction(bool pair, bool trial) {
+    const int q = 1 - r_;
+    if (exact_) {
+      if (pair) enqueue_pair();
+      enqueue_two_loop();
+      if (trial)
+        c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
+          launch_axpy_point(w_->X[r_], &c_->dsync->t, w_->d, w_->X[q], w_->dim, c_->stream);
+        });
+      return;
+    }
+    c_->launch(K_LBFGS, 8.0 * w_->dim * (2.0 * w_->mem + 6.0), [&] {
+      launch_compact_prepare(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->G[r_],
+                             w_->S, w_->Y, w_->dim, &c_->dsync->h, w_->cs, mem_, w_->dim,
+                             w_->cpart, c_->sc, c_->stream);
+    });
+    c_->launch(K_LBFGS, 8.0 * w_->dim * (2.0 * w_->mem + 4.0), [&] {
+      launch_compact_direction(w_->G[r_], w_->S, w_->Y, w_->dim, &c_->dsync->h, w_->cs, w_->d,
+                               w_->X[r_], &c_->dsync->t, trial ? w_->X[q] : nullptr, w_->dim,
+                               c_->partials, c_->sc, c_->dsync->tl, c_->red_blocks, c_->stream);
+    });
   }
 
   // ---- bookkeeping ---------------------------------------------------------
@@ -355,16 +386,16 @@ class Solver {
           bool have_first = false;
           if (res_->iterations == 0) {
             run_seq(pending_pair ? "PD" : "D", [&] {
-              if (pending_pair) enqueue_pair();
-              enqueue_two_loop();
+              enqueue_direction(pending_pair, false);
               c_->enqueue_fetch();
             });
           } else {
             c_->h_sync->t = 1.0;  // t_init (lbfgs.hpp:150)
             run_seq(pending_pair ? "PDT" : "DT", [&] {
-              if (pending_pair) enqueue_pair();
-              enqueue_two_loop();
-              enqueue_trial();
+              enqueue_t();
+              enqueue_direction(pending_pair, true);
+              enqueue_eval(c_, w_->X[1 - r_], mode_eval_, w_->G[1 - r_], w_->d,
+                           o_.upper_bound_offset, use_active_);
               c_->enqueue_fetch();
             });
             have_first = true;

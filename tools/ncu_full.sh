@@ -1,0 +1,7 @@
+#!/bin/bash
+# --set full on selected kernels of the second fast-mode config-2 solve.
+TAG=${1:-f}
+REGEX=${2:-k_eval}
+python tests/_gpu_solve_once.py > gpurun_out/solve_once_$TAG.log 2>&1 && \
+ncu --set full --import-source on --cache-control none --clock-control none -k regex:"$REGEX" -s ${3:-400} -c ${4:-2} -o gpurun_out/prof_$TAG python tests/_gpu_solve_once.py > gpurun_out/ncu_$TAG.log 2>&1
+echo DONE $?
