@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgsot.so")
+LIB_PATH = os.environ.get("GSOT_LIB") or os.path.join(HERE, "lib", "libgsot.so")
 
 GSOT_OK = 0
 STATUS_NAMES = {

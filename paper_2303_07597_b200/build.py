@@ -16,6 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libgsot.so")
+# Diagnostic variants: GSOT_NVCC_DEFINES="-DGSOT_PHASE_CLOCKS" GSOT_LIB_OUT=... (never the product)
+EXTRA = os.environ.get("GSOT_NVCC_DEFINES", "").split()
 SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu", "gsot_solver.cu", "gsot_exact.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -28,20 +30,21 @@ FLAGS = [
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
+    LIB = os.environ.get("GSOT_LIB_OUT") or globals()["LIB"]
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in ("gsot_internal.cuh", "gsot_device.cuh", "gsot_ctx.cuh")] + [os.path.join(ROOT, "include", "gsot.h")]
     if (not force and os.path.exists(LIB)
             and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps)):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    objdir = os.path.join(HERE, "lib", "obj")
+    objdir = os.path.join(HERE, "lib", "obj" + ("_diag" if EXTRA else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s).replace(".cu", ".o"))
         objs.append(o)
-        cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
+        cmd = [NVCC, *FLAGS, *EXTRA, "-c", s, "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)

@@ -115,7 +115,7 @@ gsot_ctx::~gsot_ctx() {
                   x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
-                  cnt_partials, cnt_slots};
+                  cnt_partials, cnt_slots, d_pub_count};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -184,7 +184,10 @@ void alloc_buffers(gsot_ctx* c) {
   c->colpart = dalloc<double>(static_cast<size_t>(L) * n, t);
   c->psi = dalloc<double>(static_cast<size_t>(L) * n, t);
   c->psicol = dalloc<double>(n, t);
-  c->partials = dalloc<double>(static_cast<size_t>(c->red_blocks) * 4 + 64, t);
+  c->partials = dalloc<double>(
+      static_cast<size_t>(std::max<int64_t>(c->red_blocks, (m + 31) / 32 + (n + 31) / 32)) * 4 +
+          64,
+      t);
   c->cnt_slots = dalloc<unsigned long long>(64 * 8, t);
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->cnt_slots, 0, sizeof(unsigned long long) * 64 * 8, c->stream));
   c->cnt_partials = dalloc<unsigned long long>(
@@ -203,9 +206,17 @@ void alloc_buffers(gsot_ctx* c) {
   c->dbeta = dalloc<double>(n, t);
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dsync = dalloc<gsot::DevSync>(1, t);
-  GSOT_CUDA_CHECK(cudaMallocHost(&c->h_sync, sizeof(gsot::DevSync)));
+  GSOT_CUDA_CHECK(cudaHostAlloc(&c->h_sync, sizeof(gsot::DevSync) + 128, cudaHostAllocMapped));
+  c->h_flag = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(c->h_sync) +
+                                                    sizeof(gsot::DevSync) + 64 -
+                                                    sizeof(gsot::DevSync) % 64);
+  GSOT_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_sync_dev), c->h_sync, 0));
+  GSOT_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_flag_dev), c->h_flag, 0));
+  c->d_pub_count = dalloc<unsigned long long>(1, t);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->d_pub_count, 0, sizeof(unsigned long long), c->stream));
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->dsync, 0, sizeof(gsot::DevSync), c->stream));
-  memset(c->h_sync, 0, sizeof(gsot::DevSync));
+  memset(c->h_sync, 0, sizeof(gsot::DevSync) + 128);
+  c->pub_expected = 0;
   c->sc = &c->dsync->sc;
   c->h_sc = &c->h_sync->sc;
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->x_eval, 0, sizeof(double) * (dim + 8), c->stream));
@@ -412,12 +423,9 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
       launch_eval(P, d_x, c->dense_tasks, c->L * c->nw, nullptr, words, c->rowpart, c->colpart,
                   c->psi, c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
   });
-  c->launch(K_FINALIZE, 0.0, [&] {
-    launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, c->psicol, c->stream);
-  });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
-    launch_objective(P, d_x, c->psicol, d_grad, d_dir, c->partials, c->red_blocks, c->sc,
-                     mode == GSOT_EVAL_SCREENED ? c->cnt_slots : nullptr, c->stream);
+    launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, d_dir, c->partials,
+                    c->sc, mode == GSOT_EVAL_SCREENED ? 1 : 0, c->stream);
   });
 }
 

@@ -2,6 +2,8 @@
 // code (gsot_ctx.cu) and the solver (gsot_solver.cu).
 #pragma once
 
+#include <atomic>
+
 #include <cuda_runtime.h>
 
 #include <functional>
@@ -26,6 +28,7 @@ struct Sequence {
   cudaGraphExec_t exec = nullptr;
   std::vector<Mark> marks;
   int kernels = 0;
+  int publishes = 0;
   ~Sequence() {
     if (exec) cudaGraphExecDestroy(exec);
     for (auto& m : marks) {
@@ -51,7 +54,7 @@ struct SolverWorkspace {
   double* Y = nullptr;
   double* audit_g = nullptr;
   CompactState* cs = nullptr;   // compact L-BFGS state (fast mode)
-  double* cpart = nullptr;      // prepare-pass partials: (mem + 1) x 64 x 5
+  double* cpart = nullptr;      // step-kernel partials (lbfgs_step_partials)
   std::map<std::string, std::unique_ptr<Sequence>> graphs;
   ~SolverWorkspace();
 };
@@ -89,7 +92,12 @@ struct gsot_ctx {
   bool have_snapshot = false;
   // scalars: one device block, one pinned mirror
   gsot::DevSync* dsync = nullptr;
-  gsot::DevSync* h_sync = nullptr;
+  gsot::DevSync* h_sync = nullptr;      // mapped pinned mirror, written by k_publish
+  gsot::DevSync* h_sync_dev = nullptr;  // its device address
+  unsigned long long* h_flag = nullptr;      // mapped completion counter
+  unsigned long long* h_flag_dev = nullptr;
+  unsigned long long* d_pub_count = nullptr;  // device copy of the counter
+  unsigned long long pub_expected = 0;        // publishes enqueued so far
   gsot::EvalScalars* sc = nullptr;    // &dsync->sc
   gsot::EvalScalars* h_sc = nullptr;  // &h_sync->sc
   int eval_grid = 148 * 4;
@@ -208,17 +216,40 @@ struct gsot_ctx {
 
   void sync() { GSOT_CUDA_CHECK(cudaStreamSynchronize(stream)); }
   void fetch_scalars() {
-    GSOT_CUDA_CHECK(
-        cudaMemcpyAsync(h_sync, dsync, sizeof(gsot::DevSync), cudaMemcpyDeviceToHost, stream));
-    sync();
+    enqueue_fetch();
+    wait_published();
     collect_marks();
   }
+  // Enqueue the publication of the scalar block to the host mirror.
   void enqueue_fetch() {
-    GSOT_CUDA_CHECK(
-        cudaMemcpyAsync(h_sync, dsync, sizeof(gsot::DevSync), cudaMemcpyDeviceToHost, stream));
+    launch(gsot::K_MISC, 0.0, [&] {
+      gsot::launch_publish(dsync, h_sync_dev, d_pub_count, h_flag_dev, partials,
+                           ws ? ws->cpart : nullptr, cnt_slots, stream);
+    });
+    if (capturing)
+      ++capturing->publishes;
+    else
+      ++pub_expected;
+  }
+  // Wait until every enqueued publication has landed in the host mirror:
+  // spin on the mapped counter (the stream is polled for errors meanwhile).
+  void wait_published() {
+    const volatile unsigned long long* f = h_flag;
+    for (uint64_t spin = 0;; ++spin) {
+      if (*f >= pub_expected) break;
+      if ((spin & 1023u) == 1023u) {
+        const cudaError_t st = cudaStreamQuery(stream);
+        if (st == cudaSuccess) {
+          if (*f >= pub_expected) break;
+          throw gsot::Error(GSOT_ERR_CUDA, "publication counter out of step with the stream");
+        }
+        if (st != cudaErrorNotReady) GSOT_CUDA_CHECK(st);
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
   }
   void reset_scalars() {
-    GSOT_CUDA_CHECK(cudaMemsetAsync(sc, 0, sizeof(gsot::EvalScalars), stream));
+    GSOT_CUDA_CHECK(cudaMemsetAsync(sc, 0, gsot::kEvalScalarsResetBytes, stream));
   }
 
   ~gsot_ctx();

@@ -156,9 +156,9 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
 namespace gsot {
 
 // Fold the 64 counter slots into sc->counters etc. and zero them (one warp).
+// Called by exactly one full warp.
 __device__ __forceinline__ void fold_counter_slots(unsigned long long* slots, EvalScalars* sc) {
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x >= 32) return;
   unsigned long long v[7];
 #pragma unroll
   for (int k = 0; k < 7; ++k) {

@@ -107,7 +107,7 @@ __global__ void k_exact_objective(DevProblem P, const double* __restrict__ x,
                                   const double* __restrict__ psi, const double* __restrict__ grad,
                                   const double* __restrict__ dvec, EvalScalars* sc,
                                   unsigned long long* cnt_slots) {
-  if (cnt_slots) fold_counter_slots(cnt_slots, sc);  // screen counters (one warp)
+  if (cnt_slots && threadIdx.x < 32) fold_counter_slots(cnt_slots, sc);  // screen counters
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double psi_sum = 0.0;
   for (int64_t j = 0; j < P.n; ++j)

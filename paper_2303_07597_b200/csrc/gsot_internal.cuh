@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -71,7 +72,16 @@ struct EvalScalars {
   unsigned int ticket;  // last-block-done counter
   int audit_violation;  // audit: first violating block + 1 (l * n + j + 1)
   long long audit_where;
+  // deferred folds, done by k_publish: per-block partials left by k_finalize
+  // (fin_blocks blocks x 4), by k_lbfgs_step (step_blocks CTAs x 2), and the
+  // screen's counter slots (cnt_pending). Not cleared by the per-evaluation
+  // reset (it covers the fields above only).
+  int fin_blocks;
+  int step_blocks;
+  int cnt_pending;
+  int pad_;
 };
+constexpr size_t kEvalScalarsResetBytes = offsetof(EvalScalars, fin_blocks);
 
 // ---- kernels (gsot_kernels.cu) ---------------------------------------------
 
@@ -113,12 +123,11 @@ int eval_blocks_per_sm(size_t smem);
 void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
                  double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s);
+// grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const double* rowpart, const double* colpart, const double* psi,
-                     double* grad, double* psicol, cudaStream_t s);
-void launch_objective(const DevProblem& P, const double* x, const double* psicol,
-                      const double* grad, const double* dvec, double* partials, int nblocks,
-                      EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s);
+                     double* grad, const double* dvec, double* partials, EvalScalars* sc,
+                     int cnt_pending, cudaStream_t s);
 void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,
                          double* out, cudaStream_t s);
 void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* words,
@@ -154,8 +163,17 @@ struct DevSync {
   EvalScalars sc;
   HistState h;
   double tl[2];  // two-loop: g.d, d.d
-  double t;      // line-search step read by the axpy kernel
+  double t;      // line-search step: host-owned, copied in by the solver
 };
+
+// Copy the scalar block into mapped host memory and then bump the host-visible
+// completion counter (system-scope release): the host spins on the counter
+// instead of a D2H copy + stream synchronisation.
+// First the pending folds (EvalScalars::fin_blocks / step_blocks /
+// cnt_pending) in a fixed order.
+void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_count,
+                    unsigned long long* host_flag, const double* fin_partials,
+                    const double* step_partials, unsigned long long* cnt_slots, cudaStream_t s);
 
 struct TwoLoopArgs {
   const double* S;  // pair slots: slot s at S + s * stride
@@ -167,15 +185,9 @@ struct TwoLoopArgs {
   int64_t dim;
   double* out;  // [0] = g.d, [1] = d.d
 };
-void launch_two_loop(const TwoLoopArgs& a, cudaStream_t s);
 // trial.x = x + t * d with t read from device memory.
 void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
                        int64_t dim, cudaStream_t s);
-// s = trial.x - x, y = g - trial.g into slot h->scratch, then the acceptance
-// test s.y > 1e-10 |s| |y| and the ring update (lbfgs.hpp:243-255).
-void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* S,
-                 double* Y, int64_t stride, HistState* h, int64_t dim, double* partials,
-                 int nblocks, EvalScalars* sc, cudaStream_t s);
 void launch_hist_reset(HistState* h, int mem, cudaStream_t s);
 void launch_dot(const double* a, const double* b, int64_t dim, double* partials, int nblocks,
                 EvalScalars* sc, int slot, cudaStream_t s);
@@ -220,20 +232,17 @@ struct CompactState {
   int k;
 };
 
-// One multi-dot pass + last-block solve. pair != 0: first form the
-// curvature pair of (xt, x, gt, g) into the scratch slot (lbfgs.hpp:243-255),
-// test it, update the ring and R / YY; then u, v for the gradient gn (= gt
-// when pair != 0) and the direction coefficients.
-void launch_compact_prepare(int pair, const double* xt, const double* x, const double* gt,
-                            const double* g, const double* gn, double* S, double* Y,
-                            int64_t stride, HistState* h, CompactState* cs, int mem, int64_t dim,
-                            double* partials, EvalScalars* sc, cudaStream_t s);
-// d = gam g + S p - Y w; out[0] = g.d, out[1] = d.d; xt_out = x + t d when
-// xt_out != null (the first trial point of the line search).
-void launch_compact_direction(const double* g, const double* S, const double* Y, int64_t stride,
-                              const HistState* h, const CompactState* cs, double* d,
-                              const double* x, const double* t, double* xt_out, int64_t dim,
-                              double* partials, EvalScalars* sc, double* out, int nblocks,
-                              cudaStream_t s);
+constexpr int kStepMaxGrid = 1024;  // CTAs of the cooperative step kernel, at most
+// Doubles of partials the step kernel needs for a history of `mem` pairs.
+size_t lbfgs_step_partials(int mem);
+// The fast-mode direction update in one cooperative launch (gsot_lbfgs.cu):
+// pair != 0 first forms the pending curvature pair s = x - xprev,
+// y = gprev - g into the scratch slot, tests it and updates the ring and
+// R / YY (lbfgs.hpp:243-255); then the compact coefficients for g, the
+// direction d, out[0] = g.d, out[1] = d.d, and xt = x + t d when xt != null.
+void launch_lbfgs_step(int pair, const double* x, const double* xprev, const double* g,
+                       const double* gprev, double* S, double* Y, int64_t stride, HistState* h,
+                       CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
+                       double* out, EvalScalars* sc, double* part, int mem, cudaStream_t s);
 
 }  // namespace gsot

@@ -163,27 +163,31 @@ __global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __res
     if (j < P.n) dbeta[j] = dsub(x[P.m + j], xs[P.m + j]);
     return;
   }
-  __shared__ double sq_sh[8][32];
-  __shared__ signed char sg_sh[8][32];
+  constexpr int kBatch = 4;  // 32-row chunks loaded per round trip
+  __shared__ double sq_sh[8][kBatch * 32];
+  __shared__ signed char sg_sh[8][kBatch * 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l = blockIdx.x * 8 + warp;
   if (l >= P.L) return;
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
   double ap = 0.0, af = 0.0, an = 0.0;
-  for (int r0 = 0; r0 < g; r0 += 32) {
-    const int r = r0 + lane;
-    double sq = 0.0;
-    signed char sgn = 0;
-    if (r < g) {
-      const double da = dsub(x[o0 + r], xs[o0 + r]);
-      sq = dmul(da, da);
-      sgn = da > 0.0 ? 1 : (da < 0.0 ? -1 : 0);
+  for (int r0 = 0; r0 < g; r0 += kBatch * 32) {
+    double xv[kBatch], sv[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const int r = r0 + b * 32 + lane;
+      xv[b] = r < g ? x[o0 + r] : 0.0;
+      sv[b] = r < g ? xs[o0 + r] : 0.0;
     }
-    sq_sh[warp][lane] = sq;
-    sg_sh[warp][lane] = sgn;
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      const double da = dsub(xv[b], sv[b]);
+      sq_sh[warp][b * 32 + lane] = dmul(da, da);
+      sg_sh[warp][b * 32 + lane] = da > 0.0 ? 1 : (da < 0.0 ? -1 : 0);
+    }
     __syncwarp();
     if (lane == 0) {
-      const int cnt = min(32, g - r0);
+      const int cnt = min(kBatch * 32, g - r0);
       for (int k = 0; k < cnt; ++k) {
         const double s = sq_sh[warp][k];
         const signed char sg = sg_sh[warp][k];
@@ -614,39 +618,51 @@ void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int nt
 // ---------------------------------------------------------------- finalize
 // grad_alpha_i = a_i - sum over non-empty chunks c of rowpart[c*m+i];
 // grad_beta_j = b_j - sum over surviving l of colpart[l][j]; psicol_j = sum
-// over surviving l of psi[l][j]. Each sum has a FIXED association: 8 slices
-// (c = s mod 8 resp. l = s mod 8), each sequential in ascending order, then
-// the 8 slice partials in slice order. Empty chunks and skipped blocks
-// contribute exact zeros, so omitting them leaves every partial unchanged:
-// the result does not depend on the screen.
-// Block (32, 8): blocks [0, m/32) handle 32 rows, the rest 32 columns.
-__global__ void __launch_bounds__(256) k_finalize(DevProblem P, const uint32_t* __restrict__ words,
-                                                  const double* __restrict__ rowpart,
-                                                  const double* __restrict__ colpart,
-                                                  const double* __restrict__ psi,
-                                                  double* __restrict__ grad,
-                                                  double* __restrict__ psicol, int row_blocks) {
-  __shared__ double sh[2][8][33];
+// over surviving l of psi[l][j]. Each sum has a FIXED association: 16
+// slices (c = s mod 16 resp. l = s mod 16), each sequential in ascending
+// order, then the 16 slice partials in slice order. Empty chunks and skipped
+// blocks contribute exact zeros, so omitting them leaves every partial
+// unchanged: the result does not depend on the screen.
+// In the same kernel: per-block partials of a.alpha, b.beta, sum psi
+// (dual.hpp:51) and the line-search slope grad.d; k_publish folds them in
+// block order (and the screen's counter slots) before the host reads them.
+// Block (32, 16): blocks [0, m/32) handle 32 rows, the rest 32 columns.
+constexpr int kFinSlices = 16;
+constexpr int kFinBatch = 10;
+
+__global__ void __launch_bounds__(32 * kFinSlices, 2) k_finalize(DevProblem P, const double* __restrict__ x,
+                                                   const uint32_t* __restrict__ words,
+                                                   const double* __restrict__ rowpart,
+                                                   const double* __restrict__ colpart,
+                                                   const double* __restrict__ psi,
+                                                   double* __restrict__ grad,
+                                                   const double* __restrict__ dvec,
+                                                   double* __restrict__ partials,
+                                                   EvalScalars* sc, int cnt_pending,
+                                                   int row_blocks) {
+  __shared__ double sh[2][kFinSlices][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double obj[4] = {0.0, 0.0, 0.0, 0.0};  // a.alpha, b.beta, psi, g.d
   if ((int)blockIdx.x < row_blocks) {
     const int64_t i = blockIdx.x * 32ll + tx;
     double acc = 0.0;
     if (i < P.m) {
       const int l = P.row_group[i];
       const uint32_t* __restrict__ wl = words + (int64_t)l * P.nw;
-      // slice ty: chunks c = ty + 8q, ascending; loads batched 8 at a time
-      for (int c0 = ty; c0 < P.nw; c0 += 64) {
-        uint32_t w[8];
-        double r[8];
+      // slice ty: chunks c = ty + 32q, ascending; all loads of a batch in flight
+      for (int c0 = ty; c0 < P.nw; c0 += kFinSlices * kFinBatch) {
+        uint32_t w[kFinBatch];
+        double r[kFinBatch];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = c0 + 8 * u;
+        for (int u = 0; u < kFinBatch; ++u) {
+          const int c = c0 + kFinSlices * u;
           w[u] = c < P.nw ? wl[c] : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = w[u] ? rowpart[(int64_t)(c0 + 8 * u) * P.m + i] : 0.0;
+        for (int u = 0; u < kFinBatch; ++u)
+          r[u] = w[u] ? rowpart[(int64_t)(c0 + kFinSlices * u) * P.m + i] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kFinBatch; ++u)
           if (w[u]) acc = dadd(acc, r[u]);
       }
     }
@@ -654,96 +670,77 @@ __global__ void __launch_bounds__(256) k_finalize(DevProblem P, const uint32_t* 
     __syncthreads();
     if (ty == 0 && i < P.m) {
       double s = sh[0][0][tx];
-      for (int q = 1; q < 8; ++q) s = dadd(s, sh[0][q][tx]);
-      grad[i] = dsub(P.a[i], s);
+      for (int q = 1; q < kFinSlices; ++q) s = dadd(s, sh[0][q][tx]);
+      const double gi = dsub(P.a[i], s);
+      grad[i] = gi;
+      obj[0] = dmul(x[i], P.a[i]);
+      if (dvec) obj[3] = dmul(gi, dvec[i]);
     }
-    return;
-  }
-  const int64_t j = (blockIdx.x - row_blocks) * 32ll + tx;
-  double acc = 0.0, ps = 0.0;
-  if (j < P.n) {
-    const int64_t c = j >> 5;
-    for (int l0 = ty; l0 < P.L; l0 += 64) {
-      bool on[8];
-      double cp[8], pp[8];
+  } else {
+    const int64_t j = (blockIdx.x - row_blocks) * 32ll + tx;
+    double acc = 0.0, ps = 0.0;
+    if (j < P.n) {
+      const int64_t c = j >> 5;
+      for (int l0 = ty; l0 < P.L; l0 += kFinSlices * kFinBatch) {
+        bool on[kFinBatch];
+        double cp[kFinBatch], pp[kFinBatch];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int l = l0 + 8 * u;
-        on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t idx = (int64_t)(l0 + 8 * u) * P.n + j;
-        cp[u] = on[u] ? colpart[idx] : 0.0;
-        pp[u] = on[u] ? psi[idx] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (on[u]) {
-          acc = dadd(acc, cp[u]);
-          ps = dadd(ps, pp[u]);
+        for (int u = 0; u < kFinBatch; ++u) {
+          const int l = l0 + kFinSlices * u;
+          on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
         }
+#pragma unroll
+        for (int u = 0; u < kFinBatch; ++u) {
+          const int64_t idx = (int64_t)(l0 + kFinSlices * u) * P.n + j;
+          cp[u] = on[u] ? colpart[idx] : 0.0;
+          pp[u] = on[u] ? psi[idx] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kFinBatch; ++u)
+          if (on[u]) {
+            acc = dadd(acc, cp[u]);
+            ps = dadd(ps, pp[u]);
+          }
+      }
+    }
+    sh[0][ty][tx] = acc;
+    sh[1][ty][tx] = ps;
+    __syncthreads();
+    if (ty == 0 && j < P.n) {
+      double s = sh[0][0][tx], p = sh[1][0][tx];
+      for (int q = 1; q < kFinSlices; ++q) {
+        s = dadd(s, sh[0][q][tx]);
+        p = dadd(p, sh[1][q][tx]);
+      }
+      const double gj = dsub(P.b[j], s);
+      grad[P.m + j] = gj;
+      obj[1] = dmul(x[P.m + j], P.b[j]);
+      obj[2] = p;
+      if (dvec) obj[3] = dmul(gj, dvec[P.m + j]);
     }
   }
-  sh[0][ty][tx] = acc;
-  sh[1][ty][tx] = ps;
-  __syncthreads();
-  if (ty == 0 && j < P.n) {
-    double s = sh[0][0][tx], p = sh[1][0][tx];
-    for (int q = 1; q < 8; ++q) {
-      s = dadd(s, sh[0][q][tx]);
-      p = dadd(p, sh[1][q][tx]);
+  if (ty == 0) {  // warp 0 holds the 32 rows / columns: fixed xor tree
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int o = 1; o <= 16; o <<= 1) obj[q] = dadd(obj[q], __shfl_xor_sync(0xffffffffu, obj[q], o));
     }
-    grad[P.m + j] = dsub(P.b[j], s);
-    psicol[j] = p;
+    if (tx < 4) partials[blockIdx.x * 4 + tx] = obj[tx == 0 ? 0 : tx == 1 ? 1 : tx == 2 ? 2 : 3];
+    if (blockIdx.x == 0 && tx == 0) {
+      sc->fin_blocks = (int)gridDim.x;
+      sc->cnt_pending = cnt_pending;
+    }
   }
 }
 
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const double* rowpart, const double* colpart, const double* psi,
-                     double* grad, double* psicol, cudaStream_t s) {
-  (void)x;
+                     double* grad, const double* dvec, double* partials, EvalScalars* sc,
+                     int cnt_pending, cudaStream_t s) {
   const int rb = (int)((P.m + 31) / 32);
   const int cb = (int)((P.n + 31) / 32);
-  k_finalize<<<rb + cb, 256, 0, s>>>(P, words, rowpart, colpart, psi, grad, psicol, rb);
-}
-
-// Objective a.alpha + b.beta - sum psi (dual.hpp:51) and optionally the
-// line-search slope grad.d, as fixed-structure reductions.
-__global__ void __launch_bounds__(256) k_objective(DevProblem P, const double* __restrict__ x,
-                                                   const double* __restrict__ psicol,
-                                                   const double* __restrict__ grad,
-                                                   const double* __restrict__ dvec,
-                                                   double* __restrict__ partials,
-                                                   EvalScalars* sc,
-                                                   unsigned long long* cnt_slots) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t dim = P.m + P.n;
-  double p[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t i = t0; i < P.m; i += stride) p[0] = dadd(p[0], dmul(x[i], P.a[i]));
-  for (int64_t j = t0; j < P.n; j += stride) {
-    p[1] = dadd(p[1], dmul(x[P.m + j], P.b[j]));
-    p[2] = dadd(p[2], psicol[j]);
-  }
-  if (dvec)
-    for (int64_t i = t0; i < dim; i += stride) p[3] = dadd(p[3], dmul(grad[i], dvec[i]));
-  double out[4];
-  const bool lastb = last_block_reduce<256, 4>(p, partials, &sc->ticket, out);
-  if (cnt_slots != nullptr && __syncthreads_or(lastb)) fold_counter_slots(cnt_slots, sc);
-  if (lastb) {
-    sc->dot_aa = out[0];
-    sc->dot_bb = out[1];
-    sc->psi_sum = out[2];
-    sc->objective = dsub(dadd(out[0], out[1]), out[2]);
-    sc->slope = out[3];
-  }
-}
-
-void launch_objective(const DevProblem& P, const double* x, const double* psicol,
-                      const double* grad, const double* dvec, double* partials, int nblocks,
-                      EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s) {
-  k_objective<<<nblocks, 256, 0, s>>>(P, x, psicol, grad, dvec, partials, sc, cnt_slots);
+  k_finalize<<<rb + cb, 32 * kFinSlices, 0, s>>>(P, x, words, rowpart, colpart, psi, grad, dvec, partials,
+                                      sc, cnt_pending, rb);
 }
 
 // ---------------------------------------------------------------- plan

@@ -1,18 +1,19 @@
-// gsot_lbfgs.cu — device vector operations of the L-BFGS ascent
-// (lbfgs.hpp:61-274). The host keeps the scalar control flow of `maximize`
-// exactly; these kernels do every O(m+n) vector operation so that only
-// scalars cross PCIe.
+// gsot_lbfgs.cu — device side of the L-BFGS ascent (lbfgs.hpp:61-274) in
+// fast mode. The host keeps the scalar control flow of `maximize`; every
+// O(m+n) vector operation of one direction update runs in ONE cooperative
+// launch (k_lbfgs_step), so only scalars cross PCIe.
 //
-// The two-loop recursion (lbfgs.hpp:109-124) runs as ONE launch of a
-// thread-block cluster (16 CTAs where the device allows non-portable
-// clusters, else 8). Each CTA owns a contiguous slice of the vectors and keeps
-// its slice of q in shared memory; every dot product is reduced inside the
-// CTA (fixed tree), published in shared memory and summed by every CTA over
-// the cluster ranks in rank order through distributed shared memory, so all
-// CTAs see the same bits and the result is deterministic. Dots are fused with
-// the update that precedes them: the recursion makes 2k+1 passes over the
-// history instead of 4k+3. Elementwise arithmetic keeps the reference's
-// one-rounding-per-operation form (q - a*y, q*c, q + (a-b)*s, x + t*d).
+// The direction uses the compact representation of the L-BFGS inverse
+// Hessian (Byrd, Nocedal & Schnabel 1994) instead of the two-loop recursion:
+// the same matrix H_k = gam I + [S Y] M [S Y]^T, but the 4k dots it needs
+// are independent (one pass over the history) and the direction is one
+// combine pass: d = gam g + S p - Y (gam w), with w = R^-1 (S^T g),
+// p = R^-T ((D + gam Y^T Y) w - gam Y^T g), R = triu(S^T Y). R and Y^T Y are
+// kept by logical position and updated by one column per accepted pair.
+// Exact mode (gsot_exact.cu) keeps the reference's two-loop instead.
+//
+// Determinism: each dot is reduced by fixed warp trees, per-CTA results are
+// folded in CTA order, the grid is a fixed function of the device.
 #include <cooperative_groups.h>
 
 #include "gsot_device.cuh"
@@ -20,211 +21,6 @@
 namespace cg = cooperative_groups;
 
 namespace gsot {
-
-namespace {
-constexpr int kTwoLoopThreads = 512;
-constexpr int kWarps = kTwoLoopThreads / 32;
-int g_cluster = 0;           // chosen cluster size (16 or 8)
-size_t g_two_loop_smem = 0;  // dynamic smem configured so far
-}  // namespace
-
-// Cluster-wide deterministic sum. `part` is this thread's partial. Uses slot
-// `parity` of the per-CTA publication buffer; one cluster barrier.
-__device__ __forceinline__ double cluster_sum(cg::cluster_group& cluster, double part,
-                                              double* warp_sh, double* pub, double* tot_sh,
-                                              int parity, int nranks) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) part = dadd(part, __shfl_xor_sync(0xffffffffu, part, o));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) warp_sh[warp] = part;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = warp_sh[0];
-    for (int w = 1; w < kWarps; ++w) s = dadd(s, warp_sh[w]);
-    pub[parity] = s;
-  }
-  cluster.sync();
-  if (warp == 0) {
-    double v = 0.0;
-    if (lane < nranks) v = cluster.map_shared_rank(pub, lane)[parity];
-    // rank-ordered sequential sum on lane 0
-    double t = 0.0;
-    for (int r = 0; r < nranks; ++r) t = dadd(t, __shfl_sync(0xffffffffu, v, r));
-    if (lane == 0) tot_sh[parity] = t;
-  }
-  __syncthreads();
-  return tot_sh[parity];
-}
-
-__global__ void __launch_bounds__(kTwoLoopThreads) k_two_loop(const TwoLoopArgs A, int use_smem) {
-  extern __shared__ double q_dyn[];
-  cg::cluster_group cluster = cg::this_cluster();
-  __shared__ double warp_sh[kWarps];
-  __shared__ double pub[2];
-  __shared__ double tot_sh[2];
-  __shared__ double a_sh[kMaxMemory];
-  const int nranks = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
-  const int64_t per = (A.dim + nranks - 1) / nranks;
-  const int64_t lo = rank * per;
-  const int64_t hi = min(A.dim, lo + per);
-  const int64_t len = hi > lo ? hi - lo : 0;
-  // q slice: shared memory when it fits, else the output vector itself
-  double* __restrict__ q = use_smem ? q_dyn : A.d + lo;
-  const double* __restrict__ g = A.g + lo;
-  // history snapshot (no CTA writes it during this kernel)
-  __shared__ const double* s_ptr[kMaxMemory];
-  __shared__ const double* y_ptr[kMaxMemory];
-  __shared__ double rho_sh[kMaxMemory];
-  __shared__ double scale_sh;
-  __shared__ int k_sh, apply_sh;
-  if (threadIdx.x == 0) {
-    const int kk = A.h->k;
-    k_sh = kk;
-    for (int i = 0; i < kk; ++i) {
-      const int slot = A.h->order[i];
-      s_ptr[i] = A.S + slot * A.stride;
-      y_ptr[i] = A.Y + slot * A.stride;
-      rho_sh[i] = A.h->rho[i];
-    }
-    // lbfgs.hpp:116-119: q *= s.y / y.y of the newest pair when y.y > 0
-    apply_sh = 0;
-    scale_sh = 1.0;
-    if (kk > 0 && A.h->yy[kk - 1] > 0.0) {
-      apply_sh = 1;
-      scale_sh = A.h->sy[kk - 1] / A.h->yy[kk - 1];
-    }
-  }
-  __syncthreads();
-  const int k = k_sh;
-  int parity = 0;
-
-  // Loop 1 (lbfgs.hpp:112-115). Pass i: q -= a_{i+1} y_{i+1} (or q = g for
-  // the first pass), then a_i = rho_i * s_i . q.
-  for (int i = k - 1; i >= 0; --i) {
-    double part = 0.0;
-    const double* __restrict__ si = s_ptr[i] + lo;
-    if (i == k - 1) {
-#pragma unroll 4
-      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
-        const double qe = g[e];
-        q[e] = qe;
-        part = dadd(part, dmul(si[e], qe));
-      }
-    } else {
-      const double ap = a_sh[i + 1];
-      const double* __restrict__ yp = y_ptr[i + 1] + lo;
-#pragma unroll 4
-      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
-        const double qe = dsub(q[e], dmul(ap, yp[e]));
-        q[e] = qe;
-        part = dadd(part, dmul(si[e], qe));
-      }
-    }
-    const double dot = cluster_sum(cluster, part, warp_sh, pub, tot_sh, parity, nranks);
-    parity ^= 1;
-    if (threadIdx.x == 0) a_sh[i] = dmul(rho_sh[i], dot);
-    __syncthreads();
-  }
-  // Close loop 1 (q -= a_0 y_0), scale by s.y / y.y (lbfgs.hpp:116-119), and
-  // run loop 2 (lbfgs.hpp:120-123) fused: pass i applies the update of i-1
-  // and reduces y_i . q.
-  double b_prev = 0.0;
-  for (int i = 0; i <= k; ++i) {
-    double part = 0.0;
-    const bool last = (i == k);
-    if (k == 0) {
-      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) q[e] = g[e];  // d = g
-    } else if (i == 0) {
-      const double a0 = a_sh[0];
-      const double* __restrict__ y0 = y_ptr[0] + lo;
-#pragma unroll 4
-      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
-        double qe = dsub(q[e], dmul(a0, y0[e]));
-        if (apply_sh) qe = dmul(qe, scale_sh);
-        q[e] = qe;
-        part = dadd(part, dmul(y0[e], qe));
-      }
-    } else {
-      const double coef = dsub(a_sh[i - 1], b_prev);
-      const double* __restrict__ sp = s_ptr[i - 1] + lo;
-      const double* __restrict__ yi = last ? nullptr : y_ptr[i] + lo;
-#pragma unroll 4
-      for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
-        const double qe = dadd(q[e], dmul(coef, sp[e]));
-        q[e] = qe;
-        if (!last) part = dadd(part, dmul(yi[e], qe));
-      }
-    }
-    if (last) break;
-    const double dot = cluster_sum(cluster, part, warp_sh, pub, tot_sh, parity, nranks);
-    parity ^= 1;
-    b_prev = dmul(rho_sh[i], dot);
-  }
-  // d = q; dir_slope = g . d and |d|^2 (lbfgs.hpp:124-126, :152).
-  double pg = 0.0, pd = 0.0;
-  double* __restrict__ d = A.d + lo;
-#pragma unroll 4
-  for (int64_t e = threadIdx.x; e < len; e += kTwoLoopThreads) {
-    const double de = q[e];
-    if (use_smem) d[e] = de;
-    pg = dadd(pg, dmul(g[e], de));
-    pd = dadd(pd, dmul(de, de));
-  }
-  const double gd = cluster_sum(cluster, pg, warp_sh, pub, tot_sh, parity, nranks);
-  parity ^= 1;
-  const double dd = cluster_sum(cluster, pd, warp_sh, pub, tot_sh, parity, nranks);
-  if (rank == 0 && threadIdx.x == 0) {
-    A.out[0] = gd;
-    A.out[1] = dd;
-  }
-  cluster.sync();  // keep every CTA's shared memory alive until remote reads finish
-}
-
-void launch_two_loop(const TwoLoopArgs& a, cudaStream_t s) {
-  if (g_cluster == 0) {
-    g_cluster = 8;
-    if (cudaFuncSetAttribute(k_two_loop, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-        cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = 16;
-      attr.val.clusterDim.y = 1;
-      attr.val.clusterDim.z = 1;
-      cfg.gridDim = dim3(16);
-      cfg.blockDim = dim3(kTwoLoopThreads);
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      int nclusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&nclusters, k_two_loop, &cfg) == cudaSuccess &&
-          nclusters > 0)
-        g_cluster = 16;
-    }
-    cudaGetLastError();
-  }
-  const int64_t per = (a.dim + g_cluster - 1) / g_cluster;
-  size_t smem = sizeof(double) * (size_t)per;
-  int use_smem = smem <= 200 * 1024 ? 1 : 0;
-  if (!use_smem) smem = 0;
-  if (smem > g_two_loop_smem) {
-    cudaFuncSetAttribute(k_two_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    g_two_loop_smem = smem;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = g_cluster;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.gridDim = dim3(g_cluster);
-  cfg.blockDim = dim3(kTwoLoopThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_two_loop, a, use_smem);
-}
 
 // trial.x = x + t * d (lbfgs.hpp:86).
 __global__ void k_axpy_point(const double* __restrict__ x, const double* __restrict__ tp,
@@ -241,81 +37,115 @@ void launch_axpy_point(const double* x, const double* t, const double* d, double
   k_axpy_point<<<grid, 256, 0, s>>>(x, t, d, out, dim);
 }
 
-// Curvature pair (lbfgs.hpp:243-255): s = trial.x - x, y = g - trial.g
-// written to the scratch slot, s.y, s.s, y.y (deterministic), then -- in
-// the last block -- the acceptance test sy > 1e-10 |s| |y| and the ring
-// update: evict the oldest pair when full, append the scratch slot.
-__global__ void __launch_bounds__(256) k_pair(const double* __restrict__ xt,
-                                              const double* __restrict__ x,
-                                              const double* __restrict__ g,
-                                              const double* __restrict__ gt,
-                                              double* __restrict__ S, double* __restrict__ Y,
-                                              int64_t stride, HistState* h, int64_t dim,
-                                              double* __restrict__ partials, EvalScalars* sc) {
-  const int scratch = h->scratch;  // read by every block before the last one updates h
-  double* __restrict__ sv = S + scratch * stride;
-  double* __restrict__ yv = Y + scratch * stride;
-  double p[3] = {0.0, 0.0, 0.0};
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const double s = dsub(xt[e], x[e]);
-    const double y = dsub(g[e], gt[e]);
-    sv[e] = s;
-    yv[e] = y;
-    p[0] = dadd(p[0], dmul(s, y));
-    p[1] = dadd(p[1], dmul(s, s));
-    p[2] = dadd(p[2], dmul(y, y));
+#ifdef GSOT_PHASE_CLOCKS
+// Diagnostic build only: per-phase SM clocks of CTA 0 / thread 0, summed.
+__device__ unsigned long long g_phase_clk[16];
+#define PHASE_MARK(i)                                                   \
+  do {                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                          \
+      const long long now = clock64();                                  \
+      atomicAdd(&g_phase_clk[i], (unsigned long long)(now - clk_prev)); \
+      clk_prev = now;                                                   \
+    }                                                                   \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
+// Warp-wide: sum of part[i * stride] for i in [0, n) -- lane runs of
+// consecutive entries (loads in flight together), then a fixed xor tree.
+__device__ __forceinline__ double warp_fold(const double* part, int n, int stride) {
+  const int lane = threadIdx.x & 31;
+  const int run = (n + 31) / 32;
+  const int i0 = lane * run, i1 = min(n, i0 + run);
+  double s = 0.0;
+  for (int ib = i0; ib < i1; ib += 16) {
+    double q[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) q[u] = ib + u < i1 ? __ldcg(part + (int64_t)(ib + u) * stride) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (ib + u < i1) s = dadd(s, q[u]);
   }
-  double out[3];
-  if (last_block_reduce<256, 3>(p, partials, &sc->ticket, out)) {
-    const double sy = out[0], ss = out[1], yy = out[2];
-    sc->extra[0] = sy;
-    sc->extra[1] = ss;
-    sc->extra[2] = yy;
-    h->last_sy = sy;
-    h->last_ss = ss;
-    h->last_yy = yy;
-    const bool accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);
-    h->accepted = accept ? 1 : 0;
-    if (accept) {
-      int k = h->k;
-      if (k == h->mem) {  // erase the oldest (lbfgs.hpp:247-251)
-        const int ev = h->order[0];
-        for (int i = 1; i < k; ++i) {
-          h->order[i - 1] = h->order[i];
-          h->rho[i - 1] = h->rho[i];
-          h->sy[i - 1] = h->sy[i];
-          h->yy[i - 1] = h->yy[i];
-        }
-        --k;
-        h->order[k] = scratch;
-        h->scratch = ev;
-      } else {
-        h->order[k] = scratch;
-        // next scratch: the lowest slot not in use
-        int next = 0;
-        for (;; ++next) {
-          bool used = false;
-          for (int i = 0; i <= k; ++i) used |= h->order[i] == next;
-          if (!used) break;
-        }
-        h->scratch = next;
-      }
-      h->rho[k] = 1.0 / sy;
-      h->sy[k] = sy;
-      h->yy[k] = yy;
-      h->k = k + 1;
+#pragma unroll
+  for (int o = 1; o <= 16; o <<= 1) s = dadd(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return s;
+}
+
+__global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevSync* host_dst,
+                                                 unsigned long long* dev_count,
+                                                 unsigned long long* host_flag,
+                                                 const double* __restrict__ fin_partials,
+                                                 const double* __restrict__ step_partials,
+                                                 unsigned long long* cnt_slots) {
+  static_assert(offsetof(DevSync, t) % 8 == 0, "DevSync is copied as 8-byte words");
+#ifdef GSOT_PHASE_CLOCKS
+  long long clk_prev = clock64();
+#endif
+  EvalScalars* sc = &src->sc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fin = sc->fin_blocks, step = sc->step_blocks, cnt = sc->cnt_pending;
+  __shared__ double f[6];
+  if (fin > 0 && warp < 4) {  // a.alpha, b.beta, psi, g.d (dual.hpp:51)
+    const double v = warp_fold(fin_partials + warp, fin, 4);
+    if (lane == 0) f[warp] = v;
+  }
+  if (step > 0 && (warp == 4 || warp == 5)) {  // g.d, d.d of the new direction
+    const double v = warp_fold(step_partials + (warp - 4), step, 2);
+    if (lane == 0) f[warp] = v;
+  }
+  if (cnt && warp == 6) fold_counter_slots(cnt_slots, sc);
+  __syncthreads();
+  PHASE_MARK(11);
+  if (threadIdx.x == 0) {
+    if (fin > 0) {
+      sc->dot_aa = f[0];
+      sc->dot_bb = f[1];
+      sc->psi_sum = f[2];
+      sc->objective = dsub(dadd(f[0], f[1]), f[2]);
+      sc->slope = f[3];
     }
+    if (step > 0) {
+      src->tl[0] = f[4];
+      src->tl[1] = f[5];
+    }
+    sc->fin_blocks = 0;
+    sc->step_blocks = 0;
+    sc->cnt_pending = 0;
+  }
+  __syncthreads();
+  // what the host reads: the scalar block, the ring's counters, the slopes
+  // (t is host-owned; it is copied to the device by the solver)
+  constexpr int kSc = (int)(sizeof(EvalScalars) / 8);
+  constexpr int kH = (int)(offsetof(HistState, order) / 8);
+  static_assert(sizeof(EvalScalars) % 8 == 0 && offsetof(HistState, order) % 8 == 0, "8-byte words");
+  const unsigned long long* a = reinterpret_cast<const unsigned long long*>(src);
+  volatile unsigned long long* b = reinterpret_cast<volatile unsigned long long*>(host_dst);
+  constexpr int kHOff = (int)(offsetof(DevSync, h) / 8), kTlOff = (int)(offsetof(DevSync, tl) / 8);
+  const int i = threadIdx.x;
+  if (i < kSc) b[i] = a[i];
+  else if (i < kSc + kH) b[kHOff + i - kSc] = a[kHOff + i - kSc];
+  else if (i < kSc + kH + 2) b[kTlOff + i - kSc - kH] = a[kTlOff + i - kSc - kH];
+  __syncthreads();
+  PHASE_MARK(12);
+  if (threadIdx.x == 0) {  // one system-scope fence (cumulative over the CTA's writes)
+    const unsigned long long c = *dev_count + 1;
+    *dev_count = c;
+    __threadfence_system();
+    PHASE_MARK(13);
+    *reinterpret_cast<volatile unsigned long long*>(host_flag) = c;
   }
 }
 
-void launch_pair(const double* xt, const double* x, const double* g, const double* gt, double* S,
-                 double* Y, int64_t stride, HistState* h, int64_t dim, double* partials,
-                 int nblocks, EvalScalars* sc, cudaStream_t s) {
-  k_pair<<<nblocks, 256, 0, s>>>(xt, x, g, gt, S, Y, stride, h, dim, partials, sc);
+void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_count,
+                    unsigned long long* host_flag, const double* fin_partials,
+                    const double* step_partials, unsigned long long* cnt_slots, cudaStream_t s) {
+  k_publish<<<1, 256, 0, s>>>(src, host_dst, dev_count, host_flag, fin_partials, step_partials,
+                              cnt_slots);
 }
 
-// Clear the history (lbfgs.hpp:102-104, :128-130).
 __global__ void k_hist_reset(HistState* h, int mem) {
   h->k = 0;
   h->mem = mem;
@@ -360,260 +190,464 @@ void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, 
   k_absmax<<<nblocks, 256, 0, s>>>(a, dim, partials, sc, slot);
 }
 
-}  // namespace gsot
 
-// ============================================================ compact L-BFGS
-namespace gsot {
-
+// ============================================================ fused L-BFGS step
+// One cooperative launch (one CTA per SM) does the whole direction update:
+//   (1) each CTA owns a slice of the vectors; one warp per history row
+//       computes s_i.y_new, y_i.y_new, s_i.g, y_i.g, and one warp the new
+//       pair s = x - x_prev, y = g_prev - g (written into the scratch slot)
+//       with s.y, s.s, y.y, s.g, y.g;            -- grid barrier --
+//   (2) CTA 0 folds the per-CTA partials in CTA order, applies the
+//       acceptance test and ring update (lbfgs.hpp:243-255), maintains R and
+//       YY and solves for p, gam w (warp 0, lanes own rows); -- grid barrier --
+//   (3) every CTA forms its slice of d and of the first trial point x + t d
+//       (lbfgs.hpp:86) and the slopes g.d, d.d;  -- grid barrier --
+//   (4) CTA 0 folds the slope partials.
 namespace {
-constexpr int kSlices = 16;  // dim slices per history row in the prepare pass
+constexpr int kStepThreads = 512;
+constexpr int kStepWarps = kStepThreads / 32;
+constexpr int kStepBatch = 8;  // elements per lane per load batch (phase 1)
+int g_step_grid = 0;
+size_t g_step_smem = 0;
+}  // namespace
+
+struct StepArgs {
+  int pair;
+  const double *x, *xprev, *g, *gprev;  // accepted point and the previous one
+  double *S, *Y;
+  int64_t stride;
+  HistState* h;
+  CompactState* cs;
+  double* d;
+  const double* t;  // line-search step (device)
+  double* xt;       // first trial point, or null
+  int64_t dim;
+  double* out;      // [0] g.d, [1] d.d
+  EvalScalars* sc;
+  double* part;     // [kStepMaxGrid][2] slope partials, then [grid][KS * 5] dot partials
+  int ks;           // memory + 1: leading dimension of R / YY in shared memory
+};
+
+
+// CTA-wide: out[v] = sum over c in [0, nc) of part[c * ld + v], v < nv.
+// Eight threads per value each sum a contiguous run of CTAs (all loads in
+// flight), then a fixed xor tree over the eight: deterministic.
+__device__ __forceinline__ void grid_fold(const double* part, int nc, int ld, int nv,
+                                          double* out) {
+  const int sub = threadIdx.x & 7;
+  const int run = (nc + 7) / 8;
+  for (int v0 = 0; v0 < nv; v0 += kStepThreads / 8) {
+    const int v = v0 + (threadIdx.x >> 3);
+    double s = 0.0;
+    if (v < nv) {
+      const int c0 = sub * run, c1 = min(nc, c0 + run);
+      for (int cb = c0; cb < c1; cb += 16) {
+        double q[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) q[u] = cb + u < c1 ? __ldcg(part + (int64_t)(cb + u) * ld + v) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (cb + u < c1) s = dadd(s, q[u]);
+      }
+    }
+    s = dadd(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = dadd(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    s = dadd(s, __shfl_xor_sync(0xffffffffu, s, 4));
+    if (v < nv && sub == 0) out[v] = s;
+  }
 }
 
-// Multi-dot pass. Row i < k: history pair i (logical) against the new pair
-// and the new gradient: s_i.y, y_i.y, s_i.gn, y_i.gn. Row k (pair != 0):
-// the new pair itself, written to the scratch slot: s.y, s.s, y.y, s.gn,
-// y.gn. Rows beyond are idle (the grid is sized for mem + 1 rows so that a
-// captured graph never changes). The last block reduces the partials in
-// slice order, applies the acceptance test and ring update, maintains R and
-// YY by logical position, and solves for the direction coefficients.
-__global__ void __launch_bounds__(256) k_compact_prepare(
-    int pair, const double* __restrict__ xt, const double* __restrict__ x,
-    const double* __restrict__ gt, const double* __restrict__ g, const double* __restrict__ gn,
-    double* __restrict__ S, double* __restrict__ Y, int64_t stride, HistState* h,
-    CompactState* cs, int64_t dim, double* __restrict__ partials, EvalScalars* sc) {
-  __shared__ double sh[8][5];
-  __shared__ bool last;
-  const int k = h->k;  // every block reads before the last block updates
-  const int scratch = h->scratch;
-  const int row = blockIdx.y;
-  const int nrows = gridDim.y;
-  const int64_t per = (dim + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = blockIdx.x * per, hi = min(dim, lo + per);
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  if (row < k) {
-    const double* __restrict__ si = S + h->order[row] * stride;
-    const double* __restrict__ yi = Y + h->order[row] * stride;
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-      const double s = si[e], y = yi[e], gg = gn[e];
-      if (pair) {
-        const double yn = dsub(g[e], gt[e]);
-        acc[0] = dadd(acc[0], dmul(s, yn));
-        acc[1] = dadd(acc[1], dmul(y, yn));
-      }
-      acc[2] = dadd(acc[2], dmul(s, gg));
-      acc[3] = dadd(acc[3], dmul(y, gg));
-    }
-  } else if (row == k && pair) {
-    double* __restrict__ sv = S + scratch * stride;
-    double* __restrict__ yv = Y + scratch * stride;
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-      const double s = dsub(xt[e], x[e]);
-      const double y = dsub(g[e], gt[e]);
-      sv[e] = s;
-      yv[e] = y;
-      const double gg = gn[e];
-      acc[0] = dadd(acc[0], dmul(s, y));
-      acc[1] = dadd(acc[1], dmul(s, s));
-      acc[2] = dadd(acc[2], dmul(y, y));
-      acc[3] = dadd(acc[3], dmul(s, gg));
-      acc[4] = dadd(acc[4], dmul(y, gg));
-    }
-  }
-  // fixed-tree block reduction of the 5 accumulators
+__global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
+  cg::grid_group grid = cg::this_grid();
+#ifdef GSOT_PHASE_CLOCKS
+  long long clk_prev = clock64();
+#endif
+  const int nc = (int)gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    double v = acc[q];
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) sh[warp][q] = v;
+  const int KS = A.ks;
+  const int ld = KS * 5;
+  __shared__ double warp_sh[2 * kStepWarps];
+  __shared__ const double* sp[kMaxMemory + 1];
+  __shared__ const double* yp[kMaxMemory + 1];
+  // slices: multiples of 32 elements so that lanes stay aligned
+  const int64_t per = ((A.dim + nc - 1) / nc + 31) / 32 * 32;
+  const int64_t lo = min(A.dim, blockIdx.x * per), hi = min(A.dim, lo + per);
+  const int k = A.h->k;  // read by every CTA before CTA 0 rewrites the ring
+  const int scratch = A.h->scratch;
+  // the step: one read per CTA, issued now, stored after phase 1
+  __shared__ double t_sh;
+  double t_reg = 0.0;
+  if (threadIdx.x == 32 && A.xt) t_reg = *A.t;
+  if (threadIdx.x < k) {
+    sp[threadIdx.x] = A.S + A.h->order[threadIdx.x] * A.stride;
+    yp[threadIdx.x] = A.Y + A.h->order[threadIdx.x] * A.stride;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const int64_t base = ((int64_t)row * gridDim.x + blockIdx.x) * 5;
-    for (int q = 0; q < 5; ++q) {
-      double v = sh[0][q];
-      for (int w = 1; w < 8; ++w) v = dadd(v, sh[w][q]);
-      partials[base + q] = v;
-    }
-    __threadfence();
-    last = atomicAdd(&sc->ticket, 1u) == gridDim.x * gridDim.y - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // reduce each (row, q) over the slices in slice order (one thread each)
-  __shared__ double red[(kMaxMemory + 1) * 5];
-  for (int t = threadIdx.x; t < nrows * 5; t += blockDim.x) {
-    const int r = t / 5, q = t % 5;
-    double pv[kSlices];  // all loads first, then the slice-ordered sum
+  // (1) one warp per row, lanes striding the slice kStepBatch elements at a time
+  const int nrows = k + (A.pair ? 1 : 0);
+  for (int r = warp; r < nrows; r += kStepWarps) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (r == k) {  // the new pair, written into the scratch slot
+      double* __restrict__ sv = A.S + scratch * A.stride;
+      double* __restrict__ yv = A.Y + scratch * A.stride;
+      for (int64_t e0 = lo + lane; e0 < hi; e0 += 32 * kStepBatch) {
+        double xs[kStepBatch], xp[kStepBatch], gs[kStepBatch], gp[kStepBatch];
 #pragma unroll
-    for (int b = 0; b < kSlices; ++b) pv[b] = __ldcg(partials + ((int64_t)r * kSlices + b) * 5 + q);
-    double v = 0.0;
+        for (int u = 0; u < kStepBatch; ++u) {
+          const int64_t e = e0 + 32 * u;
+          const bool in = e < hi;
+          xs[u] = in ? A.x[e] : 0.0;
+          xp[u] = in ? A.xprev[e] : 0.0;
+          gs[u] = in ? A.g[e] : 0.0;
+          gp[u] = in ? A.gprev[e] : 0.0;
+        }
 #pragma unroll
-    for (int b = 0; b < kSlices; ++b) v = dadd(v, pv[b]);
-    red[t] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  sc->ticket = 0u;
-  int kk = k;
-  double u[kMaxMemory + 1], vv[kMaxMemory + 1];
-  for (int i = 0; i < k; ++i) {
-    u[i] = red[i * 5 + 2];
-    vv[i] = red[i * 5 + 3];
-  }
-  if (pair) {
-    const double sy = red[k * 5 + 0], ss = red[k * 5 + 1], yy = red[k * 5 + 2];
-    sc->extra[0] = sy;
-    sc->extra[1] = ss;
-    sc->extra[2] = yy;
-    h->last_sy = sy;
-    h->last_ss = ss;
-    h->last_yy = yy;
-    const bool accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);  // lbfgs.hpp:246
-    h->accepted = accept ? 1 : 0;
-    if (accept) {
-      double sy_new[kMaxMemory], yy_new[kMaxMemory];
-      for (int i = 0; i < k; ++i) {
-        sy_new[i] = red[i * 5 + 0];  // s_i . y_new
-        yy_new[i] = red[i * 5 + 1];  // y_i . y_new
+        for (int u = 0; u < kStepBatch; ++u) {
+          const int64_t e = e0 + 32 * u;
+          if (e >= hi) break;
+          const double s = dsub(xs[u], xp[u]), y = dsub(gp[u], gs[u]);
+          sv[e] = s;
+          yv[e] = y;
+          acc[0] = dadd(acc[0], dmul(s, y));
+          acc[1] = dadd(acc[1], dmul(s, s));
+          acc[2] = dadd(acc[2], dmul(y, y));
+          acc[3] = dadd(acc[3], dmul(s, gs[u]));
+          acc[4] = dadd(acc[4], dmul(y, gs[u]));
+        }
       }
-      int first = 0;
-      if (k == h->mem) {  // evict the oldest (lbfgs.hpp:247-251)
-        first = 1;
-        const int ev = h->order[0];
-        for (int i = 1; i < k; ++i) {
-          h->order[i - 1] = h->order[i];
-          h->rho[i - 1] = h->rho[i];
-          h->sy[i - 1] = h->sy[i];
-          h->yy[i - 1] = h->yy[i];
-          for (int j = 1; j < k; ++j) {
-            cs->R[(i - 1) * kMaxMemory + (j - 1)] = cs->R[i * kMaxMemory + j];
-            cs->YY[(i - 1) * kMaxMemory + (j - 1)] = cs->YY[i * kMaxMemory + j];
+    } else {  // history row r: s_r.y_new, y_r.y_new, s_r.g, y_r.g
+      const double* __restrict__ si = sp[r];
+      const double* __restrict__ yi = yp[r];
+      for (int64_t e0 = lo + lane; e0 < hi; e0 += 32 * kStepBatch) {
+        double ss[kStepBatch], ys[kStepBatch], gs[kStepBatch], gp[kStepBatch];
+#pragma unroll
+        for (int u = 0; u < kStepBatch; ++u) {
+          const int64_t e = e0 + 32 * u;
+          const bool in = e < hi;
+          ss[u] = in ? si[e] : 0.0;
+          ys[u] = in ? yi[e] : 0.0;
+          gs[u] = in ? A.g[e] : 0.0;
+          gp[u] = (in && A.pair) ? A.gprev[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kStepBatch; ++u) {
+          const int64_t e = e0 + 32 * u;
+          if (e >= hi) break;
+          if (A.pair) {
+            const double yn = dsub(gp[u], gs[u]);
+            acc[0] = dadd(acc[0], dmul(ss[u], yn));
+            acc[1] = dadd(acc[1], dmul(ys[u], yn));
           }
+          acc[2] = dadd(acc[2], dmul(ss[u], gs[u]));
+          acc[3] = dadd(acc[3], dmul(ys[u], gs[u]));
         }
-        kk = k - 1;
-        h->order[kk] = scratch;
-        h->scratch = ev;
-      } else {
-        h->order[k] = scratch;
-        int next = 0;
-        for (;; ++next) {
-          bool used = false;
-          for (int i = 0; i <= k; ++i) used |= h->order[i] == next;
-          if (!used) break;
-        }
-        h->scratch = next;
       }
-      for (int i = 0; i < kk; ++i) {  // shift u, v and the new column
-        u[i] = u[i + first];
-        vv[i] = vv[i + first];
-        cs->R[i * kMaxMemory + kk] = sy_new[i + first];
-        cs->YY[i * kMaxMemory + kk] = yy_new[i + first];
-        cs->YY[kk * kMaxMemory + i] = yy_new[i + first];
-      }
-      cs->R[kk * kMaxMemory + kk] = sy;
-      cs->YY[kk * kMaxMemory + kk] = yy;
-      u[kk] = red[k * 5 + 3];
-      vv[kk] = red[k * 5 + 4];
-      h->rho[kk] = 1.0 / sy;
-      h->sy[kk] = sy;
-      h->yy[kk] = yy;
-      kk += 1;
-      h->k = kk;
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      double v = acc[q];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) A.part[2 * kStepMaxGrid + (int64_t)blockIdx.x * ld + r * 5 + q] = v;
     }
   }
-  // gam (lbfgs.hpp:116-119), then w = R^-1 u, z = (D + gam YY) w - gam v,
-  // p = R^-T z; d = gam g + S p - gam Y w.
-  double gam = 1.0;
-  if (kk > 0 && h->yy[kk - 1] > 0.0) gam = h->sy[kk - 1] / h->yy[kk - 1];
-  double w[kMaxMemory], p[kMaxMemory];
-  for (int i = kk - 1; i >= 0; --i) {
-    double t = u[i];
-    for (int j = i + 1; j < kk; ++j) t -= cs->R[i * kMaxMemory + j] * w[j];
-    w[i] = t / cs->R[i * kMaxMemory + i];
+  if (threadIdx.x == 32) t_sh = t_reg;
+  PHASE_MARK(0);
+  grid.sync();
+  PHASE_MARK(1);
+  // (2) CTA 0: fold, ring update, R / YY maintenance, compact solve
+  if (blockIdx.x == 0) {
+    extern __shared__ double step_dyn[];  // R, YY: KS x KS each
+    double* R = step_dyn;
+    double* YY = R + KS * KS;
+    __shared__ double red[(kMaxMemory + 1) * 5];
+    __shared__ double uu[kMaxMemory + 1], vv[kMaxMemory + 1];
+    __shared__ HistState hs;
+    __shared__ int fl[3];  // accepted, evicted-first, count after
+    grid_fold(A.part + 2 * kStepMaxGrid, nc, ld, nrows * 5, red);
+    for (int t = threadIdx.x; t < (int)(sizeof(HistState) / sizeof(int)); t += blockDim.x)
+      reinterpret_cast<int*>(&hs)[t] = reinterpret_cast<const int*>(A.h)[t];
+    for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
+      const int i = t / k, jj = t % k;
+      R[i * KS + jj] = A.cs->R[i * kMaxMemory + jj];
+      YY[i * KS + jj] = A.cs->YY[i * kMaxMemory + jj];
+    }
+    __syncthreads();
+    PHASE_MARK(2);
+    if (threadIdx.x == 0) {
+      int accept = 0, first = 0, kk = k;
+      if (A.pair) {
+        const double sy = red[k * 5 + 0], ss = red[k * 5 + 1], yy = red[k * 5 + 2];
+        A.sc->extra[0] = sy;
+        A.sc->extra[1] = ss;
+        A.sc->extra[2] = yy;
+        hs.last_sy = sy;
+        hs.last_ss = ss;
+        hs.last_yy = yy;
+        accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);  // lbfgs.hpp:246
+        hs.accepted = accept;
+        if (accept) {
+          if (k == hs.mem) {  // evict the oldest (lbfgs.hpp:247-251)
+            first = 1;
+            const int ev = hs.order[0];
+            for (int i = 1; i < k; ++i) {
+              hs.order[i - 1] = hs.order[i];
+              hs.rho[i - 1] = hs.rho[i];
+              hs.sy[i - 1] = hs.sy[i];
+              hs.yy[i - 1] = hs.yy[i];
+            }
+            hs.order[k - 1] = scratch;
+            hs.scratch = ev;
+          } else {
+            hs.order[k] = scratch;
+            int next = 0;
+            for (;; ++next) {
+              bool used = false;
+              for (int i = 0; i <= k; ++i) used |= hs.order[i] == next;
+              if (!used) break;
+            }
+            hs.scratch = next;
+          }
+          kk = k - first;
+          hs.rho[kk] = 1.0 / sy;
+          hs.sy[kk] = sy;
+          hs.yy[kk] = yy;
+          hs.k = kk + 1;
+        }
+      }
+      fl[0] = accept;
+      fl[1] = first;
+      fl[2] = accept ? kk + 1 : k;
+    }
+    __syncthreads();
+    PHASE_MARK(3);
+    const int accept = fl[0], first = fl[1], kn = fl[2];
+    if (accept && first) {  // shift R and YY up-left by one
+      const int n1 = k - 1;
+      double tr[8], ty[8];
+      int c = 0;
+      for (int t = threadIdx.x; t < n1 * n1; t += blockDim.x, ++c) {
+        const int i = t / n1 + 1, jj = t % n1 + 1;
+        tr[c] = R[i * KS + jj];
+        ty[c] = YY[i * KS + jj];
+      }
+      __syncthreads();
+      c = 0;
+      for (int t = threadIdx.x; t < n1 * n1; t += blockDim.x, ++c) {
+        const int i = t / n1, jj = t % n1;
+        R[i * KS + jj] = tr[c];
+        YY[i * KS + jj] = ty[c];
+      }
+    }
+    __syncthreads();
+    const int c0 = kn - 1;  // logical position of the new pair
+    for (int i = threadIdx.x; i < kn; i += blockDim.x) {
+      const int src = accept ? (i < c0 ? i + first : k) : i;
+      const bool nw = accept && i == c0;
+      uu[i] = red[src * 5 + (nw ? 3 : 2)];  // s_i . g
+      vv[i] = red[src * 5 + (nw ? 4 : 3)];  // y_i . g
+      if (accept && i < c0) {
+        R[i * KS + c0] = red[src * 5 + 0];   // s_i . y_new
+        YY[i * KS + c0] = red[src * 5 + 1];  // y_i . y_new
+        YY[c0 * KS + i] = red[src * 5 + 1];
+      }
+      if (nw) {
+        R[c0 * KS + c0] = hs.sy[c0];
+        YY[c0 * KS + c0] = hs.yy[c0];
+      }
+    }
+    __syncthreads();
+    PHASE_MARK(4);
+    if (warp == 0) {
+      // gam (lbfgs.hpp:116-119); w = R^-1 u, z = (D + gam YY) w - gam v,
+      // p = R^-T z. Lane i owns row i; substitutions are column oriented
+      // (one broadcast per step), diagonal reciprocals computed up front.
+      double gam = 1.0;
+      if (kn > 0 && hs.yy[kn - 1] > 0.0) gam = hs.sy[kn - 1] / hs.yy[kn - 1];
+      if (kn <= 32) {
+        const bool act = lane < kn;
+        const double rii = act ? R[lane * KS + lane] : 1.0;
+        const double rinv = 1.0 / rii;
+        double tv = act ? uu[lane] : 0.0;
+        double wl = 0.0;
+        for (int i = kn - 1; i >= 0; --i) {
+          const double wi = __shfl_sync(0xffffffffu, dmul(tv, rinv), i);
+          if (lane == i) wl = wi;
+          if (lane < i) tv = dsub(tv, dmul(R[lane * KS + i], wi));
+        }
+        double z = act ? dsub(dmul(rii, wl), dmul(gam, vv[lane])) : 0.0;
+        for (int j = 0; j < kn; ++j) {
+          const double wj = __shfl_sync(0xffffffffu, wl, j);
+          if (act) z = dadd(z, dmul(dmul(gam, YY[lane * KS + j]), wj));
+        }
+        double pl = 0.0;
+        for (int j = 0; j < kn; ++j) {
+          const double pj = __shfl_sync(0xffffffffu, dmul(z, rinv), j);
+          if (lane == j) pl = pj;
+          if (act && lane > j) z = dsub(z, dmul(R[j * KS + lane], pj));
+        }
+        if (act) {
+          A.cs->p[lane] = pl;
+          A.cs->w[lane] = dmul(gam, wl);
+        }
+      } else {  // long memories: the same substitutions through shared memory
+        __shared__ double tv[kMaxMemory + 1], wv[kMaxMemory + 1], pv[kMaxMemory + 1];
+        for (int i = lane; i < kn; i += 32) tv[i] = uu[i];
+        __syncwarp();
+        for (int i = kn - 1; i >= 0; --i) {
+          const double wi = dmul(tv[i], 1.0 / R[i * KS + i]);
+          __syncwarp();
+          if (lane == 0) wv[i] = wi;
+          for (int j = lane; j < i; j += 32) tv[j] = dsub(tv[j], dmul(R[j * KS + i], wi));
+          __syncwarp();
+        }
+        for (int i = lane; i < kn; i += 32) {
+          double z = dsub(dmul(R[i * KS + i], wv[i]), dmul(gam, vv[i]));
+          for (int j = 0; j < kn; ++j) z = dadd(z, dmul(dmul(gam, YY[i * KS + j]), wv[j]));
+          tv[i] = z;
+        }
+        __syncwarp();
+        for (int j = 0; j < kn; ++j) {
+          const double pj = dmul(tv[j], 1.0 / R[j * KS + j]);
+          __syncwarp();
+          if (lane == 0) pv[j] = pj;
+          for (int i = j + 1 + lane; i < kn; i += 32) tv[i] = dsub(tv[i], dmul(R[j * KS + i], pj));
+          __syncwarp();
+        }
+        for (int i = lane; i < kn; i += 32) {
+          A.cs->p[i] = pv[i];
+          A.cs->w[i] = dmul(gam, wv[i]);
+        }
+      }
+      if (lane == 0) {
+        A.cs->gam = gam;
+        A.cs->k = kn;
+      }
+    }
+    for (int t = threadIdx.x; t < (int)(sizeof(HistState) / sizeof(int)); t += blockDim.x)
+      reinterpret_cast<int*>(A.h)[t] = reinterpret_cast<const int*>(&hs)[t];
+    for (int t = threadIdx.x; t < kn * kn; t += blockDim.x) {  // R, YY back
+      const int i = t / kn, jj = t % kn;
+      A.cs->R[i * kMaxMemory + jj] = R[i * KS + jj];
+      A.cs->YY[i * kMaxMemory + jj] = YY[i * KS + jj];
+    }
+    PHASE_MARK(5);
   }
-  for (int i = 0; i < kk; ++i) {
-    double t = cs->R[i * kMaxMemory + i] * w[i] - gam * vv[i];
-    for (int j = 0; j < kk; ++j) t += gam * cs->YY[i * kMaxMemory + j] * w[j];
-    for (int j = 0; j < i; ++j) t -= cs->R[j * kMaxMemory + i] * p[j];
-    p[i] = t / cs->R[i * kMaxMemory + i];
-  }
-  for (int i = 0; i < kk; ++i) {
-    cs->p[i] = p[i];
-    cs->w[i] = gam * w[i];
-    cs->u[i] = u[i];
-    cs->v[i] = vv[i];
-  }
-  cs->gam = gam;
-  cs->k = kk;
-}
-
-void launch_compact_prepare(int pair, const double* xt, const double* x, const double* gt,
-                            const double* g, const double* gn, double* S, double* Y,
-                            int64_t stride, HistState* h, CompactState* cs, int mem, int64_t dim,
-                            double* partials, EvalScalars* sc, cudaStream_t s) {
-  // rows: the history capacity + 1, static so that captured graphs never change
-  dim3 grid(kSlices, (unsigned)(mem + 1));
-  k_compact_prepare<<<grid, 256, 0, s>>>(pair, xt, x, gt, g, gn, S, Y, stride, h, cs, dim,
-                                         partials, sc);
-}
-
-// d = gam g + sum_i p_i s_i - sum_i w_i y_i (per element, i ascending), the
-// slopes g.d and d.d, and the first trial point x + t d.
-__global__ void __launch_bounds__(256) k_compact_direction(
-    const double* __restrict__ g, const double* __restrict__ S, const double* __restrict__ Y,
-    int64_t stride, const HistState* __restrict__ h, const CompactState* __restrict__ cs,
-    double* __restrict__ d, const double* __restrict__ x, const double* __restrict__ tp,
-    double* __restrict__ xt, int64_t dim, double* __restrict__ partials, EvalScalars* sc,
-    double* __restrict__ out) {
-  __shared__ const double* sp[kMaxMemory];
-  __shared__ const double* yp[kMaxMemory];
-  __shared__ double pc[kMaxMemory], wc[kMaxMemory];
-  __shared__ int ks;
-  __shared__ double gs;
-  if (threadIdx.x == 0) {
-    ks = cs->k;
-    gs = cs->gam;
-  }
+  grid.sync();
+  PHASE_MARK(6);
+  // (3) direction slice: all 2 x 16 history loads of an element in flight
+  __shared__ double lc[2 * kMaxMemory + 2];
+  __shared__ int kn_sh;
+  if (threadIdx.x == 0) kn_sh = __ldcg(&A.cs->k);
   __syncthreads();
-  const int k = ks;
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    sp[i] = S + h->order[i] * stride;
-    yp[i] = Y + h->order[i] * stride;
-    pc[i] = cs->p[i];
-    wc[i] = cs->w[i];
+  const int kk = kn_sh;
+  for (int t = threadIdx.x; t < kk; t += blockDim.x) {
+    lc[t] = __ldcg(&A.cs->p[t]);
+    lc[kMaxMemory + t] = __ldcg(&A.cs->w[t]);
+    const int slot = __ldcg(&A.h->order[t]);
+    sp[t] = A.S + slot * A.stride;
+    yp[t] = A.Y + slot * A.stride;
   }
+  if (threadIdx.x == 0) lc[2 * kMaxMemory] = __ldcg(&A.cs->gam);
   __syncthreads();
-  const double gam = gs;
-  const double t = xt ? *tp : 0.0;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const double ge = g[e];
+  PHASE_MARK(7);
+  const double gam = lc[2 * kMaxMemory];
+  const double t = t_sh;
+  double pg = 0.0, pd = 0.0;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += kStepThreads) {
+    const double ge = A.g[e];
+    const double xe = A.xt ? A.x[e] : 0.0;
     double de = dmul(gam, ge);
-    for (int i = 0; i < k; ++i) de = dadd(de, dmul(pc[i], sp[i][e]));
-    for (int i = 0; i < k; ++i) de = dsub(de, dmul(wc[i], yp[i][e]));
-    d[e] = de;
-    if (xt) xt[e] = dadd(x[e], dmul(t, de));  // lbfgs.hpp:86
-    acc[0] = dadd(acc[0], dmul(ge, de));
-    acc[1] = dadd(acc[1], dmul(de, de));
+    for (int i0 = 0; i0 < kk; i0 += 16) {
+      double vs[16], vy[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        vs[u] = i0 + u < kk ? __ldcg(sp[i0 + u] + e) : 0.0;
+        vy[u] = i0 + u < kk ? __ldcg(yp[i0 + u] + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (i0 + u < kk) de = dadd(de, dmul(lc[i0 + u], vs[u]));
+      if (i0 + 16 >= kk) {  // the y terms after every s term (fixed order)
+        for (int j0 = 0; j0 < i0; j0 += 16)
+          for (int u = 0; u < 16; ++u)
+            if (j0 + u < kk) de = dsub(de, dmul(lc[kMaxMemory + j0 + u], __ldcg(yp[j0 + u] + e)));
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (i0 + u < kk) de = dsub(de, dmul(lc[kMaxMemory + i0 + u], vy[u]));
+      }
+    }
+    A.d[e] = de;
+    if (A.xt) A.xt[e] = dadd(xe, dmul(t, de));  // lbfgs.hpp:86
+    pg = dadd(pg, dmul(ge, de));
+    pd = dadd(pd, dmul(de, de));
   }
-  double r[2];
-  if (last_block_reduce<256, 2>(acc, partials, &sc->ticket, r)) {
-    out[0] = r[0];
-    out[1] = r[1];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    pg = dadd(pg, __shfl_xor_sync(0xffffffffu, pg, o));
+    pd = dadd(pd, __shfl_xor_sync(0xffffffffu, pd, o));
   }
+  if (lane == 0) {
+    warp_sh[warp] = pg;
+    warp_sh[kStepWarps + warp] = pd;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {  // CTA partial; k_publish folds them (fixed order)
+    double v = warp_sh[threadIdx.x * kStepWarps];
+    for (int w = 1; w < kStepWarps; ++w) v = dadd(v, warp_sh[threadIdx.x * kStepWarps + w]);
+    A.part[blockIdx.x * 2 + threadIdx.x] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->step_blocks = nc;
+  PHASE_MARK(10);
 }
 
-void launch_compact_direction(const double* g, const double* S, const double* Y, int64_t stride,
-                              const HistState* h, const CompactState* cs, double* d,
-                              const double* x, const double* t, double* xt_out, int64_t dim,
-                              double* partials, EvalScalars* sc, double* out, int nblocks,
-                              cudaStream_t s) {
-  k_compact_direction<<<nblocks, 256, 0, s>>>(g, S, Y, stride, h, cs, d, x, t, xt_out, dim,
-                                              partials, sc, out);
+#ifdef GSOT_PHASE_CLOCKS
+extern "C" __attribute__((visibility("default"))) int gsot_debug_phase_clocks(unsigned long long* out,
+                                                                               int n) {
+  if (out) cudaMemcpyFromSymbol(out, g_phase_clk, sizeof(unsigned long long) * (n < 16 ? n : 16));
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z));
+  return 0;
+}
+#endif
+
+// One CTA per SM (the kernel needs all 64K registers of an SM per CTA).
+int lbfgs_step_grid() {
+  if (g_step_grid == 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_step_grid = std::max(1, std::min(sms, kStepMaxGrid));
+  }
+  return g_step_grid;
+}
+
+size_t lbfgs_step_partials(int mem) {
+  return (size_t)kStepMaxGrid * ((size_t)(mem + 1) * 5 + 2);
+}
+
+void launch_lbfgs_step(int pair, const double* x, const double* xprev, const double* g,
+                       const double* gprev, double* S, double* Y, int64_t stride, HistState* h,
+                       CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
+                       double* out, EvalScalars* sc, double* part, int mem, cudaStream_t s) {
+  const int grid = lbfgs_step_grid();
+  StepArgs A{pair, x, xprev, g, gprev, S, Y, stride, h, cs, d, t, xt, dim, out, sc, part, mem + 1};
+  const size_t smem = sizeof(double) * 2 * (size_t)(mem + 1) * (mem + 1);
+  if (smem > 48 * 1024 && smem > g_step_smem) {
+    cudaFuncSetAttribute(k_lbfgs_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    g_step_smem = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_lbfgs_step, A);
 }
 
 }  // namespace gsot

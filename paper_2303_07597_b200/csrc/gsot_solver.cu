@@ -13,6 +13,8 @@
 // captured once per context and replayed (the line-search step t and the
 // pair history live in device memory, so the graphs never change). Audit
 // mode runs the same sequences eagerly and re-verifies every evaluation.
+#include <cstdio>
+#include <cstdlib>
 #include <math.h>
 #include <string.h>
 
@@ -53,7 +55,19 @@ class Solver {
            (exact_ ? "/exact" : "");
   }
 
+  ~Solver() {
+    if (diag_) {
+      cudaEventDestroy(diag_ev_[0]);
+      cudaEventDestroy(diag_ev_[1]);
+    }
+  }
+
   void run(double* x_out) {
+    if (std::getenv("GSOT_DIAG_SEQ") && graphs_) {
+      diag_ = true;
+      GSOT_CUDA_CHECK(cudaEventCreate(&diag_ev_[0]));
+      GSOT_CUDA_CHECK(cudaEventCreate(&diag_ev_[1]));
+    }
     const int64_t dim = w_->dim;
     r_ = 0;
     GSOT_CUDA_CHECK(cudaMemsetAsync(w_->X[0], 0, sizeof(double) * dim, c_->stream));
@@ -70,6 +84,10 @@ class Solver {
     const auto t0 = std::chrono::steady_clock::now();
     maximize();
     const auto t1 = std::chrono::steady_clock::now();
+    if (diag_)
+      std::fprintf(stderr, "[gsot diag] sequences %ld  device %.1f us/seq  host round trip %.1f us/seq\n",
+                   (long)diag_n_, 1e6 * diag_dev_ / std::max<int64_t>(1, diag_n_),
+                   1e6 * diag_host_ / std::max<int64_t>(1, diag_n_));
     res_->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
     if (x_out)
       GSOT_CUDA_CHECK(cudaMemcpyAsync(x_out, w_->X[r_], sizeof(double) * dim,
@@ -82,6 +100,11 @@ class Solver {
   }
 
  private:
+  bool diag_ = false;
+  cudaEvent_t diag_ev_[2] = {nullptr, nullptr};
+  double diag_dev_ = 0.0, diag_host_ = 0.0;
+  int64_t diag_n_ = 0;
+
   void ensure_workspace() {
     const int64_t dim = c_->m + c_->n;
     const int mem = std::max(1, o_.lbfgs_memory);
@@ -103,7 +126,7 @@ class Solver {
     ws->S = dalloc<double>(static_cast<size_t>(mem + 1) * dim, t);
     ws->Y = dalloc<double>(static_cast<size_t>(mem + 1) * dim, t);
     ws->cs = dalloc<CompactState>(1, t);
-    ws->cpart = dalloc<double>(static_cast<size_t>(mem + 2) * 64 * 5, t);
+    ws->cpart = dalloc<double>(lbfgs_step_partials(mem), t);
   }
 
   // ---- device sequences ----------------------------------------------------
@@ -114,6 +137,7 @@ class Solver {
   void run_seq(const char* name, const std::function<void()>& body) {
     if (!graphs_) {
       body();
+      c_->wait_published();
       c_->sync();
       c_->collect_marks();
       return;
@@ -142,16 +166,33 @@ class Solver {
       it = w_->graphs.emplace(key, std::move(sq)).first;
     }
     Sequence& sq = *it->second;
+    if (diag_) GSOT_CUDA_CHECK(cudaEventRecord(diag_ev_[0], c_->stream));
+    const auto h0 = std::chrono::steady_clock::now();
     GSOT_CUDA_CHECK(cudaGraphLaunch(sq.exec, c_->stream));
+    if (diag_) GSOT_CUDA_CHECK(cudaEventRecord(diag_ev_[1], c_->stream));
     c_->launches += sq.kernels;
-    c_->sync();
+    c_->pub_expected += static_cast<unsigned long long>(sq.publishes);
+    if (sq.publishes > 0) c_->wait_published();
+    if (sq.publishes == 0 || !sq.marks.empty()) c_->sync();
+    if (diag_) {  // GSOT_DIAG_SEQ: device time vs host round trip per sequence
+      c_->sync();
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, diag_ev_[0], diag_ev_[1]);
+      diag_dev_ += ms * 1e-3;
+      diag_host_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+      diag_n_ += 1;
+    }
     for (const auto& mk : sq.marks) c_->account(mk);
   }
 
-  void enqueue_t() {  // the line-search step, read by the axpy kernel
+  // The line-search step: the host writes it into the pinned mirror, a copy
+  // node moves it to the device (GPU reads of mapped host memory measured
+  // ~100 us per sequence on the B200 boxes; the copy node costs far less).
+  void enqueue_t() {
     GSOT_CUDA_CHECK(cudaMemcpyAsync(&c_->dsync->t, &c_->h_sync->t, sizeof(double),
                                     cudaMemcpyHostToDevice, c_->stream));
   }
+  const double* t_dev() const { return &c_->dsync->t; }
   void enqueue_two_loop() {  // lbfgs.hpp:109-126
     TwoLoopArgs A;
     A.S = w_->S;
@@ -163,28 +204,21 @@ class Solver {
     A.dim = w_->dim;
     A.out = c_->dsync->tl;
     c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 4.0), [&] {
-      if (exact_)
-        launch_exact_two_loop(A, c_->stream);
-      else
-        launch_two_loop(A, c_->stream);
+      launch_exact_two_loop(A, c_->stream);
     });
   }
   void enqueue_pair() {  // res = X[r] (just accepted), previous res = X[1-r]
     const int q = 1 - r_;
     c_->launch(K_LBFGS, 8.0 * w_->dim * 6.0, [&] {
-      if (exact_)
-        launch_exact_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim,
-                          &c_->dsync->h, w_->dim, c_->sc, c_->stream);
-      else
-        launch_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim,
-                    &c_->dsync->h, w_->dim, c_->partials, c_->red_blocks, c_->sc, c_->stream);
+      launch_exact_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim,
+                        &c_->dsync->h, w_->dim, c_->sc, c_->stream);
     });
   }
   void enqueue_trial() {  // trial = X[r] + t d into X[1-r], evaluated into G[1-r]
     const int q = 1 - r_;
     enqueue_t();
     c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
-      launch_axpy_point(w_->X[r_], &c_->dsync->t, w_->d, w_->X[q], w_->dim, c_->stream);
+      launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->stream);
     });
     enqueue_eval(c_, w_->X[q], mode_eval_, w_->G[q], w_->d, o_.upper_bound_offset, use_active_);
   }
@@ -193,8 +227,7 @@ class Solver {
   // pending curvature pair of the last acceptance (lbfgs.hpp:243-255) and
   // followed by the first trial point x + t d into the trial buffer.
   // Exact mode: the reference's two-loop with sequential dots. Fast mode:
-  // the compact representation (one multi-dot pass with a last-block solve,
-  // one combine pass that also forms the trial point).
+  // the compact representation in one cooperative launch (gsot_lbfgs.cu).
   void enqueue_direction(bool pair, bool trial) {
     const int q = 1 - r_;
     if (exact_) {
@@ -202,19 +235,15 @@ class Solver {
       enqueue_two_loop();
       if (trial)
         c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
-          launch_axpy_point(w_->X[r_], &c_->dsync->t, w_->d, w_->X[q], w_->dim, c_->stream);
+          launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->stream);
         });
       return;
     }
-    c_->launch(K_LBFGS, 8.0 * w_->dim * (2.0 * w_->mem + 6.0), [&] {
-      launch_compact_prepare(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->G[r_],
-                             w_->S, w_->Y, w_->dim, &c_->dsync->h, w_->cs, mem_, w_->dim,
-                             w_->cpart, c_->sc, c_->stream);
-    });
-    c_->launch(K_LBFGS, 8.0 * w_->dim * (2.0 * w_->mem + 4.0), [&] {
-      launch_compact_direction(w_->G[r_], w_->S, w_->Y, w_->dim, &c_->dsync->h, w_->cs, w_->d,
-                               w_->X[r_], &c_->dsync->t, trial ? w_->X[q] : nullptr, w_->dim,
-                               c_->partials, c_->sc, c_->dsync->tl, c_->red_blocks, c_->stream);
+    c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 10.0), [&] {
+      launch_lbfgs_step(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->S, w_->Y,
+                        w_->dim, &c_->dsync->h, w_->cs, w_->d, t_dev(),
+                        trial ? w_->X[q] : nullptr, w_->dim, c_->dsync->tl, c_->sc, w_->cpart, mem_,
+                        c_->stream);
     });
   }
 

@@ -3,5 +3,5 @@
 # second solve of the process): python tests/_gpu_solve_once.py
 TAG=${1:-k}
 python tests/_gpu_solve_once.py > gpurun_out/solve_once_$TAG.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none -s 1700 -c 1300 --csv --log-file gpurun_out/launches_$TAG.csv python tests/_gpu_solve_once.py > gpurun_out/ncu_$TAG.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_$TAG.csv python tests/_gpu_solve_once.py 1 prof > gpurun_out/ncu_$TAG.log 2>&1
 echo DONE $?
