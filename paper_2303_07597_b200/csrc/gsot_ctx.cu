@@ -194,8 +194,8 @@ void alloc_buffers(gsot_ctx* c) {
       static_cast<size_t>(std::max<int64_t>(c->num_sms * 64, L * ((nw + 7) / 8))) * 8, t);
   c->words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dense_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
-  c->dense_tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
-  c->tasks = dalloc<int2>(static_cast<size_t>(L) * nw, t);
+  c->dense_tasks = dalloc<gsot::TaskDesc>(static_cast<size_t>(L) * nw, t);
+  c->tasks = dalloc<gsot::TaskDesc>(static_cast<size_t>(L) * nw, t);
   c->snap_x = dalloc<double>(dim + 8, t);
   c->zs = dalloc<double>(static_cast<size_t>(L) * n, t);
   c->ks = dalloc<double>(static_cast<size_t>(L) * n, t);
@@ -241,38 +241,17 @@ void alloc_buffers(gsot_ctx* c) {
   GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_sqrt_g, sqrt_g.data(), sizeof(double) * L,
                                   cudaMemcpyHostToDevice, c->stream));
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_words(c->dense_words, c->L, c->nw, c->n, c->stream); });
-  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->dense_tasks, c->d_group_order, c->L, c->nw, c->stream); });
-  // Persistent eval grid: staging buffers sized to the tallest group (whole
-  // tile per warp when it fits), then as many blocks per SM as shared
-  // memory allows (the per-block task list shrinks as the grid grows).
+  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->problem(), c->dense_tasks, c->d_group_order, c->stream); });
+  // Persistent eval grid: two shared-memory segments of up to 128 rows per
+  // CTA (the tallest group when it fits), as many CTAs per SM as shared
+  // memory allows (GSOT_EVAL_SEG overrides the segment rows for tuning).
   {
     const int gmax = *std::max_element(c->sizes.begin(), c->sizes.end());
-    const int64_t nchunks = static_cast<int64_t>(c->L) * c->nw;
-    std::vector<int> cands;
-    const char* ev = std::getenv("GSOT_EVAL_BUF");  // tuning override (rows; 0 = streaming)
-    if (ev) {
-      cands.push_back(std::atoi(ev));
-    } else {
-      cands.push_back(0);  // register streaming, highest occupancy
-    }
-    if (gmax <= 104) cands.push_back(std::max(16, gmax));  // whole tile per warp (TMA)
-    for (int b : {96, 64, 32}) cands.push_back(b);         // streamed in two halves
-    c->eval_buf = 32;
-    c->eval_grid = c->num_sms;
-    bool done = false;
-    for (int buf : cands) {
-      for (int bps = 4; bps >= 1 && !done; --bps) {
-        const int64_t grid = static_cast<int64_t>(c->num_sms) * bps;
-        const int cap = static_cast<int>((nchunks + grid - 1) / grid);
-        const size_t smem = gsot::eval_smem_bytes(buf, cap);
-        if (static_cast<size_t>(bps) * (smem + 2048) > 228 * 1024) continue;
-        if (gsot::eval_blocks_per_sm(smem) < bps) continue;
-        c->eval_buf = buf;
-        c->eval_grid = static_cast<int>(grid);
-        done = true;
-      }
-      if (done) break;
-    }
+    int seg = gsot::eval_buf_rows(gmax);
+    if (const char* ev = std::getenv("GSOT_EVAL_SEG")) seg = std::max(8, std::min(128, std::atoi(ev)));
+    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0));
+    c->eval_buf = seg;
+    c->eval_grid = c->num_sms * bps;
   }
   c->sync();
 }

@@ -82,8 +82,8 @@ struct gsot_ctx {
   unsigned long long* cnt_partials = nullptr;  // spare counter partials
   unsigned long long* cnt_slots = nullptr;     // screen counters, 64 x 8
   uint32_t *words = nullptr, *dense_words = nullptr;
-  int2* dense_tasks = nullptr;  // canonical chunk order (largest groups first)
-  int2* tasks = nullptr;        // screened work list (non-empty chunks)
+  gsot::TaskDesc* dense_tasks = nullptr;  // every chunk, largest groups first
+  gsot::TaskDesc* tasks = nullptr;        // screened work list (non-empty chunks)
   // screening state
   double *snap_x = nullptr, *zs = nullptr, *ks = nullptr, *os = nullptr;
   double *dpos = nullptr, *dfull = nullptr, *dneg = nullptr, *dbeta = nullptr;

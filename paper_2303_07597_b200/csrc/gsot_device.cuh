@@ -138,6 +138,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// The same with a suspend-time hint: the waiting warp sleeps in the barrier
+// instead of spinning through issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!done);
+}
 // global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned.
 // The proxy fence orders the warp's earlier generic reads of the buffer
 // before the async-proxy write.
@@ -156,6 +169,12 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
 namespace gsot {
 
 // Fold the 64 counter slots into sc->counters etc. and zero them (one warp).
+// max(f, 0) by bit operations (f finite): a negative f, -0 included, -> +0.
+__device__ __forceinline__ double relu(double f) {
+  const long long b = __double_as_longlong(f);
+  return __longlong_as_double(b & ~(b >> 63));
+}
+
 // Called by exactly one full warp.
 __device__ __forceinline__ void fold_counter_slots(unsigned long long* slots, EvalScalars* sc) {
   const int lane = threadIdx.x & 31;

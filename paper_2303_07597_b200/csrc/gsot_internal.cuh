@@ -83,6 +83,14 @@ struct EvalScalars {
 };
 constexpr size_t kEvalScalarsResetBytes = offsetof(EvalScalars, fin_blocks);
 
+// One evaluation task: block row group l x 32-column chunk c, with what the
+// eval kernel's producer needs to start the tile copy in one 32-byte load.
+struct alignas(16) TaskDesc {
+  int l, c, o0, g;  // group, chunk, first row, rows
+  uint32_t word;    // survivor bits of the chunk's columns
+  int pad[3];
+};
+
 // ---- kernels (gsot_kernels.cu) ---------------------------------------------
 
 // Per-kernel-class counters for gsot_profile_*.
@@ -112,7 +120,7 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 // Counters accumulate into 64 slots x 8 (cnt_slots); the objective kernel
 // folds them into EvalScalars and zeroes the slots.
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
-                   const double* dbeta, double ub_offset, uint32_t* words, int2* tasks,
+                   const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s);
 // Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
@@ -120,7 +128,7 @@ size_t eval_smem_bytes(int buf_rows, int cap);
 int eval_blocks_per_sm(size_t smem);
 // ntasks >= 0: `tasks` holds that many entries (dense list); -1: the
 // screened list, length *ntasks_dev (written by the screen kernel).
-void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int ntasks,
+void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
                  double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
@@ -135,7 +143,7 @@ void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* wo
 void launch_audit_active(const DevProblem& P, const double* x, const uint32_t* active_words,
                          EvalScalars* sc, cudaStream_t s);
 void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaStream_t s);
-void launch_dense_tasks(int2* tasks, const int32_t* group_order, int32_t L, int32_t nw,
+void launch_dense_tasks(const DevProblem& P, TaskDesc* tasks, const int32_t* group_order,
                         cudaStream_t s);
 
 // L-BFGS vector kernels (gsot_lbfgs.cu).

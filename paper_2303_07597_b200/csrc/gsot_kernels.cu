@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 const double* __restrict__ dpos,
                                                 const double* __restrict__ dbeta,
                                                 double ub_offset, uint32_t* __restrict__ words,
-                                                int2* __restrict__ tasks, EvalScalars* sc,
+                                                TaskDesc* __restrict__ tasks, EvalScalars* sc,
                                                 unsigned long long* __restrict__ cnt_slots) {
   __shared__ unsigned long long cnt[8][7];
   __shared__ int base;
@@ -307,7 +307,14 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   if (lane == 0 && ws != 0u && c < P.nw) {
     int pos = base;
     for (int w = 0; w < warp; ++w) pos += (int)cnt[w][6];
-    tasks[pos] = make_int2(l, (int)c);
+    TaskDesc d;
+    d.l = l;
+    d.c = (int)c;
+    d.o0 = P.off[l];
+    d.g = P.off[l + 1] - d.o0;
+    d.word = ws;
+    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    tasks[pos] = d;
   }
   // block totals into one of 64 counter slots (spread, no fences); the
   // objective kernel's last block folds the slots into sc->counters
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
 }
 
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
-                   const double* dbeta, double ub_offset, uint32_t* words, int2* tasks,
+                   const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s) {
   dim3 grid((unsigned)((P.nw * 32 + 255) / 256), (unsigned)P.L);
   k_screen<<<grid, 256, 0, s>>>(P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc, cnt_slots);
@@ -341,236 +348,236 @@ void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaSt
   k_fill_words<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(words, L, nw, n);
 }
 // Dense task order: largest groups first (long chains start early).
-__global__ void k_dense_tasks(int2* tasks, const int32_t* __restrict__ order, int32_t L,
-                              int32_t nw) {
+__global__ void k_dense_tasks(DevProblem P, TaskDesc* tasks, const int32_t* __restrict__ order) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)L * nw) return;
-  tasks[t] = make_int2(order[t / nw], (int)(t % nw));
+  if (t >= (int64_t)P.L * P.nw) return;
+  TaskDesc d;
+  d.l = order[t / P.nw];
+  d.c = (int)(t % P.nw);
+  d.o0 = P.off[d.l];
+  d.g = P.off[d.l + 1] - d.o0;
+  const int64_t rem = P.n - (int64_t)d.c * 32;
+  d.word = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+  d.pad[0] = d.pad[1] = d.pad[2] = 0;
+  tasks[t] = d;
 }
-void launch_dense_tasks(int2* tasks, const int32_t* order, int32_t L, int32_t nw,
+void launch_dense_tasks(const DevProblem& P, TaskDesc* tasks, const int32_t* order,
                         cudaStream_t s) {
-  const int64_t total = (int64_t)L * nw;
-  k_dense_tasks<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(tasks, order, L, nw);
+  const int64_t total = (int64_t)P.L * P.nw;
+  k_dense_tasks<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(P, tasks, order);
 }
 
 // ---------------------------------------------------------------- fused eval
-// Persistent blocks; block b owns the chunks t = b + G*q of the canonical
-// chunk order (largest groups first, interleaved so every block samples
-// every group). Phase 0: the block collects its non-empty chunks (survivor
-// word != 0) into a shared-memory task list. Phase 1: its warps drain the
-// list through a shared counter. One warp per (group l, 32-column chunk c)
-// task: the g_l x 32 tile is contiguous, so lane 0 stages it into the warp's
-// shared buffer with ONE TMA bulk copy (cp.async.bulk + mbarrier); groups
-// taller than the buffer stream through its two halves (copy of segment s+1
-// in flight while segment s is computed). Lane = column j = 32c + lane,
-// active iff its survivor bit is set.
-//   pass 1, sequential over the block's rows: z^2 = sum [f]+^2, sum [f]+;
-//   scale = (1 - tau/z)/gamma when z > tau (grad_block, regularizer.hpp:
-//   64-74); psi = (z - tau)^2 / (2 gamma) (closed form of psi_block,
-//   regularizer.hpp:78-91); column partial scale * sum [f]+;
-//   pass 2, 16 rows at a time: T = scale * [f]+ transpose-reduced across the
-//   warp into per-row partials of the chunk, stored at rowpart[c*m + row].
+// Persistent, warp-specialised CTAs drain the task list (the compact
+// screened list, or every chunk in dense mode) through a global cursor; ONE
+// CTA per task = (group l, 32-column chunk c). The task's g_l x 32 tile is
+// contiguous in HBM, so a producer warp stages it -- with the g_l entries of
+// alpha -- into shared memory with TMA bulk copies (cp.async.bulk + mbarrier
+// complete_tx) in segments of at most `seg` rows through two slots (full /
+// empty mbarriers), running ahead into the next task; four consumer warps
+// compute. Within a segment, consumer warp w owns a contiguous run of rows;
+// lane = column j = 32c + lane, active iff its survivor bit is set.
+//   pass 1: [f]+ = max(alpha_i + beta_j - C_ij, 0) replaces the cost in
+//   shared memory; z^2 = sum [f]+^2 and sum [f]+ per column (per-warp chains
+//   over the warp's rows, segment after segment; the warp partials then added
+//   in warp order); scale = (1 - tau/z)/gamma when z > tau (grad_block,
+//   regularizer.hpp:64-74); psi = (z - tau)^2 / (2 gamma) (closed form of
+//   psi_block, regularizer.hpp:78-91); column partial
+//   scale * sum [f]+;
+//   pass 2: row partials sum_j scale_j [f]+_ij of the chunk (T summed over
+//   the chunk's columns), stored at rowpart[c*m + row]. A tile that fits one
+//   segment is still resident; a taller one is streamed again.
+// Every association depends only on g_l and the segment size, never on
+// which blocks survived: dense and screened evaluations agree bitwise.
 // The plan is never stored.
 struct EvalArgs {
   DevProblem P;
   const double* x;
-  const int2* order;  // canonical chunk order
-  int nchunks;
+  const TaskDesc* order;  // task list
   const uint32_t* words;  // survivor words (dense: all valid columns)
   double* rowpart;
   double* colpart;
   double* psi;
-  int buf_rows;  // rows per warp buffer (whole tile when g <= buf_rows)
-  int* next_chunk;  // global claim cursor (zeroed per evaluation)
+  int seg;          // rows per shared-memory segment (<= kEvalMaxSeg)
+  int* next_task;   // global claim cursor (zeroed per evaluation)
   int ntasks;       // >= 0: list length; -1: read *ntasks_dev (screened)
   const int* ntasks_dev;
-  int batch;        // tasks claimed per atomic
 };
 
-constexpr int kEvalWarps = 8;
+constexpr int kEvalWarps = 4;                        // consumer warps
+constexpr int kEvalThreads = 32 * (kEvalWarps + 1);  // + one producer warp
+constexpr int kEvalMaxSeg = 128;                     // rows per segment (4 warps x 32 rows)
 
-__global__ void __launch_bounds__(256) k_eval(const EvalArgs A) {
+struct EvalTask {
+  int l, c, g, o0, nseg, valid;
+  uint32_t word;
+};
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEvalWarps) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
   extern __shared__ __align__(128) unsigned char eval_smem[];
   const DevProblem& P = A.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int B = A.buf_rows, H = A.buf_rows / 2;  // whole buffer / half (B = 0: streaming)
-  double* buf = reinterpret_cast<double*>(eval_smem) + (size_t)warp * B * 32;
-  __shared__ uint64_t bars[kEvalWarps][2];
-  if (B > 0 && lane == 0) {
-    mbar_init(&bars[warp][0], 1);
-    mbar_init(&bars[warp][1], 1);
+  double* slots = reinterpret_cast<double*>(eval_smem);  // [2][seg * 32] cost segments
+  double* aslots = slots + 2 * (size_t)A.seg * 32;       // [2][seg + 2] alpha segments
+  __shared__ uint64_t full[2], empty[2];
+  __shared__ EvalTask tinfo[2];  // by the slot of the task's first segment
+  __shared__ double zsh[kEvalWarps][32], ssh[kEvalWarps][32];
+  __shared__ double scale_sh[32];
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], kEvalWarps);
+    mbar_init(&empty[1], kEvalWarps);
+    mbar_fence_init();
   }
-  mbar_fence_init();
-  __syncwarp();
-  uint32_t ph[2] = {0u, 0u};
-  // Dynamic scheduling over the compact work list: a warp claims `batch`
-  // consecutive tasks per atomic (1 for the sparse screened list, a few for
-  // the dense list).
-  const int ntasks = A.ntasks >= 0 ? A.ntasks : *(volatile const int*)A.ntasks_dev;
+  __syncthreads();
+  if (warp == kEvalWarps) {  // ---- producer
+    if (lane != 0) return;
+    const int ntasks = A.ntasks >= 0 ? A.ntasks : *(volatile const int*)A.ntasks_dev;
+    auto fetch = [&](int t) {  // claimed task -> descriptor (one 32-byte load)
+      EvalTask T{};
+      T.valid = t < ntasks;
+      if (T.valid) {
+        const int4 a = __ldg(reinterpret_cast<const int4*>(A.order + t));
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(A.order + t) + 4);
+        T.l = a.x;
+        T.c = a.y;
+        T.o0 = a.z;
+        T.g = a.w;
+        T.word = w;
+        T.nseg = (T.g + A.seg - 1) / A.seg;
+      }
+      return T;
+    };
+    uint32_t e = 0;
+    EvalTask T = fetch(atomicAdd(A.next_task, 1));
+    int tn = T.valid ? atomicAdd(A.next_task, 1) : ntasks;  // claimed one task ahead
+    for (;;) {
+      const double* tile = P.C + 32 * ((int64_t)P.nw * T.o0 + (int64_t)T.c * T.g);
+      const int ne = !T.valid ? 1 : T.nseg == 1 ? 1 : 2 * T.nseg;
+      EvalTask Tn{};
+      for (int k = 0; k < ne; ++k, ++e) {
+        const int slot = e & 1u;
+        if (e >= 2) mbar_wait_sleep(&empty[slot], ((e >> 1) - 1) & 1u);
+        if (k == 0) tinfo[slot] = T;
+        if (!T.valid) {
+          mbar_arrive(&full[slot]);  // end marker
+          return;
+        }
+        // alpha rides along with each cost segment (x is 16-byte aligned)
+        const int r0 = (k < T.nseg ? k : k - T.nseg) * A.seg, rows = min(A.seg, T.g - r0);
+        const int64_t a0 = (T.o0 + r0) & ~1ll;  // 16-byte aligned superset of the rows
+        const uint32_t abytes = (uint32_t)(((T.o0 + r0 + rows - a0) + 1) & ~1ll) * 8u;
+        mbar_expect_tx(&full[slot], (uint32_t)rows * 256u + abytes);
+        tma_load_1d(slots + (size_t)slot * A.seg * 32, tile + (int64_t)r0 * 32,
+                    (uint32_t)rows * 256u, &full[slot]);
+        tma_load_1d(aslots + (size_t)slot * (A.seg + 2), A.x + a0, abytes, &full[slot]);
+        if (k == 0) {  // decode the next task and claim the one after while this one loads
+          Tn = fetch(tn);
+          tn = Tn.valid ? atomicAdd(A.next_task, 1) : ntasks;
+        }
+      }
+      T = Tn;
+    }
+  }
+  // ---- consumers
+  const int rr = lane & 15, hh = lane >> 4;  // row-reduction roles (pass 2)
+  int roff[16];  // byte offsets of this lane's 16 columns, rotated by rr (no bank conflicts)
+#pragma unroll
+  for (int q = 0; q < 16; ++q) roff[q] = (hh * 16 + ((q + rr) & 15)) * 8;
+  uint32_t e = 0;
   for (;;) {
-    int base = 0;
-    if (lane == 0) base = atomicAdd(A.next_chunk, A.batch);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= ntasks) break;
-   const int bend = min(ntasks, base + A.batch);
-   for (int t = base; t < bend; ++t) {
-    const int2 tk = A.order[t];
-    const uint32_t word = A.words[(int64_t)tk.x * P.nw + tk.y];
-    const int l = tk.x, c = tk.y;
-    const int64_t j = (int64_t)c * 32 + lane;
-    const bool act = (word >> lane) & 1u;
-    const int o0 = P.off[l];
-    const int g = P.off[l + 1] - o0;
-    const double* __restrict__ al = A.x + o0;
+    mbar_wait_sleep(&full[e & 1u], (e >> 1) & 1u);
+    const EvalTask T = tinfo[e & 1u];
+    if (!T.valid) break;
+    const int64_t j = (int64_t)T.c * 32 + lane;
+    const bool act = (T.word >> lane) & 1u;
     const double bj = act ? A.x[P.m + j] : 0.0;
-    const double* tile = P.C + 32 * ((int64_t)P.nw * o0 + (int64_t)c * g);
-    if (B == 0) {  // register-streaming path: no staging, loads batched per lane
-      const double* __restrict__ cp = tile + lane;
-      double z2 = 0.0, sv = 0.0;
+    double z2 = 0.0, sv = 0.0;
+    double scr[16];  // scales of this lane's 16 rotated columns
+    const int ne = T.nseg == 1 ? 1 : 2 * T.nseg;
+    for (int k = 0; k < ne; ++k, ++e) {
+      const int slot = e & 1u;
+      if (k > 0) mbar_wait_sleep(&full[slot], (e >> 1) & 1u);
+      double* __restrict__ buf = slots + (size_t)slot * A.seg * 32;
+      const int sgm = k < T.nseg ? k : k - T.nseg;
+      const int r0 = sgm * A.seg, rows = min(A.seg, T.g - r0);
+      const int R = (rows + kEvalWarps - 1) / kEvalWarps;
+      const int w0 = min(rows, warp * R), w1 = min(rows, w0 + R);
+      const double* __restrict__ as = aslots + (size_t)slot * (A.seg + 2) + ((T.o0 + r0) & 1);
+      double* __restrict__ col = buf + lane;
       if (act) {
-        int r = 0;
-        for (; r + 8 <= g; r += 8) {
-          double cc[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) cc[k] = __ldg(cp + 32 * (r + k));
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const double f = residual(__ldg(al + r + k), bj, cc[k]);
-            const double v = f > 0.0 ? f : 0.0;
+        if (k < T.nseg) {  // pass 1: accumulate, [f]+ in place of the cost
+#pragma unroll 4
+          for (int r = w0; r < w1; ++r) {
+            const double v = relu(residual(as[r], bj, col[r * 32]));
             z2 = dadd(z2, dmul(v, v));
             sv = dadd(sv, v);
+            col[r * 32] = v;
+          }
+        } else {  // re-streamed segment: [f]+ only
+#pragma unroll 4
+          for (int r = w0; r < w1; ++r) col[r * 32] = relu(residual(as[r], bj, col[r * 32]));
+        }
+      }
+      if (k == T.nseg - 1) {  // pass 1 complete: the warps in order (warp 0)
+        zsh[warp][lane] = z2;
+        ssh[warp][lane] = sv;
+        consumer_sync();
+        if (warp == 0) {
+          double zz = zsh[0][lane], ss = ssh[0][lane];
+#pragma unroll
+          for (int w = 1; w < kEvalWarps; ++w) {
+            zz = dadd(zz, zsh[w][lane]);
+            ss = dadd(ss, ssh[w][lane]);
+          }
+          const double z = sqrt(zz);
+          const bool nz = act && z > P.tau;
+          const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
+          scale_sh[lane] = scale;
+          if (act) {
+            const int64_t idx = (int64_t)T.l * P.n + j;
+            A.colpart[idx] = dmul(scale, ss);
+            double ps = 0.0;
+            if (nz) {
+              const double d = dsub(z, P.tau);
+              ps = ddiv(dmul(d, d), dmul(2.0, P.gamma));
+            }
+            A.psi[idx] = ps;
           }
         }
-        for (; r < g; ++r) {
-          const double f = residual(__ldg(al + r), bj, __ldg(cp + 32 * r));
-          const double v = f > 0.0 ? f : 0.0;
-          z2 = dadd(z2, dmul(v, v));
-          sv = dadd(sv, v);
-        }
-      }
-      const double z = sqrt(z2);
-      const bool nz = act && z > P.tau;
-      const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
-      if (act) {
-        const int64_t idx = (int64_t)l * P.n + j;
-        A.colpart[idx] = dmul(scale, sv);
-        double ps = 0.0;
-        if (nz) {
-          const double e = dsub(z, P.tau);
-          ps = ddiv(dmul(e, e), dmul(2.0, P.gamma));
-        }
-        A.psi[idx] = ps;
-      }
-      double* __restrict__ rp = A.rowpart + (int64_t)c * P.m + o0;
-      if (__ballot_sync(0xffffffffu, nz) == 0u) {
-        for (int r = lane; r < g; r += 32) rp[r] = 0.0;
-        continue;
-      }
-      for (int r0 = 0; r0 < g; r0 += 16) {
-        double v[16];
+        consumer_sync();
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int r = r0 + k;
-          const bool in = nz && r < g;
-          const double cc = in ? __ldg(cp + 32 * r) : 0.0;
-          const double a = r < g ? __ldg(al + r) : 0.0;
-          const double f = residual(a, bj, cc);
-          v[k] = (in && f > 0.0) ? dmul(scale, f) : 0.0;
-        }
-        transpose_reduce16(v, lane);
-        if (lane < 16 && r0 + lane < g) rp[r0 + lane] = v[0];
+        for (int q = 0; q < 16; ++q) scr[q] = scale_sh[roff[q] >> 3];
       }
-      continue;
-    }
-    const bool whole = g <= B;
-    // segment s: rows [s*H, min(g, (s+1)*H)) in half (s & 1) of the buffer
-    const int nseg = whole ? 1 : (g + H - 1) / H;
-    auto issue = [&](int sgm) {  // lane 0 only
-      if (whole) {
-        mbar_expect_tx(&bars[warp][0], (uint32_t)g * 256u);
-        tma_load_1d(buf, tile, (uint32_t)g * 256u, &bars[warp][0]);
-      } else {
-        const int r0 = sgm * H, rows = min(H, g - r0), hb = sgm & 1;
-        mbar_expect_tx(&bars[warp][hb], (uint32_t)rows * 256u);
-        tma_load_1d(buf + (size_t)hb * H * 32, tile + (int64_t)r0 * 32, (uint32_t)rows * 256u,
-                    &bars[warp][hb]);
-      }
-    };
-    auto wait_seg = [&](int sgm) {
-      const int hb = whole ? 0 : (sgm & 1);
-      mbar_wait(&bars[warp][hb], ph[hb]);
-      ph[hb] ^= 1u;
-    };
-    auto row_ptr = [&](int r) -> const double* {  // row r of the current residency
-      return whole ? buf + (size_t)r * 32 : buf + (size_t)(((r / H) & 1) * H + (r % H)) * 32;
-    };
-
-    // pass 1
-    if (lane == 0) {
-      issue(0);
-      if (!whole && nseg > 1) issue(1);
-    }
-    double z2 = 0.0, sv = 0.0;
-    for (int sgm = 0; sgm < nseg; ++sgm) {
-      wait_seg(sgm);
-      const int r0 = whole ? 0 : sgm * H, r1 = whole ? g : min(g, r0 + H);
-      if (act) {
-        for (int r = r0; r < r1; ++r) {
-          const double f = residual(__ldg(al + r), bj, row_ptr(r)[lane]);
-          const double v = f > 0.0 ? f : 0.0;
-          z2 = dadd(z2, dmul(v, v));
-          sv = dadd(sv, v);
-        }
-      }
-      __syncwarp();
-      if (!whole && lane == 0 && sgm + 2 < nseg) issue(sgm + 2);
-    }
-    const double z = sqrt(z2);
-    const bool nz = act && z > P.tau;
-    const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
-    if (act) {
-      const int64_t idx = (int64_t)l * P.n + j;
-      A.colpart[idx] = dmul(scale, sv);
-      double ps = 0.0;
-      if (nz) {
-        const double e = dsub(z, P.tau);
-        ps = ddiv(dmul(e, e), dmul(2.0, P.gamma));
-      }
-      A.psi[idx] = ps;
-    }
-    double* __restrict__ rp = A.rowpart + (int64_t)c * P.m + o0;
-    const unsigned nzm = __ballot_sync(0xffffffffu, nz);
-    if (nzm == 0u) {
-      for (int r = lane; r < g; r += 32) rp[r] = 0.0;
-      __syncwarp();
-      continue;
-    }
-    // pass 2 (the whole tile is still resident; a streamed one is re-read)
-    if (!whole && lane == 0) {
-      issue(0);
-      if (nseg > 1) issue(1);
-    }
-    for (int sgm = 0; sgm < nseg; ++sgm) {
-      if (!whole) wait_seg(sgm);
-      const int r0s = whole ? 0 : sgm * H, r1s = whole ? g : min(g, r0s + H);
-      for (int r0 = r0s; r0 < r1s; r0 += 16) {
-        double v[16];
+      if (T.nseg == 1 || k >= T.nseg) {
+        // pass 2: row partial sum_j scale_j [f]+_ij of the chunk. Lane (rr, hh)
+        // sums half hh of a row (columns in rotated order: no bank conflicts),
+        // then the two halves; 16 rows at a time. Inactive columns have scale
+        // 0 and a finite entry: an exact zero, as in a dense evaluation.
+        __syncwarp();
+        for (int rb = w0; rb < w1; rb += 16) {
+          double acc = 0.0;
+          if (rr < w1 - rb) {
+            const char* __restrict__ row = reinterpret_cast<const char*>(buf + (rb + rr) * 32);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int r = r0 + k;
-          const bool in = nz && r < r1s;
-          const double cc = in ? row_ptr(r)[lane] : 0.0;
-          const double a = r < r1s ? __ldg(al + r) : 0.0;
-          const double f = residual(a, bj, cc);
-          v[k] = (in && f > 0.0) ? dmul(scale, f) : 0.0;
+            for (int q = 0; q < 16; ++q)
+              acc = dadd(acc, dmul(scr[q], *reinterpret_cast<const double*>(row + roff[q])));
+          }
+          acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, 16));
+          if (hh == 0 && rr < w1 - rb) A.rowpart[(int64_t)T.c * P.m + T.o0 + r0 + rb + rr] = acc;
         }
-        transpose_reduce16(v, lane);
-        if (lane < 16 && r0 + lane < r1s) rp[r0 + lane] = v[0];
       }
       __syncwarp();
-      if (!whole && lane == 0 && sgm + 2 < nseg) issue(sgm + 2);
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
     }
-   }
   }
 }
 
@@ -579,15 +586,12 @@ int g_eval_per_sm = 0;
 int g_eval_smem_attr = 0;
 }
 
-int eval_buf_rows(int gmax) {
-  // whole tile per warp when it fits 8 warps x rows x 256 B in ~200 KB,
-  // else 96-row buffers streamed as two 48-row halves
-  return gmax <= 96 ? std::max(16, gmax) : 96;
-}
+// Rows per segment: the tallest group when it fits, else kEvalMaxSeg.
+int eval_buf_rows(int gmax) { return std::max(8, std::min(gmax, kEvalMaxSeg)); }
 
-size_t eval_smem_bytes(int buf_rows, int cap) {
+size_t eval_smem_bytes(int seg, int cap) {
   (void)cap;
-  return sizeof(double) * (size_t)kEvalWarps * buf_rows * 32;
+  return sizeof(double) * 2 * ((size_t)seg * 32 + seg + 2);
 }
 
 int eval_blocks_per_sm(size_t smem) {
@@ -596,23 +600,26 @@ int eval_blocks_per_sm(size_t smem) {
     g_eval_smem_attr = (int)smem;
   }
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval, 256, smem) != cudaSuccess || n < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval, kEvalThreads, smem) !=
+          cudaSuccess ||
+      n < 1)
     n = 1;
   g_eval_per_sm = n;
   return n;
 }
 
-void launch_eval(const DevProblem& P, const double* x, const int2* tasks, int ntasks,
+void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s) {
-  EvalArgs A{P, x, tasks, P.L * P.nw, words, rowpart, colpart, psi, buf_rows, next_chunk,
-             ntasks, ntasks_dev, ntasks >= 0 ? 4 : 1};
-  const size_t smem = eval_smem_bytes(buf_rows, 0);
+                 double* psi, int seg, int grid, int* next_task, cudaStream_t s) {
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0)
+    throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
+  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev};
+  const size_t smem = eval_smem_bytes(seg, 0);
   if ((int)smem > g_eval_smem_attr) {
     cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     g_eval_smem_attr = (int)smem;
   }
-  k_eval<<<grid, 256, smem, s>>>(A);
+  k_eval<<<grid, kEvalThreads, smem, s>>>(A);
 }
 
 // ---------------------------------------------------------------- finalize
