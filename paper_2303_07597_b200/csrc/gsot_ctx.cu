@@ -373,12 +373,12 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
   const DevProblem P = c->problem();
-  c->reset_scalars();
+  if (mode != GSOT_EVAL_SCREENED) c->reset_scalars();  // screened: k_delta zeroes the cursors
   const uint32_t* words = c->dense_words;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
     c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
-      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->sc, c->stream);
     });
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
@@ -458,7 +458,7 @@ void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active) {
   c->reset_scalars();
   if (use_active) {
     c->launch(K_DELTA, 16.0 * (c->m + c->n), [&] {
-      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->stream);
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, c->stream);
     });
     c->launch(K_ACTIVE, 16.0 * c->L * c->n + 4.0 * c->L * c->nw, [&] {
       launch_active(P, c->ks, c->os, c->dfull, c->dneg, c->dbeta, c->active_words, c->sc,

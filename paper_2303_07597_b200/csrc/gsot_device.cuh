@@ -169,6 +169,13 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
 namespace gsot {
 
 // Fold the 64 counter slots into sc->counters etc. and zero them (one warp).
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor drains; pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible. pdl_trigger()
+// lets the successor launch early. Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // max(f, 0) by bit operations (f finite): a negative f, -0 included, -> +0.
 __device__ __forceinline__ double relu(double f) {
   const long long b = __double_as_longlong(f);

@@ -91,6 +91,24 @@ struct alignas(16) TaskDesc {
   int pad[3];
 };
 
+// Launch with programmatic stream serialisation (PDL) unless GSOT_PDL=0.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- kernels (gsot_kernels.cu) ---------------------------------------------
 
 // Per-kernel-class counters for gsot_profile_*.
@@ -111,8 +129,10 @@ void launch_relayout(const DevProblem& P, const double* src_colmajor, int64_t j0
 void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                      cudaStream_t s);
 void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStream_t s);
+// Screened evaluations: k_delta also zeroes the per-evaluation cursors and
+// counters of sc (instead of a memset node ahead of the chain).
 void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
-                  double* dfull, double* dneg, double* dbeta, cudaStream_t s);
+                  double* dfull, double* dneg, double* dbeta, EvalScalars* sc, cudaStream_t s);
 void launch_active(const DevProblem& P, const double* ks, const double* os, const double* dfull,
                    const double* dneg, const double* dbeta, uint32_t* active_words,
                    EvalScalars* sc, cudaStream_t s);

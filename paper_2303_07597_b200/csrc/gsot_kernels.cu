@@ -18,9 +18,19 @@
 // stored row-major; tile (l, c) starts at element 32 * (nw * off_l + c * g_l).
 // A warp (lane = column) walking the block rows reads one contiguous 256-byte
 // row of the tile per load.
+#include <cstdlib>
+
 #include "gsot_device.cuh"
 
 namespace gsot {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GSOT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // ---------------------------------------------------------------- relayout
 // Column-major m x n (device) chunk [j0, j0+ncols) -> column-tiled layout,
@@ -157,7 +167,16 @@ __global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __res
                                                double* __restrict__ dpos,
                                                double* __restrict__ dfull,
                                                double* __restrict__ dneg,
-                                               double* __restrict__ dbeta, int group_blocks) {
+                                               double* __restrict__ dbeta, int group_blocks,
+                                               EvalScalars* sc) {
+  pdl_trigger();
+  if (sc != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {  // per-evaluation cursors
+    sc->ntasks = 0;
+    sc->next_task = 0;
+    sc->ticket = 0u;
+    sc->audit_violation = 0;
+    sc->audit_where = 0;
+  }
   if ((int)blockIdx.x >= group_blocks) {
     const int64_t j = ((int64_t)blockIdx.x - group_blocks) * blockDim.x + threadIdx.x;
     if (j < P.n) dbeta[j] = dsub(x[P.m + j], xs[P.m + j]);
@@ -206,10 +225,10 @@ __global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __res
 }
 
 void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
-                  double* dfull, double* dneg, double* dbeta, cudaStream_t s) {
+                  double* dfull, double* dneg, double* dbeta, EvalScalars* sc, cudaStream_t s) {
   const int gb = (P.L + 7) / 8;
   const int bb = (int)((P.n + 255) / 256);
-  k_delta<<<gb + bb, 256, 0, s>>>(P, x, xs, dpos, dfull, dneg, dbeta, gb);
+  k_delta<<<gb + bb, 256, 0, s>>>(P, x, xs, dpos, dfull, dneg, dbeta, gb, sc);
 }
 
 // ---------------------------------------------------------------- active set
@@ -266,6 +285,8 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 unsigned long long* __restrict__ cnt_slots) {
   __shared__ unsigned long long cnt[8][7];
   __shared__ int base;
+  pdl_wait();
+  pdl_trigger();
   const int l = blockIdx.y;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -330,7 +351,8 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s) {
   dim3 grid((unsigned)((P.nw * 32 + 255) / 256), (unsigned)P.L);
-  k_screen<<<grid, 256, 0, s>>>(P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc, cnt_slots);
+  launch_pdl(k_screen, grid, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc,
+             cnt_slots);
 }
 
 
@@ -430,6 +452,8 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
   __shared__ EvalTask tinfo[2];  // by the slot of the task's first segment
   __shared__ double zsh[kEvalWarps][32], ssh[kEvalWarps][32];
   __shared__ double scale_sh[32];
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -619,7 +643,7 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
     cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     g_eval_smem_attr = (int)smem;
   }
-  k_eval<<<grid, kEvalThreads, smem, s>>>(A);
+  launch_pdl(k_eval, dim3(grid), dim3(kEvalThreads), smem, s, A);
 }
 
 // ---------------------------------------------------------------- finalize
@@ -648,6 +672,8 @@ __global__ void __launch_bounds__(32 * kFinSlices, 2) k_finalize(DevProblem P, c
                                                    EvalScalars* sc, int cnt_pending,
                                                    int row_blocks) {
   __shared__ double sh[2][kFinSlices][33];
+  pdl_wait();
+  pdl_trigger();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double obj[4] = {0.0, 0.0, 0.0, 0.0};  // a.alpha, b.beta, psi, g.d
   if ((int)blockIdx.x < row_blocks) {
@@ -746,8 +772,8 @@ void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words
                      int cnt_pending, cudaStream_t s) {
   const int rb = (int)((P.m + 31) / 32);
   const int cb = (int)((P.n + 31) / 32);
-  k_finalize<<<rb + cb, 32 * kFinSlices, 0, s>>>(P, x, words, rowpart, colpart, psi, grad, dvec, partials,
-                                      sc, cnt_pending, rb);
+  launch_pdl(k_finalize, dim3(rb + cb), dim3(32 * kFinSlices), 0, s, P, x, words, rowpart, colpart,
+             psi, grad, dvec, partials, sc, cnt_pending, rb);
 }
 
 // ---------------------------------------------------------------- plan

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
 #ifdef GSOT_PHASE_CLOCKS
   long long clk_prev = clock64();
 #endif
+  pdl_wait();
   EvalScalars* sc = &src->sc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fin = sc->fin_blocks, step = sc->step_blocks, cnt = sc->cnt_pending;
@@ -142,8 +143,8 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
 void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_count,
                     unsigned long long* host_flag, const double* fin_partials,
                     const double* step_partials, unsigned long long* cnt_slots, cudaStream_t s) {
-  k_publish<<<1, 256, 0, s>>>(src, host_dst, dev_count, host_flag, fin_partials, step_partials,
-                              cnt_slots);
+  launch_pdl(k_publish, dim3(1), dim3(256), 0, s, src, host_dst, dev_count, host_flag,
+             fin_partials, step_partials, cnt_slots);
 }
 
 __global__ void k_hist_reset(HistState* h, int mem) {
