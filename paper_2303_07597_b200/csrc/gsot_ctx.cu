@@ -115,7 +115,7 @@ gsot_ctx::~gsot_ctx() {
                   x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
-                  cnt_partials, cnt_slots, d_pub_count};
+                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -194,6 +194,8 @@ void alloc_buffers(gsot_ctx* c) {
       static_cast<size_t>(std::max<int64_t>(c->num_sms * 64, L * ((nw + 7) / 8))) * 8, t);
   c->words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dense_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
+  c->gmask = dalloc<uint32_t>(static_cast<size_t>(L) * ((nw + 31) / 32), t);
+  c->dense_gmask = dalloc<uint32_t>(static_cast<size_t>(L) * ((nw + 31) / 32), t);
   c->dense_tasks = dalloc<gsot::TaskDesc>(static_cast<size_t>(L) * nw, t);
   c->tasks = dalloc<gsot::TaskDesc>(static_cast<size_t>(L) * nw, t);
   c->snap_x = dalloc<double>(dim + 8, t);
@@ -241,6 +243,7 @@ void alloc_buffers(gsot_ctx* c) {
   GSOT_CUDA_CHECK(cudaMemcpyAsync(c->d_sqrt_g, sqrt_g.data(), sizeof(double) * L,
                                   cudaMemcpyHostToDevice, c->stream));
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_words(c->dense_words, c->L, c->nw, c->n, c->stream); });
+  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_gmask(c->dense_gmask, c->L, c->nw, c->stream); });
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->problem(), c->dense_tasks, c->d_group_order, c->stream); });
   // Persistent eval grid: two shared-memory segments of up to 128 rows per
   // CTA (the tallest group when it fits), as many CTAs per SM as shared
@@ -378,11 +381,12 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
     c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
-      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->sc, c->stream);
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->sc, c->gmask,
+                   c->stream);
     });
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
-                    ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->stream);
+                    ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask, c->stream);
     });
     words = c->words;
   }
@@ -403,8 +407,9 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
                   c->psi, c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
-    launch_finalize(P, d_x, words, c->rowpart, c->colpart, c->psi, d_grad, d_dir, c->partials,
-                    c->sc, mode == GSOT_EVAL_SCREENED ? 1 : 0, c->stream);
+    launch_finalize(P, d_x, words, mode == GSOT_EVAL_SCREENED ? c->gmask : c->dense_gmask,
+                    c->rowpart, c->colpart, c->psi, d_grad, d_dir, c->partials, c->sc,
+                    mode == GSOT_EVAL_SCREENED ? 1 : 0, c->stream);
   });
 }
 
@@ -458,7 +463,8 @@ void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active) {
   c->reset_scalars();
   if (use_active) {
     c->launch(K_DELTA, 16.0 * (c->m + c->n), [&] {
-      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, c->stream);
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, nullptr,
+                   c->stream);
     });
     c->launch(K_ACTIVE, 16.0 * c->L * c->n + 4.0 * c->L * c->nw, [&] {
       launch_active(P, c->ks, c->os, c->dfull, c->dneg, c->dbeta, c->active_words, c->sc,

@@ -82,6 +82,7 @@ struct gsot_ctx {
   unsigned long long* cnt_partials = nullptr;  // spare counter partials
   unsigned long long* cnt_slots = nullptr;     // screen counters, 64 x 8
   uint32_t *words = nullptr, *dense_words = nullptr;
+  uint32_t *gmask = nullptr, *dense_gmask = nullptr;  // per-group non-empty chunk masks
   gsot::TaskDesc* dense_tasks = nullptr;  // every chunk, largest groups first
   gsot::TaskDesc* tasks = nullptr;        // screened work list (non-empty chunks)
   // screening state

@@ -132,16 +132,19 @@ void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStre
 // Screened evaluations: k_delta also zeroes the per-evaluation cursors and
 // counters of sc (instead of a memset node ahead of the chain).
 void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
-                  double* dfull, double* dneg, double* dbeta, EvalScalars* sc, cudaStream_t s);
+                  double* dfull, double* dneg, double* dbeta, EvalScalars* sc, uint32_t* gmask,
+                  cudaStream_t s);
 void launch_active(const DevProblem& P, const double* ks, const double* os, const double* dfull,
                    const double* dneg, const double* dbeta, uint32_t* active_words,
                    EvalScalars* sc, cudaStream_t s);
 // Upper-bound screen (screening.hpp:252-275): survivor words + counters.
 // Counters accumulate into 64 slots x 8 (cnt_slots); the objective kernel
 // folds them into EvalScalars and zeroes the slots.
+// Per-group chunk masks gmask[l][c / 32] bit c % 32: chunk (l, c) non-empty.
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
-                   EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s);
+                   EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
+                   cudaStream_t s);
 // Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
 size_t eval_smem_bytes(int buf_rows, int cap);
@@ -153,9 +156,9 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
                  double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
-                     const double* rowpart, const double* colpart, const double* psi,
-                     double* grad, const double* dvec, double* partials, EvalScalars* sc,
-                     int cnt_pending, cudaStream_t s);
+                     const uint32_t* gmask, const double* rowpart, const double* colpart,
+                     const double* psi, double* grad, const double* dvec, double* partials,
+                     EvalScalars* sc, int cnt_pending, cudaStream_t s);
 void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,
                          double* out, cudaStream_t s);
 void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* words,
@@ -163,6 +166,7 @@ void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* wo
 void launch_audit_active(const DevProblem& P, const double* x, const uint32_t* active_words,
                          EvalScalars* sc, cudaStream_t s);
 void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaStream_t s);
+void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s);
 void launch_dense_tasks(const DevProblem& P, TaskDesc* tasks, const int32_t* group_order,
                         cudaStream_t s);
 

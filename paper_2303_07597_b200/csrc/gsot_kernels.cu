@@ -168,14 +168,17 @@ __global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __res
                                                double* __restrict__ dfull,
                                                double* __restrict__ dneg,
                                                double* __restrict__ dbeta, int group_blocks,
-                                               EvalScalars* sc) {
+                                               EvalScalars* sc, uint32_t* __restrict__ gmask) {
   pdl_trigger();
-  if (sc != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {  // per-evaluation cursors
-    sc->ntasks = 0;
-    sc->next_task = 0;
-    sc->ticket = 0u;
-    sc->audit_violation = 0;
-    sc->audit_where = 0;
+  if (sc != nullptr) {  // screened evaluation: per-evaluation cursors, empty chunk masks
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sc->ntasks = 0;
+      sc->next_task = 0;
+      sc->ticket = 0u;
+      sc->audit_violation = 0;
+      sc->audit_where = 0;
+    }
+    (void)gmask;  // the screen writes every chunk-mask word
   }
   if ((int)blockIdx.x >= group_blocks) {
     const int64_t j = ((int64_t)blockIdx.x - group_blocks) * blockDim.x + threadIdx.x;
@@ -225,10 +228,11 @@ __global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __res
 }
 
 void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
-                  double* dfull, double* dneg, double* dbeta, EvalScalars* sc, cudaStream_t s) {
+                  double* dfull, double* dneg, double* dbeta, EvalScalars* sc, uint32_t* gmask,
+                  cudaStream_t s) {
   const int gb = (P.L + 7) / 8;
   const int bb = (int)((P.n + 255) / 256);
-  k_delta<<<gb + bb, 256, 0, s>>>(P, x, xs, dpos, dfull, dneg, dbeta, gb, sc);
+  k_delta<<<gb + bb, 256, 0, s>>>(P, x, xs, dpos, dfull, dneg, dbeta, gb, sc, gmask);
 }
 
 // ---------------------------------------------------------------- active set
@@ -273,89 +277,106 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 // FastGradDispatcher::column's per-block decision (screening.hpp:252-275):
 // active-set members are computed without a bound; every other block gets
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
-// skipped iff z_bar <= tau. One warp per (group, 32-column) chunk writes the
-// survivor word; GradStats::PerCall counters go through per-block partials
-// and a last-block sum (integer, order-independent; no contended atomics).
+// skipped iff z_bar <= tau. CTA (k, l) screens the 32 chunks of group l
+// covered by chunk-mask word k (1024 columns); each warp takes four chunks
+// with all loads in flight and writes their survivor words. The CTA writes
+// its chunk-mask word, reserves its non-empty chunks' work-list slots with
+// ONE atomic, and adds its GradStats::PerCall counters into one of 64 slots
+// (integers: order-free).
 __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
                                                 const double* __restrict__ dpos,
                                                 const double* __restrict__ dbeta,
                                                 double ub_offset, uint32_t* __restrict__ words,
                                                 TaskDesc* __restrict__ tasks, EvalScalars* sc,
-                                                unsigned long long* __restrict__ cnt_slots) {
-  __shared__ unsigned long long cnt[8][7];
+                                                unsigned long long* __restrict__ cnt_slots,
+                                                uint32_t* __restrict__ gmask) {
+  __shared__ unsigned long long cnt[8][6];
+  __shared__ uint32_t cw[32];  // survivor word of each of the CTA's chunks
   __shared__ int base;
   pdl_wait();
   pdl_trigger();
-  const int l = blockIdx.y;
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c = j >> 5;
-  const bool valid = j < P.n;
-  bool in_active = false;
-  if (valid && aw != nullptr) in_active = (aw[(int64_t)l * P.nw + c] >> lane) & 1u;
-  const bool evaluated = valid && !in_active;
-  bool surv = in_active;
-  if (evaluated) {
-    const double db = dbeta[j];
-    const double db_pos = db > 0.0 ? db : 0.0;
-    const double zbar =
-        dadd(dadd(dadd(zs[(int64_t)l * P.n + j], dpos[l]), dmul(P.sqrt_g[l], db_pos)), ub_offset);
-    surv = !(zbar <= P.tau);
+  const int l = blockIdx.y;
+  const int cb = blockIdx.x * 32;  // first chunk
+  const double dp = dpos[l], sg = P.sqrt_g[l];
+  const unsigned long long g = (unsigned long long)(P.off[l + 1] - P.off[l]);
+  double zv[4], db[4];
+  uint32_t am[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {  // chunk cb + warp + 8u, all loads first
+    const int c = cb + warp + 8 * u;
+    const int64_t j = (int64_t)c * 32 + lane;
+    const bool valid = c < P.nw && j < P.n;
+    am[u] = (c < P.nw && aw != nullptr) ? aw[(int64_t)l * P.nw + c] : 0u;
+    zv[u] = valid ? zs[(int64_t)l * P.n + j] : 0.0;
+    db[u] = valid ? dbeta[j] : 0.0;
   }
-  const unsigned wa = __ballot_sync(0xffffffffu, in_active);
-  const unsigned we = __ballot_sync(0xffffffffu, evaluated);
-  const unsigned ws = __ballot_sync(0xffffffffu, surv);
-  if (lane == 0) {
-    const unsigned long long g = (unsigned long long)(P.off[l + 1] - P.off[l]);
-    if (c < P.nw) words[(int64_t)l * P.nw + c] = ws;
-    cnt[warp][0] = __popc(wa);
-    cnt[warp][1] = __popc(we & ~ws);
-    cnt[warp][2] = __popc(we & ws);
-    cnt[warp][3] = __popc(we);
-    cnt[warp][4] = (unsigned long long)__popc(ws) * g;  // survivors' rows
-    cnt[warp][5] = ws ? g : 0;                          // task rows
-    cnt[warp][6] = ws ? 1 : 0;                          // tasks
+  unsigned long long my[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = cb + warp + 8 * u;
+    const int64_t j = (int64_t)c * 32 + lane;
+    const bool valid = c < P.nw && j < P.n;
+    const bool in_active = valid && ((am[u] >> lane) & 1u);
+    const bool evaluated = valid && !in_active;
+    bool surv = in_active;
+    if (evaluated) {
+      const double db_pos = db[u] > 0.0 ? db[u] : 0.0;
+      const double zbar = dadd(dadd(dadd(zv[u], dp), dmul(sg, db_pos)), ub_offset);
+      surv = !(zbar <= P.tau);
+    }
+    const unsigned wa = __ballot_sync(0xffffffffu, in_active);
+    const unsigned we = __ballot_sync(0xffffffffu, evaluated);
+    const unsigned ws = __ballot_sync(0xffffffffu, surv);
+    if (lane == 0) {
+      if (c < P.nw) words[(int64_t)l * P.nw + c] = ws;
+      cw[warp + 8 * u] = ws;
+      my[0] += __popc(wa);
+      my[1] += __popc(we & ~ws);
+      my[2] += __popc(we & ws);
+      my[3] += __popc(we);
+      my[4] += (unsigned long long)__popc(ws) * g;  // survivors' rows
+      my[5] += ws ? g : 0ull;                       // task rows
+    }
   }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) cnt[warp][k] = my[k];
   __syncthreads();
-  // work list: one atomic per block reserves its non-empty chunks' slots
-  if (threadIdx.x == 0) {
-    int nt = 0;
-    for (int w = 0; w < 8; ++w) nt += (int)cnt[w][6];
-    base = nt ? atomicAdd(&sc->ntasks, nt) : 0;
-  }
-  __syncthreads();
-  if (lane == 0 && ws != 0u && c < P.nw) {
-    int pos = base;
-    for (int w = 0; w < warp; ++w) pos += (int)cnt[w][6];
-    TaskDesc d;
-    d.l = l;
-    d.c = (int)c;
-    d.o0 = P.off[l];
-    d.g = P.off[l + 1] - d.o0;
-    d.word = ws;
-    d.pad[0] = d.pad[1] = d.pad[2] = 0;
-    tasks[pos] = d;
-  }
-  // block totals into one of 64 counter slots (spread, no fences); the
-  // objective kernel's last block folds the slots into sc->counters
-  if (threadIdx.x < 6) {
-    unsigned long long t = 0;
-    for (int w = 0; w < 8; ++w) t += cnt[w][threadIdx.x];
-    const unsigned slot = (blockIdx.y * gridDim.x + blockIdx.x) & 63u;
-    if (t) atomicAdd(cnt_slots + slot * 8 + threadIdx.x, t);
+  if (warp == 0) {  // chunk mask word, work-list slots (chunk order within the CTA)
+    const uint32_t w = cw[lane];
+    const unsigned ne = __ballot_sync(0xffffffffu, w != 0u);
+    if (lane == 0) {
+      gmask[(int64_t)l * ((P.nw + 31) / 32) + blockIdx.x] = ne;
+      base = ne ? atomicAdd(&sc->ntasks, __popc(ne)) : 0;
+    }
+    __syncwarp();
+    if (w != 0u) {
+      TaskDesc d;
+      d.l = l;
+      d.c = cb + lane;
+      d.o0 = P.off[l];
+      d.g = (int)g;
+      d.word = w;
+      d.pad[0] = d.pad[1] = d.pad[2] = 0;
+      tasks[base + __popc(ne & ((1u << lane) - 1u))] = d;
+    }
+  } else if (warp == 1 && lane < 6) {
+    unsigned long long s = 0ull;
+    for (int w = 0; w < 8; ++w) s += cnt[w][lane];
+    if (s) atomicAdd(cnt_slots + ((blockIdx.y * gridDim.x + blockIdx.x) & 63u) * 8 + lane, s);
   }
 }
 
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
-                   EvalScalars* sc, unsigned long long* cnt_slots, cudaStream_t s) {
-  dim3 grid((unsigned)((P.nw * 32 + 255) / 256), (unsigned)P.L);
+                   EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
+                   cudaStream_t s) {
+  const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)P.L);
   launch_pdl(k_screen, grid, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc,
-             cnt_slots);
+             cnt_slots, gmask);
 }
-
-
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
 __global__ void k_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n) {
@@ -369,6 +390,21 @@ void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaSt
   const int64_t total = (int64_t)L * nw;
   k_fill_words<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(words, L, nw, n);
 }
+
+// Dense chunk masks: every chunk of every group.
+__global__ void k_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw) {
+  const int nmw = (nw + 31) / 32;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)L * nmw) return;
+  const int k = (int)(t % nmw);
+  const int rem = nw - 32 * k;
+  gmask[t] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+}
+void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s) {
+  const int64_t total = (int64_t)L * ((nw + 31) / 32);
+  k_fill_gmask<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(gmask, L, nw);
+}
+
 // Dense task order: largest groups first (long chains start early).
 __global__ void k_dense_tasks(DevProblem P, TaskDesc* tasks, const int32_t* __restrict__ order) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -649,54 +685,73 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
 // ---------------------------------------------------------------- finalize
 // grad_alpha_i = a_i - sum over non-empty chunks c of rowpart[c*m+i];
 // grad_beta_j = b_j - sum over surviving l of colpart[l][j]; psicol_j = sum
-// over surviving l of psi[l][j]. Each sum has a FIXED association: 16
-// slices (c = s mod 16 resp. l = s mod 16), each sequential in ascending
-// order, then the 16 slice partials in slice order. Empty chunks and skipped
+// over surviving l of psi[l][j]. Each sum has a FIXED association: 8
+// slices (c = s mod 8 resp. l = s mod 8), each sequential in ascending
+// order, then the 8 slice partials in slice order. Empty chunks and skipped
 // blocks contribute exact zeros, so omitting them leaves every partial
-// unchanged: the result does not depend on the screen.
+// unchanged: the result does not depend on the screen. Rows find their
+// group's non-empty chunks in the per-group chunk masks (staged in shared
+// memory), columns in the survivor words.
 // In the same kernel: per-block partials of a.alpha, b.beta, sum psi
 // (dual.hpp:51) and the line-search slope grad.d; k_publish folds them in
 // block order (and the screen's counter slots) before the host reads them.
-// Block (32, 16): blocks [0, m/32) handle 32 rows, the rest 32 columns.
-constexpr int kFinSlices = 16;
-constexpr int kFinBatch = 10;
+// Block (32, 8): blocks [0, m/32) handle 32 rows, the rest 32 columns.
+constexpr int kFinSlices = 8;
+constexpr int kFinBatch = 8;
+constexpr int kFinMaskCap = 2048;  // mask words staged per row block
 
-__global__ void __launch_bounds__(32 * kFinSlices, 2) k_finalize(DevProblem P, const double* __restrict__ x,
-                                                   const uint32_t* __restrict__ words,
-                                                   const double* __restrict__ rowpart,
-                                                   const double* __restrict__ colpart,
-                                                   const double* __restrict__ psi,
-                                                   double* __restrict__ grad,
-                                                   const double* __restrict__ dvec,
-                                                   double* __restrict__ partials,
-                                                   EvalScalars* sc, int cnt_pending,
-                                                   int row_blocks) {
+__global__ void __launch_bounds__(32 * kFinSlices, 4) k_finalize(
+    DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
+    const uint32_t* __restrict__ gmask, const double* __restrict__ rowpart,
+    const double* __restrict__ colpart, const double* __restrict__ psi, double* __restrict__ grad,
+    const double* __restrict__ dvec, double* __restrict__ partials, EvalScalars* sc,
+    int cnt_pending, int row_blocks) {
   __shared__ double sh[2][kFinSlices][33];
+  __shared__ uint32_t msk[kFinMaskCap];
   pdl_wait();
   pdl_trigger();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double obj[4] = {0.0, 0.0, 0.0, 0.0};  // a.alpha, b.beta, psi, g.d
   if ((int)blockIdx.x < row_blocks) {
-    const int64_t i = blockIdx.x * 32ll + tx;
+    const int nmw = (P.nw + 31) / 32;
+    const int64_t i0 = blockIdx.x * 32ll;
+    const int lf = P.row_group[i0];
+    const int ll = P.row_group[P.m - 1 < i0 + 31 ? P.m - 1 : i0 + 31];
+    const bool staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
+    if (staged)
+      for (int k = threadIdx.x; k < (ll - lf + 1) * nmw; k += blockDim.x)
+        msk[k] = gmask[(int64_t)lf * nmw + k];
+    __syncthreads();
+    const int64_t i = i0 + tx;
     double acc = 0.0;
     if (i < P.m) {
       const int l = P.row_group[i];
-      const uint32_t* __restrict__ wl = words + (int64_t)l * P.nw;
-      // slice ty: chunks c = ty + 32q, ascending; all loads of a batch in flight
-      for (int c0 = ty; c0 < P.nw; c0 += kFinSlices * kFinBatch) {
-        uint32_t w[kFinBatch];
-        double r[kFinBatch];
+      const uint32_t* gm = staged ? msk + (int64_t)(l - lf) * nmw : gmask + (int64_t)l * nmw;
+      const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
+      int k = 0;
+      uint32_t cur = nmw > 0 ? gm[0] & sel : 0u;
+      for (;;) {  // batches of the slice's non-empty chunks, ascending c
+        int idx[kFinBatch];
+        int cnt = 0;
 #pragma unroll
-        for (int u = 0; u < kFinBatch; ++u) {
-          const int c = c0 + kFinSlices * u;
-          w[u] = c < P.nw ? wl[c] : 0u;
+        for (int q = 0; q < kFinBatch; ++q) {
+          while (cur == 0u && k + 1 < nmw) cur = gm[++k] & sel;
+          idx[q] = -1;
+          if (cur != 0u) {
+            const int b = __ffs(cur) - 1;
+            cur &= cur - 1u;
+            idx[q] = 32 * k + b;
+            ++cnt;
+          }
         }
+        if (cnt == 0) break;
+        double v[kFinBatch];
 #pragma unroll
-        for (int u = 0; u < kFinBatch; ++u)
-          r[u] = w[u] ? rowpart[(int64_t)(c0 + kFinSlices * u) * P.m + i] : 0.0;
+        for (int q = 0; q < kFinBatch; ++q) v[q] = idx[q] >= 0 ? rowpart[(int64_t)idx[q] * P.m + i] : 0.0;
 #pragma unroll
-        for (int u = 0; u < kFinBatch; ++u)
-          if (w[u]) acc = dadd(acc, r[u]);
+        for (int q = 0; q < kFinBatch; ++q)
+          if (idx[q] >= 0) acc = dadd(acc, v[q]);
+        if (cnt < kFinBatch) break;
       }
     }
     sh[0][ty][tx] = acc;
@@ -714,22 +769,22 @@ __global__ void __launch_bounds__(32 * kFinSlices, 2) k_finalize(DevProblem P, c
     double acc = 0.0, ps = 0.0;
     if (j < P.n) {
       const int64_t c = j >> 5;
-      for (int l0 = ty; l0 < P.L; l0 += kFinSlices * kFinBatch) {
-        bool on[kFinBatch];
-        double cp[kFinBatch], pp[kFinBatch];
+      for (int l0 = ty; l0 < P.L; l0 += kFinSlices * 16) {
+        bool on[16];
 #pragma unroll
-        for (int u = 0; u < kFinBatch; ++u) {
+        for (int u = 0; u < 16; ++u) {
           const int l = l0 + kFinSlices * u;
           on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
         }
+        double cp[16], pp[16];
 #pragma unroll
-        for (int u = 0; u < kFinBatch; ++u) {
+        for (int u = 0; u < 16; ++u) {
           const int64_t idx = (int64_t)(l0 + kFinSlices * u) * P.n + j;
           cp[u] = on[u] ? colpart[idx] : 0.0;
           pp[u] = on[u] ? psi[idx] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < kFinBatch; ++u)
+        for (int u = 0; u < 16; ++u)
           if (on[u]) {
             acc = dadd(acc, cp[u]);
             ps = dadd(ps, pp[u]);
@@ -767,13 +822,13 @@ __global__ void __launch_bounds__(32 * kFinSlices, 2) k_finalize(DevProblem P, c
 }
 
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
-                     const double* rowpart, const double* colpart, const double* psi,
-                     double* grad, const double* dvec, double* partials, EvalScalars* sc,
-                     int cnt_pending, cudaStream_t s) {
+                     const uint32_t* gmask, const double* rowpart, const double* colpart,
+                     const double* psi, double* grad, const double* dvec, double* partials,
+                     EvalScalars* sc, int cnt_pending, cudaStream_t s) {
   const int rb = (int)((P.m + 31) / 32);
   const int cb = (int)((P.n + 31) / 32);
-  launch_pdl(k_finalize, dim3(rb + cb), dim3(32 * kFinSlices), 0, s, P, x, words, rowpart, colpart,
-             psi, grad, dvec, partials, sc, cnt_pending, rb);
+  launch_pdl(k_finalize, dim3(rb + cb), dim3(32 * kFinSlices), 0, s, P, x, words, gmask, rowpart,
+             colpart, psi, grad, dvec, partials, sc, cnt_pending, rb);
 }
 
 // ---------------------------------------------------------------- plan
