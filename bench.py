@@ -292,14 +292,10 @@ def run_ours(args, world, rank, local, pg):
                     lbfgs_memory=10, history_cap=0)
     for _ in range(args.warmup):
         ctx.solve(**solve_kw)
-    ctx.profile((1 << 0) | (1 << 1))  # capture the profiled graphs outside the timed region
-    ctx.solve(**solve_kw)
 
-    # ---- timed region: K solves on the resident instance
-    ctx.profile_reset()
-    # CUDA events only around the two HBM-streaming kernels (eval, snapshot):
-    # event nodes around every kernel would perturb the step
-    ctx.profile((1 << 0) | (1 << 1))
+    # ---- timed region: K solves on the resident instance, no instrumentation
+    # (event nodes between kernels would break the programmatic launch chain)
+    ctx.profile(False)
     launches0 = ctx.kernel_launches()
     clocks = ClockSampler(local)
     clocks.start()
@@ -318,16 +314,27 @@ def run_ours(args, world, rank, local, pg):
     ms = ctx.timer_stop()
     barrier(pg)
     clk = clocks.stop()
-    ctx.profile(False)
     launches = ctx.kernel_launches() - launches0
+    ms_max = allreduce(pg, ms, "max")
+    calls_tot = allreduce(pg, float(calls), "sum")
+    value = calls_tot / (ms_max / 1e3)
+
+    # ---- roofline pass: the same K solves again with CUDA events around the
+    # two HBM-streaming kernels (eval, snapshot) on the solver stream
+    ctx.profile((1 << 0) | (1 << 1))
+    ctx.solve(**solve_kw)  # capture the profiled graphs outside the measured pass
+    ctx.profile_reset()
+    ctx.profile((1 << 0) | (1 << 1))
+    ctx.timer_start()
+    for _ in range(args.steps):
+        ctx.solve(**solve_kw)
+    ms_prof = ctx.timer_stop()
+    ctx.profile(False)
     kinds = {}
     for k, name in KIND_NAMES.items():
         kms, kbytes, kn = ctx.profile_read(k)
         if kn:
             kinds[name] = {"ms": kms, "bytes": kbytes, "launches": kn}
-    ms_max = allreduce(pg, ms, "max")
-    calls_tot = allreduce(pg, float(calls), "sum")
-    value = calls_tot / (ms_max / 1e3)
 
     # roofline of the dominant HBM kernel (largest device-time share among
     # the kernels with algorithmic byte counts)
@@ -342,7 +349,10 @@ def run_ours(args, world, rank, local, pg):
                 "traffic": traffic,
                 "bytes_per_launch": d["bytes"] / d["launches"],
                 "ms_per_launch": d["ms"] / d["launches"],
-                "share_of_step": d["ms"] / ms}
+                "share_of_step": d["ms"] / ms_prof,
+                "measured": "CUDA events around every launch of the kernel on the solver stream, "
+                            "over a second pass of the same K solves (the value pass runs "
+                            "uninstrumented)"}
 
     # ---- e2e through the C ABI with host buffers
     e2e = run_e2e(args, ctx, cfg, gamma, mu, solve_kw, pg)
