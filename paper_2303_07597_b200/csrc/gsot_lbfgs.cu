@@ -231,30 +231,36 @@ struct StepArgs {
 
 
 // CTA-wide: out[v] = sum over c in [0, nc) of part[c * ld + v], v < nv.
-// Eight threads per value each sum a contiguous run of CTAs (all loads in
-// flight), then a fixed xor tree over the eight: deterministic.
+// Thread (sub, v) = (tid / 64, tid % 64) sums a contiguous run of CTAs for
+// value v (64 consecutive threads read 64 consecutive values: coalesced, all
+// loads of the run in flight), then the 8 runs are added in a fixed tree.
 __device__ __forceinline__ void grid_fold(const double* part, int nc, int ld, int nv,
                                           double* out) {
-  const int sub = threadIdx.x & 7;
+  __shared__ double fs[8][64];
+  const int sub = threadIdx.x >> 6, vl = threadIdx.x & 63;
   const int run = (nc + 7) / 8;
-  for (int v0 = 0; v0 < nv; v0 += kStepThreads / 8) {
-    const int v = v0 + (threadIdx.x >> 3);
+  for (int v0 = 0; v0 < nv; v0 += 64) {
+    const int v = v0 + vl;
     double s = 0.0;
     if (v < nv) {
       const int c0 = sub * run, c1 = min(nc, c0 + run);
-      for (int cb = c0; cb < c1; cb += 16) {
-        double q[16];
+      for (int cb = c0; cb < c1; cb += 24) {
+        double q[24];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) q[u] = cb + u < c1 ? __ldcg(part + (int64_t)(cb + u) * ld + v) : 0.0;
+        for (int u = 0; u < 24; ++u) q[u] = cb + u < c1 ? __ldcg(part + (int64_t)(cb + u) * ld + v) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
+        for (int u = 0; u < 24; ++u)
           if (cb + u < c1) s = dadd(s, q[u]);
       }
     }
-    s = dadd(s, __shfl_xor_sync(0xffffffffu, s, 1));
-    s = dadd(s, __shfl_xor_sync(0xffffffffu, s, 2));
-    s = dadd(s, __shfl_xor_sync(0xffffffffu, s, 4));
-    if (v < nv && sub == 0) out[v] = s;
+    fs[sub][vl] = s;
+    __syncthreads();
+    if (threadIdx.x < 64 && v0 + threadIdx.x < nv)
+      out[v0 + threadIdx.x] = dadd(dadd(dadd(fs[0][threadIdx.x], fs[1][threadIdx.x]),
+                                        dadd(fs[2][threadIdx.x], fs[3][threadIdx.x])),
+                                   dadd(dadd(fs[4][threadIdx.x], fs[5][threadIdx.x]),
+                                        dadd(fs[6][threadIdx.x], fs[7][threadIdx.x])));
+    __syncthreads();
   }
 }
 
@@ -279,6 +285,33 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
   __shared__ double t_sh;
   double t_reg = 0.0;
   if (threadIdx.x == 32 && A.xt) t_reg = *A.t;
+  // every CTA stages the ring state and R / YY (logical positions) now: the
+  // solve runs redundantly in every CTA after the grid barrier (identical
+  // inputs, identical bits), so no second barrier is needed; CTA 0 alone
+  // writes the state back (after the barrier, so no CTA reads it late)
+  extern __shared__ double step_dyn[];  // R, YY: KS x KS each
+  double* R = step_dyn;
+  double* YY = R + KS * KS;
+  __shared__ double red[(kMaxMemory + 1) * 5];
+  __shared__ double uu[kMaxMemory + 1], vv[kMaxMemory + 1];
+  __shared__ double lc[2 * kMaxMemory + 2];  // p, gam w, gam
+  __shared__ HistState hs;
+  __shared__ int fl[3];  // accepted, evicted-first, count after
+  // (loads issued now into registers, stored after phase 1: the latency overlaps it)
+  constexpr int kHsWords = (int)(sizeof(HistState) / sizeof(int));
+  static_assert(kHsWords <= 2 * kStepThreads, "HistState staging");
+  int hs_reg[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = threadIdx.x + q * kStepThreads;
+    hs_reg[q] = t < kHsWords ? reinterpret_cast<const int*>(A.h)[t] : 0;
+  }
+  double r_reg = 0.0, y_reg = 0.0;  // R / YY entry tid (k^2 <= 512; longer memories below)
+  if (threadIdx.x < k * k) {
+    const int i = threadIdx.x / k, jj = threadIdx.x % k;
+    r_reg = A.cs->R[i * kMaxMemory + jj];
+    y_reg = A.cs->YY[i * kMaxMemory + jj];
+  }
   if (threadIdx.x < k) {
     sp[threadIdx.x] = A.S + A.h->order[threadIdx.x] * A.stride;
     yp[threadIdx.x] = A.Y + A.h->order[threadIdx.x] * A.stride;
@@ -353,35 +386,38 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
     }
   }
   if (threadIdx.x == 32) t_sh = t_reg;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = threadIdx.x + q * kStepThreads;
+    if (t < kHsWords) reinterpret_cast<int*>(&hs)[t] = hs_reg[q];
+  }
+  if (threadIdx.x < k * k) {
+    const int i = threadIdx.x / k, jj = threadIdx.x % k;
+    R[i * KS + jj] = r_reg;
+    YY[i * KS + jj] = y_reg;
+  }
+  for (int t = threadIdx.x + kStepThreads; t < k * k; t += kStepThreads) {
+    const int i = t / k, jj = t % k;
+    R[i * KS + jj] = A.cs->R[i * kMaxMemory + jj];
+    YY[i * KS + jj] = A.cs->YY[i * kMaxMemory + jj];
+  }
   PHASE_MARK(0);
   grid.sync();
   PHASE_MARK(1);
-  // (2) CTA 0: fold, ring update, R / YY maintenance, compact solve
-  if (blockIdx.x == 0) {
-    extern __shared__ double step_dyn[];  // R, YY: KS x KS each
-    double* R = step_dyn;
-    double* YY = R + KS * KS;
-    __shared__ double red[(kMaxMemory + 1) * 5];
-    __shared__ double uu[kMaxMemory + 1], vv[kMaxMemory + 1];
-    __shared__ HistState hs;
-    __shared__ int fl[3];  // accepted, evicted-first, count after
+  // (2) every CTA: fold, ring update, R / YY maintenance, compact solve
+  {
     grid_fold(A.part + 2 * kStepMaxGrid, nc, ld, nrows * 5, red);
-    for (int t = threadIdx.x; t < (int)(sizeof(HistState) / sizeof(int)); t += blockDim.x)
-      reinterpret_cast<int*>(&hs)[t] = reinterpret_cast<const int*>(A.h)[t];
-    for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
-      const int i = t / k, jj = t % k;
-      R[i * KS + jj] = A.cs->R[i * kMaxMemory + jj];
-      YY[i * KS + jj] = A.cs->YY[i * kMaxMemory + jj];
-    }
     __syncthreads();
     PHASE_MARK(2);
     if (threadIdx.x == 0) {
       int accept = 0, first = 0, kk = k;
       if (A.pair) {
         const double sy = red[k * 5 + 0], ss = red[k * 5 + 1], yy = red[k * 5 + 2];
-        A.sc->extra[0] = sy;
-        A.sc->extra[1] = ss;
-        A.sc->extra[2] = yy;
+        if (blockIdx.x == 0) {
+          A.sc->extra[0] = sy;
+          A.sc->extra[1] = ss;
+          A.sc->extra[2] = yy;
+        }
         hs.last_sy = sy;
         hs.last_ss = ss;
         hs.last_yy = yy;
@@ -488,8 +524,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
           if (act && lane > j) z = dsub(z, dmul(R[j * KS + lane], pj));
         }
         if (act) {
-          A.cs->p[lane] = pl;
-          A.cs->w[lane] = dmul(gam, wl);
+          lc[lane] = pl;
+          lc[kMaxMemory + lane] = dmul(gam, wl);
         }
       } else {  // long memories: the same substitutions through shared memory
         __shared__ double tv[kMaxMemory + 1], wv[kMaxMemory + 1], pv[kMaxMemory + 1];
@@ -516,42 +552,31 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
           __syncwarp();
         }
         for (int i = lane; i < kn; i += 32) {
-          A.cs->p[i] = pv[i];
-          A.cs->w[i] = dmul(gam, wv[i]);
+          lc[i] = pv[i];
+          lc[kMaxMemory + i] = dmul(gam, wv[i]);
         }
       }
-      if (lane == 0) {
-        A.cs->gam = gam;
-        A.cs->k = kn;
+      if (lane == 0) lc[2 * kMaxMemory] = gam;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+      for (int t = threadIdx.x; t < (int)(sizeof(HistState) / sizeof(int)); t += blockDim.x)
+        reinterpret_cast<int*>(A.h)[t] = reinterpret_cast<const int*>(&hs)[t];
+      for (int t = threadIdx.x; t < kn * kn; t += blockDim.x) {  // R, YY back
+        const int i = t / kn, jj = t % kn;
+        A.cs->R[i * kMaxMemory + jj] = R[i * KS + jj];
+        A.cs->YY[i * kMaxMemory + jj] = YY[i * KS + jj];
       }
     }
-    for (int t = threadIdx.x; t < (int)(sizeof(HistState) / sizeof(int)); t += blockDim.x)
-      reinterpret_cast<int*>(A.h)[t] = reinterpret_cast<const int*>(&hs)[t];
-    for (int t = threadIdx.x; t < kn * kn; t += blockDim.x) {  // R, YY back
-      const int i = t / kn, jj = t % kn;
-      A.cs->R[i * kMaxMemory + jj] = R[i * KS + jj];
-      A.cs->YY[i * kMaxMemory + jj] = YY[i * KS + jj];
+    if (threadIdx.x < kn) {  // this CTA's pointers to the (new) ring order
+      sp[threadIdx.x] = A.S + hs.order[threadIdx.x] * A.stride;
+      yp[threadIdx.x] = A.Y + hs.order[threadIdx.x] * A.stride;
     }
     PHASE_MARK(5);
   }
-  grid.sync();
-  PHASE_MARK(6);
-  // (3) direction slice: all 2 x 16 history loads of an element in flight
-  __shared__ double lc[2 * kMaxMemory + 2];
-  __shared__ int kn_sh;
-  if (threadIdx.x == 0) kn_sh = __ldcg(&A.cs->k);
-  __syncthreads();
-  const int kk = kn_sh;
-  for (int t = threadIdx.x; t < kk; t += blockDim.x) {
-    lc[t] = __ldcg(&A.cs->p[t]);
-    lc[kMaxMemory + t] = __ldcg(&A.cs->w[t]);
-    const int slot = __ldcg(&A.h->order[t]);
-    sp[t] = A.S + slot * A.stride;
-    yp[t] = A.Y + slot * A.stride;
-  }
-  if (threadIdx.x == 0) lc[2 * kMaxMemory] = __ldcg(&A.cs->gam);
   __syncthreads();
   PHASE_MARK(7);
+  const int kk = fl[2];
   const double gam = lc[2 * kMaxMemory];
   const double t = t_sh;
   double pg = 0.0, pd = 0.0;
