@@ -376,17 +376,19 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
   const DevProblem P = c->problem();
-  if (mode != GSOT_EVAL_SCREENED) c->reset_scalars();  // screened: k_delta zeroes the cursors
+  if (mode != GSOT_EVAL_SCREENED || exact) c->reset_scalars();  // fast screened: zeroed by k_publish
   const uint32_t* words = c->dense_words;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
-    c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
-      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, c->sc, c->gmask,
-                   c->stream);
-    });
+    if (exact)  // reference-order group norms; fast mode fuses them into the screen
+      c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
+        launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, nullptr,
+                     c->stream);
+      });
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
-                    ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask, c->stream);
+                    ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
+                    exact ? nullptr : d_x, exact ? nullptr : c->snap_x, c->stream);
     });
     words = c->words;
   }

@@ -129,8 +129,9 @@ void launch_relayout(const DevProblem& P, const double* src_colmajor, int64_t j0
 void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                      cudaStream_t s);
 void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStream_t s);
-// Screened evaluations: k_delta also zeroes the per-evaluation cursors and
-// counters of sc (instead of a memset node ahead of the chain).
+// Screened evaluations start from zeroed per-evaluation cursors of sc
+// (ntasks, next_task, ticket, audit fields): k_publish resets them after it
+// copies them out, the context starts zeroed, other paths use a memset.
 void launch_delta(const DevProblem& P, const double* x, const double* xs, double* dpos,
                   double* dfull, double* dneg, double* dbeta, EvalScalars* sc, uint32_t* gmask,
                   cudaStream_t s);
@@ -144,7 +145,7 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
-                   cudaStream_t s);
+                   const double* x, const double* xs, cudaStream_t s);
 // Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
 size_t eval_smem_bytes(int buf_rows, int cap);

@@ -170,16 +170,8 @@ __global__ void __launch_bounds__(256) k_delta(DevProblem P, const double* __res
                                                double* __restrict__ dbeta, int group_blocks,
                                                EvalScalars* sc, uint32_t* __restrict__ gmask) {
   pdl_trigger();
-  if (sc != nullptr) {  // screened evaluation: per-evaluation cursors, empty chunk masks
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      sc->ntasks = 0;
-      sc->next_task = 0;
-      sc->ticket = 0u;
-      sc->audit_violation = 0;
-      sc->audit_where = 0;
-    }
-    (void)gmask;  // the screen writes every chunk-mask word
-  }
+  (void)sc;
+  (void)gmask;
   if ((int)blockIdx.x >= group_blocks) {
     const int64_t j = ((int64_t)blockIdx.x - group_blocks) * blockDim.x + threadIdx.x;
     if (j < P.n) dbeta[j] = dsub(x[P.m + j], xs[P.m + j]);
@@ -290,17 +282,20 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 double ub_offset, uint32_t* __restrict__ words,
                                                 TaskDesc* __restrict__ tasks, EvalScalars* sc,
                                                 unsigned long long* __restrict__ cnt_slots,
-                                                uint32_t* __restrict__ gmask) {
+                                                uint32_t* __restrict__ gmask,
+                                                const double* __restrict__ x,
+                                                const double* __restrict__ xs) {
   __shared__ unsigned long long cnt[8][6];
   __shared__ uint32_t cw[32];  // survivor word of each of the CTA's chunks
+  __shared__ double dsh[8];
   __shared__ int base;
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int l = blockIdx.y;
   const int cb = blockIdx.x * 32;  // first chunk
-  const double dp = dpos[l], sg = P.sqrt_g[l];
-  const unsigned long long g = (unsigned long long)(P.off[l + 1] - P.off[l]);
+  const int o0 = P.off[l];
+  const unsigned long long g = (unsigned long long)(P.off[l + 1] - o0);
   double zv[4], db[4];
   uint32_t am[4];
 #pragma unroll
@@ -310,8 +305,30 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
     const bool valid = c < P.nw && j < P.n;
     am[u] = (c < P.nw && aw != nullptr) ? aw[(int64_t)l * P.nw + c] : 0u;
     zv[u] = valid ? zs[(int64_t)l * P.n + j] : 0.0;
-    db[u] = valid ? dbeta[j] : 0.0;
+    db[u] = valid ? (x ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j]) : 0.0;
   }
+  double dp;
+  if (x) {
+    // fused delta (fast mode): |[alpha_l - alpha~_l]+| over the group's rows,
+    // per-thread strided chains, then a fixed tree (every CTA of the group
+    // computes the same bits)
+    double acc = 0.0;
+    for (int r = threadIdx.x; r < (int)g; r += blockDim.x) {
+      const double d = dsub(x[o0 + r], xs[o0 + r]);
+      if (d > 0.0) acc = dadd(acc, dmul(d, d));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) dsh[warp] = acc;
+    __syncthreads();
+    double t = dsh[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t = dadd(t, dsh[w]);
+    dp = sqrt(t);
+  } else {
+    dp = dpos[l];  // k_delta's reference-order norm (exact mode)
+  }
+  const double sg = P.sqrt_g[l];
   unsigned long long my[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -372,10 +389,10 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
-                   cudaStream_t s) {
+                   const double* x, const double* xs, cudaStream_t s) {
   const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)P.L);
   launch_pdl(k_screen, grid, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc,
-             cnt_slots, gmask);
+             cnt_slots, gmask, x, xs);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
