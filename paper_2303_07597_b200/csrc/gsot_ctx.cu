@@ -115,7 +115,7 @@ gsot_ctx::~gsot_ctx() {
                   x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
-                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask};
+                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, tl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -215,6 +215,14 @@ void alloc_buffers(gsot_ctx* c) {
   GSOT_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_sync_dev), c->h_sync, 0));
   GSOT_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_flag_dev), c->h_flag, 0));
   c->d_pub_count = dalloc<unsigned long long>(1, t);
+#ifdef GSOT_PHASE_CLOCKS
+  if (std::getenv("GSOT_TIMELINE")) {  // diagnostic kernel timeline
+    c->tl = dalloc<unsigned long long>(64, t);
+    unsigned long long init[64] = {};
+    for (int k = 0; k < 8; ++k) init[2 * k] = ~0ull;
+    GSOT_CUDA_CHECK(cudaMemcpy(c->tl, init, sizeof(init), cudaMemcpyHostToDevice));
+  }
+#endif
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->d_pub_count, 0, sizeof(unsigned long long), c->stream));
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->dsync, 0, sizeof(gsot::DevSync), c->stream));
   memset(c->h_sync, 0, sizeof(gsot::DevSync) + 128);
@@ -887,3 +895,14 @@ GSOT_API int gsot_timer(gsot_ctx* ctx, int op, double* ms) {
 }
 
 }  // extern "C"
+
+#ifdef GSOT_PHASE_CLOCKS
+// Diagnostic builds: the folded kernel timeline (64 words, see gsot_device.cuh).
+extern "C" __attribute__((visibility("default"))) int gsot_debug_timeline(gsot_ctx* c,
+                                                                          unsigned long long* out) {
+  if (!c || !c->tl) return GSOT_ERR_STATE;
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(out, c->tl, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
+#endif

@@ -83,6 +83,7 @@ struct gsot_ctx {
   unsigned long long* cnt_slots = nullptr;     // screen counters, 64 x 8
   uint32_t *words = nullptr, *dense_words = nullptr;
   uint32_t *gmask = nullptr, *dense_gmask = nullptr;  // per-group non-empty chunk masks
+  unsigned long long* tl = nullptr;  // diagnostic kernel timeline (GSOT_TIMELINE=1, diag builds)
   gsot::TaskDesc* dense_tasks = nullptr;  // every chunk, largest groups first
   gsot::TaskDesc* tasks = nullptr;        // screened work list (non-empty chunks)
   // screening state
@@ -135,6 +136,7 @@ struct gsot_ctx {
     P.gamma = gamma;
     P.mu = mu;
     P.tau = mu * gamma;
+    P.tl = tl;
     return P;
   }
 
@@ -225,7 +227,7 @@ struct gsot_ctx {
   void enqueue_fetch() {
     launch(gsot::K_MISC, 0.0, [&] {
       gsot::launch_publish(dsync, h_sync_dev, d_pub_count, h_flag_dev, partials,
-                           ws ? ws->cpart : nullptr, cnt_slots, stream);
+                           ws ? ws->cpart : nullptr, cnt_slots, tl, stream);
     });
     if (capturing)
       ++capturing->publishes;

@@ -176,6 +176,27 @@ namespace gsot {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Diagnostic kernel timeline (builds with -DGSOT_PHASE_CLOCKS only): per
+// kernel id, the first block entry and the last block exit of the current
+// device sequence (globaltimer ns); k_publish folds them into per-sequence
+// offsets. No-ops in the product build.
+#ifdef GSOT_PHASE_CLOCKS
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_ENTER(tlp, k) \
+  do { if ((tlp) && threadIdx.x == 0) atomicMin(&(tlp)[2 * (k)], gtimer()); } while (0)
+#define TL_EXIT(tlp, k) \
+  do { if ((tlp) && threadIdx.x == 0) atomicMax(&(tlp)[2 * (k) + 1], gtimer()); } while (0)
+#else
+#define TL_ENTER(tlp, k) do { } while (0)
+#define TL_EXIT(tlp, k) do { } while (0)
+#endif
+enum TimelineId { TL_SCREEN = 0, TL_EVAL = 1, TL_FINALIZE = 2, TL_PUBLISH = 3, TL_STEP = 4,
+                  TL_AXPY = 5, TL_DELTA = 6, TL_SNAPSHOT = 7 };
+
 // max(f, 0) by bit operations (f finite): a negative f, -0 included, -> +0.
 __device__ __forceinline__ double relu(double f) {
   const long long b = __double_as_longlong(f);

@@ -55,6 +55,7 @@ struct DevProblem {
   const double* a;        // m
   const double* b;        // n
   double gamma, mu, tau;  // tau = mu * gamma (core.hpp:70)
+  unsigned long long* tl; // diagnostic timeline (GSOT_PHASE_CLOCKS builds only), else null
 };
 
 // Device scalars written by the reduction kernels and read back with one
@@ -206,7 +207,8 @@ struct DevSync {
 // cnt_pending) in a fixed order.
 void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_count,
                     unsigned long long* host_flag, const double* fin_partials,
-                    const double* step_partials, unsigned long long* cnt_slots, cudaStream_t s);
+                    const double* step_partials, unsigned long long* cnt_slots,
+                    unsigned long long* tl, cudaStream_t s);
 
 struct TwoLoopArgs {
   const double* S;  // pair slots: slot s at S + s * stride
@@ -276,6 +278,7 @@ size_t lbfgs_step_partials(int mem);
 void launch_lbfgs_step(int pair, const double* x, const double* xprev, const double* g,
                        const double* gprev, double* S, double* Y, int64_t stride, HistState* h,
                        CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
-                       double* out, EvalScalars* sc, double* part, int mem, cudaStream_t s);
+                       double* out, EvalScalars* sc, double* part, int mem,
+                       unsigned long long* tl, cudaStream_t s);
 
 }  // namespace gsot

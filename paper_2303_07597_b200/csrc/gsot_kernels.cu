@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   __shared__ int base;
   pdl_wait();
   pdl_trigger();
+  TL_ENTER(P.tl, TL_SCREEN);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int l = blockIdx.y;
   const int cb = blockIdx.x * 32;  // first chunk
@@ -384,6 +385,7 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
     for (int w = 0; w < 8; ++w) s += cnt[w][lane];
     if (s) atomicAdd(cnt_slots + ((blockIdx.y * gridDim.x + blockIdx.x) & 63u) * 8 + lane, s);
   }
+  TL_EXIT(P.tl, TL_SCREEN);
 }
 
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
@@ -507,6 +509,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
   __shared__ double scale_sh[32];
   pdl_wait();
   pdl_trigger();
+  TL_ENTER(P.tl, TL_EVAL);
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
@@ -656,6 +659,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
       if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
     }
   }
+  TL_EXIT(P.tl, TL_EVAL);
 }
 
 namespace {
@@ -727,6 +731,7 @@ __global__ void __launch_bounds__(32 * kFinSlices, 4) k_finalize(
   __shared__ uint32_t msk[kFinMaskCap];
   pdl_wait();
   pdl_trigger();
+  TL_ENTER(P.tl, TL_FINALIZE);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double obj[4] = {0.0, 0.0, 0.0, 0.0};  // a.alpha, b.beta, psi, g.d
   if ((int)blockIdx.x < row_blocks) {
@@ -836,6 +841,7 @@ __global__ void __launch_bounds__(32 * kFinSlices, 4) k_finalize(
       sc->cnt_pending = cnt_pending;
     }
   }
+  TL_EXIT(P.tl, TL_FINALIZE);
 }
 
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,

@@ -25,6 +25,7 @@ namespace gsot {
 // trial.x = x + t * d (lbfgs.hpp:86).
 __global__ void k_axpy_point(const double* __restrict__ x, const double* __restrict__ tp,
                              const double* __restrict__ d, double* __restrict__ out, int64_t dim) {
+  pdl_trigger();
   const double t = *tp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
        e += (int64_t)gridDim.x * blockDim.x)
@@ -79,12 +80,14 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
                                                  unsigned long long* host_flag,
                                                  const double* __restrict__ fin_partials,
                                                  const double* __restrict__ step_partials,
-                                                 unsigned long long* cnt_slots) {
+                                                 unsigned long long* cnt_slots,
+                                                 unsigned long long* tl) {
   static_assert(offsetof(DevSync, t) % 8 == 0, "DevSync is copied as 8-byte words");
 #ifdef GSOT_PHASE_CLOCKS
   long long clk_prev = clock64();
 #endif
   pdl_wait();
+  TL_ENTER(tl, TL_PUBLISH);
   EvalScalars* sc = &src->sc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fin = sc->fin_blocks, step = sc->step_blocks, cnt = sc->cnt_pending;
@@ -142,14 +145,31 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
     __threadfence_system();
     PHASE_MARK(13);
     *reinterpret_cast<volatile unsigned long long*>(host_flag) = c;
+#ifdef GSOT_PHASE_CLOCKS
+    if (tl) {  // fold this sequence's kernel windows into offsets from its first entry
+      TL_EXIT(tl, TL_PUBLISH);
+      unsigned long long s0 = ~0ull;
+      for (int k = 0; k < 8; ++k) s0 = tl[2 * k] < s0 ? tl[2 * k] : s0;
+      for (int k = 0; k < 8; ++k)
+        if (tl[2 * k] != ~0ull) {
+          tl[16 + 4 * k] += tl[2 * k] - s0;
+          tl[16 + 4 * k + 1] += tl[2 * k + 1] - s0;
+          tl[16 + 4 * k + 2] += 1;
+          tl[2 * k] = ~0ull;
+          tl[2 * k + 1] = 0;
+        }
+      tl[63] += 1;
+    }
+#endif
   }
 }
 
 void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_count,
                     unsigned long long* host_flag, const double* fin_partials,
-                    const double* step_partials, unsigned long long* cnt_slots, cudaStream_t s) {
+                    const double* step_partials, unsigned long long* cnt_slots,
+                    unsigned long long* tl, cudaStream_t s) {
   launch_pdl(k_publish, dim3(1), dim3(256), 0, s, src, host_dst, dev_count, host_flag,
-             fin_partials, step_partials, cnt_slots);
+             fin_partials, step_partials, cnt_slots, tl);
 }
 
 __global__ void k_hist_reset(HistState* h, int mem) {
@@ -232,6 +252,7 @@ struct StepArgs {
   EvalScalars* sc;
   double* part;     // [kStepMaxGrid][2] slope partials, then [grid][KS * 5] dot partials
   int ks;           // memory + 1: leading dimension of R / YY in shared memory
+  unsigned long long* tl;  // diagnostic timeline or null
 };
 
 
@@ -271,6 +292,8 @@ __device__ __forceinline__ void grid_fold(const double* part, int nc, int ld, in
 
 __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
   cg::grid_group grid = cg::this_grid();
+  pdl_trigger();  // the screen may launch early; it waits for this grid
+  TL_ENTER(A.tl, TL_STEP);
 #ifdef GSOT_PHASE_CLOCKS
   long long clk_prev = clock64();
 #endif
@@ -630,6 +653,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->step_blocks = nc;
   PHASE_MARK(10);
+  TL_EXIT(A.tl, TL_STEP);
 }
 
 #ifdef GSOT_PHASE_CLOCKS
@@ -660,9 +684,10 @@ size_t lbfgs_step_partials(int mem) {
 void launch_lbfgs_step(int pair, const double* x, const double* xprev, const double* g,
                        const double* gprev, double* S, double* Y, int64_t stride, HistState* h,
                        CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
-                       double* out, EvalScalars* sc, double* part, int mem, cudaStream_t s) {
+                       double* out, EvalScalars* sc, double* part, int mem,
+                       unsigned long long* tl, cudaStream_t s) {
   const int grid = lbfgs_step_grid();
-  StepArgs A{pair, x, xprev, g, gprev, S, Y, stride, h, cs, d, t, xt, dim, out, sc, part, mem + 1};
+  StepArgs A{pair, x, xprev, g, gprev, S, Y, stride, h, cs, d, t, xt, dim, out, sc, part, mem + 1, tl};
   const size_t smem = sizeof(double) * 2 * (size_t)(mem + 1) * (mem + 1);
   if (smem > 48 * 1024 && smem > g_step_smem) {
     cudaFuncSetAttribute(k_lbfgs_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

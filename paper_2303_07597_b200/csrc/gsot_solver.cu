@@ -243,7 +243,7 @@ class Solver {
       launch_lbfgs_step(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->S, w_->Y,
                         w_->dim, &c_->dsync->h, w_->cs, w_->d, t_dev(),
                         trial ? w_->X[q] : nullptr, w_->dim, c_->dsync->tl, c_->sc, w_->cpart, mem_,
-                        c_->stream);
+                        c_->tl, c_->stream);
     });
   }
 
