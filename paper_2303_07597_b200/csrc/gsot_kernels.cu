@@ -719,125 +719,152 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
 // Block (32, 8): blocks [0, m/32) handle 32 rows, the rest 32 columns.
 constexpr int kFinSlices = 8;
 constexpr int kFinBatch = 8;
-constexpr int kFinMaskCap = 2048;  // mask words staged per row block
+constexpr int kFinMaskCap = 1024;  // mask words staged per row unit
 
-__global__ void __launch_bounds__(32 * kFinSlices, 4) k_finalize(
+// Block = two independent units of (32 rows or columns) x 8 slices. Everything
+// that does not depend on the evaluation (x, d, marginals, the chunk masks and
+// survivor words written by the screen, which completed before the evaluation
+// started) is loaded before the programmatic wait.
+__global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
     DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
     const uint32_t* __restrict__ gmask, const double* __restrict__ rowpart,
     const double* __restrict__ colpart, const double* __restrict__ psi, double* __restrict__ grad,
     const double* __restrict__ dvec, double* __restrict__ partials, EvalScalars* sc,
-    int cnt_pending, int row_blocks) {
-  __shared__ double sh[2][kFinSlices][33];
-  __shared__ uint32_t msk[kFinMaskCap];
+    int cnt_pending, int row_blocks, int units) {
+  __shared__ double sh[2][2][kFinSlices][33];
+  __shared__ uint32_t msk[2][kFinMaskCap];
+  const int half = threadIdx.x >> 8, t = threadIdx.x & 255;
+  const int tx = t & 31, ty = t >> 5;
+  const int unit = 2 * blockIdx.x + half;
+  const bool is_row = unit < row_blocks;
+  const bool live = unit < units;
+  double obj[4] = {0.0, 0.0, 0.0, 0.0};  // a.alpha, b.beta, psi, g.d
+  double acc = 0.0, ps = 0.0;
+  // ---- before the wait
+  int64_t i = -1, j = -1;
+  double marg = 0.0, xv = 0.0, dv = 0.0;
+  const int nmw = (P.nw + 31) / 32;
+  int lf = 0;
+  bool staged = false;
+  bool on[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) on[u] = false;
+  if (live && is_row) {
+    const int64_t i0 = unit * 32ll;
+    i = i0 + tx < P.m ? i0 + tx : -1;
+    if (i >= 0) {
+      marg = P.a[i];
+      xv = x[i];
+      dv = dvec ? dvec[i] : 0.0;
+    }
+    lf = P.row_group[i0];
+    const int ll = P.row_group[P.m - 1 < i0 + 31 ? P.m - 1 : i0 + 31];
+    staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
+    if (staged)
+      for (int k = t; k < (ll - lf + 1) * nmw; k += 256) msk[half][k] = gmask[(int64_t)lf * nmw + k];
+  } else if (live) {
+    const int64_t jj = (unit - row_blocks) * 32ll + tx;
+    j = jj < P.n ? jj : -1;
+    if (j >= 0) {
+      marg = P.b[j];
+      xv = x[P.m + j];
+      dv = dvec ? dvec[P.m + j] : 0.0;
+      const int64_t c = j >> 5;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {  // groups l = ty + 8u (L <= 128 in one round)
+        const int l = ty + kFinSlices * u;
+        on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
+      }
+    }
+  }
+  __syncthreads();
   pdl_wait();
   pdl_trigger();
   TL_ENTER(P.tl, TL_FINALIZE);
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  double obj[4] = {0.0, 0.0, 0.0, 0.0};  // a.alpha, b.beta, psi, g.d
-  if ((int)blockIdx.x < row_blocks) {
-    const int nmw = (P.nw + 31) / 32;
-    const int64_t i0 = blockIdx.x * 32ll;
-    const int lf = P.row_group[i0];
-    const int ll = P.row_group[P.m - 1 < i0 + 31 ? P.m - 1 : i0 + 31];
-    const bool staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
-    if (staged)
-      for (int k = threadIdx.x; k < (ll - lf + 1) * nmw; k += blockDim.x)
-        msk[k] = gmask[(int64_t)lf * nmw + k];
-    __syncthreads();
-    const int64_t i = i0 + tx;
-    double acc = 0.0;
-    if (i < P.m) {
-      const int l = P.row_group[i];
-      const uint32_t* gm = staged ? msk + (int64_t)(l - lf) * nmw : gmask + (int64_t)l * nmw;
-      const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
-      int k = 0;
-      uint32_t cur = nmw > 0 ? gm[0] & sel : 0u;
-      for (;;) {  // batches of the slice's non-empty chunks, ascending c
-        int idx[kFinBatch];
-        int cnt = 0;
+  if (i >= 0) {
+    const int l = P.row_group[i];
+    const uint32_t* gm = staged ? msk[half] + (int64_t)(l - lf) * nmw : gmask + (int64_t)l * nmw;
+    const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
+    int k = 0;
+    uint32_t cur = nmw > 0 ? gm[0] & sel : 0u;
+    for (;;) {  // batches of the slice's non-empty chunks, ascending c
+      int idx[kFinBatch];
+      int cnt = 0;
 #pragma unroll
-        for (int q = 0; q < kFinBatch; ++q) {
-          while (cur == 0u && k + 1 < nmw) cur = gm[++k] & sel;
-          idx[q] = -1;
-          if (cur != 0u) {
-            const int b = __ffs(cur) - 1;
-            cur &= cur - 1u;
-            idx[q] = 32 * k + b;
-            ++cnt;
-          }
+      for (int q = 0; q < kFinBatch; ++q) {
+        while (cur == 0u && k + 1 < nmw) cur = gm[++k] & sel;
+        idx[q] = -1;
+        if (cur != 0u) {
+          const int b = __ffs(cur) - 1;
+          cur &= cur - 1u;
+          idx[q] = 32 * k + b;
+          ++cnt;
         }
-        if (cnt == 0) break;
-        double v[kFinBatch];
-#pragma unroll
-        for (int q = 0; q < kFinBatch; ++q) v[q] = idx[q] >= 0 ? rowpart[(int64_t)idx[q] * P.m + i] : 0.0;
-#pragma unroll
-        for (int q = 0; q < kFinBatch; ++q)
-          if (idx[q] >= 0) acc = dadd(acc, v[q]);
-        if (cnt < kFinBatch) break;
       }
+      if (cnt == 0) break;
+      double v[kFinBatch];
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q) v[q] = idx[q] >= 0 ? rowpart[(int64_t)idx[q] * P.m + i] : 0.0;
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q)
+        if (idx[q] >= 0) acc = dadd(acc, v[q]);
+      if (cnt < kFinBatch) break;
     }
-    sh[0][ty][tx] = acc;
-    __syncthreads();
-    if (ty == 0 && i < P.m) {
-      double s = sh[0][0][tx];
-      for (int q = 1; q < kFinSlices; ++q) s = dadd(s, sh[0][q][tx]);
-      const double gi = dsub(P.a[i], s);
-      grad[i] = gi;
-      obj[0] = dmul(x[i], P.a[i]);
-      if (dvec) obj[3] = dmul(gi, dvec[i]);
-    }
-  } else {
-    const int64_t j = (blockIdx.x - row_blocks) * 32ll + tx;
-    double acc = 0.0, ps = 0.0;
-    if (j < P.n) {
-      const int64_t c = j >> 5;
-      for (int l0 = ty; l0 < P.L; l0 += kFinSlices * 16) {
-        bool on[16];
+  } else if (j >= 0) {
+    for (int l0 = ty; l0 < P.L; l0 += kFinSlices * 16) {
+      if (l0 != ty) {  // more than 128 groups: the next round of survivor bits
+        const int64_t c = j >> 5;
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int l = l0 + kFinSlices * u;
           on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
         }
-        double cp[16], pp[16];
+      }
+      double cp[16], pp[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int64_t idx = (int64_t)(l0 + kFinSlices * u) * P.n + j;
-          cp[u] = on[u] ? colpart[idx] : 0.0;
-          pp[u] = on[u] ? psi[idx] : 0.0;
+      for (int u = 0; u < 16; ++u) {
+        const int64_t idx = (int64_t)(l0 + kFinSlices * u) * P.n + j;
+        cp[u] = on[u] ? colpart[idx] : 0.0;
+        pp[u] = on[u] ? psi[idx] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (on[u]) {
+          acc = dadd(acc, cp[u]);
+          ps = dadd(ps, pp[u]);
         }
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-          if (on[u]) {
-            acc = dadd(acc, cp[u]);
-            ps = dadd(ps, pp[u]);
-          }
-      }
-    }
-    sh[0][ty][tx] = acc;
-    sh[1][ty][tx] = ps;
-    __syncthreads();
-    if (ty == 0 && j < P.n) {
-      double s = sh[0][0][tx], p = sh[1][0][tx];
-      for (int q = 1; q < kFinSlices; ++q) {
-        s = dadd(s, sh[0][q][tx]);
-        p = dadd(p, sh[1][q][tx]);
-      }
-      const double gj = dsub(P.b[j], s);
-      grad[P.m + j] = gj;
-      obj[1] = dmul(x[P.m + j], P.b[j]);
-      obj[2] = p;
-      if (dvec) obj[3] = dmul(gj, dvec[P.m + j]);
     }
   }
-  if (ty == 0) {  // warp 0 holds the 32 rows / columns: fixed xor tree
+  sh[half][0][ty][tx] = acc;
+  sh[half][1][ty][tx] = ps;
+  __syncthreads();
+  if (ty == 0 && live) {
+    if (i >= 0 || j >= 0) {
+      double s = sh[half][0][0][tx], p = sh[half][1][0][tx];
+      for (int q = 1; q < kFinSlices; ++q) {
+        s = dadd(s, sh[half][0][q][tx]);
+        p = dadd(p, sh[half][1][q][tx]);
+      }
+      const double gv = dsub(marg, s);
+      if (i >= 0) {
+        grad[i] = gv;
+        obj[0] = dmul(xv, marg);
+      } else {
+        grad[P.m + j] = gv;
+        obj[1] = dmul(xv, marg);
+        obj[2] = p;
+      }
+      if (dvec) obj[3] = dmul(gv, dv);
+    }
+    // warp 0 of the unit holds its 32 rows / columns: fixed xor tree
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
       for (int o = 1; o <= 16; o <<= 1) obj[q] = dadd(obj[q], __shfl_xor_sync(0xffffffffu, obj[q], o));
     }
-    if (tx < 4) partials[blockIdx.x * 4 + tx] = obj[tx == 0 ? 0 : tx == 1 ? 1 : tx == 2 ? 2 : 3];
-    if (blockIdx.x == 0 && tx == 0) {
-      sc->fin_blocks = (int)gridDim.x;
+    if (tx < 4) partials[unit * 4 + tx] = obj[tx == 0 ? 0 : tx == 1 ? 1 : tx == 2 ? 2 : 3];
+    if (unit == 0 && tx == 0) {
+      sc->fin_blocks = units;
       sc->cnt_pending = cnt_pending;
     }
   }
@@ -850,8 +877,9 @@ void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words
                      EvalScalars* sc, int cnt_pending, cudaStream_t s) {
   const int rb = (int)((P.m + 31) / 32);
   const int cb = (int)((P.n + 31) / 32);
-  launch_pdl(k_finalize, dim3(rb + cb), dim3(32 * kFinSlices), 0, s, P, x, words, gmask, rowpart,
-             colpart, psi, grad, dvec, partials, sc, cnt_pending, rb);
+  const int units = rb + cb;
+  launch_pdl(k_finalize, dim3((units + 1) / 2), dim3(64 * kFinSlices), 0, s, P, x, words, gmask,
+             rowpart, colpart, psi, grad, dvec, partials, sc, cnt_pending, rb, units);
 }
 
 // ---------------------------------------------------------------- plan
