@@ -115,7 +115,7 @@ gsot_ctx::~gsot_ctx() {
                   x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
-                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, tl};
+                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -196,6 +196,9 @@ void alloc_buffers(gsot_ctx* c) {
   c->dense_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->gmask = dalloc<uint32_t>(static_cast<size_t>(L) * ((nw + 31) / 32), t);
   c->dense_gmask = dalloc<uint32_t>(static_cast<size_t>(L) * ((nw + 31) / 32), t);
+  c->cmask = dalloc<uint32_t>(static_cast<size_t>(nw) * ((L + 31) / 32), t);
+  c->dense_cmask = dalloc<uint32_t>(static_cast<size_t>(nw) * ((L + 31) / 32), t);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->cmask, 0, sizeof(uint32_t) * nw * ((L + 31) / 32), c->stream));
   c->dense_tasks = dalloc<gsot::TaskDesc>(static_cast<size_t>(L) * nw, t);
   c->tasks = dalloc<gsot::TaskDesc>(static_cast<size_t>(L) * nw, t);
   c->snap_x = dalloc<double>(dim + 8, t);
@@ -252,6 +255,7 @@ void alloc_buffers(gsot_ctx* c) {
                                   cudaMemcpyHostToDevice, c->stream));
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_words(c->dense_words, c->L, c->nw, c->n, c->stream); });
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_gmask(c->dense_gmask, c->L, c->nw, c->stream); });
+  c->launch(gsot::K_MISC, 0, [&] { gsot::launch_fill_cmask(c->dense_cmask, c->L, c->nw, c->stream); });
   c->launch(gsot::K_MISC, 0, [&] { gsot::launch_dense_tasks(c->problem(), c->dense_tasks, c->d_group_order, c->stream); });
   // Persistent eval grid: two shared-memory segments of up to 128 rows per
   // CTA (the tallest group when it fits), as many CTAs per SM as shared
@@ -378,7 +382,7 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
 namespace gsot {
 
 void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad,
-                  const double* d_dir, double ub_offset, bool use_active) {
+                  const double* d_dir, double ub_offset, bool use_active, bool dbeta_ready) {
   const bool exact = (mode_flags & GSOT_EVAL_EXACT) != 0;
   const int mode = mode_flags & 1;
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
@@ -396,7 +400,8 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
                     ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
-                    exact ? nullptr : d_x, exact ? nullptr : c->snap_x, c->stream);
+                    exact ? nullptr : c->cmask, exact ? nullptr : d_x,
+                    exact ? nullptr : c->snap_x, dbeta_ready ? 1 : 0, c->num_sms, c->stream);
     });
     words = c->words;
   }
@@ -417,9 +422,10 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
                   c->psi, c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
-    launch_finalize(P, d_x, words, mode == GSOT_EVAL_SCREENED ? c->gmask : c->dense_gmask,
-                    c->rowpart, c->colpart, c->psi, d_grad, d_dir, c->partials, c->sc,
-                    mode == GSOT_EVAL_SCREENED ? 1 : 0, c->stream);
+    const bool scr = mode == GSOT_EVAL_SCREENED;
+    launch_finalize(P, d_x, words, scr ? c->gmask : c->dense_gmask,
+                    scr ? c->cmask : c->dense_cmask, scr ? 1 : 0, c->rowpart, c->colpart,
+                    c->psi, d_grad, d_dir, c->partials, c->sc, scr ? 1 : 0, c->stream);
   });
 }
 

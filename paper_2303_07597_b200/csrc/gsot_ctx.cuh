@@ -83,6 +83,7 @@ struct gsot_ctx {
   unsigned long long* cnt_slots = nullptr;     // screen counters, 64 x 8
   uint32_t *words = nullptr, *dense_words = nullptr;
   uint32_t *gmask = nullptr, *dense_gmask = nullptr;  // per-group non-empty chunk masks
+  uint32_t *cmask = nullptr, *dense_cmask = nullptr;  // per-chunk non-empty group masks
   unsigned long long* tl = nullptr;  // diagnostic kernel timeline (GSOT_TIMELINE=1, diag builds)
   gsot::TaskDesc* dense_tasks = nullptr;  // every chunk, largest groups first
   gsot::TaskDesc* tasks = nullptr;        // screened work list (non-empty chunks)
@@ -269,8 +270,9 @@ struct EvalOut {
 // Enqueue the fused evaluation at device state d_x (length m+n) into d_grad,
 // with the line-search slope against d_dir when non-null. No sync; the
 // scalars land in c->dsync->sc.
+// dbeta_ready: the kernel that produced d_x also wrote c->dbeta (fast solves).
 void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, const double* d_dir,
-                  double ub_offset, bool use_active);
+                  double ub_offset, bool use_active, bool dbeta_ready = false);
 // Read back the result of the last enqueue_eval after c->fetch_scalars().
 EvalOut eval_result(gsot_ctx* c, int mode);
 EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,

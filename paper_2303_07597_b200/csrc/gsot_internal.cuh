@@ -146,7 +146,8 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
-                   const double* x, const double* xs, cudaStream_t s);
+                   uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
+                   int num_sms, cudaStream_t s);
 // Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
 size_t eval_smem_bytes(int buf_rows, int cap);
@@ -158,9 +159,10 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
                  double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
-                     const uint32_t* gmask, const double* rowpart, const double* colpart,
-                     const double* psi, double* grad, const double* dvec, double* partials,
-                     EvalScalars* sc, int cnt_pending, cudaStream_t s);
+                     const uint32_t* gmask, uint32_t* cmask, int clear_cmask,
+                     const double* rowpart, const double* colpart, const double* psi,
+                     double* grad, const double* dvec, double* partials, EvalScalars* sc,
+                     int cnt_pending, cudaStream_t s);
 void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,
                          double* out, cudaStream_t s);
 void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* words,
@@ -169,6 +171,8 @@ void launch_audit_active(const DevProblem& P, const double* x, const uint32_t* a
                          EvalScalars* sc, cudaStream_t s);
 void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaStream_t s);
 void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s);
+// Per-chunk group masks cmask[c][l / 32] bit l % 32: (l, c) non-empty.
+void launch_fill_cmask(uint32_t* cmask, int32_t L, int32_t nw, cudaStream_t s);
 void launch_dense_tasks(const DevProblem& P, TaskDesc* tasks, const int32_t* group_order,
                         cudaStream_t s);
 
@@ -221,8 +225,10 @@ struct TwoLoopArgs {
   double* out;  // [0] = g.d, [1] = d.d
 };
 // trial.x = x + t * d with t read from device memory.
+// trial.x = x + t * d with t read from device memory; with dbeta != null also
+// dbeta_j = out[m + j] - snap[m + j] for the screen.
 void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
-                       int64_t dim, cudaStream_t s);
+                       int64_t dim, int64_t m, const double* snap, double* dbeta, cudaStream_t s);
 void launch_hist_reset(HistState* h, int mem, cudaStream_t s);
 void launch_dot(const double* a, const double* b, int64_t dim, double* partials, int nblocks,
                 EvalScalars* sc, int slot, cudaStream_t s);
@@ -279,6 +285,7 @@ void launch_lbfgs_step(int pair, const double* x, const double* xprev, const dou
                        const double* gprev, double* S, double* Y, int64_t stride, HistState* h,
                        CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
                        double* out, EvalScalars* sc, double* part, int mem,
-                       unsigned long long* tl, cudaStream_t s);
+                       unsigned long long* tl, int64_t m, const double* snap, double* dbeta,
+                       cudaStream_t s);
 
 }  // namespace gsot

@@ -269,12 +269,14 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 // FastGradDispatcher::column's per-block decision (screening.hpp:252-275):
 // active-set members are computed without a bound; every other block gets
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
-// skipped iff z_bar <= tau. CTA (k, l) screens the 32 chunks of group l
-// covered by chunk-mask word k (1024 columns); each warp takes four chunks
-// with all loads in flight and writes their survivor words. The CTA writes
-// its chunk-mask word, reserves its non-empty chunks' work-list slots with
-// ONE atomic, and adds its GradStats::PerCall counters into one of 64 slots
-// (integers: order-free).
+// skipped iff z_bar <= tau. CTA (k, l) screens the 64 chunks of group l
+// covered by chunk-mask words 2k, 2k+1 (2048 columns); each warp takes eight
+// chunks with all loads in flight and writes their survivor words. The CTA
+// writes its chunk-mask words, (fast mode) marks its non-empty chunks in the
+// per-chunk group masks, reserves their work-list slots with ONE atomic, and
+// adds its GradStats::PerCall counters into one of 64 slots (integers:
+// order-free). One CTA per unit keeps every unit's short dependency chain
+// overlapped with the others on the SM.
 __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
                                                 const double* __restrict__ dpos,
@@ -283,10 +285,11 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 TaskDesc* __restrict__ tasks, EvalScalars* sc,
                                                 unsigned long long* __restrict__ cnt_slots,
                                                 uint32_t* __restrict__ gmask,
+                                                uint32_t* __restrict__ cmask,
                                                 const double* __restrict__ x,
-                                                const double* __restrict__ xs) {
+                                                const double* __restrict__ xs, int dbeta_ready) {
   __shared__ unsigned long long cnt[8][6];
-  __shared__ uint32_t cw[32];  // survivor word of each of the CTA's chunks
+  __shared__ uint32_t cw[64];  // survivor word of each of the CTA's chunks
   __shared__ double dsh[8];
   __shared__ int base;
   pdl_wait();
@@ -294,19 +297,22 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   TL_ENTER(P.tl, TL_SCREEN);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int l = blockIdx.y;
-  const int cb = blockIdx.x * 32;  // first chunk
+  const int cb = blockIdx.x * 64;  // first chunk (two chunk-mask words per CTA)
   const int o0 = P.off[l];
   const unsigned long long g = (unsigned long long)(P.off[l + 1] - o0);
-  double zv[4], db[4];
-  uint32_t am[4];
+  // dbeta from memory (exact mode: k_delta; fast solves: the step / trial
+  // kernels), else inline from x and the snapshot
+  const bool db_inline = x != nullptr && !dbeta_ready;
+  double zv[8], db[8];
+  uint32_t am[8];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {  // chunk cb + warp + 8u, all loads first
+  for (int u = 0; u < 8; ++u) {  // chunk cb + warp + 8u, all loads first
     const int c = cb + warp + 8 * u;
     const int64_t j = (int64_t)c * 32 + lane;
     const bool valid = c < P.nw && j < P.n;
     am[u] = (c < P.nw && aw != nullptr) ? aw[(int64_t)l * P.nw + c] : 0u;
     zv[u] = valid ? zs[(int64_t)l * P.n + j] : 0.0;
-    db[u] = valid ? (x ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j]) : 0.0;
+    db[u] = valid ? (db_inline ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j]) : 0.0;
   }
   double dp;
   if (x) {
@@ -330,55 +336,68 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
     dp = dpos[l];  // k_delta's reference-order norm (exact mode)
   }
   const double sg = P.sqrt_g[l];
-  unsigned long long my[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+  uint32_t my[6] = {0u, 0u, 0u, 0u, 0u, 0u};  // per CTA: at most 2048 blocks x g rows
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < 8; ++u) {
     const int c = cb + warp + 8 * u;
-    const int64_t j = (int64_t)c * 32 + lane;
-    const bool valid = c < P.nw && j < P.n;
-    const bool in_active = valid && ((am[u] >> lane) & 1u);
-    const bool evaluated = valid && !in_active;
-    bool surv = in_active;
-    if (evaluated) {
-      const double db_pos = db[u] > 0.0 ? db[u] : 0.0;
-      const double zbar = dadd(dadd(dadd(zv[u], dp), dmul(sg, db_pos)), ub_offset);
+    const int64_t j0 = (int64_t)c * 32;
+    // valid columns of the chunk; active-set members come straight from the word
+    const uint32_t vmask = c >= P.nw ? 0u : (P.n - j0 >= 32 ? 0xffffffffu : ((1u << (P.n - j0)) - 1u));
+    const uint32_t wa = am[u] & vmask;
+    const uint32_t we = vmask & ~wa;
+    bool surv = false;
+    if ((we >> lane) & 1u) {
+      const double zbar = dadd(dadd(dadd(zv[u], dp), dmul(sg, relu(db[u]))), ub_offset);
       surv = !(zbar <= P.tau);
     }
-    const unsigned wa = __ballot_sync(0xffffffffu, in_active);
-    const unsigned we = __ballot_sync(0xffffffffu, evaluated);
-    const unsigned ws = __ballot_sync(0xffffffffu, surv);
+    const uint32_t ws = __ballot_sync(0xffffffffu, surv) | wa;
     if (lane == 0) {
       if (c < P.nw) words[(int64_t)l * P.nw + c] = ws;
       cw[warp + 8 * u] = ws;
+      const uint32_t ns = __popc(ws), ne = __popc(we), nsv = __popc(we & ws);
       my[0] += __popc(wa);
-      my[1] += __popc(we & ~ws);
-      my[2] += __popc(we & ws);
-      my[3] += __popc(we);
-      my[4] += (unsigned long long)__popc(ws) * g;  // survivors' rows
-      my[5] += ws ? g : 0ull;                       // task rows
+      my[1] += ne - nsv;
+      my[2] += nsv;
+      my[3] += ne;
+      my[4] += ns * (uint32_t)g;      // survivors' rows
+      my[5] += ws ? (uint32_t)g : 0u;  // task rows
     }
   }
   if (lane == 0)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) cnt[warp][k] = my[k];
+    for (int k = 0; k < 6; ++k) cnt[warp][k] = my[k];  // widened
   __syncthreads();
-  if (warp == 0) {  // chunk mask word, work-list slots (chunk order within the CTA)
-    const uint32_t w = cw[lane];
-    const unsigned ne = __ballot_sync(0xffffffffu, w != 0u);
+  if (warp == 0) {  // chunk-mask words, work-list slots (chunk order within the CTA)
+    const uint32_t w0 = cw[lane], w1 = cw[32 + lane];
+    const unsigned ne0 = __ballot_sync(0xffffffffu, w0 != 0u);
+    const unsigned ne1 = __ballot_sync(0xffffffffu, w1 != 0u);
+    const int nmw = (P.nw + 31) / 32;
     if (lane == 0) {
-      gmask[(int64_t)l * ((P.nw + 31) / 32) + blockIdx.x] = ne;
-      base = ne ? atomicAdd(&sc->ntasks, __popc(ne)) : 0;
+      gmask[(int64_t)l * nmw + 2 * blockIdx.x] = ne0;
+      if (2 * (int)blockIdx.x + 1 < nmw) gmask[(int64_t)l * nmw + 2 * blockIdx.x + 1] = ne1;
+      const int tot = __popc(ne0) + __popc(ne1);
+      base = tot ? atomicAdd(&sc->ntasks, tot) : 0;
+    }
+    const int nlw = (P.L + 31) / 32;
+    if (cmask) {
+      if (w0 != 0u) atomicOr(cmask + (int64_t)(cb + lane) * nlw + (l >> 5), 1u << (l & 31));
+      if (w1 != 0u) atomicOr(cmask + (int64_t)(cb + 32 + lane) * nlw + (l >> 5), 1u << (l & 31));
     }
     __syncwarp();
-    if (w != 0u) {
-      TaskDesc d;
-      d.l = l;
+    TaskDesc d;
+    d.l = l;
+    d.o0 = o0;
+    d.g = (int)g;
+    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    if (w0 != 0u) {
       d.c = cb + lane;
-      d.o0 = P.off[l];
-      d.g = (int)g;
-      d.word = w;
-      d.pad[0] = d.pad[1] = d.pad[2] = 0;
-      tasks[base + __popc(ne & ((1u << lane) - 1u))] = d;
+      d.word = w0;
+      tasks[base + __popc(ne0 & ((1u << lane) - 1u))] = d;
+    }
+    if (w1 != 0u) {
+      d.c = cb + 32 + lane;
+      d.word = w1;
+      tasks[base + __popc(ne0) + __popc(ne1 & ((1u << lane) - 1u))] = d;
     }
   } else if (warp == 1 && lane < 6) {
     unsigned long long s = 0ull;
@@ -391,10 +410,12 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
-                   const double* x, const double* xs, cudaStream_t s) {
-  const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)P.L);
+                   uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
+                   int num_sms, cudaStream_t s) {
+  (void)num_sms;
+  const dim3 grid((unsigned)((P.nw + 63) / 64), (unsigned)P.L);
   launch_pdl(k_screen, grid, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc,
-             cnt_slots, gmask, x, xs);
+             cnt_slots, gmask, cmask, x, xs, dbeta_ready);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
@@ -422,6 +443,20 @@ __global__ void k_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw) {
 void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s) {
   const int64_t total = (int64_t)L * ((nw + 31) / 32);
   k_fill_gmask<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(gmask, L, nw);
+}
+
+// Dense per-chunk group masks: every group of every chunk.
+__global__ void k_fill_cmask(uint32_t* cmask, int32_t L, int32_t nw) {
+  const int nlw = (L + 31) / 32;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nw * nlw) return;
+  const int k = (int)(t % nlw);
+  const int rem = L - 32 * k;
+  cmask[t] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+}
+void launch_fill_cmask(uint32_t* cmask, int32_t L, int32_t nw, cudaStream_t s) {
+  const int64_t total = (int64_t)nw * ((L + 31) / 32);
+  k_fill_cmask<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(cmask, L, nw);
 }
 
 // Dense task order: largest groups first (long chains start early).
@@ -727,10 +762,10 @@ constexpr int kFinMaskCap = 1024;  // mask words staged per row unit
 // started) is loaded before the programmatic wait.
 __global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
     DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
-    const uint32_t* __restrict__ gmask, const double* __restrict__ rowpart,
-    const double* __restrict__ colpart, const double* __restrict__ psi, double* __restrict__ grad,
-    const double* __restrict__ dvec, double* __restrict__ partials, EvalScalars* sc,
-    int cnt_pending, int row_blocks, int units) {
+    const uint32_t* __restrict__ gmask, uint32_t* __restrict__ cmask, int clear_cmask,
+    const double* __restrict__ rowpart, const double* __restrict__ colpart,
+    const double* __restrict__ psi, double* __restrict__ grad, const double* __restrict__ dvec,
+    double* __restrict__ partials, EvalScalars* sc, int cnt_pending, int row_blocks, int units) {
   __shared__ double sh[2][2][kFinSlices][33];
   __shared__ uint32_t msk[2][kFinMaskCap];
   const int half = threadIdx.x >> 8, t = threadIdx.x & 255;
@@ -746,9 +781,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
   const int nmw = (P.nw + 31) / 32;
   int lf = 0;
   bool staged = false;
-  bool on[16];
-#pragma unroll
-  for (int u = 0; u < 16; ++u) on[u] = false;
+  const int nlw = (P.L + 31) / 32;
   if (live && is_row) {
     const int64_t i0 = unit * 32ll;
     i = i0 + tx < P.m ? i0 + tx : -1;
@@ -763,21 +796,21 @@ __global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
     if (staged)
       for (int k = t; k < (ll - lf + 1) * nmw; k += 256) msk[half][k] = gmask[(int64_t)lf * nmw + k];
   } else if (live) {
-    const int64_t jj = (unit - row_blocks) * 32ll + tx;
+    const int64_t c = unit - row_blocks;
+    const int64_t jj = c * 32 + tx;
     j = jj < P.n ? jj : -1;
     if (j >= 0) {
       marg = P.b[j];
       xv = x[P.m + j];
       dv = dvec ? dvec[P.m + j] : 0.0;
-      const int64_t c = j >> 5;
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {  // groups l = ty + 8u (L <= 128 in one round)
-        const int l = ty + kFinSlices * u;
-        on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
-      }
     }
+    staged = nlw <= kFinMaskCap;  // the chunk's group mask (non-empty (l, c))
+    if (staged)
+      for (int k = t; k < nlw; k += 256) msk[half][k] = cmask[c * nlw + k];
   }
   __syncthreads();
+  if (clear_cmask && live && !is_row && staged)  // consumed: empty for the next screen
+    for (int k = t; k < nlw; k += 256) cmask[(unit - row_blocks) * (int64_t)nlw + k] = 0u;
   pdl_wait();
   pdl_trigger();
   TL_ENTER(P.tl, TL_FINALIZE);
@@ -811,28 +844,44 @@ __global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
       if (cnt < kFinBatch) break;
     }
   } else if (j >= 0) {
-    for (int l0 = ty; l0 < P.L; l0 += kFinSlices * 16) {
-      if (l0 != ty) {  // more than 128 groups: the next round of survivor bits
-        const int64_t c = j >> 5;
+    const int64_t c = j >> 5;
+    const uint32_t* cm = staged ? msk[half] : cmask + c * nlw;
+    const uint32_t sel = 0x01010101u << ty;  // groups l = ty mod 8 within a mask word
+    int k = 0;
+    uint32_t cur = nlw > 0 ? cm[0] & sel : 0u;
+    for (;;) {  // batches of the slice's non-empty (l, c), ascending l
+      int gl[kFinBatch];
+      int cnt = 0;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int l = l0 + kFinSlices * u;
-          on[u] = l < P.L && ((words[(int64_t)l * P.nw + c] >> tx) & 1u);
+      for (int q = 0; q < kFinBatch; ++q) {
+        while (cur == 0u && k + 1 < nlw) cur = cm[++k] & sel;
+        gl[q] = -1;
+        if (cur != 0u) {
+          const int b = __ffs(cur) - 1;
+          cur &= cur - 1u;
+          gl[q] = 32 * k + b;
+          ++cnt;
         }
       }
-      double cp[16], pp[16];
+      if (cnt == 0) break;
+      bool on[kFinBatch];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int64_t idx = (int64_t)(l0 + kFinSlices * u) * P.n + j;
-        cp[u] = on[u] ? colpart[idx] : 0.0;
-        pp[u] = on[u] ? psi[idx] : 0.0;
+      for (int q = 0; q < kFinBatch; ++q)
+        on[q] = gl[q] >= 0 && ((words[(int64_t)gl[q] * P.nw + c] >> tx) & 1u);
+      double cp[kFinBatch], pp[kFinBatch];
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q) {
+        const int64_t idx = (int64_t)(on[q] ? gl[q] : 0) * P.n + j;
+        cp[q] = on[q] ? colpart[idx] : 0.0;
+        pp[q] = on[q] ? psi[idx] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (on[u]) {
-          acc = dadd(acc, cp[u]);
-          ps = dadd(ps, pp[u]);
+      for (int q = 0; q < kFinBatch; ++q)
+        if (on[q]) {
+          acc = dadd(acc, cp[q]);
+          ps = dadd(ps, pp[q]);
         }
+      if (cnt < kFinBatch) break;
     }
   }
   sh[half][0][ty][tx] = acc;
@@ -872,14 +921,16 @@ __global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
 }
 
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
-                     const uint32_t* gmask, const double* rowpart, const double* colpart,
-                     const double* psi, double* grad, const double* dvec, double* partials,
-                     EvalScalars* sc, int cnt_pending, cudaStream_t s) {
+                     const uint32_t* gmask, uint32_t* cmask, int clear_cmask,
+                     const double* rowpart, const double* colpart, const double* psi,
+                     double* grad, const double* dvec, double* partials, EvalScalars* sc,
+                     int cnt_pending, cudaStream_t s) {
   const int rb = (int)((P.m + 31) / 32);
   const int cb = (int)((P.n + 31) / 32);
   const int units = rb + cb;
   launch_pdl(k_finalize, dim3((units + 1) / 2), dim3(64 * kFinSlices), 0, s, P, x, words, gmask,
-             rowpart, colpart, psi, grad, dvec, partials, sc, cnt_pending, rb, units);
+             cmask, clear_cmask, rowpart, colpart, psi, grad, dvec, partials, sc, cnt_pending, rb,
+             units);
 }
 
 // ---------------------------------------------------------------- plan

@@ -24,18 +24,23 @@ namespace gsot {
 
 // trial.x = x + t * d (lbfgs.hpp:86).
 __global__ void k_axpy_point(const double* __restrict__ x, const double* __restrict__ tp,
-                             const double* __restrict__ d, double* __restrict__ out, int64_t dim) {
+                             const double* __restrict__ d, double* __restrict__ out, int64_t dim,
+                             int64_t m, const double* __restrict__ snap,
+                             double* __restrict__ dbeta) {
   pdl_trigger();
   const double t = *tp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < dim;
-       e += (int64_t)gridDim.x * blockDim.x)
-    out[e] = dadd(x[e], dmul(t, d[e]));
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = dadd(x[e], dmul(t, d[e]));
+    out[e] = v;
+    if (dbeta && e >= m) dbeta[e - m] = dsub(v, snap[e]);  // compute_delta_norms' dbeta
+  }
 }
 
 void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
-                       int64_t dim, cudaStream_t s) {
+                       int64_t dim, int64_t m, const double* snap, double* dbeta, cudaStream_t s) {
   const int grid = (int)std::min<int64_t>((dim + 255) / 256, 148 * 4);
-  k_axpy_point<<<grid, 256, 0, s>>>(x, t, d, out, dim);
+  k_axpy_point<<<grid, 256, 0, s>>>(x, t, d, out, dim, m, snap, dbeta);
 }
 
 #ifdef GSOT_PHASE_CLOCKS
@@ -150,6 +155,11 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
       TL_EXIT(tl, TL_PUBLISH);
       unsigned long long s0 = ~0ull;
       for (int k = 0; k < 8; ++k) s0 = tl[2 * k] < s0 ? tl[2 * k] : s0;
+      if (tl[2 * TL_EVAL] != ~0ull && tl[2 * TL_EVAL + 1] - tl[2 * TL_EVAL] < 40000ull) {
+        tl[56] += tl[2 * TL_EVAL + 1] - tl[2 * TL_EVAL];  // steady-state (sparse) evaluations
+        tl[57] += 1;
+        tl[58] += tl[2 * TL_PUBLISH + 1] - s0;  // and their sequence span
+      }
       for (int k = 0; k < 8; ++k)
         if (tl[2 * k] != ~0ull) {
           tl[16 + 4 * k] += tl[2 * k] - s0;
@@ -253,6 +263,9 @@ struct StepArgs {
   double* part;     // [kStepMaxGrid][2] slope partials, then [grid][KS * 5] dot partials
   int ks;           // memory + 1: leading dimension of R / YY in shared memory
   unsigned long long* tl;  // diagnostic timeline or null
+  int64_t m;               // with dbeta: dbeta_j = xt[m + j] - snap[m + j]
+  const double* snap;
+  double* dbeta;
 };
 
 
@@ -632,7 +645,11 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
       }
     }
     A.d[e] = de;
-    if (A.xt) A.xt[e] = dadd(xe, dmul(t, de));  // lbfgs.hpp:86
+    if (A.xt) {
+      const double v = dadd(xe, dmul(t, de));  // lbfgs.hpp:86
+      A.xt[e] = v;
+      if (A.dbeta && e >= A.m) A.dbeta[e - A.m] = dsub(v, A.snap[e]);
+    }
     pg = dadd(pg, dmul(ge, de));
     pd = dadd(pd, dmul(de, de));
   }
@@ -685,9 +702,11 @@ void launch_lbfgs_step(int pair, const double* x, const double* xprev, const dou
                        const double* gprev, double* S, double* Y, int64_t stride, HistState* h,
                        CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
                        double* out, EvalScalars* sc, double* part, int mem,
-                       unsigned long long* tl, cudaStream_t s) {
+                       unsigned long long* tl, int64_t m, const double* snap, double* dbeta,
+                       cudaStream_t s) {
   const int grid = lbfgs_step_grid();
-  StepArgs A{pair, x, xprev, g, gprev, S, Y, stride, h, cs, d, t, xt, dim, out, sc, part, mem + 1, tl};
+  StepArgs A{pair, x, xprev, g, gprev, S, Y, stride, h, cs, d, t, xt, dim, out, sc, part, mem + 1,
+             tl, m, snap, dbeta};
   const size_t smem = sizeof(double) * 2 * (size_t)(mem + 1) * (mem + 1);
   if (smem > 48 * 1024 && smem > g_step_smem) {
     cudaFuncSetAttribute(k_lbfgs_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

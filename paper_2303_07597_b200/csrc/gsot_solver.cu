@@ -193,6 +193,8 @@ class Solver {
                                     cudaMemcpyHostToDevice, c_->stream));
   }
   const double* t_dev() const { return &c_->dsync->t; }
+  // fast screened solves: the step / trial kernels also write dbeta for the screen
+  bool fast_screen() const { return screened_ && !exact_; }
   void enqueue_two_loop() {  // lbfgs.hpp:109-126
     TwoLoopArgs A;
     A.S = w_->S;
@@ -218,9 +220,11 @@ class Solver {
     const int q = 1 - r_;
     enqueue_t();
     c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
-      launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->stream);
+      launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->m, c_->snap_x,
+                        fast_screen() ? c_->dbeta : nullptr, c_->stream);
     });
-    enqueue_eval(c_, w_->X[q], mode_eval_, w_->G[q], w_->d, o_.upper_bound_offset, use_active_);
+    enqueue_eval(c_, w_->X[q], mode_eval_, w_->G[q], w_->d, o_.upper_bound_offset, use_active_,
+                 fast_screen());
   }
 
   // The search direction (lbfgs.hpp:109-126), optionally preceded by the
@@ -235,7 +239,8 @@ class Solver {
       enqueue_two_loop();
       if (trial)
         c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
-          launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->stream);
+          launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->m, c_->snap_x,
+                            nullptr, c_->stream);
         });
       return;
     }
@@ -243,7 +248,8 @@ class Solver {
       launch_lbfgs_step(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->S, w_->Y,
                         w_->dim, &c_->dsync->h, w_->cs, w_->d, t_dev(),
                         trial ? w_->X[q] : nullptr, w_->dim, c_->dsync->tl, c_->sc, w_->cpart, mem_,
-                        c_->tl, c_->stream);
+                        c_->tl, c_->m, c_->snap_x, fast_screen() ? c_->dbeta : nullptr,
+                        c_->stream);
     });
   }
 
@@ -424,7 +430,7 @@ class Solver {
               enqueue_t();
               enqueue_direction(pending_pair, true);
               enqueue_eval(c_, w_->X[1 - r_], mode_eval_, w_->G[1 - r_], w_->d,
-                           o_.upper_bound_offset, use_active_);
+                           o_.upper_bound_offset, use_active_, fast_screen());
               c_->enqueue_fetch();
             });
             have_first = true;

@@ -31,4 +31,8 @@ for k, nm in enumerate(names):
     s = (buf[16 + 4 * k] - base[16 + 4 * k]) / n / 1e3
     e = (buf[16 + 4 * k + 1] - base[16 + 4 * k + 1]) / n / 1e3
     print(f'  {nm:9s} n={n:4d}  start {s:7.2f} us  end {e:7.2f} us  window {e - s:6.2f} us')
+ns = buf[57] - base[57]
+if ns:
+    print(f'  sparse evals (< 40 us): n={ns}  eval window {(buf[56] - base[56]) / ns / 1e3:.2f} us  '
+          f'sequence span {(buf[58] - base[58]) / ns / 1e3:.2f} us')
 PY
