@@ -538,14 +538,12 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* slots = reinterpret_cast<double*>(eval_smem);  // [2][seg * 32] cost segments
   double* aslots = slots + 2 * (size_t)A.seg * 32;       // [2][seg + 2] alpha segments
+  double* bslots = aslots + 2 * (size_t)(A.seg + 2);     // [2][34] the task's beta chunk
   __shared__ uint64_t full[2], empty[2];
   __shared__ EvalTask tinfo[2];  // by the slot of the task's first segment
   __shared__ double zsh[kEvalWarps][32], ssh[kEvalWarps][32];
   __shared__ double scale_sh[32];
-  pdl_wait();
-  pdl_trigger();
-  TL_ENTER(P.tl, TL_EVAL);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // barrier set-up overlaps the predecessor's tail
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
     mbar_init(&empty[0], kEvalWarps);
@@ -553,6 +551,9 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  TL_ENTER(P.tl, TL_EVAL);
   if (warp == kEvalWarps) {  // ---- producer
     if (lane != 0) return;
     const int ntasks = A.ntasks >= 0 ? A.ntasks : *(volatile const int*)A.ntasks_dev;
@@ -571,9 +572,11 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
       }
       return T;
     };
+    // CTA b starts with task b; further tasks are claimed from grid onwards
+    const int G = (int)gridDim.x;
     uint32_t e = 0;
-    EvalTask T = fetch(atomicAdd(A.next_task, 1));
-    int tn = T.valid ? atomicAdd(A.next_task, 1) : ntasks;  // claimed one task ahead
+    EvalTask T = fetch(blockIdx.x);
+    int tn = T.valid ? G + atomicAdd(A.next_task, 1) : ntasks;  // claimed one task ahead
     for (;;) {
       const double* tile = P.C + 32 * ((int64_t)P.nw * T.o0 + (int64_t)T.c * T.g);
       const int ne = !T.valid ? 1 : T.nseg == 1 ? 1 : 2 * T.nseg;
@@ -590,13 +593,19 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
         const int r0 = (k < T.nseg ? k : k - T.nseg) * A.seg, rows = min(A.seg, T.g - r0);
         const int64_t a0 = (T.o0 + r0) & ~1ll;  // 16-byte aligned superset of the rows
         const uint32_t abytes = (uint32_t)(((T.o0 + r0 + rows - a0) + 1) & ~1ll) * 8u;
-        mbar_expect_tx(&full[slot], (uint32_t)rows * 256u + abytes);
+        // the task's beta chunk rides along with its first segment
+        const int64_t b0 = (P.m + 32ll * T.c) & ~1ll;
+        const int64_t bn = P.m + P.n - b0 < 34 ? P.m + P.n - b0 : 34;
+        const uint32_t bbytes = k == 0 ? (uint32_t)((bn + 1) & ~1ll) * 8u : 0u;
+        mbar_expect_tx(&full[slot], (uint32_t)rows * 256u + abytes + bbytes);
         tma_load_1d(slots + (size_t)slot * A.seg * 32, tile + (int64_t)r0 * 32,
                     (uint32_t)rows * 256u, &full[slot]);
         tma_load_1d(aslots + (size_t)slot * (A.seg + 2), A.x + a0, abytes, &full[slot]);
-        if (k == 0) {  // decode the next task and claim the one after while this one loads
+        if (k == 0) {
+          tma_load_1d(bslots + (size_t)slot * 34, A.x + b0, bbytes, &full[slot]);
+          // decode the next task and claim the one after while this one loads
           Tn = fetch(tn);
-          tn = Tn.valid ? atomicAdd(A.next_task, 1) : ntasks;
+          tn = Tn.valid ? G + atomicAdd(A.next_task, 1) : ntasks;
         }
       }
       T = Tn;
@@ -614,7 +623,8 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
     if (!T.valid) break;
     const int64_t j = (int64_t)T.c * 32 + lane;
     const bool act = (T.word >> lane) & 1u;
-    const double bj = act ? A.x[P.m + j] : 0.0;
+    const double bj =
+        act ? bslots[(size_t)(e & 1u) * 34 + ((P.m + 32ll * T.c) & 1) + lane] : 0.0;
     double z2 = 0.0, sv = 0.0;
     double scr[16];  // scales of this lane's 16 rotated columns
     const int ne = T.nseg == 1 ? 1 : 2 * T.nseg;
@@ -707,7 +717,7 @@ int eval_buf_rows(int gmax) { return std::max(8, std::min(gmax, kEvalMaxSeg)); }
 
 size_t eval_smem_bytes(int seg, int cap) {
   (void)cap;
-  return sizeof(double) * 2 * ((size_t)seg * 32 + seg + 2);
+  return sizeof(double) * 2 * ((size_t)seg * 32 + seg + 2 + 34);
 }
 
 int eval_blocks_per_sm(size_t smem) {
