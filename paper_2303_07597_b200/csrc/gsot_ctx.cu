@@ -115,7 +115,8 @@ gsot_ctx::~gsot_ctx() {
                   x_eval,   g_eval,  rowpart,       colpart,     psi,      psicol,  partials,
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
-                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl};
+                  cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
+                  d_one};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -218,6 +219,11 @@ void alloc_buffers(gsot_ctx* c) {
   GSOT_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_sync_dev), c->h_sync, 0));
   GSOT_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_flag_dev), c->h_flag, 0));
   c->d_pub_count = dalloc<unsigned long long>(1, t);
+  c->d_one = dalloc<double>(1, t);
+  {
+    const double one = 1.0;
+    GSOT_CUDA_CHECK(cudaMemcpy(c->d_one, &one, sizeof(double), cudaMemcpyHostToDevice));
+  }
 #ifdef GSOT_PHASE_CLOCKS
   if (std::getenv("GSOT_TIMELINE")) {  // diagnostic kernel timeline
     c->tl = dalloc<unsigned long long>(64, t);

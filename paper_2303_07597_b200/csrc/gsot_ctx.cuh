@@ -84,6 +84,7 @@ struct gsot_ctx {
   uint32_t *words = nullptr, *dense_words = nullptr;
   uint32_t *gmask = nullptr, *dense_gmask = nullptr;  // per-group non-empty chunk masks
   uint32_t *cmask = nullptr, *dense_cmask = nullptr;  // per-chunk non-empty group masks
+  double* d_one = nullptr;  // device constant 1.0 (t_init of direction sequences)
   unsigned long long* tl = nullptr;  // diagnostic kernel timeline (GSOT_TIMELINE=1, diag builds)
   gsot::TaskDesc* dense_tasks = nullptr;  // every chunk, largest groups first
   gsot::TaskDesc* tasks = nullptr;        // screened work list (non-empty chunks)

@@ -193,6 +193,9 @@ class Solver {
                                     cudaMemcpyHostToDevice, c_->stream));
   }
   const double* t_dev() const { return &c_->dsync->t; }
+  // the first trial of a direction sequence uses t_init = 1 (lbfgs.hpp:150):
+  // a device constant, so those graphs carry no copy node
+  const double* t_one() const { return c_->d_one; }
   // fast screened solves: the step / trial kernels also write dbeta for the screen
   bool fast_screen() const { return screened_ && !exact_; }
   void enqueue_two_loop() {  // lbfgs.hpp:109-126
@@ -239,14 +242,14 @@ class Solver {
       enqueue_two_loop();
       if (trial)
         c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
-          launch_axpy_point(w_->X[r_], t_dev(), w_->d, w_->X[q], w_->dim, c_->m, c_->snap_x,
+          launch_axpy_point(w_->X[r_], t_one(), w_->d, w_->X[q], w_->dim, c_->m, c_->snap_x,
                             nullptr, c_->stream);
         });
       return;
     }
     c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 10.0), [&] {
       launch_lbfgs_step(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->S, w_->Y,
-                        w_->dim, &c_->dsync->h, w_->cs, w_->d, t_dev(),
+                        w_->dim, &c_->dsync->h, w_->cs, w_->d, t_one(),
                         trial ? w_->X[q] : nullptr, w_->dim, c_->dsync->tl, c_->sc, w_->cpart, mem_,
                         c_->tl, c_->m, c_->snap_x, fast_screen() ? c_->dbeta : nullptr,
                         c_->stream);
@@ -425,9 +428,7 @@ class Solver {
               c_->enqueue_fetch();
             });
           } else {
-            c_->h_sync->t = 1.0;  // t_init (lbfgs.hpp:150)
-            run_seq(pending_pair ? "PDT" : "DT", [&] {
-              enqueue_t();
+            run_seq(pending_pair ? "PDT" : "DT", [&] {  // first trial at t_init = 1
               enqueue_direction(pending_pair, true);
               enqueue_eval(c_, w_->X[1 - r_], mode_eval_, w_->G[1 - r_], w_->d,
                            o_.upper_bound_offset, use_active_, fast_screen());
