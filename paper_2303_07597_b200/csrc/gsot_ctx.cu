@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdio>
 #include <deque>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -116,7 +117,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one};
+                  d_one, staging, d_bad};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h_sync) cudaFreeHost(h_sync);
@@ -316,12 +317,83 @@ void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const doubl
                     " indices, cost has " + std::to_string(c->m) + " rows");
 }
 
+// Context cache: gsot_destroy parks a context's device state (buffers,
+// stream, captured graphs) and gsot_create of the same shape and partition
+// on the same device takes it back, re-uploading only the data. Repeated
+// solves of same-shape instances then skip allocation, frees and graph
+// capture (like a caching allocator). GSOT_CTX_CACHE=0 disables it.
+namespace {
+std::mutex g_cache_mu;
+std::vector<gsot_ctx*> g_cache;
+constexpr size_t kCacheMax = 2;
+
+bool cache_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GSOT_CTX_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+gsot_ctx* cache_take(int64_t m, int64_t n, const int32_t* sizes, int32_t L) {
+  if (!cache_enabled()) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  for (size_t k = 0; k < g_cache.size(); ++k) {
+    gsot_ctx* c = g_cache[k];
+    if (c->device == dev && c->m == m && c->n == n && c->L == L &&
+        std::equal(c->sizes.begin(), c->sizes.end(), sizes)) {
+      g_cache.erase(g_cache.begin() + k);
+      return c;
+    }
+  }
+  return nullptr;
+}
+}  // namespace
+
+void park_or_delete(gsot_ctx* c) {
+  if (!c) return;
+  if (!cache_enabled() || !c->cacheable || cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    delete c;
+    return;
+  }
+  gsot_ctx* evict = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    g_cache.push_back(c);
+    if (g_cache.size() > kCacheMax) {
+      evict = g_cache.front();
+      g_cache.erase(g_cache.begin());
+    }
+  }
+  delete evict;
+}
+
 gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int64_t n,
                         const int32_t* sizes, int32_t L, const double* a, const double* b,
                         double gamma, double mu) {
-  auto* c = new gsot_ctx();
+  gsot_ctx* c = (sizes && L > 0 && m > 0 && n > 0) ? cache_take(m, n, sizes, L) : nullptr;
+  const bool reused = c != nullptr;
+  if (!c) c = new gsot_ctx();
+  c->cacheable = false;  // until the new data is in
   try {
-    setup_shape(c, m, n, sizes, L, gamma, mu);
+    if (reused) {  // same shape and partition: device state as parked
+      check_params(gamma, mu);
+      if (gamma != c->gamma || mu != c->mu) {
+        c->gamma = gamma;
+        c->mu = mu;
+        if (c->ws) c->ws->graphs.clear();  // graphs bake (gamma, mu) into kernel parameters
+      }
+      c->have_snapshot = false;
+      c->active_count = 0;
+      GSOT_CUDA_CHECK(cudaMemsetAsync(c->sc, 0, sizeof(gsot::EvalScalars), c->stream));
+      GSOT_CUDA_CHECK(cudaMemsetAsync(c->cnt_slots, 0, sizeof(unsigned long long) * 64 * 8, c->stream));
+      GSOT_CUDA_CHECK(cudaMemsetAsync(
+          c->cmask, 0, sizeof(uint32_t) * c->nw * ((c->L + 31) / 32), c->stream));
+    } else {
+      setup_shape(c, m, n, sizes, L, gamma, mu);
+    }
     if (c->off[L] != m) {
       // The reference checks the cover last (core.hpp:134-138) but the
       // layout needs it; the scan order of the remaining checks is kept.
@@ -346,17 +418,21 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
                   "group partition: partition covers " + std::to_string(c->off[L]) +
                       " indices, cost has " + std::to_string(m) + " rows");
     }
-    init_device(c);
-    alloc_buffers(c);
+    if (!reused) {
+      init_device(c);
+      alloc_buffers(c);
+    }
     set_marginals(c, a, b);
-    unsigned long long* d_bad = nullptr;
-    GSOT_CUDA_CHECK(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    // Upload in column chunks through a staging buffer (bounded extra HBM;
+    // kept by the context for the next upload of a cached context).
+    if (!c->d_bad) GSOT_CUDA_CHECK(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
+    unsigned long long* d_bad = c->d_bad;
     GSOT_CUDA_CHECK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), c->stream));
-    // Upload in column chunks through a staging buffer (bounded extra HBM).
     const int64_t chunk_cols =
         std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(256) << 20) / (8 * m)));
-    double* staging = nullptr;
-    if (!cost_on_device) GSOT_CUDA_CHECK(cudaMalloc(&staging, sizeof(double) * m * chunk_cols));
+    if (!cost_on_device && !c->staging)
+      GSOT_CUDA_CHECK(cudaMalloc(&c->staging, sizeof(double) * m * chunk_cols));
+    double* staging = c->staging;
     for (int64_t j0 = 0; j0 < n; j0 += chunk_cols) {
       const int64_t nc = std::min(chunk_cols, n - j0);
       const double* src = nullptr;
@@ -372,8 +448,7 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
       });
     }
     finish_validation(c, d_bad, a, b, nullptr);
-    if (staging) cudaFree(staging);
-    cudaFree(d_bad);
+    c->cacheable = true;
     return c;
   } catch (...) {
     delete c;
@@ -569,7 +644,7 @@ GSOT_API int gsot_create_device(const double* d_cost, int64_t m, int64_t n,
   });
 }
 
-GSOT_API void gsot_destroy(gsot_ctx* ctx) { delete ctx; }
+GSOT_API void gsot_destroy(gsot_ctx* ctx) { park_or_delete(ctx); }
 
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu) {
   return guard([&] {

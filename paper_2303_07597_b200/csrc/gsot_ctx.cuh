@@ -85,6 +85,8 @@ struct gsot_ctx {
   uint32_t *gmask = nullptr, *dense_gmask = nullptr;  // per-group non-empty chunk masks
   uint32_t *cmask = nullptr, *dense_cmask = nullptr;  // per-chunk non-empty group masks
   double* d_one = nullptr;  // device constant 1.0 (t_init of direction sequences)
+  double* staging = nullptr;            // host-cost upload staging (column chunks)
+  unsigned long long* d_bad = nullptr;  // first invalid cost entry (validation)
   unsigned long long* tl = nullptr;  // diagnostic kernel timeline (GSOT_TIMELINE=1, diag builds)
   gsot::TaskDesc* dense_tasks = nullptr;  // every chunk, largest groups first
   gsot::TaskDesc* tasks = nullptr;        // screened work list (non-empty chunks)
@@ -110,6 +112,7 @@ struct gsot_ctx {
   // solver
   std::unique_ptr<gsot::SolverWorkspace> ws;
   uint64_t graph_epoch = 0;  // bumped when baked-in parameters change
+  bool cacheable = false;    // created from data (gsot_create / _device): may be parked
   // measurement
   bool profile = false;
   unsigned profile_mask = 0;  // kinds bracketed with events (bit per KernelKind)
