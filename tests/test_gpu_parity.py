@@ -2,9 +2,10 @@
 reference's golden fixtures.
 
 Tolerances (BASELINE.json north_star):
-* per-block values -- plan entries, snapshot norms z~/k~/o~, the nonzero
-  block set, active set, screening counters -- BITWISE (the kernels compute
-  each block in the reference's order of operations);
+* per-block values -- plan entries (gsot_plan_columns), snapshot norms
+  z~/k~/o~, the screening decisions and counters, the active set -- BITWISE
+  (those kernels compute each block in the reference's order of operations;
+  the fused evaluation re-associates its per-column norms, fast mode);
 * objective within 1e-9 relative;
 * gradient within 1e-9 scale-aware: |g - g_ref| <= 1e-9 * (a_i + sum_j T_ij)
   for grad_alpha and 1e-9 * (b_j + sum_i T_ij) for grad_beta (the sums cancel
@@ -380,3 +381,39 @@ def test_config2_full_size_properties(o):
     assert abs(g[: p.m].sum() - g[p.m:].sum()) <= 1e-12
     assert_eval_close(o, p, x, obj, g)
     ctx.close()
+
+
+def test_context_cache_reuse_is_clean(o):
+    # gsot_destroy parks a context's device state and gsot_create of the same
+    # shape and partition takes it back (buffers, stream, captured graphs).
+    # A context created from new data (and new gamma, mu) on reused state must
+    # behave exactly as a fresh one.
+    sizes = [12, 7, 30, 1, 9]
+    p1, _ = random_problem(sizes, 50, 0.4, 0.7, 11)
+    p2, _ = random_problem(sizes, 50, 0.25, 0.9, 12)
+    kw = dict(mode=1, max_outer_loops=6, grad_tol=1e-12)
+    c1 = ctx_of(p1)
+    c1.solve(**kw)
+    c1.close()  # parked
+    c2 = ctx_of(p2)  # same shape: takes the parked state
+    c3 = ctx_of(p2)  # fresh state (the cache is empty now)
+    rng = np.random.default_rng(2)
+    x = rng.normal(scale=0.05, size=p2.m + p2.n)
+    for c in (c2, c3):
+        obj, g, _ = c.eval(x)
+        assert_eval_close(o, p2, x, obj, g)
+    r2, r3 = c2.solve(**kw), c3.solve(**kw)
+    assert np.array_equal(r2["x"], r3["x"]) and r2["objective"] == r3["objective"]
+    assert r2["grad_calls"] == r3["grad_calls"]
+    assert r2["blocks_skipped"] == r3["blocks_skipped"]
+    c2.close()
+    # an invalid instance of the cached shape fails as usual and leaves no state
+    bad = Problem(p2.cost.copy(), p2.sizes, p2.a, p2.b, p2.gamma, p2.mu)
+    bad.cost[3, 2] = -1.0
+    with pytest.raises(G.NegativeCost):
+        ctx_of(bad)
+    c4 = ctx_of(p1)
+    obj, g, _ = c4.eval(x)
+    assert_eval_close(o, p1, x, obj, g)
+    c4.close()
+    c3.close()
