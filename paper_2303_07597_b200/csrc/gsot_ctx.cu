@@ -274,6 +274,9 @@ void alloc_buffers(gsot_ctx* c) {
     const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0));
     c->eval_buf = seg;
     c->eval_grid = c->num_sms * bps;
+    if (std::getenv("GSOT_DIAG_SEQ"))
+      std::fprintf(stderr, "[gsot diag] eval: %d rows per segment, %d CTAs per SM, %zu B shared\n",
+                   seg, bps, gsot::eval_smem_bytes(seg, 0));
   }
   c->sync();
 }

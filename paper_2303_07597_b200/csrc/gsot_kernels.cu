@@ -723,6 +723,9 @@ size_t eval_smem_bytes(int seg, int cap) {
 int eval_blocks_per_sm(size_t smem) {
   if ((int)smem > g_eval_smem_attr) {
     cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // all of the unified L1 / shared array as shared memory: one more CTA
+    // (one more tile in flight) per SM
+    cudaFuncSetAttribute(k_eval, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     g_eval_smem_attr = (int)smem;
   }
   int n = 0;
