@@ -265,8 +265,9 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
   k_active<<<grid, 256, 0, s>>>(P, ks, os, dfull, dneg, dbeta, aw, sc);
 }
 
-// ---------------------------------------------------------------- screen
-// FastGradDispatcher::column's per-block decision (screening.hpp:252-275):
+// ---------------------------------------------------------------- screen (small)
+// FastGradDispatcher::column's per-block decision (screening.hpp:252-275),
+// layout for small problems (few CTAs of the transposed kernel below):
 // active-set members are computed without a bound; every other block gets
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
 // skipped iff z_bar <= tau. CTA (k, l) screens the 64 chunks of group l
@@ -277,7 +278,7 @@ void launch_active(const DevProblem& P, const double* ks, const double* os, cons
 // adds its GradStats::PerCall counters into one of 64 slots (integers:
 // order-free). One CTA per unit keeps every unit's short dependency chain
 // overlapped with the others on the SM.
-__global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __restrict__ zs,
+__global__ void __launch_bounds__(256) k_screen_rows(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
                                                 const double* __restrict__ dpos,
                                                 const double* __restrict__ dbeta,
@@ -407,15 +408,179 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   TL_EXIT(P.tl, TL_SCREEN);
 }
 
+// ---------------------------------------------------------------- screen
+// FastGradDispatcher::column's per-block decision (screening.hpp:252-275):
+// active-set members are computed without a bound; every other block gets
+// z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
+// skipped iff z_bar <= tau.
+// CTA (kx, ky) covers groups 8 ky .. 8 ky + 7 (one warp each) and the 32
+// chunks of chunk-mask word kx (one lane each), so each lane builds ONE
+// survivor word from its chunk's 32 columns sequentially -- no per-chunk
+// ballots or lane-0 bookkeeping. Bounds and dbeta are transposed through
+// shared memory 16 columns at a time (coalesced global loads, padded rows:
+// no bank conflicts). Per warp: the survivor words, the group's chunk-mask
+// word (one ballot), the group's delta norm (fast mode: fused, fixed tree);
+// per CTA: one atomic reserving the non-empty chunks' work-list slots, the
+// per-chunk group masks (one atomic per chunk), and the GradStats::PerCall
+// counters into one of 64 slots (integers: order-free).
+constexpr int kScrWarps = 8;   // groups per CTA
+constexpr int kScrHalf = 16;   // columns per transposition round
+
+__global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __restrict__ zs,
+                                                const uint32_t* __restrict__ aw,
+                                                const double* __restrict__ dpos,
+                                                const double* __restrict__ dbeta,
+                                                double ub_offset, uint32_t* __restrict__ words,
+                                                TaskDesc* __restrict__ tasks, EvalScalars* sc,
+                                                unsigned long long* __restrict__ cnt_slots,
+                                                uint32_t* __restrict__ gmask,
+                                                uint32_t* __restrict__ cmask,
+                                                const double* __restrict__ x,
+                                                const double* __restrict__ xs, int dbeta_ready) {
+  __shared__ double zt[kScrWarps][32][kScrHalf + 1];  // [group][chunk][column]
+  __shared__ double dbt[32][kScrHalf + 1];            // [chunk][column]
+  __shared__ unsigned long long cnt[kScrWarps][6];
+  __shared__ int wn[kScrWarps];                        // non-empty chunks per warp
+  __shared__ uint32_t gbits[kScrWarps][32];            // for the per-chunk group masks
+  __shared__ int base;
+  pdl_wait();
+  pdl_trigger();
+  TL_ENTER(P.tl, TL_SCREEN);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * 32;
+  const int l = blockIdx.y * kScrWarps + warp;
+  const bool lvalid = l < P.L;
+  const int c = c0 + lane;  // this lane's chunk
+  const bool cvalid = c < P.nw;
+  const bool db_inline = x != nullptr && !dbeta_ready;
+  const int o0 = lvalid ? P.off[l] : 0;
+  const int g = lvalid ? P.off[l + 1] - o0 : 0;
+  const uint32_t am = (lvalid && cvalid && aw != nullptr) ? aw[(int64_t)l * P.nw + c] : 0u;
+  double dp = 0.0;
+  if (x) {
+    // fused delta (fast mode): |[alpha_l - alpha~_l]+| over the group's rows,
+    // lane-strided chains, then a fixed xor tree
+    double acc = 0.0;
+    for (int r = lane; r < g; r += 32) {
+      const double d = dsub(x[o0 + r], xs[o0 + r]);
+      if (d > 0.0) acc = dadd(acc, dmul(d, d));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    dp = sqrt(acc);
+  } else if (lvalid) {
+    dp = dpos[l];  // k_delta's reference-order norm (exact mode)
+  }
+  const double sg = lvalid ? P.sqrt_g[l] : 0.0;
+  uint32_t surv = 0u;  // evaluated columns with z_bar > tau
+#pragma unroll 1
+  for (int h = 0; h < 32 / kScrHalf; ++h) {
+    const int cb = h * kScrHalf;  // first column of the round within each chunk
+    __syncthreads();  // the previous round's buffers are consumed
+    // dbeta of the 32 chunks' columns cb..cb+15 (shared by the groups)
+    for (int q = threadIdx.x; q < 32 * kScrHalf; q += blockDim.x) {
+      const int ci = q / kScrHalf, k = q % kScrHalf;
+      const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
+      double v = 0.0;
+      if (c0 + ci < P.nw && j < P.n) v = db_inline ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j];
+      dbt[ci][k] = v;
+    }
+    // this warp's group: z~ of the 32 chunks' columns cb..cb+15, two chunks
+    // per coalesced load (half-warp = 16 consecutive columns)
+#pragma unroll 4
+    for (int q = 0; q < 16; ++q) {
+      const int ci = 2 * q + (lane >> 4), k = lane & 15;
+      const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
+      zt[warp][ci][k] = (lvalid && c0 + ci < P.nw && j < P.n) ? zs[(int64_t)l * P.n + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScrHalf; ++k) {
+      const double zbar =
+          dadd(dadd(dadd(zt[warp][lane][k], dp), dmul(sg, relu(dbt[lane][k]))), ub_offset);
+      surv |= (zbar <= P.tau ? 0u : 1u) << (cb + k);
+    }
+  }
+  // masks of this lane's chunk
+  const int64_t j0 = (int64_t)c * 32;
+  const uint32_t vmask = (!lvalid || !cvalid) ? 0u
+                         : (P.n - j0 >= 32 ? 0xffffffffu : ((1u << (P.n - j0)) - 1u));
+  const uint32_t wa = am & vmask;
+  const uint32_t we = vmask & ~wa;
+  const uint32_t ws = (surv & we) | wa;
+  if (lvalid && cvalid) words[(int64_t)l * P.nw + c] = ws;
+  const unsigned ne = __ballot_sync(0xffffffffu, ws != 0u);
+  if (lvalid && lane == 0) gmask[(int64_t)l * ((P.nw + 31) / 32) + blockIdx.x] = ne;
+  // GradStats counters of this lane's chunk, warp-reduced
+  unsigned long long v[6];
+  const uint32_t nsv = __popc(we & ws), nev = __popc(we);
+  v[0] = __popc(wa);
+  v[1] = nev - nsv;
+  v[2] = nsv;
+  v[3] = nev;
+  v[4] = (unsigned long long)__popc(ws) * (unsigned)g;  // survivors' rows
+  v[5] = ws ? (unsigned long long)g : 0ull;             // task rows
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) cnt[warp][q] = v[q];
+    wn[warp] = __popc(ne);
+  }
+  gbits[warp][lane] = ws ? (1u << (l & 31)) : 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < kScrWarps; ++w) tot += wn[w];
+    base = tot ? atomicAdd(&sc->ntasks, tot) : 0;
+  }
+  if (threadIdx.x >= 32 && threadIdx.x < 38) {
+    const int q = threadIdx.x - 32;
+    unsigned long long s = 0ull;
+    for (int w = 0; w < kScrWarps; ++w) s += cnt[w][q];
+    if (s) atomicAdd(cnt_slots + ((blockIdx.y * gridDim.x + blockIdx.x) & 63u) * 8 + q, s);
+  }
+  if (cmask && warp == 1) {  // per-chunk group masks: one atomic per chunk
+    // groups 8 ky .. 8 ky + 7 share one mask word (8 divides 32)
+    uint32_t bits = 0u;
+#pragma unroll
+    for (int w = 0; w < kScrWarps; ++w) bits |= gbits[w][lane];
+    if (bits && cvalid)
+      atomicOr(cmask + (int64_t)c * ((P.L + 31) / 32) + ((blockIdx.y * kScrWarps) >> 5), bits);
+  }
+  __syncthreads();
+  if (ws != 0u) {
+    int pos = base + __popc(ne & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) pos += wn[w];
+    TaskDesc d;
+    d.l = l;
+    d.c = c;
+    d.o0 = o0;
+    d.g = g;
+    d.word = ws;
+    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    tasks[pos] = d;
+  }
+  TL_EXIT(P.tl, TL_SCREEN);
+}
+
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
                    int num_sms, cudaStream_t s) {
-  (void)num_sms;
-  const dim3 grid((unsigned)((P.nw + 63) / 64), (unsigned)P.L);
-  launch_pdl(k_screen, grid, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks, sc,
-             cnt_slots, gmask, cmask, x, xs, dbeta_ready);
+  const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)((P.L + kScrWarps - 1) / kScrWarps));
+  if ((int64_t)grid.x * grid.y < 4ll * num_sms) {  // small: one CTA per (group, 2048 columns)
+    const dim3 g2((unsigned)((P.nw + 63) / 64), (unsigned)P.L);
+    launch_pdl(k_screen_rows, g2, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks,
+               sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready);
+    return;
+  }
+  launch_pdl(k_screen, grid, dim3(32 * kScrWarps), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words,
+             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
