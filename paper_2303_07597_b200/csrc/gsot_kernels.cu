@@ -938,7 +938,7 @@ constexpr int kFinMaskCap = 1024;  // mask words staged per row unit
 // that does not depend on the evaluation (x, d, marginals, the chunk masks and
 // survivor words written by the screen, which completed before the evaluation
 // started) is loaded before the programmatic wait.
-__global__ void __launch_bounds__(64 * kFinSlices, 2) k_finalize(
+__global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
     const uint32_t* __restrict__ gmask, uint32_t* __restrict__ cmask, int clear_cmask,
     const double* __restrict__ rowpart, const double* __restrict__ colpart,
