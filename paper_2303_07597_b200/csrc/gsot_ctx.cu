@@ -472,11 +472,16 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
   const DevProblem P = c->problem();
-  if (mode != GSOT_EVAL_SCREENED || exact) c->reset_scalars();  // fast screened: zeroed by k_publish
+  if (mode != GSOT_EVAL_SCREENED || exact) c->reset_scalars();  // screened: zeroed by k_publish
   const uint32_t* words = c->dense_words;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
-    if (exact)  // reference-order group norms; fast mode fuses them into the screen
+    // Fast solves fuse the group delta norms into the screen (the step / trial
+    // kernel wrote dbeta); every other screened evaluation -- exact mode and
+    // the API's gsot_eval -- takes the reference-order norms of k_delta, so
+    // its decisions and counters are the reference's bit for bit.
+    const bool fused = dbeta_ready && !exact;
+    if (!fused)
       c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
         launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, nullptr,
                      c->stream);
@@ -484,8 +489,8 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
                     ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
-                    exact ? nullptr : c->cmask, exact ? nullptr : d_x,
-                    exact ? nullptr : c->snap_x, dbeta_ready ? 1 : 0, c->num_sms, c->stream);
+                    exact ? nullptr : c->cmask, fused ? d_x : nullptr, fused ? c->snap_x : nullptr,
+                    fused ? 1 : 0, c->num_sms, c->stream);
     });
     words = c->words;
   }
