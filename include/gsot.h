@@ -102,6 +102,11 @@ GSOT_API int gsot_create(const double* cost, int64_t m, int64_t n, const int32_t
 GSOT_API int gsot_create_device(const double* d_cost, int64_t m, int64_t n,
                                 const int32_t* group_sizes, int32_t L, const double* a,
                                 const double* b, double gamma, double mu, gsot_ctx** out);
+/* Release a context. Contexts made by gsot_create / gsot_create_device park
+ * their device state (buffers, stream, captured graphs) in a small
+ * process-wide cache; a later create of the same shape and partition on the
+ * same device reuses it and only uploads the new data. GSOT_CTX_CACHE=0 in the
+ * environment frees immediately instead. */
 GSOT_API void gsot_destroy(gsot_ctx* ctx);
 /* Replace (gamma, mu) keeping the resident cost (RegParams ctor checks). */
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu);
