@@ -107,7 +107,7 @@ struct gsot_ctx {
   gsot::EvalScalars* sc = nullptr;    // &dsync->sc
   gsot::EvalScalars* h_sc = nullptr;  // &h_sync->sc
   int eval_grid = 148 * 4;
-  int eval_buf = 96;  // rows per warp staging buffer in k_eval
+  int eval_buf = 96;  // rows per shared-memory segment in k_eval
   int red_blocks = 148 * 2;
   // solver
   std::unique_ptr<gsot::SolverWorkspace> ws;

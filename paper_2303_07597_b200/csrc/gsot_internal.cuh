@@ -156,7 +156,7 @@ int eval_blocks_per_sm(size_t smem);
 // screened list, length *ntasks_dev (written by the screen kernel).
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int buf_rows, int grid, int* next_chunk, cudaStream_t s);
+                 double* psi, int seg, int grid, int* next_task, cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const uint32_t* gmask, uint32_t* cmask, int clear_cmask,

@@ -18,9 +18,12 @@
 // stored row-major; tile (l, c) starts at element 32 * (nw * off_l + c * g_l).
 // A warp (lane = column) walking the block rows reads one contiguous 256-byte
 // row of the tile per load.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "gsot_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gsot {
 
@@ -683,7 +686,9 @@ struct EvalArgs {
 
 constexpr int kEvalWarps = 4;                        // consumer warps
 constexpr int kEvalThreads = 32 * (kEvalWarps + 1);  // + one producer warp
-constexpr int kEvalMaxSeg = 128;                     // rows per segment (4 warps x 32 rows)
+constexpr int kEvalMaxSeg = 128;
+// alpha slot length in doubles: seg + 2 (aligned superset), even (16-byte slots)
+__host__ __device__ constexpr int aslot_len(int seg) { return (seg + 3) & ~1; }                     // rows per segment (4 warps x 32 rows)
 
 struct EvalTask {
   int l, c, g, o0, nseg, valid;
@@ -703,7 +708,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* slots = reinterpret_cast<double*>(eval_smem);  // [2][seg * 32] cost segments
   double* aslots = slots + 2 * (size_t)A.seg * 32;       // [2][seg + 2] alpha segments
-  double* bslots = aslots + 2 * (size_t)(A.seg + 2);     // [2][34] the task's beta chunk
+  double* bslots = aslots + 2 * (size_t)aslot_len(A.seg);     // [2][34] the task's beta chunk
   __shared__ uint64_t full[2], empty[2];
   __shared__ EvalTask tinfo[2];  // by the slot of the task's first segment
   __shared__ double zsh[kEvalWarps][32], ssh[kEvalWarps][32];
@@ -765,7 +770,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
         mbar_expect_tx(&full[slot], (uint32_t)rows * 256u + abytes + bbytes);
         tma_load_1d(slots + (size_t)slot * A.seg * 32, tile + (int64_t)r0 * 32,
                     (uint32_t)rows * 256u, &full[slot]);
-        tma_load_1d(aslots + (size_t)slot * (A.seg + 2), A.x + a0, abytes, &full[slot]);
+        tma_load_1d(aslots + (size_t)slot * aslot_len(A.seg), A.x + a0, abytes, &full[slot]);
         if (k == 0) {
           tma_load_1d(bslots + (size_t)slot * 34, A.x + b0, bbytes, &full[slot]);
           // decode the next task and claim the one after while this one loads
@@ -801,7 +806,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
       const int r0 = sgm * A.seg, rows = min(A.seg, T.g - r0);
       const int R = (rows + kEvalWarps - 1) / kEvalWarps;
       const int w0 = min(rows, warp * R), w1 = min(rows, w0 + R);
-      const double* __restrict__ as = aslots + (size_t)slot * (A.seg + 2) + ((T.o0 + r0) & 1);
+      const double* __restrict__ as = aslots + (size_t)slot * aslot_len(A.seg) + ((T.o0 + r0) & 1);
       double* __restrict__ col = buf + lane;
       if (act) {
         if (k < T.nseg) {  // pass 1: accumulate, [f]+ in place of the cost
@@ -882,7 +887,7 @@ int eval_buf_rows(int gmax) { return std::max(8, std::min(gmax, kEvalMaxSeg)); }
 
 size_t eval_smem_bytes(int seg, int cap) {
   (void)cap;
-  return sizeof(double) * 2 * ((size_t)seg * 32 + seg + 2 + 34);
+  return sizeof(double) * 2 * ((size_t)seg * 32 + aslot_len(seg) + 34);
 }
 
 int eval_blocks_per_sm(size_t smem) {
@@ -909,10 +914,7 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
     throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
   EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev};
   const size_t smem = eval_smem_bytes(seg, 0);
-  if ((int)smem > g_eval_smem_attr) {
-    cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    g_eval_smem_attr = (int)smem;
-  }
+  if ((int)smem > g_eval_smem_attr) eval_blocks_per_sm(smem);
   launch_pdl(k_eval, dim3(grid), dim3(kEvalThreads), smem, s, A);
 }
 
