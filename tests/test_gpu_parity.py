@@ -417,3 +417,30 @@ def test_context_cache_reuse_is_clean(o):
     assert_eval_close(o, p1, x, obj, g)
     c4.close()
     c3.close()
+
+
+def test_many_groups_screen_layout(o):
+    # L x n large enough (>= 4 CTAs per SM of work) for the transposed screen
+    # kernel (lane = chunk, warp = group): decisions and counters still the
+    # reference's, screened == dense bitwise, and a fast solve (fused group
+    # norms in the screen) follows the baseline solve bit for bit.
+    sizes = [3] * 1000
+    p, rng = random_problem(sizes, 5000, 0.3, 0.6, 21, weighted=True)
+    ctx = ctx_of(p)
+    x0 = np.zeros(p.m + p.n)
+    x1 = np.concatenate([rng.uniform(-0.1, 1.2, p.m), rng.uniform(-0.1, 1.2, p.n)]) * 1e-3
+    x2 = x1 + 1e-5 * rng.normal(size=x1.size)
+    ctx.init_snapshot(x0)
+    ctx.refresh(x1, True)
+    mem_o, _ = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+    obj_s, g_s, st = ctx.eval(x2, screened=True)
+    ga, gb, c_o, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem_o, x2[: p.m], x2[p.m:])
+    assert [st.in_active, st.skipped, st.unskipped, st.upper_bounds] == c_o.tolist()
+    assert_eval_close(o, p, x2, obj_s, g_s, None, np.concatenate([ga, gb]))
+    obj_d, g_d, _ = ctx.eval(x2)
+    assert obj_d == obj_s and np.array_equal(g_d, g_s)
+    rb = ctx.solve(mode=0, max_outer_loops=3, grad_tol=1e-12)
+    rf = ctx.solve(mode=1, max_outer_loops=3, grad_tol=1e-12)
+    assert np.array_equal(rf["x"], rb["x"]) and rf["objective"] == rb["objective"]
+    assert rf["blocks_skipped"] > 0
+    ctx.close()
