@@ -271,12 +271,16 @@ void alloc_buffers(gsot_ctx* c) {
     const int gmax = *std::max_element(c->sizes.begin(), c->sizes.end());
     int seg = gsot::eval_buf_rows(gmax);
     if (const char* ev = std::getenv("GSOT_EVAL_SEG")) seg = std::max(8, std::min(128, std::atoi(ev)));
-    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0));
+    // tiles taller than a segment: the recomputing variant (k_eval<true>)
+    bool rec = gmax > seg;
+    if (const char* ev = std::getenv("GSOT_EVAL_RECOMPUTE")) rec = std::atoi(ev) != 0;
+    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0), rec);
+    c->eval_recompute = rec;
     c->eval_buf = seg;
     c->eval_grid = c->num_sms * bps;
     if (std::getenv("GSOT_DIAG_SEQ"))
-      std::fprintf(stderr, "[gsot diag] eval: %d rows per segment, %d CTAs per SM, %zu B shared\n",
-                   seg, bps, gsot::eval_smem_bytes(seg, 0));
+      std::fprintf(stderr, "[gsot diag] eval: %d rows per segment, %d CTAs per SM, %zu B shared%s\n",
+                   seg, bps, gsot::eval_smem_bytes(seg, 0), rec ? ", recompute" : "");
   }
   c->sync();
 }
@@ -505,10 +509,11 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
     if (mode == GSOT_EVAL_SCREENED)
       launch_eval(P, d_x, c->tasks, -1, &c->sc->ntasks, words, c->rowpart, c->colpart, c->psi,
-                  c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
+                  c->eval_buf, c->eval_recompute, c->eval_grid, &c->sc->next_task, c->stream);
     else
       launch_eval(P, d_x, c->dense_tasks, c->L * c->nw, nullptr, words, c->rowpart, c->colpart,
-                  c->psi, c->eval_buf, c->eval_grid, &c->sc->next_task, c->stream);
+                  c->psi, c->eval_buf, c->eval_recompute, c->eval_grid, &c->sc->next_task,
+                  c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
     const bool scr = mode == GSOT_EVAL_SCREENED;

@@ -108,6 +108,7 @@ struct gsot_ctx {
   gsot::EvalScalars* h_sc = nullptr;  // &h_sync->sc
   int eval_grid = 148 * 4;
   int eval_buf = 96;  // rows per shared-memory segment in k_eval
+  bool eval_recompute = false;  // k_eval<true>: some block is taller than a segment
   int red_blocks = 148 * 2;
   // solver
   std::unique_ptr<gsot::SolverWorkspace> ws;

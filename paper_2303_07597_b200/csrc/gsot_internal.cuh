@@ -151,12 +151,13 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
 // Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
 size_t eval_smem_bytes(int buf_rows, int cap);
-int eval_blocks_per_sm(size_t smem);
+int eval_blocks_per_sm(size_t smem, bool recompute);
 // ntasks >= 0: `tasks` holds that many entries (dense list); -1: the
 // screened list, length *ntasks_dev (written by the screen kernel).
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int seg, int grid, int* next_task, cudaStream_t s);
+                 double* psi, int seg, bool recompute, int grid, int* next_task,
+                 cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const uint32_t* gmask, uint32_t* cmask, int clear_cmask,

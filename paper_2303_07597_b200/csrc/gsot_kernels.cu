@@ -702,7 +702,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
+// kRecompute (used when some block is taller than a segment): pass 1 leaves
+// the cost in shared memory and pass 2 recomputes [f]+ from it, so a tile
+// streamed twice needs no in-place rewrite either -- about half the shared
+// memory traffic per element of such tiles, for more registers (3 CTAs per
+// SM). Otherwise pass 1 writes [f]+ in place and pass 2 reads it (4 CTAs).
+template <bool kRecompute>
+__global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const EvalArgs A) {
   extern __shared__ __align__(128) unsigned char eval_smem[];
   const DevProblem& P = A.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -744,6 +750,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
     };
     // CTA b starts with task b; further tasks are claimed from grid onwards
     const int G = (int)gridDim.x;
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     uint32_t e = 0;
     EvalTask T = fetch(blockIdx.x);
     int tn = T.valid ? G + atomicAdd(A.next_task, 1) : ntasks;  // claimed one task ahead
@@ -760,7 +767,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
           return;
         }
         // alpha rides along with each cost segment (x is 16-byte aligned)
-        const int r0 = (k < T.nseg ? k : k - T.nseg) * A.seg, rows = min(A.seg, T.g - r0);
+        const int r0 = (k < T.nseg ? k : 2 * T.nseg - 1 - k) * A.seg, rows = min(A.seg, T.g - r0);
         const int64_t a0 = (T.o0 + r0) & ~1ll;  // 16-byte aligned superset of the rows
         const uint32_t abytes = (uint32_t)(((T.o0 + r0 + rows - a0) + 1) & ~1ll) * 8u;
         // the task's beta chunk rides along with its first segment
@@ -768,8 +775,11 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
         const int64_t bn = P.m + P.n - b0 < 34 ? P.m + P.n - b0 : 34;
         const uint32_t bbytes = k == 0 ? (uint32_t)((bn + 1) & ~1ll) * 8u : 0u;
         mbar_expect_tx(&full[slot], (uint32_t)rows * 256u + abytes + bbytes);
-        tma_load_1d(slots + (size_t)slot * A.seg * 32, tile + (int64_t)r0 * 32,
-                    (uint32_t)rows * 256u, &full[slot]);
+        // a tile streamed twice stays in L2 between its passes (evict_last
+        // on the first pass); everything else is read once (evict_first)
+        tma_load_1d_hint(slots + (size_t)slot * A.seg * 32, tile + (int64_t)r0 * 32,
+                         (uint32_t)rows * 256u, &full[slot],
+                         (T.nseg > 1 && k < T.nseg) ? pol_keep : pol_stream);
         tma_load_1d(aslots + (size_t)slot * aslot_len(A.seg), A.x + a0, abytes, &full[slot]);
         if (k == 0) {
           tma_load_1d(bslots + (size_t)slot * 34, A.x + b0, bbytes, &full[slot]);
@@ -783,41 +793,42 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
   }
   // ---- consumers
   const int rr = lane & 15, hh = lane >> 4;  // row-reduction roles (pass 2)
-  int roff[16];  // byte offsets of this lane's 16 columns, rotated by rr (no bank conflicts)
-#pragma unroll
-  for (int q = 0; q < 16; ++q) roff[q] = (hh * 16 + ((q + rr) & 15)) * 8;
+  // column of this lane's q-th term, rotated by rr (no bank conflicts)
+  auto rcol = [&](int q) { return hh * 16 + ((q + rr) & 15); };
   uint32_t e = 0;
   for (;;) {
     mbar_wait_sleep(&full[e & 1u], (e >> 1) & 1u);
     const EvalTask T = tinfo[e & 1u];
     if (!T.valid) break;
+    const uint32_t s0 = e & 1u;  // the slot of the task's first segment (its beta chunk)
     const int64_t j = (int64_t)T.c * 32 + lane;
     const bool act = (T.word >> lane) & 1u;
     const double bj =
         act ? bslots[(size_t)(e & 1u) * 34 + ((P.m + 32ll * T.c) & 1) + lane] : 0.0;
     double z2 = 0.0, sv = 0.0;
-    double scr[16];  // scales of this lane's 16 rotated columns
+    double scr[16], bq[16];  // scales and betas of this lane's 16 rotated columns
     const int ne = T.nseg == 1 ? 1 : 2 * T.nseg;
     for (int k = 0; k < ne; ++k, ++e) {
       const int slot = e & 1u;
       if (k > 0) mbar_wait_sleep(&full[slot], (e >> 1) & 1u);
       double* __restrict__ buf = slots + (size_t)slot * A.seg * 32;
-      const int sgm = k < T.nseg ? k : k - T.nseg;
+      const int sgm = k < T.nseg ? k : 2 * T.nseg - 1 - k;  // pass 2 backwards (L2-warm first)
       const int r0 = sgm * A.seg, rows = min(A.seg, T.g - r0);
       const int R = (rows + kEvalWarps - 1) / kEvalWarps;
       const int w0 = min(rows, warp * R), w1 = min(rows, w0 + R);
       const double* __restrict__ as = aslots + (size_t)slot * aslot_len(A.seg) + ((T.o0 + r0) & 1);
       double* __restrict__ col = buf + lane;
-      if (act) {
-        if (k < T.nseg) {  // pass 1: accumulate, [f]+ in place of the cost
+      if (act && k < T.nseg) {  // pass 1: accumulate ([f]+ in place of the cost)
 #pragma unroll 4
-          for (int r = w0; r < w1; ++r) {
-            const double v = relu(residual(as[r], bj, col[r * 32]));
-            z2 = dadd(z2, dmul(v, v));
-            sv = dadd(sv, v);
-            col[r * 32] = v;
-          }
-        } else {  // re-streamed segment: [f]+ only
+        for (int r = w0; r < w1; ++r) {
+          const double v = relu(residual(as[r], bj, col[r * 32]));
+          z2 = dadd(z2, dmul(v, v));
+          sv = dadd(sv, v);
+          if constexpr (!kRecompute) col[r * 32] = v;
+        }
+      }
+      if constexpr (!kRecompute) {
+        if (act && k >= T.nseg) {  // re-streamed segment: [f]+ only
 #pragma unroll 4
           for (int r = w0; r < w1; ++r) col[r * 32] = relu(residual(as[r], bj, col[r * 32]));
         }
@@ -849,22 +860,34 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
           }
         }
         consumer_sync();
+        // scales and betas of this lane's 16 rotated columns (the task's beta
+        // slot is not reused before its last segment; columns >= n: 0)
+        const double* bsl = bslots + (size_t)s0 * 34 + ((P.m + 32ll * T.c) & 1);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) scr[q] = scale_sh[roff[q] >> 3];
+        for (int q = 0; q < 16; ++q) {
+          scr[q] = scale_sh[rcol(q)];
+          if constexpr (kRecompute) bq[q] = 32ll * T.c + rcol(q) < P.n ? bsl[rcol(q)] : 0.0;
+        }
       }
       if (T.nseg == 1 || k >= T.nseg) {
-        // pass 2: row partial sum_j scale_j [f]+_ij of the chunk. Lane (rr, hh)
-        // sums half hh of a row (columns in rotated order: no bank conflicts),
-        // then the two halves; 16 rows at a time. Inactive columns have scale
-        // 0 and a finite entry: an exact zero, as in a dense evaluation.
+        // pass 2: row partial sum_j scale_j [f]+_ij of the chunk ([f]+ read,
+        // or recomputed from the resident cost: the same bits as pass 1). Lane
+        // (rr, hh) sums half hh of a row (columns in rotated order: no bank
+        // conflicts), then the two halves; 16 rows at a time. Inactive columns
+        // have scale 0 and a finite [f]+: an exact zero, as in a dense evaluation.
         __syncwarp();
         for (int rb = w0; rb < w1; rb += 16) {
           double acc = 0.0;
           if (rr < w1 - rb) {
-            const char* __restrict__ row = reinterpret_cast<const char*>(buf + (rb + rr) * 32);
+            const double* __restrict__ row = buf + (rb + rr) * 32;
+            const double ar = kRecompute ? as[rb + rr] : 0.0;
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              acc = dadd(acc, dmul(scr[q], *reinterpret_cast<const double*>(row + roff[q])));
+            for (int q = 0; q < 16; ++q) {
+              if constexpr (kRecompute)
+                acc = dadd(acc, dmul(scr[q], relu(residual(ar, bq[q], row[rcol(q)]))));
+              else
+                acc = dadd(acc, dmul(scr[q], row[rcol(q)]));
+            }
           }
           acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, 16));
           if (hh == 0 && rr < w1 - rb) A.rowpart[(int64_t)T.c * P.m + T.o0 + r0 + rb + rr] = acc;
@@ -878,8 +901,7 @@ __global__ void __launch_bounds__(kEvalThreads, 4) k_eval(const EvalArgs A) {
 }
 
 namespace {
-int g_eval_per_sm = 0;
-int g_eval_smem_attr = 0;
+int g_eval_smem_attr[2] = {0, 0};
 }
 
 // Rows per segment: the tallest group when it fits, else kEvalMaxSeg.
@@ -890,32 +912,35 @@ size_t eval_smem_bytes(int seg, int cap) {
   return sizeof(double) * 2 * ((size_t)seg * 32 + aslot_len(seg) + 34);
 }
 
-int eval_blocks_per_sm(size_t smem) {
-  if ((int)smem > g_eval_smem_attr) {
-    cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static void (*eval_kernel(bool recompute))(const EvalArgs) {
+  return recompute ? k_eval<true> : k_eval<false>;
+}
+
+int eval_blocks_per_sm(size_t smem, bool recompute) {
+  auto kern = eval_kernel(recompute);
+  if ((int)smem > g_eval_smem_attr[recompute]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // all of the unified L1 / shared array as shared memory: one more CTA
     // (one more tile in flight) per SM
-    cudaFuncSetAttribute(k_eval, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    g_eval_smem_attr = (int)smem;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    g_eval_smem_attr[recompute] = (int)smem;
   }
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval, kEvalThreads, smem) !=
-          cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kEvalThreads, smem) != cudaSuccess ||
       n < 1)
     n = 1;
-  g_eval_per_sm = n;
   return n;
 }
 
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int seg, int grid, int* next_task, cudaStream_t s) {
+                 double* psi, int seg, bool recompute, int grid, int* next_task, cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0)
     throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
   EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev};
   const size_t smem = eval_smem_bytes(seg, 0);
-  if ((int)smem > g_eval_smem_attr) eval_blocks_per_sm(smem);
-  launch_pdl(k_eval, dim3(grid), dim3(kEvalThreads), smem, s, A);
+  if ((int)smem > g_eval_smem_attr[recompute]) eval_blocks_per_sm(smem, recompute);
+  launch_pdl(eval_kernel(recompute), dim3(grid), dim3(kEvalThreads), smem, s, A);
 }
 
 // ---------------------------------------------------------------- finalize

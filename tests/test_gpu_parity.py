@@ -189,6 +189,7 @@ STRUCTURES = {
     "odd_ragged": ([3, 33, 1, 7, 64, 65, 2], 97),
     "n_one": ([4, 5], 1),
     "n_33": ([9, 9, 9], 33),
+    "tall_groups": ([1000, 130, 129, 40, 7], 75),
 }
 
 
@@ -444,3 +445,55 @@ def test_many_groups_screen_layout(o):
     assert np.array_equal(rf["x"], rb["x"]) and rf["objective"] == rb["objective"]
     assert rf["blocks_skipped"] > 0
     ctx.close()
+
+
+def test_tall_blocks_streamed_twice(o):
+    # Blocks taller than one shared-memory segment (128 rows) are streamed
+    # twice by one CTA (pass 1 forwards, pass 2 backwards): 30000 rows (235
+    # segments), 1000 rows (8), 129 rows (a 1-row last segment). Against the
+    # oracle, screened == dense bitwise, repeatable, fast == baseline bitwise.
+    sizes = [30000, 1000, 129, 3]
+    p, rng = random_problem(sizes, 40, 0.3, 0.6, 31, weighted=True)
+    ctx = ctx_of(p)
+    x0 = np.zeros(p.m + p.n)
+    x1 = np.concatenate([rng.uniform(-0.1, 1.2, p.m) * 1e-4, rng.uniform(-0.1, 1.2, p.n)])
+    x2 = x1 + 1e-6 * rng.normal(size=x1.size)
+    obj, g, _ = ctx.eval(x1)
+    assert_eval_close(o, p, x1, obj, g)
+    ctx.init_snapshot(x0)
+    ctx.refresh(x1, True)
+    mem_o, _ = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+    obj_s, g_s, st = ctx.eval(x2, screened=True)
+    ga, gb, c_o, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem_o, x2[: p.m], x2[p.m:])
+    assert [st.in_active, st.skipped, st.unskipped, st.upper_bounds] == c_o.tolist()
+    assert_eval_close(o, p, x2, obj_s, g_s, None, np.concatenate([ga, gb]))
+    obj_d, g_d, _ = ctx.eval(x2)
+    assert obj_d == obj_s and np.array_equal(g_d, g_s)
+    for _ in range(3):
+        obj_r, g_r, _ = ctx.eval(x2)
+        assert obj_r == obj_d and np.array_equal(g_r, g_d)
+    rb = ctx.solve(mode=0, max_outer_loops=3, grad_tol=1e-12)
+    rf = ctx.solve(mode=1, max_outer_loops=3, grad_tol=1e-12)
+    assert np.array_equal(rf["x"], rb["x"]) and rf["objective"] == rb["objective"]
+    ctx.close()
+
+
+@pytest.mark.parametrize("sizes", [[100, 28, 5], [300, 129, 7]])
+def test_eval_variants_agree_bitwise(o, sizes, monkeypatch):
+    # k_eval<false> writes [f]+ in place, k_eval<true> (chosen when a block is
+    # taller than a segment) recomputes it in pass 2: the same bits either way.
+    p, rng = random_problem(sizes, 70, 0.3, 0.6, 41, weighted=True)
+    x = np.concatenate([rng.uniform(-0.1, 1.2, p.m) * 1e-3, rng.uniform(-0.1, 1.2, p.n)])
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("GSOT_EVAL_RECOMPUTE", v)
+        monkeypatch.setenv("GSOT_CTX_CACHE", "0")
+        ctx = ctx_of(p)
+        ctx.init_snapshot(np.zeros(p.m + p.n))
+        ctx.refresh(x, True)
+        out.append((ctx.eval(x)[:2], ctx.eval(x * 1.01, screened=True)[:2]))
+        ctx.close()
+    (d0, s0), (d1, s1) = out
+    assert d0[0] == d1[0] and np.array_equal(d0[1], d1[1])
+    assert s0[0] == s1[0] and np.array_equal(s0[1], s1[1])
+    assert_eval_close(o, p, x, d1[0], d1[1])

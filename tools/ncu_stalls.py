@@ -1,6 +1,6 @@
 """Top warp-stall SASS lines of one kernel in an ncu report.
 
-    python tools/ncu_stalls.py REPORT.ncu-rep KERNEL_REGEX [N]
+    python tools/ncu_stalls.py REPORT.ncu-rep KERNEL_REGEX [N] [LAUNCH_SKIP]
 """
 import csv
 import io
@@ -10,7 +10,7 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                      "--launch-count", "1", "--print-source", "sass"], capture_output=True,
+                      "--launch-skip", sys.argv[4] if len(sys.argv) > 4 else "0", "--launch-count", "1", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))[1:]
 h = rows[0]
