@@ -23,7 +23,8 @@ UNIT = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, 
 
 
 def short(name: str) -> str:
-    return name.split("(")[0].replace("gsot::", "").replace("void ", "").strip()
+    # template arguments dropped (k_eval<0> and k_eval<1> are both "k_eval")
+    return name.split("(")[0].split("<")[0].replace("gsot::", "").replace("void ", "").strip()
 
 
 def launches(tag: str):
