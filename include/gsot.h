@@ -23,6 +23,7 @@
  *  GradStats::PerCall           screening.hpp:181  gsot_call_stats
  *  recover_plan                 dual.hpp:116-128   gsot_plan_columns (column-streamed)
  *  plan nonzero blocks          dual.hpp:139-169   gsot_block_mask
+ *  plan_diagnostics(recover_plan) dual.hpp:130-169 gsot_plan_diagnostics
  *  solve / solve_baseline /     solver.hpp:92-293  gsot_solve
  *    solve_fast / audit_solve
  *  SolverOptions, Solution      solver.hpp:25-42   gsot_solver_options, gsot_solve_result
@@ -166,6 +167,19 @@ GSOT_API int gsot_block_mask(gsot_ctx* ctx, const double* x, uint8_t* nonzero);
  * values. */
 GSOT_API int gsot_plan_columns(gsot_ctx* ctx, const double* x, int64_t j0, int64_t j1,
                                double* out);
+/* PlanDiagnostics (dual.hpp:130-135) of the plan at x. */
+typedef struct gsot_plan_diag {
+  double marginal_res_a; /* |T 1 - a|_inf */
+  double marginal_res_b; /* |T' 1 - b|_inf */
+  double group_sparsity; /* fraction of (group, column) blocks that are all 0.0 */
+  double mass;           /* sum of all plan entries */
+} gsot_plan_diag;
+/* plan_diagnostics(recover_plan(x), inst) (dual.hpp:116-128, :139-169)
+ * computed on the device without storing the plan: group_sparsity is exact
+ * (the same all-zero test on bitwise plan entries); the residuals and mass
+ * come from device row / column sums (fixed order, not the reference's
+ * summation order: reported, not asserted, as in the reference). */
+GSOT_API int gsot_plan_diagnostics(gsot_ctx* ctx, const double* x, gsot_plan_diag* out);
 
 /* ---- Stage 2: the whole solve -------------------------------------------- */
 

@@ -211,6 +211,41 @@ void go_recover_plan(const go_problem* p, const double* alpha, const double* bet
   go_plan_columns(p, alpha, beta, 0, p->n, plan);
 }
 
+void go_plan_diagnostics(const go_problem* p, const double* plan,
+                         double* out) { /* dual.hpp:139-169 */
+  const int64_t m = p->m, n = p->n;
+  /* rowwise().sum(): row i summed over j in order (sequential Eigen reduction) */
+  double ra = 0.0, rb = 0.0, mass = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j < n; ++j) s += plan[i + j * m];
+    const double d = fabs(s - p->a[i]);
+    ra = (i == 0 || d > ra) ? d : ra; /* cwiseAbs().maxCoeff() */
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s += plan[i + j * m];
+    const double d = fabs(s - p->b[j]);
+    rb = (j == 0 || d > rb) ? d : rb;
+  }
+  for (int64_t e = 0; e < m * n; ++e) mass += plan[e]; /* t.plan.sum(), storage order */
+  long zero_blocks = 0;
+  for (int64_t j = 0; j < n; ++j)
+    for (int l = 0; l < p->L; ++l) {
+      int all_zero = 1;
+      for (int64_t i = p->offsets[l]; i < p->offsets[l] + p->sizes[l]; ++i)
+        if (plan[i + j * m] != 0.0) {
+          all_zero = 0;
+          break;
+        }
+      zero_blocks += all_zero;
+    }
+  out[0] = ra;
+  out[1] = rb;
+  out[2] = (double)zero_blocks / ((double)p->L * (double)n);
+  out[3] = mass;
+}
+
 /* ---------------------------------------------------------------- screening */
 
 void go_take_snapshot(const go_problem* p, const double* alpha, const double* beta, double* z,

@@ -60,6 +60,10 @@ void go_recover_plan(const go_problem* p, const double* alpha, const double* bet
 void go_plan_columns(const go_problem* p, const double* alpha, const double* beta, int64_t j0,
                      int64_t j1, double* out);
 
+/* dual.hpp:139-169 plan_diagnostics of an m x n column-major plan:
+ * out = {marginal_res_a, marginal_res_b, group_sparsity, mass}. */
+void go_plan_diagnostics(const go_problem* p, const double* plan, double* out);
+
 /* screening.hpp:24-50 take_snapshot: z,k,o are L x n column-major. */
 void go_take_snapshot(const go_problem* p, const double* alpha, const double* beta, double* z,
                       double* k, double* o);

@@ -119,6 +119,26 @@ int ref_eval(const double* cost, int64_t m, int64_t n, const int32_t* sizes, int
   }
 }
 
+// plan_diagnostics(recover_plan(x)) (dual.hpp:116-169); out = {res_a, res_b,
+// group_sparsity, mass}. plan_in (optional) replaces the recovered plan.
+int ref_plan_diagnostics(const double* cost, int64_t m, int64_t n, const int32_t* sizes, int32_t L,
+                         const double* a, const double* b, const double* plan_in, double* out) {
+  try {
+    ProblemInstance inst = make(cost, m, n, sizes, L, a, b);
+    TransportPlan t;
+    t.plan.resize(m, n);
+    std::memcpy(t.plan.data(), plan_in, sizeof(double) * static_cast<size_t>(m * n));
+    const PlanDiagnostics d = plan_diagnostics(t, inst);
+    out[0] = d.marginal_res_a;
+    out[1] = d.marginal_res_b;
+    out[2] = d.group_sparsity;
+    out[3] = d.mass;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 int ref_plan(const double* cost, int64_t m, int64_t n, const int32_t* sizes, int32_t L,
              const double* a, const double* b, double gamma, double mu, const double* alpha,
              const double* beta, double* plan) {

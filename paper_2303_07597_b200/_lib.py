@@ -57,6 +57,12 @@ class SolveResultC(C.Structure):
 
 
 # Every entry point of include/gsot.h with its C signature.
+class PlanDiagC(C.Structure):
+    """gsot_plan_diag (PlanDiagnostics, dual.hpp:130-135)."""
+    _fields_ = [("marginal_res_a", C.c_double), ("marginal_res_b", C.c_double),
+                ("group_sparsity", C.c_double), ("mass", C.c_double)]
+
+
 _vp, _dp, _ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int32)
 SIGNATURES = {
     "gsot_last_error": (C.c_char_p, []),
@@ -79,6 +85,7 @@ SIGNATURES = {
     "gsot_active_set": (C.c_int, [_vp, _vp, C.POINTER(C.c_int64)]),
     "gsot_block_mask": (C.c_int, [_vp, _vp, _vp]),
     "gsot_plan_columns": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp]),
+    "gsot_plan_diagnostics": (C.c_int, [_vp, _vp, C.POINTER(PlanDiagC)]),
     "gsot_default_solver_options": (None, [C.POINTER(SolverOptionsC)]),
     "gsot_solve": (C.c_int, [_vp, C.POINTER(SolverOptionsC), _vp, C.POINTER(SolveResultC), _vp,
                              C.c_int64]),

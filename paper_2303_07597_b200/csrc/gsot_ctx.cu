@@ -5,6 +5,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <cstdlib>
 #include <chrono>
 #include <cstdio>
@@ -807,6 +809,50 @@ GSOT_API int gsot_plan_columns(gsot_ctx* ctx, const double* x, int64_t j0, int64
                                       ctx->stream));
     }
     ctx->sync();
+  });
+}
+
+GSOT_API int gsot_plan_diagnostics(gsot_ctx* ctx, const double* x, gsot_plan_diag* out) {
+  return guard([&] {
+    checked(ctx);
+    if (!out) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null output");
+    upload_x(ctx, x);
+    const gsot::DevProblem P = ctx->problem();
+    const int64_t m = ctx->m, n = ctx->n;
+    GSOT_CUDA_CHECK(cudaMemsetAsync(ctx->cnt_partials, 0, sizeof(unsigned long long), ctx->stream));
+    ctx->launch(gsot::K_MISC, 16.0 * m * n, [&] {
+      gsot::launch_plan_diag(P, ctx->x_eval, ctx->rowpart, ctx->colpart, ctx->cnt_partials,
+                             ctx->stream);
+    });
+    ctx->launch(gsot::K_MISC, 8.0 * (static_cast<double>(ctx->nw) * m + static_cast<double>(ctx->L) * n),
+                [&] {
+                  gsot::launch_plan_diag_fold(P, ctx->rowpart, ctx->colpart, ctx->g_eval,
+                                              ctx->stream);
+                });
+    std::vector<double> sums(static_cast<size_t>(m + n)), a(static_cast<size_t>(m)),
+        b(static_cast<size_t>(n));
+    unsigned long long zero = 0;
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(sums.data(), ctx->g_eval, sizeof(double) * (m + n),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(a.data(), ctx->d_a, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(b.data(), ctx->d_b, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(&zero, ctx->cnt_partials, sizeof(zero), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+    ctx->sync();
+    // (T 1 - a).cwiseAbs().maxCoeff(), (T' 1 - b)..., T.sum() (dual.hpp:143-147)
+    double ra = std::abs(sums[0] - a[0]), rb = std::abs(sums[m] - b[0]), mass = 0.0;
+    for (int64_t i = 0; i < m; ++i) ra = std::max(ra, std::abs(sums[i] - a[i]));
+    for (int64_t j = 0; j < n; ++j) {
+      rb = std::max(rb, std::abs(sums[m + j] - b[j]));
+      mass += sums[m + j];
+    }
+    out->marginal_res_a = ra;
+    out->marginal_res_b = rb;
+    out->group_sparsity = static_cast<double>(zero) /
+                          (static_cast<double>(ctx->L) * static_cast<double>(n));
+    out->mass = mass;
   });
 }
 

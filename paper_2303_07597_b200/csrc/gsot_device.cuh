@@ -10,6 +10,9 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+// fused multiply-add (one rounding): fast-mode evaluation only, never on an
+// exact-order path
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
 
 // f = (alpha_i + beta_j) - c_ij, regularizer.hpp:57.
 __device__ __forceinline__ double residual(double alpha_i, double beta_j, double c) {
@@ -218,9 +221,13 @@ enum TimelineId { TL_SCREEN = 0, TL_EVAL = 1, TL_FINALIZE = 2, TL_PUBLISH = 3, T
                   TL_AXPY = 5, TL_DELTA = 6, TL_SNAPSHOT = 7 };
 
 // max(f, 0) by bit operations (f finite): a negative f, -0 included, -> +0.
+// Spelled on the two 32-bit halves (one shift, two and-nots on the integer
+// pipe; the 64-bit form compiles to two compares and two selects).
 __device__ __forceinline__ double relu(double f) {
-  const long long b = __double_as_longlong(f);
-  return __longlong_as_double(b & ~(b >> 63));
+  const int hi = __double2hiint(f), lo = __double2loint(f);
+  int s;
+  asm("shr.s32 %0, %1, 31;" : "=r"(s) : "r"(hi));
+  return __hiloint2double(hi & ~s, lo & ~s);
 }
 
 // Called by exactly one full warp.

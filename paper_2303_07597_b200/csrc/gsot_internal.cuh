@@ -164,6 +164,13 @@ void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words
                      const double* rowpart, const double* colpart, const double* psi,
                      double* grad, const double* dvec, double* partials, EvalScalars* sc,
                      int cnt_pending, cudaStream_t s);
+// plan_diagnostics at x: per-chunk row sums into rowpart, per-block column
+// sums into colpart, all-zero block count added to *zero_blocks; the fold
+// writes plan row sums to sums[0, m) and column sums to sums[m, m + n).
+void launch_plan_diag(const DevProblem& P, const double* x, double* rowpart, double* colpart,
+                      unsigned long long* zero_blocks, cudaStream_t s);
+void launch_plan_diag_fold(const DevProblem& P, const double* rowpart, const double* colpart,
+                           double* sums, cudaStream_t s);
 void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,
                          double* out, cudaStream_t s);
 void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* words,

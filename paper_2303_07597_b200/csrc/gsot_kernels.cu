@@ -793,8 +793,12 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
   }
   // ---- consumers
   const int rr = lane & 15, hh = lane >> 4;  // row-reduction roles (pass 2)
-  // column of this lane's q-th term, rotated by rr (no bank conflicts)
-  auto rcol = [&](int q) { return hh * 16 + ((q + rr) & 15); };
+  // first column of this lane's p-th column pair, rotated by rr: the eight
+  // lanes of a quarter warp read eight distinct 16-byte words of their rows
+  // (no bank conflicts for 16-byte shared loads)
+  int pcol[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) pcol[p] = hh * 16 + 2 * ((p + rr) & 7);
   uint32_t e = 0;
   for (;;) {
     mbar_wait_sleep(&full[e & 1u], (e >> 1) & 1u);
@@ -806,7 +810,7 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
     const double bj =
         act ? bslots[(size_t)(e & 1u) * 34 + ((P.m + 32ll * T.c) & 1) + lane] : 0.0;
     double z2 = 0.0, sv = 0.0;
-    double scr[16], bq[16];  // scales and betas of this lane's 16 rotated columns
+    double scr[16], bq[16];  // scales and betas of this lane's 8 rotated column pairs
     const int ne = T.nseg == 1 ? 1 : 2 * T.nseg;
     for (int k = 0; k < ne; ++k, ++e) {
       const int slot = e & 1u;
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
 #pragma unroll 4
         for (int r = w0; r < w1; ++r) {
           const double v = relu(residual(as[r], bj, col[r * 32]));
-          z2 = dadd(z2, dmul(v, v));
+          z2 = dfma(v, v, z2);
           sv = dadd(sv, v);
           if constexpr (!kRecompute) col[r * 32] = v;
         }
@@ -865,16 +869,18 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
         const double* bsl = bslots + (size_t)s0 * 34 + ((P.m + 32ll * T.c) & 1);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          scr[q] = scale_sh[rcol(q)];
-          if constexpr (kRecompute) bq[q] = 32ll * T.c + rcol(q) < P.n ? bsl[rcol(q)] : 0.0;
+          const int cq = pcol[q >> 1] + (q & 1);
+          scr[q] = scale_sh[cq];
+          if constexpr (kRecompute) bq[q] = 32ll * T.c + cq < P.n ? bsl[cq] : 0.0;
         }
       }
       if (T.nseg == 1 || k >= T.nseg) {
         // pass 2: row partial sum_j scale_j [f]+_ij of the chunk ([f]+ read,
         // or recomputed from the resident cost: the same bits as pass 1). Lane
-        // (rr, hh) sums half hh of a row (columns in rotated order: no bank
-        // conflicts), then the two halves; 16 rows at a time. Inactive columns
-        // have scale 0 and a finite [f]+: an exact zero, as in a dense evaluation.
+        // (rr, hh) sums half hh of a row, two columns per 16-byte load (pairs in
+        // rotated order: no bank conflicts), then the two halves; 16 rows at a
+        // time. Inactive columns have scale 0 and a finite [f]+: an exact zero,
+        // as in a dense evaluation.
         __syncwarp();
         for (int rb = w0; rb < w1; rb += 16) {
           double acc = 0.0;
@@ -882,11 +888,15 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
             const double* __restrict__ row = buf + (rb + rr) * 32;
             const double ar = kRecompute ? as[rb + rr] : 0.0;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              if constexpr (kRecompute)
-                acc = dadd(acc, dmul(scr[q], relu(residual(ar, bq[q], row[rcol(q)]))));
-              else
-                acc = dadd(acc, dmul(scr[q], row[rcol(q)]));
+            for (int p = 0; p < 8; ++p) {
+              const double2 v = *reinterpret_cast<const double2*>(row + pcol[p]);
+              if constexpr (kRecompute) {
+                acc = dfma(scr[2 * p], relu(residual(ar, bq[2 * p], v.x)), acc);
+                acc = dfma(scr[2 * p + 1], relu(residual(ar, bq[2 * p + 1], v.y)), acc);
+              } else {
+                acc = dfma(scr[2 * p], v.x, acc);
+                acc = dfma(scr[2 * p + 1], v.y, acc);
+              }
             }
           }
           acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, 16));
@@ -1169,6 +1179,80 @@ void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64
                          double* out, cudaStream_t s) {
   dim3 grid((unsigned)((ncols + 255) / 256), (unsigned)P.L);
   k_plan<<<grid, 256, 0, s>>>(P, x, j0, ncols, out);
+}
+
+// ---------------------------------------------------------------- plan diagnostics
+// plan_diagnostics(recover_plan(x)) (dual.hpp:116-128, :139-169) without
+// storing the plan. One warp per (group l, 32-column chunk c), lane = column:
+// the plan entries are k_plan's (bitwise grad_block values); per column the
+// block's entry sum (sequential in rows) goes to colpart[l*n + j]; per row the
+// chunk's entry sum (fixed xor tree over the 32 lanes) to rowpart[c*m + i];
+// blocks whose entries are all exactly 0.0 are counted (the reference's
+// all_zero test, dual.hpp:153-162).
+__global__ void __launch_bounds__(128) k_plan_diag(DevProblem P, const double* __restrict__ x,
+                                                   double* __restrict__ rowpart,
+                                                   double* __restrict__ colpart,
+                                                   unsigned long long* __restrict__ zero_blocks) {
+  const int lane = threadIdx.x & 31;
+  const int l = blockIdx.y * 4 + (threadIdx.x >> 5);
+  if (l >= P.L) return;  // whole warp
+  const int c = blockIdx.x;
+  const int64_t j = 32ll * c + lane;
+  const bool valid = j < P.n;
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const double z = valid ? block_z(P, x, l, j) : 0.0;
+  const bool nz = valid && z > P.tau;
+  const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
+  const double bj = valid ? x[P.m + j] : 0.0;
+  const double* __restrict__ cp = block_ptr(P, o0, g, valid ? j : 32ll * c);
+  double colsum = 0.0;
+  bool any = false;
+  for (int r = 0; r < g; ++r) {
+    double t = 0.0;
+    if (nz) {
+      const double f = residual(__ldg(x + o0 + r), bj, cp[32 * r]);
+      t = f > 0.0 ? dmul(scale, f) : 0.0;
+    }
+    colsum = dadd(colsum, t);
+    any = any || t != 0.0;
+    double rs = t;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) rs = dadd(rs, __shfl_xor_sync(0xffffffffu, rs, o));
+    if (lane == 0) rowpart[(int64_t)c * P.m + o0 + r] = rs;
+  }
+  if (valid) colpart[(int64_t)l * P.n + j] = colsum;
+  const unsigned zero = __ballot_sync(0xffffffffu, valid && !any);
+  if (lane == 0 && zero) atomicAdd(zero_blocks, (unsigned long long)__popc(zero));
+}
+
+// Plan row sums (over the chunks, in chunk order) into out[0, m) and column
+// sums (over the groups, in group order) into out[m, m + n).
+__global__ void __launch_bounds__(256) k_plan_diag_fold(DevProblem P,
+                                                        const double* __restrict__ rowpart,
+                                                        const double* __restrict__ colpart,
+                                                        double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < P.m) {
+    double s = 0.0;
+    for (int c = 0; c < P.nw; ++c) s = dadd(s, rowpart[(int64_t)c * P.m + t]);
+    out[t] = s;
+  } else if (t < P.m + P.n) {
+    const int64_t j = t - P.m;
+    double s = 0.0;
+    for (int l = 0; l < P.L; ++l) s = dadd(s, colpart[(int64_t)l * P.n + j]);
+    out[t] = s;
+  }
+}
+
+void launch_plan_diag(const DevProblem& P, const double* x, double* rowpart, double* colpart,
+                      unsigned long long* zero_blocks, cudaStream_t s) {
+  k_plan_diag<<<dim3((unsigned)P.nw, (unsigned)((P.L + 3) / 4)), 128, 0, s>>>(P, x, rowpart, colpart,
+                                                                            zero_blocks);
+}
+
+void launch_plan_diag_fold(const DevProblem& P, const double* rowpart, const double* colpart,
+                           double* sums, cudaStream_t s) {
+  k_plan_diag_fold<<<(unsigned)((P.m + P.n + 255) / 256), 256, 0, s>>>(P, rowpart, colpart, sums);
 }
 
 // ---------------------------------------------------------------- audit

@@ -364,6 +364,12 @@ class Context:
         _raise(_lib.lib().gsot_plan_columns(self._h, _ptr(_f64(x)), int(j0), int(j1), _ptr(out)))
         return out.reshape(self.m, j1 - j0, order="F")
 
+    def plan_diagnostics(self, x) -> "PlanDiagnostics":
+        """plan_diagnostics(recover_plan(x)) on the device (gsot_plan_diagnostics)."""
+        d = _lib.PlanDiagC()
+        _raise(_lib.lib().gsot_plan_diagnostics(self._h, _ptr(_f64(x)), C.byref(d)))
+        return PlanDiagnostics(d.marginal_res_a, d.marginal_res_b, d.group_sparsity, d.mass)
+
     def solve(self, mode: int = 1, snapshot_interval: int = 10, grad_tol: float = 1e-6,
               max_outer_loops: int = 200, lbfgs_memory: int = 10,
               upper_bound_offset: float = 0.0, history_cap: int = 0, exact: bool = False):
@@ -465,6 +471,12 @@ class PlanDiagnostics:
     marginal_res_b: float = 0.0
     group_sparsity: float = 0.0
     mass: float = 0.0
+
+
+def state_plan_diagnostics(s: DualState, inst: ProblemInstance, p: RegParams) -> PlanDiagnostics:
+    """plan_diagnostics(recover_plan(s, inst, p), inst) computed on the device
+    without materialising the m x n plan (gsot_plan_diagnostics)."""
+    return inst.context(p).plan_diagnostics(_state_vec(s, inst))
 
 
 def plan_diagnostics(t: TransportPlan, inst: ProblemInstance) -> PlanDiagnostics:

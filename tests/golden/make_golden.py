@@ -82,6 +82,9 @@ def record(ref: RefLib, name: str, p: Problem, seed: int, out: dict):
             out[f"{sk}/history"] = r["history"]
         rp = ref.solve(q, mode=1, max_outer_loops=20, grad_tol=1e-7, plan=True)
         out[f"{key}/solve_plan"] = rp["plan"]
+        # plan_diagnostics (dual.hpp:139-169) of the plan at s2 and at the solution
+        out[f"{key}/plan_diag"] = ref.plan_diagnostics(q, out[f"{key}/plan"])
+        out[f"{key}/solve_plan_diag"] = ref.plan_diagnostics(q, rp["plan"])
 
 
 def main():

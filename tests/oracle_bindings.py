@@ -184,6 +184,15 @@ class Oracle:
                                  be.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p))
         return out.reshape(p.m, p.n, order="F")
 
+    def plan_diagnostics(self, p: Problem, plan) -> np.ndarray:
+        """dual.hpp:139-169 on an m x n plan: [res_a, res_b, group_sparsity, mass]."""
+        gp, keep = self._gp(p)
+        pl = np.asfortranarray(plan, np.float64)
+        out = np.empty(4)
+        self.lib.go_plan_diagnostics(C.byref(gp), pl.ctypes.data_as(C.c_void_p),
+                                     out.ctypes.data_as(C.c_void_p))
+        return out
+
     def snapshot(self, p: Problem, alpha, beta):
         gp, keep = self._gp(p)
         al = np.ascontiguousarray(alpha, np.float64)
@@ -342,6 +351,15 @@ class RefLib:
                                out.ctypes.data_as(C.c_void_p))
         assert st == 0
         return out.reshape(p.m, p.n, order="F")
+
+    def plan_diagnostics(self, p: Problem, plan) -> np.ndarray:
+        keep, a = self._args(p)
+        pl = np.asfortranarray(plan, np.float64)
+        out = np.empty(4)
+        st = self.lib.ref_plan_diagnostics(*a, pl.ctypes.data_as(C.c_void_p),
+                                           out.ctypes.data_as(C.c_void_p))
+        assert st == 0, self.lib.ref_last_error()
+        return out
 
     def snapshot(self, p: Problem, alpha, beta):
         keep, a = self._args(p)

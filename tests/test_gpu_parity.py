@@ -108,6 +108,33 @@ def test_golden_eval_plan_snapshot_active(o, gold, name, pi):
     ctx.close()
 
 
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_golden_plan_diagnostics(gold, name, pi):
+    """gsot_plan_diagnostics against the reference's plan_diagnostics of its own
+    recovered plans (dual.hpp:139-169): the all-zero block fraction exactly;
+    residuals and mass within 1e-12 relative (device sums in a fixed order,
+    the reference's in Eigen's)."""
+    p = gold_problem(gold, name, pi)
+    key = f"{name}/p{pi}"
+    ctx = ctx_of(p)
+    for x, ref in ((gold[f"{key}/s2/x"], gold[f"{key}/plan_diag"]),
+                   (gold[f"{key}/solve1/x"], gold[f"{key}/solve_plan_diag"])):
+        d = ctx.plan_diagnostics(x)
+        assert d.group_sparsity == ref[2]
+        for got, want in ((d.marginal_res_a, ref[0]), (d.marginal_res_b, ref[1]), (d.mass, ref[3])):
+            assert abs(got - want) <= 1e-12 * max(1.0, abs(want)), (got, want)
+    ctx.close()
+
+
+def test_plan_diagnostics_zero_plan():
+    # test_dual.cpp:209-217 on the device: C = 0, x = 0 -> every block z = 0 <= tau
+    q = Problem(np.zeros((4, 2)), np.array([2, 2], np.int32), np.full(4, .25), np.full(2, .5),
+                1.0, 1.0)
+    d = ctx_of(q).plan_diagnostics(np.zeros(6))
+    assert (d.marginal_res_a, d.marginal_res_b, d.group_sparsity, d.mass) == (0.25, 0.5, 1.0, 0.0)
+
+
 def test_golden_hand_examples(gold):
     h = Problem(np.zeros((1, 1)), np.array([1], np.int32), np.ones(1), np.ones(1), 1.0, 0.5)
     ctx = ctx_of(h)

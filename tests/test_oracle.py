@@ -195,6 +195,29 @@ def test_oracle_reproduces_reference_golden_bitwise(o, gold, name, pi):
         assert np.array_equal(r["history"], gold[f"{sk}/history"])
 
 
+def test_plan_diagnostics_known_answers(o):
+    # test_dual.cpp:209-217: the zero plan of a 4 x 2 instance with groups {2, 2}
+    p = _problem(np.zeros((4, 2)), [2, 2], np.full(4, 0.25), vec(0.5, 0.5), 1.0, 1.0)
+    assert o.plan_diagnostics(p, np.zeros((4, 2))).tolist() == [0.25, 0.5, 1.0, 0.0]
+    # :219-227: the independent coupling a b' has (near-)exact marginals, mass 1
+    rng = np.random.default_rng(41)
+    a = rng.uniform(0.1, 1, 6)
+    b = rng.uniform(0.1, 1, 4)
+    p = _problem(rng.uniform(0, 1, (6, 4)), [2, 2, 2], a / a.sum(), b / b.sum(), 1.0, 1.0)
+    d = o.plan_diagnostics(p, np.outer(p.a, p.b))
+    assert d[0] <= 1e-14 and d[1] <= 1e-14 and d[2] == 0.0 and abs(d[3] - 1.0) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_oracle_plan_diagnostics_golden_bitwise(o, gold, name, pi):
+    p = _gold_problem(gold, name, pi)
+    key = f"{name}/p{pi}"
+    assert np.array_equal(o.plan_diagnostics(p, gold[f"{key}/plan"]), gold[f"{key}/plan_diag"])
+    assert np.array_equal(o.plan_diagnostics(p, gold[f"{key}/solve_plan"]),
+                          gold[f"{key}/solve_plan_diag"])
+
+
 def test_oracle_hand_golden(o, gold):
     p = _problem(np.zeros((1, 1)), [1], vec(1.0), vec(1.0), 1.0, 0.5)
     assert o.objective(p, vec(1.0), vec(0.0)) == gold["hand/1x1/objective"][0]
@@ -242,6 +265,19 @@ def test_oracle_equals_reference_random(o, seed):
             O = o.solve(p, mode=mode, max_outer_loops=10)
             assert np.array_equal(R["x"], O["x"]) and R["objective"] == O["objective"]
             assert np.array_equal(R["history"], O["history"])
+
+
+@needs_ref
+def test_oracle_plan_diagnostics_equals_reference_random(o):
+    ref = RefLib()
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        sizes = rng.integers(1, 9, size=5).astype(np.int32)
+        m, n = int(sizes.sum()), int(rng.integers(2, 30))
+        p = Problem(rng.uniform(0, 2, (m, n)), sizes, np.full(m, 1 / m), np.full(n, 1 / n), 1.0, 1.0)
+        plan = rng.uniform(0, 1e-2, (m, n)) * (rng.uniform(0, 1, (m, n)) < 0.3)
+        plan[: sizes[0], :] = 0.0  # whole zero blocks
+        assert np.array_equal(o.plan_diagnostics(p, plan), ref.plan_diagnostics(p, plan))
 
 
 @needs_ref
