@@ -276,13 +276,15 @@ void alloc_buffers(gsot_ctx* c) {
     // tiles taller than a segment: the recomputing variant (k_eval<true>)
     bool rec = gmax > seg;
     if (const char* ev = std::getenv("GSOT_EVAL_RECOMPUTE")) rec = std::atoi(ev) != 0;
-    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0), rec);
+    const int var = gsot::eval_variant(gmax, seg, rec);
+    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0), var);
     c->eval_recompute = rec;
+    c->eval_variant = var;
     c->eval_buf = seg;
     c->eval_grid = c->num_sms * bps;
     if (std::getenv("GSOT_DIAG_SEQ"))
-      std::fprintf(stderr, "[gsot diag] eval: %d rows per segment, %d CTAs per SM, %zu B shared%s\n",
-                   seg, bps, gsot::eval_smem_bytes(seg, 0), rec ? ", recompute" : "");
+      std::fprintf(stderr, "[gsot diag] eval: %d rows per segment, %d CTAs per SM, %zu B shared, variant %d\n",
+                   seg, bps, gsot::eval_smem_bytes(seg, 0), var);
   }
   c->sync();
 }
@@ -511,10 +513,10 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
     if (mode == GSOT_EVAL_SCREENED)
       launch_eval(P, d_x, c->tasks, -1, &c->sc->ntasks, words, c->rowpart, c->colpart, c->psi,
-                  c->eval_buf, c->eval_recompute, c->eval_grid, &c->sc->next_task, c->stream);
+                  c->eval_buf, c->eval_variant, c->eval_grid, &c->sc->next_task, c->stream);
     else
       launch_eval(P, d_x, c->dense_tasks, c->L * c->nw, nullptr, words, c->rowpart, c->colpart,
-                  c->psi, c->eval_buf, c->eval_recompute, c->eval_grid, &c->sc->next_task,
+                  c->psi, c->eval_buf, c->eval_variant, c->eval_grid, &c->sc->next_task,
                   c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {

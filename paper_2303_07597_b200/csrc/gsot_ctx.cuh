@@ -109,6 +109,7 @@ struct gsot_ctx {
   int eval_grid = 148 * 4;
   int eval_buf = 96;  // rows per shared-memory segment in k_eval
   bool eval_recompute = false;  // k_eval<true>: some block is taller than a segment
+  int eval_variant = 0;         // gsot::eval_variant (0 / 1 recompute / 2 short tiles)
   int red_blocks = 148 * 2;
   // solver
   std::unique_ptr<gsot::SolverWorkspace> ws;
@@ -142,6 +143,7 @@ struct gsot_ctx {
     P.gamma = gamma;
     P.mu = mu;
     P.tau = mu * gamma;
+    P.half_inv_gamma = 0.5 / gamma;
     P.tl = tl;
     return P;
   }

@@ -55,6 +55,7 @@ struct DevProblem {
   const double* a;        // m
   const double* b;        // n
   double gamma, mu, tau;  // tau = mu * gamma (core.hpp:70)
+  double half_inv_gamma;  // 0.5 / gamma (fast-mode psi)
   unsigned long long* tl; // diagnostic timeline (GSOT_PHASE_CLOCKS builds only), else null
 };
 
@@ -151,12 +152,15 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
 // Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
 size_t eval_smem_bytes(int buf_rows, int cap);
-int eval_blocks_per_sm(size_t smem, bool recompute);
+// k_eval variant for a context: 0 in place / 4 consumer warps, 1 recomputing
+// (tiles taller than a segment), 2 in place / 2 consumer warps (short tiles)
+int eval_variant(int gmax, int seg, bool recompute);
+int eval_blocks_per_sm(size_t smem, int variant);
 // ntasks >= 0: `tasks` holds that many entries (dense list); -1: the
 // screened list, length *ntasks_dev (written by the screen kernel).
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int seg, bool recompute, int grid, int* next_task,
+                 double* psi, int seg, int variant, int grid, int* next_task,
                  cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,

@@ -684,8 +684,10 @@ struct EvalArgs {
   const int* ntasks_dev;
 };
 
-constexpr int kEvalWarps = 4;                        // consumer warps
-constexpr int kEvalThreads = 32 * (kEvalWarps + 1);  // + one producer warp
+// consumer warps per CTA: 4, or 2 for short tiles (at most kEvalShortRows rows:
+// fewer warps per tile, more tiles in flight per SM); + one producer warp
+__host__ __device__ constexpr int eval_threads(int nw) { return 32 * (nw + 1); }
+constexpr int kEvalShortRows = 64;
 constexpr int kEvalMaxSeg = 128;
 // alpha slot length in doubles: seg + 2 (aligned superset), even (16-byte slots)
 __host__ __device__ constexpr int aslot_len(int seg) { return (seg + 3) & ~1; }                     // rows per segment (4 warps x 32 rows)
@@ -695,8 +697,9 @@ struct EvalTask {
   uint32_t word;
 };
 
+template <int NW>
 __device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEvalWarps) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -707,8 +710,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // streamed twice needs no in-place rewrite either -- about half the shared
 // memory traffic per element of such tiles, for more registers (3 CTAs per
 // SM). Otherwise pass 1 writes [f]+ in place and pass 2 reads it (4 CTAs).
-template <bool kRecompute>
-__global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const EvalArgs A) {
+template <bool kRecompute, int kEvalWarps>
+__global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kEvalWarps == 4 ? 4 : 7))
+    k_eval(const EvalArgs A) {
   extern __shared__ __align__(128) unsigned char eval_smem[];
   const DevProblem& P = A.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -840,7 +844,7 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
       if (k == T.nseg - 1) {  // pass 1 complete: the warps in order (warp 0)
         zsh[warp][lane] = z2;
         ssh[warp][lane] = sv;
-        consumer_sync();
+        consumer_sync<kEvalWarps>();
         if (warp == 0) {
           double zz = zsh[0][lane], ss = ssh[0][lane];
 #pragma unroll
@@ -848,22 +852,27 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
             zz = dadd(zz, zsh[w][lane]);
             ss = dadd(ss, ssh[w][lane]);
           }
+          // scale = (1 - tau/z)/gamma as (z - tau)/(gamma z) and psi =
+          // (z - tau)^2/(2 gamma) with 1/(2 gamma) hoisted: one division per
+          // column on the tile's serial section
+          // (the recomputing variant, whose tiles are tall, keeps the
+          // two-division form: measured faster there)
           const double z = sqrt(zz);
           const bool nz = act && z > P.tau;
-          const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
+          const double d = dsub(z, P.tau);
+          const double scale = !nz ? 0.0
+                               : kRecompute ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma)
+                                            : ddiv(d, dmul(P.gamma, z));
           scale_sh[lane] = scale;
           if (act) {
             const int64_t idx = (int64_t)T.l * P.n + j;
             A.colpart[idx] = dmul(scale, ss);
-            double ps = 0.0;
-            if (nz) {
-              const double d = dsub(z, P.tau);
-              ps = ddiv(dmul(d, d), dmul(2.0, P.gamma));
-            }
-            A.psi[idx] = ps;
+            A.psi[idx] = !nz ? 0.0
+                         : kRecompute ? ddiv(dmul(d, d), dmul(2.0, P.gamma))
+                                      : dmul(dmul(d, d), P.half_inv_gamma);
           }
         }
-        consumer_sync();
+        consumer_sync<kEvalWarps>();
         // scales and betas of this lane's 16 rotated columns (the task's beta
         // slot is not reused before its last segment; columns >= n: 0)
         const double* bsl = bslots + (size_t)s0 * 34 + ((P.m + 32ll * T.c) & 1);
@@ -911,7 +920,7 @@ __global__ void __launch_bounds__(kEvalThreads, kRecompute ? 3 : 4) k_eval(const
 }
 
 namespace {
-int g_eval_smem_attr[2] = {0, 0};
+int g_eval_smem_attr[3] = {0, 0, 0};
 }
 
 // Rows per segment: the tallest group when it fits, else kEvalMaxSeg.
@@ -922,21 +931,30 @@ size_t eval_smem_bytes(int seg, int cap) {
   return sizeof(double) * 2 * ((size_t)seg * 32 + aslot_len(seg) + 34);
 }
 
-static void (*eval_kernel(bool recompute))(const EvalArgs) {
-  return recompute ? k_eval<true> : k_eval<false>;
+// variant: 0 in place (4 consumer warps), 1 recomputing (4), 2 in place (2)
+static void (*eval_kernel(int variant))(const EvalArgs) {
+  return variant == 1 ? k_eval<true, 4> : variant == 2 ? k_eval<false, 2> : k_eval<false, 4>;
+}
+static int eval_nthreads(int variant) { return eval_threads(variant == 2 ? 2 : 4); }
+
+int eval_variant(int gmax, int seg, bool recompute) {
+  if (recompute) return 1;
+  if (const char* ev = std::getenv("GSOT_EVAL_NW")) return std::atoi(ev) == 2 && gmax <= kEvalShortRows ? 2 : 0;
+  return gmax <= kEvalShortRows && seg >= gmax ? 2 : 0;
 }
 
-int eval_blocks_per_sm(size_t smem, bool recompute) {
-  auto kern = eval_kernel(recompute);
-  if ((int)smem > g_eval_smem_attr[recompute]) {
+int eval_blocks_per_sm(size_t smem, int variant) {
+  auto kern = eval_kernel(variant);
+  if ((int)smem > g_eval_smem_attr[variant]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // all of the unified L1 / shared array as shared memory: one more CTA
     // (one more tile in flight) per SM
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    g_eval_smem_attr[recompute] = (int)smem;
+    g_eval_smem_attr[variant] = (int)smem;
   }
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kEvalThreads, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, eval_nthreads(variant), smem) !=
+          cudaSuccess ||
       n < 1)
     n = 1;
   return n;
@@ -944,13 +962,13 @@ int eval_blocks_per_sm(size_t smem, bool recompute) {
 
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int seg, bool recompute, int grid, int* next_task, cudaStream_t s) {
+                 double* psi, int seg, int variant, int grid, int* next_task, cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0)
     throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
   EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev};
   const size_t smem = eval_smem_bytes(seg, 0);
-  if ((int)smem > g_eval_smem_attr[recompute]) eval_blocks_per_sm(smem, recompute);
-  launch_pdl(eval_kernel(recompute), dim3(grid), dim3(kEvalThreads), smem, s, A);
+  if ((int)smem > g_eval_smem_attr[variant]) eval_blocks_per_sm(smem, variant);
+  launch_pdl(eval_kernel(variant), dim3(grid), dim3(eval_nthreads(variant)), smem, s, A);
 }
 
 // ---------------------------------------------------------------- finalize
