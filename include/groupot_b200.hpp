@@ -13,19 +13,32 @@
 //   groupot::dual_gradient(s, inst, p, ga, gb) groupot::b200::Device::gradient(s, ga, gb)
 //   groupot::recover_plan(s, inst, p)          groupot::b200::Device::plan(s)
 //   ObjectiveFn / GradientFn closures          groupot::b200::Device::callbacks()
+//   plan_diagnostics(recover_plan(s), inst)    groupot::b200::Device::plan_diagnostics(s)
+//   groupot::run_grid(inst, grid, nc, pc, sink) groupot::b200::run_grid(...) (one warm
+//                                              device context for the whole grid;
+//                                              uses "groupot/bench.hpp" when on the path)
 //
 // Inputs are read straight from the Eigen storage (column-major cost, as
 // ProblemInstance holds it, solver.hpp:47-55); status codes are rethrown as
 // the reference's exception classes (errors.hpp) with their fields.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
 
 #include "gsot.h"
+#if __has_include("groupot/bench.hpp")
+#include "groupot/bench.hpp"  // BenchRecord, GridSpec (run_grid)
+#define GSOT_B200_HAVE_BENCH 1
+#else
+#define GSOT_B200_HAVE_BENCH 0
+#endif
 
 namespace groupot {
 namespace b200 {
@@ -94,6 +107,33 @@ class Device {
     check(gsot_plan_columns(ctx_, x_.data(), 0, n_, t.plan.data()));
     return t;
   }
+  // plan_diagnostics(recover_plan(s), inst) (dual.hpp:116-169) without the
+  // m x n plan: the all-zero block fraction exactly, residuals / mass from
+  // device row and column sums
+  PlanDiagnostics plan_diagnostics(const DualState& s) {
+    pack(s);
+    gsot_plan_diag d;
+    check(gsot_plan_diagnostics(ctx_, x_.data(), &d));
+    PlanDiagnostics r;
+    r.marginal_res_a = d.marginal_res_a;
+    r.marginal_res_b = d.marginal_res_b;
+    r.group_sparsity = d.group_sparsity;
+    r.mass = d.mass;
+    return r;
+  }
+  // build_active_set(take_snapshot(s, inst), s, p, groups).count
+  // (screening.hpp:24-50, :147-166): the active set at the snapshot point
+  long long active_set_size(const DualState& s) {
+    pack(s);
+    check(gsot_init_snapshot(ctx_, x_.data()));
+    check(gsot_refresh(ctx_, x_.data(), 1));
+    int64_t count = 0;
+    check(gsot_active_set(ctx_, nullptr, &count));
+    return static_cast<long long>(count);
+  }
+  // new RegParams on the resident instance (no re-upload, no re-validation of C)
+  void set_params(const RegParams& p) { check(gsot_set_params(ctx_, p.gamma(), p.mu())); }
+
   // ObjectiveFn / GradientFn for the reference's maximize (lbfgs.hpp:32-33):
   // one fused device evaluation serves both calls at the same x.
   std::pair<ObjectiveFn, GradientFn> callbacks() {
@@ -143,9 +183,20 @@ inline bool& exact_order() {
 
 namespace detail {
 
-inline Solution run(const ProblemInstance& inst, const RegParams& p, const SolverOptions& opts,
-                    int mode, double ub_offset, AuditReport* report) {
-  Device dev(inst, p);
+inline int mode_code(SolverMode mode) {
+  switch (mode) {
+    case SolverMode::baseline: return GSOT_MODE_BASELINE;
+    case SolverMode::fast: return GSOT_MODE_FAST;
+    case SolverMode::fast_no_lower_bound: return GSOT_MODE_FAST_NO_LOWER_BOUND;
+    case SolverMode::audit: return GSOT_MODE_AUDIT;
+  }
+  throw Error("unknown solver mode");
+}
+
+// One solve on a resident instance (solver.hpp:92-293 through gsot_solve);
+// with_plan: recover the m x n plan into Solution::plan (finish_solution).
+inline Solution run_on(Device& dev, const ProblemInstance& inst, const SolverOptions& opts,
+                       int mode, double ub_offset, AuditReport* report, bool with_plan) {
   gsot_solver_options o;
   gsot_default_solver_options(&o);
   o.snapshot_interval = opts.snapshot_interval;
@@ -167,7 +218,7 @@ inline Solution run(const ProblemInstance& inst, const RegParams& p, const Solve
   std::memcpy(sol.state.alpha.data(), x.data(), sizeof(double) * static_cast<size_t>(m));
   std::memcpy(sol.state.beta.data(), x.data() + m, sizeof(double) * static_cast<size_t>(n));
   sol.objective = r.objective;
-  sol.plan = dev.plan(sol.state);
+  if (with_plan) sol.plan = dev.plan(sol.state);
   sol.stats.blocks_in_active_set = r.blocks_in_active_set;
   sol.stats.blocks_skipped = r.blocks_skipped;
   sol.stats.blocks_unskipped = r.blocks_unskipped;
@@ -188,6 +239,12 @@ inline Solution run(const ProblemInstance& inst, const RegParams& p, const Solve
     report->gradient_calls = r.audit_gradient_calls;
   }
   return sol;
+}
+
+inline Solution run(const ProblemInstance& inst, const RegParams& p, const SolverOptions& opts,
+                    int mode, double ub_offset, AuditReport* report) {
+  Device dev(inst, p);
+  return run_on(dev, inst, opts, mode, ub_offset, report, true);
 }
 
 }  // namespace detail
@@ -225,6 +282,62 @@ inline Solution solve(const ProblemInstance& inst, const RegParams& p,
   }
   throw Error("unknown solver mode");
 }
+
+// run_grid (bench.hpp:137-180): the (gamma, rho, mode) grid in the reference's
+// deterministic order, on ONE device context: the cost is uploaded and
+// validated once, each (gamma, rho) only swaps the parameters. Records carry
+// the reference's fields (make_record, bench.hpp:99-126) with the plan
+// diagnostics computed on the device; active_set_size_final is the fresh
+// active-set build at the solution for non-baseline modes (bench.hpp:168-175).
+// The sink receives each Solution without its m x n plan unless with_plans.
+#if GSOT_B200_HAVE_BENCH
+inline std::vector<BenchRecord> run_grid(
+    const ProblemInstance& inst, const GridSpec& grid, int num_classes, int per_class,
+    const std::function<void(const BenchRecord&, const Solution&)>& sink = nullptr,
+    bool with_plans = false) {
+  std::vector<BenchRecord> rows;
+  std::unique_ptr<Device> dev;
+  for (const double gamma : grid.gammas) {
+    for (const double rho : grid.rhos) {
+      const RegParams p = params_from_rho(gamma, rho);  // core.hpp:148-151 (throws alike)
+      if (!dev)
+        dev = std::make_unique<Device>(inst, p);
+      else
+        dev->set_params(p);
+      for (const SolverMode mode : grid.modes) {
+        SolverOptions opts = grid.base;
+        opts.mode = mode;
+        Solution sol = detail::run_on(*dev, inst, opts, detail::mode_code(mode), 0.0, nullptr,
+                                      with_plans);
+        BenchRecord r;
+        r.mode = to_string(mode);
+        r.num_classes = num_classes;
+        r.per_class = per_class;
+        r.m = static_cast<long>(inst.m());
+        r.n = static_cast<long>(inst.n());
+        r.gamma = gamma;
+        r.rho = rho;
+        r.iterations = sol.iterations;
+        r.outer_loops = static_cast<long>(sol.stats.outer_loops);
+        r.wall_ms = std::chrono::duration<double, std::milli>(sol.wall_time).count();
+        r.objective = sol.objective;
+        r.blocks_computed = sol.stats.blocks_in_active_set + sol.stats.blocks_unskipped;
+        r.blocks_skipped = sol.stats.blocks_skipped;
+        r.upper_bounds_evaluated = sol.stats.upper_bounds_evaluated;
+        const PlanDiagnostics diag = dev->plan_diagnostics(sol.state);
+        r.group_sparsity = diag.group_sparsity;
+        r.marginal_res_a = diag.marginal_res_a;
+        r.marginal_res_b = diag.marginal_res_b;
+        r.converged = sol.converged;
+        if (mode != SolverMode::baseline) r.active_set_size_final = dev->active_set_size(sol.state);
+        if (sink) sink(r, sol);
+        rows.push_back(std::move(r));
+      }
+    }
+  }
+  return rows;
+}
+#endif
 
 }  // namespace b200
 }  // namespace groupot

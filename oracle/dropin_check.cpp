@@ -3,10 +3,12 @@
 // the same ProblemInstance. Built by oracle/Makefile into oracle/_ref/ (it
 // needs the reference headers, present in the build container only) and run
 // on the GPU box by tests/test_gpu_dropin.py. Prints one JSON object.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <exception>
 
+#include "groupot/bench.hpp"
 #include "groupot/data_io.hpp"
 #include "groupot/solver.hpp"
 #include "groupot_b200.hpp"
@@ -72,6 +74,54 @@ int main() {
                 std::abs(d.objective - r.objective) / std::abs(r.objective),
                 max_abs_diff(r.plan.plan, d.plan.plan), (long)r.stats.grad_calls,
                 (long)d.stats.grad_calls);
+  }
+  // run_grid (bench.hpp:137-180): the reference's grid driver vs the drop-in
+  // one on a warm device context, exact-order solves (bitwise trajectories):
+  // every integer field, the objective, the sparsity and the final active
+  // set equal; the residuals within 1e-12
+  {
+    GridSpec grid;
+    grid.gammas = {1.0, 0.1};
+    grid.rhos = {0.2, 0.8};
+    grid.modes = {SolverMode::baseline, SolverMode::fast, SolverMode::fast_no_lower_bound};
+    grid.base.max_outer_loops = 4;
+    grid.base.grad_tol = 1e-12;
+    int sink_calls = 0;
+    const auto ref_rows = groupot::run_grid(inst, grid, 4, 25);
+    b200::exact_order() = true;
+    const auto dev_rows = b200::run_grid(
+        inst, grid, 4, 25,
+        [&](const BenchRecord&, const Solution& sol) { sink_calls += sol.stats.grad_calls > 0; });
+    b200::exact_order() = false;
+    int ints_equal = ref_rows.size() == dev_rows.size(), obj_equal = 1, sparsity_equal = 1;
+    int csv_fields = 1;
+    double res_abs = 0.0;
+    for (size_t i = 0; i < std::min(ref_rows.size(), dev_rows.size()); ++i) {
+      const BenchRecord &r = ref_rows[i], &d = dev_rows[i];
+      ints_equal &= r.mode == d.mode && r.m == d.m && r.n == d.n && r.gamma == d.gamma &&
+                    r.rho == d.rho && r.iterations == d.iterations &&
+                    r.outer_loops == d.outer_loops && r.blocks_computed == d.blocks_computed &&
+                    r.blocks_skipped == d.blocks_skipped &&
+                    r.upper_bounds_evaluated == d.upper_bounds_evaluated &&
+                    r.active_set_size_final == d.active_set_size_final &&
+                    r.converged == d.converged;
+      obj_equal &= r.objective == d.objective;
+      sparsity_equal &= r.group_sparsity == d.group_sparsity;
+      res_abs = std::max(res_abs, std::max(std::abs(r.marginal_res_a - d.marginal_res_a),
+                                           std::abs(r.marginal_res_b - d.marginal_res_b)));
+      // the record's CSV row has the schema's 19 fields (bench.hpp:37-68). (The
+      // reference's parse_csv_row reads toks[i] and i++ in one call's arguments,
+      // bench.hpp:76, an unspecified order that GCC resolves past the last field:
+      // it is not used here.)
+      const std::string row = to_csv_row(d);
+      csv_fields &= std::count(row.begin(), row.end(), ',') == 18 &&
+                    row.compare(0, d.mode.size(), d.mode) == 0;
+    }
+    std::printf(", \"grid\": {\"rows\": [%zu, %zu], \"ints_equal\": %d, \"obj_equal\": %d, "
+                "\"sparsity_equal\": %d, \"res_abs\": %.3e, \"sink_calls\": %d, "
+                "\"csv_roundtrip\": %d}",
+                ref_rows.size(), dev_rows.size(), ints_equal, obj_equal, sparsity_equal, res_abs,
+                sink_calls, csv_fields);
   }
   // error behaviour: the same exception type and fields
   {

@@ -159,6 +159,15 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
         tl[56] += tl[2 * TL_EVAL + 1] - tl[2 * TL_EVAL];  // steady-state (sparse) evaluations
         tl[57] += 1;
         tl[58] += tl[2 * TL_PUBLISH + 1] - s0;  // and their sequence span
+        for (int k = 0; k < 4; ++k) {  // screen, eval, finalize, publish windows
+          tl[48 + 2 * k] += tl[2 * k] - s0;
+          tl[49 + 2 * k] += tl[2 * k + 1] - s0;
+        }
+        if (tl[2 * TL_STEP] != ~0ull) {
+          tl[59] += tl[2 * TL_STEP] - s0;
+          tl[60] += tl[2 * TL_STEP + 1] - s0;
+          tl[61] += 1;
+        }
       }
       for (int k = 0; k < 8; ++k)
         if (tl[2 * k] != ~0ull) {

@@ -698,6 +698,102 @@ def solve(inst: ProblemInstance, p: RegParams, opts: SolverOptions | None = None
     raise Error("unknown solver mode")
 
 
+# --------------------------------------------------------------- bench.hpp
+
+
+@dataclass
+class BenchRecord:
+    """One row of benchmark output; field order is the CSV schema (bench.hpp:15-35)."""
+    mode: str = ""
+    num_classes: int = 0
+    per_class: int = 0
+    m: int = 0
+    n: int = 0
+    gamma: float = 0.0
+    rho: float = 0.0
+    iterations: int = 0
+    outer_loops: int = 0
+    wall_ms: float = 0.0
+    objective: float = 0.0
+    blocks_computed: int = 0
+    blocks_skipped: int = 0
+    upper_bounds_evaluated: int = 0
+    active_set_size_final: int = 0
+    group_sparsity: float = 0.0
+    marginal_res_a: float = 0.0
+    marginal_res_b: float = 0.0
+    converged: bool = False
+
+
+def bench_csv_header() -> str:
+    """bench.hpp:37-42."""
+    return ("mode,num_classes,per_class,m,n,gamma,rho,iterations,outer_loops,"
+            "wall_ms,objective,blocks_computed,blocks_skipped,"
+            "upper_bounds_evaluated,active_set_size_final,group_sparsity,"
+            "marginal_res_a,marginal_res_b,converged")
+
+
+def _fmt(v: float) -> str:  # detail::format_double, data_io.hpp:185-189 ("%.17g")
+    return "%.17g" % v
+
+
+def to_csv_row(r: BenchRecord) -> str:
+    """bench.hpp:44-68."""
+    ints = lambda *v: [str(int(x)) for x in v]  # noqa: E731
+    return ",".join([r.mode] + ints(r.num_classes, r.per_class, r.m, r.n)
+                    + [_fmt(r.gamma), _fmt(r.rho)] + ints(r.iterations, r.outer_loops)
+                    + [_fmt(r.wall_ms), _fmt(r.objective)]
+                    + ints(r.blocks_computed, r.blocks_skipped, r.upper_bounds_evaluated,
+                           r.active_set_size_final)
+                    + [_fmt(r.group_sparsity), _fmt(r.marginal_res_a), _fmt(r.marginal_res_b)]
+                    + ints(1 if r.converged else 0))
+
+
+@dataclass
+class GridSpec:
+    """bench.hpp:130-136: four group-term balances by seven strengths, both modes."""
+    gammas: list = field(default_factory=lambda: [1e3, 1e2, 1e1, 1e0, 1e-1, 1e-2, 1e-3])
+    rhos: list = field(default_factory=lambda: [0.2, 0.4, 0.6, 0.8])
+    modes: list = field(default_factory=lambda: [SolverMode.baseline, SolverMode.fast])
+    base: SolverOptions = field(default_factory=SolverOptions)
+
+
+def run_grid(inst: ProblemInstance, grid: GridSpec, num_classes: int, per_class: int,
+             sink=None) -> list:
+    """run_grid (bench.hpp:137-180) in the reference's (gamma, rho, mode) order on the
+    instance's one device context (the cost is uploaded and validated once; each
+    (gamma, rho) only swaps the parameters). Plan diagnostics are computed on the
+    device (gsot_plan_diagnostics); active_set_size_final is the active set built at
+    the solution for non-baseline modes. sink(record, solution) fires after every run."""
+    rows = []
+    for gamma in grid.gammas:
+        for rho in grid.rhos:
+            p = params_from_rho(gamma, rho)
+            for mode in grid.modes:
+                opts = SolverOptions(grid.base.snapshot_interval, grid.base.grad_tol,
+                                     grid.base.max_outer_loops, grid.base.lbfgs_memory,
+                                     SolverMode(mode))
+                sol = solve(inst, p, opts)
+                ctx = inst.context(p)
+                x = _state_vec(sol.state, inst)
+                d = ctx.plan_diagnostics(x)
+                rec = BenchRecord(
+                    to_string(mode), num_classes, per_class, inst.m(), inst.n(), gamma, rho,
+                    sol.iterations, sol.stats.outer_loops,
+                    sol.wall_time.total_seconds() * 1e3, sol.objective,
+                    sol.stats.blocks_in_active_set + sol.stats.blocks_unskipped,
+                    sol.stats.blocks_skipped, sol.stats.upper_bounds_evaluated, 0,
+                    d.group_sparsity, d.marginal_res_a, d.marginal_res_b, sol.converged)
+                if mode != SolverMode.baseline:
+                    ctx.init_snapshot(x)
+                    ctx.refresh(x, True)
+                    rec.active_set_size_final = ctx.active_set()[1]
+                if sink is not None:
+                    sink(rec, sol)
+                rows.append(rec)
+    return rows
+
+
 # --------------------------------------------------------------- data inputs
 
 

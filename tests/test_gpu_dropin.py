@@ -29,5 +29,10 @@ def test_reference_api_through_the_adapter():
         assert m["obj_rel"] <= 1e-6
         if m["converged"][0]:
             assert m["plan_abs"] <= 1e-6
+    # run_grid (bench.hpp:137-180) on one warm device context, exact-order solves
+    g = d["grid"]
+    assert g["rows"] == [12, 12] and g["sink_calls"] == 12 and g["csv_roundtrip"] == 1
+    assert g["ints_equal"] == 1 and g["obj_equal"] == 1 and g["sparsity_equal"] == 1
+    assert g["res_abs"] <= 1e-12
     assert d["negative_cost_fields"] == 1 and d["marginal_fields"] == 1
     assert d["audit_violation"] == 1

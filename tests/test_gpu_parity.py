@@ -336,6 +336,45 @@ def test_python_mirror_api(o):
     assert 0.0 <= d.group_sparsity <= 1.0 and d.mass > 0
 
 
+def test_python_run_grid(o, gold):
+    """run_grid (bench.hpp:137-180) through the Python mirror on the reference's
+    own synthetic instance: the reference's (gamma, rho, mode) order, one
+    record per run, each record equal to the solve and the device diagnostics
+    it summarises, the CSV schema of bench.hpp:37-68; objectives near the
+    oracle's solves (fast mode re-associates sums: 1e-6 relative)."""
+    p = gold_problem(gold, "synth", 0)
+    inst = G.ProblemInstance(p.cost, p.a, p.b, G.GroupPartition(p.sizes))
+    grid = G.GridSpec(gammas=[1.0, 0.1], rhos=[0.2, 0.8],
+                      modes=[G.SolverMode.baseline, G.SolverMode.fast],
+                      base=G.SolverOptions(max_outer_loops=4, grad_tol=1e-12))
+    seen = []
+    rows = G.run_grid(inst, grid, 5, 20, sink=lambda r, sol: seen.append((r, sol)))
+    assert [(r.gamma, r.rho, r.mode) for r in rows] == [
+        (g, r, m) for g in (1.0, 0.1) for r in (0.2, 0.8) for m in ("baseline", "fast")]
+    assert len(seen) == len(rows) and all(a is r for (a, _), r in zip(seen, rows))
+    assert G.bench_csv_header().count(",") == 18
+    for rec, sol in seen:
+        assert len(G.to_csv_row(rec).split(",")) == 19
+        prm = G.params_from_rho(rec.gamma, rec.rho)
+        q = Problem(p.cost, p.sizes, p.a, p.b, prm.gamma(), prm.mu())
+        mode = 0 if rec.mode == "baseline" else 1
+        ro = o.solve(q, mode=mode, max_outer_loops=4, grad_tol=1e-12)
+        assert abs(rec.objective - ro["objective"]) <= 1e-6 * abs(ro["objective"])
+        assert rec.iterations == sol.iterations and rec.objective == sol.objective
+        assert rec.blocks_computed == sol.stats.blocks_in_active_set + sol.stats.blocks_unskipped
+        d = G.state_plan_diagnostics(sol.state, inst, prm)
+        assert (rec.group_sparsity, rec.marginal_res_a, rec.marginal_res_b) == \
+            (d.group_sparsity, d.marginal_res_a, d.marginal_res_b)
+        ref = o.plan_diagnostics(q, o.plan(q, sol.state.alpha, sol.state.beta))
+        assert rec.group_sparsity == ref[2]
+        if rec.mode == "baseline":
+            assert rec.active_set_size_final == 0
+        else:
+            mem, cnt = o.active_set(q, sol.state.alpha, sol.state.beta, sol.state.alpha,
+                                    sol.state.beta)
+            assert rec.active_set_size_final == cnt
+
+
 # ------------------------------------------------------------ configs
 
 

@@ -35,4 +35,13 @@ ns = buf[57] - base[57]
 if ns:
     print(f'  sparse evals (< 40 us): n={ns}  eval window {(buf[56] - base[56]) / ns / 1e3:.2f} us  '
           f'sequence span {(buf[58] - base[58]) / ns / 1e3:.2f} us')
+    for k, nm in enumerate(names[:4]):
+        s = (buf[48 + 2 * k] - base[48 + 2 * k]) / ns / 1e3
+        e = (buf[49 + 2 * k] - base[49 + 2 * k]) / ns / 1e3
+        print(f'    sparse {nm:9s} start {s:7.2f} us  end {e:7.2f} us  window {e - s:6.2f} us')
+    nst = buf[61] - base[61]
+    if nst:
+        s = (buf[59] - base[59]) / nst / 1e3
+        e = (buf[60] - base[60]) / nst / 1e3
+        print(f'    sparse step      start {s:7.2f} us  end {e:7.2f} us  window {e - s:6.2f} us (n={nst})')
 PY
