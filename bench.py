@@ -62,58 +62,100 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    (pynvml, every 5 ms, from a thread; device-wide counters, no CUDA
+    interaction), else nvidia-smi every 100 ms. begin()/end() bracket the
+    timed region; only samples taken between them are reported."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.nvml = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons set)
+        self.on = False
+        self.stop_ev = threading.Event()
 
     def start(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            self.nvml = (N, h, mx, bits)
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll_nvml(self):
+        N, h, mx, bits = self.nvml
+        while not self.stop_ev.is_set():
+            if self.on:
+                try:
+                    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(sm), float(mx),
+                                         {nm for nm, b in bits.items() if r & b}))
+                except Exception:
+                    pass
+            time.sleep(0.005)
 
-    def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
+    def _read_smi(self):
+        for ln in self.proc.stdout:
+            if not self.on:
+                continue
+            parts = [p.strip() for p in ln.strip().split(",")]
             if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                sm, mx = float(parts[0]), float(parts[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+            self.samples.append((sm, mx, {nm for nm, v in zip(self.NAMES, parts[3:7])
+                                          if v.lower() == "active"}))
+
+    def begin(self):
+        self.on = True
+
+    def end(self):
+        self.on = False
+
+    def stop(self):
+        self.on = False
+        self.stop_ev.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [x[0] for x in self.samples]
+        reasons = set().union(*[x[2] for x in self.samples])
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_init():
@@ -300,6 +342,7 @@ def run_ours(args, world, rank, local, pg):
     clocks = ClockSampler(local)
     clocks.start()
     barrier(pg)
+    clocks.begin()
     ctx.timer_start()
     calls, iters_done, solve_ms = 0, 0, []
     blocks, tasks = 0, 0
@@ -312,6 +355,7 @@ def run_ours(args, world, rank, local, pg):
         blocks += r["eval_blocks"]
         tasks += r["eval_tasks"]
     ms = ctx.timer_stop()
+    clocks.end()
     barrier(pg)
     clk = clocks.stop()
     launches = ctx.kernel_launches() - launches0
@@ -344,12 +388,28 @@ def run_ours(args, world, rank, local, pg):
     d = cand[dom]
     achieved = (d["bytes"] / d["launches"]) / (d["ms"] / d["launches"] / 1e3) / 1e9
     traffic = ncu_traffic(dom)
+    # the same launches split by regime: near-dense evaluations (at least half
+    # the dense bytes; bandwidth-bound) and the screened rest (latency-bound)
+    regimes = None
+    if dom == "k_eval":
+        nms, nbytes, nn = ctx.profile_read(8)
+        tot = kinds["k_eval"]
+        regimes = {}
+        for name, (rms, rbytes, rn) in (("near_dense", (nms, nbytes, nn)),
+                                         ("screened", (tot["ms"] - nms, tot["bytes"] - nbytes,
+                                                       tot["launches"] - nn))):
+            if rn > 0 and rms > 0:
+                a = rbytes / (rms / 1e3) / 1e9
+                regimes[name] = {"launches": rn, "bytes_per_launch": rbytes / rn,
+                                 "us_per_launch": 1e3 * rms / rn, "achieved": a,
+                                 "frac": a / peak, "share_of_eval_time": rms / tot["ms"]}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
                 "traffic": traffic,
                 "bytes_per_launch": d["bytes"] / d["launches"],
                 "ms_per_launch": d["ms"] / d["launches"],
                 "share_of_step": d["ms"] / ms_prof,
+                "regimes": regimes,
                 "measured": "CUDA events around every launch of the kernel on the solver stream, "
                             "over a second pass of the same K solves (the value pass runs "
                             "uninstrumented)"}

@@ -261,8 +261,10 @@ GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double
 /* Per-kernel-class device time (CUDA events on the context stream, event
  * nodes inside the solver's graphs) and algorithmic bytes since the last
  * reset. kind: 0 eval(fused blocks), 1 snapshot, 2 bounds, 3 active set,
- * 4 finalize, 5 lbfgs vector ops, 6 delta norms, 7 misc. enable: 0 off,
- * negative every class, positive a bit mask (1 << kind) of the classes. */
+ * 4 finalize, 5 lbfgs vector ops, 6 delta norms, 7 misc; read-only kind 8:
+ * the eval launches that read at least half the dense bytes (near-dense).
+ * enable: 0 off, negative every class, positive a bit mask (1 << kind) of
+ * the classes 0-7. */
 GSOT_API int gsot_profile_enable(gsot_ctx* ctx, int enable);
 GSOT_API int gsot_profile_read(gsot_ctx* ctx, int kind, double* ms, double* bytes,
                                int64_t* launches);

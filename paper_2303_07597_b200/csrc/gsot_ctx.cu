@@ -997,7 +997,7 @@ GSOT_API int gsot_profile_read(gsot_ctx* ctx, int kind, double* ms, double* byte
                                int64_t* launches) {
   return guard([&] {
     checked(ctx);
-    if (kind < 0 || kind >= gsot::K_NKINDS) throw Error(GSOT_ERR_INVALID_ARGUMENT, "bad kind");
+    if (kind < 0 || kind >= gsot::K_NSTATS) throw Error(GSOT_ERR_INVALID_ARGUMENT, "bad kind");
     ctx->collect_marks();
     if (ms) *ms = ctx->prof_ms[kind];
     if (bytes) *bytes = ctx->prof_bytes[kind];
@@ -1009,7 +1009,7 @@ GSOT_API int gsot_profile_reset(gsot_ctx* ctx) {
   return guard([&] {
     checked(ctx);
     ctx->collect_marks();
-    for (int k = 0; k < gsot::K_NKINDS; ++k) {
+    for (int k = 0; k < gsot::K_NSTATS; ++k) {
       ctx->prof_ms[k] = 0;
       ctx->prof_bytes[k] = 0;
       ctx->prof_launches[k] = 0;

@@ -120,9 +120,9 @@ struct gsot_ctx {
   unsigned profile_mask = 0;  // kinds bracketed with events (bit per KernelKind)
   std::vector<gsot::Mark> marks;
   std::vector<cudaEvent_t> event_pool;
-  double prof_ms[gsot::K_NKINDS] = {};
-  double prof_bytes[gsot::K_NKINDS] = {};
-  int64_t prof_launches[gsot::K_NKINDS] = {};
+  double prof_ms[gsot::K_NSTATS] = {};
+  double prof_bytes[gsot::K_NSTATS] = {};
+  int64_t prof_launches[gsot::K_NSTATS] = {};
   int64_t launches = 0;
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
   // stream capture in progress: marks/kernels go to the sequence
@@ -208,9 +208,15 @@ struct gsot_ctx {
   void account(const gsot::Mark& mk) {
     float ms = 0.f;
     GSOT_CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
+    const double bytes = mk.bytes < 0 ? screened_eval_bytes() : mk.bytes;
     prof_ms[mk.kind] += ms;
-    prof_bytes[mk.kind] += mk.bytes < 0 ? screened_eval_bytes() : mk.bytes;
+    prof_bytes[mk.kind] += bytes;
     prof_launches[mk.kind] += 1;
+    if (mk.kind == gsot::K_EVAL && bytes >= 4.0 * static_cast<double>(m) * static_cast<double>(n)) {
+      prof_ms[gsot::K_EVAL_NEAR_DENSE] += ms;
+      prof_bytes[gsot::K_EVAL_NEAR_DENSE] += bytes;
+      prof_launches[gsot::K_EVAL_NEAR_DENSE] += 1;
+    }
   }
 
   // After a synchronisation: fold eager marks into the counters.

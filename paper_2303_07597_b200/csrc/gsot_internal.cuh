@@ -123,7 +123,11 @@ enum KernelKind {
   K_LBFGS = 5,
   K_DELTA = 6,
   K_MISC = 7,
-  K_NKINDS = 8
+  K_NKINDS = 8,
+  // statistics only (not a launch kind): the K_EVAL launches that read at
+  // least half the dense bytes (near-dense evaluations, bandwidth-bound)
+  K_EVAL_NEAR_DENSE = 8,
+  K_NSTATS = 9
 };
 
 void launch_relayout(const DevProblem& P, const double* src_colmajor, int64_t j0, int64_t ncols,

@@ -562,17 +562,20 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
           if (lane == i) wl = wi;
           if (lane < i) tv = dsub(tv, dmul(R[lane * KS + i], wi));
         }
+        PHASE_MARK(6);
         double z = act ? dsub(dmul(rii, wl), dmul(gam, vv[lane])) : 0.0;
         for (int j = 0; j < kn; ++j) {
           const double wj = __shfl_sync(0xffffffffu, wl, j);
           if (act) z = dadd(z, dmul(dmul(gam, YY[lane * KS + j]), wj));
         }
+        PHASE_MARK(8);
         double pl = 0.0;
         for (int j = 0; j < kn; ++j) {
           const double pj = __shfl_sync(0xffffffffu, dmul(z, rinv), j);
           if (lane == j) pl = pj;
           if (act && lane > j) z = dsub(z, dmul(R[j * KS + lane], pj));
         }
+        PHASE_MARK(9);
         if (act) {
           lc[lane] = pl;
           lc[kMaxMemory + lane] = dmul(gam, wl);

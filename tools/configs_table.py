@@ -9,7 +9,7 @@ import sys
 src, dst = sys.argv[1], sys.argv[2]
 d = json.load(open(src))
 shutil.copy(src, dst + ".json")
-L = ["# L-BFGS solve times, all five configs (round 1)", "",
+L = ["# L-BFGS solve times, all five configs", "",
      "Command: `python tools/solve_configs.py --e2e --reps 2` on one B200 (gpurun). Synthetic",
      "instances per SURVEY.md §8(d) (seed = config id), cost generated on device; snapshot",
      "interval 10, memory 10, grad_tol 1e-12 (runs to the iteration budget). `solve ms` is the",
