@@ -91,6 +91,10 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
 #ifdef GSOT_PHASE_CLOCKS
   long long clk_prev = clock64();
 #endif
+  // the completion counter is written only by earlier publishes, which
+  // completed before this sequence was launched: read it before the wait
+  unsigned long long count0 = 0;
+  if (threadIdx.x == 0) count0 = *dev_count;
   pdl_wait();
   TL_ENTER(tl, TL_PUBLISH);
   EvalScalars* sc = &src->sc;
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
     sc->ticket = 0u;
     sc->audit_violation = 0;
     sc->audit_where = 0;
-    const unsigned long long c = *dev_count + 1;
+    const unsigned long long c = count0 + 1;
     *dev_count = c;
     __threadfence_system();
     PHASE_MARK(13);
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
   const int k = A.h->k;  // read by every CTA before CTA 0 rewrites the ring
   const int scratch = A.h->scratch;
   // the step: one read per CTA, issued now, stored after phase 1
-  __shared__ double t_sh;
+  __shared__ double t_sh, gam_sh;
   double t_reg = 0.0;
   if (threadIdx.x == 32 && A.xt) t_reg = *A.t;
   // every CTA stages the ring state and R / YY (logical positions) now: the
@@ -459,6 +463,20 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
     grid_fold(A.part + 2 * kStepMaxGrid, nc, ld, nrows * 5, red);
     __syncthreads();
     PHASE_MARK(2);
+    if (threadIdx.x == 32) {  // gam (lbfgs.hpp:116-119) of the newest pair, beside the ring update
+      bool fresh = false;
+      double sy = 0.0, yy = 0.0;
+      if (A.pair) {
+        sy = red[k * 5 + 0];
+        yy = red[k * 5 + 2];
+        fresh = sy > 1e-10 * sqrt(red[k * 5 + 1]) * sqrt(yy);  // the acceptance test below
+      }
+      if (!fresh) {  // no new pair: thread 0 leaves the ring's sy / yy untouched
+        sy = k > 0 ? hs.sy[k - 1] : 0.0;
+        yy = k > 0 ? hs.yy[k - 1] : 0.0;
+      }
+      gam_sh = (fresh || k > 0) && yy > 0.0 ? sy / yy : 1.0;
+    }
     if (threadIdx.x == 0) {
       int accept = 0, first = 0, kk = k;
       if (A.pair) {
@@ -549,12 +567,11 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
       // gam (lbfgs.hpp:116-119); w = R^-1 u, z = (D + gam YY) w - gam v,
       // p = R^-T z. Lane i owns row i; substitutions are column oriented
       // (one broadcast per step), diagonal reciprocals computed up front.
-      double gam = 1.0;
-      if (kn > 0 && hs.yy[kn - 1] > 0.0) gam = hs.sy[kn - 1] / hs.yy[kn - 1];
+      const double gam = gam_sh;
       if (kn <= 32) {
         const bool act = lane < kn;
         const double rii = act ? R[lane * KS + lane] : 1.0;
-        const double rinv = 1.0 / rii;
+        const double rinv = act ? hs.rho[lane] : 1.0;  // 1 / s_i.y_i, kept with the ring
         double tv = act ? uu[lane] : 0.0;
         double wl = 0.0;
         for (int i = kn - 1; i >= 0; --i) {
