@@ -108,6 +108,16 @@ GSOT_API int gsot_create_device(const double* d_cost, int64_t m, int64_t n,
  * process-wide cache; a later create of the same shape and partition on the
  * same device reuses it and only uploads the new data. GSOT_CTX_CACHE=0 in the
  * environment frees immediately instead. */
+/* A column shard of a larger instance (multi-GPU column sharding, DESIGN.md
+ * §8): cost is the m x n_shard column block (column-major), b_shard the
+ * shard's entries of b, a the row marginal or zeros. Validated like
+ * gsot_create except that the marginals are checked entrywise only (their
+ * sums are the full instance's). With a = 0, gsot_eval's grad[0, m) is minus
+ * the shard's plan row sums and its objective b_shard.beta_shard - psi_shard:
+ * the terms a sharded driver all-reduces. */
+GSOT_API int gsot_create_shard(const double* cost, int64_t m, int64_t n_shard,
+                               const int32_t* group_sizes, int32_t L, const double* a,
+                               const double* b_shard, double gamma, double mu, gsot_ctx** out);
 GSOT_API void gsot_destroy(gsot_ctx* ctx);
 /* Replace (gamma, mu) keeping the resident cost (RegParams ctor checks). */
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu);

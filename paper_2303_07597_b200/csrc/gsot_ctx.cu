@@ -79,7 +79,9 @@ double compensated_sum(const double* v, int64_t n) {  // core.hpp:85-98
   return sum + comp;
 }
 
-void check_marginal(const double* v, int64_t n, char which) {  // core.hpp:100-112
+// shard: a column shard's partial marginals (gsot_create_shard) are checked
+// entrywise only; the sum is the driver's (the full instance's) business.
+void check_marginal(const double* v, int64_t n, char which, bool shard = false) {  // core.hpp:100-112
   for (int64_t i = 0; i < n; ++i) {
     if (!(v[i] >= 0.0) || !std::isfinite(v[i])) {
       Error e(GSOT_ERR_MARGINAL_NOT_NORMALIZED,
@@ -90,6 +92,7 @@ void check_marginal(const double* v, int64_t n, char which) {  // core.hpp:100-1
       throw e;
     }
   }
+  if (shard) return;
   const double sum = compensated_sum(v, n);
   if (std::abs(sum - 1.0) > 1e-12) {
     Error e(GSOT_ERR_MARGINAL_NOT_NORMALIZED,
@@ -297,7 +300,7 @@ void set_marginals(gsot_ctx* c, const double* a, const double* b) {
 // validate_instance (core.hpp:117-139) order: cost scan (first offender in
 // j-major order, computed on device during the upload), a, b, partition.
 void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const double* a,
-                       const double* b, const double* d_src_for_value) {
+                       const double* b, const double* d_src_for_value, bool shard = false) {
   unsigned long long first_bad = 0;
   GSOT_CUDA_CHECK(cudaMemcpyAsync(&first_bad, d_first_bad, sizeof(first_bad),
                                   cudaMemcpyDeviceToHost, c->stream));
@@ -320,8 +323,8 @@ void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const doubl
     e.detail.value = value;
     throw e;
   }
-  check_marginal(a, c->m, 'a');
-  check_marginal(b, c->n, 'b');
+  check_marginal(a, c->m, 'a', shard);
+  check_marginal(b, c->n, 'b', shard);
   if (c->off[c->L] != c->m)
     throw Error(GSOT_ERR_PARTITION_MISMATCH,
                 "group partition: partition covers " + std::to_string(c->off[c->L]) +
@@ -383,7 +386,7 @@ void park_or_delete(gsot_ctx* c) {
 
 gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int64_t n,
                         const int32_t* sizes, int32_t L, const double* a, const double* b,
-                        double gamma, double mu) {
+                        double gamma, double mu, bool shard = false) {
   gsot_ctx* c = (sizes && L > 0 && m > 0 && n > 0) ? cache_take(m, n, sizes, L) : nullptr;
   const bool reused = c != nullptr;
   if (!c) c = new gsot_ctx();
@@ -423,8 +426,8 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
             }
           }
       }
-      check_marginal(a, m, 'a');
-      check_marginal(b, n, 'b');
+      check_marginal(a, m, 'a', shard);
+      check_marginal(b, n, 'b', shard);
       throw Error(GSOT_ERR_PARTITION_MISMATCH,
                   "group partition: partition covers " + std::to_string(c->off[L]) +
                       " indices, cost has " + std::to_string(m) + " rows");
@@ -458,7 +461,7 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
         gsot::launch_relayout(c->problem(), src, j0, nc, c->C, d_bad, c->stream);
       });
     }
-    finish_validation(c, d_bad, a, b, nullptr);
+    finish_validation(c, d_bad, a, b, nullptr, shard);
     c->cacheable = true;
     return c;
   } catch (...) {
@@ -658,6 +661,16 @@ GSOT_API int gsot_create_device(const double* d_cost, int64_t m, int64_t n,
     if (!out || !d_cost || !a || !b) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
     *out = create_common(d_cost, true, m, n, group_sizes, L, a, b, gamma, mu);
+  });
+}
+
+GSOT_API int gsot_create_shard(const double* cost, int64_t m, int64_t n_shard,
+                               const int32_t* group_sizes, int32_t L, const double* a,
+                               const double* b_shard, double gamma, double mu, gsot_ctx** out) {
+  return guard([&] {
+    if (!out || !cost || !a || !b_shard) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    *out = create_common(cost, false, m, n_shard, group_sizes, L, a, b_shard, gamma, mu, true);
   });
 }
 

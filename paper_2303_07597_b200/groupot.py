@@ -296,6 +296,20 @@ class Context:
         return cls(h.value)
 
     @classmethod
+    def shard_from_arrays(cls, cost_block, sizes, a, b_block, gamma: float,
+                          mu: float) -> "Context":
+        """A column shard (gsot_create_shard): marginals checked entrywise only."""
+        cost = np.asfortranarray(cost_block, dtype=np.float64)
+        m, n = cost.shape
+        sizes = np.ascontiguousarray(sizes, dtype=np.int32)
+        a, b = _f64(a), _f64(b_block)
+        h = C.c_void_p()
+        st = _lib.lib().gsot_create_shard(_ptr(cost), m, n, _ptr(sizes), len(sizes), _ptr(a),
+                                          _ptr(b), float(gamma), float(mu), C.byref(h))
+        _raise(st)
+        return cls(h.value)
+
+    @classmethod
     def from_config(cls, cfg: int, seed: int, gamma: float, mu: float) -> "Context":
         h = C.c_void_p()
         _raise(_lib.lib().gsot_create_config(int(cfg), int(seed), float(gamma), float(mu),
