@@ -118,6 +118,11 @@ GSOT_API int gsot_create_device(const double* d_cost, int64_t m, int64_t n,
 GSOT_API int gsot_create_shard(const double* cost, int64_t m, int64_t n_shard,
                                const int32_t* group_sizes, int32_t L, const double* a,
                                const double* b_shard, double gamma, double mu, gsot_ctx** out);
+/* The same with the column block already in device memory (column-major). */
+GSOT_API int gsot_create_shard_device(const double* d_cost, int64_t m, int64_t n_shard,
+                                      const int32_t* group_sizes, int32_t L, const double* a,
+                                      const double* b_shard, double gamma, double mu,
+                                      gsot_ctx** out);
 GSOT_API void gsot_destroy(gsot_ctx* ctx);
 /* Replace (gamma, mu) keeping the resident cost (RegParams ctor checks). */
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu);

@@ -674,6 +674,17 @@ GSOT_API int gsot_create_shard(const double* cost, int64_t m, int64_t n_shard,
   });
 }
 
+GSOT_API int gsot_create_shard_device(const double* d_cost, int64_t m, int64_t n_shard,
+                                      const int32_t* group_sizes, int32_t L, const double* a,
+                                      const double* b_shard, double gamma, double mu,
+                                      gsot_ctx** out) {
+  return guard([&] {
+    if (!out || !d_cost || !a || !b_shard) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    *out = create_common(d_cost, true, m, n_shard, group_sizes, L, a, b_shard, gamma, mu, true);
+  });
+}
+
 GSOT_API void gsot_destroy(gsot_ctx* ctx) { park_or_delete(ctx); }
 
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu) {

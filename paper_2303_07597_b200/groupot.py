@@ -310,6 +310,20 @@ class Context:
         return cls(h.value)
 
     @classmethod
+    def shard_from_device(cls, d_cost_ptr: int, m: int, n_shard: int, sizes, a, b_block,
+                          gamma: float, mu: float) -> "Context":
+        """gsot_create_shard_device: the m x n_shard column block (column-major) at
+        device address d_cost_ptr."""
+        sizes = np.ascontiguousarray(sizes, dtype=np.int32)
+        a, b = _f64(a), _f64(b_block)
+        h = C.c_void_p()
+        st = _lib.lib().gsot_create_shard_device(C.c_void_p(d_cost_ptr), int(m), int(n_shard),
+                                                 _ptr(sizes), len(sizes), _ptr(a), _ptr(b),
+                                                 float(gamma), float(mu), C.byref(h))
+        _raise(st)
+        return cls(h.value)
+
+    @classmethod
     def from_config(cls, cfg: int, seed: int, gamma: float, mu: float) -> "Context":
         h = C.c_void_p()
         _raise(_lib.lib().gsot_create_config(int(cfg), int(seed), float(gamma), float(mu),

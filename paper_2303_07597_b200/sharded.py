@@ -80,14 +80,14 @@ class ShardedProblem:
     evaluator(x_local, screened) -> (objective_p, grad_local, counters4)."""
 
     def __init__(self, cost_block, sizes, a, b_block, gamma: float, mu: float, comm: Comm,
-                 evaluator=None):
+                 evaluator=None, ctx=None):
         self.a = np.ascontiguousarray(a, np.float64)
         self.m = self.a.size
         self.n_p = int(np.asarray(b_block).size)
         self.comm = comm
         self.evaluator = evaluator
-        self.ctx = None
-        if evaluator is None:
+        self.ctx = ctx  # a prebuilt shard context (Context.shard_from_device)
+        if evaluator is None and ctx is None:
             self.ctx = G.Context.shard_from_arrays(cost_block, sizes, np.zeros(self.m), b_block,
                                                    gamma, mu)
 
