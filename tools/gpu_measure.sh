@@ -2,7 +2,7 @@
 # Round measurement on one GPU box: tests, bench (both arms), ncu launch list
 # + --set full captures (bench workload), dense-eval captures, all five
 # configs.   bash tools/gpu_measure.sh TAG
-TAG=${1:-r2}
+TAG=${1:-r1h}
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_$TAG.log 2>&1; echo pytest $?
 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke_$TAG.log 2>&1; echo smoke $?
