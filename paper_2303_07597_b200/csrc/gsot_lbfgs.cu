@@ -101,9 +101,44 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fin = sc->fin_blocks, step = sc->step_blocks, cnt = sc->cnt_pending;
   __shared__ double f[6];
-  if (fin > 0 && warp < 4) {  // a.alpha, b.beta, psi, g.d (dual.hpp:51)
-    const double v = warp_fold(fin_partials + warp, fin, 4);
-    if (lane == 0) f[warp] = v;
+  __shared__ double fw[8][4];
+  if (fin > 0) {  // a.alpha, b.beta, psi, g.d (dual.hpp:51): every thread folds a
+    // contiguous run of unit partials (all loads in flight), then a fixed xor
+    // tree per warp and the warps in order
+    const int run = (fin + 255) / 256;
+    const int i0 = min(fin, (int)threadIdx.x * run), i1 = min(fin, i0 + run);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int ib = i0; ib < i1; ib += 8) {
+      double2 q[8][2];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2 z{0.0, 0.0};
+        const double2* pp = reinterpret_cast<const double2*>(fin_partials + 4ll * (ib + u));
+        q[u][0] = ib + u < i1 ? __ldcg(pp) : z;
+        q[u][1] = ib + u < i1 ? __ldcg(pp + 1) : z;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (ib + u < i1) {
+          a0 = dadd(a0, q[u][0].x);
+          a1 = dadd(a1, q[u][0].y);
+          a2 = dadd(a2, q[u][1].x);
+          a3 = dadd(a3, q[u][1].y);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      a0 = dadd(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+      a1 = dadd(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+      a2 = dadd(a2, __shfl_xor_sync(0xffffffffu, a2, o));
+      a3 = dadd(a3, __shfl_xor_sync(0xffffffffu, a3, o));
+    }
+    if (lane == 0) {
+      fw[warp][0] = a0;
+      fw[warp][1] = a1;
+      fw[warp][2] = a2;
+      fw[warp][3] = a3;
+    }
   }
   if (step > 0 && (warp == 4 || warp == 5)) {  // g.d, d.d of the new direction
     const double v = warp_fold(step_partials + (warp - 4), step, 2);
@@ -114,6 +149,12 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
   PHASE_MARK(11);
   if (threadIdx.x == 0) {
     if (fin > 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double v = fw[0][q];
+        for (int w = 1; w < 8; ++w) v = dadd(v, fw[w][q]);
+        f[q] = v;
+      }
       sc->dot_aa = f[0];
       sc->dot_bb = f[1];
       sc->psi_sum = f[2];
