@@ -489,8 +489,9 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
       dbt[ci][k] = v;
     }
     // this warp's group: z~ of the 32 chunks' columns cb..cb+15, two chunks
-    // per coalesced load (half-warp = 16 consecutive columns)
-#pragma unroll 4
+    // per coalesced load (half-warp = 16 consecutive columns), all 16 loads
+    // in flight together
+#pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int ci = 2 * q + (lane >> 4), k = lane & 15;
       const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
