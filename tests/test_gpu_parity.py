@@ -450,6 +450,40 @@ def test_config2_full_size_properties(o):
     ctx.close()
 
 
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_full_size_properties_configs_3_to_5(cfg):
+    """BASELINE configs 3-5 at full size (8 / 9.6 / 40 GB of cost), through
+    size-independent properties: screened == dense bitwise and repeatable,
+    the GradStats identity, sum(grad_alpha) = 1 - mass = sum(grad_beta), the
+    device plan diagnostics' mass and nonzero-block count consistent with the
+    gradient and the block mask, and the exact-order (reference-order)
+    evaluation within 1e-9 of the fast one."""
+    gamma, mu = {3: (0.1, 0.2), 4: (0.05, 0.3), 5: (0.1, 0.5)}[cfg]
+    ctx = G.Context.from_config(cfg, cfg, gamma, mu)
+    m, n, L = ctx.m, ctx.n, ctx.L
+    r = ctx.solve(mode=1, max_outer_loops=1, grad_tol=1e-12)
+    x = r["x"]
+    obj, g, st_d = ctx.eval(x)
+    assert st_d.unskipped == L * n
+    obj2, g2, _ = ctx.eval(x)
+    assert obj2 == obj and np.array_equal(g2, g)
+    ctx.init_snapshot(x * 0.999)
+    ctx.refresh(x, True)  # active set from the 0.999 x snapshot, new snapshot at x
+    obj_s, g_s, st = ctx.eval(x, screened=True)
+    assert obj_s == obj and np.array_equal(g_s, g)
+    assert st.in_active + st.skipped + st.unskipped == L * n and st.skipped > 0
+    sa, sb = g[:m].sum(), g[m:].sum()
+    assert abs(sa - sb) <= 1e-12
+    d = ctx.plan_diagnostics(x)
+    assert abs(d.mass - (1.0 - sa)) <= 1e-10
+    nz = int(ctx.block_mask(x).sum())
+    assert nz == round((1.0 - d.group_sparsity) * L * n)
+    obj_x, g_x, _ = ctx.eval(x, exact=True)
+    assert abs(obj_x - obj) <= 1e-9 * abs(obj)
+    assert np.max(np.abs(g_x - g)) <= 1e-9 * max(1.0, float(np.max(np.abs(g))))
+    ctx.close()
+
+
 def test_context_cache_reuse_is_clean(o):
     # gsot_destroy parks a context's device state and gsot_create of the same
     # shape and partition takes it back (buffers, stream, captured graphs).
