@@ -263,6 +263,48 @@ def test_structures_eval_and_screen(o, struct, gamma, mu):
     ctx.close()
 
 
+@pytest.mark.parametrize("struct", sorted(STRUCTURES))
+def test_structures_plan_diagnostics(o, struct):
+    """gsot_plan_diagnostics on every structure (singletons, n = 1, n = 33, tall
+    and ragged groups) against the oracle's plan_diagnostics of its own plan:
+    the all-zero block fraction exactly, residuals and mass within 1e-12."""
+    sizes, n = STRUCTURES[struct]
+    p, rng = random_problem(sizes, n, 0.5, 0.4, 7 + len(struct), weighted=True)
+    ctx = ctx_of(p)
+    for scale in (0.0, 0.5, 1.5):
+        x = scale * np.concatenate([rng.uniform(-0.2, 1.6, p.m), rng.uniform(-0.2, 1.6, p.n)])
+        d = ctx.plan_diagnostics(x)
+        ref = o.plan_diagnostics(p, o.plan(p, x[: p.m], x[p.m:]))
+        assert d.group_sparsity == ref[2]
+        for got, want in ((d.marginal_res_a, ref[0]), (d.marginal_res_b, ref[1]), (d.mass, ref[3])):
+            assert abs(got - want) <= 1e-12 * max(1.0, abs(want)), (struct, scale, got, want)
+    ctx.close()
+
+
+def test_python_run_grid_all_modes(o, gold):
+    """run_grid over every solver mode: audit and fast-no-lb runs report the final
+    active set like fast (bench.hpp:168-175); the same instance context serves
+    every run (one upload)."""
+    p = gold_problem(gold, "ragged", 1)
+    inst = G.ProblemInstance(p.cost, p.a, p.b, G.GroupPartition(p.sizes))
+    modes = [G.SolverMode.baseline, G.SolverMode.fast, G.SolverMode.fast_no_lower_bound,
+             G.SolverMode.audit]
+    grid = G.GridSpec(gammas=[0.5], rhos=[0.3], modes=modes,
+                      base=G.SolverOptions(max_outer_loops=3, grad_tol=1e-12))
+    rows = G.run_grid(inst, grid, len(p.sizes), 0)
+    assert [r.mode for r in rows] == ["baseline", "fast", "fast-no-lb", "audit"]
+    assert rows[0].active_set_size_final == 0 and rows[0].blocks_skipped == 0
+    # the screened modes reproduce the baseline trajectory bit for bit (Theorem 2):
+    # the same solution, hence the same diagnostics and final active set
+    for r in rows[1:]:
+        assert (r.objective, r.iterations) == (rows[0].objective, rows[0].iterations)
+        assert (r.group_sparsity, r.marginal_res_a, r.marginal_res_b) == \
+            (rows[0].group_sparsity, rows[0].marginal_res_a, rows[0].marginal_res_b)
+        assert r.active_set_size_final == rows[1].active_set_size_final
+        assert r.blocks_computed + r.blocks_skipped == rows[0].blocks_computed
+    assert rows[1].blocks_skipped > 0
+
+
 def test_fast_equals_baseline_bitwise_on_device(o):
     # SPEC.md:315/:320 (Theorem 2): the screened solve follows the unscreened
     # trajectory exactly.
