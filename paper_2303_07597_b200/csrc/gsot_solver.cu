@@ -142,6 +142,18 @@ class Solver {
       c_->collect_marks();
       return;
     }
+    // per-solve lookup cache by (name literal, buffer parity): the string key
+    // and map search run once per sequence kind, not once per launch
+    Sequence* cached = nullptr;
+    for (const auto& ce : seq_cache_)
+      if (ce.name == name && ce.r == r_) {
+        cached = ce.seq;
+        break;
+      }
+    if (cached) {
+      launch_seq(*cached);
+      return;
+    }
     const std::string key =
         std::string(name) + "/" + std::to_string(r_) + "/" + key_ + "/" + std::to_string(c_->graph_epoch);
     auto it = w_->graphs.find(key);
@@ -165,7 +177,18 @@ class Solver {
       GSOT_CUDA_CHECK(cudaGraphDestroy(g));
       it = w_->graphs.emplace(key, std::move(sq)).first;
     }
-    Sequence& sq = *it->second;
+    seq_cache_.push_back({name, r_, it->second.get()});
+    launch_seq(*it->second);
+  }
+
+  struct SeqCacheEntry {
+    const char* name;
+    int r;
+    Sequence* seq;
+  };
+  std::vector<SeqCacheEntry> seq_cache_;
+
+  void launch_seq(Sequence& sq) {
     if (diag_) GSOT_CUDA_CHECK(cudaEventRecord(diag_ev_[0], c_->stream));
     const auto h0 = std::chrono::steady_clock::now();
     GSOT_CUDA_CHECK(cudaGraphLaunch(sq.exec, c_->stream));
