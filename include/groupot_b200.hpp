@@ -205,7 +205,10 @@ inline Solution run_on(Device& dev, const ProblemInstance& inst, const SolverOpt
   o.lbfgs_memory = opts.lbfgs_memory;
   o.mode = mode;
   o.upper_bound_offset = ub_offset;
-  o.flags = exact_order() ? GSOT_SOLVE_EXACT : 0;
+  o.flags = (exact_order() ? GSOT_SOLVE_EXACT : 0) |
+            (mode == GSOT_MODE_AUDIT && opts.mode == SolverMode::fast_no_lower_bound
+                 ? GSOT_SOLVE_NO_ACTIVE_SET
+                 : 0);
   const Eigen::Index m = inst.m(), n = inst.n();
   std::vector<double> x(static_cast<size_t>(m + n));
   const int64_t cap = static_cast<int64_t>(opts.snapshot_interval) * opts.max_outer_loops * 64 + 16;

@@ -216,7 +216,13 @@ typedef struct gsot_solver_options {
   int32_t flags;             /* GSOT_SOLVE_EXACT: reference-order sums and dots */
 } gsot_solver_options;
 
-enum { GSOT_SOLVE_EXACT = 1 };
+enum {
+  GSOT_SOLVE_EXACT = 1,
+  /* with GSOT_MODE_AUDIT: audit a fast_no_lower_bound solve (no active set),
+   * i.e. audit_solve of a SolverOptions whose mode is fast_no_lower_bound
+   * (solver.hpp:271) */
+  GSOT_SOLVE_NO_ACTIVE_SET = 2
+};
 
 /* Solution (solver.hpp:33-42) minus the dense state/plan (returned through
  * x_out and gsot_plan_columns), GradStats totals (screening.hpp:173-180)

@@ -75,6 +75,21 @@ int main() {
                 max_abs_diff(r.plan.plan, d.plan.plan), (long)r.stats.grad_calls,
                 (long)d.stats.grad_calls);
   }
+  // audit_solve of a fast_no_lower_bound SolverOptions (solver.hpp:271): no active set
+  {
+    SolverOptions o;
+    o.mode = SolverMode::fast_no_lower_bound;
+    o.max_outer_loops = 10;
+    const auto [r, rr] = groupot::audit_solve(inst, p, o);
+    b200::exact_order() = true;
+    const auto [d, dr] = b200::audit_solve(inst, p, o);
+    b200::exact_order() = false;
+    std::printf(", \"audit_nolb\": {\"iters\": [%d, %d], \"grad_calls\": [%ld, %ld], "
+                "\"in_active\": [%lld, %lld], \"active_checks\": [%ld, %ld], \"obj_equal\": %d}",
+                r.iterations, d.iterations, (long)r.stats.grad_calls, (long)d.stats.grad_calls,
+                (long long)r.stats.blocks_in_active_set, (long long)d.stats.blocks_in_active_set,
+                (long)rr.active_checks, (long)dr.active_checks, (int)(r.objective == d.objective));
+  }
   // run_grid (bench.hpp:137-180): the reference's grid driver vs the drop-in
   // one on a warm device context, exact-order solves (bitwise trajectories):
   // every integer field, the objective, the sparsity and the final active

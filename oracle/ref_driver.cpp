@@ -229,7 +229,7 @@ int ref_fast_gradient(const double* cost, int64_t m, int64_t n, const int32_t* s
   }
 }
 
-// solve(): mode 0 baseline, 1 fast, 2 fast-no-lb, 3 audit. out_scalars:
+// solve(): mode 0 baseline, 1 fast, 2 fast-no-lb, 3 audit, 4 audit of fast-no-lb. out_scalars:
 // [objective, wall_seconds]; out_ints: [iterations, converged,
 // line_search_failed, outer_loops, grad_calls, in_active, skipped,
 // unskipped, upper_bounds]. history: grad_calls x 4 (cap rows). plan
@@ -247,11 +247,12 @@ int ref_solve(const double* cost, int64_t m, int64_t n, const int32_t* sizes, in
     o.grad_tol = grad_tol;
     o.max_outer_loops = max_outer_loops;
     o.lbfgs_memory = lbfgs_memory;
-    o.mode = mode == 0   ? SolverMode::baseline
-             : mode == 1 ? SolverMode::fast
-             : mode == 2 ? SolverMode::fast_no_lower_bound
-                         : SolverMode::audit;
-    Solution sol = mode == 3 ? audit_solve(inst, p, o, ub_offset).first : solve(inst, p, o);
+    // mode 4: audit_solve of a fast_no_lower_bound SolverOptions (solver.hpp:271)
+    o.mode = mode == 0                ? SolverMode::baseline
+             : mode == 1              ? SolverMode::fast
+             : mode == 2 || mode == 4 ? SolverMode::fast_no_lower_bound
+                                      : SolverMode::audit;
+    Solution sol = mode >= 3 ? audit_solve(inst, p, o, ub_offset).first : solve(inst, p, o);
     std::memcpy(x_out, sol.state.alpha.data(), sizeof(double) * static_cast<size_t>(m));
     std::memcpy(x_out + m, sol.state.beta.data(), sizeof(double) * static_cast<size_t>(n));
     out_scalars[0] = sol.objective;

@@ -42,7 +42,8 @@ class Solver {
          int64_t hist_cap)
       : c_(c), o_(o), res_(res), hist_(hist), hist_cap_(hist_cap) {
     screened_ = o.mode != GSOT_MODE_BASELINE;
-    use_active_ = o.mode == GSOT_MODE_FAST || o.mode == GSOT_MODE_AUDIT;
+    use_active_ = o.mode == GSOT_MODE_FAST ||
+                  (o.mode == GSOT_MODE_AUDIT && !(o.flags & GSOT_SOLVE_NO_ACTIVE_SET));
     audit_ = o.mode == GSOT_MODE_AUDIT;
     graphs_ = !audit_;
     exact_ = (o.flags & GSOT_SOLVE_EXACT) != 0;
@@ -52,7 +53,7 @@ class Solver {
     w_ = c_->ws.get();
     key_ = std::to_string(o.mode) + "/" + std::to_string(o.lbfgs_memory) + "/" +
            std::to_string(o.upper_bound_offset) + "/" + std::to_string(c_->profile ? c_->profile_mask : 0u) +
-           (exact_ ? "/exact" : "");
+           (exact_ ? "/exact" : "") + (use_active_ ? "" : "/nolb");
   }
 
   ~Solver() {

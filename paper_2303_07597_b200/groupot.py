@@ -400,11 +400,13 @@ class Context:
 
     def solve(self, mode: int = 1, snapshot_interval: int = 10, grad_tol: float = 1e-6,
               max_outer_loops: int = 200, lbfgs_memory: int = 10,
-              upper_bound_offset: float = 0.0, history_cap: int = 0, exact: bool = False):
-        """gsot_solve; exact=True runs the reference-order sums (bitwise trajectory)."""
+              upper_bound_offset: float = 0.0, history_cap: int = 0, exact: bool = False,
+              no_active_set: bool = False):
+        """gsot_solve; exact=True runs the reference-order sums (bitwise trajectory);
+        no_active_set=True with mode 3 audits a fast_no_lower_bound solve."""
         o = _lib.SolverOptionsC(int(snapshot_interval), float(grad_tol), int(max_outer_loops),
                                 int(lbfgs_memory), int(mode), float(upper_bound_offset),
-                                1 if exact else 0)
+                                (1 if exact else 0) | (2 if no_active_set else 0))
         x = np.empty(self.m + self.n)
         r = _lib.SolveResultC()
         hist = np.zeros(max(1, history_cap) * 4, np.int64)
@@ -681,12 +683,12 @@ class Solution:
 
 
 def _run(inst: ProblemInstance, p: RegParams, opts: SolverOptions, mode: int,
-         ub_offset: float = 0.0):
+         ub_offset: float = 0.0, no_active_set: bool = False):
     ctx = inst.context(p)
     cap = opts.snapshot_interval * opts.max_outer_loops * 64 + 16
     res = ctx.solve(mode=mode, snapshot_interval=opts.snapshot_interval, grad_tol=opts.grad_tol,
                     max_outer_loops=opts.max_outer_loops, lbfgs_memory=opts.lbfgs_memory,
-                    upper_bound_offset=ub_offset, history_cap=cap)
+                    upper_bound_offset=ub_offset, history_cap=cap, no_active_set=no_active_set)
     return res
 
 
@@ -707,9 +709,9 @@ def audit_solve(inst: ProblemInstance, p: RegParams, opts: SolverOptions | None 
     opts = opts or SolverOptions()
     if opts.mode == SolverMode.baseline:
         return solve_baseline(inst, p, opts), AuditReport()
-    if opts.mode == SolverMode.fast_no_lower_bound:
-        raise Error("audit of fast-no-lb is not exposed by gsot_solve")
-    res = _run(inst, p, opts, 3, upper_bound_offset)
+    # solver.hpp:271: the active set is used unless the options say fast_no_lower_bound
+    res = _run(inst, p, opts, 3, upper_bound_offset,
+               no_active_set=opts.mode == SolverMode.fast_no_lower_bound)
     rep = AuditReport(res["audit_skip_checks"], res["audit_active_checks"],
                       res["audit_column_compares"], res["audit_gradient_calls"])
     return Solution(inst, p, res), rep

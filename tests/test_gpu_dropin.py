@@ -29,6 +29,10 @@ def test_reference_api_through_the_adapter():
         assert m["obj_rel"] <= 1e-6
         if m["converged"][0]:
             assert m["plan_abs"] <= 1e-6
+    # audit_solve of fast_no_lower_bound options: no active set, exact order -> identical
+    a = d["audit_nolb"]
+    assert a["iters"][0] == a["iters"][1] and a["grad_calls"][0] == a["grad_calls"][1]
+    assert a["in_active"] == [0, 0] and a["active_checks"] == [0, 0] and a["obj_equal"] == 1
     # run_grid (bench.hpp:137-180) on one warm device context, exact-order solves
     g = d["grid"]
     assert g["rows"] == [12, 12] and g["sink_calls"] == 12 and g["csv_roundtrip"] == 1

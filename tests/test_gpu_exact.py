@@ -82,3 +82,21 @@ def test_exact_solve_config1_bitwise(o):
     assert r["objective"] == ro["objective"]
     assert np.array_equal(ctx.plan_columns(r["x"], 0, p.n), ro["plan"])  # final plan bitwise
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+def test_exact_audit_without_active_set_bitwise(o, gold, name):
+    """audit_solve of a fast_no_lower_bound SolverOptions (solver.hpp:271: no
+    active set, every decision re-verified) through GSOT_SOLVE_NO_ACTIVE_SET:
+    bitwise the oracle's mode-4 trajectory, no active-set checks."""
+    gamma, mu = gold[f"{name}/p1/params"]
+    p = Problem(gold[f"{name}/cost"], gold[f"{name}/sizes"], gold[f"{name}/a"], gold[f"{name}/b"],
+                float(gamma), float(mu))
+    ctx = G.Context.from_arrays(p.cost, p.sizes, p.a, p.b, p.gamma, p.mu)
+    r = ctx.solve(mode=3, max_outer_loops=6, grad_tol=1e-12, history_cap=10000, exact=True,
+                  no_active_set=True)
+    ro = o.solve(p, mode=4, max_outer_loops=6, grad_tol=1e-12)
+    assert np.array_equal(r["history"], ro["history"]) and r["blocks_in_active_set"] == 0
+    assert np.array_equal(r["x"], ro["x"]) and r["objective"] == ro["objective"]
+    assert r["audit_active_checks"] == 0 and r["audit_gradient_calls"] == r["grad_calls"]
+    ctx.close()

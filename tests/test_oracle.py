@@ -260,7 +260,7 @@ def test_oracle_equals_reference_random(o, seed):
         assert obj == o.objective(p, *x)
         g2 = o.gradient(p, *x)
         assert np.array_equal(ga, g2[0]) and np.array_equal(gb, g2[1])
-        for mode in (0, 1, 2, 3):
+        for mode in (0, 1, 2, 3, 4):  # 4: audit_solve of a fast_no_lower_bound SolverOptions
             R = ref.solve(p, mode=mode, max_outer_loops=10)
             O = o.solve(p, mode=mode, max_outer_loops=10)
             assert np.array_equal(R["x"], O["x"]) and R["objective"] == O["objective"]
