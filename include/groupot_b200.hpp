@@ -13,6 +13,7 @@
 //   groupot::dual_gradient(s, inst, p, ga, gb) groupot::b200::Device::gradient(s, ga, gb)
 //   groupot::recover_plan(s, inst, p)          groupot::b200::Device::plan(s)
 //   ObjectiveFn / GradientFn closures          groupot::b200::Device::callbacks()
+//   FastGradDispatcher + run_screened wiring   groupot::b200::Device::screened_callbacks()
 //   plan_diagnostics(recover_plan(s), inst)    groupot::b200::Device::plan_diagnostics(s)
 //   groupot::run_grid(inst, grid, nc, pc, sink) groupot::b200::run_grid(...) (one warm
 //                                              device context for the whole grid;
@@ -134,6 +135,58 @@ class Device {
   // new RegParams on the resident instance (no re-upload, no re-validation of C)
   void set_params(const RegParams& p) { check(gsot_set_params(ctx_, p.gamma(), p.mu())); }
 
+  // The screened plug-in level (FastGradDispatcher, screening.hpp:206-315, as
+  // run_screened wires it, solver.hpp:133-250): init the snapshot at x0, then
+  // ObjectiveFn / GradientFn that evaluate with block skipping (and the active
+  // set), and the ChunkHook that refreshes. The reference's own maximize
+  // driven by these is solve_fast; `stats` collects GradStats (per call
+  // history included). exact: reference-order sums (GSOT_EVAL_EXACT).
+  struct Screened {
+    ObjectiveFn objective;
+    GradientFn gradient;
+    ChunkHook hook;
+    std::shared_ptr<GradStats> stats;
+  };
+  Screened screened_callbacks(const Eigen::VectorXd& x0, bool use_active_set, bool exact = false) {
+    check(gsot_init_snapshot(ctx_, x0.data()));
+    auto st = std::make_shared<GradStats>();
+    const int mode = GSOT_EVAL_SCREENED | (exact ? GSOT_EVAL_EXACT : 0);
+    auto eval = [this, st, mode](const Eigen::VectorXd& x) {
+      const size_t dim = static_cast<size_t>(m_ + n_);
+      if (have_scache_ && scache_x_.size() == dim &&
+          std::memcmp(scache_x_.data(), x.data(), sizeof(double) * dim) == 0)
+        return;
+      scache_x_.assign(x.data(), x.data() + dim);
+      sg_.resize(dim);
+      gsot_call_stats cs;
+      check(gsot_eval(ctx_, scache_x_.data(), mode, &scache_obj_, sg_.data(), &cs));
+      have_scache_ = true;
+      st->blocks_in_active_set += cs.in_active;  // screening.hpp:280-287
+      st->blocks_skipped += cs.skipped;
+      st->blocks_unskipped += cs.unskipped;
+      st->upper_bounds_evaluated += cs.upper_bounds;
+      ++st->grad_calls;
+      st->history.push_back({cs.in_active, cs.skipped, cs.unskipped, cs.upper_bounds});
+    };
+    Screened r;
+    r.stats = st;
+    r.objective = [eval, this](const Eigen::VectorXd& x) {
+      eval(x);
+      return scache_obj_;
+    };
+    r.gradient = [eval, this](const Eigen::VectorXd& x, Eigen::VectorXd& out) {
+      eval(x);
+      out.resize(m_ + n_);
+      std::memcpy(out.data(), sg_.data(), sizeof(double) * static_cast<size_t>(m_ + n_));
+    };
+    r.hook = [this, st, use_active_set](int, const Eigen::VectorXd& x) {
+      check(gsot_refresh(ctx_, x.data(), use_active_set ? 1 : 0));  // screening.hpp:231-235
+      ++st->outer_loops;
+      have_scache_ = false;  // a new snapshot: the next call screens afresh
+    };
+    return r;
+  }
+
   // ObjectiveFn / GradientFn for the reference's maximize (lbfgs.hpp:32-33):
   // one fused device evaluation serves both calls at the same x.
   std::pair<ObjectiveFn, GradientFn> callbacks() {
@@ -173,6 +226,9 @@ class Device {
   std::vector<double> x_, g_, cache_x_;
   double cache_obj_ = 0.0;
   bool have_cache_ = false;
+  std::vector<double> sg_, scache_x_;  // screened callbacks' evaluation cache
+  double scache_obj_ = 0.0;
+  bool have_scache_ = false;
 };
 
 // Exact-order solves (bitwise the reference's trajectory; verification mode).

@@ -75,6 +75,29 @@ int main() {
                 max_abs_diff(r.plan.plan, d.plan.plan), (long)r.stats.grad_calls,
                 (long)d.stats.grad_calls);
   }
+  // the reference's own maximize driving the device's screened callbacks
+  // (FastGradDispatcher level) == the reference's solve_fast, exact order
+  {
+    SolverOptions so;
+    so.max_outer_loops = 5;
+    so.grad_tol = 1e-12;
+    const Solution rf = groupot::solve_fast(inst, p, so);
+    auto cb = dev.screened_callbacks(Eigen::VectorXd::Zero(inst.m() + inst.n()), true, true);
+    const MaximizeResult rd = maximize(cb.objective, cb.gradient,
+                                       Eigen::VectorXd::Zero(inst.m() + inst.n()),
+                                       detail::to_lbfgs_options(so), cb.hook);
+    bool hist = rf.stats.history.size() == cb.stats->history.size();
+    for (size_t i = 0; hist && i < rf.stats.history.size(); ++i) {
+      const auto &a = rf.stats.history[i], &b = cb.stats->history[i];
+      hist = a.in_active == b.in_active && a.skipped == b.skipped && a.unskipped == b.unskipped &&
+             a.upper_bounds == b.upper_bounds;
+    }
+    double xd = 0.0;
+    for (Eigen::Index i = 0; i < inst.m(); ++i) xd = std::max(xd, std::abs(rd.x[i] - rf.state.alpha[i]));
+    std::printf(", \"screened_maximize\": {\"iters\": [%d, %d], \"history_equal\": %d, "
+                "\"x_abs\": %.3e, \"skipped\": %lld}",
+                rf.iterations, rd.iterations, (int)hist, xd, (long long)cb.stats->blocks_skipped);
+  }
   // audit_solve of a fast_no_lower_bound SolverOptions (solver.hpp:271): no active set
   {
     SolverOptions o;

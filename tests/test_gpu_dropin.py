@@ -29,6 +29,10 @@ def test_reference_api_through_the_adapter():
         assert m["obj_rel"] <= 1e-6
         if m["converged"][0]:
             assert m["plan_abs"] <= 1e-6
+    # the reference's maximize over the device's screened callbacks == solve_fast
+    sm = d["screened_maximize"]
+    assert sm["iters"][0] == sm["iters"][1] and sm["history_equal"] == 1
+    assert sm["x_abs"] == 0.0 and sm["skipped"] > 0
     # audit_solve of fast_no_lower_bound options: no active set, exact order -> identical
     a = d["audit_nolb"]
     assert a["iters"][0] == a["iters"][1] and a["grad_calls"][0] == a["grad_calls"][1]
