@@ -24,6 +24,7 @@
  *  recover_plan                 dual.hpp:116-128   gsot_plan_columns (column-streamed)
  *  plan nonzero blocks          dual.hpp:139-169   gsot_block_mask
  *  plan_diagnostics(recover_plan) dual.hpp:130-169 gsot_plan_diagnostics
+ *  primal_objective(recover_plan) core.hpp:153-180  gsot_primal_objective
  *  solve / solve_baseline /     solver.hpp:92-293  gsot_solve
  *    solve_fast / audit_solve
  *  SolverOptions, Solution      solver.hpp:25-42   gsot_solver_options, gsot_solve_result
@@ -195,6 +196,12 @@ typedef struct gsot_plan_diag {
  * come from device row / column sums (fixed order, not the reference's
  * summation order: reported, not asserted, as in the reference). */
 GSOT_API int gsot_plan_diagnostics(gsot_ctx* ctx, const double* x, gsot_plan_diag* out);
+/* primal_objective(recover_plan(x), inst, p) (core.hpp:153-180): <T, C> plus
+ * gamma (|T_j|^2 / 2 + mu sum_l |T_{l,j}|) over the columns, on the device
+ * without storing the plan (per-block sums, then columns in group order:
+ * not the reference's summation order; within ~1e-12 relative). With the
+ * dual objective it gives the duality gap. */
+GSOT_API int gsot_primal_objective(gsot_ctx* ctx, const double* x, double* out);
 
 /* ---- Stage 2: the whole solve -------------------------------------------- */
 

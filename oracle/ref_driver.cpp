@@ -139,6 +139,22 @@ int ref_plan_diagnostics(const double* cost, int64_t m, int64_t n, const int32_t
   }
 }
 
+// primal_objective(plan, inst, p) (core.hpp:167-180) of a given m x n plan.
+int ref_primal_objective(const double* cost, int64_t m, int64_t n, const int32_t* sizes, int32_t L,
+                         const double* a, const double* b, double gamma, double mu,
+                         const double* plan_in, double* out) {
+  try {
+    ProblemInstance inst = make(cost, m, n, sizes, L, a, b);
+    TransportPlan t;
+    t.plan.resize(m, n);
+    std::memcpy(t.plan.data(), plan_in, sizeof(double) * static_cast<size_t>(m * n));
+    *out = primal_objective(t, inst, RegParams(gamma, mu));
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 int ref_plan(const double* cost, int64_t m, int64_t n, const int32_t* sizes, int32_t L,
              const double* a, const double* b, double gamma, double mu, const double* alpha,
              const double* beta, double* plan) {

@@ -90,6 +90,7 @@ SIGNATURES = {
     "gsot_block_mask": (C.c_int, [_vp, _vp, _vp]),
     "gsot_plan_columns": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp]),
     "gsot_plan_diagnostics": (C.c_int, [_vp, _vp, C.POINTER(PlanDiagC)]),
+    "gsot_primal_objective": (C.c_int, [_vp, _vp, _dp]),
     "gsot_default_solver_options": (None, [C.POINTER(SolverOptionsC)]),
     "gsot_solve": (C.c_int, [_vp, C.POINTER(SolverOptionsC), _vp, C.POINTER(SolveResultC), _vp,
                              C.c_int64]),

@@ -882,6 +882,29 @@ GSOT_API int gsot_plan_diagnostics(gsot_ctx* ctx, const double* x, gsot_plan_dia
   });
 }
 
+GSOT_API int gsot_primal_objective(gsot_ctx* ctx, const double* x, double* out) {
+  return guard([&] {
+    checked(ctx);
+    if (!out) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null output");
+    upload_x(ctx, x);
+    const gsot::DevProblem P = ctx->problem();
+    const int64_t m = ctx->m, n = ctx->n;
+    ctx->launch(gsot::K_MISC, 8.0 * m * n, [&] {
+      gsot::launch_plan_primal(P, ctx->x_eval, ctx->colpart, ctx->stream);
+    });
+    ctx->launch(gsot::K_MISC, 8.0 * static_cast<double>(ctx->L) * n, [&] {
+      gsot::launch_plan_diag_fold(P, ctx->rowpart, ctx->colpart, ctx->g_eval, ctx->stream);
+    });
+    std::vector<double> cols(static_cast<size_t>(n));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(cols.data(), ctx->g_eval + m, sizeof(double) * n,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    double v = 0.0;
+    for (int64_t j = 0; j < n; ++j) v += cols[j];
+    *out = v;
+  });
+}
+
 GSOT_API void gsot_default_solver_options(gsot_solver_options* o) {
   if (!o) return;
   o->snapshot_interval = 10;  // solver.hpp:26-30

@@ -177,6 +177,8 @@ void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words
 // writes plan row sums to sums[0, m) and column sums to sums[m, m + n).
 void launch_plan_diag(const DevProblem& P, const double* x, double* rowpart, double* colpart,
                       unsigned long long* zero_blocks, cudaStream_t s);
+// primal_objective at x: each block's share of <T, C> + regularizer into colpart.
+void launch_plan_primal(const DevProblem& P, const double* x, double* colpart, cudaStream_t s);
 void launch_plan_diag_fold(const DevProblem& P, const double* rowpart, const double* colpart,
                            double* sums, cudaStream_t s);
 void launch_plan_columns(const DevProblem& P, const double* x, int64_t j0, int64_t ncols,

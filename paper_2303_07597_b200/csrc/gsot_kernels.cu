@@ -1244,6 +1244,41 @@ __global__ void __launch_bounds__(128) k_plan_diag(DevProblem P, const double* _
   if (lane == 0 && zero) atomicAdd(zero_blocks, (unsigned long long)__popc(zero));
 }
 
+// primal_objective(recover_plan(x)) (core.hpp:153-180) per block: the plan
+// entries of k_plan (bitwise), then sum t c, |t|^2 and the block's norm give
+// the block's share <T_b, C_b> + gamma (|T_b|^2 / 2 + mu |T_b|), written to
+// colpart[l * n + j]; the fold sums them per column (in group order).
+__global__ void __launch_bounds__(128) k_plan_primal(DevProblem P, const double* __restrict__ x,
+                                                     double* __restrict__ colpart) {
+  const int lane = threadIdx.x & 31;
+  const int l = blockIdx.y * 4 + (threadIdx.x >> 5);
+  if (l >= P.L) return;
+  const int64_t j = 32ll * blockIdx.x + lane;
+  if (j >= P.n) return;
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const double z = block_z(P, x, l, j);
+  double v = 0.0;
+  if (z > P.tau) {
+    const double scale = ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma);
+    const double bj = x[P.m + j];
+    const double* __restrict__ cp = block_ptr(P, o0, g, j);
+    double tc = 0.0, tt = 0.0;
+    for (int r = 0; r < g; ++r) {
+      const double c = cp[32 * r];
+      const double f = residual(__ldg(x + o0 + r), bj, c);
+      const double t = f > 0.0 ? dmul(scale, f) : 0.0;
+      tc = dadd(tc, dmul(t, c));
+      tt = dadd(tt, dmul(t, t));
+    }
+    v = dadd(tc, dmul(P.gamma, dadd(dmul(0.5, tt), dmul(P.mu, sqrt(tt)))));
+  }
+  colpart[(int64_t)l * P.n + j] = v;
+}
+
+void launch_plan_primal(const DevProblem& P, const double* x, double* colpart, cudaStream_t s) {
+  k_plan_primal<<<dim3((unsigned)P.nw, (unsigned)((P.L + 3) / 4)), 128, 0, s>>>(P, x, colpart);
+}
+
 // Plan row sums (over the chunks, in chunk order) into out[0, m) and column
 // sums (over the groups, in group order) into out[m, m + n).
 __global__ void __launch_bounds__(256) k_plan_diag_fold(DevProblem P,

@@ -392,6 +392,12 @@ class Context:
         _raise(_lib.lib().gsot_plan_columns(self._h, _ptr(_f64(x)), int(j0), int(j1), _ptr(out)))
         return out.reshape(self.m, j1 - j0, order="F")
 
+    def primal_objective(self, x) -> float:
+        """primal_objective(recover_plan(x)) on the device (gsot_primal_objective)."""
+        v = C.c_double()
+        _raise(_lib.lib().gsot_primal_objective(self._h, _ptr(_f64(x)), C.byref(v)))
+        return v.value
+
     def plan_diagnostics(self, x) -> "PlanDiagnostics":
         """plan_diagnostics(recover_plan(x)) on the device (gsot_plan_diagnostics)."""
         d = _lib.PlanDiagC()
@@ -501,6 +507,33 @@ class PlanDiagnostics:
     marginal_res_b: float = 0.0
     group_sparsity: float = 0.0
     mass: float = 0.0
+
+
+def regularizer_value(column, groups: GroupPartition, p: RegParams) -> float:
+    """gamma (|t|^2 / 2 + mu sum_l |t_[l]|) of one plan column (core.hpp:153-165)."""
+    col = _f64(column).reshape(-1)
+    if col.size != groups.total_size():
+        raise DimensionMismatch(f"dimension mismatch: column length {col.size} vs partition size "
+                                f"{groups.total_size()}")
+    norms = sum(float(np.linalg.norm(col[groups.offset(l): groups.offset(l) + groups.size(l)]))
+                for l in range(groups.num_groups()))
+    return p.gamma() * (0.5 * float(col @ col) + p.mu() * norms)
+
+
+def primal_objective(t: TransportPlan, inst: ProblemInstance, p: RegParams) -> float:
+    """<T, C> plus the regularizer over the plan's columns (core.hpp:167-180);
+    numpy on a given plan (state_primal_objective computes it on the device)."""
+    P = t.plan
+    if P.shape != (inst.m(), inst.n()):
+        raise DimensionMismatch(f"dimension mismatch: plan is {P.shape[0]}x{P.shape[1]}, cost is "
+                                f"{inst.m()}x{inst.n()}")
+    return float(np.sum(P * inst.cost)) + sum(regularizer_value(P[:, j], inst.groups, p)
+                                              for j in range(P.shape[1]))
+
+
+def state_primal_objective(s: DualState, inst: ProblemInstance, p: RegParams) -> float:
+    """primal_objective(recover_plan(s), inst, p) on the device (gsot_primal_objective)."""
+    return inst.context(p).primal_objective(_state_vec(s, inst))
 
 
 def state_plan_diagnostics(s: DualState, inst: ProblemInstance, p: RegParams) -> PlanDiagnostics:

@@ -352,6 +352,15 @@ class RefLib:
         assert st == 0
         return out.reshape(p.m, p.n, order="F")
 
+    def primal_objective(self, p: Problem, plan) -> float:
+        keep, a = self._args(p)
+        pl = np.asfortranarray(plan, np.float64)
+        out = C.c_double()
+        st = self.lib.ref_primal_objective(*a, C.c_double(p.gamma), C.c_double(p.mu),
+                                           pl.ctypes.data_as(C.c_void_p), C.byref(out))
+        assert st == 0, self.lib.ref_last_error()
+        return out.value
+
     def plan_diagnostics(self, p: Problem, plan) -> np.ndarray:
         keep, a = self._args(p)
         pl = np.asfortranarray(plan, np.float64)

@@ -127,6 +127,26 @@ def test_golden_plan_diagnostics(gold, name, pi):
     ctx.close()
 
 
+@pytest.mark.parametrize("name", ["synth", "ragged"])
+def test_primal_objective_and_duality_gap(o, gold, name):
+    """gsot_primal_objective against primal_objective of the oracle's plan
+    (core.hpp:167-180; the mirror's numpy restatement is pinned to the
+    reference on CPU), within 1e-12 relative; and the Fenchel-Young identity
+    for the plan T = grad psi(f): primal(T) - dual(x) = -x . grad dual(x)."""
+    p = gold_problem(gold, name, 1)
+    inst = G.ProblemInstance(p.cost, p.a, p.b, G.GroupPartition(p.sizes))
+    prm = G.RegParams(p.gamma, p.mu)
+    ctx = ctx_of(p)
+    for x in (gold[f"{name}/p1/s2/x"], gold[f"{name}/p1/solve1/x"]):
+        got = ctx.primal_objective(x)
+        want = G.primal_objective(G.TransportPlan(o.plan(p, x[: p.m], x[p.m:])), inst, prm)
+        assert abs(got - want) <= 1e-12 * max(1.0, abs(want)), (got, want)
+        obj, g, _ = ctx.eval(x)
+        gap, fy = got - obj, -float(x @ g)
+        assert abs(gap - fy) <= 1e-10 * max(1.0, abs(got), float(np.abs(x).max())), (gap, fy)
+    ctx.close()
+
+
 def test_plan_diagnostics_zero_plan():
     # test_dual.cpp:209-217 on the device: C = 0, x = 0 -> every block z = 0 <= tau
     q = Problem(np.zeros((4, 2)), np.array([2, 2], np.int32), np.full(4, .25), np.full(2, .5),

@@ -281,6 +281,26 @@ def test_oracle_plan_diagnostics_equals_reference_random(o):
 
 
 @needs_ref
+def test_primal_objective_restatement_matches_reference():
+    """The Python mirror's primal_objective / regularizer_value (numpy; the
+    device computes the same quantity, test_gpu_parity) against the
+    reference's primal_objective (core.hpp:153-180) on random plans."""
+    import paper_2303_07597_b200 as G
+
+    ref = RefLib()
+    rng = np.random.default_rng(17)
+    for _ in range(3):
+        sizes = rng.integers(1, 9, size=5).astype(np.int32)
+        m, n = int(sizes.sum()), int(rng.integers(2, 30))
+        p = Problem(rng.uniform(0, 2, (m, n)), sizes, np.full(m, 1 / m), np.full(n, 1 / n), 0.7, 0.4)
+        plan = rng.uniform(0, 1e-2, (m, n)) * (rng.uniform(0, 1, (m, n)) < 0.5)
+        inst = G.ProblemInstance(p.cost, p.a, p.b, G.GroupPartition(p.sizes))
+        got = G.primal_objective(G.TransportPlan(plan), inst, G.RegParams(p.gamma, p.mu))
+        want = ref.primal_objective(p, plan)
+        assert abs(got - want) <= 1e-13 * abs(want)
+
+
+@needs_ref
 def test_oracle_rng_and_cost_match_reference(o):
     ref = RefLib()
     for kind in (0, 1, 2):
