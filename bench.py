@@ -447,7 +447,14 @@ def run_ours(args, world, rank, local, pg):
             "evals_per_solve": calls / args.steps,
             "iterations_per_solve": iters_done / args.steps,
             "screening": {"blocks_computed_frac": blocks / (calls * ctx.L * ctx.n),
-                          "active_lanes_per_task": blocks / max(tasks, 1)},
+                          "active_lanes_per_task": blocks / max(tasks, 1),
+                          # cost bytes per evaluation (config 2: every group has
+                          # m / L rows): dense, the skipped-block minimum (the
+                          # computed blocks' rows) and what the 32-column tiles read
+                          "cost_bytes_per_eval": {
+                              "dense": 8.0 * ctx.m * ctx.n,
+                              "skipped_block_minimum": 8.0 * (ctx.m / ctx.L) * blocks / calls,
+                              "tiles_read": 256.0 * (ctx.m / ctx.L) * tasks / calls}},
             "roofline": roofline,
             "kernels": kinds,
             "gpu_launches": launches,
