@@ -3,7 +3,8 @@ The second solve is bracketed by cudaProfilerStart/Stop (ncu
 --profile-from-start off captures exactly that solve)."""
 import ctypes
 import sys
-sys.path.insert(0, '.')
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2303_07597_b200 as G
 rt = ctypes.CDLL("libcudart.so.12") if len(sys.argv) > 2 else None
 ctx = G.Context.from_config(2, 2, 0.1, 0.5)

@@ -4,8 +4,8 @@
 #   bash tools/ncu_dense.sh TAG
 TAG=${1:-d}
 NCU="ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_eval"
-python tests/_gpu_solve_once.py 0 prof > gpurun_out/dense2_$TAG.log 2>&1 && \
-  $NCU -s 6 -c 2 -o gpurun_out/prof_${TAG}_c2 python tests/_gpu_solve_once.py 0 prof >> gpurun_out/dense2_$TAG.log 2>&1
+python tools/_gpu_solve_once.py 0 prof > gpurun_out/dense2_$TAG.log 2>&1 && \
+  $NCU -s 6 -c 2 -o gpurun_out/prof_${TAG}_c2 python tools/_gpu_solve_once.py 0 prof >> gpurun_out/dense2_$TAG.log 2>&1
 echo c2 $?
 for c in 4 5; do
   $NCU -s 4 -c 2 -o gpurun_out/prof_${TAG}_c$c python tools/_gpu_solve_cfg.py $c 1 > gpurun_out/dense${c}_$TAG.log 2>&1
