@@ -989,6 +989,7 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
 constexpr int kFinSlices = 8;
 constexpr int kFinBatch = 8;
 constexpr int kFinMaskCap = 1024;  // mask words staged per row unit
+constexpr int kFinListCap = 256;   // compacted chunks per slice (units within one group)
 
 // Block = two independent units of (32 rows or columns) x 8 slices. Everything
 // that does not depend on the evaluation (x, d, marginals, the chunk masks and
@@ -1002,6 +1003,11 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     double* __restrict__ partials, EvalScalars* sc, int cnt_pending, int row_blocks, int units) {
   __shared__ double sh[2][2][kFinSlices][33];
   __shared__ uint32_t msk[2][kFinMaskCap];
+  // row unit inside one group: each slice's non-empty chunks (c = slice mod 8,
+  // ascending), compacted once by the slice's warp before the programmatic
+  // wait instead of every lane scanning the group's chunk mask
+  __shared__ int clist[2][kFinSlices][kFinListCap];
+  __shared__ int ccount[2][kFinSlices];
   const int half = threadIdx.x >> 8, t = threadIdx.x & 255;
   const int tx = t & 31, ty = t >> 5;
   const int unit = 2 * blockIdx.x + half;
@@ -1014,7 +1020,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   double marg = 0.0, xv = 0.0, dv = 0.0;
   const int nmw = (P.nw + 31) / 32;
   int lf = 0;
-  bool staged = false;
+  bool staged = false, coop = false;
   const int nlw = (P.L + 31) / 32;
   if (live && is_row) {
     const int64_t i0 = unit * 32ll;
@@ -1026,9 +1032,29 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     }
     lf = P.row_group[i0];
     const int ll = P.row_group[P.m - 1 < i0 + 31 ? P.m - 1 : i0 + 31];
-    staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
-    if (staged)
-      for (int k = t; k < (ll - lf + 1) * nmw; k += 256) msk[half][k] = gmask[(int64_t)lf * nmw + k];
+    coop = lf == ll && (P.nw + kFinSlices - 1) / kFinSlices <= kFinListCap;
+    if (coop) {
+      const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
+      int base = 0;
+      for (int kb = 0; kb < nmw; kb += 32) {
+        const uint32_t w = kb + tx < nmw ? gmask[(int64_t)lf * nmw + kb + tx] & sel : 0u;
+        const int cnt = __popc(w);
+        int pre = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, pre, o);
+          if (tx >= o) pre += y;
+        }
+        int pos = base + pre - cnt;
+        for (uint32_t ww = w; ww != 0u; ww &= ww - 1u) clist[half][ty][pos++] = 32 * (kb + tx) + __ffs(ww) - 1;
+        base += __shfl_sync(0xffffffffu, pre, 31);
+      }
+      if (tx == 0) ccount[half][ty] = base;
+    } else {
+      staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
+      if (staged)
+        for (int k = t; k < (ll - lf + 1) * nmw; k += 256) msk[half][k] = gmask[(int64_t)lf * nmw + k];
+    }
   } else if (live) {
     const int64_t c = unit - row_blocks;
     const int64_t jj = c * 32 + tx;
@@ -1048,7 +1074,19 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   pdl_wait();
   pdl_trigger();
   TL_ENTER(P.tl, TL_FINALIZE);
-  if (i >= 0) {
+  if (i >= 0 && coop) {  // the slice's compacted chunks, ascending: the same sum order
+    const int* __restrict__ cl = clist[half][ty];
+    const int nc = ccount[half][ty];
+    for (int b = 0; b < nc; b += kFinBatch) {
+      double v[kFinBatch];
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q)
+        v[q] = b + q < nc ? rowpart[(int64_t)cl[b + q] * P.m + i] : 0.0;
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q)
+        if (b + q < nc) acc = dadd(acc, v[q]);
+    }
+  } else if (i >= 0) {
     const int l = P.row_group[i];
     const uint32_t* gm = staged ? msk[half] + (int64_t)(l - lf) * nmw : gmask + (int64_t)l * nmw;
     const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
