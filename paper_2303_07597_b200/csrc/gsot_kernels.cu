@@ -1069,6 +1069,28 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
       for (int k = t; k < nlw; k += 256) msk[half][k] = cmask[c * nlw + k];
   }
   __syncthreads();
+  if (live && !is_row && staged && (P.L + kFinSlices - 1) / kFinSlices <= kFinListCap) {
+    // column unit: the slice's non-empty groups (l = slice mod 8, ascending)
+    // from the staged group mask, compacted by the slice's warp
+    coop = true;
+    const uint32_t sel = 0x01010101u << ty;
+    int base = 0;
+    for (int kb = 0; kb < nlw; kb += 32) {
+      const uint32_t w = kb + tx < nlw ? msk[half][kb + tx] & sel : 0u;
+      const int cnt = __popc(w);
+      int pre = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, pre, o);
+        if (tx >= o) pre += y;
+      }
+      int pos = base + pre - cnt;
+      for (uint32_t ww = w; ww != 0u; ww &= ww - 1u) clist[half][ty][pos++] = 32 * (kb + tx) + __ffs(ww) - 1;
+      base += __shfl_sync(0xffffffffu, pre, 31);
+    }
+    if (tx == 0) ccount[half][ty] = base;
+    __syncwarp();
+  }
   if (clear_cmask && live && !is_row && staged)  // consumed: empty for the next screen
     for (int k = t; k < nlw; k += 256) cmask[(unit - row_blocks) * (int64_t)nlw + k] = 0u;
   pdl_wait();
@@ -1114,6 +1136,29 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
       for (int q = 0; q < kFinBatch; ++q)
         if (idx[q] >= 0) acc = dadd(acc, v[q]);
       if (cnt < kFinBatch) break;
+    }
+  } else if (j >= 0 && coop) {  // the slice's compacted groups, ascending: the same sum order
+    const int64_t c = j >> 5;
+    const int* __restrict__ cl = clist[half][ty];
+    const int nc = ccount[half][ty];
+    for (int b = 0; b < nc; b += kFinBatch) {
+      bool on[kFinBatch];
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q)
+        on[q] = b + q < nc && ((words[(int64_t)cl[b + q] * P.nw + c] >> tx) & 1u);
+      double cp[kFinBatch], pp[kFinBatch];
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q) {
+        const int64_t idx = (int64_t)(on[q] ? cl[b + q] : 0) * P.n + j;
+        cp[q] = on[q] ? colpart[idx] : 0.0;
+        pp[q] = on[q] ? psi[idx] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kFinBatch; ++q)
+        if (on[q]) {
+          acc = dadd(acc, cp[q]);
+          ps = dadd(ps, pp[q]);
+        }
     }
   } else if (j >= 0) {
     const int64_t c = j >> 5;
