@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   // ascending), compacted once by the slice's warp before the programmatic
   // wait instead of every lane scanning the group's chunk mask
   __shared__ int clist[2][kFinSlices][kFinListCap];
-  __shared__ int ccount[2][kFinSlices];
+  __shared__ int ccount[2][2 * kFinSlices];
   const int half = threadIdx.x >> 8, t = threadIdx.x & 255;
   const int tx = t & 31, ty = t >> 5;
   const int unit = 2 * blockIdx.x + half;
@@ -1032,24 +1032,30 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     }
     lf = P.row_group[i0];
     const int ll = P.row_group[P.m - 1 < i0 + 31 ? P.m - 1 : i0 + 31];
-    coop = lf == ll && (P.nw + kFinSlices - 1) / kFinSlices <= kFinListCap;
+    // one group: one list of up to kFinListCap chunks per slice; two groups
+    // (a group boundary inside the unit): one list per group, half the cap each
+    const int per = (P.nw + kFinSlices - 1) / kFinSlices;
+    coop = (lf == ll && per <= kFinListCap) || (ll == lf + 1 && per <= kFinListCap / 2);
     if (coop) {
       const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
-      int base = 0;
-      for (int kb = 0; kb < nmw; kb += 32) {
-        const uint32_t w = kb + tx < nmw ? gmask[(int64_t)lf * nmw + kb + tx] & sel : 0u;
-        const int cnt = __popc(w);
-        int pre = cnt;
+      for (int gi = 0; gi <= ll - lf; ++gi) {
+        int* __restrict__ out = clist[half][ty] + gi * (kFinListCap / 2);
+        int base = 0;
+        for (int kb = 0; kb < nmw; kb += 32) {
+          const uint32_t w = kb + tx < nmw ? gmask[(int64_t)(lf + gi) * nmw + kb + tx] & sel : 0u;
+          const int cnt = __popc(w);
+          int pre = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, pre, o);
-          if (tx >= o) pre += y;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (tx >= o) pre += y;
+          }
+          int pos = base + pre - cnt;
+          for (uint32_t ww = w; ww != 0u; ww &= ww - 1u) out[pos++] = 32 * (kb + tx) + __ffs(ww) - 1;
+          base += __shfl_sync(0xffffffffu, pre, 31);
         }
-        int pos = base + pre - cnt;
-        for (uint32_t ww = w; ww != 0u; ww &= ww - 1u) clist[half][ty][pos++] = 32 * (kb + tx) + __ffs(ww) - 1;
-        base += __shfl_sync(0xffffffffu, pre, 31);
+        if (tx == 0) ccount[half][ty + gi * kFinSlices] = base;
       }
-      if (tx == 0) ccount[half][ty] = base;
     } else {
       staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
       if (staged)
@@ -1097,8 +1103,9 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   pdl_trigger();
   TL_ENTER(P.tl, TL_FINALIZE);
   if (i >= 0 && coop) {  // the slice's compacted chunks, ascending: the same sum order
-    const int* __restrict__ cl = clist[half][ty];
-    const int nc = ccount[half][ty];
+    const int gi = P.row_group[i] - lf;  // 0, or 1 past a group boundary
+    const int* __restrict__ cl = clist[half][ty] + gi * (kFinListCap / 2);
+    const int nc = ccount[half][ty + gi * kFinSlices];
     for (int b = 0; b < nc; b += kFinBatch) {
       double v[kFinBatch];
 #pragma unroll
