@@ -25,6 +25,7 @@
 #pragma once
 
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -44,7 +45,7 @@
 namespace groupot {
 namespace b200 {
 
-// Status -> the reference's exception types (errors.hpp:190-271).
+// Status -> the reference's exception types (errors.hpp:9-89).
 inline void check(int st) {
   if (st == GSOT_OK) return;
   gsot_error_detail d;
@@ -61,7 +62,7 @@ inline void check(int st) {
       strip(std::string("marginal ").append(1, d.which).append(": ").c_str());
       throw MarginalNotNormalized(d.which, d.index, msg);
     case GSOT_ERR_PARTITION_MISMATCH: strip("group partition: "); throw PartitionMismatch(msg);
-    case GSOT_ERR_RHO_OUT_OF_RANGE: throw Error(msg);
+    case GSOT_ERR_RHO_OUT_OF_RANGE: throw RhoOutOfRange(d.value);
     case GSOT_ERR_AUDIT_VIOLATION: strip("audit violation: "); throw AuditViolation(msg);
     default: throw Error(msg);
   }
@@ -72,8 +73,20 @@ class Device {
  public:
   Device(const ProblemInstance& inst, const RegParams& p) : m_(inst.m()), n_(inst.n()) {
     std::vector<int32_t> sizes(inst.groups.sizes().begin(), inst.groups.sizes().end());
-    if (inst.a.size() != m_ || inst.b.size() != n_)
-      throw DimensionMismatch("marginals do not match the cost matrix");
+    if (inst.a.size() != m_ || inst.b.size() != n_) {
+      // validate_instance order (core.hpp:117-131): the cost scan comes
+      // first; gsot_create cannot take mismatched marginals, so it runs here.
+      for (Eigen::Index j = 0; j < n_; ++j)
+        for (Eigen::Index i = 0; i < m_; ++i) {
+          const double c = inst.cost(i, j);
+          if (!(c >= 0.0) || !std::isfinite(c)) throw NegativeCost(i, j, c);
+        }
+      if (inst.a.size() != m_)
+        throw DimensionMismatch("marginal a has length " + std::to_string(inst.a.size()) +
+                                ", cost has " + std::to_string(m_) + " rows");
+      throw DimensionMismatch("marginal b has length " + std::to_string(inst.b.size()) +
+                              ", cost has " + std::to_string(n_) + " columns");
+    }
     check(gsot_create(inst.cost.data(), m_, n_, sizes.data(), static_cast<int32_t>(sizes.size()),
                       inst.a.data(), inst.b.data(), p.gamma(), p.mu(), &ctx_));
   }
@@ -267,7 +280,10 @@ inline Solution run_on(Device& dev, const ProblemInstance& inst, const SolverOpt
                  : 0);
   const Eigen::Index m = inst.m(), n = inst.n();
   std::vector<double> x(static_cast<size_t>(m + n));
-  const int64_t cap = static_cast<int64_t>(opts.snapshot_interval) * opts.max_outer_loops * 64 + 16;
+  // worst case per accepted iteration: two attempts of max_bracket (40) +
+  // max_zoom (12) evaluations (lbfgs.hpp:11-30), plus the initial call
+  const int64_t cap =
+      static_cast<int64_t>(opts.snapshot_interval) * opts.max_outer_loops * 2 * (40 + 12) + 16;
   std::vector<int64_t> hist(static_cast<size_t>(cap) * 4);
   gsot_solve_result r;
   check(gsot_solve(dev.handle(), &o, x.data(), &r, hist.data(), cap));

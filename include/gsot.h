@@ -60,13 +60,13 @@ extern "C" {
 
 typedef enum gsot_status {
   GSOT_OK = 0,
-  GSOT_ERR_DIMENSION_MISMATCH = 1,      /* errors.hpp:196-200 DimensionMismatch */
-  GSOT_ERR_NEGATIVE_COST = 2,           /* errors.hpp:202-213 NegativeCost */
-  GSOT_ERR_MARGINAL_NOT_NORMALIZED = 3, /* errors.hpp:215-223 MarginalNotNormalized */
-  GSOT_ERR_PARTITION_MISMATCH = 4,      /* errors.hpp:225-229 PartitionMismatch */
-  GSOT_ERR_INVALID_ARGUMENT = 5,        /* errors.hpp:190-194 Error (RegParams, core.hpp:61-66) */
-  GSOT_ERR_RHO_OUT_OF_RANGE = 6,        /* errors.hpp:231-238 RhoOutOfRange */
-  GSOT_ERR_AUDIT_VIOLATION = 7,         /* errors.hpp:267-271 AuditViolation */
+  GSOT_ERR_DIMENSION_MISMATCH = 1,      /* errors.hpp:14-18 DimensionMismatch */
+  GSOT_ERR_NEGATIVE_COST = 2,           /* errors.hpp:20-31 NegativeCost */
+  GSOT_ERR_MARGINAL_NOT_NORMALIZED = 3, /* errors.hpp:33-41 MarginalNotNormalized */
+  GSOT_ERR_PARTITION_MISMATCH = 4,      /* errors.hpp:43-47 PartitionMismatch */
+  GSOT_ERR_INVALID_ARGUMENT = 5,        /* errors.hpp:9-12 Error (RegParams, core.hpp:61-66) */
+  GSOT_ERR_RHO_OUT_OF_RANGE = 6,        /* errors.hpp:49-56 RhoOutOfRange (detail.value = rho) */
+  GSOT_ERR_AUDIT_VIOLATION = 7,         /* errors.hpp:85-89 AuditViolation */
   GSOT_ERR_CUDA = 8,                    /* no device / CUDA runtime failure */
   GSOT_ERR_OUT_OF_MEMORY = 9,
   GSOT_ERR_STATE = 10 /* call order violated (e.g. screened eval before a snapshot) */
@@ -125,6 +125,10 @@ GSOT_API int gsot_create_shard_device(const double* d_cost, int64_t m, int64_t n
                                       const double* b_shard, double gamma, double mu,
                                       gsot_ctx** out);
 GSOT_API void gsot_destroy(gsot_ctx* ctx);
+/* Free every parked context's device state now (the cache of gsot_destroy).
+ * Returns the number of contexts freed. A create that runs out of device
+ * memory drains the cache and retries once by itself. */
+GSOT_API int64_t gsot_cache_clear(void);
 /* Replace (gamma, mu) keeping the resident cost (RegParams ctor checks). */
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu);
 /* Problem shape: m, n, L and the device bytes held by the context. */
@@ -162,6 +166,11 @@ GSOT_API int gsot_eval(gsot_ctx* ctx, const double* x, int mode, double* objecti
 GSOT_API int gsot_eval_device(gsot_ctx* ctx, const double* d_x, int mode, double* objective,
                               double* d_grad, gsot_call_stats* stats);
 
+/* FastGradDispatcher's upper_bound_offset (screening.hpp:206-215, the
+ * fault-injection knob audit_solve exposes, solver.hpp:266-270) for later
+ * SCREENED gsot_eval calls on this context; 0.0 (the default) is the safe
+ * screen. */
+GSOT_API int gsot_set_upper_bound_offset(gsot_ctx* ctx, double offset);
 /* FastGradDispatcher::init (screening.hpp:220-227): snapshot at x, empty
  * active set. */
 GSOT_API int gsot_init_snapshot(gsot_ctx* ctx, const double* x);

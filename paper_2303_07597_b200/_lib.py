@@ -78,7 +78,9 @@ SIGNATURES = {
     "gsot_create_shard_device": (C.c_int, [_vp, C.c_int64, C.c_int64, _vp, C.c_int32, _vp, _vp,
                                            C.c_double, C.c_double, C.POINTER(_vp)]),
     "gsot_destroy": (None, [_vp]),
+    "gsot_cache_clear": (C.c_int64, []),
     "gsot_set_params": (C.c_int, [_vp, C.c_double, C.c_double]),
+    "gsot_set_upper_bound_offset": (C.c_int, [_vp, C.c_double]),
     "gsot_shape": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _ip,
                              C.POINTER(C.c_int64)]),
     "gsot_eval": (C.c_int, [_vp, _vp, C.c_int, _dp, _vp, C.POINTER(CallStats)]),

@@ -364,6 +364,17 @@ gsot_ctx* cache_take(int64_t m, int64_t n, const int32_t* sizes, int32_t L) {
   }
   return nullptr;
 }
+
+// Free every parked context (all devices). Returns how many were freed.
+size_t cache_drain() {
+  std::vector<gsot_ctx*> victims;
+  {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    victims.swap(g_cache);
+  }
+  for (gsot_ctx* v : victims) delete v;
+  return victims.size();
+}
 }  // namespace
 
 void park_or_delete(gsot_ctx* c) {
@@ -433,8 +444,20 @@ gsot_ctx* create_common(const double* cost, bool cost_on_device, int64_t m, int6
                       " indices, cost has " + std::to_string(m) + " rows");
     }
     if (!reused) {
-      init_device(c);
-      alloc_buffers(c);
+      try {
+        init_device(c);
+        alloc_buffers(c);
+      } catch (const Error& e) {
+        // Parked contexts hold HBM (a config-5 cost alone is 40 GB): on an
+        // allocation failure free them all and retry once on a fresh context.
+        if (e.status != GSOT_ERR_OUT_OF_MEMORY || cache_drain() == 0) throw;
+        cudaGetLastError();
+        delete c;
+        c = new gsot_ctx();
+        setup_shape(c, m, n, sizes, L, gamma, mu);
+        init_device(c);
+        alloc_buffers(c);
+      }
     }
     set_marginals(c, a, b);
     // Upload in column chunks through a staging buffer (bounded extra HBM;
@@ -634,9 +657,12 @@ GSOT_API const char* gsot_version(void) { return "gsot-b200 0.1 (sm_100a)"; }
 
 GSOT_API int gsot_params_from_rho(double gamma, double rho, double* gamma_eff, double* mu_eff) {
   return guard([&] {
-    if (!(rho > 0.0) || !(rho < 1.0))  // core.hpp:148-151
-      throw Error(GSOT_ERR_RHO_OUT_OF_RANGE,
-                  "rho = " + std::to_string(rho) + " is outside the open interval (0,1)");
+    if (!(rho > 0.0) || !(rho < 1.0)) {  // core.hpp:148-151, errors.hpp:49-56
+      Error e(GSOT_ERR_RHO_OUT_OF_RANGE,
+              "rho = " + std::to_string(rho) + " is outside the open interval (0,1)");
+      e.detail.value = rho;  // RhoOutOfRange::rho
+      throw e;
+    }
     const double g = gamma * (1.0 - rho), mu = rho / (1.0 - rho);
     check_params(g, mu);
     if (gamma_eff) *gamma_eff = g;
@@ -687,6 +713,16 @@ GSOT_API int gsot_create_shard_device(const double* d_cost, int64_t m, int64_t n
 
 GSOT_API void gsot_destroy(gsot_ctx* ctx) { park_or_delete(ctx); }
 
+GSOT_API int64_t gsot_cache_clear(void) { return static_cast<int64_t>(cache_drain()); }
+
+GSOT_API int gsot_set_upper_bound_offset(gsot_ctx* ctx, double offset) {
+  return guard([&] {
+    checked(ctx);
+    if (!std::isfinite(offset)) throw Error(GSOT_ERR_INVALID_ARGUMENT, "non-finite offset");
+    ctx->ub_offset = offset;
+  });
+}
+
 GSOT_API int gsot_set_params(gsot_ctx* ctx, double gamma, double mu) {
   return guard([&] {
     checked(ctx);
@@ -716,7 +752,7 @@ GSOT_API int gsot_eval(gsot_ctx* ctx, const double* x, int mode, double* objecti
     checked(ctx);
     if (mode < 0 || mode > 3) throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
     upload_x(ctx, x);
-    EvalOut e = eval_device(ctx, ctx->x_eval, mode, ctx->g_eval, nullptr, 0.0, true);
+    EvalOut e = eval_device(ctx, ctx->x_eval, mode, ctx->g_eval, nullptr, ctx->ub_offset, true);
     if (grad) {
       GSOT_CUDA_CHECK(cudaMemcpyAsync(grad, ctx->g_eval, sizeof(double) * (ctx->m + ctx->n),
                                       cudaMemcpyDeviceToHost, ctx->stream));
@@ -735,7 +771,7 @@ GSOT_API int gsot_eval_device(gsot_ctx* ctx, const double* d_x, int mode, double
     if (mode < 0 || mode > 3) throw Error(GSOT_ERR_INVALID_ARGUMENT, "unknown eval mode");
     GSOT_CUDA_CHECK(cudaMemcpyAsync(ctx->x_eval, d_x, sizeof(double) * (ctx->m + ctx->n),
                                     cudaMemcpyDeviceToDevice, ctx->stream));
-    EvalOut e = eval_device(ctx, ctx->x_eval, mode, d_grad, nullptr, 0.0, true);
+    EvalOut e = eval_device(ctx, ctx->x_eval, mode, d_grad, nullptr, ctx->ub_offset, true);
     if (objective) *objective = e.objective;
     if (stats) *stats = e.stats;
   });

@@ -63,6 +63,7 @@ struct SolverWorkspace {
 
 struct gsot_ctx {
   int device = 0;
+  double ub_offset = 0.0;  // FastGradDispatcher upper_bound_offset for gsot_eval (screening.hpp:211)
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   int64_t m = 0, n = 0;

@@ -30,7 +30,7 @@ from . import _lib
 
 
 class Error(RuntimeError):
-    """Base of every error raised by this library (errors.hpp:190-194)."""
+    """Base of every error raised by this library (errors.hpp:9-12)."""
 
 
 class DimensionMismatch(Error):
@@ -84,7 +84,7 @@ def _raise(status: int) -> None:
     if status == 4:
         raise PartitionMismatch(msg)
     if status == 6:
-        raise RhoOutOfRange(msg)
+        raise RhoOutOfRange(msg, d.value)
     if status == 7:
         raise AuditViolation(msg)
     if status == 8:
@@ -250,15 +250,30 @@ class TransportPlan:
     plan: np.ndarray
 
 
+def _check_marginal_lengths(cost: np.ndarray, a: np.ndarray, b: np.ndarray) -> None:
+    """validate_instance's order (core.hpp:117-131) when a marginal has the
+    wrong length: the library cannot take such a pair, so the cost scan that
+    comes first in the reference (first offender in j-major order) runs here
+    before the DimensionMismatch; both messages are the reference's."""
+    m, n = cost.shape
+    if a.size == m and b.size == n:
+        return
+    flat = np.asarray(cost, dtype=np.float64).reshape(-1, order="F")
+    bad = np.flatnonzero(~(np.isfinite(flat) & (flat >= 0.0)))
+    if bad.size:
+        k = int(bad[0])
+        i, j, v = k % m, k // m, float(flat[k])
+        raise NegativeCost(f"cost({i},{j}) = {v:.6f} is negative or non-finite", i, j, v)
+    if a.size != m:
+        raise DimensionMismatch(
+            f"dimension mismatch: marginal a has length {a.size}, cost has {m} rows")
+    raise DimensionMismatch(
+        f"dimension mismatch: marginal b has length {b.size}, cost has {n} columns")
+
+
 def validate_instance(inst: ProblemInstance) -> None:
     """core.hpp:117-139 (run by the library while uploading the cost)."""
-    if inst.a.size != inst.m():
-        raise DimensionMismatch(
-            f"dimension mismatch: marginal a has length {inst.a.size}, cost has {inst.m()} rows")
-    if inst.b.size != inst.n():
-        raise DimensionMismatch(
-            f"dimension mismatch: marginal b has length {inst.b.size}, cost has {inst.n()} "
-            "columns")
+    _check_marginal_lengths(inst.cost, inst.a, inst.b)
     ctx = Context.from_instance(inst, RegParams(1.0, 1.0))
     ctx.close()
 
@@ -277,10 +292,7 @@ class Context:
 
     @classmethod
     def from_instance(cls, inst: ProblemInstance, p: RegParams) -> "Context":
-        if inst.a.size != inst.m() or inst.b.size != inst.n():
-            raise DimensionMismatch(
-                f"dimension mismatch: marginals ({inst.a.size},{inst.b.size}) vs cost "
-                f"{inst.m()}x{inst.n()}")
+        _check_marginal_lengths(inst.cost, inst.a, inst.b)
         return cls.from_arrays(inst.cost, inst.groups.sizes(), inst.a, inst.b, p.gamma(), p.mu())
 
     @classmethod
@@ -289,6 +301,7 @@ class Context:
         m, n = cost.shape
         sizes = np.ascontiguousarray(sizes, dtype=np.int32)
         a, b = _f64(a), _f64(b)
+        _check_marginal_lengths(cost, a, b)
         h = C.c_void_p()
         st = _lib.lib().gsot_create(_ptr(cost), m, n, _ptr(sizes), len(sizes), _ptr(a), _ptr(b),
                                     float(gamma), float(mu), C.byref(h))
@@ -363,6 +376,9 @@ class Context:
         st.in_active, st.skipped, st.unskipped, st.upper_bounds = (
             cs.in_active, cs.skipped, cs.unskipped, cs.upper_bounds)
         return obj.value, g, st
+
+    def set_upper_bound_offset(self, offset: float) -> None:
+        _raise(_lib.lib().gsot_set_upper_bound_offset(self._h, float(offset)))
 
     def init_snapshot(self, x) -> None:
         _raise(_lib.lib().gsot_init_snapshot(self._h, _ptr(_f64(x))))
@@ -448,6 +464,11 @@ class Context:
         ms = C.c_double()
         _raise(_lib.lib().gsot_timer(self._h, 1, C.byref(ms)))
         return ms.value
+
+
+def cache_clear() -> int:
+    """Free the device state parked by closed contexts (gsot_cache_clear)."""
+    return int(_lib.lib().gsot_cache_clear())
 
 
 def set_device(device: int) -> None:
@@ -626,10 +647,9 @@ class FastGradDispatcher:
 
     def __init__(self, inst: ProblemInstance, p: RegParams, stats: GradStats,
                  use_active_set: bool, upper_bound_offset: float = 0.0):
-        if upper_bound_offset != 0.0:
-            raise Error("upper_bound_offset is supported through audit_solve only")
         self.inst, self.p, self.stats = inst, p, stats
         self.use_active_set = use_active_set
+        self.upper_bound_offset = float(upper_bound_offset)
         self._ctx = inst.context(p)
 
     def init(self, s: DualState) -> None:
@@ -639,7 +659,11 @@ class FastGradDispatcher:
         self._ctx.refresh(_state_vec(s, self.inst), self.use_active_set)
 
     def gradient(self, s: DualState):
-        obj, g, st = self._ctx.eval(_state_vec(s, self.inst), screened=True)
+        self._ctx.set_upper_bound_offset(self.upper_bound_offset)
+        try:
+            obj, g, st = self._ctx.eval(_state_vec(s, self.inst), screened=True)
+        finally:
+            self._ctx.set_upper_bound_offset(0.0)
         self.stats.blocks_in_active_set += st.in_active
         self.stats.blocks_skipped += st.skipped
         self.stats.blocks_unskipped += st.unskipped

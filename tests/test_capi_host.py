@@ -78,8 +78,11 @@ def test_params_from_rho():
     assert abs(p2.gamma() - 2.0) <= 1e-15 and abs(p2.mu() - 4.0) <= 1e-14
     assert abs(p2.tau() - 8.0) <= 1e-14
     for rho in (0.0, 1.0, -0.2, 1.3):
-        with pytest.raises(G.RhoOutOfRange):
+        with pytest.raises(G.RhoOutOfRange) as ei:
             G.params_from_rho(1.0, rho)
+        # errors.hpp:49-56: the field and the message of RhoOutOfRange(rho)
+        assert ei.value.rho == rho
+        assert str(ei.value) == f"rho = {rho:.6f} is outside the open interval (0,1)"
     with pytest.raises(G.Error):
         G.RegParams(0.0, 1.0)
     with pytest.raises(G.Error):
@@ -107,9 +110,18 @@ def test_dimension_checks_precede_device_work():
         G.dual_gradient(bad, inst, G.RegParams(1.0, 1.0))
     with pytest.raises(G.DimensionMismatch):
         G.recover_plan(bad, inst, G.RegParams(1.0, 1.0))
-    with pytest.raises(G.DimensionMismatch):
+    with pytest.raises(G.DimensionMismatch) as ei:
         G.validate_instance(G.ProblemInstance(np.zeros((3, 2)), [1.0], [0.5, 0.5],
                                               G.GroupPartition([3])))
+    assert str(ei.value) == "dimension mismatch: marginal a has length 1, cost has 3 rows"
+    # core.hpp:117-131: the cost scan precedes the length checks, so a
+    # negative entry wins over a wrong-length marginal (first offender j-major)
+    cost = np.zeros((3, 2))
+    cost[2, 0], cost[0, 1] = -1.0, -2.0
+    with pytest.raises(G.NegativeCost) as ei:
+        G.validate_instance(G.ProblemInstance(cost, [1.0], [0.5, 0.5], G.GroupPartition([3])))
+    assert (ei.value.row, ei.value.col, ei.value.value) == (2, 0, -1.0)
+    assert str(ei.value) == "cost(2,0) = -1.000000 is negative or non-finite"
 
 
 def test_cost_is_frozen():

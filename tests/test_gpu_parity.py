@@ -398,6 +398,39 @@ def test_python_mirror_api(o):
     assert 0.0 <= d.group_sparsity <= 1.0 and d.mass > 0
 
 
+def test_python_dispatcher_upper_bound_offset(o):
+    """FastGradDispatcher(inst, p, stats, use_active_set, upper_bound_offset)
+    (screening.hpp:206-215, :264): a negative offset skips blocks the safe
+    screen would compute (audit_solve's fault injection), so the gradient
+    may differ from the dense one; decisions and counters follow the oracle's
+    dispatcher with the same offset, and the gradient is the oracle's."""
+    p, rng = random_problem([12, 7, 30, 1, 9], 60, 0.4, 0.7, 5, weighted=True)
+    inst = G.ProblemInstance(p.cost, p.a, p.b, G.GroupPartition(p.sizes))
+    prm = G.RegParams(p.gamma, p.mu)
+    x0 = np.zeros(p.m + p.n)
+    x1 = np.concatenate([rng.uniform(-0.1, 1.2, p.m), rng.uniform(-0.1, 1.2, p.n)]) * 0.05
+    x2 = x1 + 1e-3 * rng.normal(size=x1.size)
+    skipped = [_dispatcher_offset_case(o, p, inst, prm, x0, x1, x2, off)
+               for off in (-0.2, 0.0, 0.05)]
+    assert skipped[0] >= skipped[1] >= skipped[2]
+
+
+def _dispatcher_offset_case(o, p, inst, prm, x0, x1, x2, offset):
+    st = G.GradStats()
+    disp = G.FastGradDispatcher(inst, prm, st, True, offset)
+    disp.init(G.DualState(x0[: p.m], x0[p.m:]))
+    disp.refresh(G.DualState(x1[: p.m], x1[p.m:]))
+    ga, gb, _ = disp.gradient(G.DualState(x2[: p.m], x2[p.m:]))
+    mem_o, _ = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+    ga_o, gb_o, cnt, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem_o, x2[: p.m], x2[p.m:],
+                                         ub_offset=offset)
+    assert list(st.history[-1]) == cnt.tolist()
+    scale = grad_scale(o, p, x2)
+    err = np.abs(np.concatenate([ga, gb]) - np.concatenate([ga_o, gb_o]))
+    assert np.all(err <= GRAD_STOL * scale)
+    return int(cnt[1])
+
+
 def test_python_run_grid(o, gold):
     """run_grid (bench.hpp:137-180) through the Python mirror on the reference's
     own synthetic instance: the reference's (gamma, rho, mode) order, one
