@@ -245,6 +245,57 @@ int ref_fast_gradient(const double* cost, int64_t m, int64_t n, const int32_t* s
   }
 }
 
+// Timing sample of the reference hot path (bench.py: the reference arm and
+// cpu_baseline). The instance is built once (its copy is not timed); then,
+// timed with steady_clock as solver.hpp:243-246 times maximize:
+//   times[2] += FastGradDispatcher init(x_a) + refresh(x_s): two take_snapshot
+//               passes and one build_active_set (screening.hpp:220-235);
+//   times[0] += dual_objective(x)                      (dual.hpp:38-52, dense
+//               in every mode, solver.hpp:161-164);
+//   times[1] += dual_gradient(x) through the dispatcher (screening.hpp:239-287).
+// repeated `reps` times. counters: the last gradient call's GradStats row.
+int ref_time_eval(const double* cost, int64_t m, int64_t n, const int32_t* sizes, int32_t L,
+                  const double* a, const double* b, double gamma, double mu,
+                  const double* alpha_a, const double* beta_a, const double* alpha_s,
+                  const double* beta_s, const double* alpha, const double* beta, int reps,
+                  double* times, int64_t* counters, double* objective) {
+  try {
+    using clock = std::chrono::steady_clock;
+    ProblemInstance inst = make(cost, m, n, sizes, L, a, b);
+    RegParams p(gamma, mu);
+    DualState sa = state(alpha_a, beta_a, m, n), ss = state(alpha_s, beta_s, m, n),
+              s = state(alpha, beta, m, n);
+    times[0] = times[1] = times[2] = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      GradStats stats;
+      FastGradDispatcher disp(inst, p, stats, true, 0.0);
+      auto t0 = clock::now();
+      disp.init(sa);
+      disp.refresh(ss, 1);
+      auto t1 = clock::now();
+      *objective = dual_objective(s, inst, p);
+      auto t2 = clock::now();
+      disp.begin_call(s);
+      Eigen::VectorXd gav, gbv;
+      dual_gradient(
+          s, inst, p, [&](int j, Eigen::VectorXd& gcol) { disp.column(j, gcol); }, gav, gbv);
+      disp.end_call();
+      auto t3 = clock::now();
+      times[2] += std::chrono::duration<double>(t1 - t0).count();
+      times[0] += std::chrono::duration<double>(t2 - t1).count();
+      times[1] += std::chrono::duration<double>(t3 - t2).count();
+      const auto& h = stats.history.back();
+      counters[0] = h.in_active;
+      counters[1] = h.skipped;
+      counters[2] = h.unskipped;
+      counters[3] = h.upper_bounds;
+    }
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 // solve(): mode 0 baseline, 1 fast, 2 fast-no-lb, 3 audit, 4 audit of fast-no-lb. out_scalars:
 // [objective, wall_seconds]; out_ints: [iterations, converged,
 // line_search_failed, outer_loops, grad_calls, in_active, skipped,

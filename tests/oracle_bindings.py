@@ -408,6 +408,23 @@ class RefLib:
         assert st == 0, self.lib.ref_last_error()
         return ga, gb, cnt, member.reshape(p.L, p.n, order="F")
 
+    def time_eval(self, p: Problem, x_a, x_s, x, reps: int = 1):
+        """ref_time_eval: the reference's dispatcher init(x_a) + refresh(x_s),
+        dual_objective(x) and the screened dual_gradient(x), each timed with
+        steady_clock (instance copy excluded). Returns (t_obj, t_grad,
+        t_refresh) in seconds summed over reps, the counters and the objective."""
+        keep, a = self._args(p)
+        vs = [self._v(v) for v in (*x_a, *x_s, *x)]
+        times = np.zeros(3)
+        cnt = np.zeros(4, np.int64)
+        obj = C.c_double()
+        st = self.lib.ref_time_eval(*a, C.c_double(p.gamma), C.c_double(p.mu),
+                                    *[v[1] for v in vs], C.c_int(reps),
+                                    times.ctypes.data_as(C.c_void_p),
+                                    cnt.ctypes.data_as(C.c_void_p), C.byref(obj))
+        assert st == 0, self.lib.ref_last_error()
+        return times, cnt, obj.value
+
     def solve(self, p: Problem, mode=1, snapshot_interval=10, grad_tol=1e-6, max_outer_loops=200,
               lbfgs_memory=10, ub_offset=0.0, plan=False):
         keep, a = self._args(p)
@@ -476,3 +493,79 @@ class RefLib:
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+class ColumnParallelOracle:
+    """The oracle over column ranges of a large instance on host threads
+    (ctypes releases the GIL): every per-block quantity -- snapshot norms,
+    screening decisions, active-set membership, plan entries -- is the
+    oracle's own (bitwise), and the column-separable sums are recombined:
+    objective = sum_r obj_r - (R-1) a.alpha, grad_alpha = sum_r ga_r - (R-1) a
+    (dual.hpp:38-52, :85-100 restricted to columns J_r). Test infrastructure
+    for BASELINE configs 3-5 (8 - 40 GB), where one single-threaded pass is
+    a minute of CPU."""
+
+    def __init__(self, p: Problem, threads: int = 0):
+        self.o = Oracle()
+        self.p = p
+        threads = threads or (os.cpu_count() or 1)
+        self.ranges = [(int(r[0]), int(r[-1]) + 1)
+                       for r in np.array_split(np.arange(p.n), min(threads, p.n))]
+        self.subs = [Problem(p.cost[:, j0:j1], p.sizes, p.a, p.b[j0:j1], p.gamma, p.mu)
+                     for j0, j1 in self.ranges]
+
+    def _map(self, fn):
+        import threading
+
+        out = [None] * len(self.subs)
+
+        def run(i):
+            out[i] = fn(i, self.subs[i], *self.ranges[i])
+
+        ths = [threading.Thread(target=run, args=(i,)) for i in range(len(self.subs))]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return out
+
+    def eval(self, x):
+        """(objective, grad) at x = [alpha; beta]."""
+        m, R = self.p.m, len(self.subs)
+        al = x[:m]
+        res = self._map(lambda i, q, j0, j1: (
+            self.o.objective(q, al, x[m + j0:m + j1]), *self.o.gradient(q, al, x[m + j0:m + j1])))
+        obj = sum(r[0] for r in res) - (R - 1) * float(self.p.a @ al)
+        ga = sum(r[1] for r in res) - (R - 1) * self.p.a
+        gb = np.concatenate([r[2] for r in res])
+        return obj, np.concatenate([ga, gb])
+
+    def block_mask(self, x):
+        """Nonzero (l, j) blocks at x: z > tau (regularizer.hpp:67), L x n."""
+        m = self.p.m
+        tau = self.p.gamma * self.p.mu
+        res = self._map(lambda i, q, j0, j1: self.o.snapshot(q, x[:m], x[m + j0:m + j1])[0])
+        return np.concatenate(res, axis=1) > tau
+
+    def fast_gradient(self, x_a, x_s, x):
+        """FastGradDispatcher after init(x_a), refresh(x_s); gradient at x:
+        (grad, counters[4])."""
+        m, R = self.p.m, len(self.subs)
+
+        def one(i, q, j0, j1):
+            sl = slice(m + j0, m + j1)
+            mem, _ = self.o.active_set(q, x_a[:m], x_a[sl], x_s[:m], x_s[sl])
+            ga, gb, cnt, _ = self.o.fast_gradient(q, x_s[:m], x_s[sl], mem, x[:m], x[sl])
+            return ga, gb, cnt
+
+        res = self._map(one)
+        ga = sum(r[0] for r in res) - (R - 1) * self.p.a
+        gb = np.concatenate([r[1] for r in res])
+        return np.concatenate([ga, gb]), sum(r[2] for r in res)
+
+    def plan_columns(self, x, cols):
+        """Plan columns `cols` (m x len(cols))."""
+        m = self.p.m
+        q = Problem(self.p.cost[:, cols], self.p.sizes, self.p.a, self.p.b[cols], self.p.gamma,
+                    self.p.mu)
+        return self.o.plan(q, x[:m], x[m:][cols])

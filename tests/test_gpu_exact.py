@@ -100,3 +100,28 @@ def test_exact_audit_without_active_set_bitwise(o, gold, name):
     assert np.array_equal(r["x"], ro["x"]) and r["objective"] == ro["objective"]
     assert r["audit_active_checks"] == 0 and r["audit_gradient_calls"] == r["grad_calls"]
     ctx.close()
+
+
+def test_exact_solve_config2_full_budget_bitwise(o):
+    """BASELINE config 2 (m = n = 10,000) over its full 200-iteration budget:
+    the exact-order device solve equals the oracle's (the reference's order of
+    operations) bit for bit -- iterations, gradient calls, per-call screening
+    counters, final state, objective and plan columns (north_star: plan within
+    1e-6 after the same number of iterations; here the difference is 0)."""
+    src, tgt, sizes, a, b = G.config_features(2, 2)
+    cost = o.cost_matrix(src, tgt)
+    cost /= cost.max()
+    p = Problem(cost, sizes, a, b, 0.1, 0.5)
+    ctx = G.Context.from_config(2, 2, 0.1, 0.5)
+    r = ctx.solve(mode=1, max_outer_loops=20, grad_tol=1e-12, history_cap=100000, exact=True)
+    ro = o.solve(p, mode=1, max_outer_loops=20, grad_tol=1e-12)
+    assert r["iterations"] == ro["iterations"] == 200
+    assert r["grad_calls"] == ro["grad_calls"]
+    assert np.array_equal(r["history"], ro["history"])
+    assert np.array_equal(r["x"], ro["x"]) and r["objective"] == ro["objective"]
+    cols = np.arange(0, p.n, 7)[:1024]
+    plan_o = o.plan(Problem(cost[:, cols], sizes, a, b[cols], 0.1, 0.5), ro["x"][:p.m],
+                    ro["x"][p.m:][cols])
+    plan = np.concatenate([ctx.plan_columns(r["x"], j, j + 1) for j in cols[:64]], axis=1)
+    assert np.array_equal(plan, plan_o[:, :64])
+    ctx.close()

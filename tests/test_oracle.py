@@ -318,3 +318,32 @@ def test_audit_fault_injection_matches_reference(o):
     R = ref.solve(p, mode=3, max_outer_loops=5, ub_offset=-1e3)
     O = o.solve(p, mode=3, max_outer_loops=5, ub_offset=-1e3)
     assert R["status"] == 7 and O["status"] == 7  # AuditViolation
+
+
+def test_column_parallel_oracle_matches_sequential(o):
+    """ColumnParallelOracle (the checker of the full-size config tests):
+    per-block results bitwise the sequential oracle's, the recombined sums
+    within 1e-13."""
+    from oracle_bindings import ColumnParallelOracle
+
+    rng = np.random.default_rng(3)
+    sizes = np.array([13, 1, 40, 7, 22], np.int32)
+    m, n = int(sizes.sum()), 97
+    a = rng.uniform(0.5, 1.5, m)
+    p = Problem(rng.uniform(0, 1, (m, n)), sizes, a / a.sum(), np.full(n, 1 / n), 0.5, 0.4)
+    x = np.concatenate([rng.uniform(0, 0.9, m), rng.uniform(0, 0.9, n)])
+    xa, xs = x * 0.99, x * 0.999
+    po = ColumnParallelOracle(p, threads=6)
+    obj, g = po.eval(x)
+    assert abs(obj - o.objective(p, x[:m], x[m:])) <= 1e-13 * abs(obj)
+    ga, gb = o.gradient(p, x[:m], x[m:])
+    assert np.max(np.abs(g - np.concatenate([ga, gb]))) <= 1e-14 * np.max(np.abs(g))
+    z, _, _ = o.snapshot(p, x[:m], x[m:])
+    assert np.array_equal(po.block_mask(x), z > p.gamma * p.mu)
+    mem, _ = o.active_set(p, xa[:m], xa[m:], xs[:m], xs[m:])
+    ga2, gb2, cnt, _ = o.fast_gradient(p, xs[:m], xs[m:], mem, x[:m], x[m:])
+    g2, cnt2 = po.fast_gradient(xa, xs, x)
+    assert cnt2.tolist() == cnt.tolist() and cnt[0] > 0 and cnt[1] > 0
+    assert np.max(np.abs(g2 - np.concatenate([ga2, gb2]))) <= 1e-14 * np.max(np.abs(g2))
+    cols = np.array([0, 5, 96, 40])
+    assert np.array_equal(po.plan_columns(x, cols), o.plan(p, x[:m], x[m:])[:, cols])
