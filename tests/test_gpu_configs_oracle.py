@@ -2,8 +2,8 @@
 cost; config 3 at every mu of its sweep) against the oracle itself, not just
 device self-consistency ("Next round" 1(b)).
 
-States come from the device's own fast-mode trajectory (iterates after 10,
-20 and 30 accepted iterations: x_a, x_s, x). The oracle runs on the host
+States come from the device's own fast-mode trajectory (iterates after 50
+and 60 accepted iterations: x_a, x_s; x a probe 0.1 (x_s - x_a) beyond x_s). The oracle runs on the host
 copy of the SAME cost entries (the device cost generator is bitwise the
 reference cost_matrix, test_gpu_parity.py) over column ranges on all host
 cores (ColumnParallelOracle: per-block values bitwise the sequential
@@ -71,7 +71,11 @@ def test_full_size_config_vs_oracle(cfg):
         ctx.set_params(gamma, mu)
         p = Problem(cost, sizes, a, b, gamma, mu)
         po = ColumnParallelOracle(p)
-        xa, xs, x = (ctx.solve(mode=1, max_outer_loops=k, grad_tol=1e-12)["x"] for k in (1, 2, 3))
+        # x_a, x_s: iterates after 50 and 60 accepted iterations; x: a trial
+        # point a tenth of the last chunk's step beyond x_s (a line-search
+        # probe along the recent direction)
+        xa, xs = (ctx.solve(mode=1, max_outer_loops=k, grad_tol=1e-12)["x"] for k in (5, 6))
+        x = xs + 0.1 * (xs - xa)
         for y in (xs, x):
             obj, g, st = ctx.eval(y)
             obj_o, g_o = po.eval(y)
