@@ -166,6 +166,12 @@ GSOT_API int gsot_eval(gsot_ctx* ctx, const double* x, int mode, double* objecti
 GSOT_API int gsot_eval_device(gsot_ctx* ctx, const double* d_x, int mode, double* objective,
                               double* d_grad, gsot_call_stats* stats);
 
+/* The reference's sequential floating-point sum ((s0 + t[0]) + t[1]) + ...
+ * (every reduction of the reference accumulates left to right, e.g.
+ * regularizer.hpp:47-51), computed in parallel on the device and bit for bit
+ * by the exact-order engine. terms: host, n doubles. */
+GSOT_API int gsot_sequential_sum(gsot_ctx* ctx, const double* terms, int64_t n, double s0,
+                                 double* out);
 /* FastGradDispatcher's upper_bound_offset (screening.hpp:206-215, the
  * fault-injection knob audit_solve exposes, solver.hpp:266-270) for later
  * SCREENED gsot_eval calls on this context; 0.0 (the default) is the safe

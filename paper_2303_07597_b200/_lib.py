@@ -81,6 +81,7 @@ SIGNATURES = {
     "gsot_cache_clear": (C.c_int64, []),
     "gsot_set_params": (C.c_int, [_vp, C.c_double, C.c_double]),
     "gsot_set_upper_bound_offset": (C.c_int, [_vp, C.c_double]),
+    "gsot_sequential_sum": (C.c_int, [_vp, _vp, C.c_int64, C.c_double, _dp]),
     "gsot_shape": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _ip,
                              C.POINTER(C.c_int64)]),
     "gsot_eval": (C.c_int, [_vp, _vp, C.c_int, _dp, _vp, C.POINTER(CallStats)]),

@@ -125,6 +125,7 @@ gsot_ctx::~gsot_ctx() {
                   d_one, staging, d_bad};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (ex_ready) gsot::exact_ws_free(ex);
   if (h_sync) cudaFreeHost(h_sync);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -503,6 +504,7 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
                   const double* d_dir, double ub_offset, bool use_active, bool dbeta_ready) {
   const bool exact = (mode_flags & GSOT_EVAL_EXACT) != 0;
   const int mode = mode_flags & 1;
+  if (exact) c->ensure_exact();
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
   const DevProblem P = c->problem();
@@ -523,15 +525,18 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
                     ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
-                    exact ? nullptr : c->cmask, fused ? d_x : nullptr, fused ? c->snap_x : nullptr,
+                    c->cmask, fused ? d_x : nullptr, fused ? c->snap_x : nullptr,
                     fused ? 1 : 0, c->num_sms, c->stream);
     });
     words = c->words;
   }
-  if (exact) {  // reference-order sums (gsot_exact.cu); the screen only counts
+  if (exact) {  // the reference's order of operations (gsot_exact2.cu)
+    const bool scr = mode == GSOT_EVAL_SCREENED;
     c->launch(K_EVAL, 0.0, [&] {
-      launch_exact_eval(P, d_x, c->colpart, c->psi, d_grad, d_dir, c->sc,
-                        mode == GSOT_EVAL_SCREENED ? c->cnt_slots : nullptr, c->stream);
+      launch_exact_eval2(P, c->ex, d_x, scr ? c->words : c->dense_words,
+                         scr ? c->gmask : c->dense_gmask, scr ? c->cmask : c->dense_cmask,
+                         scr ? 1 : 0, d_grad, d_dir, c->sc, scr ? c->cnt_slots : nullptr,
+                         c->stream);
     });
     return;
   }
@@ -714,6 +719,31 @@ GSOT_API int gsot_create_shard_device(const double* d_cost, int64_t m, int64_t n
 GSOT_API void gsot_destroy(gsot_ctx* ctx) { park_or_delete(ctx); }
 
 GSOT_API int64_t gsot_cache_clear(void) { return static_cast<int64_t>(cache_drain()); }
+
+GSOT_API int gsot_sequential_sum(gsot_ctx* ctx, const double* terms, int64_t n, double s0,
+                                 double* out) {
+  return guard([&] {
+    checked(ctx);
+    if (n < 0 || (n > 0 && !terms) || !out) throw Error(GSOT_ERR_INVALID_ARGUMENT, "bad arguments");
+    ctx->ensure_exact();
+    double* d = dalloc<double>(static_cast<size_t>(n) + 1, nullptr);
+    double* r = dalloc<double>(1, nullptr);
+    try {
+      if (n > 0)
+        GSOT_CUDA_CHECK(cudaMemcpyAsync(d, terms, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                        ctx->stream));
+      ctx->launch(gsot::K_MISC, 8.0 * n, [&] { gsot::launch_seqsum(d, n, s0, ctx->ex, r, ctx->stream); });
+      GSOT_CUDA_CHECK(cudaMemcpyAsync(out, r, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+    } catch (...) {
+      cudaFree(d);
+      cudaFree(r);
+      throw;
+    }
+    cudaFree(d);
+    cudaFree(r);
+  });
+}
 
 GSOT_API int gsot_set_upper_bound_offset(gsot_ctx* ctx, double offset) {
   return guard([&] {

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "gsot_internal.cuh"
+#include "gsot_exact2.cuh"
 
 namespace gsot {
 
@@ -112,6 +113,9 @@ struct gsot_ctx {
   bool eval_recompute = false;  // k_eval<true>: some block is taller than a segment
   int eval_variant = 0;         // gsot::eval_variant (0 / 1 recompute / 2 short tiles)
   int red_blocks = 148 * 2;
+  // exact-order mode buffers (gsot_exact2.cu), allocated on first use
+  gsot::ExactWs ex;
+  bool ex_ready = false;
   // solver
   std::unique_ptr<gsot::SolverWorkspace> ws;
   uint64_t graph_epoch = 0;  // bumped when baked-in parameters change
@@ -147,6 +151,16 @@ struct gsot_ctx {
     P.half_inv_gamma = 0.5 / gamma;
     P.tl = tl;
     return P;
+  }
+
+  // Exact-order buffers (never during stream capture: the solver and the
+  // eval entry points call this before they enqueue).
+  void ensure_exact() {
+    if (ex_ready) return;
+    if (capturing) throw gsot::Error(GSOT_ERR_STATE, "exact-order buffers allocated during capture");
+    GSOT_CUDA_CHECK(cudaStreamSynchronize(stream));
+    gsot::exact_ws_alloc(ex, problem(), sizes, &bytes);
+    ex_ready = true;
   }
 
   cudaEvent_t take_event() {

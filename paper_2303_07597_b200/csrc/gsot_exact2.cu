@@ -1,0 +1,634 @@
+// gsot_exact2.cu — exact-order mode (GSOT_EVAL_EXACT / GSOT_SOLVE_EXACT) at
+// speed: every floating-point operation of the reference's hot path in the
+// reference's own order, so a device solve is bitwise the reference's
+// trajectory (tests/test_gpu_exact.py), without one-thread sequential loops.
+//
+//   k_ex_cols     one warp per 32-column chunk, walking the chunk's work
+//                 tiles in ascending group order: per block (lane = column)
+//                 z = pos_part_norm, the scale (1 - tau/z)/gamma and psi_block
+//                 with its dot / sq chains, all sequential over the block rows
+//                 (regularizer.hpp:23-91); the column sum of the plan entries
+//                 continues across the groups in row order, so
+//                 grad_beta_j = b_j - sum_entries(gcol_j) exactly
+//                 (dual.hpp:97-98). Nonzero blocks' psi are listed per column.
+//   k_ex_rows     one warp per 32-row slab of a group (lane = row), walking
+//                 the group's nonzero tiles in ascending column order:
+//                 grad_alpha_i = ((a_i - T_i0) - T_i1) - ...   (dual.hpp:91, :96).
+//   k_ex_scalars  cluster kernel: psi_sum in (j outer, l inner) order
+//                 (dual.hpp:44-50), alpha.a, beta.b (dual.hpp:51) and the
+//                 line-search slope grad.d (lbfgs.hpp:89) as four sequential
+//                 sums through the gsot_seqsum.cuh engine.
+//   k_ex_direction cluster kernel: the curvature pair and its test
+//                 (lbfgs.hpp:243-255) and the two-loop recursion (lbfgs.hpp:
+//                 109-126), every dot a sequential sum through the engine,
+//                 every vector update elementwise in the reference's order.
+//
+// Skipped and zero blocks contribute literal +0.0 (grad_block's zero fill,
+// psi_block's 0.0): adding or subtracting +0.0 leaves every partial sum
+// unchanged (they are never -0.0 under round-to-nearest), so the chains visit
+// only nonzero terms.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "gsot_device.cuh"
+#include "gsot_exact2.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gsot {
+
+using seq::Chain;
+using seq::EngineSmem;
+using seq::kClusterCtas;
+using seq::kThreads;
+
+// ---------------------------------------------------------------- columns
+
+__global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __restrict__ x,
+                                                 const uint32_t* __restrict__ words,
+                                                 uint32_t* __restrict__ cmask, int clear_cmask,
+                                                 double* __restrict__ scale_out,
+                                                 double* __restrict__ psiT, int* __restrict__ cntj,
+                                                 uint32_t* __restrict__ nzw,
+                                                 double* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (c >= P.nw) return;
+  const int64_t j = static_cast<int64_t>(c) * 32 + lane;
+  const bool valid = j < P.n;
+  const double bj = valid ? x[P.m + j] : 0.0;
+  const int nlw = (P.L + 31) / 32;
+  double colacc = 0.0;
+  int cnt = 0;
+  for (int w = 0; w < nlw; ++w) {
+    uint32_t mask = cmask[static_cast<int64_t>(c) * nlw + w];
+    if (clear_cmask) {
+      __syncwarp();
+      if (lane == 0) cmask[static_cast<int64_t>(c) * nlw + w] = 0u;  // consumed
+    }
+    while (mask) {
+      const int l = 32 * w + __ffs(mask) - 1;
+      mask &= mask - 1u;
+      const uint32_t sw = words[static_cast<int64_t>(l) * P.nw + c];
+      if (sw == 0u) continue;
+      const bool act = (sw >> lane) & 1u;
+      const int o0 = P.off[l], g = P.off[l + 1] - o0;
+      const double* __restrict__ al = x + o0;
+      const double* __restrict__ tp = P.C + 32 * (static_cast<int64_t>(P.nw) * o0 +
+                                                  static_cast<int64_t>(c) * g) + lane;
+      // pos_part_norm: acc += v * v over the rows, ascending (regularizer.hpp:23-30)
+      double z2 = 0.0;
+      int r = 0;
+      for (; r + 8 <= g; r += 8) {
+        double cv[8], av[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          cv[q] = act ? tp[32 * (r + q)] : 0.0;
+          av[q] = __ldg(al + r + q);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double f = residual(av[q], bj, cv[q]);
+          const double v = f > 0.0 ? f : 0.0;
+          z2 = dadd(z2, dmul(v, v));
+        }
+      }
+      for (; r < g; ++r) {
+        const double f = residual(__ldg(al + r), bj, act ? tp[32 * r] : 0.0);
+        const double v = f > 0.0 ? f : 0.0;
+        z2 = dadd(z2, dmul(v, v));
+      }
+      const double z = sqrt(z2);
+      const bool nz = act && z > P.tau;
+      const uint32_t nzword = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0) nzw[static_cast<int64_t>(l) * P.nw + c] = nzword;
+      if (nzword == 0u) continue;
+      // grad_block / psi_block (regularizer.hpp:64-91): scale, then one more
+      // pass for the plan entries, psi's dot / sq chains and the column sum
+      const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
+      double dot = 0.0, sq = 0.0;
+      r = 0;
+      for (; r + 8 <= g; r += 8) {
+        double cv[8], av[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          cv[q] = nz ? tp[32 * (r + q)] : 0.0;
+          av[q] = __ldg(al + r + q);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double f = residual(av[q], bj, cv[q]);
+          const double gg = f > 0.0 ? dmul(scale, f) : 0.0;
+          dot = dadd(dot, dmul(f, gg));
+          sq = dadd(sq, dmul(gg, gg));
+          if (f > 0.0) colacc = dadd(colacc, gg);
+        }
+      }
+      for (; r < g; ++r) {
+        const double f = residual(__ldg(al + r), bj, nz ? tp[32 * r] : 0.0);
+        const double gg = f > 0.0 ? dmul(scale, f) : 0.0;
+        dot = dadd(dot, dmul(f, gg));
+        sq = dadd(sq, dmul(gg, gg));
+        if (f > 0.0) colacc = dadd(colacc, gg);
+      }
+      if (nz) {
+        scale_out[static_cast<int64_t>(l) * P.n + j] = scale;
+        psiT[j * P.L + cnt] =
+            dsub(dot, dmul(P.gamma, dadd(dmul(0.5, sq), dmul(P.mu, sqrt(sq)))));
+        ++cnt;
+      }
+    }
+  }
+  if (valid) {
+    grad[P.m + j] = dsub(P.b[j], colacc);
+    cntj[j] = cnt;
+  }
+}
+
+// ---------------------------------------------------------------- rows
+
+__global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __restrict__ x,
+                                                 const uint32_t* __restrict__ words,
+                                                 const uint32_t* __restrict__ gmask,
+                                                 const uint32_t* __restrict__ nzw,
+                                                 const double* __restrict__ scale,
+                                                 const int4* __restrict__ slabs, int nslabs,
+                                                 double* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int sidx = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (sidx >= nslabs) return;
+  const int4 sl = slabs[sidx];
+  const int l = sl.x, r0 = sl.y, nr = sl.z;
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const bool valid = lane < nr;
+  const int64_t i = static_cast<int64_t>(o0) + r0 + lane;
+  const double ai = valid ? x[i] : 0.0;
+  double acc = valid ? P.a[i] : 0.0;  // grad_alpha = a (dual.hpp:91)
+  const int nmw = (P.nw + 31) / 32;
+  for (int w = 0; w < nmw; ++w) {
+    uint32_t cm = gmask[static_cast<int64_t>(l) * nmw + w];
+    while (cm) {
+      const int c = 32 * w + __ffs(cm) - 1;
+      cm &= cm - 1u;
+      const int64_t wi = static_cast<int64_t>(l) * P.nw + c;
+      const uint32_t nz = words[wi] & nzw[wi];
+      if (nz == 0u) continue;
+      const int64_t jk = static_cast<int64_t>(c) * 32 + lane;
+      const bool mine = (nz >> lane) & 1u;
+      const double bk = mine ? x[P.m + jk] : 0.0;
+      const double sk = mine ? scale[static_cast<int64_t>(l) * P.n + jk] : 0.0;
+      const double* __restrict__ row =
+          P.C + 32 * (static_cast<int64_t>(P.nw) * o0 + static_cast<int64_t>(c) * g + r0 + lane);
+      double cv[32];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 v = valid ? *reinterpret_cast<const double2*>(row + 2 * q)
+                                : make_double2(0.0, 0.0);
+        cv[2 * q] = v.x;
+        cv[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const double b = __shfl_sync(0xffffffffu, bk, k);
+        const double s = __shfl_sync(0xffffffffu, sk, k);
+        if ((nz >> k) & 1u) {  // grad_alpha -= gcol_j, j ascending (dual.hpp:96)
+          const double f = residual(ai, b, cv[k]);
+          if (f > 0.0) acc = dsub(acc, dmul(s, f));
+        }
+      }
+    }
+  }
+  if (valid) grad[i] = acc;
+}
+
+// ---------------------------------------------------------------- scalars
+
+struct ScalarArgs {
+  DevProblem P;
+  const double* x;
+  const double* grad;
+  const double* dvec;
+  const double* psiT;
+  const int* cntj;
+  int* lenC;
+  int* offC;
+  double* flat;
+  double* tv;
+  int64_t tv_stride;
+  seq::Scratch scr;
+  EvalScalars* sc;
+  unsigned long long* cnt_slots;
+};
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
+    k_ex_scalars(ScalarArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
+  __shared__ Chain ch[4];
+  cg::cluster_group cl = cg::this_cluster();
+  const DevProblem& P = A.P;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cta = static_cast<int>(cl.block_rank());
+  const int gw = cta * (kThreads / 32) + warp, gnw = kClusterCtas * (kThreads / 32);
+  const int64_t gt = static_cast<int64_t>(cta) * kThreads + threadIdx.x;
+  const int64_t gstride = static_cast<int64_t>(kClusterCtas) * kThreads;
+  const int64_t dim = P.m + P.n;
+  // 1. psi terms per chunk; dot terms (alpha_i * a_i, beta_j * b_j, grad_e * d_e)
+  for (int c = gw; c < P.nw; c += gnw) {
+    const int64_t j = static_cast<int64_t>(c) * 32 + lane;
+    int v = j < P.n ? A.cntj[j] : 0;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) A.lenC[c] = v;
+  }
+  double* t1 = A.tv;
+  double* t2 = A.tv + A.tv_stride;
+  double* t3 = A.tv + 2 * A.tv_stride;
+  for (int64_t e = gt; e < dim; e += gstride) {
+    if (e < P.m)
+      t1[e] = dmul(A.x[e], P.a[e]);  // s.alpha.dot(inst.a)
+    else
+      t2[e - P.m] = dmul(A.x[e], P.b[e - P.m]);  // s.beta.dot(inst.b)
+    if (A.dvec) t3[e] = dmul(A.grad[e], A.dvec[e]);  // p.grad.dot(d)
+  }
+  cl.sync();
+  // 2. chunk offsets of the psi chain (CTA 0)
+  if (cta == 0) {
+    __shared__ int wtot[kThreads / 32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < P.nw; base += kThreads) {
+      const int c = base + threadIdx.x;
+      const int v = c < P.nw ? __ldcg(A.lenC + c) : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wtot[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const int w = lane < kThreads / 32 ? wtot[lane] : 0;
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane >= o) wi += y;
+        }
+        if (lane < kThreads / 32) wtot[lane] = wi - w;
+      }
+      __syncthreads();
+      if (c < P.nw) A.offC[c] = carry + wtot[warp] + incl - v;
+      __syncthreads();
+      if (threadIdx.x == kThreads - 1) carry += wtot[warp] + incl;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) A.offC[P.nw] = carry;
+  }
+  cl.sync();
+  // 3. the psi chain terms in (j outer, l inner) order
+  for (int c = gw; c < P.nw; c += gnw) {
+    const int64_t j = static_cast<int64_t>(c) * 32 + lane;
+    const int v = j < P.n ? A.cntj[j] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int64_t pos = __ldcg(A.offC + c) + (incl - v);
+    for (int q = 0; q < v; ++q) A.flat[pos + q] = A.psiT[j * P.L + q];
+  }
+  cl.sync();
+  // 4. the four sequential sums
+  if (threadIdx.x == 0) {
+    const int64_t npsi = __ldcg(A.offC + P.nw);
+    ch[0] = seq::make_chain(A.flat, npsi, 0.0);
+    ch[1] = seq::make_chain(t1, P.m, 0.0);
+    ch[2] = seq::make_chain(t2, P.n, 0.0);
+    ch[3] = seq::make_chain(t3, A.dvec ? dim : 0, 0.0);
+  }
+  __syncthreads();
+  seq::engine(ch, A.dvec ? 4 : 3, A.scr, sm);
+  if (cta == 0) {
+    if (warp == 1 && A.cnt_slots) fold_counter_slots(A.cnt_slots, A.sc);  // screen counters
+    if (threadIdx.x == 0) {
+      const double psi_sum = sm.res[0], da = sm.res[1], db = sm.res[2];
+      A.sc->dot_aa = da;
+      A.sc->dot_bb = db;
+      A.sc->psi_sum = psi_sum;
+      A.sc->objective = dsub(dadd(da, db), psi_sum);  // dual.hpp:51
+      A.sc->slope = A.dvec ? sm.res[3] : 0.0;
+    }
+  }
+}
+
+template <typename T>
+static T* dalloc_raw(int64_t count, size_t* tally) {
+  T* p = nullptr;
+  if (count <= 0) count = 1;
+  GSOT_CUDA_CHECK(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+  if (tally) *tally += sizeof(T) * static_cast<size_t>(count);
+  return p;
+}
+
+void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>& sizes,
+                    size_t* tally) {
+  const int64_t Ln = static_cast<int64_t>(P.L) * P.n;
+  const int64_t dim = P.m + P.n;
+  w.scale = dalloc_raw<double>(Ln, tally);
+  w.psiT = dalloc_raw<double>(Ln, tally);
+  w.flat = dalloc_raw<double>(Ln, tally);
+  w.cntj = dalloc_raw<int>(P.n, tally);
+  w.nzw = dalloc_raw<uint32_t>(static_cast<int64_t>(P.L) * P.nw, tally);
+  w.lenC = dalloc_raw<int>(P.nw, tally);
+  w.offC = dalloc_raw<int>(P.nw + 1, tally);
+  w.tv_stride = (dim + 63) / 64 * 64;
+  w.tv = dalloc_raw<double>(4 * w.tv_stride, tally);
+  w.scr.segsum = dalloc_raw<double>(seq::kMaxChains * seq::kMaxSegs, tally);
+  w.scr.pieces = dalloc_raw<seq::Piece>(
+      static_cast<int64_t>(seq::kMaxChains) * seq::kMaxSegs * seq::kMaxPieces, tally);
+  w.scr.np = dalloc_raw<int>(seq::kMaxChains * seq::kMaxSegs, tally);
+  std::vector<int4> sl;
+  for (int32_t l = 0; l < P.L; ++l)
+    for (int32_t r = 0; r < sizes[l]; r += 32) sl.push_back(make_int4(l, r, std::min(32, sizes[l] - r), 0));
+  w.nslabs = static_cast<int>(sl.size());
+  w.slabs = dalloc_raw<int4>(w.nslabs, tally);
+  GSOT_CUDA_CHECK(cudaMemcpy(w.slabs, sl.data(), sizeof(int4) * sl.size(), cudaMemcpyHostToDevice));
+}
+
+void exact_ws_free(ExactWs& w) {
+  void* ptrs[] = {w.scale, w.psiT, w.flat, w.cntj, w.nzw, w.lenC, w.offC, w.tv,
+                  w.scr.segsum, w.scr.pieces, w.scr.np, w.slabs};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  w = ExactWs{};
+}
+
+static size_t engine_smem() { return sizeof(EngineSmem); }
+
+template <typename K, typename Arg>
+static void launch_cluster(K kern, const Arg& a, cudaStream_t s) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    GSOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(engine_smem())));
+    attr_done = true;
+  }
+  kern<<<kClusterCtas, kThreads, engine_smem(), s>>>(a);
+  GSOT_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
+                        const uint32_t* words, const uint32_t* gmask, uint32_t* cmask,
+                        int clear_cmask, double* grad, const double* dvec, EvalScalars* sc,
+                        unsigned long long* cnt_slots, cudaStream_t s) {
+  k_ex_cols<<<(P.nw + 3) / 4, 128, 0, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
+                                            W.cntj, W.nzw, grad);
+  k_ex_rows<<<(W.nslabs + 3) / 4, 128, 0, s>>>(P, x, words, gmask, W.nzw, W.scale, W.slabs,
+                                                W.nslabs, grad);
+  ScalarArgs A;
+  A.P = P;
+  A.x = x;
+  A.grad = grad;
+  A.dvec = dvec;
+  A.psiT = W.psiT;
+  A.cntj = W.cntj;
+  A.lenC = W.lenC;
+  A.offC = W.offC;
+  A.flat = W.flat;
+  A.tv = W.tv;
+  A.tv_stride = W.tv_stride;
+  A.scr = W.scr;
+  A.sc = sc;
+  A.cnt_slots = cnt_slots;
+  launch_cluster(k_ex_scalars, A, s);
+}
+
+// ---------------------------------------------------------------- direction
+
+struct DirKArgs {
+  ExactDirArgs a;
+  double* tv;
+  int64_t tv_stride;
+  seq::Scratch scr;
+};
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
+    k_ex_direction(DirKArgs K) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
+  __shared__ Chain ch[3];
+  __shared__ double a_loc[kMaxMemory];
+  __shared__ int kk, order[kMaxMemory + 1];
+  __shared__ double rho[kMaxMemory + 1], hsy[kMaxMemory + 1], hyy[kMaxMemory + 1];
+  cg::cluster_group cl = cg::this_cluster();
+  const ExactDirArgs& A = K.a;
+  const int cta = static_cast<int>(cl.block_rank());
+  const int64_t gt = static_cast<int64_t>(cta) * kThreads + threadIdx.x;
+  const int64_t gstride = static_cast<int64_t>(kClusterCtas) * kThreads;
+  const int64_t dim = A.dim;
+  double* t0 = K.tv;
+  double* t1 = K.tv + K.tv_stride;
+  double* t2 = K.tv + 2 * K.tv_stride;
+  HistState* H = A.h;
+
+  if (A.pair) {  // s = x_{k+1} - x_k, y = g_k - g_{k+1} (lbfgs.hpp:243-244)
+    const int scratch = *reinterpret_cast<volatile int*>(&H->scratch);
+    double* __restrict__ sv = A.S + scratch * A.stride;
+    double* __restrict__ yv = A.Y + scratch * A.stride;
+    for (int64_t e = gt; e < dim; e += gstride) {
+      const double s = dsub(A.x[e], A.xprev[e]);
+      const double y = dsub(A.gprev[e], A.g[e]);
+      sv[e] = s;
+      yv[e] = y;
+      t0[e] = dmul(s, y);
+      t1[e] = dmul(s, s);
+      t2[e] = dmul(y, y);
+    }
+    cl.sync();
+    if (threadIdx.x == 0) {
+      ch[0] = seq::make_chain(t0, dim, 0.0);
+      ch[1] = seq::make_chain(t1, dim, 0.0);
+      ch[2] = seq::make_chain(t2, dim, 0.0);
+    }
+    __syncthreads();
+    seq::engine(ch, 3, K.scr, sm);
+    if (cta == 0 && threadIdx.x == 0) {  // acceptance test and ring update (lbfgs.hpp:246-255)
+      const double sy = sm.res[0], ss = sm.res[1], yy = sm.res[2];
+      A.sc->extra[0] = sy;
+      A.sc->extra[1] = ss;
+      A.sc->extra[2] = yy;
+      H->last_sy = sy;
+      H->last_ss = ss;
+      H->last_yy = yy;
+      const bool accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);
+      H->accepted = accept ? 1 : 0;
+      if (accept) {
+        int k = H->k;
+        if (k == H->mem) {
+          const int ev = H->order[0];
+          for (int i = 1; i < k; ++i) {
+            H->order[i - 1] = H->order[i];
+            H->rho[i - 1] = H->rho[i];
+            H->sy[i - 1] = H->sy[i];
+            H->yy[i - 1] = H->yy[i];
+          }
+          --k;
+          H->order[k] = scratch;
+          H->scratch = ev;
+        } else {
+          H->order[k] = scratch;
+          int next = 0;
+          for (;; ++next) {
+            bool used = false;
+            for (int i = 0; i <= k; ++i) used |= H->order[i] == next;
+            if (!used) break;
+          }
+          H->scratch = next;
+        }
+        H->rho[k] = 1.0 / sy;
+        H->sy[k] = sy;
+        H->yy[k] = yy;
+        H->k = k + 1;
+      }
+      __threadfence();
+    }
+    cl.sync();
+  }
+  if (threadIdx.x == 0) {
+    volatile HistState* vh = H;
+    kk = vh->k;
+    for (int i = 0; i < kk; ++i) {
+      order[i] = vh->order[i];
+      rho[i] = vh->rho[i];
+      hsy[i] = vh->sy[i];
+      hyy[i] = vh->yy[i];
+    }
+  }
+  __syncthreads();
+  const int k = kk;
+  double* __restrict__ q = A.d;
+  // q = g; for i = k-1 .. 0: a_i = rho_i s_i.q; q -= a_i y_i   (lbfgs.hpp:109-115)
+  for (int i = k - 1; i >= 0; --i) {
+    const double* __restrict__ si = A.S + order[i] * A.stride;
+    const double* __restrict__ yp = i + 1 < k ? A.Y + order[i + 1] * A.stride : nullptr;
+    const double ap = i + 1 < k ? a_loc[i + 1] : 0.0;
+    for (int64_t e = gt; e < dim; e += gstride) {
+      const double qe = yp ? dsub(q[e], dmul(ap, yp[e])) : A.g[e];
+      q[e] = qe;
+      t0[e] = dmul(si[e], qe);
+    }
+    cl.sync();
+    if (threadIdx.x == 0) ch[0] = seq::make_chain(t0, dim, 0.0);
+    __syncthreads();
+    seq::engine(ch, 1, K.scr, sm);
+    if (threadIdx.x == 0) a_loc[i] = dmul(rho[i], sm.res[0]);
+    __syncthreads();
+    cl.sync();  // every CTA is done reading t0 before it is rewritten
+  }
+  // the pending q -= a_0 y_0 and the scaling q *= s.y / y.y (lbfgs.hpp:116-119),
+  // then for i = 0 .. k-1: b = rho_i y_i.q; q += (a_i - b) s_i  (lbfgs.hpp:120-124)
+  const double cscale = (k > 0 && hyy[k - 1] > 0.0) ? ddiv(hsy[k - 1], hyy[k - 1]) : 1.0;
+  const bool do_scale = k > 0 && hyy[k - 1] > 0.0;
+  double coef_prev = 0.0;
+  for (int i = 0; i <= k; ++i) {
+    // i < k: round i of the second loop; i == k: the final g.d, d.d
+    const double* __restrict__ yi = i < k ? A.Y + order[i] * A.stride : nullptr;
+    const double* __restrict__ sp = i > 0 ? A.S + order[i - 1] * A.stride : nullptr;
+    const double* __restrict__ y0 = k > 0 ? A.Y + order[0] * A.stride : nullptr;
+    const double a0 = k > 0 ? a_loc[0] : 0.0;
+    for (int64_t e = gt; e < dim; e += gstride) {
+      double qe;
+      if (k == 0) {
+        qe = A.g[e];  // d = g
+      } else if (i == 0) {
+        qe = dsub(q[e], dmul(a0, y0[e]));
+        if (do_scale) qe = dmul(qe, cscale);
+      } else {
+        qe = dadd(q[e], dmul(coef_prev, sp[e]));
+      }
+      q[e] = qe;
+      if (i < k) {
+        t0[e] = dmul(yi[e], qe);
+      } else {
+        t0[e] = dmul(A.g[e], qe);  // res.gradient.dot(d) (lbfgs.hpp:126)
+        t1[e] = dmul(qe, qe);      // d.squaredNorm() (d.norm(), lbfgs.hpp:152)
+      }
+    }
+    cl.sync();
+    if (threadIdx.x == 0) {
+      ch[0] = seq::make_chain(t0, dim, 0.0);
+      ch[1] = seq::make_chain(t1, dim, 0.0);
+    }
+    __syncthreads();
+    seq::engine(ch, i < k ? 1 : 2, K.scr, sm);
+    if (i < k) coef_prev = dsub(a_loc[i], dmul(rho[i], sm.res[0]));
+    __syncthreads();
+    if (i < k) cl.sync();
+  }
+  if (cta == 0 && threadIdx.x == 0) {
+    A.out[0] = sm.res[0];
+    A.out[1] = sm.res[1];
+  }
+}
+
+void launch_exact_direction(const ExactDirArgs& a, const ExactWs& W, cudaStream_t s) {
+  DirKArgs K;
+  K.a = a;
+  K.tv = W.tv;
+  K.tv_stride = W.tv_stride;
+  K.scr = W.scr;
+  launch_cluster(k_ex_direction, K, s);
+}
+
+// ---------------------------------------------------------------- dots / test hook
+
+struct DotArgs {
+  const double* a;
+  const double* b;  // null: sum of a
+  int64_t n;
+  double s0;
+  double* tv;
+  seq::Scratch scr;
+  double* out;
+};
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
+    k_ex_dot(DotArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
+  __shared__ Chain ch[1];
+  cg::cluster_group cl = cg::this_cluster();
+  const int cta = static_cast<int>(cl.block_rank());
+  const int64_t gt = static_cast<int64_t>(cta) * kThreads + threadIdx.x;
+  const int64_t gstride = static_cast<int64_t>(kClusterCtas) * kThreads;
+  const double* terms = A.a;
+  if (A.b) {
+    for (int64_t e = gt; e < A.n; e += gstride) A.tv[e] = dmul(A.a[e], A.b[e]);
+    terms = A.tv;
+  }
+  cl.sync();
+  if (threadIdx.x == 0) ch[0] = seq::make_chain(terms, A.n, A.s0);
+  __syncthreads();
+  seq::engine(ch, 1, A.scr, sm);
+  if (cta == 0 && threadIdx.x == 0) *A.out = sm.res[0];
+}
+
+void launch_exact_dot2(const double* a, const double* b, int64_t n, const ExactWs& W,
+                       EvalScalars* sc, int slot, cudaStream_t s) {
+  DotArgs A{a, b, n, 0.0, W.tv, W.scr, &sc->extra[slot]};
+  launch_cluster(k_ex_dot, A, s);
+}
+
+void launch_seqsum(const double* terms, int64_t n, double s0, const ExactWs& W, double* out,
+                   cudaStream_t s) {
+  DotArgs A{terms, nullptr, n, s0, W.tv, W.scr, out};
+  launch_cluster(k_ex_dot, A, s);
+}
+
+}  // namespace gsot

@@ -49,6 +49,7 @@ class Solver {
     exact_ = (o.flags & GSOT_SOLVE_EXACT) != 0;
     mode_eval_ = (screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE) | (exact_ ? GSOT_EVAL_EXACT : 0);
     mem_ = std::max(1, o.lbfgs_memory);
+    if (exact_) c_->ensure_exact();
     ensure_workspace();
     w_ = c_->ws.get();
     key_ = std::to_string(o.mode) + "/" + std::to_string(o.lbfgs_memory) + "/" +
@@ -262,8 +263,22 @@ class Solver {
   void enqueue_direction(bool pair, bool trial) {
     const int q = 1 - r_;
     if (exact_) {
-      if (pair) enqueue_pair();
-      enqueue_two_loop();
+      ExactDirArgs a;
+      a.pair = pair ? 1 : 0;
+      a.x = w_->X[r_];
+      a.xprev = w_->X[q];
+      a.g = w_->G[r_];
+      a.gprev = w_->G[q];
+      a.S = w_->S;
+      a.Y = w_->Y;
+      a.stride = w_->dim;
+      a.h = &c_->dsync->h;
+      a.d = w_->d;
+      a.dim = w_->dim;
+      a.out = c_->dsync->tl;
+      a.sc = c_->sc;
+      c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 10.0),
+                 [&] { launch_exact_direction(a, c_->ex, c_->stream); });
       if (trial)
         c_->launch(K_LBFGS, 24.0 * w_->dim, [&] {
           launch_axpy_point(w_->X[r_], t_one(), w_->d, w_->X[q], w_->dim, c_->m, c_->snap_x,
@@ -472,7 +487,7 @@ class Solver {
             c_->reset_scalars();
             c_->launch(K_LBFGS, 16.0 * w_->dim, [&] {
               if (exact_)
-                launch_exact_dot(w_->G[r_], w_->G[r_], w_->dim, c_->sc, 0, c_->stream);
+                launch_exact_dot2(w_->G[r_], w_->G[r_], w_->dim, c_->ex, c_->sc, 0, c_->stream);
               else
                 launch_dot(w_->G[r_], w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0,
                            c_->stream);

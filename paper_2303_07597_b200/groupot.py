@@ -377,6 +377,14 @@ class Context:
             cs.in_active, cs.skipped, cs.unskipped, cs.upper_bounds)
         return obj.value, g, st
 
+    def sequential_sum(self, terms, s0: float = 0.0) -> float:
+        """((s0 + t0) + t1) + ... exactly as a sequential loop rounds it, computed
+        by the device's exact-order engine (gsot_sequential_sum)."""
+        t = _f64(terms)
+        out = C.c_double()
+        _raise(_lib.lib().gsot_sequential_sum(self._h, _ptr(t), t.size, float(s0), C.byref(out)))
+        return out.value
+
     def set_upper_bound_offset(self, offset: float) -> None:
         _raise(_lib.lib().gsot_set_upper_bound_offset(self._h, float(offset)))
 

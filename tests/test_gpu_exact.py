@@ -125,3 +125,38 @@ def test_exact_solve_config2_full_budget_bitwise(o):
     plan = np.concatenate([ctx.plan_columns(r["x"], j, j + 1) for j in cols[:64]], axis=1)
     assert np.array_equal(plan, plan_o[:, :64])
     ctx.close()
+
+
+def _adversarial(rng, kind, n):
+    if kind == 0:  # half-ulp ties galore on a unit start
+        return rng.integers(-8, 9, size=n) * 2.0 ** -54 + (rng.random(n) < 0.01) * 1.0
+    if kind == 1:  # zeros mixed with normals
+        return np.where(rng.random(n) < 0.5, 0.0, rng.normal(size=n))
+    if kind == 2:  # few-bit terms over 60 binades, random signs
+        return ((rng.integers(0, 4, size=n) * 0.5 + 1) * 2.0 ** rng.integers(-60, 3, size=n)
+                * np.sign(rng.normal(size=n)))
+    if kind == 3:  # 1 then +-ulp-scale terms (ties at the binade top)
+        return np.concatenate([[1.0], rng.integers(-3, 4, size=n - 1) * 2.0 ** -53])
+    if kind == 4:  # subnormal scale
+        return rng.normal(size=n) * 1e-310
+    if kind == 5:  # cancellation: a random walk around zero
+        return rng.normal(size=n) * 10.0 ** rng.integers(-3, 3, size=n)
+    return rng.random(n)  # monotone growth
+
+
+@pytest.mark.parametrize("n", [1, 7, 300, 5000, 100_000, 1_200_000])
+def test_sequential_sum_engine_bitwise(n):
+    """gsot_sequential_sum (the exact-order engine, gsot_seqsum.cuh) equals the
+    left-to-right loop ((s0 + t0) + t1) + ... bit for bit on adversarial
+    inputs: exact ties, zeros, few-bit terms across 60 binades, subnormals,
+    cancellation around zero, monotone growth; several starts."""
+    ctx = G.Context.from_arrays(np.full((4, 3), 0.5), [4], np.full(4, 0.25), np.full(3, 1 / 3),
+                                1.0, 1.0)
+    rng = np.random.default_rng(n)
+    for kind in range(7):
+        v = _adversarial(rng, kind, n)
+        for s0 in (0.0, 1.0, -0.75, 1e-5):
+            ref = np.cumsum(np.concatenate([[s0], v]))[-1]  # sequential (np.add.accumulate)
+            got = ctx.sequential_sum(v, s0)
+            assert got == ref or (np.isnan(got) and np.isnan(ref)), (kind, s0, got, ref)
+    ctx.close()
