@@ -720,6 +720,10 @@ GSOT_API void gsot_destroy(gsot_ctx* ctx) { park_or_delete(ctx); }
 
 GSOT_API int64_t gsot_cache_clear(void) { return static_cast<int64_t>(cache_drain()); }
 
+extern "C" __attribute__((visibility("default"))) int gsot_debug_seq_prof(unsigned long long* out8) {
+  return guard([&] { gsot::read_seq_prof(out8); });
+}
+
 GSOT_API int gsot_sequential_sum(gsot_ctx* ctx, const double* terms, int64_t n, double s0,
                                  double* out) {
   return guard([&] {

@@ -349,10 +349,17 @@ void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>&
   w.offC = dalloc_raw<int>(P.nw + 1, tally);
   w.tv_stride = (dim + 63) / 64 * 64;
   w.tv = dalloc_raw<double>(4 * w.tv_stride, tally);
-  w.scr.segsum = dalloc_raw<double>(seq::kMaxChains * seq::kMaxSegs, tally);
-  w.scr.pieces = dalloc_raw<seq::Piece>(
-      static_cast<int64_t>(seq::kMaxChains) * seq::kMaxSegs * seq::kMaxPieces, tally);
-  w.scr.np = dalloc_raw<int>(seq::kMaxChains * seq::kMaxSegs, tally);
+  const int64_t NS = static_cast<int64_t>(seq::kMaxChains) * seq::kMaxSegs;
+  const int64_t NG = static_cast<int64_t>(seq::kMaxChains) * seq::kMaxGroups;
+  w.scr.segsum = dalloc_raw<double>(NS, tally);
+  w.scr.pieces = dalloc_raw<seq::Piece>(NS * seq::kMaxPieces, tally);
+  w.scr.np = dalloc_raw<int>(NS, tally);
+  w.scr.tail = dalloc_raw<int>(NS, tally);
+  w.scr.tailx = dalloc_raw<double>(NS, tally);
+  w.scr.gpieces = dalloc_raw<seq::Piece>(NG * seq::kMaxGPieces, tally);
+  w.scr.gnp = dalloc_raw<int>(NG, tally);
+  w.scr.gtail = dalloc_raw<int>(NG, tally);
+  w.scr.gtailx = dalloc_raw<double>(NG, tally);
   std::vector<int4> sl;
   for (int32_t l = 0; l < P.L; ++l)
     for (int32_t r = 0; r < sizes[l]; r += 32) sl.push_back(make_int4(l, r, std::min(32, sizes[l] - r), 0));
@@ -363,7 +370,8 @@ void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>&
 
 void exact_ws_free(ExactWs& w) {
   void* ptrs[] = {w.scale, w.psiT, w.flat, w.cntj, w.nzw, w.lenC, w.offC, w.tv,
-                  w.scr.segsum, w.scr.pieces, w.scr.np, w.slabs};
+                  w.scr.segsum, w.scr.pieces, w.scr.np, w.scr.tail, w.scr.tailx,
+                  w.scr.gpieces, w.scr.gnp, w.scr.gtail, w.scr.gtailx, w.slabs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   w = ExactWs{};
@@ -441,6 +449,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
     const int scratch = *reinterpret_cast<volatile int*>(&H->scratch);
     double* __restrict__ sv = A.S + scratch * A.stride;
     double* __restrict__ yv = A.Y + scratch * A.stride;
+#pragma unroll 4
     for (int64_t e = gt; e < dim; e += gstride) {
       const double s = dsub(A.x[e], A.xprev[e]);
       const double y = dsub(A.gprev[e], A.g[e]);
@@ -518,6 +527,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
     const double* __restrict__ si = A.S + order[i] * A.stride;
     const double* __restrict__ yp = i + 1 < k ? A.Y + order[i + 1] * A.stride : nullptr;
     const double ap = i + 1 < k ? a_loc[i + 1] : 0.0;
+#pragma unroll 4
     for (int64_t e = gt; e < dim; e += gstride) {
       const double qe = yp ? dsub(q[e], dmul(ap, yp[e])) : A.g[e];
       q[e] = qe;
@@ -542,6 +552,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
     const double* __restrict__ sp = i > 0 ? A.S + order[i - 1] * A.stride : nullptr;
     const double* __restrict__ y0 = k > 0 ? A.Y + order[0] * A.stride : nullptr;
     const double a0 = k > 0 ? a_loc[0] : 0.0;
+#pragma unroll 4
     for (int64_t e = gt; e < dim; e += gstride) {
       double qe;
       if (k == 0) {
@@ -629,6 +640,18 @@ void launch_seqsum(const double* terms, int64_t n, double s0, const ExactWs& W, 
                    cudaStream_t s) {
   DotArgs A{terms, nullptr, n, s0, W.tv, W.scr, out};
   launch_cluster(k_ex_dot, A, s);
+}
+
+// Diagnostic: the engine's phase clocks (-DGSOT_SEQ_PROF builds), 8 values,
+// then reset. Returns 0 values in product builds.
+void read_seq_prof(unsigned long long* out) {
+#ifdef GSOT_SEQ_PROF
+  cudaMemcpyFromSymbol(out, seq::g_seq_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(seq::g_seq_prof, z, sizeof(z));
+#else
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+#endif
 }
 
 }  // namespace gsot

@@ -63,4 +63,6 @@ void launch_exact_dot2(const double* a, const double* b, int64_t n, const ExactW
 void launch_seqsum(const double* terms, int64_t n, double s0, const ExactWs& W, double* out,
                    cudaStream_t s);
 
+void read_seq_prof(unsigned long long* out);
+
 }  // namespace gsot
