@@ -449,31 +449,24 @@ def configs_table(args, head_cfg: int, head: dict, clocks) -> dict:
                           "evals_per_s": r["calls"] / (r["ms"] / 1e3),
                           "iterations": r["iters"] / reps,
                           "blocks_computed_frac": r["blocks"] / (r["calls"] * ctx.L * ctx.n)}
+            if cfg in args.exact_configs:
+                table[key]["exact"] = exact_solve(ctx, iters, clocks)
         ctx.close()
         G.cache_clear()
     return table
 
 
-def parity_pinned(args, clocks) -> dict:
-    """Exact-order mode (GSOT_SOLVE_EXACT: the reference's own summation
-    order, bitwise the reference's trajectory, tests/test_gpu_exact.py):
-    its solve time on the configs it finishes within the bench's budget."""
-    import paper_2303_07597_b200 as G
-
-    out = {}
-    for cfg in args.exact_configs:
-        gamma, mu, iters = CONFIGS[cfg]
-        ctx = G.Context.from_config(cfg, cfg, gamma, mu)
-        kw = dict(solve_kw(iters), exact=True)
-        ctx.solve(**kw)
-        clocks.begin()
-        r = timed_solves(ctx, kw, 1)
-        clocks.end()
-        out[f"config{cfg}"] = {"solve_ms": r["ms"], "evals_per_s": r["calls"] / (r["ms"] / 1e3),
-                               "evals_per_solve": r["calls"], "iterations": r["iters"]}
-        ctx.close()
-        G.cache_clear()
-    return out
+def exact_solve(ctx, iters: int, clocks) -> dict:
+    """Exact-order mode (GSOT_SOLVE_EXACT: every sum in the reference's own
+    order, so the trajectory is bitwise the reference's -- tests/
+    test_gpu_exact.py): one warm-up and one timed solve on the context."""
+    kw = dict(solve_kw(iters), exact=True)
+    ctx.solve(**kw)
+    clocks.begin()
+    r = timed_solves(ctx, kw, 1)
+    clocks.end()
+    return {"solve_ms": r["ms"], "evals_per_s": r["calls"] / (r["ms"] / 1e3),
+            "evals_per_solve": r["calls"], "iterations": r["iters"]}
 
 
 def run_ours(args, world, rank, local, pg):
@@ -549,12 +542,15 @@ def run_ours(args, world, rank, local, pg):
                             f"stream, over a second pass of {nprof} solves (the value pass "
                             f"runs uninstrumented)"}
     m_, n_, L_ = ctx.m, ctx.n, ctx.L
+    # ---- the parity-pinned (exact-order, bitwise-reference) mode on this config
+    exact = exact_solve(ctx, iters, clocks) if cfg in args.exact_configs else None
     ctx.close()
     G.cache_clear()
 
-    # ---- all five configs, and the parity-pinned (exact-order) mode
+    # ---- all five configs (fast and exact-order mode)
     table = configs_table(args, cfg, head, clocks)
-    exact = parity_pinned(args, clocks)
+    if exact is not None and f"config{cfg}" in table:
+        table[f"config{cfg}"]["exact"] = exact
     clk = clocks.stop()
 
     # ---- e2e through the C ABI with host buffers
@@ -592,7 +588,11 @@ def run_ours(args, world, rank, local, pg):
         "kernels": kinds,
         "gpu_launches": launches,
         "configs": table,
-        "parity_pinned": exact,
+        "parity_pinned": None if exact is None else dict(
+            exact, mode="exact-order (GSOT_SOLVE_EXACT): the reference's own order of every "
+                        "floating-point operation; the solve is bitwise the reference's "
+                        "trajectory (tests/test_gpu_exact.py), unlike fast mode whose "
+                        "re-associated sums diverge on these unconverged solves"),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -762,7 +762,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--ref-reps", type=int, default=1)
     ap.add_argument("--exact-configs", type=lambda s: [int(c) for c in s.split(",") if c],
-                    default=[1])
+                    default=[1, 2, 3, 4, 5])
     ap.add_argument("--skip-large", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
