@@ -36,7 +36,8 @@
 
 #include "gsot.h"
 #if __has_include("groupot/bench.hpp")
-#include "groupot/bench.hpp"  // BenchRecord, GridSpec (run_grid)
+#include "groupot/bench.hpp"    // BenchRecord, GridSpec (run_grid)
+#include "groupot/data_io.hpp"  // LabeledSamples, UnlabeledSamples, partition_from_labels
 #define GSOT_B200_HAVE_BENCH 1
 #else
 #define GSOT_B200_HAVE_BENCH 0
@@ -90,11 +91,46 @@ class Device {
     check(gsot_create(inst.cost.data(), m_, n_, sizes.data(), static_cast<int32_t>(sizes.size()),
                       inst.a.data(), inst.b.data(), p.gamma(), p.mu(), &ctx_));
   }
+  // make_instance (data_io.hpp:157-181) straight into HBM: the cost of the
+  // samples (cost_matrix, data_io.hpp:101-123) is computed on the device,
+  // divided by its maximum when normalize_cost, with make_instance's
+  // marginals (uniform, or the normalised sample weights when use_weights)
+  // and partition_from_labels; validated like validate_instance. The
+  // m x n cost never exists on the host (gsot_create_features).
+  Device(const LabeledSamples& src, const UnlabeledSamples& tgt, bool normalize_cost,
+         bool use_weights, const RegParams& p)
+      : m_(src.features.rows()), n_(tgt.features.rows()) {
+    const Eigen::Index d = src.features.cols();
+    if (tgt.features.cols() != d)
+      throw InconsistentDimension(1, "target has " + std::to_string(tgt.features.cols()) +
+                                         " features, source has " + std::to_string(d));
+    const GroupPartition groups = partition_from_labels(src.labels);
+    std::vector<int32_t> sizes(groups.sizes().begin(), groups.sizes().end());
+    Eigen::VectorXd a, b;
+    if (use_weights && src.weights.size() == m_)
+      a = src.weights / src.weights.sum();
+    else
+      a = Eigen::VectorXd::Constant(m_, 1.0 / static_cast<double>(m_));
+    if (use_weights && tgt.weights.size() == n_)
+      b = tgt.weights / tgt.weights.sum();
+    else
+      b = Eigen::VectorXd::Constant(n_, 1.0 / static_cast<double>(n_));
+    std::vector<double> sf(static_cast<size_t>(m_ * d)), tf(static_cast<size_t>(n_ * d));
+    for (Eigen::Index i = 0; i < m_; ++i)  // row-major features
+      for (Eigen::Index k = 0; k < d; ++k) sf[static_cast<size_t>(i * d + k)] = src.features(i, k);
+    for (Eigen::Index j = 0; j < n_; ++j)
+      for (Eigen::Index k = 0; k < d; ++k) tf[static_cast<size_t>(j * d + k)] = tgt.features(j, k);
+    check(gsot_create_features(sf.data(), m_, tf.data(), n_, d, sizes.data(),
+                               static_cast<int32_t>(sizes.size()), a.data(), b.data(),
+                               normalize_cost ? 1 : 0, p.gamma(), p.mu(), &ctx_));
+  }
   ~Device() { gsot_destroy(ctx_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;
 
   gsot_ctx* handle() const { return ctx_; }
+  Eigen::Index m() const { return m_; }
+  Eigen::Index n() const { return n_; }
 
   // dual_objective (dual.hpp:38-52)
   double objective(const DualState& s) {
@@ -264,7 +300,7 @@ inline int mode_code(SolverMode mode) {
 
 // One solve on a resident instance (solver.hpp:92-293 through gsot_solve);
 // with_plan: recover the m x n plan into Solution::plan (finish_solution).
-inline Solution run_on(Device& dev, const ProblemInstance& inst, const SolverOptions& opts,
+inline Solution run_on(Device& dev, const SolverOptions& opts,
                        int mode, double ub_offset, AuditReport* report, bool with_plan) {
   gsot_solver_options o;
   gsot_default_solver_options(&o);
@@ -278,7 +314,7 @@ inline Solution run_on(Device& dev, const ProblemInstance& inst, const SolverOpt
             (mode == GSOT_MODE_AUDIT && opts.mode == SolverMode::fast_no_lower_bound
                  ? GSOT_SOLVE_NO_ACTIVE_SET
                  : 0);
-  const Eigen::Index m = inst.m(), n = inst.n();
+  const Eigen::Index m = dev.m(), n = dev.n();
   std::vector<double> x(static_cast<size_t>(m + n));
   // worst case per accepted iteration: two attempts of max_bracket (40) +
   // max_zoom (12) evaluations (lbfgs.hpp:11-30), plus the initial call
@@ -319,7 +355,7 @@ inline Solution run_on(Device& dev, const ProblemInstance& inst, const SolverOpt
 inline Solution run(const ProblemInstance& inst, const RegParams& p, const SolverOptions& opts,
                     int mode, double ub_offset, AuditReport* report) {
   Device dev(inst, p);
-  return run_on(dev, inst, opts, mode, ub_offset, report, true);
+  return run_on(dev, opts, mode, ub_offset, report, true);
 }
 
 }  // namespace detail
@@ -358,6 +394,21 @@ inline Solution solve(const ProblemInstance& inst, const RegParams& p,
   throw Error("unknown solver mode");
 }
 
+// solve (solver.hpp:284-293) on a resident device instance (e.g. built from
+// CSV samples with the Device(LabeledSamples, UnlabeledSamples, ...)
+// constructor): baseline, fast and fast_no_lower_bound; with_plan recovers
+// the m x n plan on the host.
+inline Solution solve(Device& dev, const SolverOptions& opts = {}, bool with_plan = false) {
+  int mode = GSOT_MODE_FAST;
+  switch (opts.mode) {
+    case SolverMode::baseline: mode = GSOT_MODE_BASELINE; break;
+    case SolverMode::fast: mode = GSOT_MODE_FAST; break;
+    case SolverMode::fast_no_lower_bound: mode = GSOT_MODE_FAST_NO_LOWER_BOUND; break;
+    case SolverMode::audit: mode = GSOT_MODE_AUDIT; break;
+  }
+  return detail::run_on(dev, opts, mode, 0.0, nullptr, with_plan);
+}
+
 // run_grid (bench.hpp:137-180): the (gamma, rho, mode) grid in the reference's
 // deterministic order, on ONE device context: the cost is uploaded and
 // validated once, each (gamma, rho) only swaps the parameters. Records carry
@@ -382,7 +433,7 @@ inline std::vector<BenchRecord> run_grid(
       for (const SolverMode mode : grid.modes) {
         SolverOptions opts = grid.base;
         opts.mode = mode;
-        Solution sol = detail::run_on(*dev, inst, opts, detail::mode_code(mode), 0.0, nullptr,
+        Solution sol = detail::run_on(*dev, opts, detail::mode_code(mode), 0.0, nullptr,
                                       with_plans);
         BenchRecord r;
         r.mode = to_string(mode);

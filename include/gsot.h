@@ -294,8 +294,21 @@ GSOT_API int gsot_config_features(int32_t cfg, uint64_t seed, double* src, doubl
  * row-major; d_cost device m x n column-major (caller-allocated). */
 GSOT_API int gsot_cost_matrix_device(const double* src, int64_t m, const double* tgt, int64_t n,
                                      int64_t d, int normalize, double* d_cost);
+/* make_instance (data_io.hpp:157-181) on the device: the cost of source
+ * features src (m x d row-major, rows grouped by class: group_sizes, the
+ * partition_from_labels of the sorted labels, data_io.hpp:127-152) and target
+ * features tgt (n x d row-major) is computed straight into HBM
+ * (cost_matrix, data_io.hpp:101-123, bitwise), divided by its maximum when
+ * normalize (and the maximum is > 0), and validated like gsot_create
+ * (validate_instance, core.hpp:117-139). a, b: the marginals make_instance
+ * chose (uniform, or the normalised sample weights). The cost never visits
+ * the host. */
+GSOT_API int gsot_create_features(const double* src, int64_t m, const double* tgt, int64_t n,
+                                  int64_t d, const int32_t* group_sizes, int32_t L,
+                                  const double* a, const double* b, int normalize, double gamma,
+                                  double mu, gsot_ctx** out);
 /* Build a context for config cfg directly on device (the cost never visits
- * the host). Also returns the host marginals/sizes if pointers non-NULL. */
+ * the host). */
 GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double mu,
                                 gsot_ctx** out);
 

@@ -161,6 +161,35 @@ int main() {
                 ref_rows.size(), dev_rows.size(), ints_equal, obj_equal, sparsity_equal, res_abs,
                 sink_calls, csv_fields);
   }
+  // CSV ingestion (data_io.hpp:270-352) -> make_instance on the device: the
+  // reference writes and reads the files, the adapter builds the instance
+  // from the samples on the GPU (the cost never on the host); exact-order
+  // solves of both are bitwise equal
+  {
+    const std::string sp = "/tmp/gsot_dropin_src.csv", tp = "/tmp/gsot_dropin_tgt.csv";
+    save_source_csv(src, sp);
+    save_target_csv(tgt, tp);
+    auto [s2, t2] = load_csv(sp, tp);
+    const ProblemInstance ri = make_instance(s2, t2, true);
+    b200::Device fdev(s2, t2, true, false, p);
+    SolverOptions so;
+    so.mode = SolverMode::fast;
+    so.max_outer_loops = 6;
+    so.grad_tol = 1e-12;
+    const Solution r = groupot::solve(ri, p, so);
+    b200::exact_order() = true;
+    const Solution d = b200::solve(fdev, so, true);
+    b200::exact_order() = false;
+    int x_equal = r.state.alpha.size() == d.state.alpha.size();
+    for (Eigen::Index i = 0; x_equal && i < r.state.alpha.size(); ++i)
+      x_equal = r.state.alpha[i] == d.state.alpha[i];
+    for (Eigen::Index j = 0; x_equal && j < r.state.beta.size(); ++j)
+      x_equal = r.state.beta[j] == d.state.beta[j];
+    std::printf(", \"csv_device\": {\"iters\": [%d, %d], \"x_equal\": %d, \"obj_equal\": %d, "
+                "\"plan_abs\": %.3e}",
+                r.iterations, d.iterations, x_equal, (int)(r.objective == d.objective),
+                max_abs_diff(r.plan.plan, d.plan.plan));
+  }
   // error behaviour: the same exception type and fields
   {
     ProblemInstance bad = inst;

@@ -296,6 +296,82 @@ int ref_time_eval(const double* cost, int64_t m, int64_t n, const int32_t* sizes
   }
 }
 
+// load_csv (data_io.hpp:270-352): shape query, then the data. Errors map to
+// status codes: 11 ParseError (detail line/col), 12 MissingLabelColumn,
+// 13 InconsistentDimension (detail line), 5 other Error; msg via
+// ref_last_error.
+int ref_load_csv(const char* src_path, const char* tgt_path, int64_t* shape /* m, n, d, sw, tw */,
+                 int64_t* detail /* line, column */, double* src_feat, int32_t* labels,
+                 double* src_w, double* tgt_feat, double* tgt_w) {
+  try {
+    auto [src, tgt] = load_csv(src_path, tgt_path);
+    shape[0] = src.features.rows();
+    shape[1] = tgt.features.rows();
+    shape[2] = src.features.cols();
+    shape[3] = src.weights.size();
+    shape[4] = tgt.weights.size();
+    if (src_feat)
+      for (Eigen::Index i = 0; i < src.features.rows(); ++i)
+        for (Eigen::Index k = 0; k < src.features.cols(); ++k)
+          src_feat[i * src.features.cols() + k] = src.features(i, k);
+    if (labels)
+      for (size_t i = 0; i < src.labels.size(); ++i) labels[i] = src.labels[i];
+    if (src_w)
+      for (Eigen::Index i = 0; i < src.weights.size(); ++i) src_w[i] = src.weights[i];
+    if (tgt_feat)
+      for (Eigen::Index i = 0; i < tgt.features.rows(); ++i)
+        for (Eigen::Index k = 0; k < tgt.features.cols(); ++k)
+          tgt_feat[i * tgt.features.cols() + k] = tgt.features(i, k);
+    if (tgt_w)
+      for (Eigen::Index i = 0; i < tgt.weights.size(); ++i) tgt_w[i] = tgt.weights[i];
+    return 0;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    detail[0] = e.line;
+    detail[1] = e.column;
+    return 11;
+  } catch (const MissingLabelColumn& e) {
+    g_err = e.what();
+    return 12;
+  } catch (const InconsistentDimension& e) {
+    g_err = e.what();
+    detail[0] = e.line;
+    return 13;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// make_instance (data_io.hpp:157-181) from the two CSV files: cost (m x n
+// column-major), a, b, group sizes (L, up to m entries).
+int ref_make_instance(const char* src_path, const char* tgt_path, int normalize, int use_weights,
+                      double* cost, double* a, double* b, int32_t* sizes, int32_t* L) {
+  try {
+    auto [src, tgt] = load_csv(src_path, tgt_path);
+    ProblemInstance inst = make_instance(src, tgt, normalize != 0, use_weights != 0);
+    std::memcpy(cost, inst.cost.data(), sizeof(double) * inst.cost.size());
+    std::memcpy(a, inst.a.data(), sizeof(double) * inst.a.size());
+    std::memcpy(b, inst.b.data(), sizeof(double) * inst.b.size());
+    *L = inst.groups.num_groups();
+    for (int l = 0; l < *L; ++l) sizes[l] = inst.groups.size(l);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// partition_from_labels (data_io.hpp:127-152): sizes into out (up to n).
+int ref_partition_from_labels(const int32_t* labels, int64_t n, int32_t* out, int32_t* L) {
+  try {
+    GroupPartition g = partition_from_labels(std::vector<int>(labels, labels + n));
+    *L = g.num_groups();
+    for (int l = 0; l < *L; ++l) out[l] = g.size(l);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 // solve(): mode 0 baseline, 1 fast, 2 fast-no-lb, 3 audit, 4 audit of fast-no-lb. out_scalars:
 // [objective, wall_seconds]; out_ints: [iterations, converged,
 // line_search_failed, outer_loops, grad_calls, in_active, skipped,

@@ -104,6 +104,9 @@ SIGNATURES = {
                                           _vp]),
     "gsot_create_config": (C.c_int, [C.c_int32, C.c_uint64, C.c_double, C.c_double,
                                      C.POINTER(_vp)]),
+    "gsot_create_features": (C.c_int, [_vp, C.c_int64, _vp, C.c_int64, C.c_int64, _vp, C.c_int32,
+                                       _vp, _vp, C.c_int, C.c_double, C.c_double,
+                                       C.POINTER(_vp)]),
     "gsot_profile_enable": (C.c_int, [_vp, C.c_int]),
     "gsot_profile_read": (C.c_int, [_vp, C.c_int, _dp, _dp, C.POINTER(C.c_int64)]),
     "gsot_profile_reset": (C.c_int, [_vp]),

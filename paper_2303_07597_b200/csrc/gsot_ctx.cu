@@ -1044,6 +1044,85 @@ GSOT_API int gsot_cost_matrix_device(const double* src, int64_t m, const double*
   });
 }
 
+namespace {
+// make_instance on the device (data_io.hpp:157-181): cost_matrix from the
+// features straight into the tiled layout (k-sequential, no FMA, bitwise the
+// reference's), C /= max(C) when normalize and max > 0, then
+// validate_instance (core.hpp:117-139) in the reference's order: the cost
+// scan (first offender, j-major), the marginals, the partition.
+gsot_ctx* create_from_features(const double* src, int64_t m, const double* tgt, int64_t n,
+                               int64_t d, const int32_t* sizes, int32_t L, const double* a,
+                               const double* b, bool normalize, double gamma, double mu) {
+  if (!src || !tgt || !sizes || !a || !b) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+  if (m <= 0 || n <= 0 || d <= 0) throw Error(GSOT_ERR_DIMENSION_MISMATCH, "empty instance");
+  auto* c = new gsot_ctx();
+  double *ds = nullptr, *dt = nullptr, *part = nullptr;
+  unsigned int* ticket = nullptr;
+  try {
+    setup_shape(c, m, n, sizes, L, gamma, mu);
+    if (c->off[L] != m)
+      throw Error(GSOT_ERR_PARTITION_MISMATCH,
+                  "group partition: partition covers " + std::to_string(c->off[L]) +
+                      " indices, cost has " + std::to_string(m) + " rows");
+    init_device(c);
+    alloc_buffers(c);
+    set_marginals(c, a, b);
+    GSOT_CUDA_CHECK(cudaMalloc(&ds, sizeof(double) * m * d));
+    GSOT_CUDA_CHECK(cudaMalloc(&dt, sizeof(double) * n * d));
+    GSOT_CUDA_CHECK(cudaMalloc(&part, sizeof(double) * (148 * 8 + 1)));
+    GSOT_CUDA_CHECK(cudaMalloc(&ticket, sizeof(unsigned int)));
+    GSOT_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), c->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(ds, src, sizeof(double) * m * d, cudaMemcpyHostToDevice,
+                                    c->stream));
+    GSOT_CUDA_CHECK(cudaMemcpyAsync(dt, tgt, sizeof(double) * n * d, cudaMemcpyHostToDevice,
+                                    c->stream));
+    const gsot::DevProblem TP = c->problem();
+    c->launch(gsot::K_MISC, 0, [&] { gsot::launch_cost_matrix(ds, m, dt, n, d, &TP, c->C, c->stream); });
+    if (normalize) {
+      // padding columns are zero (memset at allocation) and the max over the
+      // padded buffer is max(C) whenever max(C) >= 0
+      const int64_t count = static_cast<int64_t>(32) * c->nw * m;
+      c->launch(gsot::K_MISC, 0, [&] {
+        gsot::launch_max_reduce(c->C, count, part, 148 * 8, part + 148 * 8, ticket, c->stream);
+      });
+      c->launch(gsot::K_MISC, 0, [&] { gsot::launch_scale_div(c->C, count, part + 148 * 8, c->stream); });
+    }
+    if (!c->d_bad) GSOT_CUDA_CHECK(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
+    GSOT_CUDA_CHECK(cudaMemsetAsync(c->d_bad, 0xff, sizeof(unsigned long long), c->stream));
+    c->launch(gsot::K_MISC, 0, [&] { gsot::launch_scan_bad(TP, c->d_bad, c->stream); });
+    c->sync();
+    cudaFree(ds);
+    cudaFree(dt);
+    cudaFree(part);
+    cudaFree(ticket);
+    ds = dt = part = nullptr;
+    ticket = nullptr;
+    finish_validation(c, c->d_bad, a, b, nullptr);
+    c->cacheable = false;
+    return c;
+  } catch (...) {
+    if (ds) cudaFree(ds);
+    if (dt) cudaFree(dt);
+    if (part) cudaFree(part);
+    if (ticket) cudaFree(ticket);
+    delete c;
+    throw;
+  }
+}
+}  // namespace
+
+GSOT_API int gsot_create_features(const double* src, int64_t m, const double* tgt, int64_t n,
+                                  int64_t d, const int32_t* group_sizes, int32_t L,
+                                  const double* a, const double* b, int normalize, double gamma,
+                                  double mu, gsot_ctx** out) {
+  return guard([&] {
+    if (!out) throw Error(GSOT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    *out = create_from_features(src, m, tgt, n, d, group_sizes, L, a, b, normalize != 0, gamma,
+                                mu);
+  });
+}
+
 GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double mu,
                                 gsot_ctx** out) {
   return guard([&] {
@@ -1056,46 +1135,8 @@ GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double
     std::vector<double> a(static_cast<size_t>(m)), b(static_cast<size_t>(n));
     std::vector<int32_t> sizes(static_cast<size_t>(L));
     gsot::config_features(cfg, seed, src.data(), tgt.data(), sizes.data(), a.data(), b.data());
-    auto* c = new gsot_ctx();
-    try {
-      setup_shape(c, m, n, sizes.data(), L, gamma, mu);
-      init_device(c);
-      alloc_buffers(c);
-      set_marginals(c, a.data(), b.data());
-      double *ds = nullptr, *dt = nullptr, *part = nullptr;
-      unsigned int* ticket = nullptr;
-      GSOT_CUDA_CHECK(cudaMalloc(&ds, sizeof(double) * m * d));
-      GSOT_CUDA_CHECK(cudaMalloc(&dt, sizeof(double) * n * d));
-      GSOT_CUDA_CHECK(cudaMalloc(&part, sizeof(double) * (148 * 8 + 1)));
-      GSOT_CUDA_CHECK(cudaMalloc(&ticket, sizeof(unsigned int)));
-      GSOT_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), c->stream));
-      GSOT_CUDA_CHECK(cudaMemcpyAsync(ds, src.data(), sizeof(double) * m * d,
-                                      cudaMemcpyHostToDevice, c->stream));
-      GSOT_CUDA_CHECK(cudaMemcpyAsync(dt, tgt.data(), sizeof(double) * n * d,
-                                      cudaMemcpyHostToDevice, c->stream));
-      const gsot::DevProblem TP = c->problem();
-      c->launch(gsot::K_MISC, 0, [&] {
-        gsot::launch_cost_matrix(ds, m, dt, n, d, &TP, c->C, c->stream);
-      });
-      // padding rows are zero (memset at allocation) and C >= 0, so the max
-      // over the padded buffer is max(C).
-      const int64_t count = static_cast<int64_t>(32) * c->nw * m;
-      c->launch(gsot::K_MISC, 0, [&] {
-        gsot::launch_max_reduce(c->C, count, part, 148 * 8, part + 148 * 8, ticket, c->stream);
-      });
-      c->launch(gsot::K_MISC, 0, [&] { gsot::launch_scale_div(c->C, count, part + 148 * 8, c->stream); });
-      c->sync();
-      cudaFree(ds);
-      cudaFree(dt);
-      cudaFree(part);
-      cudaFree(ticket);
-      check_marginal(a.data(), m, 'a');
-      check_marginal(b.data(), n, 'b');
-      *out = c;
-    } catch (...) {
-      delete c;
-      throw;
-    }
+    *out = create_from_features(src.data(), m, tgt.data(), n, d, sizes.data(), L, a.data(),
+                                b.data(), true, gamma, mu);
   });
 }
 

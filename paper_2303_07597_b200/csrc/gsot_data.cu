@@ -304,6 +304,34 @@ __global__ void k_scale_div(double* __restrict__ C, int64_t count, const double*
     C[e] = __ddiv_rn(C[e], dv);
 }
 
+// validate_instance's cost scan (core.hpp:118-123) over the column-tiled
+// layout: the first entry in j-major order with !(c >= 0) || !isfinite(c),
+// as min(j * m + i) into *first_bad. Thread per (row, chunk): 32 columns.
+__global__ void __launch_bounds__(256) k_scan_bad(DevProblem P, unsigned long long* first_bad) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= P.m) return;
+  const int l = P.row_group[i];
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const double* row = P.C + 32 * ((int64_t)P.nw * o0 + (int64_t)c * g + (i - o0));
+  unsigned long long bad = ~0ull;
+  for (int k = 0; k < 32; ++k) {
+    const int64_t j = (int64_t)c * 32 + k;
+    if (j >= P.n) break;
+    const double v = row[k];
+    if (!(v >= 0.0) || !isfinite(v)) {
+      bad = (unsigned long long)(j * P.m + i);
+      break;
+    }
+  }
+  if (bad != ~0ull) atomicMin(first_bad, bad);
+}
+
+void launch_scan_bad(const DevProblem& P, unsigned long long* first_bad, cudaStream_t s) {
+  dim3 grid((unsigned)((P.m + 255) / 256), (unsigned)P.nw);
+  k_scan_bad<<<grid, 256, 0, s>>>(P, first_bad);
+}
+
 void launch_scale_div(double* C, int64_t count, const double* div, cudaStream_t s) {
   const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 32);
   k_scale_div<<<grid, 256, 0, s>>>(C, count, div);

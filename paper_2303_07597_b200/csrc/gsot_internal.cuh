@@ -272,6 +272,8 @@ void launch_cost_matrix(const double* src, int64_t m, const double* tgt, int64_t
 void launch_max_reduce(const double* C, int64_t count, double* partials, int nblocks,
                        double* out, unsigned int* ticket, cudaStream_t s);
 void launch_scale_div(double* C, int64_t count, const double* divisor, cudaStream_t s);
+// validate_instance's cost scan over the tiled layout: first offender (j*m+i).
+void launch_scan_bad(const DevProblem& P, unsigned long long* first_bad, cudaStream_t s);
 
 }  // namespace gsot
 

@@ -569,3 +569,57 @@ class ColumnParallelOracle:
         q = Problem(self.p.cost[:, cols], self.p.sizes, self.p.a, self.p.b[cols], self.p.gamma,
                     self.p.mu)
         return self.o.plan(q, x[:m], x[m:][cols])
+
+
+def ref_load_csv(src_path: str, tgt_path: str):
+    """The reference's load_csv (data_io.hpp:270-352) through ref_driver:
+    ('ok', src_features, labels, src_weights, tgt_features, tgt_weights) or
+    ('error', status, line, column, message)."""
+    lib = RefLib().lib
+    shape = np.zeros(5, np.int64)
+    det = np.zeros(2, np.int64)
+    st = lib.ref_load_csv(src_path.encode(), tgt_path.encode(), shape.ctypes.data_as(C.c_void_p),
+                          det.ctypes.data_as(C.c_void_p), None, None, None, None, None)
+    if st != 0:
+        return ("error", int(st), int(det[0]), int(det[1]), lib.ref_last_error().decode())
+    m, n, d, sw, tw = (int(v) for v in shape)
+    sf, tf = np.empty((m, d)), np.empty((n, d))
+    lab = np.empty(m, np.int32)
+    swv, twv = np.empty(max(sw, 1)), np.empty(max(tw, 1))
+    st = lib.ref_load_csv(src_path.encode(), tgt_path.encode(), shape.ctypes.data_as(C.c_void_p),
+                          det.ctypes.data_as(C.c_void_p), sf.ctypes.data_as(C.c_void_p),
+                          lab.ctypes.data_as(C.c_void_p), swv.ctypes.data_as(C.c_void_p),
+                          tf.ctypes.data_as(C.c_void_p), twv.ctypes.data_as(C.c_void_p))
+    assert st == 0
+    return ("ok", sf, lab.tolist(), swv[:sw], tf, twv[:tw])
+
+
+def ref_make_instance(src_path: str, tgt_path: str, m: int, n: int, normalize: bool,
+                      use_weights: bool):
+    """The reference's make_instance from the CSV pair: (cost, a, b, sizes)
+    or ('error', status, message)."""
+    lib = RefLib().lib
+    cost = np.empty(m * n)
+    a, b = np.empty(m), np.empty(n)
+    sizes = np.empty(m, np.int32)
+    L = C.c_int32()
+    st = lib.ref_make_instance(src_path.encode(), tgt_path.encode(), C.c_int(int(normalize)),
+                               C.c_int(int(use_weights)), cost.ctypes.data_as(C.c_void_p),
+                               a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                               sizes.ctypes.data_as(C.c_void_p), C.byref(L))
+    if st != 0:
+        return ("error", int(st), lib.ref_last_error().decode())
+    return cost.reshape(m, n, order="F"), a, b, sizes[: L.value]
+
+
+def ref_partition_from_labels(labels):
+    """('ok', sizes) or ('error', status, message)."""
+    lib = RefLib().lib
+    lab = np.ascontiguousarray(labels, np.int32)
+    out = np.empty(max(1, lab.size), np.int32)
+    L = C.c_int32()
+    st = lib.ref_partition_from_labels(lab.ctypes.data_as(C.c_void_p), C.c_int64(lab.size),
+                                       out.ctypes.data_as(C.c_void_p), C.byref(L))
+    if st != 0:
+        return ("error", int(st), lib.ref_last_error().decode())
+    return ("ok", out[: L.value].tolist())

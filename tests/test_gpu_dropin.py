@@ -42,5 +42,9 @@ def test_reference_api_through_the_adapter():
     assert g["rows"] == [12, 12] and g["sink_calls"] == 12 and g["csv_roundtrip"] == 1
     assert g["ints_equal"] == 1 and g["obj_equal"] == 1 and g["sparsity_equal"] == 1
     assert g["res_abs"] <= 1e-12
+    # CSV files -> load_csv -> the adapter's make_instance on the device
+    c = d["csv_device"]
+    assert c["iters"][0] == c["iters"][1] and c["x_equal"] == 1 and c["obj_equal"] == 1
+    assert c["plan_abs"] == 0.0
     assert d["negative_cost_fields"] == 1 and d["marginal_fields"] == 1
     assert d["audit_violation"] == 1
