@@ -39,10 +39,7 @@ namespace cg = cooperative_groups;
 
 namespace gsot {
 
-using seq::Chain;
-using seq::EngineSmem;
-using seq::kClusterCtas;
-using seq::kThreads;
+constexpr int kThreads = seq2::kT;
 
 // ---------------------------------------------------------------- columns
 
@@ -217,23 +214,20 @@ struct ScalarArgs {
   double* flat;
   double* tv;
   int64_t tv_stride;
-  seq::Scratch scr;
   EvalScalars* sc;
   unsigned long long* cnt_slots;
 };
 
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
-    k_ex_scalars(ScalarArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) k_ex_scalars(ScalarArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
-  __shared__ Chain ch[4];
+  seq2::Smem2& sm = *reinterpret_cast<seq2::Smem2*>(smem_raw);
   cg::cluster_group cl = cg::this_cluster();
   const DevProblem& P = A.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cta = static_cast<int>(cl.block_rank());
-  const int gw = cta * (kThreads / 32) + warp, gnw = kClusterCtas * (kThreads / 32);
+  const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
+  const int gw = cta * (kThreads / 32) + warp, gnw = ncta * (kThreads / 32);
   const int64_t gt = static_cast<int64_t>(cta) * kThreads + threadIdx.x;
-  const int64_t gstride = static_cast<int64_t>(kClusterCtas) * kThreads;
+  const int64_t gstride = static_cast<int64_t>(ncta) * kThreads;
   const int64_t dim = P.m + P.n;
   // 1. psi terms per chunk; dot terms (alpha_i * a_i, beta_j * b_j, grad_e * d_e)
   for (int c = gw; c < P.nw; c += gnw) {
@@ -303,17 +297,16 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
     const int64_t pos = __ldcg(A.offC + c) + (incl - v);
     for (int q = 0; q < v; ++q) A.flat[pos + q] = A.psiT[j * P.L + q];
   }
-  cl.sync();
-  // 4. the four sequential sums
   if (threadIdx.x == 0) {
     const int64_t npsi = __ldcg(A.offC + P.nw);
-    ch[0] = seq::make_chain(A.flat, npsi, 0.0);
-    ch[1] = seq::make_chain(t1, P.m, 0.0);
-    ch[2] = seq::make_chain(t2, P.n, 0.0);
-    ch[3] = seq::make_chain(t3, A.dvec ? dim : 0, 0.0);
+    sm.ch[0] = seq2::Chain2{A.flat, npsi, 0.0};
+    sm.ch[1] = seq2::Chain2{t1, P.m, 0.0};
+    sm.ch[2] = seq2::Chain2{t2, P.n, 0.0};
+    sm.ch[3] = seq2::Chain2{t3, A.dvec ? dim : 0, 0.0};
   }
-  __syncthreads();
-  seq::engine(ch, A.dvec ? 4 : 3, A.scr, sm);
+  cl.sync();
+  // 4. the four sequential sums
+  seq2::engine2(A.dvec ? 4 : 3, sm);
   if (cta == 0) {
     if (warp == 1 && A.cnt_slots) fold_counter_slots(A.cnt_slots, A.sc);  // screen counters
     if (threadIdx.x == 0) {
@@ -325,6 +318,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
       A.sc->slope = A.dvec ? sm.res[3] : 0.0;
     }
   }
+  cl.sync();  // no CTA exits while another may still read its shared memory
 }
 
 template <typename T>
@@ -348,18 +342,7 @@ void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>&
   w.lenC = dalloc_raw<int>(P.nw, tally);
   w.offC = dalloc_raw<int>(P.nw + 1, tally);
   w.tv_stride = (dim + 63) / 64 * 64;
-  w.tv = dalloc_raw<double>(4 * w.tv_stride, tally);
-  const int64_t NS = static_cast<int64_t>(seq::kMaxChains) * seq::kMaxSegs;
-  const int64_t NG = static_cast<int64_t>(seq::kMaxChains) * seq::kMaxGroups;
-  w.scr.segsum = dalloc_raw<double>(NS, tally);
-  w.scr.pieces = dalloc_raw<seq::Piece>(NS * seq::kMaxPieces, tally);
-  w.scr.np = dalloc_raw<int>(NS, tally);
-  w.scr.tail = dalloc_raw<int>(NS, tally);
-  w.scr.tailx = dalloc_raw<double>(NS, tally);
-  w.scr.gpieces = dalloc_raw<seq::Piece>(NG * seq::kMaxGPieces, tally);
-  w.scr.gnp = dalloc_raw<int>(NG, tally);
-  w.scr.gtail = dalloc_raw<int>(NG, tally);
-  w.scr.gtailx = dalloc_raw<double>(NG, tally);
+  w.tv = dalloc_raw<double>(kTermBufs * w.tv_stride, tally);
   std::vector<int4> sl;
   for (int32_t l = 0; l < P.L; ++l)
     for (int32_t r = 0; r < sizes[l]; r += 32) sl.push_back(make_int4(l, r, std::min(32, sizes[l] - r), 0));
@@ -369,26 +352,53 @@ void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>&
 }
 
 void exact_ws_free(ExactWs& w) {
-  void* ptrs[] = {w.scale, w.psiT, w.flat, w.cntj, w.nzw, w.lenC, w.offC, w.tv,
-                  w.scr.segsum, w.scr.pieces, w.scr.np, w.scr.tail, w.scr.tailx,
-                  w.scr.gpieces, w.scr.gnp, w.scr.gtail, w.scr.gtailx, w.slabs};
+  void* ptrs[] = {w.scale, w.psiT, w.flat, w.cntj, w.nzw, w.lenC, w.offC, w.tv, w.slabs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   w = ExactWs{};
 }
 
-static size_t engine_smem() { return sizeof(EngineSmem); }
-
+// One cluster of kThreads-thread CTAs: 16 CTAs where the device can co-schedule
+// a non-portable 16-CTA cluster of the kernel, else 8 (decided once per kernel).
 template <typename K, typename Arg>
 static void launch_cluster(K kern, const Arg& a, cudaStream_t s) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    GSOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(engine_smem())));
-    attr_done = true;
+  static int ncta = 0;
+  const int smem = static_cast<int>(sizeof(seq2::Smem2));
+  if (ncta == 0) {
+    ncta = 8;
+    GSOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = seq2::kMaxCtas;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(seq2::kMaxCtas);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1)
+        ncta = seq2::kMaxCtas;
+    }
+    (void)cudaGetLastError();
   }
-  kern<<<kClusterCtas, kThreads, engine_smem(), s>>>(a);
-  GSOT_CUDA_CHECK(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ncta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(ncta);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  GSOT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
 void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
@@ -411,7 +421,6 @@ void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
   A.flat = W.flat;
   A.tv = W.tv;
   A.tv_stride = W.tv_stride;
-  A.scr = W.scr;
   A.sc = sc;
   A.cnt_slots = cnt_slots;
   launch_cluster(k_ex_scalars, A, s);
@@ -423,34 +432,48 @@ struct DirKArgs {
   ExactDirArgs a;
   double* tv;
   int64_t tv_stride;
-  seq::Scratch scr;
 };
 
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
-    k_ex_direction(DirKArgs K) {
+// The pair test and the two-loop recursion on one cluster. Every vector is
+// split into CTA slices matching the engine's per-thread blocks (thread g owns
+// terms [g b, g b + b), b = ceil(dim / threads)), so the elementwise work of
+// a slice and the sequential sums over it need only CTA barriers; the dots'
+// terms alternate between two buffer sets (call parity): a remote CTA's
+// stitch may still read the previous call's terms.
+__global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
-  __shared__ Chain ch[3];
+  seq2::Smem2& sm = *reinterpret_cast<seq2::Smem2*>(smem_raw);
+  __shared__ HistState hs;
   __shared__ double a_loc[kMaxMemory];
-  __shared__ int kk, order[kMaxMemory + 1];
-  __shared__ double rho[kMaxMemory + 1], hsy[kMaxMemory + 1], hyy[kMaxMemory + 1];
   cg::cluster_group cl = cg::this_cluster();
   const ExactDirArgs& A = K.a;
-  const int cta = static_cast<int>(cl.block_rank());
-  const int64_t gt = static_cast<int64_t>(cta) * kThreads + threadIdx.x;
-  const int64_t gstride = static_cast<int64_t>(kClusterCtas) * kThreads;
+  const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
   const int64_t dim = A.dim;
-  double* t0 = K.tv;
-  double* t1 = K.tv + K.tv_stride;
-  double* t2 = K.tv + 2 * K.tv_stride;
+  const int64_t b = seq2::block_len(dim, ncta * kThreads);
+  const int64_t lo = min(dim, static_cast<int64_t>(cta) * kThreads * b);
+  const int64_t hi = min(dim, lo + kThreads * b);
   HistState* H = A.h;
+  int call = 0;
+  auto buf = [&](int q) { return K.tv + (static_cast<int64_t>(call & 1) * 3 + q) * K.tv_stride; };
+  // every CTA works on its own copy of the ring state (CTA 0 writes it back)
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(HistState) / 4); i += kThreads)
+    reinterpret_cast<int*>(&hs)[i] = reinterpret_cast<const volatile int*>(H)[i];
+  __syncthreads();
 
   if (A.pair) {  // s = x_{k+1} - x_k, y = g_k - g_{k+1} (lbfgs.hpp:243-244)
-    const int scratch = *reinterpret_cast<volatile int*>(&H->scratch);
+    const int scratch = hs.scratch;
     double* __restrict__ sv = A.S + scratch * A.stride;
     double* __restrict__ yv = A.Y + scratch * A.stride;
+    double* t0 = buf(0);
+    double* t1 = buf(1);
+    double* t2 = buf(2);
+    if (threadIdx.x == 0) {
+      sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
+      sm.ch[1] = seq2::Chain2{t1, dim, 0.0};
+      sm.ch[2] = seq2::Chain2{t2, dim, 0.0};
+    }
 #pragma unroll 4
-    for (int64_t e = gt; e < dim; e += gstride) {
+    for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
       const double s = dsub(A.x[e], A.xprev[e]);
       const double y = dsub(A.gprev[e], A.g[e]);
       sv[e] = s;
@@ -459,101 +482,96 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
       t1[e] = dmul(s, s);
       t2[e] = dmul(y, y);
     }
-    cl.sync();
-    if (threadIdx.x == 0) {
-      ch[0] = seq::make_chain(t0, dim, 0.0);
-      ch[1] = seq::make_chain(t1, dim, 0.0);
-      ch[2] = seq::make_chain(t2, dim, 0.0);
-    }
     __syncthreads();
-    seq::engine(ch, 3, K.scr, sm);
-    if (cta == 0 && threadIdx.x == 0) {  // acceptance test and ring update (lbfgs.hpp:246-255)
+    seq2::engine2(3, sm);
+    ++call;
+    if (threadIdx.x == 0) {  // acceptance test and ring update (lbfgs.hpp:246-255)
       const double sy = sm.res[0], ss = sm.res[1], yy = sm.res[2];
-      A.sc->extra[0] = sy;
-      A.sc->extra[1] = ss;
-      A.sc->extra[2] = yy;
-      H->last_sy = sy;
-      H->last_ss = ss;
-      H->last_yy = yy;
+      if (cta == 0) {
+        A.sc->extra[0] = sy;
+        A.sc->extra[1] = ss;
+        A.sc->extra[2] = yy;
+      }
+      hs.last_sy = sy;
+      hs.last_ss = ss;
+      hs.last_yy = yy;
       const bool accept = sy > 1e-10 * sqrt(ss) * sqrt(yy);
-      H->accepted = accept ? 1 : 0;
+      hs.accepted = accept ? 1 : 0;
       if (accept) {
-        int k = H->k;
-        if (k == H->mem) {
-          const int ev = H->order[0];
+        int k = hs.k;
+        if (k == hs.mem) {
+          const int ev = hs.order[0];
           for (int i = 1; i < k; ++i) {
-            H->order[i - 1] = H->order[i];
-            H->rho[i - 1] = H->rho[i];
-            H->sy[i - 1] = H->sy[i];
-            H->yy[i - 1] = H->yy[i];
+            hs.order[i - 1] = hs.order[i];
+            hs.rho[i - 1] = hs.rho[i];
+            hs.sy[i - 1] = hs.sy[i];
+            hs.yy[i - 1] = hs.yy[i];
           }
           --k;
-          H->order[k] = scratch;
-          H->scratch = ev;
+          hs.order[k] = scratch;
+          hs.scratch = ev;
         } else {
-          H->order[k] = scratch;
+          hs.order[k] = scratch;
           int next = 0;
           for (;; ++next) {
             bool used = false;
-            for (int i = 0; i <= k; ++i) used |= H->order[i] == next;
+            for (int i = 0; i <= k; ++i) used |= hs.order[i] == next;
             if (!used) break;
           }
-          H->scratch = next;
+          hs.scratch = next;
         }
-        H->rho[k] = 1.0 / sy;
-        H->sy[k] = sy;
-        H->yy[k] = yy;
-        H->k = k + 1;
+        hs.rho[k] = 1.0 / sy;
+        hs.sy[k] = sy;
+        hs.yy[k] = yy;
+        hs.k = k + 1;
       }
-      __threadfence();
     }
-    cl.sync();
-  }
-  if (threadIdx.x == 0) {
-    volatile HistState* vh = H;
-    kk = vh->k;
-    for (int i = 0; i < kk; ++i) {
-      order[i] = vh->order[i];
-      rho[i] = vh->rho[i];
-      hsy[i] = vh->sy[i];
-      hyy[i] = vh->yy[i];
+    __syncthreads();
+    if (cta == 0) {
+      for (int i = threadIdx.x; i < static_cast<int>(sizeof(HistState) / 4); i += kThreads)
+        reinterpret_cast<int*>(H)[i] = reinterpret_cast<const int*>(&hs)[i];
     }
   }
-  __syncthreads();
-  const int k = kk;
+  const int k = hs.k;
   double* __restrict__ q = A.d;
   // q = g; for i = k-1 .. 0: a_i = rho_i s_i.q; q -= a_i y_i   (lbfgs.hpp:109-115)
   for (int i = k - 1; i >= 0; --i) {
-    const double* __restrict__ si = A.S + order[i] * A.stride;
-    const double* __restrict__ yp = i + 1 < k ? A.Y + order[i + 1] * A.stride : nullptr;
+    const double* __restrict__ si = A.S + hs.order[i] * A.stride;
+    const double* __restrict__ yp = i + 1 < k ? A.Y + hs.order[i + 1] * A.stride : nullptr;
     const double ap = i + 1 < k ? a_loc[i + 1] : 0.0;
+    double* t0 = buf(0);
+    if (threadIdx.x == 0) sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
 #pragma unroll 4
-    for (int64_t e = gt; e < dim; e += gstride) {
+    for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
       const double qe = yp ? dsub(q[e], dmul(ap, yp[e])) : A.g[e];
       q[e] = qe;
       t0[e] = dmul(si[e], qe);
     }
-    cl.sync();
-    if (threadIdx.x == 0) ch[0] = seq::make_chain(t0, dim, 0.0);
     __syncthreads();
-    seq::engine(ch, 1, K.scr, sm);
-    if (threadIdx.x == 0) a_loc[i] = dmul(rho[i], sm.res[0]);
+    seq2::engine2(1, sm);
+    ++call;
+    if (threadIdx.x == 0) a_loc[i] = dmul(hs.rho[i], sm.res[0]);
     __syncthreads();
-    cl.sync();  // every CTA is done reading t0 before it is rewritten
   }
   // the pending q -= a_0 y_0 and the scaling q *= s.y / y.y (lbfgs.hpp:116-119),
   // then for i = 0 .. k-1: b = rho_i y_i.q; q += (a_i - b) s_i  (lbfgs.hpp:120-124)
-  const double cscale = (k > 0 && hyy[k - 1] > 0.0) ? ddiv(hsy[k - 1], hyy[k - 1]) : 1.0;
-  const bool do_scale = k > 0 && hyy[k - 1] > 0.0;
+  const double cscale = (k > 0 && hs.yy[k - 1] > 0.0) ? ddiv(hs.sy[k - 1], hs.yy[k - 1]) : 1.0;
+  const bool do_scale = k > 0 && hs.yy[k - 1] > 0.0;
   double coef_prev = 0.0;
   for (int i = 0; i <= k; ++i) {
     // i < k: round i of the second loop; i == k: the final g.d, d.d
-    const double* __restrict__ yi = i < k ? A.Y + order[i] * A.stride : nullptr;
-    const double* __restrict__ sp = i > 0 ? A.S + order[i - 1] * A.stride : nullptr;
-    const double* __restrict__ y0 = k > 0 ? A.Y + order[0] * A.stride : nullptr;
+    const double* __restrict__ yi = i < k ? A.Y + hs.order[i] * A.stride : nullptr;
+    const double* __restrict__ sp = i > 0 ? A.S + hs.order[i - 1] * A.stride : nullptr;
+    const double* __restrict__ y0 = k > 0 ? A.Y + hs.order[0] * A.stride : nullptr;
     const double a0 = k > 0 ? a_loc[0] : 0.0;
+    double* t0 = buf(0);
+    double* t1 = buf(1);
+    if (threadIdx.x == 0) {
+      sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
+      sm.ch[1] = seq2::Chain2{t1, dim, 0.0};
+    }
 #pragma unroll 4
-    for (int64_t e = gt; e < dim; e += gstride) {
+    for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
       double qe;
       if (k == 0) {
         qe = A.g[e];  // d = g
@@ -571,21 +589,16 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
         t1[e] = dmul(qe, qe);      // d.squaredNorm() (d.norm(), lbfgs.hpp:152)
       }
     }
-    cl.sync();
-    if (threadIdx.x == 0) {
-      ch[0] = seq::make_chain(t0, dim, 0.0);
-      ch[1] = seq::make_chain(t1, dim, 0.0);
-    }
     __syncthreads();
-    seq::engine(ch, i < k ? 1 : 2, K.scr, sm);
-    if (i < k) coef_prev = dsub(a_loc[i], dmul(rho[i], sm.res[0]));
-    __syncthreads();
-    if (i < k) cl.sync();
+    seq2::engine2(i < k ? 1 : 2, sm);
+    ++call;
+    if (i < k) coef_prev = dsub(a_loc[i], dmul(hs.rho[i], sm.res[0]));
   }
   if (cta == 0 && threadIdx.x == 0) {
     A.out[0] = sm.res[0];
     A.out[1] = sm.res[1];
   }
+  cl.sync();  // no CTA exits while another may still read its shared memory
 }
 
 void launch_exact_direction(const ExactDirArgs& a, const ExactWs& W, cudaStream_t s) {
@@ -593,7 +606,6 @@ void launch_exact_direction(const ExactDirArgs& a, const ExactWs& W, cudaStream_
   K.a = a;
   K.tv = W.tv;
   K.tv_stride = W.tv_stride;
-  K.scr = W.scr;
   launch_cluster(k_ex_direction, K, s);
 }
 
@@ -605,40 +617,38 @@ struct DotArgs {
   int64_t n;
   double s0;
   double* tv;
-  seq::Scratch scr;
   double* out;
 };
 
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kThreads)
-    k_ex_dot(DotArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) k_ex_dot(DotArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
-  __shared__ Chain ch[1];
+  seq2::Smem2& sm = *reinterpret_cast<seq2::Smem2*>(smem_raw);
   cg::cluster_group cl = cg::this_cluster();
-  const int cta = static_cast<int>(cl.block_rank());
-  const int64_t gt = static_cast<int64_t>(cta) * kThreads + threadIdx.x;
-  const int64_t gstride = static_cast<int64_t>(kClusterCtas) * kThreads;
+  const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
+  const int64_t b = seq2::block_len(A.n, ncta * kThreads);
+  const int64_t lo = min(A.n, static_cast<int64_t>(cta) * kThreads * b);
+  const int64_t hi = min(A.n, lo + kThreads * b);
   const double* terms = A.a;
   if (A.b) {
-    for (int64_t e = gt; e < A.n; e += gstride) A.tv[e] = dmul(A.a[e], A.b[e]);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) A.tv[e] = dmul(A.a[e], A.b[e]);
     terms = A.tv;
   }
-  cl.sync();
-  if (threadIdx.x == 0) ch[0] = seq::make_chain(terms, A.n, A.s0);
+  if (threadIdx.x == 0) sm.ch[0] = seq2::Chain2{terms, A.n, A.s0};
   __syncthreads();
-  seq::engine(ch, 1, A.scr, sm);
+  seq2::engine2(1, sm);
   if (cta == 0 && threadIdx.x == 0) *A.out = sm.res[0];
+  cl.sync();  // no CTA exits while another may still read its shared memory
 }
 
 void launch_exact_dot2(const double* a, const double* b, int64_t n, const ExactWs& W,
                        EvalScalars* sc, int slot, cudaStream_t s) {
-  DotArgs A{a, b, n, 0.0, W.tv, W.scr, &sc->extra[slot]};
+  DotArgs A{a, b, n, 0.0, W.tv, &sc->extra[slot]};
   launch_cluster(k_ex_dot, A, s);
 }
 
 void launch_seqsum(const double* terms, int64_t n, double s0, const ExactWs& W, double* out,
                    cudaStream_t s) {
-  DotArgs A{terms, nullptr, n, s0, W.tv, W.scr, out};
+  DotArgs A{terms, nullptr, n, s0, W.tv, out};
   launch_cluster(k_ex_dot, A, s);
 }
 

@@ -5,12 +5,15 @@
 #pragma once
 
 #include "gsot_internal.cuh"
-#include "gsot_seqsum.cuh"
+#include "gsot_seqsum2.cuh"
 
 namespace gsot {
 
 // Device buffers of the exact-order evaluation and direction (allocated on
 // the first exact-mode call of a context).
+// term buffers: two call parities x three chains (gsot_exact2.cu)
+constexpr int kTermBufs = 6;
+
 struct ExactWs {
   double* scale = nullptr;   // L x n: block scale (1 - tau/z)/gamma of nonzero blocks
   double* psiT = nullptr;    // n x L: per column, its nonzero blocks' psi in group order
@@ -19,11 +22,10 @@ struct ExactWs {
   int* lenC = nullptr;       // nw: psi terms per chunk
   int* offC = nullptr;       // nw + 1: their exclusive prefix
   double* flat = nullptr;    // psi chain terms in (j, l) order (at most L x n)
-  double* tv = nullptr;      // 4 x tv_stride: dot-chain terms
+  double* tv = nullptr;      // kTermBufs x tv_stride: dot-chain terms
   int64_t tv_stride = 0;
   int4* slabs = nullptr;     // 32-row slabs of the groups: {l, first row in group, rows, 0}
   int nslabs = 0;
-  seq::Scratch scr{};
 };
 
 void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>& sizes,

@@ -1,0 +1,474 @@
+// gsot_seqsum2.cuh — the reference's SEQUENTIAL floating-point sums in
+// parallel and bit for bit, latency-first (exact-order mode).
+//
+// Same arithmetic foundation as gsot_seqsum.cuh (translation invariance of a
+// run inside a binade; Piece, chain_piece, try_apply, compose), organised for
+// the shortest critical path on one thread-block cluster:
+//
+//   1. every thread of the cluster owns one contiguous block of b terms
+//      (b = ceil(len / threads)); approximate block sums, a CTA scan and one
+//      cluster barrier give each thread an approximate start s^ (thread 0:
+//      the exact start);
+//   2. each thread runs its block from s^ ("leaf"): at most kLeafCap runs in
+//      both mantissa parities, a run ending where a step leaves the allowed
+//      binades, that term kept inline as a serial term;
+//   3. lane 0 of each warp composes its 32 leaves into the warp's piece list
+//      (runs continued across leaves where the left end is a valid start of
+//      the right run), then one lane per chain composes the CTA's warp lists
+//      into the CTA's list;
+//   4. one more cluster barrier, then EVERY CTA stitches the CTA lists in
+//      order from the exact start (try_apply: an exact translation; inline
+//      serial terms: the reference's addition), so the result is in every
+//      CTA with no broadcast. A piece that does not apply, and serial terms
+//      not kept inline, are replayed with the reference's own additions.
+//
+// Every step of the stitch is either the reference's addition or an exact
+// translation, so the result is the sequential sum for any input; fallbacks
+// only cost time. Two cluster barriers per call.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "gsot_seqsum.cuh"
+
+namespace gsot {
+namespace seq2 {
+
+using seq::dbits;
+using seq::dinf;
+using seq::Piece;
+#ifdef GSOT_SEQ_PROF
+using seq::g_seq_prof;
+#endif
+
+constexpr int kT = 256;            // threads per CTA of the engine's kernels
+constexpr int kWarps = kT / 32;    // warps per CTA
+constexpr int kMaxCh = 4;          // chains per engine call
+constexpr int kMaxCtas = 16;       // cluster size (16 where the device allows, else 8)
+constexpr int kLeafCap = 2;        // runs per leaf (later terms of the leaf: replayed)
+constexpr int kWarpCap = 16;       // pieces per warp list (later terms of the warp: replayed)
+constexpr int kCtaCap = 64;        // pieces per CTA list (else the stitch takes the warp lists)
+constexpr int kBatch = 16;         // terms loaded per round trip by one thread
+constexpr int kStage = 9472;       // terms of a one-chain call's CTA slice staged in shared memory
+
+struct Chain2 {
+  const double* terms;
+  int64_t len;
+  double s0;
+};
+
+// A piece list's tail: nonzero serial terms after its last piece (>= 2:
+// replay them from memory; the value when exactly one).
+struct Tail {
+  int n;
+  double x;
+};
+
+// Dynamic shared memory of the engine's kernels.
+struct Smem2 {
+  Chain2 ch[kMaxCh];
+  double ctot[kMaxCh];                     // CTA approximate totals (read remotely)
+  double wsum[kMaxCh][kWarps];             // scan scratch: warp totals
+  Piece lp[kT][kLeafCap];                  // leaf runs (one chain at a time)
+  int lnp[kT];
+  Tail ltl[kT];
+  Piece wl[kMaxCh][kWarps][kWarpCap];      // warp lists
+  int wnp[kMaxCh][kWarps];
+  Tail wtl[kMaxCh][kWarps];
+  Piece cl[kMaxCh][kCtaCap];               // CTA lists (read remotely by the stitch)
+  int cnp[kMaxCh];                         // their length; -1: incomplete, use the warp lists
+  Tail ctl[kMaxCh];
+  Piece st[kMaxCh][kCtaCap];               // stitch: a remote CTA's list, staged
+  double res[kMaxCh];
+  double stage[kStage];                    // a one-chain call's CTA slice (coalesced copy)
+};
+static_assert(sizeof(Smem2) <= 227 * 1024, "engine shared memory exceeds the per-CTA limit");
+
+// One thread's block: at most kLeafCap runs (gsot_seqsum.cuh's LaneSpec, its
+// pieces in shared memory). Pieces carry absolute term indices.
+struct Leaf {
+  double s;                   // speculative value between runs
+  double st0, st1, t0, t1;    // open run
+  double lo0, hi0, lo1, hi1;  // min distance to the lower / upper bound of the current binade
+  double u2;                  // 2 ulp of the run start
+  long long bst;              // bits of the run start
+  double xpre;
+  int k0, np, npre;
+  bool open, ok1, full;
+  Piece* out;
+
+  __device__ __forceinline__ void init(double shat, Piece* o) {
+    s = shat;
+    open = full = false;
+    np = npre = 0;
+    xpre = 0.0;
+    out = o;
+  }
+  __device__ __forceinline__ void serial(double x) {
+    if (npre == 0) xpre = x;
+    ++npre;
+  }
+  __device__ __forceinline__ bool inside(double v) const {
+    const long long b = dbits(v);
+    const int ex = static_cast<int>((b >> 52) & 0x7ff);
+    return ((b ^ bst) >= 0) && ex > 54 && ex <= static_cast<int>((bst >> 52) & 0x7ff);
+  }
+  __device__ __forceinline__ bool try_open(int k) {
+    const int ex = static_cast<int>((dbits(s) >> 52) & 0x7ff);
+    if (ex <= 54 || ex >= 0x7fe) return false;  // zero, tiny or huge: serial term
+    bst = dbits(s);
+    const double u = __longlong_as_double(static_cast<long long>(ex - 52) << 52);
+    u2 = dadd(u, u);
+    const double a0 = fabs(s);
+    const double highb = __longlong_as_double(static_cast<long long>(ex + 1) << 52);
+    const double up = dadd(a0, u);
+    const double a1 = up < highb ? up : dsub(a0, u);
+    st0 = s;
+    st1 = s < 0.0 ? -a1 : a1;
+    t0 = st0;
+    t1 = st1;
+    lo0 = hi0 = lo1 = hi1 = dinf();
+    seq::LaneSpec::margins(t0, lo0, hi0);
+    seq::LaneSpec::margins(t1, lo1, hi1);
+    ok1 = true;
+    k0 = k;
+    open = true;
+    return true;
+  }
+  __device__ __forceinline__ void close(int k1) {
+    Piece& p = out[np++];
+    p.st[0] = st0;
+    p.st[1] = st1;
+    p.en[0] = t0;
+    p.en[1] = t1;
+    const double inf = dinf();
+    const bool v0 = lo0 >= u2 && hi0 >= u2;
+    const bool v1 = ok1 && lo1 >= u2 && hi1 >= u2;
+    p.dlo[0] = v0 ? dsub(u2, lo0) : inf;
+    p.dhi[0] = v0 ? dsub(hi0, u2) : -inf;
+    p.dlo[1] = v1 ? dsub(u2, lo1) : inf;
+    p.dhi[1] = v1 ? dsub(hi1, u2) : -inf;
+    p.xpre = xpre;
+    p.k0 = k0;
+    p.k1 = k1;
+    p.npre = npre;
+    p.pad = 0;
+    open = false;
+    npre = 0;
+    s = t0;
+    if (np == kLeafCap) full = true;
+  }
+  __device__ __forceinline__ void step(double x, int k) {
+    if (full || x == 0.0) return;  // +-0 terms leave every partial sum unchanged
+    if (!open && !try_open(k)) {
+      s = dadd(s, x);
+      serial(x);
+      return;
+    }
+    const double n0 = dadd(t0, x);
+    if (!inside(n0)) {  // the run ends; this term is serial
+      close(k);
+      s = n0;
+      serial(x);
+      return;
+    }
+    const double n1 = dadd(t1, x);
+    ok1 = ok1 && inside(n1);
+    t0 = n0;
+    t1 = n1;
+    seq::LaneSpec::margins(n0, lo0, hi0);
+    seq::LaneSpec::margins(n1, lo1, hi1);
+  }
+};
+
+// The reference's additions over v[k0, k1) by a whole warp (every lane
+// carries the same s), 128 terms per round trip; zero terms cost nothing.
+__device__ __forceinline__ double serial_warp4(double s, const double* __restrict__ v, int k0,
+                                               int k1) {
+  const int lane = threadIdx.x & 31;
+  for (int b = k0; b < k1; b += 128) {
+    double t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = b + 32 * j + lane;
+      t[j] = k < k1 ? __ldcg(v + k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      unsigned nzm = __ballot_sync(0xffffffffu, t[j] != 0.0);
+      while (nzm) {
+        const int q = __ffs(nzm) - 1;
+        nzm &= nzm - 1u;
+        s = dadd(s, __shfl_sync(0xffffffffu, t[j], q));
+      }
+    }
+  }
+  return s;
+}
+
+// Terms per thread of a chain of len terms over P threads: odd, so threads
+// reading their blocks from a staged slice hit distinct shared-memory banks.
+__host__ __device__ __forceinline__ int64_t block_len(int64_t len, int P) {
+  return ((len + P - 1) / P) | 1;
+}
+
+// Thread g's block of a chain of len terms over P threads.
+__device__ __forceinline__ void block_of(int64_t len, int P, int g, int64_t& k0, int64_t& k1) {
+  const int64_t b = block_len(len, P);
+  k0 = min(len, static_cast<int64_t>(g) * b);
+  k1 = min(len, k0 + b);
+}
+
+// The engine: called by every thread of every CTA of the cluster, with
+// sm.ch[0 .. nch) set and every chain's terms written and visible
+// cluster-wide. Results in sm.res[c] after the final __syncthreads.
+//
+// Reuse across calls: a remote CTA reads this CTA's ctot between barrier 1
+// and barrier 2 of a call, and its list (cl / cnp / ctl) after barrier 2
+// until it arrives at barrier 1 of the next call; this CTA rewrites ctot
+// only after barrier 2 and its list only after barrier 1 of the next call.
+// The stitch may replay any CTA's terms, so callers alternate term buffers
+// between consecutive calls (a buffer is rewritten only after the next
+// call's barrier 1).
+static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
+  const int P = ncta * kT;
+  const int g = cta * kT + static_cast<int>(threadIdx.x);
+  if (cta == 0 && threadIdx.x == 0) SEQ_CNT(7, 1);
+  SEQ_PROF_T(t_a);
+  // ---- 1. approximate block sums, CTA scan, CTA totals. A one-chain call
+  // whose CTA slice fits is first staged into shared memory with coalesced
+  // loads (per-thread blocks read from global memory touch one line per lane)
+  const int64_t slo = min(sm.ch[0].len, static_cast<int64_t>(cta) * kT * block_len(sm.ch[0].len, P));
+  const int64_t shi = min(sm.ch[0].len, slo + kT * block_len(sm.ch[0].len, P));
+  const bool staged = nch == 1 && shi - slo <= kStage;
+  if (staged) {
+    const double* __restrict__ src = sm.ch[0].terms + slo;
+    const int n = static_cast<int>(shi - slo);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n; i += kT) sm.stage[i] = __ldcg(src + i);
+    __syncthreads();
+  }
+  double excl[kMaxCh];
+#pragma unroll
+  for (int c = 0; c < kMaxCh; ++c) {
+    excl[c] = 0.0;
+    if (c >= nch) continue;
+    int64_t k0, k1;
+    block_of(sm.ch[c].len, P, g, k0, k1);
+    const double* __restrict__ v = sm.ch[c].terms;
+    double s = 0.0;
+    if (staged) {
+      for (int64_t k = k0; k < k1; ++k) s += sm.stage[k - slo];
+    } else {
+      for (int64_t kb = k0; kb < k1; kb += kBatch) {
+        double x[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) x[q] = kb + q < k1 ? __ldcg(v + kb + q) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) s += x[q];
+      }
+    }
+    double incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) sm.wsum[c][warp] = incl;
+    excl[c] = incl - s;
+  }
+  __syncthreads();
+  if (warp < nch) {  // warp c scans chain c's warp totals
+    const double w = lane < kWarps ? sm.wsum[warp][lane] : 0.0;
+    double wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kWarps) sm.wsum[warp][lane] = wi - w;
+    if (lane == kWarps - 1) sm.ctot[warp] = wi;
+  }
+  SEQ_PROF_T(t_b);
+  cl.sync();  // barrier 1: CTA totals visible cluster-wide
+  SEQ_PROF_T(t_c);
+  // ---- 2. leaf runs from the approximate starts; 3. warp lists (lane 0)
+  for (int c = 0; c < nch; ++c) {
+    double pre = lane < cta ? *cl.map_shared_rank(&sm.ctot[c], lane) : 0.0;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    const double shat = g == 0 ? sm.ch[c].s0 : sm.ch[c].s0 + (pre + (sm.wsum[c][warp] + excl[c]));
+    int64_t k0, k1;
+    block_of(sm.ch[c].len, P, g, k0, k1);
+    const double* __restrict__ v = sm.ch[c].terms;
+    Leaf lf;
+    lf.init(shat, sm.lp[threadIdx.x]);
+    if (staged) {
+      for (int64_t k = k0; k < k1; ++k) lf.step(sm.stage[k - slo], static_cast<int>(k));
+    } else {
+      for (int64_t kb = k0; kb < k1; kb += kBatch) {
+        double x[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) x[q] = kb + q < k1 ? __ldcg(v + kb + q) : 0.0;
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) lf.step(x[q], static_cast<int>(kb + q));
+      }
+    }
+    if (lf.open && !lf.full) lf.close(static_cast<int>(k1));
+    sm.lnp[threadIdx.x] = lf.np;
+    sm.ltl[threadIdx.x] = Tail{lf.full ? 2 : lf.npre, lf.xpre};
+    __syncwarp();
+    if (lane == 0) {  // the warp's list over its 32 leaves
+      int t;
+      double tx;
+      const int base = warp * 32;
+      sm.wnp[c][warp] = seq::compose(
+          32,
+          [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
+            nq = sm.lnp[base + q];
+            tq = sm.ltl[base + q].n;
+            xq = sm.ltl[base + q].x;
+            return sm.lp[base + q];
+          },
+          sm.wl[c][warp], kWarpCap, &t, &tx);
+      sm.wtl[c][warp] = Tail{t, tx};
+    }
+    __syncwarp();
+  }
+  SEQ_PROF_T(t_d);
+  __syncthreads();
+  if (warp < nch && lane == 0) {  // the CTA's list of chain c over its warp lists
+    const int c = warp;
+    int tot = 0;
+    for (int q = 0; q < kWarps; ++q) tot += sm.wnp[c][q];
+    if (tot <= kCtaCap) {  // fits without stopping (chaining only shortens it)
+      int t;
+      double tx;
+      sm.cnp[c] = seq::compose(
+          kWarps,
+          [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
+            nq = sm.wnp[c][q];
+            tq = sm.wtl[c][q].n;
+            xq = sm.wtl[c][q].x;
+            return sm.wl[c][q];
+          },
+          sm.cl[c], kCtaCap, &t, &tx);
+      sm.ctl[c] = Tail{t, tx};
+    } else {
+      sm.cnp[c] = -1;
+    }
+  }
+  SEQ_PROF_T(t_e);
+  cl.sync();  // barrier 2: CTA lists visible cluster-wide
+  SEQ_PROF_T(t_f);
+  // ---- 4. stitch (every CTA; warp c: chain c): each CTA's list (or, when it
+  // did not fit, each of its warp lists) staged into shared memory in one
+  // round trip, then applied in order
+  if (warp < nch) {
+    const int c = warp;
+    const Chain2 C = sm.ch[c];
+    const int64_t bt = block_len(C.len, P);  // terms per thread
+    double s = C.s0;
+    const bool prof = cta == 0 && lane == 0;
+    Piece* stg = sm.st[c];
+    // apply np staged pieces over terms [k, kend) and then the list's tail
+    unsigned long long t_apply = 0, t_replay = 0;
+    auto apply_list = [&](int np, Tail tl, int k, int kend) {
+      SEQ_PROF_T(ta0);
+#pragma unroll 2
+      for (int i = 0; i < np; ++i) {
+        // every field loaded before s is needed (the loads do not depend on
+        // s, so they overlap the previous piece's dependent chain)
+        const Piece& p = stg[i];
+        const double st0 = p.st[0], st1 = p.st[1], en0 = p.en[0], en1 = p.en[1];
+        const double lo0 = p.dlo[0], lo1 = p.dlo[1], hi0 = p.dhi[0], hi1 = p.dhi[1];
+        const double xpre = p.xpre;
+        const int npre = p.npre, pk0 = p.k0, pk1 = p.k1;
+        if (npre == 1) {
+          s = dadd(s, xpre);
+        } else if (npre > 1) {
+          if (prof && c == 0) {
+            SEQ_CNT(8, 1);
+            SEQ_CNT(9, pk0 - k);
+          }
+          s = serial_warp4(s, C.terms, k, pk0);
+        }
+        if (prof && c == 0) SEQ_CNT(npre == 0 ? 15 : 6, 1);
+        // try_apply (gsot_seqsum.cuh) on the loaded fields
+        const long long bs = dbits(s), b0 = dbits(st0);
+        const bool odd = ((bs ^ b0) & 1) != 0;
+        const double delta = dsub(s, odd ? st1 : st0);
+        const double sh = s < 0.0 ? -delta : delta;
+        const bool ok = (((bs ^ b0) >> 52) == 0) && sh >= (odd ? lo1 : lo0) && sh <= (odd ? hi1 : hi0);
+        if (ok) {
+          s = dadd(odd ? en1 : en0, delta);
+        } else {
+          s = serial_warp4(s, C.terms, pk0, pk1);
+        }
+        k = pk1;
+      }
+      SEQ_PROF_T(ta1);
+      if (tl.n == 1) {
+        s = dadd(s, tl.x);
+      } else if (tl.n > 1) {
+        if (prof) SEQ_CNT(10, 1);
+        s = serial_warp4(s, C.terms, k, kend);
+      }
+      SEQ_PROF_T(ta2);
+#ifdef GSOT_SEQ_PROF
+      t_apply += ta1 - ta0;
+      t_replay += ta2 - ta1;
+      if (prof) SEQ_CNT(12, np);
+#endif
+    };
+    // CTA r's list header and pieces: loaded into registers (in flight while
+    // the previous list is applied), then stored into staging buffer r & 1
+    for (int r = 0; r < ncta; ++r) {
+      const int np = *cl.map_shared_rank(&sm.cnp[c], r);
+      const Tail tl = *cl.map_shared_rank(&sm.ctl[c], r);
+      __syncwarp();
+      if (lane < np) stg[lane] = *cl.map_shared_rank(&sm.cl[c][lane], r);
+      if (lane + 32 < np) stg[lane + 32] = *cl.map_shared_rank(&sm.cl[c][lane + 32], r);
+      __syncwarp();
+      const int k0 = static_cast<int>(min(C.len, static_cast<int64_t>(r) * kT * bt));
+      const int k1 = static_cast<int>(min(C.len, static_cast<int64_t>(r + 1) * kT * bt));
+      if (np >= 0) {
+        apply_list(np, tl, k0, k1);
+        continue;
+      }
+      if (prof) SEQ_CNT(11, 1);
+      for (int w = 0; w < kWarps; ++w) {  // the CTA's list did not fit: its warp lists
+        const int wn = *cl.map_shared_rank(&sm.wnp[c][w], r);
+        const Tail wt = *cl.map_shared_rank(&sm.wtl[c][w], r);
+        __syncwarp();
+        if (lane < wn) stg[lane] = *cl.map_shared_rank(&sm.wl[c][w][lane], r);
+        __syncwarp();
+        const int w0 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32) * bt));
+        const int w1 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32 + 32) * bt));
+        apply_list(wn, wt, w0, w1);
+      }
+    }
+    if (lane == 0) sm.res[c] = s;
+#ifdef GSOT_SEQ_PROF
+    if (prof && c == 0) {
+      SEQ_CNT(13, t_apply);
+      SEQ_CNT(14, t_replay);
+    }
+#endif
+  }
+  SEQ_PROF_T(t_g);
+  __syncthreads();
+  SEQ_PROF_ADD(0, t_a, t_b);  // block sums + CTA scan
+  SEQ_PROF_ADD(1, t_b, t_c);  // barrier 1
+  SEQ_PROF_ADD(2, t_c, t_d);  // starts + leaf runs + warp lists
+  SEQ_PROF_ADD(3, t_d, t_e);  // CTA list
+  SEQ_PROF_ADD(4, t_e, t_f);  // barrier 2
+  SEQ_PROF_ADD(5, t_f, t_g);  // stitch (warp 0: chain 0)
+}
+
+}  // namespace seq2
+}  // namespace gsot
