@@ -144,6 +144,193 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
   }
 }
 
+// k_ex_cols2: the same computation, with each warp streaming its chunk's
+// tiles through its own TMA ring (cp.async.bulk of contiguous 32-row tile
+// segments and the matching alpha rows into shared memory, mbarrier
+// completion; lane 0 issues, every lane waits). A tile of at most kExD
+// segments stays resident for pass 2; a taller one is streamed again for
+// pass 2 only when it has a nonzero block. One CTA per SM, kExNW warps, each
+// an independent chunk owner (the column chains run across the groups of the
+// chunk in order). Requires L <= kExGmax (else k_ex_cols).
+constexpr int kExNW = 4;       // warps per CTA
+constexpr int kExD = 5;        // ring slots per warp
+constexpr int kExSR = 32;      // rows per segment
+constexpr int kExGmax = 1024;  // groups listed per chunk
+constexpr int kExAl = kExSR + 2;  // alpha slot (aligned superset), even
+
+struct alignas(128) ExColWarp {
+  double seg[kExD][kExSR * 32];
+  double al[kExD][kExAl];
+  uint64_t full[kExD];
+  int grp[kExGmax];
+  uint32_t gsw[kExGmax];
+};
+
+__global__ void __launch_bounds__(32 * kExNW, 1)
+    k_ex_cols2(DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
+               uint32_t* __restrict__ cmask, int clear_cmask, double* __restrict__ scale_out,
+               double* __restrict__ psiT, int* __restrict__ cntj, uint32_t* __restrict__ nzw,
+               double* __restrict__ grad) {
+  extern __shared__ __align__(128) unsigned char exc_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ExColWarp& W = reinterpret_cast<ExColWarp*>(exc_smem)[warp];
+  if (lane == 0) {
+    for (int q = 0; q < kExD; ++q) mbar_init(&W.full[q], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const int nlw = (P.L + 31) / 32;
+  uint32_t head = 0, tail = 0;  // ring: segments issued / consumed (this warp)
+  // issue segment s of tile (o0, g, c) into the next slot (lane 0)
+  auto issue = [&](int c, int o0, int g, int sgi) {
+    const int slot = head % kExD;
+    const int r0 = sgi * kExSR, rows = min(kExSR, g - r0);
+    const int64_t a0 = (o0 + r0) & ~1ll;
+    const uint32_t abytes = static_cast<uint32_t>(((o0 + r0 + rows - a0) + 1) & ~1ll) * 8u;
+    const double* tile = P.C + 32 * (static_cast<int64_t>(P.nw) * o0 + static_cast<int64_t>(c) * g);
+    mbar_expect_tx(&W.full[slot], static_cast<uint32_t>(rows) * 256u + abytes);
+    tma_load_1d(W.seg[slot], tile + static_cast<int64_t>(r0) * 32, static_cast<uint32_t>(rows) * 256u,
+                &W.full[slot]);
+    tma_load_1d(W.al[slot], x + a0, abytes, &W.full[slot]);
+    ++head;
+  };
+  for (int c = blockIdx.x * kExNW + warp; c < P.nw; c += gridDim.x * kExNW) {
+    const int64_t j = static_cast<int64_t>(c) * 32 + lane;
+    const bool valid = j < P.n;
+    const double bj = valid ? x[P.m + j] : 0.0;
+    // the chunk's surviving tiles in ascending group order
+    int ng = 0;
+    for (int w = 0; w < nlw; ++w) {
+      const uint32_t mask = cmask[static_cast<int64_t>(c) * nlw + w];
+      const int l = 32 * w + lane;
+      const uint32_t sw = (mask >> lane) & 1u ? words[static_cast<int64_t>(l) * P.nw + c] : 0u;
+      const uint32_t b = __ballot_sync(0xffffffffu, sw != 0u);
+      if (sw != 0u) {
+        const int pos = ng + __popc(b & ((1u << lane) - 1u));
+        W.grp[pos] = l;
+        W.gsw[pos] = sw;
+      }
+      ng += __popc(b);
+      if (clear_cmask && lane == 0 && mask) cmask[static_cast<int64_t>(c) * nlw + w] = 0u;  // consumed
+    }
+    __syncwarp();
+    // producer cursor (pt, ps): the next tile / pass-1 segment to issue, in
+    // consumption order. It never runs past a tall tile whose pass 1 is fully
+    // issued (stop_at) until that tile is done: its pass 2 comes next.
+    int pt = 0, ps = 0, stop_at = -1;
+    auto tile_geom = [&](int t, int& o0, int& g) {
+      const int l = W.grp[t];
+      o0 = __ldg(P.off + l);
+      g = __ldg(P.off + l + 1) - o0;
+    };
+    auto pump = [&](int cur) {
+      while (pt < ng && head - tail < static_cast<uint32_t>(kExD) && stop_at < cur) {
+        int o0, g;
+        tile_geom(pt, o0, g);
+        const int ns = (g + kExSR - 1) / kExSR;
+        if (lane == 0) {
+          issue(c, o0, g, ps);
+        } else {
+          ++head;
+        }
+        if (++ps == ns) {
+          ps = 0;
+          if (ns > kExD) stop_at = pt;
+          ++pt;
+        }
+      }
+    };
+    double colacc = 0.0;
+    int cnt = 0;
+    for (int t = 0; t < ng; ++t) {
+      const int l = W.grp[t];
+      const uint32_t sw = W.gsw[t];
+      const bool act = (sw >> lane) & 1u;
+      int o0, g;
+      tile_geom(t, o0, g);
+      const int ns = (g + kExSR - 1) / kExSR;
+      const bool resident = ns <= kExD;
+      // pass 1: pos_part_norm, acc += v * v over the rows, ascending
+      // (regularizer.hpp:23-30)
+      double z2 = 0.0;
+      for (int q = 0; q < ns; ++q) {
+        pump(t);
+        const uint32_t k = resident ? tail + q : tail;
+        mbar_wait(&W.full[k % kExD], (k / kExD) & 1u);
+        const double* __restrict__ sg = W.seg[k % kExD] + lane;
+        const double* __restrict__ as = W.al[k % kExD] + ((o0 + q * kExSR) & 1);
+        const int rows = min(kExSR, g - q * kExSR);
+#pragma unroll 8
+        for (int r = 0; r < rows; ++r) {
+          const double f = residual(as[r], bj, act ? sg[32 * r] : 0.0);
+          const double v = f > 0.0 ? f : 0.0;
+          z2 = dadd(z2, dmul(v, v));
+        }
+        if (!resident) {  // a tall tile's segment is released at once
+          __syncwarp();
+          ++tail;
+        }
+      }
+      const double z = sqrt(z2);
+      const bool nz = act && z > P.tau;
+      const uint32_t nzword = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0) nzw[static_cast<int64_t>(l) * P.nw + c] = nzword;
+      if (nzword != 0u) {
+        // grad_block / psi_block (regularizer.hpp:64-91): scale, then the plan
+        // entries, psi's dot / sq chains and the column sum
+        const double scale = nz ? ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma) : 0.0;
+        double dot = 0.0, sq = 0.0;
+        int issued = 0;  // a tall tile streamed again (the ring is empty here)
+        for (int q = 0; q < ns; ++q) {
+          uint32_t k = tail + q;
+          if (!resident) {
+            while (issued < ns && head - tail < static_cast<uint32_t>(kExD)) {
+              if (lane == 0) {
+                issue(c, o0, g, issued);
+              } else {
+                ++head;
+              }
+              ++issued;
+            }
+            k = tail;
+            mbar_wait(&W.full[k % kExD], (k / kExD) & 1u);
+          }
+          const double* __restrict__ sg = W.seg[k % kExD] + lane;
+          const double* __restrict__ as = W.al[k % kExD] + ((o0 + q * kExSR) & 1);
+          const int rows = min(kExSR, g - q * kExSR);
+#pragma unroll 8
+          for (int r = 0; r < rows; ++r) {
+            const double f = residual(as[r], bj, nz ? sg[32 * r] : 0.0);
+            const double gg = f > 0.0 ? dmul(scale, f) : 0.0;
+            dot = dadd(dot, dmul(f, gg));
+            sq = dadd(sq, dmul(gg, gg));
+            if (f > 0.0) colacc = dadd(colacc, gg);
+          }
+          if (!resident) {
+            __syncwarp();
+            ++tail;
+          }
+        }
+        if (nz) {
+          scale_out[static_cast<int64_t>(l) * P.n + j] = scale;
+          psiT[j * P.L + cnt] =
+              dsub(dot, dmul(P.gamma, dadd(dmul(0.5, sq), dmul(P.mu, sqrt(sq)))));
+          ++cnt;
+        }
+      }
+      if (resident) {
+        __syncwarp();
+        tail += ns;
+      }
+    }
+    if (valid) {
+      grad[P.m + j] = dsub(P.b[j], colacc);
+      cntj[j] = cnt;
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- rows
 
 __global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __restrict__ x,
@@ -405,8 +592,22 @@ void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
                         const uint32_t* words, const uint32_t* gmask, uint32_t* cmask,
                         int clear_cmask, double* grad, const double* dvec, EvalScalars* sc,
                         unsigned long long* cnt_slots, cudaStream_t s) {
-  k_ex_cols<<<(P.nw + 3) / 4, 128, 0, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
-                                            W.cntj, W.nzw, grad);
+  if (P.L <= kExGmax) {
+    static int nsm = 0;
+    const int smem = static_cast<int>(sizeof(ExColWarp) * kExNW);
+    if (nsm == 0) {
+      GSOT_CUDA_CHECK(cudaFuncSetAttribute(k_ex_cols2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      int dev = 0;
+      GSOT_CUDA_CHECK(cudaGetDevice(&dev));
+      GSOT_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int grid = std::min(nsm, (P.nw + kExNW - 1) / kExNW);
+    k_ex_cols2<<<grid, 32 * kExNW, smem, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
+                                              W.cntj, W.nzw, grad);
+  } else {
+    k_ex_cols<<<(P.nw + 3) / 4, 128, 0, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
+                                              W.cntj, W.nzw, grad);
+  }
   k_ex_rows<<<(W.nslabs + 3) / 4, 128, 0, s>>>(P, x, words, gmask, W.nzw, W.scale, W.slabs,
                                                 W.nslabs, grad);
   ScalarArgs A;

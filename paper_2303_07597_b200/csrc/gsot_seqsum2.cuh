@@ -376,7 +376,9 @@ static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
     const bool prof = cta == 0 && lane == 0;
     Piece* stg = sm.st[c];
     // apply np staged pieces over terms [k, kend) and then the list's tail
+#ifdef GSOT_SEQ_PROF
     unsigned long long t_apply = 0, t_replay = 0;
+#endif
     auto apply_list = [&](int np, Tail tl, int k, int kend) {
       SEQ_PROF_T(ta0);
 #pragma unroll 2
