@@ -45,11 +45,11 @@ constexpr int kT = 256;            // threads per CTA of the engine's kernels
 constexpr int kWarps = kT / 32;    // warps per CTA
 constexpr int kMaxCh = 4;          // chains per engine call
 constexpr int kMaxCtas = 16;       // cluster size (16 where the device allows, else 8)
-constexpr int kLeafCap = 2;        // runs per leaf (later terms of the leaf: replayed)
+constexpr int kLeafCap = 4;        // runs per leaf (later terms of the leaf: replayed)
 constexpr int kWarpCap = 16;       // pieces per warp list (later terms of the warp: replayed)
 constexpr int kCtaCap = 64;        // pieces per CTA list (else the stitch takes the warp lists)
 constexpr int kBatch = 16;         // terms loaded per round trip by one thread
-constexpr int kStage = 9472;       // terms of a one-chain call's CTA slice staged in shared memory
+constexpr int kStage = 3328;       // terms of a one-chain call's CTA slice staged in shared memory
 
 struct Chain2 {
   const double* terms;
@@ -206,6 +206,37 @@ __device__ __forceinline__ double serial_warp4(double s, const double* __restric
   return s;
 }
 
+// kBatch terms v[kb, kb + kBatch) (zeros past k1), with 16-byte loads where
+// the batch is whole (v 16-byte aligned): half the L1 wavefronts of a warp
+// whose lanes read distinct blocks.
+__device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t kb, int64_t k1,
+                                           double (&x)[kBatch]) {
+  if (kb + kBatch <= k1) {
+    if ((kb & 1) == 0) {
+      const double2* p = reinterpret_cast<const double2*>(v + kb);
+#pragma unroll
+      for (int q = 0; q < kBatch / 2; ++q) {
+        const double2 t = __ldcg(p + q);
+        x[2 * q] = t.x;
+        x[2 * q + 1] = t.y;
+      }
+    } else {
+      x[0] = __ldcg(v + kb);
+      const double2* p = reinterpret_cast<const double2*>(v + kb + 1);
+#pragma unroll
+      for (int q = 0; q < kBatch / 2 - 1; ++q) {
+        const double2 t = __ldcg(p + q);
+        x[1 + 2 * q] = t.x;
+        x[2 + 2 * q] = t.y;
+      }
+      x[kBatch - 1] = __ldcg(v + kb + kBatch - 1);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) x[q] = kb + q < k1 ? __ldcg(v + kb + q) : 0.0;
+  }
+}
+
 // Terms per thread of a chain of len terms over P threads: odd, so threads
 // reading their blocks from a staged slice hit distinct shared-memory banks.
 __host__ __device__ __forceinline__ int64_t block_len(int64_t len, int P) {
@@ -266,8 +297,7 @@ static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
     } else {
       for (int64_t kb = k0; kb < k1; kb += kBatch) {
         double x[kBatch];
-#pragma unroll
-        for (int q = 0; q < kBatch; ++q) x[q] = kb + q < k1 ? __ldcg(v + kb + q) : 0.0;
+        load_batch(v, kb, k1, x);
 #pragma unroll
         for (int q = 0; q < kBatch; ++q) s += x[q];
       }
@@ -312,8 +342,7 @@ static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
     } else {
       for (int64_t kb = k0; kb < k1; kb += kBatch) {
         double x[kBatch];
-#pragma unroll
-        for (int q = 0; q < kBatch; ++q) x[q] = kb + q < k1 ? __ldcg(v + kb + q) : 0.0;
+        load_batch(v, kb, k1, x);
 #pragma unroll
         for (int q = 0; q < kBatch; ++q) lf.step(x[q], static_cast<int>(kb + q));
       }
