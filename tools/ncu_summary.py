@@ -1,11 +1,12 @@
 """Summarise ncu captures from gpurun_out/ into profiles/ (committed evidence).
 
-    python tools/ncu_summary.py TAG
+    python tools/ncu_summary.py TAG [--cmd "..."] [--full PROF_TAG ...] [--traffic-cfg C]
 
 Reads gpurun_out/launches_TAG.csv (gpu__time_duration + dram bytes per launch,
-cold-cache, serialised) and gpurun_out/prof_TAG.ncu-rep (--set full), writes
-profiles/ncu_TAG.md and profiles/ncu_traffic.json (per-kernel DRAM bytes per
-launch, read by bench.py's roofline.traffic).
+cold-cache, serialised) and gpurun_out/prof_<PROF_TAG>.ncu-rep (--set full
+captures), writes profiles/ncu_TAG.md and, with --traffic-cfg C,
+profiles/ncu_traffic_cfgC.json (per-kernel DRAM bytes per launch of the full
+captures, read by bench.py's roofline.traffic).
 """
 from __future__ import annotations
 
@@ -79,13 +80,20 @@ def full(tag: str):
 
 
 def main():
-    tag = sys.argv[1]
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("tag")
+    ap.add_argument("--cmd", default="python bench.py --steps 1 --warmup 1 --no-cpu-baseline")
+    ap.add_argument("--full", nargs="*", default=None)
+    ap.add_argument("--traffic-cfg", type=int, default=None)
+    args = ap.parse_args()
+    tag = args.tag
     agg = launches(tag)
     tot = sum(a["us"] for a in agg.values())
     lines = [f"# ncu summary `{tag}`", "",
-             "Command: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline` (config 2; the "
-             "launch list covers setup + the first solves; per-launch times are cold-cache and "
-             "serialised: compare shares, not absolutes).", "",
+             f"Command: `{args.cmd}` (per-launch times are cold-cache and serialised under ncu: "
+             "compare shares, not absolutes).", "",
              "| kernel | launches | total us | mean us | share | DRAM read MB/launch | DRAM write MB/launch |",
              "|---|---|---|---|---|---|---|"]
     traffic = {}
@@ -95,7 +103,9 @@ def main():
                      f"{a['read'] / n / 1e6:.3f} | {a['write'] / n / 1e6:.3f} |")
         traffic[k] = {"dram_bytes_per_launch": (a["read"] + a["write"]) / n, "launches": n,
                       "mean_us": a["us"] / n, "source": f"profiles/ncu_{tag}.md"}
-    fl = full(tag)
+    fl = []
+    for ft in (args.full if args.full is not None else [tag]):
+        fl += [dict(d, capture=ft) for d in full(ft)]
     if fl:
         lines += ["", "## `--set full` captures", "",
                   "| kernel | " + " | ".join(k for k in fl[0] if k != "kernel") + " |",
@@ -106,8 +116,9 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
-        json.dump(traffic, f, indent=1)
+    if args.traffic_cfg is not None:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.traffic_cfg}.json"), "w") as f:
+            json.dump(traffic, f, indent=1)
     print("\n".join(lines))
 
 
