@@ -151,21 +151,22 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
 // segments stays resident for pass 2; a taller one is streamed again for
 // pass 2 only when it has a nonzero block. One CTA per SM, kExNW warps, each
 // an independent chunk owner (the column chains run across the groups of the
-// chunk in order). Requires L <= kExGmax (else k_ex_cols).
-constexpr int kExNW = 4;       // warps per CTA
-constexpr int kExD = 5;        // ring slots per warp
+// chunk in order). Requires L <= kExG (else k_ex_cols).
 constexpr int kExSR = 32;      // rows per segment
-constexpr int kExGmax = 1024;  // groups listed per chunk
 constexpr int kExAl = kExSR + 2;  // alpha slot (aligned superset), even
+constexpr int kExGmax = 1024;  // groups listed per chunk (largest variant)
 
+// one warp's ring (kExD slots) and its chunk's list of surviving tiles (kExG)
+template <int kExD, int kExG>
 struct alignas(128) ExColWarp {
   double seg[kExD][kExSR * 32];
   double al[kExD][kExAl];
   uint64_t full[kExD];
-  int grp[kExGmax];
-  uint32_t gsw[kExGmax];
+  int grp[kExG];
+  uint32_t gsw[kExG];
 };
 
+template <int kExNW, int kExD, int kExG>
 __global__ void __launch_bounds__(32 * kExNW, 1)
     k_ex_cols2(DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
                uint32_t* __restrict__ cmask, int clear_cmask, double* __restrict__ scale_out,
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
                double* __restrict__ grad) {
   extern __shared__ __align__(128) unsigned char exc_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  ExColWarp& W = reinterpret_cast<ExColWarp*>(exc_smem)[warp];
+  ExColWarp<kExD, kExG>& W = reinterpret_cast<ExColWarp<kExD, kExG>*>(exc_smem)[warp];
   if (lane == 0) {
     for (int q = 0; q < kExD; ++q) mbar_init(&W.full[q], 1);
     mbar_fence_init();
@@ -534,6 +535,7 @@ void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>&
   for (int32_t l = 0; l < P.L; ++l)
     for (int32_t r = 0; r < sizes[l]; r += 32) sl.push_back(make_int4(l, r, std::min(32, sizes[l] - r), 0));
   w.nslabs = static_cast<int>(sl.size());
+  w.gmin = *std::min_element(sizes.begin(), sizes.end());
   w.slabs = dalloc_raw<int4>(w.nslabs, tally);
   GSOT_CUDA_CHECK(cudaMemcpy(w.slabs, sl.data(), sizeof(int4) * sl.size(), cudaMemcpyHostToDevice));
 }
@@ -592,18 +594,30 @@ void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
                         const uint32_t* words, const uint32_t* gmask, uint32_t* cmask,
                         int clear_cmask, double* grad, const double* dvec, EvalScalars* sc,
                         unsigned long long* cnt_slots, cudaStream_t s) {
-  if (P.L <= kExGmax) {
-    static int nsm = 0;
-    const int smem = static_cast<int>(sizeof(ExColWarp) * kExNW);
-    if (nsm == 0) {
-      GSOT_CUDA_CHECK(cudaFuncSetAttribute(k_ex_cols2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      int dev = 0;
-      GSOT_CUDA_CHECK(cudaGetDevice(&dev));
-      GSOT_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    GSOT_CUDA_CHECK(cudaGetDevice(&dev));
+    GSOT_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  auto run = [&](auto kern, int nwarps, int smem) {
+    static int attr = 0;  // per instantiation of the lambda's kernel type
+    if (attr < smem) {
+      GSOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = smem;
     }
-    const int grid = std::min(nsm, (P.nw + kExNW - 1) / kExNW);
-    k_ex_cols2<<<grid, 32 * kExNW, smem, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
-                                              W.cntj, W.nzw, grad);
+    const int grid = std::min(nsm, (P.nw + nwarps - 1) / nwarps);
+    kern<<<grid, 32 * nwarps, smem, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT, W.cntj,
+                                         W.nzw, grad);
+  };
+  const char* ev = std::getenv("GSOT_EXACT_COLS");
+  const int pick = ev ? std::atoi(ev) : 0;
+  // every tile taller than the 5-slot ring anyway (config 5): 8 warps per SM
+  // (more chunks in flight) with 3-slot rings
+  if (P.L <= 256 && (pick == 2 || (pick == 0 && W.gmin > 5 * kExSR))) {
+    run(k_ex_cols2<8, 3, 256>, 8, static_cast<int>(sizeof(ExColWarp<3, 256>) * 8));
+  } else if (P.L <= kExGmax) {
+    run(k_ex_cols2<4, 5, kExGmax>, 4, static_cast<int>(sizeof(ExColWarp<5, kExGmax>) * 4));
   } else {
     k_ex_cols<<<(P.nw + 3) / 4, 128, 0, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
                                               W.cntj, W.nzw, grad);

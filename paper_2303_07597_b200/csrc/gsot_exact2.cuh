@@ -26,6 +26,7 @@ struct ExactWs {
   int64_t tv_stride = 0;
   int4* slabs = nullptr;     // 32-row slabs of the groups: {l, first row in group, rows, 0}
   int nslabs = 0;
+  int gmin = 0;              // smallest group (kernel variant choice)
 };
 
 void exact_ws_alloc(ExactWs& w, const DevProblem& P, const std::vector<int32_t>& sizes,

@@ -160,3 +160,31 @@ def test_sequential_sum_engine_bitwise(n):
             got = ctx.sequential_sum(v, s0)
             assert got == ref or (np.isnan(got) and np.isnan(ref)), (kind, s0, got, ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("sizes", [[300, 17, 170, 64, 161, 1], [700, 33]])
+def test_exact_tall_groups_eval_and_solve_bitwise(o, sizes):
+    """Groups taller than the exact column kernel's resident ring (more than 5
+    segments of 32 rows: streamed twice, the second pass only for tiles with a
+    nonzero block) next to short ones and a one-row group: the exact-order
+    evaluation at several states and a 30-iteration exact solve equal the
+    oracle bit for bit."""
+    rng = np.random.default_rng(len(sizes))
+    sizes = np.array(sizes, np.int32)
+    m, n = int(sizes.sum()), 200
+    cost = rng.uniform(0.0, 1.0, (m, n))
+    p = Problem(cost, sizes, np.full(m, 1.0 / m), np.full(n, 1.0 / n), 0.3, 0.2)
+    ctx = G.Context.from_arrays(p.cost, p.sizes, p.a, p.b, p.gamma, p.mu)
+    for scale in (0.2, 0.6, 1.0):
+        x = scale * rng.uniform(0.0, 1.0, m + n)
+        obj, g, _ = ctx.eval(x, exact=True)
+        obj_o = o.objective(p, x[:m], x[m:])
+        ga, gb = o.gradient(p, x[:m], x[m:])
+        assert obj == obj_o
+        assert np.array_equal(g, np.concatenate([ga, gb]))
+    r = ctx.solve(mode=1, max_outer_loops=3, grad_tol=1e-12, history_cap=10000, exact=True)
+    ro = o.solve(p, mode=1, max_outer_loops=3, grad_tol=1e-12)
+    assert r["iterations"] == ro["iterations"] and r["grad_calls"] == ro["grad_calls"]
+    assert np.array_equal(r["history"], ro["history"])
+    assert np.array_equal(r["x"], ro["x"]) and r["objective"] == ro["objective"]
+    ctx.close()
