@@ -674,6 +674,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
   for (int i = threadIdx.x; i < static_cast<int>(sizeof(HistState) / 4); i += kThreads)
     reinterpret_cast<int*>(&hs)[i] = reinterpret_cast<const volatile int*>(H)[i];
   __syncthreads();
+  // every vector this CTA's slice will read, prefetched into L2 up front (the
+  // evaluation's cost stream evicts them between directions): the elementwise
+  // steps between the sequential sums then hit L2 instead of DRAM
+  if (threadIdx.x < 32 && hi > lo) {
+    auto pf = [&](const double* v) {  // the 16-byte-aligned interior of v[lo, hi)
+      const uintptr_t a0 = (reinterpret_cast<uintptr_t>(v + lo) + 15) & ~static_cast<uintptr_t>(15);
+      const uintptr_t a1 = reinterpret_cast<uintptr_t>(v + hi) & ~static_cast<uintptr_t>(15);
+      if (a1 > a0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
+                     "r"(static_cast<uint32_t>(a1 - a0))
+                     : "memory");
+    };
+    const int t = threadIdx.x;
+    if (t < hs.k) {
+      pf(A.S + hs.order[t] * A.stride);
+      pf(A.Y + hs.order[t] * A.stride);
+    }
+    if (t == 31) {
+      pf(A.g);
+      if (A.pair) {
+        pf(A.x);
+        pf(A.xprev);
+        pf(A.gprev);
+        pf(A.S + hs.scratch * A.stride);
+        pf(A.Y + hs.scratch * A.stride);
+      }
+    }
+  }
 
   if (A.pair) {  // s = x_{k+1} - x_k, y = g_k - g_{k+1} (lbfgs.hpp:243-244)
     const int scratch = hs.scratch;
@@ -756,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
     const double ap = i + 1 < k ? a_loc[i + 1] : 0.0;
     double* t0 = buf(0);
     if (threadIdx.x == 0) sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
-#pragma unroll 4
+#pragma unroll 8
     for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
       const double qe = yp ? dsub(q[e], dmul(ap, yp[e])) : A.g[e];
       q[e] = qe;

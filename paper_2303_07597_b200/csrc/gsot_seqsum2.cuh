@@ -48,7 +48,7 @@ constexpr int kMaxCtas = 16;       // cluster size (16 where the device allows, 
 constexpr int kLeafCap = 4;        // runs per leaf (later terms of the leaf: replayed)
 constexpr int kWarpCap = 16;       // pieces per warp list (later terms of the warp: replayed)
 constexpr int kCtaCap = 64;        // pieces per CTA list (else the stitch takes the warp lists)
-constexpr int kBatch = 16;         // terms loaded per round trip by one thread
+constexpr int kBatch = 8;          // terms loaded per round trip by one thread
 constexpr int kStage = 3328;       // terms of a one-chain call's CTA slice staged in shared memory
 
 struct Chain2 {
@@ -250,17 +250,191 @@ __device__ __forceinline__ void block_of(int64_t len, int P, int g, int64_t& k0,
   k1 = min(len, k0 + b);
 }
 
+// ---- engine phases, each a separate (non-inlined) function: the serial parts
+// run in one or a few warps, and a compact hot loop stays in the instruction
+// cache (an inlined engine is tens of thousands of instructions)
+
+// This thread's approximate block sum of chain c (phase 1).
+static __device__ __noinline__ double block_sum(const Smem2& sm, int c, int P, int g, bool staged,
+                                                int64_t slo) {
+  int64_t k0, k1;
+  block_of(sm.ch[c].len, P, g, k0, k1);
+  double s = 0.0;
+  if (staged) {
+#pragma unroll 1
+    for (int64_t k = k0; k < k1; ++k) s += sm.stage[k - slo];
+  } else {
+    const double* __restrict__ v = sm.ch[c].terms;
+#pragma unroll 1
+    for (int64_t kb = k0; kb < k1; kb += kBatch) {
+      double x[kBatch];
+      load_batch(v, kb, k1, x);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) s += x[q];
+    }
+  }
+  return s;
+}
+
+// This thread's leaf of chain c from the approximate start shat (phase 2).
+static __device__ __noinline__ void run_leaf(Smem2& sm, int c, int P, int g, bool staged,
+                                             int64_t slo, double shat) {
+  int64_t k0, k1;
+  block_of(sm.ch[c].len, P, g, k0, k1);
+  Leaf lf;
+  lf.init(shat, sm.lp[threadIdx.x]);
+  if (staged) {
+#pragma unroll 1
+    for (int64_t k = k0; k < k1; ++k) lf.step(sm.stage[k - slo], static_cast<int>(k));
+  } else {
+    const double* __restrict__ v = sm.ch[c].terms;
+#pragma unroll 1
+    for (int64_t kb = k0; kb < k1; kb += kBatch) {
+      double x[kBatch];
+      load_batch(v, kb, k1, x);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) lf.step(x[q], static_cast<int>(kb + q));
+    }
+  }
+  if (lf.open && !lf.full) lf.close(static_cast<int>(k1));
+  sm.lnp[threadIdx.x] = lf.np;
+  sm.ltl[threadIdx.x] = Tail{lf.full ? 2 : lf.npre, lf.xpre};
+}
+
+// The warp's piece list over its 32 leaves (phase 3, one lane).
+static __device__ __noinline__ void compose_warp(Smem2& sm, int c, int warp) {
+  int t;
+  double tx;
+  const int base = warp * 32;
+  sm.wnp[c][warp] = seq::compose(
+      32,
+      [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
+        nq = sm.lnp[base + q];
+        tq = sm.ltl[base + q].n;
+        xq = sm.ltl[base + q].x;
+        return sm.lp[base + q];
+      },
+      sm.wl[c][warp], kWarpCap, &t, &tx);
+  sm.wtl[c][warp] = Tail{t, tx};
+}
+
+// The CTA's list over its warp lists (phase 3, one lane per chain); -1 when
+// it would not fit (the stitch then takes the warp lists).
+static __device__ __noinline__ void compose_cta(Smem2& sm, int c) {
+  int tot = 0;
+  for (int q = 0; q < kWarps; ++q) tot += sm.wnp[c][q];
+  if (tot > kCtaCap) {
+    sm.cnp[c] = -1;
+    return;
+  }
+  int t;
+  double tx;
+  sm.cnp[c] = seq::compose(
+      kWarps,
+      [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
+        nq = sm.wnp[c][q];
+        tq = sm.wtl[c][q].n;
+        xq = sm.wtl[c][q].x;
+        return sm.wl[c][q];
+      },
+      sm.cl[c], kCtaCap, &t, &tx);
+  sm.ctl[c] = Tail{t, tx};
+}
+
+// The reference's additions over v[k0, k1) by a whole warp (every lane
+// carries s), 128 terms per round trip; zero terms cost nothing.
+static __device__ __noinline__ double serial_terms(double s, const double* __restrict__ v, int k0,
+                                                   int k1) {
+  return serial_warp4(s, v, k0, k1);
+}
+
+// s through np staged pieces over terms [k, kend), then the list's tail (one
+// warp, every lane carries s).
+static __device__ __noinline__ double apply_list(double s, const Piece* __restrict__ stg, int np,
+                                                 Tail tl, int k, int kend,
+                                                 const double* __restrict__ terms) {
+#pragma unroll 1
+  for (int i = 0; i < np; ++i) {
+    // every field loaded before s is needed (the loads do not depend on s)
+    const Piece& p = stg[i];
+    const double st0 = p.st[0], st1 = p.st[1], en0 = p.en[0], en1 = p.en[1];
+    const double lo0 = p.dlo[0], lo1 = p.dlo[1], hi0 = p.dhi[0], hi1 = p.dhi[1];
+    const double xpre = p.xpre;
+    const int npre = p.npre, pk0 = p.k0, pk1 = p.k1;
+    if (npre == 1) {
+      s = dadd(s, xpre);
+    } else if (npre > 1) {
+      s = serial_terms(s, terms, k, pk0);
+    }
+    // try_apply (gsot_seqsum.cuh) on the loaded fields
+    const long long bs = dbits(s), b0 = dbits(st0);
+    const bool odd = ((bs ^ b0) & 1) != 0;
+    const double delta = dsub(s, odd ? st1 : st0);
+    const double sh = s < 0.0 ? -delta : delta;
+    const bool ok = (((bs ^ b0) >> 52) == 0) && sh >= (odd ? lo1 : lo0) && sh <= (odd ? hi1 : hi0);
+    s = ok ? dadd(odd ? en1 : en0, delta) : serial_terms(s, terms, pk0, pk1);
+    k = pk1;
+  }
+  if (tl.n == 1) {
+    s = dadd(s, tl.x);
+  } else if (tl.n > 1) {
+    s = serial_terms(s, terms, k, kend);
+  }
+  return s;
+}
+
+// Phase 4 for chain c (one warp): every CTA's list in order from the exact
+// start, each staged into shared memory in one round trip (a CTA whose list
+// did not fit: its warp lists).
+static __device__ __noinline__ double stitch(Smem2& sm, int c, int P) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int lane = threadIdx.x & 31;
+  const int ncta = static_cast<int>(cl.num_blocks());
+  const Chain2 C = sm.ch[c];
+  const int64_t bt = block_len(C.len, P);  // terms per thread
+  double s = C.s0;
+  Piece* stg = sm.st[c];
+#pragma unroll 1
+  for (int r = 0; r < ncta; ++r) {
+    const int np = *cl.map_shared_rank(&sm.cnp[c], r);
+    const int k0 = static_cast<int>(min(C.len, static_cast<int64_t>(r) * kT * bt));
+    const int k1 = static_cast<int>(min(C.len, static_cast<int64_t>(r + 1) * kT * bt));
+    if (np >= 0) {
+      const Tail tl = *cl.map_shared_rank(&sm.ctl[c], r);
+      __syncwarp();
+      if (lane < np) stg[lane] = *cl.map_shared_rank(&sm.cl[c][lane], r);
+      if (lane + 32 < np) stg[lane + 32] = *cl.map_shared_rank(&sm.cl[c][lane + 32], r);
+      __syncwarp();
+      s = apply_list(s, stg, np, tl, k0, k1, C.terms);
+      continue;
+    }
+    if (cl.block_rank() == 0 && lane == 0) SEQ_CNT(11, 1);
+#pragma unroll 1
+    for (int w = 0; w < kWarps; ++w) {  // the CTA's list did not fit: its warp lists
+      const int wn = *cl.map_shared_rank(&sm.wnp[c][w], r);
+      const Tail wt = *cl.map_shared_rank(&sm.wtl[c][w], r);
+      __syncwarp();
+      if (lane < wn) stg[lane] = *cl.map_shared_rank(&sm.wl[c][w][lane], r);
+      __syncwarp();
+      const int w0 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32) * bt));
+      const int w1 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32 + 32) * bt));
+      s = apply_list(s, stg, wn, wt, w0, w1, C.terms);
+    }
+  }
+  return s;
+}
+
 // The engine: called by every thread of every CTA of the cluster, with
 // sm.ch[0 .. nch) set and every chain's terms written and visible
 // cluster-wide. Results in sm.res[c] after the final __syncthreads.
 //
 // Reuse across calls: a remote CTA reads this CTA's ctot between barrier 1
-// and barrier 2 of a call, and its list (cl / cnp / ctl) after barrier 2
-// until it arrives at barrier 1 of the next call; this CTA rewrites ctot
-// only after barrier 2 and its list only after barrier 1 of the next call.
-// The stitch may replay any CTA's terms, so callers alternate term buffers
-// between consecutive calls (a buffer is rewritten only after the next
-// call's barrier 1).
+// and barrier 2 of a call, and its lists after barrier 2 until it arrives at
+// barrier 1 of the next call; this CTA rewrites ctot only after barrier 2 and
+// its lists only after barrier 1 of the next call. The stitch may replay any
+// CTA's terms, so callers alternate term buffers between consecutive calls
+// (a buffer is rewritten only after the next call's barrier 1).
 static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -288,20 +462,7 @@ static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
   for (int c = 0; c < kMaxCh; ++c) {
     excl[c] = 0.0;
     if (c >= nch) continue;
-    int64_t k0, k1;
-    block_of(sm.ch[c].len, P, g, k0, k1);
-    const double* __restrict__ v = sm.ch[c].terms;
-    double s = 0.0;
-    if (staged) {
-      for (int64_t k = k0; k < k1; ++k) s += sm.stage[k - slo];
-    } else {
-      for (int64_t kb = k0; kb < k1; kb += kBatch) {
-        double x[kBatch];
-        load_batch(v, kb, k1, x);
-#pragma unroll
-        for (int q = 0; q < kBatch; ++q) s += x[q];
-      }
-    }
+    const double s = block_sum(sm, c, P, g, staged, slo);
     double incl = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -326,176 +487,58 @@ static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
   SEQ_PROF_T(t_b);
   cl.sync();  // barrier 1: CTA totals visible cluster-wide
   SEQ_PROF_T(t_c);
+#ifdef GSOT_SEQ_PROF
+  unsigned long long t_runs_end = 0;
+#endif
   // ---- 2. leaf runs from the approximate starts; 3. warp lists (lane 0)
-  for (int c = 0; c < nch; ++c) {
+#pragma unroll
+  for (int c = 0; c < kMaxCh; ++c) {
+    if (c >= nch) continue;
     double pre = lane < cta ? *cl.map_shared_rank(&sm.ctot[c], lane) : 0.0;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
     const double shat = g == 0 ? sm.ch[c].s0 : sm.ch[c].s0 + (pre + (sm.wsum[c][warp] + excl[c]));
-    int64_t k0, k1;
-    block_of(sm.ch[c].len, P, g, k0, k1);
-    const double* __restrict__ v = sm.ch[c].terms;
-    Leaf lf;
-    lf.init(shat, sm.lp[threadIdx.x]);
-    if (staged) {
-      for (int64_t k = k0; k < k1; ++k) lf.step(sm.stage[k - slo], static_cast<int>(k));
-    } else {
-      for (int64_t kb = k0; kb < k1; kb += kBatch) {
-        double x[kBatch];
-        load_batch(v, kb, k1, x);
-#pragma unroll
-        for (int q = 0; q < kBatch; ++q) lf.step(x[q], static_cast<int>(kb + q));
-      }
-    }
-    if (lf.open && !lf.full) lf.close(static_cast<int>(k1));
-    sm.lnp[threadIdx.x] = lf.np;
-    sm.ltl[threadIdx.x] = Tail{lf.full ? 2 : lf.npre, lf.xpre};
+    run_leaf(sm, c, P, g, staged, slo, shat);
     __syncwarp();
-    if (lane == 0) {  // the warp's list over its 32 leaves
-      int t;
-      double tx;
-      const int base = warp * 32;
-      sm.wnp[c][warp] = seq::compose(
-          32,
-          [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
-            nq = sm.lnp[base + q];
-            tq = sm.ltl[base + q].n;
-            xq = sm.ltl[base + q].x;
-            return sm.lp[base + q];
-          },
-          sm.wl[c][warp], kWarpCap, &t, &tx);
-      sm.wtl[c][warp] = Tail{t, tx};
+    SEQ_PROF_T(t_r);
+#ifdef GSOT_SEQ_PROF
+    if (c == 0) t_runs_end = t_r;
+#endif
+    if (lane == 0) {
+#ifdef GSOT_SEQ_PROF
+      const unsigned long long tw0 = clock64();
+      int lsum = 0;
+      for (int q = 0; q < 32; ++q) lsum += sm.lnp[warp * 32 + q];
+#endif
+      compose_warp(sm, c, warp);
+#ifdef GSOT_SEQ_PROF
+      if (cta == 0 && c == 0) {
+        SEQ_CNT(8, lsum);
+        SEQ_CNT(9, sm.wnp[c][warp]);
+        SEQ_CNT(12, clock64() - tw0);
+        SEQ_CNT(13, 1);
+      }
+#endif
     }
     __syncwarp();
   }
   SEQ_PROF_T(t_d);
   __syncthreads();
-  if (warp < nch && lane == 0) {  // the CTA's list of chain c over its warp lists
-    const int c = warp;
-    int tot = 0;
-    for (int q = 0; q < kWarps; ++q) tot += sm.wnp[c][q];
-    if (tot <= kCtaCap) {  // fits without stopping (chaining only shortens it)
-      int t;
-      double tx;
-      sm.cnp[c] = seq::compose(
-          kWarps,
-          [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
-            nq = sm.wnp[c][q];
-            tq = sm.wtl[c][q].n;
-            xq = sm.wtl[c][q].x;
-            return sm.wl[c][q];
-          },
-          sm.cl[c], kCtaCap, &t, &tx);
-      sm.ctl[c] = Tail{t, tx};
-    } else {
-      sm.cnp[c] = -1;
-    }
-  }
+  if (warp < nch && lane == 0) compose_cta(sm, warp);
   SEQ_PROF_T(t_e);
   cl.sync();  // barrier 2: CTA lists visible cluster-wide
   SEQ_PROF_T(t_f);
-  // ---- 4. stitch (every CTA; warp c: chain c): each CTA's list (or, when it
-  // did not fit, each of its warp lists) staged into shared memory in one
-  // round trip, then applied in order
+  // ---- 4. stitch (every CTA; warp c: chain c)
   if (warp < nch) {
-    const int c = warp;
-    const Chain2 C = sm.ch[c];
-    const int64_t bt = block_len(C.len, P);  // terms per thread
-    double s = C.s0;
-    const bool prof = cta == 0 && lane == 0;
-    Piece* stg = sm.st[c];
-    // apply np staged pieces over terms [k, kend) and then the list's tail
-#ifdef GSOT_SEQ_PROF
-    unsigned long long t_apply = 0, t_replay = 0;
-#endif
-    auto apply_list = [&](int np, Tail tl, int k, int kend) {
-      SEQ_PROF_T(ta0);
-#pragma unroll 2
-      for (int i = 0; i < np; ++i) {
-        // every field loaded before s is needed (the loads do not depend on
-        // s, so they overlap the previous piece's dependent chain)
-        const Piece& p = stg[i];
-        const double st0 = p.st[0], st1 = p.st[1], en0 = p.en[0], en1 = p.en[1];
-        const double lo0 = p.dlo[0], lo1 = p.dlo[1], hi0 = p.dhi[0], hi1 = p.dhi[1];
-        const double xpre = p.xpre;
-        const int npre = p.npre, pk0 = p.k0, pk1 = p.k1;
-        if (npre == 1) {
-          s = dadd(s, xpre);
-        } else if (npre > 1) {
-          if (prof && c == 0) {
-            SEQ_CNT(8, 1);
-            SEQ_CNT(9, pk0 - k);
-          }
-          s = serial_warp4(s, C.terms, k, pk0);
-        }
-        if (prof && c == 0) SEQ_CNT(npre == 0 ? 15 : 6, 1);
-        // try_apply (gsot_seqsum.cuh) on the loaded fields
-        const long long bs = dbits(s), b0 = dbits(st0);
-        const bool odd = ((bs ^ b0) & 1) != 0;
-        const double delta = dsub(s, odd ? st1 : st0);
-        const double sh = s < 0.0 ? -delta : delta;
-        const bool ok = (((bs ^ b0) >> 52) == 0) && sh >= (odd ? lo1 : lo0) && sh <= (odd ? hi1 : hi0);
-        if (ok) {
-          s = dadd(odd ? en1 : en0, delta);
-        } else {
-          s = serial_warp4(s, C.terms, pk0, pk1);
-        }
-        k = pk1;
-      }
-      SEQ_PROF_T(ta1);
-      if (tl.n == 1) {
-        s = dadd(s, tl.x);
-      } else if (tl.n > 1) {
-        if (prof) SEQ_CNT(10, 1);
-        s = serial_warp4(s, C.terms, k, kend);
-      }
-      SEQ_PROF_T(ta2);
-#ifdef GSOT_SEQ_PROF
-      t_apply += ta1 - ta0;
-      t_replay += ta2 - ta1;
-      if (prof) SEQ_CNT(12, np);
-#endif
-    };
-    // CTA r's list header and pieces: loaded into registers (in flight while
-    // the previous list is applied), then stored into staging buffer r & 1
-    for (int r = 0; r < ncta; ++r) {
-      const int np = *cl.map_shared_rank(&sm.cnp[c], r);
-      const Tail tl = *cl.map_shared_rank(&sm.ctl[c], r);
-      __syncwarp();
-      if (lane < np) stg[lane] = *cl.map_shared_rank(&sm.cl[c][lane], r);
-      if (lane + 32 < np) stg[lane + 32] = *cl.map_shared_rank(&sm.cl[c][lane + 32], r);
-      __syncwarp();
-      const int k0 = static_cast<int>(min(C.len, static_cast<int64_t>(r) * kT * bt));
-      const int k1 = static_cast<int>(min(C.len, static_cast<int64_t>(r + 1) * kT * bt));
-      if (np >= 0) {
-        apply_list(np, tl, k0, k1);
-        continue;
-      }
-      if (prof) SEQ_CNT(11, 1);
-      for (int w = 0; w < kWarps; ++w) {  // the CTA's list did not fit: its warp lists
-        const int wn = *cl.map_shared_rank(&sm.wnp[c][w], r);
-        const Tail wt = *cl.map_shared_rank(&sm.wtl[c][w], r);
-        __syncwarp();
-        if (lane < wn) stg[lane] = *cl.map_shared_rank(&sm.wl[c][w][lane], r);
-        __syncwarp();
-        const int w0 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32) * bt));
-        const int w1 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32 + 32) * bt));
-        apply_list(wn, wt, w0, w1);
-      }
-    }
-    if (lane == 0) sm.res[c] = s;
-#ifdef GSOT_SEQ_PROF
-    if (prof && c == 0) {
-      SEQ_CNT(13, t_apply);
-      SEQ_CNT(14, t_replay);
-    }
-#endif
+    const double s = stitch(sm, warp, P);
+    if (lane == 0) sm.res[warp] = s;
   }
   SEQ_PROF_T(t_g);
   __syncthreads();
   SEQ_PROF_ADD(0, t_a, t_b);  // block sums + CTA scan
   SEQ_PROF_ADD(1, t_b, t_c);  // barrier 1
   SEQ_PROF_ADD(2, t_c, t_d);  // starts + leaf runs + warp lists
+  SEQ_PROF_ADD(15, t_c, t_runs_end);  // starts + leaf runs of chain 0
   SEQ_PROF_ADD(3, t_d, t_e);  // CTA list
   SEQ_PROF_ADD(4, t_e, t_f);  // barrier 2
   SEQ_PROF_ADD(5, t_f, t_g);  // stitch (warp 0: chain 0)

@@ -15,8 +15,8 @@ sys.path.insert(0, ROOT)
 import paper_2303_07597_b200 as G  # noqa: E402
 from paper_2303_07597_b200 import _lib  # noqa: E402
 
-NAMES = {6: "pieces npre>=1 (ch0)", 15: "pieces npre=0 (ch0)", 8: "replays npre>1 (ch0)", 9: "replayed terms npre>1", 7: "engine calls", 10: "tails replayed", 11: "CTA lists too long", 12: "pieces (CTA 0, all chains)",
-         13: "apply cycles (chain 0)", 14: "tail replay cycles (chain 0)"}
+NAMES = {7: "engine calls", 8: "leaf pieces (cta0 ch0)", 9: "warp-list pieces", 11: "CTA lists too long",
+         12: "warp compose cycles", 13: "warp composes"}
 PHASES = ["sums+scan", "barrier1", "runs+warp trees", "CTA root", "barrier2", "stitch"]
 h = _lib.lib()
 h.gsot_debug_seq_prof.argtypes = [C.c_void_p]
@@ -27,7 +27,8 @@ def show(tag):
     h.gsot_debug_seq_prof(buf)
     n = max(1, buf[7])
     print(tag, {NAMES[k]: buf[k] for k in NAMES})
-    print("   us/call:", {PHASES[i]: round(buf[i] / n / 1.9e3, 2) for i in range(6) if i != 6})
+    print("   us/call:", {PHASES[i]: round(buf[i] / n / 1.9e3, 2) for i in range(6) if i != 6},
+          "of which runs (chain 0):", round(buf[15] / n / 1.9e3, 2))
 
 
 ctx = G.Context.from_arrays(np.full((4, 3), 0.5), [4], np.full(4, 0.25), np.full(3, 1 / 3), 1.0, 1.0)
