@@ -483,7 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_scalars(ScalarArgs A) {
       if (lane >= o) incl += y;
     }
     const int64_t pos = __ldcg(A.offC + c) + (incl - v);
-    for (int q = 0; q < v; ++q) A.flat[pos + q] = A.psiT[j * P.L + q];
+    const double* __restrict__ src = A.psiT + j * P.L;
+#pragma unroll 8
+    for (int q = 0; q < v; ++q) A.flat[pos + q] = src[q];
   }
   if (threadIdx.x == 0) {
     const int64_t npsi = __ldcg(A.offC + P.nw);

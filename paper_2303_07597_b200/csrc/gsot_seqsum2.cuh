@@ -11,7 +11,8 @@
 //      the exact start);
 //   2. each thread runs its block from s^ ("leaf"): at most kLeafCap runs in
 //      both mantissa parities, a run ending where a step leaves the allowed
-//      binades, that term kept inline as a serial term;
+//      binades (above the start's, or tiny), that term kept inline as a
+//      serial term; runs may change sign (signed shift margins);
 //   3. lane 0 of each warp composes its 32 leaves into the warp's piece list
 //      (runs continued across leaves where the left end is a valid start of
 //      the right run), then one lane per chain composes the CTA's warp lists
@@ -108,10 +109,22 @@ struct Leaf {
     if (npre == 0) xpre = x;
     ++npre;
   }
+  // a run value may be of either sign and in any binade between 2^-968 and
+  // the start's: the true path is the run shifted by delta, and rounding
+  // commutes with the shift while both paths' values share a binade (the
+  // signed margins below) and delta is a multiple of 2 ulp of that binade
+  // (every binade at or below the start's)
   __device__ __forceinline__ bool inside(double v) const {
-    const long long b = dbits(v);
-    const int ex = static_cast<int>((b >> 52) & 0x7ff);
-    return ((b ^ bst) >= 0) && ex > 54 && ex <= static_cast<int>((bst >> 52) & 0x7ff);
+    const int ex = static_cast<int>((dbits(v) >> 52) & 0x7ff);
+    return ex > 54 && ex <= static_cast<int>((bst >> 52) & 0x7ff);
+  }
+  // the shifts delta keeping v + delta in v's binade: delta > -dneg, < dpos
+  __device__ __forceinline__ static void smargins(double v, double& dneg, double& dpos) {
+    const double a = fabs(v);
+    const double lb = __longlong_as_double(dbits(a) & 0x7ff0000000000000ll);
+    const double below = dsub(a, lb), above = dsub(dadd(lb, lb), a);  // exact
+    dneg = fmin(dneg, v > 0.0 ? below : above);
+    dpos = fmin(dpos, v > 0.0 ? above : below);
   }
   __device__ __forceinline__ bool try_open(int k) {
     const int ex = static_cast<int>((dbits(s) >> 52) & 0x7ff);
@@ -128,8 +141,8 @@ struct Leaf {
     t0 = st0;
     t1 = st1;
     lo0 = hi0 = lo1 = hi1 = dinf();
-    seq::LaneSpec::margins(t0, lo0, hi0);
-    seq::LaneSpec::margins(t1, lo1, hi1);
+    smargins(t0, lo0, hi0);
+    smargins(t1, lo1, hi1);
     ok1 = true;
     k0 = k;
     open = true;
@@ -141,13 +154,16 @@ struct Leaf {
     p.st[1] = st1;
     p.en[0] = t0;
     p.en[1] = t1;
+    // lo / hi: allowed negative / positive shift of the start; the piece
+    // stores the allowed shift of |s| (sign of the start), 2 ulp kept in reserve
     const double inf = dinf();
     const bool v0 = lo0 >= u2 && hi0 >= u2;
     const bool v1 = ok1 && lo1 >= u2 && hi1 >= u2;
-    p.dlo[0] = v0 ? dsub(u2, lo0) : inf;
-    p.dhi[0] = v0 ? dsub(hi0, u2) : -inf;
-    p.dlo[1] = v1 ? dsub(u2, lo1) : inf;
-    p.dhi[1] = v1 ? dsub(hi1, u2) : -inf;
+    const bool pos = st0 > 0.0;
+    p.dlo[0] = v0 ? dsub(u2, pos ? lo0 : hi0) : inf;
+    p.dhi[0] = v0 ? dsub(pos ? hi0 : lo0, u2) : -inf;
+    p.dlo[1] = v1 ? dsub(u2, pos ? lo1 : hi1) : inf;
+    p.dhi[1] = v1 ? dsub(pos ? hi1 : lo1, u2) : -inf;
     p.xpre = xpre;
     p.k0 = k0;
     p.k1 = k1;
@@ -176,8 +192,8 @@ struct Leaf {
     ok1 = ok1 && inside(n1);
     t0 = n0;
     t1 = n1;
-    seq::LaneSpec::margins(n0, lo0, hi0);
-    seq::LaneSpec::margins(n1, lo1, hi1);
+    smargins(n0, lo0, hi0);
+    smargins(n1, lo1, hi1);
   }
 };
 
@@ -243,6 +259,96 @@ __host__ __device__ __forceinline__ int64_t block_len(int64_t len, int P) {
   return ((len + P - 1) / P) | 1;
 }
 
+// Continue `cur` through `nx` (adjacent, no serial term between): per parity
+// run of cur whose end lies in nx's start binade and range, the continued run
+// is concrete (its end is nx's end shifted, exact) and its shift range
+// narrows. Runs may change sign (the shift ranges are kept relative to each
+// piece's start sign, so a sign change between cur's start and nx's start
+// mirrors nx's range). cur is updated only when a parity run continues.
+__device__ __forceinline__ bool chain2(Piece& cur, const Piece& nx) {
+  const long long bn0 = dbits(nx.st[0]);
+  const bool same = (cur.st[0] < 0.0) == (nx.st[0] < 0.0);
+  double en[2], lo[2], hi[2];
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    en[r] = cur.en[r];
+    lo[r] = dinf();
+    hi[r] = -dinf();
+    if (!(cur.dlo[r] <= cur.dhi[r])) continue;
+    const double e = cur.en[r];
+    const long long be = dbits(e);
+    if (((be ^ bn0) >> 52) != 0) continue;  // not nx's start binade
+    const bool odd = ((be ^ bn0) & 1) != 0;
+    const double nst = odd ? nx.st[1] : nx.st[0];
+    const double nen = odd ? nx.en[1] : nx.en[0];
+    const double nlo = odd ? nx.dlo[1] : nx.dlo[0];
+    const double nhi = odd ? nx.dhi[1] : nx.dhi[0];
+    const double c = dsub(e, nst);  // exact
+    const double C = e < 0.0 ? -c : c;
+    if (!(C >= nlo && C <= nhi)) continue;
+    const double l = fmax(cur.dlo[r], same ? __dsub_ru(nlo, C) : __dsub_ru(C, nhi));
+    const double h = fmin(cur.dhi[r], same ? __dsub_rd(nhi, C) : __dsub_rd(C, nlo));
+    if (!(l <= h)) continue;
+    en[r] = dadd(nen, c);  // exact: the run continued through nx's terms
+    lo[r] = l;
+    hi[r] = h;
+    any = true;
+  }
+  if (any) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      cur.en[r] = en[r];
+      cur.dlo[r] = lo[r];
+      cur.dhi[r] = hi[r];
+    }
+    cur.k1 = nx.k1;
+  }
+  return any;
+}
+
+// gsot_seqsum.cuh's compose with chain2 (sign-changing runs).
+template <typename Unit>
+__device__ __forceinline__ int compose2(int nunits, Unit unit, Piece* __restrict__ out, int cap,
+                                        int* tail, double* tailx) {
+  int no = 0;
+  bool have = false, stopped = false;
+  Piece cur;
+  int pend = 0;
+  double pendx = 0.0;
+  for (int q = 0; q < nunits && !stopped; ++q) {
+    int nq, tq;
+    double xq;
+    const Piece* pq = unit(q, nq, tq, xq);
+    for (int t = 0; t < nq; ++t) {
+      Piece nx = pq[t];
+      const int npre = pend + nx.npre;
+      if (npre == 1 && pend == 1) nx.xpre = pendx;
+      nx.npre = npre;
+      pend = 0;
+      if (have && npre == 0 && chain2(cur, nx)) continue;
+      if (have) {
+        out[no++] = cur;
+        if (no == cap) {
+          have = false;
+          stopped = true;
+          break;
+        }
+      }
+      cur = nx;
+      have = true;
+    }
+    if (tq > 0) {
+      if (pend == 0 && tq == 1) pendx = xq;
+      pend += tq;
+    }
+  }
+  if (have) out[no++] = cur;
+  *tail = stopped ? 2 : pend;
+  *tailx = pendx;
+  return no;
+}
+
 // Thread g's block of a chain of len terms over P threads.
 __device__ __forceinline__ void block_of(int64_t len, int P, int g, int64_t& k0, int64_t& k1) {
   const int64_t b = block_len(len, P);
@@ -306,7 +412,7 @@ static __device__ __noinline__ void compose_warp(Smem2& sm, int c, int warp) {
   int t;
   double tx;
   const int base = warp * 32;
-  sm.wnp[c][warp] = seq::compose(
+  sm.wnp[c][warp] = compose2(
       32,
       [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
         nq = sm.lnp[base + q];
@@ -329,7 +435,7 @@ static __device__ __noinline__ void compose_cta(Smem2& sm, int c) {
   }
   int t;
   double tx;
-  sm.cnp[c] = seq::compose(
+  sm.cnp[c] = compose2(
       kWarps,
       [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
         nq = sm.wnp[c][q];

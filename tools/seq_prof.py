@@ -15,8 +15,7 @@ sys.path.insert(0, ROOT)
 import paper_2303_07597_b200 as G  # noqa: E402
 from paper_2303_07597_b200 import _lib  # noqa: E402
 
-NAMES = {7: "engine calls", 8: "leaf pieces (cta0 ch0)", 9: "warp-list pieces", 11: "CTA lists too long",
-         12: "warp compose cycles", 13: "warp composes"}
+NAMES = {7: "engine calls", 8: "leaf pieces (cta0 ch0)", 9: "warp-list pieces", 11: "CTA lists too long"}
 PHASES = ["sums+scan", "barrier1", "runs+warp trees", "CTA root", "barrier2", "stitch"]
 h = _lib.lib()
 h.gsot_debug_seq_prof.argtypes = [C.c_void_p]
