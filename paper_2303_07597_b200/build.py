@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libgsot.so")
 # Diagnostic variants: GSOT_NVCC_DEFINES="-DGSOT_PHASE_CLOCKS" GSOT_LIB_OUT=... (never the product)
 EXTRA = os.environ.get("GSOT_NVCC_DEFINES", "").split()
-SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu", "gsot_solver.cu", "gsot_exact.cu", "gsot_exact2.cu"]
+SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu", "gsot_solver.cu", "gsot_exact2.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -32,7 +32,7 @@ FLAGS = [
 def build(verbose: bool = False, force: bool = False) -> str:
     LIB = os.environ.get("GSOT_LIB_OUT") or globals()["LIB"]
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in ("gsot_internal.cuh", "gsot_device.cuh", "gsot_ctx.cuh", "gsot_seqsum.cuh", "gsot_seqsum2.cuh", "gsot_exact2.cuh")] + [os.path.join(ROOT, "include", "gsot.h")]
+    deps = srcs + [os.path.join(CSRC, h) for h in ("gsot_internal.cuh", "gsot_device.cuh", "gsot_ctx.cuh", "gsot_seqsum.cuh", "gsot_exact2.cuh")] + [os.path.join(ROOT, "include", "gsot.h")]
     if (not force and os.path.exists(LIB)
             and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps)):
         return LIB

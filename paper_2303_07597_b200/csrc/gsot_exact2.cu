@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 
 namespace gsot {
 
-constexpr int kThreads = seq2::kT;
+constexpr int kThreads = seq::kT;
 
 // ---------------------------------------------------------------- columns
 
@@ -408,7 +408,7 @@ struct ScalarArgs {
 
 __global__ void __launch_bounds__(kThreads, 1) k_ex_scalars(ScalarArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  seq2::Smem2& sm = *reinterpret_cast<seq2::Smem2*>(smem_raw);
+  seq::Smem2& sm = *reinterpret_cast<seq::Smem2*>(smem_raw);
   cg::cluster_group cl = cg::this_cluster();
   const DevProblem& P = A.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -489,14 +489,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_scalars(ScalarArgs A) {
   }
   if (threadIdx.x == 0) {
     const int64_t npsi = __ldcg(A.offC + P.nw);
-    sm.ch[0] = seq2::Chain2{A.flat, npsi, 0.0};
-    sm.ch[1] = seq2::Chain2{t1, P.m, 0.0};
-    sm.ch[2] = seq2::Chain2{t2, P.n, 0.0};
-    sm.ch[3] = seq2::Chain2{t3, A.dvec ? dim : 0, 0.0};
+    sm.ch[0] = seq::Chain2{A.flat, npsi, 0.0};
+    sm.ch[1] = seq::Chain2{t1, P.m, 0.0};
+    sm.ch[2] = seq::Chain2{t2, P.n, 0.0};
+    sm.ch[3] = seq::Chain2{t3, A.dvec ? dim : 0, 0.0};
   }
   cl.sync();
   // 4. the four sequential sums
-  seq2::engine2(A.dvec ? 4 : 3, sm);
+  seq::engine2(A.dvec ? 4 : 3, sm);
   if (cta == 0) {
     if (warp == 1 && A.cnt_slots) fold_counter_slots(A.cnt_slots, A.sc);  // screen counters
     if (threadIdx.x == 0) {
@@ -554,7 +554,7 @@ void exact_ws_free(ExactWs& w) {
 template <typename K, typename Arg>
 static void launch_cluster(K kern, const Arg& a, cudaStream_t s) {
   static int ncta = 0;
-  const int smem = static_cast<int>(sizeof(seq2::Smem2));
+  const int smem = static_cast<int>(sizeof(seq::Smem2));
   if (ncta == 0) {
     ncta = 8;
     GSOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -563,17 +563,17 @@ static void launch_cluster(K kern, const Arg& a, cudaStream_t s) {
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = seq2::kMaxCtas;
+      at[0].val.clusterDim.x = seq::kMaxCtas;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(seq2::kMaxCtas);
+      cfg.gridDim = dim3(seq::kMaxCtas);
       cfg.blockDim = dim3(kThreads);
       cfg.dynamicSmemBytes = smem;
       cfg.attrs = at;
       cfg.numAttrs = 1;
       int n = 0;
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n >= 1)
-        ncta = seq2::kMaxCtas;
+        ncta = seq::kMaxCtas;
     }
     (void)cudaGetLastError();
   }
@@ -659,14 +659,14 @@ struct DirKArgs {
 // stitch may still read the previous call's terms.
 __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  seq2::Smem2& sm = *reinterpret_cast<seq2::Smem2*>(smem_raw);
+  seq::Smem2& sm = *reinterpret_cast<seq::Smem2*>(smem_raw);
   __shared__ HistState hs;
   __shared__ double a_loc[kMaxMemory];
   cg::cluster_group cl = cg::this_cluster();
   const ExactDirArgs& A = K.a;
   const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
   const int64_t dim = A.dim;
-  const int64_t b = seq2::block_len(dim, ncta * kThreads);
+  const int64_t b = seq::block_len(dim, ncta * kThreads);
   const int64_t lo = min(dim, static_cast<int64_t>(cta) * kThreads * b);
   const int64_t hi = min(dim, lo + kThreads * b);
   HistState* H = A.h;
@@ -713,9 +713,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
     double* t1 = buf(1);
     double* t2 = buf(2);
     if (threadIdx.x == 0) {
-      sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
-      sm.ch[1] = seq2::Chain2{t1, dim, 0.0};
-      sm.ch[2] = seq2::Chain2{t2, dim, 0.0};
+      sm.ch[0] = seq::Chain2{t0, dim, 0.0};
+      sm.ch[1] = seq::Chain2{t1, dim, 0.0};
+      sm.ch[2] = seq::Chain2{t2, dim, 0.0};
     }
 #pragma unroll 4
     for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
       t2[e] = dmul(y, y);
     }
     __syncthreads();
-    seq2::engine2(3, sm);
+    seq::engine2(3, sm);
     ++call;
     if (threadIdx.x == 0) {  // acceptance test and ring update (lbfgs.hpp:246-255)
       const double sy = sm.res[0], ss = sm.res[1], yy = sm.res[2];
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
     const double* __restrict__ yp = i + 1 < k ? A.Y + hs.order[i + 1] * A.stride : nullptr;
     const double ap = i + 1 < k ? a_loc[i + 1] : 0.0;
     double* t0 = buf(0);
-    if (threadIdx.x == 0) sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
+    if (threadIdx.x == 0) sm.ch[0] = seq::Chain2{t0, dim, 0.0};
 #pragma unroll 8
     for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
       const double qe = yp ? dsub(q[e], dmul(ap, yp[e])) : A.g[e];
@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
       t0[e] = dmul(si[e], qe);
     }
     __syncthreads();
-    seq2::engine2(1, sm);
+    seq::engine2(1, sm);
     ++call;
     if (threadIdx.x == 0) a_loc[i] = dmul(hs.rho[i], sm.res[0]);
     __syncthreads();
@@ -812,8 +812,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
     double* t0 = buf(0);
     double* t1 = buf(1);
     if (threadIdx.x == 0) {
-      sm.ch[0] = seq2::Chain2{t0, dim, 0.0};
-      sm.ch[1] = seq2::Chain2{t1, dim, 0.0};
+      sm.ch[0] = seq::Chain2{t0, dim, 0.0};
+      sm.ch[1] = seq::Chain2{t1, dim, 0.0};
     }
 #pragma unroll 4
     for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_direction(DirKArgs K) {
       }
     }
     __syncthreads();
-    seq2::engine2(i < k ? 1 : 2, sm);
+    seq::engine2(i < k ? 1 : 2, sm);
     ++call;
     if (i < k) coef_prev = dsub(a_loc[i], dmul(hs.rho[i], sm.res[0]));
   }
@@ -867,10 +867,10 @@ struct DotArgs {
 
 __global__ void __launch_bounds__(kThreads, 1) k_ex_dot(DotArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  seq2::Smem2& sm = *reinterpret_cast<seq2::Smem2*>(smem_raw);
+  seq::Smem2& sm = *reinterpret_cast<seq::Smem2*>(smem_raw);
   cg::cluster_group cl = cg::this_cluster();
   const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
-  const int64_t b = seq2::block_len(A.n, ncta * kThreads);
+  const int64_t b = seq::block_len(A.n, ncta * kThreads);
   const int64_t lo = min(A.n, static_cast<int64_t>(cta) * kThreads * b);
   const int64_t hi = min(A.n, lo + kThreads * b);
   const double* terms = A.a;
@@ -878,9 +878,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ex_dot(DotArgs A) {
     for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) A.tv[e] = dmul(A.a[e], A.b[e]);
     terms = A.tv;
   }
-  if (threadIdx.x == 0) sm.ch[0] = seq2::Chain2{terms, A.n, A.s0};
+  if (threadIdx.x == 0) sm.ch[0] = seq::Chain2{terms, A.n, A.s0};
   __syncthreads();
-  seq2::engine2(1, sm);
+  seq::engine2(1, sm);
   if (cta == 0 && threadIdx.x == 0) *A.out = sm.res[0];
   cl.sync();  // no CTA exits while another may still read its shared memory
 }

@@ -5,7 +5,7 @@
 #pragma once
 
 #include "gsot_internal.cuh"
-#include "gsot_seqsum2.cuh"
+#include "gsot_seqsum.cuh"
 
 namespace gsot {
 

@@ -232,17 +232,6 @@ void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_cou
                     const double* step_partials, unsigned long long* cnt_slots,
                     unsigned long long* tl, cudaStream_t s);
 
-struct TwoLoopArgs {
-  const double* S;  // pair slots: slot s at S + s * stride
-  const double* Y;
-  int64_t stride;
-  const HistState* h;
-  const double* g;
-  double* d;
-  int64_t dim;
-  double* out;  // [0] = g.d, [1] = d.d
-};
-// trial.x = x + t * d with t read from device memory.
 // trial.x = x + t * d with t read from device memory; with dbeta != null also
 // dbeta_j = out[m + j] - snap[m + j] for the screen.
 void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
@@ -252,17 +241,6 @@ void launch_dot(const double* a, const double* b, int64_t dim, double* partials,
                 EvalScalars* sc, int slot, cudaStream_t s);
 void launch_absmax(const double* a, int64_t dim, double* partials, int nblocks, EvalScalars* sc,
                    int slot, cudaStream_t s);
-
-// Exact-order mode (gsot_exact.cu).
-void launch_exact_eval(const DevProblem& P, const double* x, double* scale, double* psi,
-                       double* grad, const double* dvec, EvalScalars* sc,
-                       unsigned long long* cnt_slots, cudaStream_t s);
-void launch_exact_two_loop(const TwoLoopArgs& a, cudaStream_t s);
-void launch_exact_pair(const double* xt, const double* x, const double* g, const double* gt,
-                       double* S, double* Y, int64_t stride, HistState* h, int64_t dim,
-                       EvalScalars* sc, cudaStream_t s);
-void launch_exact_dot(const double* a, const double* b, int64_t dim, EvalScalars* sc, int slot,
-                      cudaStream_t s);
 
 // Cost-matrix construction (gsot_data.cu).
 // tiled == nullptr: column-major m x n output; otherwise the column-tiled

@@ -10,7 +10,7 @@
 // combine pass: d = gam g + S p - Y (gam w), with w = R^-1 (S^T g),
 // p = R^-T ((D + gam Y^T Y) w - gam Y^T g), R = triu(S^T Y). R and Y^T Y are
 // kept by logical position and updated by one column per accepted pair.
-// Exact mode (gsot_exact.cu) keeps the reference's two-loop instead.
+// Exact mode (gsot_exact2.cu) keeps the reference's two-loop instead.
 //
 // Determinism: each dot is reduced by fixed warp trees, per-CTA results are
 // folded in CTA order, the grid is a fixed function of the device.

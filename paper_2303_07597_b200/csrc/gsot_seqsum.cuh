@@ -1,40 +1,36 @@
-// gsot_seqsum.cuh — the reference's SEQUENTIAL floating-point sums, computed
-// in parallel and bit for bit (exact-order mode).
+// gsot_seqsum.cuh — the reference's SEQUENTIAL floating-point sums in
+// parallel and bit for bit, latency-first (exact-order mode).
 //
-// The reference accumulates every reduction left to right (`acc += v[i]`,
-// Eigen's dot / sum / squaredNorm in the oracle's sequential build,
-// regularizer.hpp:23-51, dual.hpp:44-51, lbfgs.hpp:109-132). A sequential sum
-// of N terms is N dependent roundings (~14 cycles each on B200); this header
-// reproduces its exact result with short dependent chains.
+// A sequential sum of N terms is N dependent roundings. It is computed in
+// parallel by speculation on translation invariance: while the partial sums
+// of a stretch of terms stay inside binades at or below the binade of the
+// stretch's start, the whole path shifted by delta (a multiple of 2 ulp of the
+// start) rounds identically, so a "run" computed from an approximate start
+// gives the exact result for the true start by one exact addition; runs from
+// both mantissa parities of the start cover any delta. Organised for the
+// shortest critical path on one thread-block cluster:
 //
-// Translation invariance. Let a "run" be the sequential sum of a stretch of
-// terms from some start t. If a true start s differs from t by delta, a
-// multiple of 2 ulp(t), and at every step both paths' exact sums stay in the
-// same binade (same sign, |x| in [2^E, 2^(E+1))), E never above the start
-// binade, then both paths round on grids that delta is a multiple of, with
-// the same ties-to-even decisions: the true path is the run shifted by delta
-// and its end is run_end + delta (exact). Runs start from t and t +- ulp
-// (both mantissa parities), so one of them is always an even shift away; a
-// run records the shifts of |s| that keep every step 2 ulp(t) inside its
-// binade (`dlo`, `dhi`). A step that leaves the allowed binades (upwards, a
-// sign change, a tiny value) ends the run; that term is applied serially.
+//   1. every thread of the cluster owns one contiguous block of b terms
+//      (b = ceil(len / threads)); approximate block sums, a CTA scan and one
+//      cluster barrier give each thread an approximate start s^ (thread 0:
+//      the exact start);
+//   2. each thread runs its block from s^ ("leaf"): at most kLeafCap runs in
+//      both mantissa parities, a run ending where a step leaves the allowed
+//      binades (above the start's, or tiny), that term kept inline as a
+//      serial term; runs may change sign (signed shift margins);
+//   3. lane 0 of each warp composes its 32 leaves into the warp's piece list
+//      (runs continued across leaves where the left end is a valid start of
+//      the right run), then one lane per chain composes the CTA's warp lists
+//      into the CTA's list;
+//   4. one more cluster barrier, then EVERY CTA stitches the CTA lists in
+//      order from the exact start (an exact translation per piece; inline
+//      serial terms: the reference's addition), so the result is in every
+//      CTA with no broadcast. A piece that does not apply, and serial terms
+//      not kept inline, are replayed with the reference's own additions.
 //
-//  A. segment sums in any order -> approximate start s^_p of each segment;
-//  B. one warp per segment: each lane runs a 1/32 sub-range speculatively
-//     from its own approximate start (a warp scan of the lane sub-sums), then
-//     lane 0 chains the lanes' runs into the segment's "pieces": a run is
-//     continued into the next one when its end lies in the next one's valid
-//     shift range (the continued path is again a concrete run of the terms),
-//     O(1) per lane instead of one dependent add per term;
-//  C. stitch: s = s0, then per piece its serial terms and the translation of
-//     the true value when it lies in the piece's range, else the reference's
-//     own additions over the piece's terms.
-//
-// Every step of C is either the reference's own addition or an exact
-// translation, so the result is the sequential sum for any input (fallbacks
-// only cost time). Pinned against sequential sums of adversarial inputs
-// (ties, zeros, cancellation, subnormals) in tests/test_gpu_exact.py and by
-// the bitwise exact-mode solves.
+// Every step of the stitch is either the reference's addition or an exact
+// translation, so the result is the sequential sum for any input; fallbacks
+// only cost time. Two cluster barriers per call.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -67,19 +63,7 @@ __device__ unsigned long long g_seq_prof[16];
   } while (0)
 #endif
 
-constexpr int kMaxPieces = 64;  // pieces per segment (later terms: serial)
-constexpr int kMaxGPieces = 256; // pieces per group of segments (later terms: serial)
-constexpr int kLanePieces = 4;  // runs per lane sub-range in B (later terms: serial)
-constexpr int kClusterCtas = 8; // CTAs of the exact-mode cluster kernels
-constexpr int kThreads = 256;   // threads per CTA of those kernels
-constexpr int kMaxSegs = 512;   // segments per chain
-constexpr int kMaxChains = 4;
-constexpr int kStage = 4096;    // terms of a segment staged in shared memory (phase B)
-constexpr int kBWarps = 4;      // warps per CTA running phases B and C1
-constexpr int kGroup = 4;       // segments chained per warp in phase C1
-constexpr int kMaxGroups = kMaxSegs / kGroup;
-
-// A run (or a chain of runs) over terms [k0, k1) of a segment.
+// A run (or a chain of runs) over terms [k0, k1).
 struct alignas(16) Piece {
   double st[2];           // starts of the two parity runs (st[0]: the speculative start)
   double en[2];           // their ends
@@ -93,31 +77,53 @@ struct alignas(16) Piece {
 __device__ __forceinline__ long long dbits(double s) { return __double_as_longlong(s); }
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
 
-// Segment length for a chain of `len` terms: about len / 64 (multiple of 64,
-// at least 256), staged whole in shared memory up to kStage terms; longer
-// only when len > kMaxSegs * kStage (then read from L2).
-__host__ __device__ __forceinline__ int seg_len(int64_t len) {
-  int64_t b = ((len + 63) / 64 + 63) / 64 * 64;
-  if (b < 256) b = 256;
-  if (b > kStage) b = kStage;
-  while ((len + b - 1) / b > kMaxSegs) b *= 2;
-  return static_cast<int>(b);
-}
 
-// The true value s through piece p when it lies in p's range.
-__device__ __forceinline__ bool try_apply(double& s, const Piece& p) {
-  const long long bs = dbits(s), b0 = dbits(p.st[0]);
-  if (((bs ^ b0) >> 52) != 0) return false;  // not the start binade
-  const bool odd = ((bs ^ b0) & 1) != 0;  // the run of s's mantissa parity
-  const double delta = dsub(s, odd ? p.st[1] : p.st[0]);  // exact, an even number of ulps
-  const double sh = s < 0.0 ? -delta : delta;
-  if (!(sh >= (odd ? p.dlo[1] : p.dlo[0]) && sh <= (odd ? p.dhi[1] : p.dhi[0]))) return false;
-  s = dadd(odd ? p.en[1] : p.en[0], delta);  // exact: the true path's value
-  return true;
-}
+constexpr int kT = 256;            // threads per CTA of the engine's kernels
+constexpr int kWarps = kT / 32;    // warps per CTA
+constexpr int kMaxCh = 4;          // chains per engine call
+constexpr int kMaxCtas = 16;       // cluster size (16 where the device allows, else 8)
+constexpr int kLeafCap = 4;        // runs per leaf (later terms of the leaf: replayed)
+constexpr int kWarpCap = 16;       // pieces per warp list (later terms of the warp: replayed)
+constexpr int kCtaCap = 64;        // pieces per CTA list (else the stitch takes the warp lists)
+constexpr int kBatch = 8;          // terms loaded per round trip by one thread
+constexpr int kStage = 3328;       // terms of a one-chain call's CTA slice staged in shared memory
 
-// One lane's speculative runs over its sub-range (terms streamed in order).
-struct LaneSpec {
+struct Chain2 {
+  const double* terms;
+  int64_t len;
+  double s0;
+};
+
+// A piece list's tail: nonzero serial terms after its last piece (>= 2:
+// replay them from memory; the value when exactly one).
+struct Tail {
+  int n;
+  double x;
+};
+
+// Dynamic shared memory of the engine's kernels.
+struct Smem2 {
+  Chain2 ch[kMaxCh];
+  double ctot[kMaxCh];                     // CTA approximate totals (read remotely)
+  double wsum[kMaxCh][kWarps];             // scan scratch: warp totals
+  Piece lp[kT][kLeafCap];                  // leaf runs (one chain at a time)
+  int lnp[kT];
+  Tail ltl[kT];
+  Piece wl[kMaxCh][kWarps][kWarpCap];      // warp lists
+  int wnp[kMaxCh][kWarps];
+  Tail wtl[kMaxCh][kWarps];
+  Piece cl[kMaxCh][kCtaCap];               // CTA lists (read remotely by the stitch)
+  int cnp[kMaxCh];                         // their length; -1: incomplete, use the warp lists
+  Tail ctl[kMaxCh];
+  Piece st[kMaxCh][kCtaCap];               // stitch: a remote CTA's list, staged
+  double res[kMaxCh];
+  double stage[kStage];                    // a one-chain call's CTA slice (coalesced copy)
+};
+static_assert(sizeof(Smem2) <= 227 * 1024, "engine shared memory exceeds the per-CTA limit");
+
+// One thread's block: at most kLeafCap runs, their pieces in shared memory.
+// Pieces carry absolute term indices.
+struct Leaf {
   double s;                   // speculative value between runs
   double st0, st1, t0, t1;    // open run
   double lo0, hi0, lo1, hi1;  // min distance to the lower / upper bound of the current binade
@@ -126,9 +132,9 @@ struct LaneSpec {
   double xpre;
   int k0, np, npre;
   bool open, ok1, full;
-  Piece* out;                 // kLanePieces slots
+  Piece* out;
 
-  __device__ void init(double shat, Piece* o) {
+  __device__ __forceinline__ void init(double shat, Piece* o) {
     s = shat;
     open = full = false;
     np = npre = 0;
@@ -139,20 +145,24 @@ struct LaneSpec {
     if (npre == 0) xpre = x;
     ++npre;
   }
-  // a run value may move to any binade of the start's sign between the
-  // start binade and 2^-968 (downwards the grids get finer)
+  // a run value may be of either sign and in any binade between 2^-968 and
+  // the start's: the true path is the run shifted by delta, and rounding
+  // commutes with the shift while both paths' values share a binade (the
+  // signed margins below) and delta is a multiple of 2 ulp of that binade
+  // (every binade at or below the start's)
   __device__ __forceinline__ bool inside(double v) const {
-    const long long b = dbits(v);
-    const int ex = static_cast<int>((b >> 52) & 0x7ff);
-    return ((b ^ bst) >= 0) && ex > 54 && ex <= static_cast<int>((bst >> 52) & 0x7ff);
+    const int ex = static_cast<int>((dbits(v) >> 52) & 0x7ff);
+    return ex > 54 && ex <= static_cast<int>((bst >> 52) & 0x7ff);
   }
-  __device__ __forceinline__ static void margins(double v, double& lo, double& hi) {
+  // the shifts delta keeping v + delta in v's binade: delta > -dneg, < dpos
+  __device__ __forceinline__ static void smargins(double v, double& dneg, double& dpos) {
     const double a = fabs(v);
     const double lb = __longlong_as_double(dbits(a) & 0x7ff0000000000000ll);
-    lo = fmin(lo, dsub(a, lb));            // exact: same binade
-    hi = fmin(hi, dsub(dadd(lb, lb), a));  // exact
+    const double below = dsub(a, lb), above = dsub(dadd(lb, lb), a);  // exact
+    dneg = fmin(dneg, v > 0.0 ? below : above);
+    dpos = fmin(dpos, v > 0.0 ? above : below);
   }
-  __device__ bool try_open(int k) {
+  __device__ __forceinline__ bool try_open(int k) {
     const int ex = static_cast<int>((dbits(s) >> 52) & 0x7ff);
     if (ex <= 54 || ex >= 0x7fe) return false;  // zero, tiny or huge: serial term
     bst = dbits(s);
@@ -167,26 +177,29 @@ struct LaneSpec {
     t0 = st0;
     t1 = st1;
     lo0 = hi0 = lo1 = hi1 = dinf();
-    margins(t0, lo0, hi0);
-    margins(t1, lo1, hi1);
+    smargins(t0, lo0, hi0);
+    smargins(t1, lo1, hi1);
     ok1 = true;
     k0 = k;
     open = true;
     return true;
   }
-  __device__ void close(int k1) {
+  __device__ __forceinline__ void close(int k1) {
     Piece& p = out[np++];
     p.st[0] = st0;
     p.st[1] = st1;
     p.en[0] = t0;
     p.en[1] = t1;
+    // lo / hi: allowed negative / positive shift of the start; the piece
+    // stores the allowed shift of |s| (sign of the start), 2 ulp kept in reserve
     const double inf = dinf();
     const bool v0 = lo0 >= u2 && hi0 >= u2;
     const bool v1 = ok1 && lo1 >= u2 && hi1 >= u2;
-    p.dlo[0] = v0 ? dsub(u2, lo0) : inf;
-    p.dhi[0] = v0 ? dsub(hi0, u2) : -inf;
-    p.dlo[1] = v1 ? dsub(u2, lo1) : inf;
-    p.dhi[1] = v1 ? dsub(hi1, u2) : -inf;
+    const bool pos = st0 > 0.0;
+    p.dlo[0] = v0 ? dsub(u2, pos ? lo0 : hi0) : inf;
+    p.dhi[0] = v0 ? dsub(pos ? hi0 : lo0, u2) : -inf;
+    p.dlo[1] = v1 ? dsub(u2, pos ? lo1 : hi1) : inf;
+    p.dhi[1] = v1 ? dsub(pos ? hi1 : lo1, u2) : -inf;
     p.xpre = xpre;
     p.k0 = k0;
     p.k1 = k1;
@@ -195,12 +208,10 @@ struct LaneSpec {
     open = false;
     npre = 0;
     s = t0;
-    if (np == kLanePieces) full = true;
+    if (np == kLeafCap) full = true;
   }
   __device__ __forceinline__ void step(double x, int k) {
-    // +-0 terms leave every partial sum unchanged (the sums are never -0
-    // under round-to-nearest), for the true path as for the runs
-    if (full || x == 0.0) return;
+    if (full || x == 0.0) return;  // +-0 terms leave every partial sum unchanged
     if (!open && !try_open(k)) {
       s = dadd(s, x);
       serial(x);
@@ -217,22 +228,82 @@ struct LaneSpec {
     ok1 = ok1 && inside(n1);
     t0 = n0;
     t1 = n1;
-    margins(n0, lo0, hi0);
-    margins(n1, lo1, hi1);
-  }
-  __device__ int finish(int len) {
-    if (open && !full) close(len);
-    return np;
+    smargins(n0, lo0, hi0);
+    smargins(n1, lo1, hi1);
   }
 };
 
-// Continue `cur` (a piece ending where `nx` starts, no serial term between):
-// per parity run of cur whose end lies in nx's range for the matching parity,
-// the continued run is concrete (its end is nx's end shifted, exact) and its
-// shift range narrows. cur is updated only when at least one parity run
-// continues (returns true); otherwise it is left as it was.
-__device__ __forceinline__ bool chain_piece(Piece& cur, const Piece& nx) {
+// The reference's additions over v[k0, k1) by a whole warp (every lane
+// carries the same s), 128 terms per round trip; zero terms cost nothing.
+__device__ __forceinline__ double serial_warp4(double s, const double* __restrict__ v, int k0,
+                                               int k1) {
+  const int lane = threadIdx.x & 31;
+  for (int b = k0; b < k1; b += 128) {
+    double t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = b + 32 * j + lane;
+      t[j] = k < k1 ? __ldcg(v + k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      unsigned nzm = __ballot_sync(0xffffffffu, t[j] != 0.0);
+      while (nzm) {
+        const int q = __ffs(nzm) - 1;
+        nzm &= nzm - 1u;
+        s = dadd(s, __shfl_sync(0xffffffffu, t[j], q));
+      }
+    }
+  }
+  return s;
+}
+
+// kBatch terms v[kb, kb + kBatch) (zeros past k1), with 16-byte loads where
+// the batch is whole (v 16-byte aligned): half the L1 wavefronts of a warp
+// whose lanes read distinct blocks.
+__device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t kb, int64_t k1,
+                                           double (&x)[kBatch]) {
+  if (kb + kBatch <= k1) {
+    if ((kb & 1) == 0) {
+      const double2* p = reinterpret_cast<const double2*>(v + kb);
+#pragma unroll
+      for (int q = 0; q < kBatch / 2; ++q) {
+        const double2 t = __ldcg(p + q);
+        x[2 * q] = t.x;
+        x[2 * q + 1] = t.y;
+      }
+    } else {
+      x[0] = __ldcg(v + kb);
+      const double2* p = reinterpret_cast<const double2*>(v + kb + 1);
+#pragma unroll
+      for (int q = 0; q < kBatch / 2 - 1; ++q) {
+        const double2 t = __ldcg(p + q);
+        x[1 + 2 * q] = t.x;
+        x[2 + 2 * q] = t.y;
+      }
+      x[kBatch - 1] = __ldcg(v + kb + kBatch - 1);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) x[q] = kb + q < k1 ? __ldcg(v + kb + q) : 0.0;
+  }
+}
+
+// Terms per thread of a chain of len terms over P threads: odd, so threads
+// reading their blocks from a staged slice hit distinct shared-memory banks.
+__host__ __device__ __forceinline__ int64_t block_len(int64_t len, int P) {
+  return ((len + P - 1) / P) | 1;
+}
+
+// Continue `cur` through `nx` (adjacent, no serial term between): per parity
+// run of cur whose end lies in nx's start binade and range, the continued run
+// is concrete (its end is nx's end shifted, exact) and its shift range
+// narrows. Runs may change sign (the shift ranges are kept relative to each
+// piece's start sign, so a sign change between cur's start and nx's start
+// mirrors nx's range). cur is updated only when a parity run continues.
+__device__ __forceinline__ bool chain2(Piece& cur, const Piece& nx) {
   const long long bn0 = dbits(nx.st[0]);
+  const bool same = (cur.st[0] < 0.0) == (nx.st[0] < 0.0);
   double en[2], lo[2], hi[2];
   bool any = false;
 #pragma unroll
@@ -252,8 +323,8 @@ __device__ __forceinline__ bool chain_piece(Piece& cur, const Piece& nx) {
     const double c = dsub(e, nst);  // exact
     const double C = e < 0.0 ? -c : c;
     if (!(C >= nlo && C <= nhi)) continue;
-    const double l = fmax(cur.dlo[r], __dsub_ru(nlo, C));
-    const double h = fmin(cur.dhi[r], __dsub_rd(nhi, C));
+    const double l = fmax(cur.dlo[r], same ? __dsub_ru(nlo, C) : __dsub_ru(C, nhi));
+    const double h = fmin(cur.dhi[r], same ? __dsub_rd(nhi, C) : __dsub_rd(C, nlo));
     if (!(l <= h)) continue;
     en[r] = dadd(nen, c);  // exact: the run continued through nx's terms
     lo[r] = l;
@@ -272,20 +343,19 @@ __device__ __forceinline__ bool chain_piece(Piece& cur, const Piece& nx) {
   return any;
 }
 
-// Chain a list of units (the lanes of a segment in phase B, the segments of a
-// group in phase C1): each unit has `np` pieces (k relative to the list) and
-// `tail` nonzero serial terms after them (tail >= 2: unknown, replay; the one
-// value in tailx when 1). Consecutive pieces with no serial term between are
-// continued (chain_piece). One thread. Writes the list's pieces to out and
-// returns their count; the list's own tail in *tail / *tailx.
+// Chain a list of units (the leaves of a warp, the warp lists of a CTA): each
+// unit has `np` pieces and `tail` nonzero serial terms after them (tail >= 2:
+// unknown, replay; the one value in tailx when 1). Consecutive pieces with no
+// serial term between are continued (chain2). One thread. Writes the list's
+// pieces to out and returns their count; the list's own tail in *tail / *tailx.
 template <typename Unit>
-__device__ __forceinline__ int compose(int nunits, Unit unit, Piece* __restrict__ out, int cap,
-                                       int* tail, double* tailx) {
+__device__ __forceinline__ int compose2(int nunits, Unit unit, Piece* __restrict__ out, int cap,
+                                        int* tail, double* tailx) {
   int no = 0;
   bool have = false, stopped = false;
   Piece cur;
-  int pend = 0;        // nonzero serial terms pending before the next piece
-  double pendx = 0.0;  // their value when exactly one
+  int pend = 0;
+  double pendx = 0.0;
   for (int q = 0; q < nunits && !stopped; ++q) {
     int nq, tq;
     double xq;
@@ -296,10 +366,10 @@ __device__ __forceinline__ int compose(int nunits, Unit unit, Piece* __restrict_
       if (npre == 1 && pend == 1) nx.xpre = pendx;
       nx.npre = npre;
       pend = 0;
-      if (have && npre == 0 && chain_piece(cur, nx)) continue;
+      if (have && npre == 0 && chain2(cur, nx)) continue;
       if (have) {
         out[no++] = cur;
-        if (no == cap) {  // out of slots: the rest is serial
+        if (no == cap) {
           have = false;
           stopped = true;
           break;
@@ -319,414 +389,306 @@ __device__ __forceinline__ int compose(int nunits, Unit unit, Piece* __restrict_
   return no;
 }
 
-// Phase B for one segment by one warp: the segment is staged in shared
-// memory (coalesced), each lane runs its sub-range from its approximate start
-// (a warp scan of the lane sub-sums), lane 0 chains the lanes' runs.
-__device__ __forceinline__ void spec_segment_warp(const double* __restrict__ v, int len,
-                                                  double shat, Piece* __restrict__ out,
-                                                  int* __restrict__ np_out,
-                                                  int* __restrict__ tail_out,
-                                                  double* __restrict__ tailx_out, double* stage,
-                                                  Piece* lp, int* lnp, int* ltail, double* lxt) {
-  const int lane = threadIdx.x & 31;
-  const bool staged = len <= kStage;
+// Thread g's block of a chain of len terms over P threads.
+__device__ __forceinline__ void block_of(int64_t len, int P, int g, int64_t& k0, int64_t& k1) {
+  const int64_t b = block_len(len, P);
+  k0 = min(len, static_cast<int64_t>(g) * b);
+  k1 = min(len, k0 + b);
+}
+
+// ---- engine phases, each a separate (non-inlined) function: the serial parts
+// run in one or a few warps, and a compact hot loop stays in the instruction
+// cache (an inlined engine is tens of thousands of instructions)
+
+// This thread's approximate block sum of chain c (phase 1).
+static __device__ __noinline__ double block_sum(const Smem2& sm, int c, int P, int g, bool staged,
+                                                int64_t slo) {
+  int64_t k0, k1;
+  block_of(sm.ch[c].len, P, g, k0, k1);
+  double s = 0.0;
   if (staged) {
-    __syncwarp();
-    const int n2 = len / 2;
-    const double2* v2 = reinterpret_cast<const double2*>(v);
-    double2* s2 = reinterpret_cast<double2*>(stage);
-#pragma unroll 4
-    for (int i = lane; i < n2; i += 32) s2[i] = __ldcg(v2 + i);
-    if ((len & 1) && lane == 0) stage[len - 1] = __ldcg(v + len - 1);
-    __syncwarp();
-  }
-  const double* src = staged ? stage : v;
-  const int sb = ((len + 31) / 32) | 1;  // odd stride: no shared-memory bank conflicts
-  const int b = min(len, lane * sb), e = min(len, b + sb);
-  double sum = 0.0;
-  for (int i = b; i < e; ++i) sum += src[i];
-  double incl = sum;
+#pragma unroll 1
+    for (int64_t k = k0; k < k1; ++k) s += sm.stage[k - slo];
+  } else {
+    const double* __restrict__ v = sm.ch[c].terms;
+#pragma unroll 1
+    for (int64_t kb = k0; kb < k1; kb += kBatch) {
+      double x[kBatch];
+      load_batch(v, kb, k1, x);
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  LaneSpec sp;
-  sp.init(lane == 0 ? shat : shat + (incl - sum), lp + lane * kLanePieces);
-  int i = b;
-  for (; i + 4 <= e; i += 4) {
-    const double x0 = src[i], x1 = src[i + 1], x2 = src[i + 2], x3 = src[i + 3];
-    sp.step(x0, i);
-    sp.step(x1, i + 1);
-    sp.step(x2, i + 2);
-    sp.step(x3, i + 3);
-  }
-  for (; i < e; ++i) sp.step(src[i], i);
-  lnp[lane] = sp.finish(e);
-  ltail[lane] = sp.full ? 2 : sp.npre;  // nonzero serial terms after the lane's last run
-  lxt[lane] = sp.xpre;
-  __syncwarp();
-  if (lane == 0) {
-    int t;
-    double tx;
-    *np_out = compose(
-        32,
-        [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
-          nq = lnp[q];
-          tq = ltail[q];
-          xq = lxt[q];
-          return lp + q * kLanePieces;
-        },
-        out, kMaxPieces, &t, &tx);
-    *tail_out = t;
-    *tailx_out = tx;
-  }
-  __syncwarp();
-}
-
-// A piece written by another CTA of the cluster (through L2).
-__device__ __forceinline__ Piece load_piece(const Piece* q) {
-  const double2* d = reinterpret_cast<const double2*>(q);
-  const double2 a = __ldcg(d), b = __ldcg(d + 1), c = __ldcg(d + 2), e = __ldcg(d + 3);
-  const double2 f = __ldcg(d + 4);
-  const int2 k = __ldcg(reinterpret_cast<const int2*>(d + 5));
-  Piece p;
-  p.st[0] = a.x;
-  p.st[1] = a.y;
-  p.en[0] = b.x;
-  p.en[1] = b.y;
-  p.dlo[0] = c.x;
-  p.dlo[1] = c.y;
-  p.dhi[0] = e.x;
-  p.dhi[1] = e.y;
-  p.xpre = f.x;
-  p.k0 = __double_as_longlong(f.y) & 0xffffffff;
-  p.k1 = static_cast<int>(static_cast<unsigned long long>(__double_as_longlong(f.y)) >> 32);
-  p.npre = k.x;
-  p.pad = 0;
-  return p;
-}
-
-// Serial terms v[k0, k1) added to s by a whole warp (loads by all lanes,
-// every lane carries the same s; all-zero blocks cost no additions).
-__device__ __forceinline__ double serial_warp(double s, const double* __restrict__ v, int k0,
-                                              int k1) {
-  const int lane = threadIdx.x & 31;
-  for (int b = k0; b < k1; b += 32) {
-    const double t = b + lane < k1 ? __ldcg(v + b + lane) : 0.0;
-    unsigned nzm = __ballot_sync(0xffffffffu, t != 0.0);
-    SEQ_CNT(13, lane == 0 ? __popc(nzm) : 0);
-    while (nzm) {
-      const int q = __ffs(nzm) - 1;
-      nzm &= nzm - 1u;
-      s = dadd(s, __shfl_sync(0xffffffffu, t, q));
+      for (int q = 0; q < kBatch; ++q) s += x[q];
     }
   }
   return s;
 }
 
-// The serial terms before a piece (npre nonzero ones in [k, p.k0)).
-__device__ __forceinline__ double pre_terms(double s, const Piece& p, const double* v, int k) {
-  if (p.npre == 1) return dadd(s, p.xpre);
-  if (p.npre > 1) return serial_warp(s, v, k, p.k0);
+// This thread's leaf of chain c from the approximate start shat (phase 2).
+static __device__ __noinline__ void run_leaf(Smem2& sm, int c, int P, int g, bool staged,
+                                             int64_t slo, double shat) {
+  int64_t k0, k1;
+  block_of(sm.ch[c].len, P, g, k0, k1);
+  Leaf lf;
+  lf.init(shat, sm.lp[threadIdx.x]);
+  if (staged) {
+#pragma unroll 1
+    for (int64_t k = k0; k < k1; ++k) lf.step(sm.stage[k - slo], static_cast<int>(k));
+  } else {
+    const double* __restrict__ v = sm.ch[c].terms;
+#pragma unroll 1
+    for (int64_t kb = k0; kb < k1; kb += kBatch) {
+      double x[kBatch];
+      load_batch(v, kb, k1, x);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) lf.step(x[q], static_cast<int>(kb + q));
+    }
+  }
+  if (lf.open && !lf.full) lf.close(static_cast<int>(k1));
+  sm.lnp[threadIdx.x] = lf.np;
+  sm.ltl[threadIdx.x] = Tail{lf.full ? 2 : lf.npre, lf.xpre};
+}
+
+// The warp's piece list over its 32 leaves (phase 3, one lane).
+static __device__ __noinline__ void compose_warp(Smem2& sm, int c, int warp) {
+  int t;
+  double tx;
+  const int base = warp * 32;
+  sm.wnp[c][warp] = compose2(
+      32,
+      [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
+        nq = sm.lnp[base + q];
+        tq = sm.ltl[base + q].n;
+        xq = sm.ltl[base + q].x;
+        return sm.lp[base + q];
+      },
+      sm.wl[c][warp], kWarpCap, &t, &tx);
+  sm.wtl[c][warp] = Tail{t, tx};
+}
+
+// The CTA's list over its warp lists (phase 3, one lane per chain); -1 when
+// it would not fit (the stitch then takes the warp lists).
+static __device__ __noinline__ void compose_cta(Smem2& sm, int c) {
+  int tot = 0;
+  for (int q = 0; q < kWarps; ++q) tot += sm.wnp[c][q];
+  if (tot > kCtaCap) {
+    sm.cnp[c] = -1;
+    return;
+  }
+  int t;
+  double tx;
+  sm.cnp[c] = compose2(
+      kWarps,
+      [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
+        nq = sm.wnp[c][q];
+        tq = sm.wtl[c][q].n;
+        xq = sm.wtl[c][q].x;
+        return sm.wl[c][q];
+      },
+      sm.cl[c], kCtaCap, &t, &tx);
+  sm.ctl[c] = Tail{t, tx};
+}
+
+// The reference's additions over v[k0, k1) by a whole warp (every lane
+// carries s), 128 terms per round trip; zero terms cost nothing.
+static __device__ __noinline__ double serial_terms(double s, const double* __restrict__ v, int k0,
+                                                   int k1) {
+  return serial_warp4(s, v, k0, k1);
+}
+
+// s through np staged pieces over terms [k, kend), then the list's tail (one
+// warp, every lane carries s).
+static __device__ __noinline__ double apply_list(double s, const Piece* __restrict__ stg, int np,
+                                                 Tail tl, int k, int kend,
+                                                 const double* __restrict__ terms) {
+#pragma unroll 1
+  for (int i = 0; i < np; ++i) {
+    // every field loaded before s is needed (the loads do not depend on s)
+    const Piece& p = stg[i];
+    const double st0 = p.st[0], st1 = p.st[1], en0 = p.en[0], en1 = p.en[1];
+    const double lo0 = p.dlo[0], lo1 = p.dlo[1], hi0 = p.dhi[0], hi1 = p.dhi[1];
+    const double xpre = p.xpre;
+    const int npre = p.npre, pk0 = p.k0, pk1 = p.k1;
+    if (npre == 1) {
+      s = dadd(s, xpre);
+    } else if (npre > 1) {
+      s = serial_terms(s, terms, k, pk0);
+    }
+    // the piece applies iff s is in its start binade and its shift in range:
+    // then the true path is the run translated (exact)
+    const long long bs = dbits(s), b0 = dbits(st0);
+    const bool odd = ((bs ^ b0) & 1) != 0;
+    const double delta = dsub(s, odd ? st1 : st0);
+    const double sh = s < 0.0 ? -delta : delta;
+    const bool ok = (((bs ^ b0) >> 52) == 0) && sh >= (odd ? lo1 : lo0) && sh <= (odd ? hi1 : hi0);
+    s = ok ? dadd(odd ? en1 : en0, delta) : serial_terms(s, terms, pk0, pk1);
+    k = pk1;
+  }
+  if (tl.n == 1) {
+    s = dadd(s, tl.x);
+  } else if (tl.n > 1) {
+    s = serial_terms(s, terms, k, kend);
+  }
   return s;
 }
 
-// One chain of the engine: `terms` materialised (len doubles), start s_init.
-struct Chain {
-  const double* terms;
-  int64_t len;
-  double s_init;
-  int B, P;
-};
-
-// Per-chain scratch in global memory.
-struct Scratch {
-  double* segsum;  // [chain][seg]
-  Piece* pieces;   // [chain][seg][kMaxPieces]
-  int* np;         // [chain][seg]
-  int* tail;       // [chain][seg]
-  double* tailx;   // [chain][seg]
-  Piece* gpieces;  // [chain][group][kMaxGPieces]
-  int* gnp;        // [chain][group]
-  int* gtail;      // [chain][group]
-  double* gtailx;  // [chain][group]
-};
-
-// Warp-level Phase A: segment sum (any order, coalesced 16-byte loads).
-__device__ __forceinline__ double warp_seg_sum(const double* __restrict__ v, int len) {
+// Phase 4 for chain c (one warp): every CTA's list in order from the exact
+// start, each staged into shared memory in one round trip (a CTA whose list
+// did not fit: its warp lists).
+static __device__ __noinline__ double stitch(Smem2& sm, int c, int P) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
   const int lane = threadIdx.x & 31;
-  const double2* v2 = reinterpret_cast<const double2*>(v);
-  double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-  for (int i = lane; i < len / 2; i += 32) {
-    const double2 t = __ldcg(v2 + i);
-    a0 += t.x;
-    a1 += t.y;
-  }
-  if ((len & 1) && lane == 0) a0 += __ldcg(v + len - 1);
-  double acc = a0 + a1;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc;
-}
-
-// Shared-memory layout of the engine inside a cluster kernel.
-struct EngineSmem {
-  double shat[kMaxChains][kMaxSegs];
-  union {
-    double stage[kBWarps][kStage];           // phase B: the segment's terms
-    Piece gbuf[kBWarps][kGroup * kMaxPieces];  // phase C1: the group's pieces
-  } u;
-  Piece lp[kBWarps][32 * kLanePieces];  // phase B: the lanes' runs
-  int lnp[kBWarps][32];
-  int ltail[kBWarps][32];
-  double lxt[kBWarps][32];
-  int gnp[kBWarps][kGroup], gtl[kBWarps][kGroup];
-  double gtx[kBWarps][kGroup];
-  Piece pbuf[kMaxChains][32];  // phase C2 batches
-  int psg[kMaxChains][32];
-  double res[kMaxChains];
-  double wsum[kThreads / 32 + 1];
-};
-
-// Phase C1 for one group of segments by one warp: the group's pieces are
-// loaded into shared memory by all lanes, lane 0 chains them across the
-// segment boundaries (k made relative to the group).
-__device__ __forceinline__ void chain_group_warp(const Scratch& sc, int c, int g, int P, int B,
-                                                 Piece* gbuf, int* gnp, int* gtl, double* gtx) {
-  const int lane = threadIdx.x & 31;
-  const int p0 = g * kGroup, ns = min(kGroup, P - p0);
-  if (lane < ns) {
-    gnp[lane] = __ldcg(sc.np + c * kMaxSegs + p0 + lane);
-    gtl[lane] = __ldcg(sc.tail + c * kMaxSegs + p0 + lane);
-    gtx[lane] = __ldcg(sc.tailx + c * kMaxSegs + p0 + lane);
-  }
-  __syncwarp();
-  for (int t = lane; t < ns * kMaxPieces; t += 32) {
-    const int q = t / kMaxPieces, i = t % kMaxPieces;
-    if (i < gnp[q]) {
-      Piece pc = load_piece(sc.pieces + (static_cast<int64_t>(c) * kMaxSegs + p0 + q) * kMaxPieces + i);
-      pc.k0 += q * B;
-      pc.k1 += q * B;
-      gbuf[t] = pc;
-    }
-  }
-  __syncwarp();
-  if (lane == 0) {
-    int t;
-    double tx;
-    sc.gnp[c * kMaxGroups + g] = compose(
-        ns,
-        [&](int q, int& nq, int& tq, double& xq) -> const Piece* {
-          nq = gnp[q];
-          tq = gtl[q];
-          xq = gtx[q];
-          return gbuf + q * kMaxPieces;
-        },
-        sc.gpieces + (static_cast<int64_t>(c) * kMaxGroups + g) * kMaxGPieces, kMaxGPieces, &t,
-        &tx);
-    sc.gtail[c * kMaxGroups + g] = t;
-    sc.gtailx[c * kMaxGroups + g] = tx;
-  }
-  __syncwarp();
-}
-
-// Phase C2 of one chain by one warp: the groups' pieces, 32 at a time, in one
-// round trip into shared memory; every lane applies them in order (the same
-// s in every lane). Returns the sum.
-__device__ __forceinline__ double stitch_chain_warp(const Chain& C, const Scratch& sc, int c,
-                                                    Piece* pbuf, int* psg) {
-  const int lane = threadIdx.x & 31;
-  const int NG = (C.P + kGroup - 1) / kGroup;
-  const int64_t GL = static_cast<int64_t>(kGroup) * C.B;  // terms per group
-  double s = C.s_init;
-  for (int g0 = 0; g0 < NG; g0 += 32) {
-    const int ng = min(32, NG - g0);
-    const int npv = lane < ng ? __ldcg(sc.gnp + c * kMaxGroups + g0 + lane) : 0;
-    const int tlv = lane < ng ? __ldcg(sc.gtail + c * kMaxGroups + g0 + lane) : 0;
-    const double txv = lane < ng ? __ldcg(sc.gtailx + c * kMaxGroups + g0 + lane) : 0.0;
-    int incl = npv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int excl = incl - npv;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int cur = 0, k = 0;  // group (within the batch) and term reached in it
-    auto finish_group = [&](int gi) {  // the group's tail after its last piece
-      const int tl = __shfl_sync(0xffffffffu, tlv, gi);
-      const double tx = __shfl_sync(0xffffffffu, txv, gi);
-      if (tl == 1) {
-        s = dadd(s, tx);
-      } else if (tl > 1) {
-        const int64_t gb = (g0 + gi) * GL;
-        s = serial_warp(s, C.terms + gb, k, static_cast<int>(min(C.len - gb, GL)));
-      }
-    };
-    for (int base = 0; base < total; base += 32) {
-      const int t = base + lane;
-      int sg = 0;
-      for (int q = 0; q < ng; ++q) {
-        const int e = __shfl_sync(0xffffffffu, excl, q);
-        const int nq = __shfl_sync(0xffffffffu, npv, q);
-        if (nq > 0 && e <= t) sg = q;
-      }
-      const int my_excl = __shfl_sync(0xffffffffu, excl, sg);
+  const int ncta = static_cast<int>(cl.num_blocks());
+  const Chain2 C = sm.ch[c];
+  const int64_t bt = block_len(C.len, P);  // terms per thread
+  double s = C.s0;
+  Piece* stg = sm.st[c];
+#pragma unroll 1
+  for (int r = 0; r < ncta; ++r) {
+    const int np = *cl.map_shared_rank(&sm.cnp[c], r);
+    const int k0 = static_cast<int>(min(C.len, static_cast<int64_t>(r) * kT * bt));
+    const int k1 = static_cast<int>(min(C.len, static_cast<int64_t>(r + 1) * kT * bt));
+    if (np >= 0) {
+      const Tail tl = *cl.map_shared_rank(&sm.ctl[c], r);
       __syncwarp();
-      if (t < total) {
-        pbuf[lane] = load_piece(sc.gpieces + (static_cast<int64_t>(c) * kMaxGroups + g0 + sg) * kMaxGPieces +
-                                (t - my_excl));
-        psg[lane] = sg;
-      }
+      if (lane < np) stg[lane] = *cl.map_shared_rank(&sm.cl[c][lane], r);
+      if (lane + 32 < np) stg[lane + 32] = *cl.map_shared_rank(&sm.cl[c][lane + 32], r);
       __syncwarp();
-      const int mcount = min(32, total - base);
-      for (int i = 0; i < mcount; ++i) {
-        const int gi = psg[i];
-        while (cur < gi) {
-          finish_group(cur);
-          ++cur;
-          k = 0;
-        }
-        const Piece& p = pbuf[i];
-        const double* v = C.terms + (g0 + cur) * GL;
-        s = pre_terms(s, p, v, k);
-        SEQ_CNT(8, lane == 0);
-        if (!try_apply(s, p)) {
-          SEQ_CNT(9, lane == 0);
-          s = serial_warp(s, v, p.k0, p.k1);
-        }
-        k = p.k1;
-      }
+      s = apply_list(s, stg, np, tl, k0, k1, C.terms);
+      continue;
     }
-    for (; cur < ng; ++cur) {
-      finish_group(cur);
-      k = 0;
+    if (cl.block_rank() == 0 && lane == 0) SEQ_CNT(11, 1);
+#pragma unroll 1
+    for (int w = 0; w < kWarps; ++w) {  // the CTA's list did not fit: its warp lists
+      const int wn = *cl.map_shared_rank(&sm.wnp[c][w], r);
+      const Tail wt = *cl.map_shared_rank(&sm.wtl[c][w], r);
+      __syncwarp();
+      if (lane < wn) stg[lane] = *cl.map_shared_rank(&sm.wl[c][w][lane], r);
+      __syncwarp();
+      const int w0 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32) * bt));
+      const int w1 = static_cast<int>(min(C.len, static_cast<int64_t>(r * kT + w * 32 + 32) * bt));
+      s = apply_list(s, stg, wn, wt, w0, w1, C.terms);
     }
-    __syncwarp();
   }
   return s;
 }
 
-// The engine, called by EVERY thread of EVERY CTA of the cluster after the
-// chains' terms are written and visible cluster-wide: A (segment sums),
-// barrier, the approximate starts (each CTA for itself), B (one warp per
-// segment), barrier, C1 (one warp per group of kGroup segments), barrier, C2
-// (every CTA stitches every chain, warp c, so no barrier is needed
-// afterwards). Results in sm.res[c] after the final __syncthreads.
-static __device__ __noinline__ void engine(const Chain* ch, int nch, const Scratch& sc,
-                                       EngineSmem& sm) {
+// The engine: called by every thread of every CTA of the cluster, with
+// sm.ch[0 .. nch) set and every chain's terms written and visible
+// cluster-wide. Results in sm.res[c] after the final __syncthreads.
+//
+// Reuse across calls: a remote CTA reads this CTA's ctot between barrier 1
+// and barrier 2 of a call, and its lists after barrier 2 until it arrives at
+// barrier 1 of the next call; this CTA rewrites ctot only after barrier 2 and
+// its lists only after barrier 1 of the next call. The stitch may replay any
+// CTA's terms, so callers alternate term buffers between consecutive calls
+// (a buffer is rewritten only after the next call's barrier 1).
+static __device__ __noinline__ void engine2(int nch, Smem2& sm) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
   const int cta = static_cast<int>(cl.block_rank()), ncta = static_cast<int>(cl.num_blocks());
-  const int gw = cta * nwarps + warp, gnw = ncta * nwarps;
+  const int P = ncta * kT;
+  const int g = cta * kT + static_cast<int>(threadIdx.x);
+  if (cta == 0 && threadIdx.x == 0) SEQ_CNT(7, 1);
   SEQ_PROF_T(t_a);
-  int total = 0, gtotal = 0;
-  for (int c = 0; c < nch; ++c) {
-    total += ch[c].P;
-    gtotal += (ch[c].P + kGroup - 1) / kGroup;
+  // ---- 1. approximate block sums, CTA scan, CTA totals. A one-chain call
+  // whose CTA slice fits is first staged into shared memory with coalesced
+  // loads (per-thread blocks read from global memory touch one line per lane)
+  const int64_t slo = min(sm.ch[0].len, static_cast<int64_t>(cta) * kT * block_len(sm.ch[0].len, P));
+  const int64_t shi = min(sm.ch[0].len, slo + kT * block_len(sm.ch[0].len, P));
+  const bool staged = nch == 1 && shi - slo <= kStage;
+  if (staged) {
+    const double* __restrict__ src = sm.ch[0].terms + slo;
+    const int n = static_cast<int>(shi - slo);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n; i += kT) sm.stage[i] = __ldcg(src + i);
+    __syncthreads();
   }
-  for (int job = gw; job < total; job += gnw) {  // A: segment sums
-    int c = 0, p = job;
-    while (p >= ch[c].P) p -= ch[c++].P;
-    const int64_t b = static_cast<int64_t>(p) * ch[c].B;
-    const int len = static_cast<int>(min(ch[c].len - b, static_cast<int64_t>(ch[c].B)));
-    const double s = warp_seg_sum(ch[c].terms + b, len);
-    if (lane == 0) sc.segsum[c * kMaxSegs + p] = s;
+  double excl[kMaxCh];
+#pragma unroll
+  for (int c = 0; c < kMaxCh; ++c) {
+    excl[c] = 0.0;
+    if (c >= nch) continue;
+    const double s = block_sum(sm, c, P, g, staged, slo);
+    double incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) sm.wsum[c][warp] = incl;
+    excl[c] = incl - s;
+  }
+  __syncthreads();
+  if (warp < nch) {  // warp c scans chain c's warp totals
+    const double w = lane < kWarps ? sm.wsum[warp][lane] : 0.0;
+    double wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kWarps) sm.wsum[warp][lane] = wi - w;
+    if (lane == kWarps - 1) sm.ctot[warp] = wi;
   }
   SEQ_PROF_T(t_b);
-  cl.sync();
+  cl.sync();  // barrier 1: CTA totals visible cluster-wide
   SEQ_PROF_T(t_c);
-  for (int c = 0; c < nch; ++c) {  // approximate starts: exclusive prefix (per CTA)
-    const int P = ch[c].P;
-    double carry = ch[c].s_init;
-    for (int base = 0; base < P; base += kThreads) {
-      const int p = base + threadIdx.x;
-      const double v = p < P ? __ldcg(sc.segsum + c * kMaxSegs + p) : 0.0;
-      double incl = v;
+#ifdef GSOT_SEQ_PROF
+  unsigned long long t_runs_end = 0;
+#endif
+  // ---- 2. leaf runs from the approximate starts; 3. warp lists (lane 0)
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) sm.wsum[warp] = incl;
-      __syncthreads();
-      double wtot = 0.0;
-      if (warp == 0) {
-        const double w = lane < nwarps ? sm.wsum[lane] : 0.0;
-        double wi = w;
+  for (int c = 0; c < kMaxCh; ++c) {
+    if (c >= nch) continue;
+    double pre = lane < cta ? *cl.map_shared_rank(&sm.ctot[c], lane) : 0.0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double y = __shfl_up_sync(0xffffffffu, wi, o);
-          if (lane >= o) wi += y;
-        }
-        if (lane < nwarps) sm.wsum[lane] = wi - w;
-        wtot = __shfl_sync(0xffffffffu, wi, 31);
-        if (lane == 0) sm.wsum[kThreads / 32] = wtot;
+    for (int o = 16; o >= 1; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    const double shat = g == 0 ? sm.ch[c].s0 : sm.ch[c].s0 + (pre + (sm.wsum[c][warp] + excl[c]));
+    run_leaf(sm, c, P, g, staged, slo, shat);
+    __syncwarp();
+    SEQ_PROF_T(t_r);
+#ifdef GSOT_SEQ_PROF
+    if (c == 0) t_runs_end = t_r;
+#endif
+    if (lane == 0) {
+#ifdef GSOT_SEQ_PROF
+      const unsigned long long tw0 = clock64();
+      int lsum = 0;
+      for (int q = 0; q < 32; ++q) lsum += sm.lnp[warp * 32 + q];
+#endif
+      compose_warp(sm, c, warp);
+#ifdef GSOT_SEQ_PROF
+      if (cta == 0 && c == 0) {
+        SEQ_CNT(8, lsum);
+        SEQ_CNT(9, sm.wnp[c][warp]);
+        SEQ_CNT(12, clock64() - tw0);
+        SEQ_CNT(13, 1);
       }
-      __syncthreads();
-      if (p < P) sm.shat[c][p] = carry + (sm.wsum[warp] + (incl - v));
-      carry += sm.wsum[kThreads / 32];
-      __syncthreads();
+#endif
     }
+    __syncwarp();
   }
-  if (threadIdx.x < nch) sm.shat[threadIdx.x][0] = ch[threadIdx.x].s_init;  // exact start
-  __syncthreads();
   SEQ_PROF_T(t_d);
-  const int bw = cta * kBWarps + warp, bnw = ncta * kBWarps;  // phase B / C1 warps
-  if (warp < kBWarps)
-    for (int job = bw; job < total; job += bnw) {  // B: one warp per segment
-      int c = 0, p = job;
-      while (p >= ch[c].P) p -= ch[c++].P;
-      const int64_t b = static_cast<int64_t>(p) * ch[c].B;
-      const int len = static_cast<int>(min(ch[c].len - b, static_cast<int64_t>(ch[c].B)));
-      const int q = c * kMaxSegs + p;
-      spec_segment_warp(ch[c].terms + b, len, sm.shat[c][p],
-                        sc.pieces + static_cast<int64_t>(q) * kMaxPieces, sc.np + q, sc.tail + q,
-                        sc.tailx + q, sm.u.stage[warp], sm.lp[warp], sm.lnp[warp],
-                        sm.ltail[warp], sm.lxt[warp]);
-    }
+  __syncthreads();
+  if (warp < nch && lane == 0) compose_cta(sm, warp);
   SEQ_PROF_T(t_e);
-  cl.sync();
+  cl.sync();  // barrier 2: CTA lists visible cluster-wide
   SEQ_PROF_T(t_f);
-  if (warp < kBWarps)
-    for (int job = bw; job < gtotal; job += bnw) {  // C1: one warp per group
-      int c = 0, g = job;
-      while (g >= (ch[c].P + kGroup - 1) / kGroup) g -= (ch[c++].P + kGroup - 1) / kGroup;
-      chain_group_warp(sc, c, g, ch[c].P, ch[c].B, sm.u.gbuf[warp], sm.gnp[warp], sm.gtl[warp],
-                       sm.gtx[warp]);
-    }
-  cl.sync();
-  SEQ_PROF_T(t_g0);
-  if (warp < nch) {  // C2: stitch
-    const double s = stitch_chain_warp(ch[warp], sc, warp, sm.pbuf[warp], sm.psg[warp]);
+  // ---- 4. stitch (every CTA; warp c: chain c)
+  if (warp < nch) {
+    const double s = stitch(sm, warp, P);
     if (lane == 0) sm.res[warp] = s;
   }
   SEQ_PROF_T(t_g);
   __syncthreads();
-  SEQ_PROF_T(t_h);
-  SEQ_PROF_ADD(0, t_a, t_b);    // A
-  SEQ_PROF_ADD(1, t_b, t_c);    // barrier after A
-  SEQ_PROF_ADD(2, t_c, t_d);    // starts
-  SEQ_PROF_ADD(3, t_d, t_e);    // B (CTA 0's own jobs)
-  SEQ_PROF_ADD(4, t_e, t_f);    // barrier after B (waits for the slowest CTA)
-  SEQ_PROF_ADD(10, t_f, t_g0);  // C1 + barrier
-  SEQ_PROF_ADD(5, t_g0, t_g);   // C2 (warp 0 = chain 0's stitch)
-  SEQ_PROF_ADD(6, t_g, t_h);    // wait for the other chains' stitches
-  SEQ_PROF_ADD(7, 0ull, 1ull);  // engine calls
-}
-
-__host__ __device__ __forceinline__ Chain make_chain(const double* terms, int64_t len, double s0) {
-  Chain c;
-  c.terms = terms;
-  c.len = len;
-  c.s_init = s0;
-  c.B = seg_len(len);
-  c.P = static_cast<int>((len + c.B - 1) / c.B);
-  return c;
+  SEQ_PROF_ADD(0, t_a, t_b);  // block sums + CTA scan
+  SEQ_PROF_ADD(1, t_b, t_c);  // barrier 1
+  SEQ_PROF_ADD(2, t_c, t_d);  // starts + leaf runs + warp lists
+  SEQ_PROF_ADD(15, t_c, t_runs_end);  // starts + leaf runs of chain 0
+  SEQ_PROF_ADD(3, t_d, t_e);  // CTA list
+  SEQ_PROF_ADD(4, t_e, t_f);  // barrier 2
+  SEQ_PROF_ADD(5, t_f, t_g);  // stitch (warp 0: chain 0)
 }
 
 }  // namespace seq

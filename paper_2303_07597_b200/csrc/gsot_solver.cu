@@ -223,27 +223,6 @@ class Solver {
   const double* t_one() const { return c_->d_one; }
   // fast screened solves: the step / trial kernels also write dbeta for the screen
   bool fast_screen() const { return screened_ && !exact_; }
-  void enqueue_two_loop() {  // lbfgs.hpp:109-126
-    TwoLoopArgs A;
-    A.S = w_->S;
-    A.Y = w_->Y;
-    A.stride = w_->dim;
-    A.h = &c_->dsync->h;
-    A.g = w_->G[r_];
-    A.d = w_->d;
-    A.dim = w_->dim;
-    A.out = c_->dsync->tl;
-    c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 4.0), [&] {
-      launch_exact_two_loop(A, c_->stream);
-    });
-  }
-  void enqueue_pair() {  // res = X[r] (just accepted), previous res = X[1-r]
-    const int q = 1 - r_;
-    c_->launch(K_LBFGS, 8.0 * w_->dim * 6.0, [&] {
-      launch_exact_pair(w_->X[r_], w_->X[q], w_->G[q], w_->G[r_], w_->S, w_->Y, w_->dim,
-                        &c_->dsync->h, w_->dim, c_->sc, c_->stream);
-    });
-  }
   void enqueue_trial() {  // trial = X[r] + t d into X[1-r], evaluated into G[1-r]
     const int q = 1 - r_;
     enqueue_t();

@@ -1,5 +1,5 @@
 """GPU, exact-order mode: with the reference's own association for every
-cross-block sum and every L-BFGS dot (gsot_exact.cu), the device evaluation
+cross-block sum and every L-BFGS dot (gsot_exact2.cu), the device evaluation
 and the whole device solve are BITWISE the reference's (the oracle is
 bitwise the reference compiled against the sequential Eigen shim,
 tests/test_oracle.py): same iterates, objective, gradient calls, per-call

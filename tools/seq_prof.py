@@ -1,4 +1,4 @@
-"""Diagnostic: stitch counters of the exact-order engine (gsot_seqsum2.cuh)
+"""Diagnostic: stitch counters of the exact-order engine (gsot_seqsum.cuh)
 from a -DGSOT_SEQ_PROF build: random sums, then one exact-order solve.
 
     GSOT_LIB=paper_2303_07597_b200/lib/libgsot_seqprof.so python tools/seq_prof.py 2
