@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
 // segments and the matching alpha rows into shared memory, mbarrier
 // completion; lane 0 issues, every lane waits). A tile of at most kExD
 // segments stays resident for pass 2; a taller one is streamed again for
-// pass 2 only when it has a nonzero block. One CTA per SM, kExNW warps, each
+// pass 2 only when it has a nonzero block. One CTA per SM, kExNW warps (4 with
+// 5-slot rings, or 12 with 2-slot rings when every tile is tall anyway), each
 // an independent chunk owner (the column chains run across the groups of the
 // chunk in order). Requires L <= kExG (else k_ex_cols).
 constexpr int kExSR = 32;      // rows per segment
@@ -614,10 +615,10 @@ void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
   };
   const char* ev = std::getenv("GSOT_EXACT_COLS");
   const int pick = ev ? std::atoi(ev) : 0;
-  // every tile taller than the 5-slot ring anyway (config 5): 8 warps per SM
-  // (more chunks in flight) with 3-slot rings
+  // every tile taller than the 5-slot ring anyway (config 5): 12 warps per SM
+  // (more chunks in flight) with 2-slot rings
   if (P.L <= 256 && (pick == 2 || (pick == 0 && W.gmin > 5 * kExSR))) {
-    run(k_ex_cols2<8, 3, 256>, 8, static_cast<int>(sizeof(ExColWarp<3, 256>) * 8));
+    run(k_ex_cols2<12, 2, 256>, 12, static_cast<int>(sizeof(ExColWarp<2, 256>) * 12));
   } else if (P.L <= kExGmax) {
     run(k_ex_cols2<4, 5, kExGmax>, 4, static_cast<int>(sizeof(ExColWarp<5, kExGmax>) * 4));
   } else {

@@ -162,13 +162,14 @@ def test_sequential_sum_engine_bitwise(n):
     ctx.close()
 
 
-@pytest.mark.parametrize("sizes", [[300, 17, 170, 64, 161, 1], [700, 33]])
+@pytest.mark.parametrize("sizes", [[300, 17, 170, 64, 161, 1], [700, 33], [300, 170, 161, 700]])
 def test_exact_tall_groups_eval_and_solve_bitwise(o, sizes):
     """Groups taller than the exact column kernel's resident ring (more than 5
     segments of 32 rows: streamed twice, the second pass only for tiles with a
-    nonzero block) next to short ones and a one-row group: the exact-order
-    evaluation at several states and a 30-iteration exact solve equal the
-    oracle bit for bit."""
+    nonzero block) next to short ones and a one-row group, and an instance
+    whose groups are all tall (the 12-warp, 2-slot kernel variant): the
+    exact-order evaluation at several states and a 30-iteration exact solve
+    equal the oracle bit for bit."""
     rng = np.random.default_rng(len(sizes))
     sizes = np.array(sizes, np.int32)
     m, n = int(sizes.sum()), 200
