@@ -335,6 +335,8 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
 
 // ---------------------------------------------------------------- rows
 
+constexpr int kRowWin = 1024;  // chunks listed per window (k_ex_rows)
+
 __global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __restrict__ x,
                                                  const uint32_t* __restrict__ words,
                                                  const uint32_t* __restrict__ gmask,
@@ -342,8 +344,9 @@ __global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __r
                                                  const double* __restrict__ scale,
                                                  const int4* __restrict__ slabs, int nslabs,
                                                  double* __restrict__ grad) {
-  const int lane = threadIdx.x & 31;
-  const int sidx = blockIdx.x * 4 + (threadIdx.x >> 5);
+  extern __shared__ __align__(16) unsigned char rows_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sidx = blockIdx.x * 4 + warp;
   if (sidx >= nslabs) return;
   const int4 sl = slabs[sidx];
   const int l = sl.x, r0 = sl.y, nr = sl.z;
@@ -352,39 +355,67 @@ __global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __r
   const int64_t i = static_cast<int64_t>(o0) + r0 + lane;
   const double ai = valid ? x[i] : 0.0;
   double acc = valid ? P.a[i] : 0.0;  // grad_alpha = a (dual.hpp:91)
+  // the group's tiles with a computed nonzero block, ascending: (chunk, word),
+  // listed by the whole warp for a window of up to kRowWin chunks at a time,
+  // so the walk can load the next tile while it adds the current one
+  int2* list = reinterpret_cast<int2*>(rows_smem) + static_cast<size_t>(warp) * kRowWin;
   const int nmw = (P.nw + 31) / 32;
-  for (int w = 0; w < nmw; ++w) {
-    uint32_t cm = gmask[static_cast<int64_t>(l) * nmw + w];
-    while (cm) {
-      const int c = 32 * w + __ffs(cm) - 1;
-      cm &= cm - 1u;
-      const int64_t wi = static_cast<int64_t>(l) * P.nw + c;
-      const uint32_t nz = words[wi] & nzw[wi];
-      if (nz == 0u) continue;
-      const int64_t jk = static_cast<int64_t>(c) * 32 + lane;
-      const bool mine = (nz >> lane) & 1u;
-      const double bk = mine ? x[P.m + jk] : 0.0;
-      const double sk = mine ? scale[static_cast<int64_t>(l) * P.n + jk] : 0.0;
-      const double* __restrict__ row =
-          P.C + 32 * (static_cast<int64_t>(P.nw) * o0 + static_cast<int64_t>(c) * g + r0 + lane);
-      double cv[32];
+  const double* __restrict__ base =
+      P.C + 32 * (static_cast<int64_t>(P.nw) * o0 + r0 + lane);
+  auto load = [&](int t, double (&cv)[32], double& bk, double& sk, uint32_t& nz) {
+    const int2 e = list[t];
+    const int c = e.x;
+    nz = static_cast<uint32_t>(e.y);
+    const int64_t jk = static_cast<int64_t>(c) * 32 + lane;
+    const bool mine = (nz >> lane) & 1u;
+    bk = mine ? x[P.m + jk] : 0.0;
+    sk = mine ? scale[static_cast<int64_t>(l) * P.n + jk] : 0.0;
+    const double* __restrict__ row = base + 32 * static_cast<int64_t>(c) * g;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const double2 v = valid ? *reinterpret_cast<const double2*>(row + 2 * q)
-                                : make_double2(0.0, 0.0);
-        cv[2 * q] = v.x;
-        cv[2 * q + 1] = v.y;
+    for (int q = 0; q < 16; ++q) {
+      const double2 v = valid ? *reinterpret_cast<const double2*>(row + 2 * q) : make_double2(0.0, 0.0);
+      cv[2 * q] = v.x;
+      cv[2 * q + 1] = v.y;
+    }
+  };
+  for (int w0 = 0; w0 < nmw; w0 += kRowWin / 32) {
+    int n = 0;
+    for (int w = w0; w < min(nmw, w0 + kRowWin / 32); ++w) {
+      const uint32_t cm = gmask[static_cast<int64_t>(l) * nmw + w];
+      const int c = 32 * w + lane;
+      uint32_t nz = 0u;
+      if ((cm >> lane) & 1u) {
+        const int64_t wi = static_cast<int64_t>(l) * P.nw + c;
+        nz = words[wi] & nzw[wi];
       }
+      const uint32_t bal = __ballot_sync(0xffffffffu, nz != 0u);
+      if (nz != 0u) list[n + __popc(bal & ((1u << lane) - 1u))] = make_int2(c, static_cast<int>(nz));
+      n += __popc(bal);
+    }
+    __syncwarp();
+    double cv[32], bk = 0.0, sk = 0.0;
+    uint32_t nz = 0u;
+    if (n > 0) load(0, cv, bk, sk, nz);
+    for (int t = 0; t < n; ++t) {
+      double cn[32], bn = 0.0, sn = 0.0;
+      uint32_t nzn = 0u;
+      if (t + 1 < n) load(t + 1, cn, bn, sn, nzn);  // in flight during this tile's chain
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const double b = __shfl_sync(0xffffffffu, bk, k);
-        const double s = __shfl_sync(0xffffffffu, sk, k);
+        const double sc = __shfl_sync(0xffffffffu, sk, k);
         if ((nz >> k) & 1u) {  // grad_alpha -= gcol_j, j ascending (dual.hpp:96)
           const double f = residual(ai, b, cv[k]);
-          if (f > 0.0) acc = dsub(acc, dmul(s, f));
+          if (f > 0.0) acc = dsub(acc, dmul(sc, f));
         }
       }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) cv[k] = cn[k];
+      bk = bn;
+      sk = sn;
+      nz = nzn;
     }
+    __syncwarp();
   }
   if (valid) grad[i] = acc;
 }
@@ -625,8 +656,16 @@ void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
     k_ex_cols<<<(P.nw + 3) / 4, 128, 0, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT,
                                               W.cntj, W.nzw, grad);
   }
-  k_ex_rows<<<(W.nslabs + 3) / 4, 128, 0, s>>>(P, x, words, gmask, W.nzw, W.scale, W.slabs,
-                                                W.nslabs, grad);
+  {
+    static int attr = 0;
+    const int rsmem = static_cast<int>(sizeof(int2) * 4 * kRowWin);
+    if (attr < rsmem) {
+      GSOT_CUDA_CHECK(cudaFuncSetAttribute(k_ex_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+      attr = rsmem;
+    }
+    k_ex_rows<<<(W.nslabs + 3) / 4, 128, rsmem, s>>>(P, x, words, gmask, W.nzw, W.scale, W.slabs,
+                                                     W.nslabs, grad);
+  }
   ScalarArgs A;
   A.P = P;
   A.x = x;
