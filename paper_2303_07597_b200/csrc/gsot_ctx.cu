@@ -122,7 +122,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one, staging, d_bad};
+                  d_one, staging, d_bad, cmin, amax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ex_ready) gsot::exact_ws_free(ex);
@@ -217,6 +217,8 @@ void alloc_buffers(gsot_ctx* c) {
   c->dfull = dalloc<double>(L, t);
   c->dneg = dalloc<double>(L, t);
   c->dbeta = dalloc<double>(n, t);
+  c->cmin = dalloc<float>(static_cast<size_t>(L) * n, t);
+  c->amax = dalloc<double>(L, t);
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dsync = dalloc<gsot::DevSync>(1, t);
   GSOT_CUDA_CHECK(cudaHostAlloc(&c->h_sync, sizeof(gsot::DevSync) + 128, cudaHostAllocMapped));
@@ -330,6 +332,8 @@ void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const doubl
     throw Error(GSOT_ERR_PARTITION_MISMATCH,
                 "group partition: partition covers " + std::to_string(c->off[c->L]) +
                     " indices, cost has " + std::to_string(c->m) + " rows");
+  // the per-block minimum cost of the valid instance (provably-zero blocks)
+  c->launch(gsot::K_MISC, 8.0 * c->m * c->n, [&] { gsot::launch_block_min(c->problem(), c->cmin, c->stream); });
 }
 
 // Context cache: gsot_destroy parks a context's device state (buffers,
@@ -530,6 +534,8 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
     });
     words = c->words;
   }
+  // per-group max alpha for the provably-zero block test (k_block_min)
+  c->launch(K_MISC, 8.0 * c->m, [&] { launch_group_amax(P, d_x, c->amax, c->stream); });
   if (exact) {  // the reference's order of operations (gsot_exact2.cu)
     const bool scr = mode == GSOT_EVAL_SCREENED;
     c->launch(K_EVAL, 0.0, [&] {

@@ -95,6 +95,10 @@ struct gsot_ctx {
   // screening state
   double *snap_x = nullptr, *zs = nullptr, *ks = nullptr, *os = nullptr;
   double *dpos = nullptr, *dfull = nullptr, *dneg = nullptr, *dbeta = nullptr;
+  // provably-zero blocks: per block min cost (float, rounded down; computed
+  // once per upload) and per group max alpha (per evaluation)
+  float* cmin = nullptr;
+  double* amax = nullptr;
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;
@@ -150,6 +154,8 @@ struct gsot_ctx {
     P.tau = mu * gamma;
     P.half_inv_gamma = 0.5 / gamma;
     P.tl = tl;
+    P.cmin = cmin;
+    P.amax = amax;
     return P;
   }
 

@@ -227,6 +227,20 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
     };
     auto pump = [&](int cur) {
       while (pt < ng && head - tail < static_cast<uint32_t>(kExD) && stop_at < cur) {
+        if (ps == 0) {  // a tile whose surviving blocks are provably zero is not read
+          const int l = W.grp[pt];
+          const int64_t jj = static_cast<int64_t>(c) * 32 + lane;
+          const bool act = (W.gsw[pt] >> lane) & 1u;
+          const bool maybe =
+              act && !(dadd(P.amax[l], x[P.m + jj]) <= static_cast<double>(P.cmin[static_cast<int64_t>(l) * P.n + jj]));
+          if (!__any_sync(0xffffffffu, maybe)) {
+            __syncwarp();
+            if (lane == 0) W.grp[pt] = -1 - l;  // marked zero for the walk
+            __syncwarp();
+            ++pt;
+            continue;
+          }
+        }
         int o0, g;
         tile_geom(pt, o0, g);
         const int ns = (g + kExSR - 1) / kExSR;
@@ -245,6 +259,11 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
     double colacc = 0.0;
     int cnt = 0;
     for (int t = 0; t < ng; ++t) {
+      pump(t);  // tile t issued (or marked provably zero) before it is read
+      if (W.grp[t] < 0) {  // provably zero: no nonzero block, no psi, no column terms
+        if (lane == 0) nzw[static_cast<int64_t>(-1 - W.grp[t]) * P.nw + c] = 0u;
+        continue;
+      }
       const int l = W.grp[t];
       const uint32_t sw = W.gsw[t];
       const bool act = (sw >> lane) & 1u;

@@ -57,6 +57,10 @@ struct DevProblem {
   double gamma, mu, tau;  // tau = mu * gamma (core.hpp:70)
   double half_inv_gamma;  // 0.5 / gamma (fast-mode psi)
   unsigned long long* tl; // diagnostic timeline (GSOT_PHASE_CLOCKS builds only), else null
+  // provably-zero blocks: cmin[l * n + j] <= min_{i in l} c_ij
+  // (float, rounded down), amax[l] = max_{i in l} alpha_i (NaN if any is NaN)
+  const float* cmin;
+  const double* amax;
 };
 
 // Device scalars written by the reduction kernels and read back with one
@@ -188,6 +192,10 @@ void launch_audit_skips(const DevProblem& P, const double* x, const uint32_t* wo
 void launch_audit_active(const DevProblem& P, const double* x, const uint32_t* active_words,
                          EvalScalars* sc, cudaStream_t s);
 void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaStream_t s);
+// Provably-zero blocks: the per-block minimum cost (once per upload) and the
+// per-group maximum of alpha (per evaluation, programmatic launch).
+void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s);
+void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s);
 void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s);
 // Per-chunk group masks cmask[c][l / 32] bit l % 32: (l, c) non-empty.
 void launch_fill_cmask(uint32_t* cmask, int32_t L, int32_t nw, cudaStream_t s);
