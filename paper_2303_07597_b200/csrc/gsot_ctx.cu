@@ -122,7 +122,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one, staging, d_bad, cmin, amax};
+                  d_one, staging, d_bad, cmin, amax, snap_rows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ex_ready) gsot::exact_ws_free(ex);
@@ -218,6 +218,8 @@ void alloc_buffers(gsot_ctx* c) {
   c->dneg = dalloc<double>(L, t);
   c->dbeta = dalloc<double>(n, t);
   c->cmin = dalloc<float>(static_cast<size_t>(L) * n, t);
+  c->snap_rows = dalloc<unsigned long long>(64, t);
+  GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_rows, 0, sizeof(unsigned long long) * 64, c->stream));
   c->amax = dalloc<double>(L, t);
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dsync = dalloc<gsot::DevSync>(1, t);
@@ -587,19 +589,21 @@ EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
   return eval_result(c, mode);
 }
 
-void enqueue_snapshot(gsot_ctx* c, const double* d_x) {  // take_snapshot (screening.hpp:24-50)
+void enqueue_snapshot(gsot_ctx* c, const double* d_x, bool lazy) {  // take_snapshot (screening.hpp:24-50)
   const DevProblem P = c->problem();
   const double Ln = static_cast<double>(c->L) * c->n;
-  c->launch(K_SNAPSHOT, 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n),
-            [&] { launch_snapshot(P, d_x, c->zs, c->ks, c->os, c->stream); });
+  if (lazy) c->launch(K_MISC, 8.0 * c->m, [&] { launch_group_amax(P, d_x, c->amax, c->stream); });
+  c->launch(K_SNAPSHOT, lazy ? -2.0 : 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n),
+            [&] { launch_snapshot(P, d_x, c->zs, c->ks, c->os, lazy, c->snap_rows, c->stream); });
+  c->snap_lazy = lazy;
   if (d_x != c->snap_x)
     GSOT_CUDA_CHECK(cudaMemcpyAsync(c->snap_x, d_x, sizeof(double) * (c->m + c->n),
                                     cudaMemcpyDeviceToDevice, c->stream));
   c->have_snapshot = true;
 }
 
-void init_snapshot_device(gsot_ctx* c, const double* d_x) {  // screening.hpp:220-227
-  enqueue_snapshot(c, d_x);
+void init_snapshot_device(gsot_ctx* c, const double* d_x, bool lazy) {  // screening.hpp:220-227
+  enqueue_snapshot(c, d_x, lazy);
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->active_words, 0,
                                   sizeof(uint32_t) * static_cast<size_t>(c->L) * c->nw, c->stream));
   c->active_count = 0;
@@ -608,7 +612,7 @@ void init_snapshot_device(gsot_ctx* c, const double* d_x) {  // screening.hpp:22
 // FastGradDispatcher::refresh (screening.hpp:231-235): active set from the
 // lower bounds against the current snapshot, then the new snapshot. The
 // active-set size lands in sc->counters[0] (reset first).
-void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active) {
+void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active, bool lazy) {
   if (!c->have_snapshot) throw Error(GSOT_ERR_STATE, "refresh requires a snapshot");
   const DevProblem P = c->problem();
   c->reset_scalars();
@@ -622,11 +626,11 @@ void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active) {
                     c->stream);
     });
   }
-  enqueue_snapshot(c, d_x);
+  enqueue_snapshot(c, d_x, lazy);
 }
 
 void refresh_device(gsot_ctx* c, const double* d_x, bool use_active) {
-  enqueue_refresh(c, d_x, use_active);
+  enqueue_refresh(c, d_x, use_active, false);
   c->fetch_scalars();
   if (use_active) c->active_count = static_cast<int64_t>(c->h_sc->counters[0]);
 }
@@ -821,7 +825,7 @@ GSOT_API int gsot_init_snapshot(gsot_ctx* ctx, const double* x) {
   return guard([&] {
     checked(ctx);
     upload_x(ctx, x);
-    init_snapshot_device(ctx, ctx->x_eval);
+    init_snapshot_device(ctx, ctx->x_eval, false);
     ctx->sync();
   });
 }
@@ -839,6 +843,10 @@ GSOT_API int gsot_snapshot_norms(gsot_ctx* ctx, double* z, double* k, double* o)
   return guard([&] {
     checked(ctx);
     if (!ctx->have_snapshot) throw Error(GSOT_ERR_STATE, "no snapshot taken");
+    if (ctx->snap_lazy) {  // the solver's last snapshot skipped zero blocks: retake it in full
+      gsot::enqueue_snapshot(ctx, ctx->snap_x, false);
+      ctx->sync();
+    }
     const int64_t Ln = static_cast<int64_t>(ctx->L) * ctx->n;
     std::vector<double> tmp(static_cast<size_t>(Ln));
     double* srcs[3] = {ctx->zs, ctx->ks, ctx->os};

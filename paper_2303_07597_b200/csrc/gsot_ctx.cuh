@@ -99,6 +99,8 @@ struct gsot_ctx {
   // once per upload) and per group max alpha (per evaluation)
   float* cmin = nullptr;
   double* amax = nullptr;
+  bool snap_lazy = false;  // the current snapshot skipped provably-zero blocks
+  unsigned long long* snap_rows = nullptr;  // 64 slots: cost rows read by lazy snapshots
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;
@@ -229,7 +231,18 @@ struct gsot_ctx {
   void account(const gsot::Mark& mk) {
     float ms = 0.f;
     GSOT_CUDA_CHECK(cudaEventElapsedTime(&ms, mk.a, mk.b));
-    const double bytes = mk.bytes < 0 ? screened_eval_bytes() : mk.bytes;
+    double bytes = mk.bytes < 0 ? screened_eval_bytes() : mk.bytes;
+    if (mk.kind == gsot::K_SNAPSHOT && mk.bytes == -2.0) {  // lazy: the rows it read
+      unsigned long long rows[64];
+      GSOT_CUDA_CHECK(cudaMemcpy(rows, snap_rows, sizeof(rows), cudaMemcpyDeviceToHost));
+      GSOT_CUDA_CHECK(cudaMemset(snap_rows, 0, sizeof(rows)));
+      double r = 0.0;
+      for (unsigned long long v : rows) r += static_cast<double>(v);
+      const double Ln = static_cast<double>(L) * n;
+      bytes = 8.0 * r + 28.0 * Ln + 8.0 * (m + n);  // rows, cmin + z~ k~ o~, x
+    }
+    if (mk.kind == gsot::K_EVAL)  // rows of provably-zero blocks are not read
+      bytes -= 8.0 * static_cast<double>(h_sc->zero_rows);
     prof_ms[mk.kind] += ms;
     prof_bytes[mk.kind] += bytes;
     prof_launches[mk.kind] += 1;
@@ -311,9 +324,10 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode, double* d_grad, cons
 EvalOut eval_result(gsot_ctx* c, int mode);
 EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
                     const double* d_dir, double ub_offset, bool use_active);
-void enqueue_snapshot(gsot_ctx* c, const double* d_x);
-void init_snapshot_device(gsot_ctx* c, const double* d_x);
-void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active);
+// lazy: provably-zero blocks not read (the solver's own snapshots)
+void enqueue_snapshot(gsot_ctx* c, const double* d_x, bool lazy);
+void init_snapshot_device(gsot_ctx* c, const double* d_x, bool lazy);
+void enqueue_refresh(gsot_ctx* c, const double* d_x, bool use_active, bool lazy);
 void refresh_device(gsot_ctx* c, const double* d_x, bool use_active);
 
 template <typename T>

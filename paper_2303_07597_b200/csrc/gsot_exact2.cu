@@ -654,10 +654,19 @@ void launch_exact_eval2(const DevProblem& P, const ExactWs& W, const double* x,
     GSOT_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   }
   auto run = [&](auto kern, int nwarps, int smem) {
-    static int attr = 0;  // per instantiation of the lambda's kernel type
-    if (attr < smem) {
+    // the dynamic shared-memory attribute of each kernel variant (a plain
+    // function-pointer type is shared by the variants: key by address)
+    static std::vector<std::pair<const void*, int>> attrs;
+    int* attr = nullptr;
+    for (auto& a : attrs)
+      if (a.first == reinterpret_cast<const void*>(kern)) attr = &a.second;
+    if (!attr) {
+      attrs.emplace_back(reinterpret_cast<const void*>(kern), 0);
+      attr = &attrs.back().second;
+    }
+    if (*attr < smem) {
       GSOT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = smem;
+      *attr = smem;
     }
     const int grid = std::min(nsm, (P.nw + nwarps - 1) / nwarps);
     kern<<<grid, 32 * nwarps, smem, s>>>(P, x, words, cmask, clear_cmask, W.scale, W.psiT, W.cntj,

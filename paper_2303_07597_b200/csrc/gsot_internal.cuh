@@ -73,6 +73,7 @@ struct EvalScalars {
   unsigned long long counters[4];  // in_active, skipped, unskipped, upper_bounds
   unsigned long long surv_rows;  // sum of g_l over surviving blocks (bytes accounting)
   unsigned long long task_rows;  // sum of g_l over work-list tasks
+  unsigned long long zero_rows;  // cost rows of surviving blocks not read (provably zero)
   int ntasks;        // screened work-list length
   int next_task;     // dynamic scheduler cursor
   unsigned int ticket;  // last-block-done counter
@@ -136,8 +137,10 @@ enum KernelKind {
 
 void launch_relayout(const DevProblem& P, const double* src_colmajor, int64_t j0, int64_t ncols,
                      double* C, unsigned long long* first_bad, cudaStream_t s);
+// lazy: provably-zero blocks not read; rows_read: 64 slots counting the cost
+// rows a lazy snapshot read (bytes accounting)
 void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
-                     cudaStream_t s);
+                     bool lazy, unsigned long long* rows_read, cudaStream_t s);
 void launch_block_z(const DevProblem& P, const double* x, double* zout, cudaStream_t s);
 // Screened evaluations start from zeroed per-evaluation cursors of sc
 // (ntasks, next_task, ticket, audit fields): k_publish resets them after it

@@ -88,16 +88,41 @@ void launch_relayout(const DevProblem& P, const double* src, int64_t j0, int64_t
 // per block, each a sequential sum over the block's rows. One thread per
 // (l, j); a warp covers one 32-column tile and reads one 256-byte tile row per
 // load.
+// lazy (the solver's own snapshots): a provably-zero block (every
+// residual <= 0, so z~ = 0 and k~ == o~ bit for bit) is not read and gets
+// z~ = k~ = o~ = 0. Only the bounds read these, and with k~ == o~ the lower
+// bound ((((k~ - A) - B) - o~) - C) - D is <= 0 < tau whatever their common
+// value, as the reference's is: every decision and counter is unchanged.
+// API snapshots are taken in full (gsot_snapshot_norms returns the reference's
+// values; a lazy snapshot is retaken in full on request).
 __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __restrict__ x,
                                                   double* __restrict__ zs,
                                                   double* __restrict__ ks,
-                                                  double* __restrict__ os) {
+                                                  double* __restrict__ os, int lazy,
+                                                  unsigned long long* __restrict__ rows_read) {
+  if (lazy) pdl_wait();  // after the group maxima of x (k_group_amax)
   const int l = blockIdx.y;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= P.n) return;
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  const bool in = j < P.n;
+  const double bj = in ? x[P.m + j] : 0.0;
+  if (lazy) {
+    const bool zero = !in || dadd(P.amax[l], bj) <= (double)P.cmin[(int64_t)l * P.n + j];
+    const unsigned read = __ballot_sync(0xffffffffu, !zero);  // bytes accounting (slots)
+    if ((threadIdx.x & 31) == 0 && read)
+      atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(read) * g);
+    if (zero) {
+      if (in) {
+        const int64_t idx = (int64_t)l * P.n + j;
+        zs[idx] = 0.0;
+        ks[idx] = 0.0;
+        os[idx] = 0.0;
+      }
+      return;
+    }
+  }
+  if (!in) return;
   const double* __restrict__ al = x + o0;
-  const double bj = x[P.m + j];
   const double* __restrict__ cp = block_ptr(P, o0, g, j);
   double az = 0.0, ak = 0.0, ao = 0.0;
 #define GSOT_SNAP_STEP(ALPHA, CVAL)                 \
@@ -125,9 +150,12 @@ __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __
 }
 
 void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
-                     cudaStream_t s) {
+                     bool lazy, unsigned long long* rows_read, cudaStream_t s) {
   dim3 grid((unsigned)((P.n + 255) / 256), (unsigned)P.L);
-  k_snapshot<<<grid, 256, 0, s>>>(P, x, zs, ks, os);
+  if (lazy)
+    launch_pdl(k_snapshot, grid, dim3(256), 0, s, P, x, zs, ks, os, 1, rows_read);
+  else
+    k_snapshot<<<grid, 256, 0, s>>>(P, x, zs, ks, os, 0, rows_read);
 }
 
 // Sequential z of one block (pos_part_norm over the block rows).
@@ -739,6 +767,7 @@ struct EvalArgs {
   int* next_task;   // global claim cursor (zeroed per evaluation)
   int ntasks;       // >= 0: list length; -1: read *ntasks_dev (screened)
   const int* ntasks_dev;
+  unsigned long long* zero_rows;  // bytes accounting: cost rows not read (provably zero)
 };
 
 // consumer warps per CTA: 4, or 2 for short tiles (at most kEvalShortRows rows:
@@ -840,7 +869,10 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
           goto producer_done;
         }
         if (T.zero) {
-          if (lane == 0) mbar_arrive(&full[slot]);  // no bytes: the consumers write zeros
+          if (lane == 0) {
+            mbar_arrive(&full[slot]);  // no bytes: the consumers write zeros
+            atomicAdd(A.zero_rows, (unsigned long long)__popc(T.word) * (unsigned long long)T.g);
+          }
         } else if (lane == 0) {
           // alpha rides along with each cost segment (x is 16-byte aligned)
           const int r0 = (k < T.nseg ? k : 2 * T.nseg - 1 - k) * A.seg, rows = min(A.seg, T.g - r0);
@@ -1053,7 +1085,11 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
                  double* psi, int seg, int variant, int grid, int* next_task, cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0)
     throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
-  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev};
+  // next_task is EvalScalars::next_task: zero_rows lives in the same block
+  EvalScalars* sc = reinterpret_cast<EvalScalars*>(reinterpret_cast<char*>(next_task) -
+                                                   offsetof(EvalScalars, next_task));
+  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev,
+             &sc->zero_rows};
   const size_t smem = eval_smem_bytes(seg, 0);
   if ((int)smem > g_eval_smem_attr[variant]) eval_blocks_per_sm(smem, variant);
   launch_pdl(eval_kernel(variant), dim3(grid), dim3(eval_nthreads(variant)), smem, s, A);

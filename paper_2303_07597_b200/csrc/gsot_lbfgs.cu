@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
   if (threadIdx.x == 0) {  // one system-scope fence (cumulative over the CTA's writes)
     sc->ntasks = 0;        // the next screened evaluation starts from zeroed cursors
     sc->next_task = 0;
+    sc->zero_rows = 0ull;
     sc->ticket = 0u;
     sc->audit_violation = 0;
     sc->audit_where = 0;

@@ -74,7 +74,7 @@ class Solver {
     r_ = 0;
     GSOT_CUDA_CHECK(cudaMemsetAsync(w_->X[0], 0, sizeof(double) * dim, c_->stream));
     c_->launch(K_LBFGS, 0.0, [&] { launch_hist_reset(&c_->dsync->h, mem_, c_->stream); });
-    if (screened_) init_snapshot_device(c_, w_->X[0]);  // solver.hpp:141-144
+    if (screened_) init_snapshot_device(c_, w_->X[0], true);  // solver.hpp:141-144
     // initial gradient + objective (lbfgs.hpp:70-71): one fused evaluation
     enqueue_eval(c_, w_->X[0], mode_eval_, w_->G[0], nullptr, o_.upper_bound_offset, use_active_);
     c_->fetch_scalars();
@@ -347,7 +347,7 @@ class Solver {
   double hook_and_norm() {
     if (!screened_) return norm_inf_now();
     run_seq("RF", [&] {
-      enqueue_refresh(c_, w_->X[r_], use_active_);
+      enqueue_refresh(c_, w_->X[r_], use_active_, true);
       c_->launch(K_LBFGS, 8.0 * w_->dim, [&] {
         launch_absmax(w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
       });
