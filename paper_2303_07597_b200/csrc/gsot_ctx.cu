@@ -515,6 +515,9 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
   const DevProblem P = c->problem();
   if (mode != GSOT_EVAL_SCREENED || exact) c->reset_scalars();  // screened: zeroed by k_publish
+  // per-group max alpha for the provably-zero block test (k_block_min): read
+  // by the screen and the evaluation
+  c->launch(K_MISC, 8.0 * c->m, [&] { launch_group_amax(P, d_x, c->amax, c->stream); });
   const uint32_t* words = c->dense_words;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
@@ -532,12 +535,10 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
                     ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
                     c->cmask, fused ? d_x : nullptr, fused ? c->snap_x : nullptr,
-                    fused ? 1 : 0, c->num_sms, c->stream);
+                    fused ? 1 : 0, d_x, c->num_sms, c->stream);
     });
     words = c->words;
   }
-  // per-group max alpha for the provably-zero block test (k_block_min)
-  c->launch(K_MISC, 8.0 * c->m, [&] { launch_group_amax(P, d_x, c->amax, c->stream); });
   if (exact) {  // the reference's order of operations (gsot_exact2.cu)
     const bool scr = mode == GSOT_EVAL_SCREENED;
     c->launch(K_EVAL, 0.0, [&] {

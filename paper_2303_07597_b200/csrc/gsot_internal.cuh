@@ -159,8 +159,9 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
-                   int num_sms, cudaStream_t s);
-// Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
+                   const double* xe, int num_sms, cudaStream_t s);
+// xe: the evaluation state (the provably-zero test; P.amax must hold its
+// group maxima). Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
 size_t eval_smem_bytes(int buf_rows, int cap);
 // k_eval variant for a context: 0 in place / 4 consumer warps, 1 recomputing

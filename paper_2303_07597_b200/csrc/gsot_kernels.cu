@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 uint32_t* __restrict__ gmask,
                                                 uint32_t* __restrict__ cmask,
                                                 const double* __restrict__ x,
-                                                const double* __restrict__ xs, int dbeta_ready) {
+                                                const double* __restrict__ xs, int dbeta_ready,
+                                                const double* __restrict__ xe) {
   __shared__ double zt[kScrWarps][32][kScrHalf + 1];  // [group][chunk][column]
   __shared__ double dbt[32][kScrHalf + 1];            // [chunk][column]
   __shared__ unsigned long long cnt[kScrWarps][6];
@@ -533,19 +534,48 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
       surv |= (zbar <= P.tau ? 0u : 1u) << (cb + k);
     }
   }
+  // provably-zero blocks among this lane's chunk's columns:
+  // max alpha + beta_j <= cmin, the same transposed rounds (cmin in zt's
+  // storage as floats, beta in dbt's)
+  uint32_t pz = 0u;  // columns possibly nonzero
+  {
+    float(*ct)[32][kScrHalf + 1] = reinterpret_cast<float(*)[32][kScrHalf + 1]>(zt);
+    const double amx = lvalid ? P.amax[l] : 0.0;
+#pragma unroll 1
+    for (int h = 0; h < 32 / kScrHalf; ++h) {
+      const int cb = h * kScrHalf;
+      __syncthreads();
+      for (int q = threadIdx.x; q < 32 * kScrHalf; q += blockDim.x) {
+        const int ci = q / kScrHalf, k = q % kScrHalf;
+        const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
+        dbt[ci][k] = (c0 + ci < P.nw && j < P.n) ? xe[P.m + j] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int ci = 2 * q + (lane >> 4), k = lane & 15;
+        const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
+        ct[warp][ci][k] = (lvalid && c0 + ci < P.nw && j < P.n) ? P.cmin[(int64_t)l * P.n + j] : 0.0f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kScrHalf; ++k)
+        pz |= (dadd(amx, dbt[lane][k]) <= (double)ct[warp][lane][k] ? 0u : 1u) << (cb + k);
+    }
+  }
   // masks of this lane's chunk
   const int64_t j0 = (int64_t)c * 32;
   const uint32_t vmask = (!lvalid || !cvalid) ? 0u
                          : (P.n - j0 >= 32 ? 0xffffffffu : ((1u << (P.n - j0)) - 1u));
   const uint32_t wa = am & vmask;
   const uint32_t we = vmask & ~wa;
-  const uint32_t ws = (surv & we) | wa;
+  const uint32_t wd = (surv & we) | wa;  // the reference's decisions (counters)
+  const uint32_t ws = wd & pz;           // what the evaluation reads
   if (lvalid && cvalid) words[(int64_t)l * P.nw + c] = ws;
   const unsigned ne = __ballot_sync(0xffffffffu, ws != 0u);
   if (lvalid && lane == 0) gmask[(int64_t)l * ((P.nw + 31) / 32) + blockIdx.x] = ne;
   // GradStats counters of this lane's chunk, warp-reduced
   unsigned long long v[6];
-  const uint32_t nsv = __popc(we & ws), nev = __popc(we);
+  const uint32_t nsv = __popc(we & wd), nev = __popc(we);
   v[0] = __popc(wa);
   v[1] = nev - nsv;
   v[2] = nsv;
@@ -603,7 +633,7 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
-                   int num_sms, cudaStream_t s) {
+                   const double* xe, int num_sms, cudaStream_t s) {
   const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)((P.L + kScrWarps - 1) / kScrWarps));
   if ((int64_t)grid.x * grid.y < 4ll * num_sms) {  // small: one CTA per (group, 2048 columns)
     const dim3 g2((unsigned)((P.nw + 63) / 64), (unsigned)P.L);
@@ -612,7 +642,7 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
     return;
   }
   launch_pdl(k_screen, grid, dim3(32 * kScrWarps), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words,
-             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready);
+             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready, xe);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
