@@ -411,6 +411,7 @@ def timed_solves(ctx, kw: dict, steps: int) -> dict:
         out["tasks"] += r["eval_tasks"]
         out["refreshes"] += r["outer_loops"]
         out["objective"] = r["objective"]
+        out["x"] = r["x"]
     out["ms"] = ctx.timer_stop()
     return out
 
@@ -547,6 +548,13 @@ def run_ours(args, world, rank, local, pg):
     ctx.close()
     G.cache_clear()
 
+    # ---- the column-sharded (multi-GPU) code path at N = 1, same config
+    shard1 = None
+    if not args.no_sharded_n1:
+        clocks.begin()
+        shard1 = sharded_n1(cfg, head["ms"] / args.steps, head["x"], min(args.steps, 3))
+        clocks.end()
+
     # ---- all five configs (fast and exact-order mode)
     table = configs_table(args, cfg, head, clocks)
     if exact is not None and f"config{cfg}" in table:
@@ -588,6 +596,7 @@ def run_ours(args, world, rank, local, pg):
         "kernels": kinds,
         "gpu_launches": launches,
         "configs": table,
+        "sharded_n1": shard1,
         "parity_pinned": None if exact is None else dict(
             exact, mode="exact-order (GSOT_SOLVE_EXACT): the reference's own order of every "
                         "floating-point operation; the solve is bitwise the reference's "
@@ -660,11 +669,10 @@ def run_e2e(args, cfg, gamma, mu, kw):
 # ------------------------------------------------------- column-sharded (N > 1)
 
 
-def run_sharded(args, world, rank, local, pg):
-    """N > 1: the config's instance column-sharded across the ranks (each
-    rank's shard context holds cost[:, J_p]); one all-reduce of m + 1 doubles
-    per evaluation (paper_2303_07597_b200/sharded.py). value counts every
-    global evaluation once: strong scaling."""
+def shard_block(cfg: int, world: int, rank: int, pg):
+    """This rank's column block of config cfg's normalised cost, on the device
+    (column-major m x n_p), with the global maximum all-reduced: the same bits
+    as the unsharded C / max C (data_io.hpp:162-165)."""
     import ctypes as C
 
     import numpy as np
@@ -673,62 +681,123 @@ def run_sharded(args, world, rank, local, pg):
     import paper_2303_07597_b200 as G
     from paper_2303_07597_b200 import sharded as S
 
-    G.set_device(local)
-    comm = S.Comm(pg)
-    cfg = args.config
-    gamma, mu, iters = CONFIGS[cfg]
     m, n, L, d = G.config_shape(cfg)
     src, tgt, sizes, a, b = G.config_features(cfg, cfg)
     j0, j1 = S.shard_columns(n, world, rank)
     npc = j1 - j0
-    block = torch.empty((npc, m), dtype=torch.float64, device="cuda")  # column-major m x npc
+    block = torch.empty((npc, m), dtype=torch.float64, device="cuda")
     tb = np.ascontiguousarray(tgt[j0:j1])
     G.groupot._raise(G._lib.lib().gsot_cost_matrix_device(
         src.ctypes.data_as(C.c_void_p), m, tb.ctypes.data_as(C.c_void_p), npc, d, 0,
         C.c_void_p(block.data_ptr())))
-    gmax = comm.allreduce(np.array([block.max().item()]), "max")[0]
-    block /= gmax  # the same bits as the unsharded C / max C (data_io.hpp:162-165)
+    gmax = torch.tensor([block.max().item()], dtype=torch.float64)
+    if pg is not None:
+        import torch.distributed as dist
+
+        gmax = gmax.cuda() if dist.get_backend() == "nccl" else gmax
+        dist.all_reduce(gmax, op=dist.ReduceOp.MAX)
+    # true division by a device tensor (a CPU-scalar divisor makes torch multiply by
+    # the reciprocal: other bits than cost_matrix's C / max C)
+    block.div_(gmax.to(device=block.device))
     torch.cuda.synchronize()
-    ctx = G.Context.shard_from_device(block.data_ptr(), m, npc, sizes, np.zeros(m), b[j0:j1],
-                                      gamma, mu)
-    sp = S.ShardedProblem(None, sizes, a, b[j0:j1], gamma, mu, comm, ctx=ctx)
-    skw = dict(mode=1, max_outer_loops=iters // 10, grad_tol=1e-12)
+    return block, (m, n, L, sizes, a, b, j0, j1)
+
+
+def sharded_solves(ctx, kw: dict, steps: int) -> dict:
+    ctx.timer_start()
+    calls = iters = 0
+    for _ in range(steps):
+        r = ctx.solve(**kw)
+        calls += r["grad_calls"]
+        iters += r["iterations"]
+    return {"ms": ctx.timer_stop(), "calls": calls, "iters": iters, "x": r["x"],
+            "objective": r["objective"]}
+
+
+def sharded_n1(cfg: int, single_ms: float, single_x, steps: int) -> dict:
+    """The column-sharded path at N = 1 on this GPU: the shard context (every
+    column, a on rank 0) with an NCCL communicator attached runs the split
+    direction update and the per-sequence all-reduces inside its graphs.
+    Compared with the single-context solve of the same config (speed, and the
+    final state bit for bit)."""
+    import numpy as np
+
+    import paper_2303_07597_b200 as G
+    from paper_2303_07597_b200 import sharded as S
+
+    gamma, mu, iters = CONFIGS[cfg]
+    block, (m, n, L, sizes, a, b, j0, j1) = shard_block(cfg, 1, 0, None)
+    ctx = S.shard_context_from_device(block.data_ptr(), m, j1 - j0, sizes, a, b[j0:j1], gamma,
+                                      mu, 0)
+    del block
+    S.attach_comm(ctx, None, "nccl")
+    kw = solve_kw(iters)
+    ctx.solve(**kw)
+    r = sharded_solves(ctx, kw, steps)
+    ctx.close()
+    G.cache_clear()
+    ms = r["ms"] / steps
+    return {"solve_ms": ms, "evals_per_s": r["calls"] / (r["ms"] / 1e3),
+            "vs_single_context": single_ms / ms,
+            "x_bitwise_equal_single_context": bool(np.array_equal(r["x"], single_x)),
+            "what": "config %d as ONE column shard (gsot_create_shard_device, a on rank 0) with "
+                    "an NCCL communicator attached (world 1): the N>1 code path -- split "
+                    "direction update, shard pack / NCCL all-reduce / unpack per sequence -- "
+                    "on one GPU, %d timed solves" % (cfg, steps)}
+
+
+def run_sharded(args, world, rank, local, pg):
+    """N > 1: the config's instance column-sharded across the ranks (each
+    rank's shard context holds cost[:, J_p]); the library's device-resident
+    solve with an NCCL communicator attached (gsot_comm_attach_nccl): per
+    device sequence one sum all-reduce of the gradient head (m doubles) and a
+    16-double tail, plus the L-BFGS dots of each direction update, all on the
+    context stream inside its CUDA graphs. value counts every global
+    evaluation once: strong scaling."""
+    import numpy as np
+    import torch
+
+    import paper_2303_07597_b200 as G
+    from paper_2303_07597_b200 import sharded as S
+
+    G.set_device(local)
+    cfg = args.config
+    gamma, mu, iters = CONFIGS[cfg]
+    block, (m, n, L, sizes, a, b, j0, j1) = shard_block(cfg, world, rank, pg)
+    npc = j1 - j0
+    ctx = S.shard_context_from_device(block.data_ptr(), m, npc, sizes, a, b[j0:j1], gamma, mu,
+                                      rank)
+    host = torch.empty((npc, m), dtype=torch.float64, pin_memory=True)
+    host.copy_(block)  # for the e2e leg
+    del block
+    torch.cuda.synchronize()
+    transport = S.attach_comm(ctx, pg, "nccl")
+    kw = solve_kw(iters)
     for _ in range(args.warmup):
-        S.solve_sharded(sp, **skw)
+        ctx.solve(**kw)
     clocks = ClockSampler(local)
     clocks.start()
     barrier(pg)
-    torch.cuda.synchronize()
     clocks.begin()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    calls = iters_done = 0
-    for _ in range(args.steps):
-        r = S.solve_sharded(sp, **skw)
-        calls += r.stats.grad_calls
-        iters_done += r.iterations
-    e1.record()
-    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches()
+    r = sharded_solves(ctx, kw, args.steps)
+    launches = ctx.kernel_launches() - launches0
     clocks.end()
     barrier(pg)
     clk = clocks.stop()
-    ms = allreduce(pg, e0.elapsed_time(e1), "max")
-    value = calls / (ms / 1e3)
-    sp.close()
-    # e2e: each rank uploads its host column block (pinned) through the C ABI
-    host = torch.empty((npc, m), dtype=torch.float64, pin_memory=True)
-    host.copy_(block)
-    del block
-    torch.cuda.synchronize()
+    ms = allreduce(pg, r["ms"], "max")
+    value = r["calls"] / (ms / 1e3)
+    ctx.close()
+    # e2e: each rank uploads its pinned host column block through the C ABI,
+    # attaches its communicator, solves, downloads its [alpha; beta_p]
     tsteps, ecalls = max(1, args.steps // 4), 0
     barrier(pg)
     t0 = time.perf_counter()
     for _ in range(tsteps):
-        c2 = G.Context.shard_from_arrays(host.numpy().T, sizes, np.zeros(m), b[j0:j1], gamma, mu)
-        sp2 = S.ShardedProblem(None, sizes, a, b[j0:j1], gamma, mu, comm, ctx=c2)
-        ecalls += S.solve_sharded(sp2, **skw).stats.grad_calls
-        sp2.close()
-    torch.cuda.synchronize()
+        c2 = S.shard_context_from_arrays(host.numpy().T, sizes, a, b[j0:j1], gamma, mu, rank)
+        S.attach_comm(c2, pg, "nccl")
+        ecalls += c2.solve(**kw)["grad_calls"]
+        c2.close()
     et = allreduce(pg, time.perf_counter() - t0, "max")
     if rank == 0:
         print(json.dumps({
@@ -740,15 +809,17 @@ def run_sharded(args, world, rank, local, pg):
                                    f"column-sharded over {world} GPUs ({iters} iterations)",
                        "m": m, "n": n, "L": L, "gamma": gamma, "mu": mu,
                        "l2": "inputs larger than L2, no flush",
-                       "parallelism": f"column shards x{world} (one all-reduce of m+1 doubles "
-                                      f"per evaluation)"},
-            "evals_per_solve": calls / args.steps, "iterations_per_solve": iters_done / args.steps,
-            "gpu_launches": None,
+                       "parallelism": f"column shards x{world}: device-resident solve per rank, "
+                                      f"{transport} all-reduce of m+16 doubles per sequence "
+                                      f"and of the L-BFGS dots per direction"},
+            "evals_per_solve": r["calls"] / args.steps,
+            "iterations_per_solve": r["iters"] / args.steps,
+            "gpu_launches": launches,
             "e2e": {"value": ecalls / et, "unit": "evals/s",
                     "h2d_bytes_per_step": 8 * m * n + 8 * (m + n),
                     "d2h_bytes_per_step": 8 * (m + n),
                     "what": "per rank gsot_create_shard from its pinned host column block + "
-                            "the sharded solve"},
+                            "communicator attach + the sharded solve + x download"},
             "clocks": clk}), flush=True)
     return 0
 
@@ -765,6 +836,7 @@ def main():
                     default=[1, 2, 3, 4, 5])
     ap.add_argument("--skip-large", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded-n1", action="store_true")
     args = ap.parse_args()
     if args.gpus > 1 and "RANK" not in os.environ:
         # one process per GPU: re-launch under torch.distributed.run

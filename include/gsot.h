@@ -280,6 +280,42 @@ GSOT_API void gsot_default_solver_options(gsot_solver_options* o);
 GSOT_API int gsot_solve(gsot_ctx* ctx, const gsot_solver_options* opts, double* x_out,
                         gsot_solve_result* result, int64_t* history, int64_t history_cap);
 
+/* ---- Multi-GPU: the column-sharded solve on the device ----
+ *
+ * The reference solves on one host (solver.hpp:284-293); its only parallel
+ * decomposition is by column. Rank p of P builds a shard
+ * context (gsot_create_shard[_device]) over its column block J_p with
+ * a = the row marginal on rank 0 and zeros on every other rank, attaches a
+ * communicator, and calls gsot_solve: the same device-resident solve (CUDA
+ * graphs, compact L-BFGS) with, per device sequence, ONE sum all-reduce of
+ * the gradient head (m doubles: a - sum_p rowsum_p) and a 16-double tail
+ * (a.alpha, b.beta, psi, g.d, the step's g.d and d.d, the GradStats
+ * counters), plus one of (memory+1)*5 doubles inside every direction update
+ * (the L-BFGS dots; the replicated alpha part counted once). Every rank then
+ * takes the same host decisions. x_out receives the rank's [alpha; beta_p].
+ * Modes: GSOT_MODE_BASELINE / FAST / FAST_NO_LOWER_BOUND; exact-order and
+ * audit solves are single-context only (GSOT_ERR_INVALID_ARGUMENT). */
+enum { GSOT_REDUCE_SUM = 0, GSOT_REDUCE_MAX = 1 };
+/* Host transport: called synchronously with `count` doubles in host memory,
+ * reduces them in place over the ranks (identical result on every rank);
+ * returns 0 on success. */
+typedef int (*gsot_allreduce_fn)(double* buf, int64_t count, int32_t op, void* user);
+/* A fresh NCCL unique id (128 bytes) for gsot_comm_attach_nccl (rank 0 makes
+ * it, the caller broadcasts it). NCCL is loaded at run time (libnccl.so.2,
+ * the process's own copy when one is loaded). */
+GSOT_API int gsot_comm_unique_id(unsigned char id[128]);
+/* Attach an NCCL communicator over the world's GPUs (one rank per GPU,
+ * collective over the ranks): the all-reduces run on the context's stream
+ * inside the solver's CUDA graphs. */
+GSOT_API int gsot_comm_attach_nccl(gsot_ctx* ctx, const unsigned char id[128], int32_t world,
+                                   int32_t rank);
+/* Attach a host transport (testing and hosts without NCCL): the solver runs
+ * its sequences eagerly and synchronises around every all-reduce. */
+GSOT_API int gsot_comm_attach_host(gsot_ctx* ctx, int32_t world, int32_t rank,
+                                   gsot_allreduce_fn fn, void* user);
+/* Detach (and destroy) the communicator: the context solves alone again. */
+GSOT_API int gsot_comm_detach(gsot_ctx* ctx);
+
 /* ---- Inputs: synthetic instances (SURVEY.md §8(d) recipe) ----------------- */
 
 /* Per-config sizes: cfg in 1..5. Returns m, n, L, d. */

@@ -113,7 +113,14 @@ SIGNATURES = {
     "gsot_kernel_launches": (C.c_int64, [_vp]),
     "gsot_set_device": (C.c_int, [C.c_int32]),
     "gsot_timer": (C.c_int, [_vp, C.c_int, _dp]),
+    "gsot_comm_unique_id": (C.c_int, [_vp]),
+    "gsot_comm_attach_nccl": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32]),
+    "gsot_comm_attach_host": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "gsot_comm_detach": (C.c_int, [_vp]),
 }
+
+# gsot_allreduce_fn (include/gsot.h): in-place reduction of host doubles.
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_int32, C.c_void_p)
 
 _lib = None
 

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libgsot.so")
 # Diagnostic variants: GSOT_NVCC_DEFINES="-DGSOT_PHASE_CLOCKS" GSOT_LIB_OUT=... (never the product)
 EXTRA = os.environ.get("GSOT_NVCC_DEFINES", "").split()
-SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu", "gsot_solver.cu", "gsot_exact2.cu"]
+SOURCES = ["gsot_kernels.cu", "gsot_lbfgs.cu", "gsot_data.cu", "gsot_ctx.cu", "gsot_solver.cu", "gsot_exact2.cu", "gsot_comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -58,7 +58,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             print(out)
     tmp = LIB + ".tmp"
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-            "-Xcompiler", "-fPIC"]
+            "-Xcompiler", "-fPIC", "-ldl"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(link)}\n{r.stdout}{r.stderr}")

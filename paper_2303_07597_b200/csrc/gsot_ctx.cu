@@ -107,6 +107,8 @@ void check_marginal(const double* v, int64_t n, char which, bool shard = false) 
 }  // namespace
 
 
+int gsot_guard_call(const std::function<void()>& f) { return guard(f); }
+
 gsot_ctx::~gsot_ctx() {
   if (stream) cudaStreamSynchronize(stream);
   ws.reset();
@@ -386,6 +388,12 @@ size_t cache_drain() {
 
 void park_or_delete(gsot_ctx* c) {
   if (!c) return;
+  if (c->comm) {  // a communicator never outlives its owner's handle
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    c->comm.reset();
+    c->pending_grad = nullptr;
+    ++c->graph_epoch;
+  }
   if (!cache_enabled() || !c->cacheable || cudaStreamSynchronize(c->stream) != cudaSuccess) {
     delete c;
     return;
@@ -510,6 +518,9 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
                   const double* d_dir, double ub_offset, bool use_active, bool dbeta_ready) {
   const bool exact = (mode_flags & GSOT_EVAL_EXACT) != 0;
   const int mode = mode_flags & 1;
+  if (exact && c->comm)
+    throw Error(GSOT_ERR_INVALID_ARGUMENT, "exact-order evaluation of a sharded context");
+  if (c->comm) c->pending_grad = d_grad;  // its head is summed over the ranks at publication
   if (exact) c->ensure_exact();
   if (mode == GSOT_EVAL_SCREENED && !c->have_snapshot)
     throw Error(GSOT_ERR_STATE, "screened evaluation requires a snapshot (gsot_init_snapshot)");
@@ -578,7 +589,7 @@ EvalOut eval_result(gsot_ctx* c, int mode_flags) {
     o.stats.unskipped = static_cast<int64_t>(c->h_sc->counters[2]);
     o.stats.upper_bounds = static_cast<int64_t>(c->h_sc->counters[3]);
   } else {
-    o.stats.unskipped = static_cast<int64_t>(c->L) * c->n;  // solver.hpp:117-119
+    o.stats.unskipped = static_cast<int64_t>(c->L) * c->n_global();  // solver.hpp:117-119
   }
   return o;
 }

@@ -60,6 +60,27 @@ struct SolverWorkspace {
   ~SolverWorkspace();
 };
 
+// A sharded context's communicator (gsot_comm.cu).
+struct ShardComm {
+  enum { kNccl = 1, kHost = 2 };
+  int kind = 0;
+  int rank = 0, world = 1;
+  void* nccl_comm = nullptr;  // ncclComm_t
+  gsot_allreduce_fn fn = nullptr;
+  void* user = nullptr;
+  double* host_buf = nullptr;  // pinned staging of the host transport
+  size_t host_cap = 0;
+  double* d_tail = nullptr;  // kShardTail doubles (k_shard_pack / k_shard_unpack)
+  double* d_red = nullptr;   // the step kernel's folded dots, (kMaxMemory + 1) * 5
+  double* d_n = nullptr;
+  int64_t n_global = 0;      // columns over all ranks
+  // In-place all-reduce of `count` device doubles on stream s (GSOT_REDUCE_*).
+  void allreduce(double* d, int64_t count, int op, cudaStream_t s);
+  void group_begin();  // NCCL group (no-op for the host transport)
+  void group_end();
+  ~ShardComm();
+};
+
 }  // namespace gsot
 
 struct gsot_ctx {
@@ -138,6 +159,13 @@ struct gsot_ctx {
   cudaEvent_t timer_a = nullptr, timer_b = nullptr;
   // stream capture in progress: marks/kernels go to the sequence
   gsot::Sequence* capturing = nullptr;
+  // column-sharded solve (gsot_comm.cu): the communicator, and the gradient
+  // whose head the next publication all-reduces (set by enqueue_eval)
+  std::unique_ptr<gsot::ShardComm> comm;
+  double* pending_grad = nullptr;
+  // dots over [alpha; beta_p] start here: the replicated alpha part counts on rank 0 only
+  int64_t dot_lo() const { return comm && comm->rank != 0 ? m : 0; }
+  int64_t n_global() const { return comm ? comm->n_global : n; }
 
   gsot::DevProblem problem() const {
     gsot::DevProblem P;
@@ -273,6 +301,18 @@ struct gsot_ctx {
   }
   // Enqueue the publication of the scalar block to the host mirror.
   void enqueue_fetch() {
+    if (comm) {  // sharded: fold, sum over the ranks, write back, then publish
+      launch(gsot::K_MISC, 0.0, [&] {
+        gsot::launch_shard_pack(dsync, partials, ws ? ws->cpart : nullptr, cnt_slots,
+                                comm->d_tail, stream);
+      });
+      comm->group_begin();
+      if (pending_grad) comm->allreduce(pending_grad, m, GSOT_REDUCE_SUM, stream);
+      comm->allreduce(comm->d_tail, gsot::kShardTail, GSOT_REDUCE_SUM, stream);
+      comm->group_end();
+      pending_grad = nullptr;
+      launch(gsot::K_MISC, 0.0, [&] { gsot::launch_shard_unpack(dsync, comm->d_tail, stream); });
+    }
     launch(gsot::K_MISC, 0.0, [&] {
       gsot::launch_publish(dsync, h_sync_dev, d_pub_count, h_flag_dev, partials,
                            ws ? ws->cpart : nullptr, cnt_slots, tl, stream);
@@ -305,6 +345,9 @@ struct gsot_ctx {
 
   ~gsot_ctx();
 };
+
+// guard() of gsot_ctx.cu for the entry points of other translation units.
+int gsot_guard_call(const std::function<void()>& f);
 
 namespace gsot {
 

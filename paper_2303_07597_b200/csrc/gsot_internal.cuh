@@ -244,6 +244,14 @@ void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_cou
                     const double* step_partials, unsigned long long* cnt_slots,
                     unsigned long long* tl, cudaStream_t s);
 
+// Column-sharded contexts (gsot_lbfgs.cu): fold the pending
+// partials into `tail` (kShardTail doubles, presence flags per group) before
+// the sum all-reduce, and write the reduced groups back after it.
+constexpr int kShardTail = 16;
+void launch_shard_pack(DevSync* src, const double* fin_partials, const double* step_partials,
+                       unsigned long long* cnt_slots, double* tail, cudaStream_t s);
+void launch_shard_unpack(DevSync* src, const double* tail, cudaStream_t s);
+
 // trial.x = x + t * d with t read from device memory; with dbeta != null also
 // dbeta_j = out[m + j] - snap[m + j] for the screen.
 void launch_axpy_point(const double* x, const double* t, const double* d, double* out,
@@ -296,6 +304,7 @@ void launch_lbfgs_step(int pair, const double* x, const double* xprev, const dou
                        CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
                        double* out, EvalScalars* sc, double* part, int mem,
                        unsigned long long* tl, int64_t m, const double* snap, double* dbeta,
-                       cudaStream_t s);
+                       cudaStream_t s, int split = 0, int64_t dot_lo = 0,
+                       double* red_io = nullptr);
 
 }  // namespace gsot

@@ -80,23 +80,13 @@ __device__ __forceinline__ double warp_fold(const double* part, int n, int strid
   return s;
 }
 
-__global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevSync* host_dst,
-                                                 unsigned long long* dev_count,
-                                                 unsigned long long* host_flag,
-                                                 const double* __restrict__ fin_partials,
-                                                 const double* __restrict__ step_partials,
-                                                 unsigned long long* cnt_slots,
-                                                 unsigned long long* tl) {
-  static_assert(offsetof(DevSync, t) % 8 == 0, "DevSync is copied as 8-byte words");
-#ifdef GSOT_PHASE_CLOCKS
-  long long clk_prev = clock64();
-#endif
-  // the completion counter is written only by earlier publishes, which
-  // completed before this sequence was launched: read it before the wait
-  unsigned long long count0 = 0;
-  if (threadIdx.x == 0) count0 = *dev_count;
-  pdl_wait();
-  TL_ENTER(tl, TL_PUBLISH);
+// The pending folds (EvalScalars::fin_blocks / step_blocks / cnt_pending),
+// in a fixed order, by all 256 threads of one CTA: k_publish, and k_shard_pack
+// before a sharded context's all-reduce. Returns with the CTA synchronised.
+__device__ __forceinline__ void publish_fold(DevSync* __restrict__ src,
+                                             const double* __restrict__ fin_partials,
+                                             const double* __restrict__ step_partials,
+                                             unsigned long long* cnt_slots) {
   EvalScalars* sc = &src->sc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fin = sc->fin_blocks, step = sc->step_blocks, cnt = sc->cnt_pending;
@@ -146,7 +136,6 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
   }
   if (cnt && warp == 6) fold_counter_slots(cnt_slots, sc);
   __syncthreads();
-  PHASE_MARK(11);
   if (threadIdx.x == 0) {
     if (fin > 0) {
 #pragma unroll
@@ -170,6 +159,28 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
     sc->cnt_pending = 0;
   }
   __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevSync* host_dst,
+                                                 unsigned long long* dev_count,
+                                                 unsigned long long* host_flag,
+                                                 const double* __restrict__ fin_partials,
+                                                 const double* __restrict__ step_partials,
+                                                 unsigned long long* cnt_slots,
+                                                 unsigned long long* tl) {
+  static_assert(offsetof(DevSync, t) % 8 == 0, "DevSync is copied as 8-byte words");
+#ifdef GSOT_PHASE_CLOCKS
+  long long clk_prev = clock64();
+#endif
+  // the completion counter is written only by earlier publishes, which
+  // completed before this sequence was launched: read it before the wait
+  unsigned long long count0 = 0;
+  if (threadIdx.x == 0) count0 = *dev_count;
+  pdl_wait();
+  TL_ENTER(tl, TL_PUBLISH);
+  EvalScalars* sc = &src->sc;
+  publish_fold(src, fin_partials, step_partials, cnt_slots);
+  PHASE_MARK(11);
   // what the host reads: the scalar block, the ring's counters, the slopes
   // (t is host-owned; it is copied to the device by the solver)
   constexpr int kSc = (int)(sizeof(EvalScalars) / 8);
@@ -235,6 +246,72 @@ void launch_publish(DevSync* src, DevSync* host_dst, unsigned long long* dev_cou
                     unsigned long long* tl, cudaStream_t s) {
   launch_pdl(k_publish, dim3(1), dim3(256), 0, s, src, host_dst, dev_count, host_flag,
              fin_partials, step_partials, cnt_slots, tl);
+}
+
+// ---- column-sharded contexts: the scalars of one device
+// sequence, summed over the ranks. k_shard_pack folds this rank's pending
+// partials exactly as k_publish would and lays the folded values out in
+// `tail` (kShardTail doubles) with one presence flag per group; after the sum
+// all-reduce k_shard_unpack writes back the groups present (identical on every
+// rank, so every rank's host takes the same decisions). The objective's terms
+// add up over ranks because only rank 0's shard carries a (a.alpha) and every
+// shard's b_p.beta_p - psi_p covers its own columns; g.d adds up because the
+// gradient head is linear in the per-rank row sums (dual.hpp:91, :96).
+__global__ void __launch_bounds__(256) k_shard_pack(DevSync* __restrict__ src,
+                                                    const double* __restrict__ fin_partials,
+                                                    const double* __restrict__ step_partials,
+                                                    unsigned long long* cnt_slots,
+                                                    double* __restrict__ tail) {
+  EvalScalars* sc = &src->sc;
+  const int fin = sc->fin_blocks, step = sc->step_blocks, cnt = sc->cnt_pending;
+  publish_fold(src, fin_partials, step_partials, cnt_slots);
+  if (threadIdx.x == 0) {
+    double t[kShardTail];
+    for (int i = 0; i < kShardTail; ++i) t[i] = 0.0;
+    if (fin > 0) {
+      t[0] = sc->dot_aa;
+      t[1] = sc->dot_bb;
+      t[2] = sc->psi_sum;
+      t[3] = sc->slope;
+      t[4] = 1.0;
+    }
+    if (step > 0) {
+      t[5] = src->tl[0];
+      t[6] = src->tl[1];
+      t[7] = 1.0;
+    }
+    if (cnt) {
+      for (int q = 0; q < 4; ++q) t[8 + q] = static_cast<double>(sc->counters[q]);
+      t[12] = 1.0;
+    }
+    for (int i = 0; i < kShardTail; ++i) tail[i] = t[i];
+  }
+}
+
+__global__ void k_shard_unpack(DevSync* __restrict__ src, const double* __restrict__ tail) {
+  EvalScalars* sc = &src->sc;
+  if (tail[4] > 0.0) {
+    sc->dot_aa = tail[0];
+    sc->dot_bb = tail[1];
+    sc->psi_sum = tail[2];
+    sc->objective = dsub(dadd(tail[0], tail[1]), tail[2]);
+    sc->slope = tail[3];
+  }
+  if (tail[7] > 0.0) {
+    src->tl[0] = tail[5];
+    src->tl[1] = tail[6];
+  }
+  if (tail[12] > 0.0)
+    for (int q = 0; q < 4; ++q) sc->counters[q] = static_cast<unsigned long long>(tail[8 + q]);
+}
+
+void launch_shard_pack(DevSync* src, const double* fin_partials, const double* step_partials,
+                       unsigned long long* cnt_slots, double* tail, cudaStream_t s) {
+  k_shard_pack<<<1, 256, 0, s>>>(src, fin_partials, step_partials, cnt_slots, tail);
+}
+
+void launch_shard_unpack(DevSync* src, const double* tail, cudaStream_t s) {
+  k_shard_unpack<<<1, 1, 0, s>>>(src, tail);
 }
 
 __global__ void k_hist_reset(HistState* h, int mem) {
@@ -321,6 +398,14 @@ struct StepArgs {
   int64_t m;               // with dbeta: dbeta_j = xt[m + j] - snap[m + j]
   const double* snap;
   double* dbeta;
+  // column-sharded contexts: split 1 runs phase (1) and leaves
+  // the folded dots in red_io ((memory + 1) * 5 doubles) for the sum
+  // all-reduce, split 2 runs phases (2)-(3) from the reduced red_io; 0 = the
+  // whole update. Dots and slopes skip elements below dot_lo (m on every rank
+  // but rank 0: the replicated alpha part counts once over the ranks).
+  int split;
+  int64_t dot_lo;
+  double* red_io;
 };
 
 
@@ -415,7 +500,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
   __syncthreads();
   // (1) one warp per row, lanes striding the slice kStepBatch elements at a time
   const int nrows = k + (A.pair ? 1 : 0);
-  for (int r = warp; r < nrows; r += kStepWarps) {
+  const int64_t dlo = A.dot_lo;
+  for (int r = warp; r < nrows && A.split != 2; r += kStepWarps) {
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (r == k) {  // the new pair, written into the scratch slot
       double* __restrict__ sv = A.S + scratch * A.stride;
@@ -438,6 +524,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
           const double s = dsub(xs[u], xp[u]), y = dsub(gp[u], gs[u]);
           sv[e] = s;
           yv[e] = y;
+          if (e < dlo) continue;
           acc[0] = dadd(acc[0], dmul(s, y));
           acc[1] = dadd(acc[1], dmul(s, s));
           acc[2] = dadd(acc[2], dmul(y, y));
@@ -463,6 +550,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
         for (int u = 0; u < kStepBatch; ++u) {
           const int64_t e = e0 + 32 * u;
           if (e >= hi) break;
+          if (e < dlo) continue;
           if (A.pair) {
             const double yn = dsub(gp[u], gs[u]);
             acc[0] = dadd(acc[0], dmul(ss[u], yn));
@@ -500,9 +588,21 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
   PHASE_MARK(0);
   grid.sync();
   PHASE_MARK(1);
+  if (A.split == 1) {  // sharded: this rank's folded dots, then the all-reduce
+    if (blockIdx.x == 0) {
+      grid_fold(A.part + 2 * kStepMaxGrid, nc, ld, nrows * 5, red);
+      __syncthreads();
+      for (int i = threadIdx.x; i < KS * 5; i += blockDim.x) A.red_io[i] = i < nrows * 5 ? red[i] : 0.0;
+    }
+    return;
+  }
   // (2) every CTA: fold, ring update, R / YY maintenance, compact solve
   {
-    grid_fold(A.part + 2 * kStepMaxGrid, nc, ld, nrows * 5, red);
+    if (A.split == 2) {
+      for (int i = threadIdx.x; i < nrows * 5; i += blockDim.x) red[i] = __ldcg(A.red_io + i);
+    } else {
+      grid_fold(A.part + 2 * kStepMaxGrid, nc, ld, nrows * 5, red);
+    }
     __syncthreads();
     PHASE_MARK(2);
     if (threadIdx.x == 32) {  // gam (lbfgs.hpp:116-119) of the newest pair, beside the ring update
@@ -721,8 +821,10 @@ __global__ void __launch_bounds__(kStepThreads) k_lbfgs_step(const StepArgs A) {
       A.xt[e] = v;
       if (A.dbeta && e >= A.m) A.dbeta[e - A.m] = dsub(v, A.snap[e]);
     }
-    pg = dadd(pg, dmul(ge, de));
-    pd = dadd(pd, dmul(de, de));
+    if (e >= dlo) {
+      pg = dadd(pg, dmul(ge, de));
+      pd = dadd(pd, dmul(de, de));
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -774,10 +876,10 @@ void launch_lbfgs_step(int pair, const double* x, const double* xprev, const dou
                        CompactState* cs, double* d, const double* t, double* xt, int64_t dim,
                        double* out, EvalScalars* sc, double* part, int mem,
                        unsigned long long* tl, int64_t m, const double* snap, double* dbeta,
-                       cudaStream_t s) {
+                       cudaStream_t s, int split, int64_t dot_lo, double* red_io) {
   const int grid = lbfgs_step_grid();
   StepArgs A{pair, x, xprev, g, gprev, S, Y, stride, h, cs, d, t, xt, dim, out, sc, part, mem + 1,
-             tl, m, snap, dbeta};
+             tl, m, snap, dbeta, split, dot_lo, red_io};
   const size_t smem = sizeof(double) * 2 * (size_t)(mem + 1) * (mem + 1);
   if (smem > 48 * 1024 && smem > g_step_smem) {
     cudaFuncSetAttribute(k_lbfgs_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

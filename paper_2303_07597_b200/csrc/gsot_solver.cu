@@ -45,8 +45,14 @@ class Solver {
     use_active_ = o.mode == GSOT_MODE_FAST ||
                   (o.mode == GSOT_MODE_AUDIT && !(o.flags & GSOT_SOLVE_NO_ACTIVE_SET));
     audit_ = o.mode == GSOT_MODE_AUDIT;
-    graphs_ = !audit_;
     exact_ = (o.flags & GSOT_SOLVE_EXACT) != 0;
+    // a sharded context (gsot_comm.cu): every publication sums over the ranks;
+    // the host transport synchronises, so its sequences run eagerly
+    sharded_ = c->comm != nullptr;
+    if (sharded_ && (exact_ || audit_))
+      throw Error(GSOT_ERR_INVALID_ARGUMENT,
+                  "sharded solves support the baseline and fast modes (no exact-order / audit)");
+    graphs_ = !audit_ && !(sharded_ && c->comm->kind == ShardComm::kHost);
     mode_eval_ = (screened_ ? GSOT_EVAL_SCREENED : GSOT_EVAL_DENSE) | (exact_ ? GSOT_EVAL_EXACT : 0);
     mem_ = std::max(1, o.lbfgs_memory);
     if (exact_) c_->ensure_exact();
@@ -54,7 +60,7 @@ class Solver {
     w_ = c_->ws.get();
     key_ = std::to_string(o.mode) + "/" + std::to_string(o.lbfgs_memory) + "/" +
            std::to_string(o.upper_bound_offset) + "/" + std::to_string(c_->profile ? c_->profile_mask : 0u) +
-           (exact_ ? "/exact" : "") + (use_active_ ? "" : "/nolb");
+           (exact_ ? "/exact" : "") + (use_active_ ? "" : "/nolb") + (sharded_ ? "/shard" : "");
   }
 
   ~Solver() {
@@ -265,13 +271,23 @@ class Solver {
         });
       return;
     }
-    c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 10.0), [&] {
-      launch_lbfgs_step(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->S, w_->Y,
-                        w_->dim, &c_->dsync->h, w_->cs, w_->d, t_one(),
-                        trial ? w_->X[q] : nullptr, w_->dim, c_->dsync->tl, c_->sc, w_->cpart, mem_,
-                        c_->tl, c_->m, c_->snap_x, fast_screen() ? c_->dbeta : nullptr,
-                        c_->stream);
-    });
+    // sharded: phase (1) -> the dots summed over the ranks -> phases (2)-(3)
+    const int splits = sharded_ ? 2 : 0;
+    for (int sp = splits ? 1 : 0; sp <= splits; ++sp) {
+      if (sp == 2)
+        c_->comm->allreduce(c_->comm->d_red, (mem_ + 1) * 5, GSOT_REDUCE_SUM, c_->stream);
+      c_->launch(K_LBFGS, 8.0 * w_->dim * (4.0 * w_->mem + 10.0), [&] {
+        launch_lbfgs_step(pair ? 1 : 0, w_->X[r_], w_->X[q], w_->G[r_], w_->G[q], w_->S, w_->Y,
+                          w_->dim, &c_->dsync->h, w_->cs, w_->d, t_one(),
+                          trial ? w_->X[q] : nullptr, w_->dim, c_->dsync->tl, c_->sc, w_->cpart,
+                          mem_, c_->tl, c_->m, c_->snap_x, fast_screen() ? c_->dbeta : nullptr,
+                          c_->stream, sp, c_->dot_lo(), sharded_ ? c_->comm->d_red : nullptr);
+      });
+    }
+  }
+  // |g|_inf over the ranks (alpha is replicated: max is idempotent)
+  void reduce_extra0(int op) {
+    if (sharded_) c_->comm->allreduce(&c_->sc->extra[0], 1, op, c_->stream);
   }
 
   // ---- bookkeeping ---------------------------------------------------------
@@ -293,7 +309,7 @@ class Solver {
       res_->eval_blocks += e.stats.in_active + e.stats.unskipped;
       res_->eval_tasks += c_->h_sc->ntasks;
     } else {
-      res_->eval_blocks += static_cast<int64_t>(c_->L) * c_->n;
+      res_->eval_blocks += static_cast<int64_t>(c_->L) * c_->n;  // this rank's blocks
       res_->eval_tasks += static_cast<int64_t>(c_->L) * c_->nw;
     }
   }
@@ -338,6 +354,7 @@ class Solver {
       c_->launch(K_LBFGS, 8.0 * w_->dim, [&] {
         launch_absmax(w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
       });
+      reduce_extra0(GSOT_REDUCE_MAX);
       c_->enqueue_fetch();
     });
     return c_->h_sc->extra[0];
@@ -351,6 +368,7 @@ class Solver {
       c_->launch(K_LBFGS, 8.0 * w_->dim, [&] {
         launch_absmax(w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0, c_->stream);
       });
+      reduce_extra0(GSOT_REDUCE_MAX);
       c_->enqueue_fetch();
     });
     const double nrm = c_->h_sc->extra[0];
@@ -468,9 +486,11 @@ class Solver {
               if (exact_)
                 launch_exact_dot2(w_->G[r_], w_->G[r_], w_->dim, c_->ex, c_->sc, 0, c_->stream);
               else
-                launch_dot(w_->G[r_], w_->G[r_], w_->dim, c_->partials, c_->red_blocks, c_->sc, 0,
+                launch_dot(w_->G[r_] + c_->dot_lo(), w_->G[r_] + c_->dot_lo(),
+                           w_->dim - c_->dot_lo(), c_->partials, c_->red_blocks, c_->sc, 0,
                            c_->stream);
             });
+            reduce_extra0(GSOT_REDUCE_SUM);
             c_->fetch_scalars();
             dir_slope = c_->h_sc->extra[0];
             dd = dir_slope;
@@ -600,6 +620,7 @@ class Solver {
   int hk_ = 0;  // history length mirrored from the device
   double res_value_ = 0.0;
   bool screened_ = false, use_active_ = false, audit_ = false, graphs_ = true, exact_ = false;
+  bool sharded_ = false;
   int mode_eval_ = GSOT_EVAL_DENSE;
 };
 

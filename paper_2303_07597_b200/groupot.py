@@ -447,6 +447,35 @@ class Context:
         res["history"] = hist[: 4 * min(history_cap, r.grad_calls)].reshape(-1, 4)
         return res
 
+    # ---- multi-GPU column sharding on the device (gsot_comm_*)
+    def attach_nccl(self, unique_id: bytes, world: int, rank: int) -> None:
+        """Attach an NCCL communicator (collective over the ranks); gsot_solve on
+        this shard context then runs the sharded solve with its all-reduces on
+        the context stream, inside the solver's CUDA graphs."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _raise(_lib.lib().gsot_comm_attach_nccl(self._h, buf, int(world), int(rank)))
+
+    def attach_host(self, world: int, rank: int, allreduce) -> None:
+        """Attach a host transport: allreduce(np.ndarray view, op) reduces the
+        doubles in place over the ranks (op 0 sum, 1 max)."""
+        def cb(ptr, count, op, _user):
+            try:
+                allreduce(np.ctypeslib.as_array(ptr, shape=(int(count),)), int(op))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failure
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._comm_cb = _lib.ALLREDUCE_FN(cb)  # kept alive with the context
+        _raise(_lib.lib().gsot_comm_attach_host(self._h, int(world), int(rank), self._comm_cb,
+                                                None))
+
+    def detach_comm(self) -> None:
+        _raise(_lib.lib().gsot_comm_detach(self._h))
+        self._comm_cb = None
+
     def profile(self, enable) -> None:
         """False: off; True: time every kernel class; int: bit mask (1 << kind)."""
         if enable is True:
@@ -472,6 +501,13 @@ class Context:
         ms = C.c_double()
         _raise(_lib.lib().gsot_timer(self._h, 1, C.byref(ms)))
         return ms.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id for Context.attach_nccl (rank 0; broadcast it)."""
+    buf = C.create_string_buffer(128)
+    _raise(_lib.lib().gsot_comm_unique_id(buf))
+    return buf.raw
 
 
 def cache_clear() -> int:

@@ -136,6 +136,62 @@ class _Torch:
         return float(v.abs().max().item()) if v.numel() else 0.0
 
 
+# ---------------------------------------------------------------------------
+# The device-resident sharded solve (gsot_comm_*): the rank's
+# shard context runs the library's own solver (CUDA graphs, compact L-BFGS,
+# PDL chain) and sums, per device sequence, the gradient head and a 16-double
+# scalar tail over the ranks (plus the L-BFGS dots inside each direction
+# update) through NCCL on the context stream, or through a host transport.
+# The host-driven driver below (solve_sharded) stays as the readable
+# restatement the CPU tests check against the oracle.
+
+
+def shard_context_from_device(d_cost_ptr: int, m: int, n_shard: int, sizes, a, b_block,
+                              gamma: float, mu: float, rank: int) -> "G.Context":
+    """Rank `rank`'s shard context: a on rank 0, zeros elsewhere, so the sum of
+    the shards' gradient heads is a - sum_p rowsum_p and of their objectives
+    a.alpha + sum_p (b_p.beta_p - psi_p) (dual.hpp:51, :91-98)."""
+    a_p = np.ascontiguousarray(a, np.float64) if rank == 0 else np.zeros(len(a))
+    return G.Context.shard_from_device(d_cost_ptr, m, n_shard, sizes, a_p, b_block, gamma, mu)
+
+
+def shard_context_from_arrays(cost_block, sizes, a, b_block, gamma: float, mu: float,
+                              rank: int) -> "G.Context":
+    a_p = np.ascontiguousarray(a, np.float64) if rank == 0 else np.zeros(len(a))
+    return G.Context.shard_from_arrays(cost_block, sizes, a_p, b_block, gamma, mu)
+
+
+def attach_comm(ctx: "G.Context", pg=None, transport: str = "auto") -> str:
+    """Attach this rank's communicator to its shard context. transport "nccl":
+    an NCCL communicator (the unique id broadcast over `pg`, or made locally at
+    world size 1); "host": sums through torch.distributed on host memory (gloo);
+    "auto": NCCL unless the process group is gloo. Returns the transport used."""
+    import torch.distributed as dist
+
+    on = pg is not None and dist.is_initialized()
+    world = dist.get_world_size() if on else 1
+    rank = dist.get_rank() if on else 0
+    if transport == "auto":
+        transport = "host" if on and dist.get_backend() == "gloo" else "nccl"
+    if transport == "nccl":
+        uid = [G.nccl_unique_id() if rank == 0 else None]
+        if on and world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        ctx.attach_nccl(uid[0], world, rank)
+        return "nccl"
+
+    import torch
+
+    def allreduce(buf: np.ndarray, op: int) -> None:
+        if world == 1:
+            return
+        t = torch.from_numpy(buf)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)
+
+    ctx.attach_host(world, rank, allreduce)
+    return "host"
+
+
 @dataclass
 class ShardStats:
     """GradStats (screening.hpp:173-188) summed over ranks."""
