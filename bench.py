@@ -532,6 +532,15 @@ def run_ours(args, world, rank, local, pg):
                 regimes[name] = {"launches": rn, "bytes_per_launch": rbytes / rn,
                                  "us_per_launch": 1e3 * rms / rn, "achieved": a,
                                  "frac": a / peak, "share_of_eval_time": rms / tot["ms"]}
+    fetched = None
+    if dom == "k_eval":  # cost bytes actually fetched (8-column quarters) vs the minimum
+        _, fbytes, fn = ctx.profile_read(9)
+        if fn:
+            fetched = {"cost_bytes_per_launch": fbytes / fn,
+                       "vs_algorithmic": fbytes / d["bytes"],
+                       "what": "64-byte quarter rows the evaluation's TMA copies moved, "
+                               "counted by the producer warps (tiles streamed twice count "
+                               "twice), over the algorithmic bytes"}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_kind,
                 "traffic": ncu_traffic(dom, cfg),
@@ -539,6 +548,7 @@ def run_ours(args, world, rank, local, pg):
                 "ms_per_launch": d["ms"] / d["launches"],
                 "share_of_step": d["ms"] / ms_prof,
                 "regimes": regimes,
+                "fetched": fetched,
                 "measured": f"CUDA events around every launch of the kernel on the solver "
                             f"stream, over a second pass of {nprof} solves (the value pass "
                             f"runs uninstrumented)"}

@@ -354,7 +354,9 @@ GSOT_API int gsot_create_config(int32_t cfg, uint64_t seed, double gamma, double
  * nodes inside the solver's graphs) and algorithmic bytes since the last
  * reset. kind: 0 eval(fused blocks), 1 snapshot, 2 bounds, 3 active set,
  * 4 finalize, 5 lbfgs vector ops, 6 delta norms, 7 misc; read-only kind 8:
- * the eval launches that read at least half the dense bytes (near-dense).
+ * the eval launches that read at least half the dense bytes (near-dense);
+ * read-only kind 9: the eval launches with bytes = the cost bytes they
+ * fetched (whole 8-column quarters of each task read), to set beside kind 0.
  * enable: 0 off, negative every class, positive a bit mask (1 << kind) of
  * the classes 0-7. */
 GSOT_API int gsot_profile_enable(gsot_ctx* ctx, int enable);

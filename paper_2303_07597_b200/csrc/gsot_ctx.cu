@@ -286,15 +286,24 @@ void alloc_buffers(gsot_ctx* c) {
     // tiles taller than a segment: the recomputing variant (k_eval<true>)
     bool rec = gmax > seg;
     if (const char* ev = std::getenv("GSOT_EVAL_RECOMPUTE")) rec = std::atoi(ev) != 0;
-    const int var = gsot::eval_variant(gmax, seg, rec);
-    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, 0), var);
+    int var = gsot::eval_variant(gmax, seg, rec);
+    int qrows = 0;
+    // groups taller than a whole-tile segment: the quarter pipeline
+    // (GSOT_EVAL_TALL_OLD=1 keeps the two-pass recomputing variant, for comparison)
+    if (var == 1 && !std::getenv("GSOT_EVAL_TALL_OLD")) {
+      var = 3;
+      qrows = gsot::eval_qrows_for(gmax);
+      seg = gsot::eval_q_short_rows(qrows);
+    }
+    const int bps = gsot::eval_blocks_per_sm(gsot::eval_smem_bytes(seg, qrows), var);
     c->eval_recompute = rec;
     c->eval_variant = var;
     c->eval_buf = seg;
+    c->eval_qrows = qrows;
     c->eval_grid = c->num_sms * bps;
     if (std::getenv("GSOT_DIAG_SEQ"))
       std::fprintf(stderr, "[gsot diag] eval: %d rows per segment, %d CTAs per SM, %zu B shared, variant %d\n",
-                   seg, bps, gsot::eval_smem_bytes(seg, 0), var);
+                   seg, bps, gsot::eval_smem_bytes(seg, qrows), var);
   }
   c->sync();
 }
@@ -319,7 +328,7 @@ void finish_validation(gsot_ctx* c, unsigned long long* d_first_bad, const doubl
     int32_t l = 0;
     while (c->off[l + 1] <= row) ++l;
     const int64_t o0 = c->off[l], g = c->sizes[l];
-    const int64_t el = 32 * (c->nw * o0 + (col >> 5) * g + (row - o0)) + (col & 31);
+    const int64_t el = gsot::cost_index(c->nw, o0, g, col, row - o0);
     GSOT_CUDA_CHECK(cudaMemcpy(&value, c->C + el, sizeof(double), cudaMemcpyDeviceToHost));
     (void)d_src_for_value;
     Error e(GSOT_ERR_NEGATIVE_COST, "cost(" + std::to_string(row) + "," + std::to_string(col) +
@@ -564,10 +573,10 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
     if (mode == GSOT_EVAL_SCREENED)
       launch_eval(P, d_x, c->tasks, -1, &c->sc->ntasks, words, c->rowpart, c->colpart, c->psi,
-                  c->eval_buf, c->eval_variant, c->eval_grid, &c->sc->next_task, c->stream);
+                  c->eval_buf, c->eval_qrows, c->eval_variant, c->eval_grid, &c->sc->next_task, c->stream);
     else
       launch_eval(P, d_x, c->dense_tasks, c->L * c->nw, nullptr, words, c->rowpart, c->colpart,
-                  c->psi, c->eval_buf, c->eval_variant, c->eval_grid, &c->sc->next_task,
+                  c->psi, c->eval_buf, c->eval_qrows, c->eval_variant, c->eval_grid, &c->sc->next_task,
                   c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {

@@ -138,7 +138,8 @@ struct gsot_ctx {
   int eval_grid = 148 * 4;
   int eval_buf = 96;  // rows per shared-memory segment in k_eval
   bool eval_recompute = false;  // k_eval<true>: some block is taller than a segment
-  int eval_variant = 0;         // gsot::eval_variant (0 / 1 recompute / 2 short tiles)
+  int eval_variant = 0;         // gsot::eval_variant (0 / 1 recompute / 2 short tiles / 3 quarters)
+  int eval_qrows = 0;           // variant 3: rows per quarter segment
   int red_blocks = 148 * 2;
   // exact-order mode buffers (gsot_exact2.cu), allocated on first use
   gsot::ExactWs ex;
@@ -274,6 +275,11 @@ struct gsot_ctx {
     prof_ms[mk.kind] += ms;
     prof_bytes[mk.kind] += bytes;
     prof_launches[mk.kind] += 1;
+    if (mk.kind == gsot::K_EVAL) {
+      prof_ms[gsot::K_EVAL_FETCHED] += ms;
+      prof_bytes[gsot::K_EVAL_FETCHED] += 64.0 * static_cast<double>(h_sc->read_qrows);
+      prof_launches[gsot::K_EVAL_FETCHED] += 1;
+    }
     if (mk.kind == gsot::K_EVAL && bytes >= 4.0 * static_cast<double>(m) * static_cast<double>(n)) {
       prof_ms[gsot::K_EVAL_NEAR_DENSE] += ms;
       prof_bytes[gsot::K_EVAL_NEAR_DENSE] += bytes;

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) k_cost(const double* __restrict__ src, in
       const int64_t j = j0 + tx + 16 * b;
       if (j >= n) continue;
       if (tiled)
-        out[32 * ((int64_t)T.nw * o0 + (j >> 5) * (int64_t)g + (i - o0)) + (j & 31)] = acc[a][b];
+        out[cost_index(T.nw, o0, g, j, i - o0)] = acc[a][b];
       else
         out[j * m + i] = acc[a][b];
     }
@@ -313,12 +313,11 @@ __global__ void __launch_bounds__(256) k_scan_bad(DevProblem P, unsigned long lo
   if (i >= P.m) return;
   const int l = P.row_group[i];
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
-  const double* row = P.C + 32 * ((int64_t)P.nw * o0 + (int64_t)c * g + (i - o0));
   unsigned long long bad = ~0ull;
   for (int k = 0; k < 32; ++k) {
     const int64_t j = (int64_t)c * 32 + k;
     if (j >= P.n) break;
-    const double v = row[k];
+    const double v = P.C[cost_index(P.nw, o0, g, j, i - o0)];
     if (!(v >= 0.0) || !isfinite(v)) {
       bad = (unsigned long long)(j * P.m + i);
       break;

@@ -19,9 +19,20 @@ __device__ __forceinline__ double residual(double alpha_i, double beta_j, double
   return dsub(dadd(alpha_i, beta_j), c);
 }
 
-// Address of row 0 of block (l, j); row r is at [32 * r].
+// Address of row 0 of block (l, j); row r is at [kRowStride * r].
 __device__ __forceinline__ const double* block_ptr(const DevProblem& P, int o0, int g, int64_t j) {
-  return P.C + 32 * ((int64_t)P.nw * o0 + (j >> 5) * (int64_t)g) + (j & 31);
+  return P.C + cost_index(P.nw, o0, g, j, 0);
+}
+
+// Quarters (8 columns) of a 32-column word with any bit set, and the lanes of a
+// set of quarters.
+__device__ __forceinline__ uint32_t quarter_mask(uint32_t word) {
+  return ((word & 0xffu) ? 1u : 0u) | ((word & 0xff00u) ? 2u : 0u) | ((word & 0xff0000u) ? 4u : 0u) |
+         ((word & 0xff000000u) ? 8u : 0u);
+}
+__device__ __forceinline__ uint32_t quarter_lanes(uint32_t qm) {
+  return ((qm & 1u) ? 0xffu : 0u) | ((qm & 2u) ? 0xff00u : 0u) | ((qm & 4u) ? 0xff0000u : 0u) |
+         ((qm & 8u) ? 0xff000000u : 0u);
 }
 
 // Warp-wide transpose-reduce of 16 rows: on entry lane t holds v[k] = value of

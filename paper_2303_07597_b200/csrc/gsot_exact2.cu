@@ -73,8 +73,7 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
       const bool act = (sw >> lane) & 1u;
       const int o0 = P.off[l], g = P.off[l + 1] - o0;
       const double* __restrict__ al = x + o0;
-      const double* __restrict__ tp = P.C + 32 * (static_cast<int64_t>(P.nw) * o0 +
-                                                  static_cast<int64_t>(c) * g) + lane;
+      const double* __restrict__ tp = P.C + cost_index(P.nw, o0, g, 32ll * c + lane, 0);
       // pos_part_norm: acc += v * v over the rows, ascending (regularizer.hpp:23-30)
       double z2 = 0.0;
       int r = 0;
@@ -82,7 +81,7 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
         double cv[8], av[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          cv[q] = act ? tp[32 * (r + q)] : 0.0;
+          cv[q] = act ? tp[kRowStride * (r + q)] : 0.0;
           av[q] = __ldg(al + r + q);
         }
 #pragma unroll
@@ -93,7 +92,7 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
         }
       }
       for (; r < g; ++r) {
-        const double f = residual(__ldg(al + r), bj, act ? tp[32 * r] : 0.0);
+        const double f = residual(__ldg(al + r), bj, act ? tp[kRowStride * r] : 0.0);
         const double v = f > 0.0 ? f : 0.0;
         z2 = dadd(z2, dmul(v, v));
       }
@@ -111,7 +110,7 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
         double cv[8], av[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          cv[q] = nz ? tp[32 * (r + q)] : 0.0;
+          cv[q] = nz ? tp[kRowStride * (r + q)] : 0.0;
           av[q] = __ldg(al + r + q);
         }
 #pragma unroll
@@ -124,7 +123,7 @@ __global__ void __launch_bounds__(128) k_ex_cols(DevProblem P, const double* __r
         }
       }
       for (; r < g; ++r) {
-        const double f = residual(__ldg(al + r), bj, nz ? tp[32 * r] : 0.0);
+        const double f = residual(__ldg(al + r), bj, nz ? tp[kRowStride * r] : 0.0);
         const double gg = f > 0.0 ? dmul(scale, f) : 0.0;
         dot = dadd(dot, dmul(f, gg));
         sq = dadd(sq, dmul(gg, gg));
@@ -184,15 +183,21 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
   const int nlw = (P.L + 31) / 32;
   uint32_t head = 0, tail = 0;  // ring: segments issued / consumed (this warp)
   // issue segment s of tile (o0, g, c) into the next slot (lane 0)
-  auto issue = [&](int c, int o0, int g, int sgi) {
+  auto issue = [&](int c, int o0, int g, int sgi, uint32_t qm) {
     const int slot = head % kExD;
     const int r0 = sgi * kExSR, rows = min(kExSR, g - r0);
     const int64_t a0 = (o0 + r0) & ~1ll;
     const uint32_t abytes = static_cast<uint32_t>(((o0 + r0 + rows - a0) + 1) & ~1ll) * 8u;
     const double* tile = P.C + 32 * (static_cast<int64_t>(P.nw) * o0 + static_cast<int64_t>(c) * g);
-    mbar_expect_tx(&W.full[slot], static_cast<uint32_t>(rows) * 256u + abytes);
-    tma_load_1d(W.seg[slot], tile + static_cast<int64_t>(r0) * 32, static_cast<uint32_t>(rows) * 256u,
-                &W.full[slot]);
+    mbar_expect_tx(&W.full[slot],
+                   static_cast<uint32_t>(rows) * 64u * static_cast<uint32_t>(__popc(qm)) + abytes);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // one contiguous run per quarter that is read
+      if ((qm >> q) & 1u)
+        tma_load_1d(W.seg[slot] + q * (kExSR * kPlaneCols),
+                    tile + static_cast<int64_t>(q) * kPlaneCols * g +
+                        static_cast<int64_t>(r0) * kRowStride,
+                    static_cast<uint32_t>(rows) * 64u, &W.full[slot]);
     tma_load_1d(W.al[slot], x + a0, abytes, &W.full[slot]);
     ++head;
   };
@@ -233,19 +238,27 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
           const bool act = (W.gsw[pt] >> lane) & 1u;
           const bool maybe =
               act && !(dadd(P.amax[l], x[P.m + jj]) <= static_cast<double>(P.cmin[static_cast<int64_t>(l) * P.n + jj]));
-          if (!__any_sync(0xffffffffu, maybe)) {
+          const uint32_t mb = __ballot_sync(0xffffffffu, maybe);
+          if (mb == 0u) {
             __syncwarp();
             if (lane == 0) W.grp[pt] = -1 - l;  // marked zero for the walk
             __syncwarp();
             ++pt;
             continue;
           }
+          // a surviving column in a quarter without a possibly-nonzero block is
+          // provably zero (z = 0: no nonzero block, no psi, no column terms):
+          // it leaves the survivor word, and its quarter is not read
+          const uint32_t keep = W.gsw[pt] & quarter_lanes(quarter_mask(mb));
+          __syncwarp();
+          if (lane == 0) W.gsw[pt] = keep;
+          __syncwarp();
         }
         int o0, g;
         tile_geom(pt, o0, g);
         const int ns = (g + kExSR - 1) / kExSR;
         if (lane == 0) {
-          issue(c, o0, g, ps);
+          issue(c, o0, g, ps, quarter_mask(W.gsw[pt]));
         } else {
           ++head;
         }
@@ -278,12 +291,12 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
         pump(t);
         const uint32_t k = resident ? tail + q : tail;
         mbar_wait(&W.full[k % kExD], (k / kExD) & 1u);
-        const double* __restrict__ sg = W.seg[k % kExD] + lane;
+        const double* __restrict__ sg = W.seg[k % kExD] + (lane >> 3) * (kExSR * kPlaneCols) + (lane & 7);
         const double* __restrict__ as = W.al[k % kExD] + ((o0 + q * kExSR) & 1);
         const int rows = min(kExSR, g - q * kExSR);
 #pragma unroll 8
         for (int r = 0; r < rows; ++r) {
-          const double f = residual(as[r], bj, act ? sg[32 * r] : 0.0);
+          const double f = residual(as[r], bj, act ? sg[kRowStride * r] : 0.0);
           const double v = f > 0.0 ? f : 0.0;
           z2 = dadd(z2, dmul(v, v));
         }
@@ -307,7 +320,7 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
           if (!resident) {
             while (issued < ns && head - tail < static_cast<uint32_t>(kExD)) {
               if (lane == 0) {
-                issue(c, o0, g, issued);
+                issue(c, o0, g, issued, quarter_mask(sw));
               } else {
                 ++head;
               }
@@ -316,12 +329,12 @@ __global__ void __launch_bounds__(32 * kExNW, 1)
             k = tail;
             mbar_wait(&W.full[k % kExD], (k / kExD) & 1u);
           }
-          const double* __restrict__ sg = W.seg[k % kExD] + lane;
+          const double* __restrict__ sg = W.seg[k % kExD] + (lane >> 3) * (kExSR * kPlaneCols) + (lane & 7);
           const double* __restrict__ as = W.al[k % kExD] + ((o0 + q * kExSR) & 1);
           const int rows = min(kExSR, g - q * kExSR);
 #pragma unroll 8
           for (int r = 0; r < rows; ++r) {
-            const double f = residual(as[r], bj, nz ? sg[32 * r] : 0.0);
+            const double f = residual(as[r], bj, nz ? sg[kRowStride * r] : 0.0);
             const double gg = f > 0.0 ? dmul(scale, f) : 0.0;
             dot = dadd(dot, dmul(f, gg));
             sq = dadd(sq, dmul(gg, gg));
@@ -380,7 +393,8 @@ __global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __r
   int2* list = reinterpret_cast<int2*>(rows_smem) + static_cast<size_t>(warp) * kRowWin;
   const int nmw = (P.nw + 31) / 32;
   const double* __restrict__ base =
-      P.C + 32 * (static_cast<int64_t>(P.nw) * o0 + r0 + lane);
+      P.C + 32 * static_cast<int64_t>(P.nw) * o0 + kRowStride * static_cast<int64_t>(r0 + lane);
+  const int64_t plane = static_cast<int64_t>(kPlaneCols) * g;  // quarter planes of a tile
   auto load = [&](int t, double (&cv)[32], double& bk, double& sk, uint32_t& nz) {
     const int2 e = list[t];
     const int c = e.x;
@@ -392,7 +406,8 @@ __global__ void __launch_bounds__(128) k_ex_rows(DevProblem P, const double* __r
     const double* __restrict__ row = base + 32 * static_cast<int64_t>(c) * g;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      const double2 v = valid ? *reinterpret_cast<const double2*>(row + 2 * q) : make_double2(0.0, 0.0);
+      const double2 v = valid ? *reinterpret_cast<const double2*>(row + (q >> 2) * plane + 2 * (q & 3))
+                              : make_double2(0.0, 0.0);
       cv[2 * q] = v.x;
       cv[2 * q + 1] = v.y;
     }

@@ -1,8 +1,12 @@
 // gsot_internal.cuh — shared declarations of the sm_100a solver library.
 //
 // Device layout: the cost lives in HBM column-tiled: for
-// group l and 32-column chunk c, a g_l x 32 row-major tile starting at
-// element 32 * (nw * off_l + c * g_l) (columns >= n are zero padding).
+// group l and 32-column chunk c, a tile of g_l x 32 entries starting at
+// element 32 * (nw * off_l + c * g_l) (columns >= n are zero padding). Inside
+// the tile the four 8-column quarters are stored one after the other, each
+// g_l x 8 row-major (64-byte rows): a quarter is ONE contiguous run of
+// g_l * 64 bytes, so an evaluation can fetch only the quarters that hold a
+// possibly-nonzero block (cost_index below).
 // Snapshot norms and per-block partials are [l][j] (j fastest) so that the
 // per-block kernels, which put consecutive target columns on consecutive
 // lanes, read and write them coalesced. Bitmasks are [l][c] words over
@@ -43,6 +47,18 @@ struct Error : std::runtime_error {
     }                                                                                     \
   } while (0)
 
+// Tile geometry: columns per quarter plane; consecutive rows of one column are
+// kRowStride elements apart.
+constexpr int kPlaneCols = 8;
+constexpr int kRowStride = kPlaneCols;
+// Element index of cost entry (row o0 + r of the group at rows [o0, o0 + g),
+// column j) in the tiled layout.
+__host__ __device__ inline int64_t cost_index(int64_t nw, int64_t o0, int64_t g, int64_t j,
+                                              int64_t r) {
+  return 32 * (nw * o0 + (j >> 5) * g) + ((j & 31) >> 3) * (kPlaneCols * g) + kRowStride * r +
+         (j & (kPlaneCols - 1));
+}
+
 // Read-only view of the resident instance passed to every kernel by value.
 struct DevProblem {
   const double* C;        // column-tiled cost, 32 * nw * m doubles
@@ -74,6 +90,7 @@ struct EvalScalars {
   unsigned long long surv_rows;  // sum of g_l over surviving blocks (bytes accounting)
   unsigned long long task_rows;  // sum of g_l over work-list tasks
   unsigned long long zero_rows;  // cost rows of surviving blocks not read (provably zero)
+  unsigned long long read_qrows; // 64-byte quarter rows of cost the evaluation fetched
   int ntasks;        // screened work-list length
   int next_task;     // dynamic scheduler cursor
   unsigned int ticket;  // last-block-done counter
@@ -132,7 +149,10 @@ enum KernelKind {
   // statistics only (not a launch kind): the K_EVAL launches that read at
   // least half the dense bytes (near-dense evaluations, bandwidth-bound)
   K_EVAL_NEAR_DENSE = 8,
-  K_NSTATS = 9
+  // statistics only: the K_EVAL launches again, with bytes = the cost bytes
+  // they actually fetched (whole 8-column quarters of the tasks they read)
+  K_EVAL_FETCHED = 9,
+  K_NSTATS = 10
 };
 
 void launch_relayout(const DevProblem& P, const double* src_colmajor, int64_t j0, int64_t ncols,
@@ -163,16 +183,22 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
 // xe: the evaluation state (the provably-zero test; P.amax must hold its
 // group maxima). Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
-size_t eval_smem_bytes(int buf_rows, int cap);
+// qrows: 0, or the quarter pipeline's rows per quarter segment (variant 3)
+size_t eval_smem_bytes(int buf_rows, int qrows);
+// quarter pipeline geometry for a tallest group of gmax rows: rows per quarter
+// segment, and the tallest group still evaluated as a whole tile
+int eval_qrows_for(int gmax);
+int eval_q_short_rows(int qrows);
 // k_eval variant for a context: 0 in place / 4 consumer warps, 1 recomputing
-// (tiles taller than a segment), 2 in place / 2 consumer warps (short tiles)
+// (tiles taller than a segment; superseded by 3, kept for comparison), 2 in
+// place / 2 consumer warps (short tiles), 3 the quarter pipeline k_eval_q
 int eval_variant(int gmax, int seg, bool recompute);
 int eval_blocks_per_sm(size_t smem, int variant);
 // ntasks >= 0: `tasks` holds that many entries (dense list); -1: the
 // screened list, length *ntasks_dev (written by the screen kernel).
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int seg, int variant, int grid, int* next_task,
+                 double* psi, int seg, int qrows, int variant, int grid, int* next_task,
                  cudaStream_t s);
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) k_relayout(DevProblem P, const double* __
       const int l = P.row_group[i];
       const int o0 = P.off[l], g = P.off[l + 1] - o0;
       const int64_t j = j0 + jj;
-      C[32 * ((int64_t)P.nw * o0 + (j >> 5) * (int64_t)g + (i - o0)) + (j & 31)] = tile[tx][k];
+      C[cost_index(P.nw, o0, g, j, i - o0)] = tile[tx][k];
     }
   }
   for (int o = 16; o >= 1; o >>= 1) {
@@ -137,11 +137,11 @@ __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __
   for (; r + 8 <= g; r += 8) {
     double c[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = __ldcs(cp + 32 * (r + k));
+    for (int k = 0; k < 8; ++k) c[k] = __ldcs(cp + kRowStride * (r + k));
 #pragma unroll
     for (int k = 0; k < 8; ++k) GSOT_SNAP_STEP(__ldg(al + r + k), c[k]);
   }
-  for (; r < g; ++r) GSOT_SNAP_STEP(__ldg(al + r), __ldcs(cp + 32 * r));
+  for (; r < g; ++r) GSOT_SNAP_STEP(__ldg(al + r), __ldcs(cp + kRowStride * r));
 #undef GSOT_SNAP_STEP
   const int64_t idx = (int64_t)l * P.n + j;
   zs[idx] = sqrt(az);
@@ -167,7 +167,7 @@ __device__ __forceinline__ double block_z(const DevProblem& P, const double* __r
   const double* __restrict__ cp = block_ptr(P, o0, g, j);
   double az = 0.0;
   for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, cp[32 * r]);
+    const double f = residual(__ldg(al + r), bj, cp[kRowStride * r]);
     const double v = f > 0.0 ? f : 0.0;
     az = dadd(az, dmul(v, v));
   }
@@ -722,10 +722,10 @@ __global__ void __launch_bounds__(256) k_block_min(DevProblem P, float* __restri
   if (t >= (int64_t)P.L * P.nw) return;
   const int l = (int)(t / P.nw), c = (int)(t % P.nw);
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
-  const double* __restrict__ tile = P.C + 32 * ((int64_t)P.nw * o0 + (int64_t)c * g) + lane;
+  const double* __restrict__ tile = P.C + cost_index(P.nw, o0, g, 32ll * c + lane, 0);
   double v = __longlong_as_double(0x7ff0000000000000ll);  // +inf
 #pragma unroll 8
-  for (int r = 0; r < g; ++r) v = fmin(v, tile[32 * r]);
+  for (int r = 0; r < g; ++r) v = fmin(v, tile[kRowStride * r]);
   const int64_t j = (int64_t)c * 32 + lane;
   if (j < P.n) cmin[(int64_t)l * P.n + j] = __double2float_rd(v);
 }
@@ -794,10 +794,12 @@ struct EvalArgs {
   double* colpart;
   double* psi;
   int seg;          // rows per shared-memory segment (<= kEvalMaxSeg)
+  int qrows;        // quarter pipeline (k_eval_q): rows per quarter segment
   int* next_task;   // global claim cursor (zeroed per evaluation)
   int ntasks;       // >= 0: list length; -1: read *ntasks_dev (screened)
   const int* ntasks_dev;
   unsigned long long* zero_rows;  // bytes accounting: cost rows not read (provably zero)
+  unsigned long long* read_qrows; // bytes accounting: 64-byte quarter rows actually fetched
 };
 
 // consumer warps per CTA: 4, or 2 for short tiles (at most kEvalShortRows rows:
@@ -806,11 +808,16 @@ __host__ __device__ constexpr int eval_threads(int nw) { return 32 * (nw + 1); }
 constexpr int kEvalShortRows = 64;
 constexpr int kEvalMaxSeg = 128;
 // alpha slot length in doubles: seg + 2 (aligned superset), even (16-byte slots)
-__host__ __device__ constexpr int aslot_len(int seg) { return (seg + 3) & ~1; }                     // rows per segment (4 warps x 32 rows)
+__host__ __device__ constexpr int aslot_len(int seg) { return (seg + 3) & ~1; }
+// A slot holds a segment as four quarter planes of [rows][8] (the tile's own
+// order). Plane length in doubles: an odd number of 64-byte rows,
+// so the planes of a half warp's 16 lanes fall on disjoint banks.
+__host__ __device__ constexpr int plane_len(int seg) { return 8 * ((seg + 1) | 1); }
 
 struct EvalTask {
   int l, c, g, o0, nseg, valid;
   uint32_t word;
+  uint32_t qm;  // quarters (8 columns) holding a surviving, possibly-nonzero block: only these are read
   int zero;  // every surviving block of the task provably zero: nothing is read
 };
 
@@ -833,8 +840,9 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
   extern __shared__ __align__(128) unsigned char eval_smem[];
   const DevProblem& P = A.P;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* slots = reinterpret_cast<double*>(eval_smem);  // [2][seg * 32] cost segments
-  double* aslots = slots + 2 * (size_t)A.seg * 32;       // [2][seg + 2] alpha segments
+  const int PS = plane_len(A.seg);
+  double* slots = reinterpret_cast<double*>(eval_smem);  // [2][4][PS] cost segments (quarter planes)
+  double* aslots = slots + 2 * (size_t)4 * PS;           // [2][seg + 2] alpha segments
   double* bslots = aslots + 2 * (size_t)aslot_len(A.seg);     // [2][34] the task's beta chunk
   __shared__ uint64_t full[2], empty[2];
   __shared__ EvalTask tinfo[2];  // by the slot of the task's first segment
@@ -847,6 +855,10 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
     mbar_init(&empty[1], kEvalWarps);
     mbar_fence_init();
   }
+  // the cost slots start zeroed (a quarter that is never fetched must not
+  // hold NaN / Inf bit patterns); generic-proxy writes before the TMA's
+  for (int i = threadIdx.x; i < 2 * 4 * PS; i += blockDim.x) slots[i] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   pdl_wait();
   pdl_trigger();
@@ -871,7 +883,10 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
         const bool act = (w >> lane) & 1u;
         const bool maybe =
             act && !(dadd(P.amax[T.l], A.x[P.m + j]) <= (double)P.cmin[(int64_t)T.l * P.n + j]);
-        T.zero = __any_sync(0xffffffffu, maybe) ? 0 : 1;
+        const uint32_t mb = __ballot_sync(0xffffffffu, maybe);
+        T.qm = ((mb & 0xffu) ? 1u : 0u) | ((mb & 0xff00u) ? 2u : 0u) | ((mb & 0xff0000u) ? 4u : 0u) |
+               ((mb & 0xff000000u) ? 8u : 0u);
+        T.zero = T.qm == 0u;
       }
       return T;
     };
@@ -904,6 +919,17 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
             atomicAdd(A.zero_rows, (unsigned long long)__popc(T.word) * (unsigned long long)T.g);
           }
         } else if (lane == 0) {
+          if (k == 0) {  // bytes accounting: surviving columns in quarters that are not read
+            uint32_t dead = 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (!((T.qm >> q) & 1u)) dead |= 0xffu << (8 * q);
+            if (dead & T.word)
+              atomicAdd(A.zero_rows,
+                        (unsigned long long)__popc(T.word & dead) * (unsigned long long)T.g);
+            atomicAdd(A.read_qrows, (unsigned long long)__popc(T.qm) * (unsigned long long)T.g *
+                                        (unsigned long long)(T.nseg == 1 ? 1 : 2));
+          }
           // alpha rides along with each cost segment (x is 16-byte aligned)
           const int r0 = (k < T.nseg ? k : 2 * T.nseg - 1 - k) * A.seg, rows = min(A.seg, T.g - r0);
           const int64_t a0 = (T.o0 + r0) & ~1ll;  // 16-byte aligned superset of the rows
@@ -912,12 +938,16 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
           const int64_t b0 = (P.m + 32ll * T.c) & ~1ll;
           const int64_t bn = P.m + P.n - b0 < 34 ? P.m + P.n - b0 : 34;
           const uint32_t bbytes = k == 0 ? (uint32_t)((bn + 1) & ~1ll) * 8u : 0u;
-          mbar_expect_tx(&full[slot], (uint32_t)rows * 256u + abytes + bbytes);
+          mbar_expect_tx(&full[slot], (uint32_t)rows * 64u * (uint32_t)__popc(T.qm) + abytes + bbytes);
           // a tile streamed twice stays in L2 between its passes (evict_last
           // on the first pass); everything else is read once (evict_first)
-          tma_load_1d_hint(slots + (size_t)slot * A.seg * 32, tile + (int64_t)r0 * 32,
-                           (uint32_t)rows * 256u, &full[slot],
-                           (T.nseg > 1 && k < T.nseg) ? pol_keep : pol_stream);
+          const uint64_t pol = (T.nseg > 1 && k < T.nseg) ? pol_keep : pol_stream;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)  // one contiguous run per live quarter
+            if ((T.qm >> q) & 1u)
+              tma_load_1d_hint(slots + ((size_t)slot * 4 + q) * PS,
+                               tile + (int64_t)q * kPlaneCols * T.g + (int64_t)r0 * kRowStride,
+                               (uint32_t)rows * 64u, &full[slot], pol);
           tma_load_1d(aslots + (size_t)slot * aslot_len(A.seg), A.x + a0, abytes, &full[slot]);
           if (k == 0) tma_load_1d(bslots + (size_t)slot * 34, A.x + b0, bbytes, &full[slot]);
         }
@@ -940,6 +970,9 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
   int pcol[8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) pcol[p] = hh * 16 + 2 * ((p + rr) & 7);
+  // pair p in the quarter planes: pairs with (p + rr) & 7 < 4 lie in the first
+  // plane of the lane's half, the others in the second
+  const int ql = lane >> 3;  // this lane's quarter (pass 1: lane = column)
   uint32_t e = 0;
   for (;;) {
     mbar_wait_sleep(&full[e & 1u], (e >> 1) & 1u);
@@ -961,6 +994,10 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
     const uint32_t s0 = e & 1u;  // the slot of the task's first segment (its beta chunk)
     const int64_t j = (int64_t)T.c * 32 + lane;
     const bool act = (T.word >> lane) & 1u;
+    // a surviving column in a quarter that was not fetched is provably zero:
+    // z2 = sv = 0 below give the exact zeros its computation would
+    const bool qlive = (T.qm >> ql) & 1u;
+    const bool live = act && qlive;
     const double bj =
         act ? bslots[(size_t)(e & 1u) * 34 + ((P.m + 32ll * T.c) & 1) + lane] : 0.0;
     double z2 = 0.0, sv = 0.0;
@@ -969,27 +1006,41 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
     for (int k = 0; k < ne; ++k, ++e) {
       const int slot = e & 1u;
       if (k > 0) mbar_wait_sleep(&full[slot], (e >> 1) & 1u);
-      double* __restrict__ buf = slots + (size_t)slot * A.seg * 32;
+      double* __restrict__ buf = slots + (size_t)slot * 4 * PS;
       const int sgm = k < T.nseg ? k : 2 * T.nseg - 1 - k;  // pass 2 backwards (L2-warm first)
       const int r0 = sgm * A.seg, rows = min(A.seg, T.g - r0);
       const int R = (rows + kEvalWarps - 1) / kEvalWarps;
       const int w0 = min(rows, warp * R), w1 = min(rows, w0 + R);
       const double* __restrict__ as = aslots + (size_t)slot * aslot_len(A.seg) + ((T.o0 + r0) & 1);
-      double* __restrict__ col = buf + lane;
-      if (act && k < T.nseg) {  // pass 1: accumulate ([f]+ in place of the cost)
+      double* __restrict__ col = buf + ql * PS + (lane & 7);
+      if constexpr (kRecompute) {
+        if (live && k < T.nseg) {  // pass 1: accumulate
 #pragma unroll 4
-        for (int r = w0; r < w1; ++r) {
-          const double v = relu(residual(as[r], bj, col[r * 32]));
-          z2 = dfma(v, v, z2);
-          sv = dadd(sv, v);
-          if constexpr (!kRecompute) col[r * 32] = v;
+          for (int r = w0; r < w1; ++r) {
+            const double v = relu(residual(as[r], bj, col[r * kRowStride]));
+            z2 = dfma(v, v, z2);
+            sv = dadd(sv, v);
+          }
         }
-      }
-      if constexpr (!kRecompute) {
-        if (act && k >= T.nseg) {  // re-streamed segment: [f]+ only
+      } else if (live) {
+        if (k < T.nseg) {  // pass 1: accumulate ([f]+ in place of the cost)
 #pragma unroll 4
-          for (int r = w0; r < w1; ++r) col[r * 32] = relu(residual(as[r], bj, col[r * 32]));
+          for (int r = w0; r < w1; ++r) {
+            const double v = relu(residual(as[r], bj, col[r * kRowStride]));
+            z2 = dfma(v, v, z2);
+            sv = dadd(sv, v);
+            col[r * kRowStride] = v;
+          }
+        } else {  // re-streamed segment: [f]+ only
+#pragma unroll 4
+          for (int r = w0; r < w1; ++r)
+            col[r * kRowStride] = relu(residual(as[r], bj, col[r * kRowStride]));
         }
+      } else if (!qlive) {
+        // the columns of a quarter that was not fetched get zeros, so pass 2
+        // never meets stale shared memory
+#pragma unroll 4
+        for (int r = w0; r < w1; ++r) col[r * kRowStride] = 0.0;
       }
       if (k == T.nseg - 1) {  // pass 1 complete: the warps in order (warp 0)
         zsh[warp][lane] = z2;
@@ -1039,16 +1090,19 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
         // (rr, hh) sums half hh of a row, two columns per 16-byte load (pairs in
         // rotated order: no bank conflicts), then the two halves; 16 rows at a
         // time. Inactive columns have scale 0 and a finite [f]+: an exact zero,
-        // as in a dense evaluation.
+        // as in a dense evaluation; a quarter that was not fetched has every
+        // scale 0 and holds zeros (in place) or stale finite costs
+        // (recomputing variant: the slots start zeroed).
         __syncwarp();
         for (int rb = w0; rb < w1; rb += 16) {
           double acc = 0.0;
           if (rr < w1 - rb) {
-            const double* __restrict__ row = buf + (rb + rr) * 32;
+            const double* __restrict__ row = buf + (rb + rr) * kRowStride;
             const double ar = kRecompute ? as[rb + rr] : 0.0;
 #pragma unroll
             for (int p = 0; p < 8; ++p) {
-              const double2 v = *reinterpret_cast<const double2*>(row + pcol[p]);
+              const double2 v = *reinterpret_cast<const double2*>(
+                  row + (pcol[p] >> 3) * PS + (pcol[p] & 7));
               if constexpr (kRecompute) {
                 acc = dfma(scr[2 * p], relu(residual(ar, bq[2 * p], v.x)), acc);
                 acc = dfma(scr[2 * p + 1], relu(residual(ar, bq[2 * p + 1], v.y)), acc);
@@ -1069,21 +1123,440 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
   TL_EXIT(P.tl, TL_EVAL);
 }
 
+
+// ---------------------------------------------------------------- quarter pipeline
+// The evaluation for instances with groups taller than a whole-tile segment
+// (variant 3). The cost tile of a task is stored as four 8-column quarter
+// planes, each one contiguous run of g_l * 64 bytes, so a
+// group of up to `qrows` rows fits a 32 KB slot one QUARTER at a time:
+//   short tasks (g <= seg): the whole tile in one slot, computed as in k_eval
+//     (lane = column; [f]+ in place; row sums from shared memory);
+//   tall tasks: one step per live quarter. Thread (warp w, lane) = (row slice
+//     rs = lane / 8, column cj = lane % 8) walks rows 16 i + 4 w + rs in pass 1
+//     ([f]+ in place, z^2 and sum [f]+ chains; a warp reads 256 contiguous
+//     bytes per step); the 16 partials per column are folded by a fixed
+//     butterfly (lanes) and in warp order; pass 2 is one thread per row over
+//     the quarter's 8 columns (16-byte loads, pairs rotated by (lane / 2) % 4:
+//     no bank conflicts), the row's sum carried in a register across the
+//     task's quarters. The tile is read ONCE; quarters without a surviving,
+//     possibly-nonzero block are never fetched.
+//   groups taller than qrows: per quarter, 2 x ceil(g / qrows) steps (pass 2
+//     streams the quarter again, from L2, and recomputes [f]+); the row sums
+//     of the task's quarters are added in global memory by the thread that
+//     owns the row.
+// As in k_eval every association depends only on the shape (g_l, seg, qrows),
+// never on the screen: quarters that are not fetched and inactive columns
+// contribute exact zeros.
+__global__ void __launch_bounds__(eval_threads(4), 3) k_eval_q(const EvalArgs A) {
+  constexpr int NW = 4;
+  extern __shared__ __align__(128) unsigned char eval_smem[];
+  const DevProblem& P = A.P;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int PS = plane_len(A.seg), QR = A.qrows;
+  const int slot_len = max(4 * PS, QR * kPlaneCols);
+  const int al_len = aslot_len(max(A.seg, QR));
+  double* slots = reinterpret_cast<double*>(eval_smem);  // [2][slot_len]
+  double* aslots = slots + 2 * (size_t)slot_len;         // [2][al_len]
+  double* bslots = aslots + 2 * (size_t)al_len;          // [2][34]
+  __shared__ uint64_t full[2], empty[2];
+  __shared__ EvalTask tinfo[2];
+  __shared__ double zsh[NW][32], ssh[NW][32];
+  __shared__ __align__(16) double scale_sh[32];
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], NW);
+    mbar_init(&empty[1], NW);
+    mbar_fence_init();
+  }
+  for (int i = threadIdx.x; i < 2 * slot_len; i += blockDim.x) slots[i] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  TL_ENTER(P.tl, TL_EVAL);
+  if (warp == NW) {  // ---- producer
+    const int ntasks = A.ntasks >= 0 ? A.ntasks : *(volatile const int*)A.ntasks_dev;
+    auto fetch = [&](int t) {
+      EvalTask T{};
+      T.valid = t < ntasks;
+      if (T.valid) {
+        const int4 a = __ldg(reinterpret_cast<const int4*>(A.order + t));
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(A.order + t) + 4);
+        T.l = a.x;
+        T.c = a.y;
+        T.o0 = a.z;
+        T.g = a.w;
+        T.word = w;
+        T.nseg = T.g <= A.seg ? 1 : (T.g + QR - 1) / QR;
+        const int64_t j = 32ll * T.c + lane;
+        const bool act = (w >> lane) & 1u;
+        const bool maybe =
+            act && !(dadd(P.amax[T.l], A.x[P.m + j]) <= (double)P.cmin[(int64_t)T.l * P.n + j]);
+        T.qm = quarter_mask(__ballot_sync(0xffffffffu, maybe));
+        T.zero = T.qm == 0u;
+      }
+      return T;
+    };
+    auto claim = [&]() {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(A.next_task, 1);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    const int G = (int)gridDim.x;
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+    uint32_t e = 0;
+    EvalTask T = fetch(blockIdx.x);
+    int tn = T.valid ? G + claim() : ntasks;
+    // one step: wait for the slot, publish the task with its first step
+    auto acquire = [&](bool first) {
+      const int slot = e & 1u;
+      if (e >= 2) mbar_wait_sleep(&empty[slot], ((e >> 1) - 1) & 1u);
+      if (first && lane == 0) tinfo[slot] = T;
+      return slot;
+    };
+    auto alpha_beta = [&](int slot, int r0, int rows, uint32_t& bytes) {  // lane 0
+      const int64_t a0 = (T.o0 + r0) & ~1ll;
+      const uint32_t abytes = (uint32_t)(((T.o0 + r0 + rows - a0) + 1) & ~1ll) * 8u;
+      const int64_t b0 = (P.m + 32ll * T.c) & ~1ll;
+      const int64_t bn = P.m + P.n - b0 < 34 ? P.m + P.n - b0 : 34;
+      const uint32_t bbytes = (uint32_t)((bn + 1) & ~1ll) * 8u;
+      bytes += abytes + bbytes;
+      mbar_expect_tx(&full[slot], bytes);
+      tma_load_1d(aslots + (size_t)slot * al_len, A.x + a0, abytes, &full[slot]);
+      tma_load_1d(bslots + (size_t)slot * 34, A.x + b0, bbytes, &full[slot]);
+    };
+    for (;;) {
+      EvalTask Tn{};
+      bool first = true;
+      auto prefetch_next = [&]() {  // decode the next task while this one loads
+        Tn = fetch(tn);
+        tn = Tn.valid ? G + claim() : ntasks;
+      };
+      if (!T.valid) {
+        const int slot = acquire(true);
+        if (lane == 0) mbar_arrive(&full[slot]);  // end marker
+        break;
+      }
+      const double* tile = P.C + 32 * ((int64_t)P.nw * T.o0 + (int64_t)T.c * T.g);
+      if (T.zero) {
+        const int slot = acquire(true);
+        if (lane == 0) {
+          mbar_arrive(&full[slot]);
+          atomicAdd(A.zero_rows, (unsigned long long)__popc(T.word) * (unsigned long long)T.g);
+        }
+        ++e;
+        prefetch_next();
+        T = Tn;
+        continue;
+      }
+      if (lane == 0) {  // bytes accounting
+        const uint32_t dead = ~quarter_lanes(T.qm);
+        if (dead & T.word)
+          atomicAdd(A.zero_rows, (unsigned long long)__popc(T.word & dead) * (unsigned long long)T.g);
+        atomicAdd(A.read_qrows, (unsigned long long)__popc(T.qm) * (unsigned long long)T.g *
+                                    (unsigned long long)(T.nseg == 1 ? 1 : 2));
+      }
+      if (T.g <= A.seg) {  // short: the whole tile (its live quarters) in one step
+        const int slot = acquire(true);
+        if (lane == 0) {
+          uint32_t bytes = (uint32_t)T.g * 64u * (uint32_t)__popc(T.qm);
+          alpha_beta(slot, 0, T.g, bytes);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if ((T.qm >> q) & 1u)
+              tma_load_1d_hint(slots + (size_t)slot * slot_len + (size_t)q * PS,
+                               tile + (int64_t)q * kPlaneCols * T.g, (uint32_t)T.g * 64u,
+                               &full[slot], pol_stream);
+        }
+        ++e;
+        prefetch_next();
+      } else {
+        const int ne = T.nseg == 1 ? 1 : 2 * T.nseg;
+        for (int q = 0; q < 4; ++q) {
+          if (!((T.qm >> q) & 1u)) continue;
+          for (int k = 0; k < ne; ++k, ++e) {
+            const int slot = acquire(first);
+            if (lane == 0) {
+              const int r0 = (k < T.nseg ? k : 2 * T.nseg - 1 - k) * QR, rows = min(QR, T.g - r0);
+              uint32_t bytes = (uint32_t)rows * 64u;
+              alpha_beta(slot, r0, rows, bytes);
+              tma_load_1d_hint(slots + (size_t)slot * slot_len,
+                               tile + (int64_t)q * kPlaneCols * T.g + (int64_t)r0 * kRowStride,
+                               (uint32_t)rows * 64u, &full[slot],
+                               (T.nseg > 1 && k < T.nseg) ? pol_keep : pol_stream);
+            }
+            if (first) {
+              first = false;
+              prefetch_next();
+            }
+          }
+        }
+      }
+      T = Tn;
+    }
+    return;
+  }
+  // ---- consumers
+  const int rr = lane & 15, hh = lane >> 4;  // short tasks, pass 2 (as k_eval)
+  int pcol[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) pcol[p] = hh * 16 + 2 * ((p + rr) & 7);
+  const int ql = lane >> 3;
+  const int rs = lane >> 3, cj = lane & 7;  // tall tasks, pass 1
+  const int rho = (lane >> 1) & 3;          // tall tasks, pass 2: pair rotation
+  const int trow = warp * 32 + lane;        // tall tasks, pass 2: first row of the thread
+  uint32_t e = 0;
+  for (;;) {
+    mbar_wait_sleep(&full[e & 1u], (e >> 1) & 1u);
+    const EvalTask T = tinfo[e & 1u];
+    if (!T.valid) break;
+    if (T.zero) {
+      for (int r = warp * 32 + lane; r < T.g; r += 32 * NW)
+        A.rowpart[(int64_t)T.c * P.m + T.o0 + r] = 0.0;
+      if (warp == 0 && ((T.word >> lane) & 1u)) {
+        const int64_t idx = (int64_t)T.l * P.n + (int64_t)T.c * 32 + lane;
+        A.colpart[idx] = 0.0;
+        A.psi[idx] = 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[e & 1u]);
+      ++e;
+      continue;
+    }
+    const int boff = (int)((P.m + 32ll * T.c) & 1);
+    if (T.g <= A.seg) {
+      // ---- short task: one resident step, lane = column (k_eval's in-place form)
+      const int slot = e & 1u;
+      double* __restrict__ buf = slots + (size_t)slot * slot_len;
+      const int64_t j = (int64_t)T.c * 32 + lane;
+      const bool act = (T.word >> lane) & 1u;
+      const bool qlive = (T.qm >> ql) & 1u;
+      const bool live = act && qlive;
+      const double bj = act ? bslots[(size_t)slot * 34 + boff + lane] : 0.0;
+      const int rows = T.g;
+      const int R = (rows + NW - 1) / NW;
+      const int w0 = min(rows, warp * R), w1 = min(rows, w0 + R);
+      const double* __restrict__ as = aslots + (size_t)slot * al_len + (T.o0 & 1);
+      double* __restrict__ col = buf + ql * PS + cj;
+      double z2 = 0.0, sv = 0.0;
+      if (live) {
+#pragma unroll 4
+        for (int r = w0; r < w1; ++r) {
+          const double v = relu(residual(as[r], bj, col[r * kRowStride]));
+          z2 = dfma(v, v, z2);
+          sv = dadd(sv, v);
+          col[r * kRowStride] = v;
+        }
+      } else if (!qlive) {  // a quarter that was not fetched gets zeros
+#pragma unroll 4
+        for (int r = w0; r < w1; ++r) col[r * kRowStride] = 0.0;
+      }
+      zsh[warp][lane] = z2;
+      ssh[warp][lane] = sv;
+      consumer_sync<NW>();
+      if (warp == 0) {
+        double zz = zsh[0][lane], ss = ssh[0][lane];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          zz = dadd(zz, zsh[w][lane]);
+          ss = dadd(ss, ssh[w][lane]);
+        }
+        const double z = sqrt(zz);
+        const bool nz = act && z > P.tau;
+        const double d = dsub(z, P.tau);
+        const double scale = !nz ? 0.0 : ddiv(d, dmul(P.gamma, z));
+        scale_sh[lane] = scale;
+        if (act) {
+          const int64_t idx = (int64_t)T.l * P.n + j;
+          A.colpart[idx] = dmul(scale, ss);
+          A.psi[idx] = !nz ? 0.0 : dmul(dmul(d, d), P.half_inv_gamma);
+        }
+      }
+      consumer_sync<NW>();
+      double scr[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) scr[q] = scale_sh[pcol[q >> 1] + (q & 1)];
+      for (int rb = w0; rb < w1; rb += 16) {
+        double acc = 0.0;
+        if (rr < w1 - rb) {
+          const double* __restrict__ row = buf + (rb + rr) * kRowStride;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const double2 v =
+                *reinterpret_cast<const double2*>(row + (pcol[p] >> 3) * PS + (pcol[p] & 7));
+            acc = dfma(scr[2 * p], v.x, acc);
+            acc = dfma(scr[2 * p + 1], v.y, acc);
+          }
+        }
+        acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, 16));
+        if (hh == 0 && rr < w1 - rb) A.rowpart[(int64_t)T.c * P.m + T.o0 + rb + rr] = acc;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      ++e;
+      continue;
+    }
+    // ---- tall task: its live quarters one after the other
+    if (warp == 0) {  // survivors in quarters that are not fetched: exact zeros
+      if (((T.word & ~quarter_lanes(T.qm)) >> lane) & 1u) {
+        const int64_t idx = (int64_t)T.l * P.n + (int64_t)T.c * 32 + lane;
+        A.colpart[idx] = 0.0;
+        A.psi[idx] = 0.0;
+      }
+    }
+    const int nseg = T.nseg;
+    double racc[4] = {0.0, 0.0, 0.0, 0.0};  // resident quarters: the rows' sums so far
+    bool first_step = true, first_q = true;
+    for (int q = 0; q < 4; ++q) {
+      if (!((T.qm >> q) & 1u)) continue;
+      const bool act = (T.word >> (8 * q + cj)) & 1u;
+      double z2 = 0.0, sv = 0.0;
+      double2 sr[4], br[4];  // this thread's rotated scale / beta pairs (pass 2)
+      const int ne = nseg == 1 ? 1 : 2 * nseg;
+      for (int k = 0; k < ne; ++k, ++e) {
+        const int slot = e & 1u;
+        if (!first_step) mbar_wait_sleep(&full[slot], (e >> 1) & 1u);
+        first_step = false;
+        double* __restrict__ buf = slots + (size_t)slot * slot_len;
+        const int sgm = k < nseg ? k : 2 * nseg - 1 - k;
+        const int r0 = sgm * QR, rows = min(QR, T.g - r0);
+        const double* __restrict__ as = aslots + (size_t)slot * al_len + ((T.o0 + r0) & 1);
+        const double* __restrict__ bs = bslots + (size_t)slot * 34 + boff + 8 * q;
+        if (k < nseg && act) {  // pass 1
+          const double bj = bs[cj];
+          double* __restrict__ colp = buf + cj;
+          if (nseg == 1) {
+#pragma unroll 4
+            for (int r = 4 * warp + rs; r < rows; r += 16) {
+              const double v = relu(residual(as[r], bj, colp[r * kRowStride]));
+              z2 = dfma(v, v, z2);
+              sv = dadd(sv, v);
+              colp[r * kRowStride] = v;
+            }
+          } else {
+#pragma unroll 4
+            for (int r = 4 * warp + rs; r < rows; r += 16) {
+              const double v = relu(residual(as[r], bj, colp[r * kRowStride]));
+              z2 = dfma(v, v, z2);
+              sv = dadd(sv, v);
+            }
+          }
+        }
+        if (k == nseg - 1) {  // pass 1 complete: fold the 16 partials per column
+          z2 = dadd(z2, __shfl_xor_sync(0xffffffffu, z2, 8));
+          sv = dadd(sv, __shfl_xor_sync(0xffffffffu, sv, 8));
+          z2 = dadd(z2, __shfl_xor_sync(0xffffffffu, z2, 16));
+          sv = dadd(sv, __shfl_xor_sync(0xffffffffu, sv, 16));
+          if (lane < 8) {
+            zsh[warp][lane] = z2;
+            ssh[warp][lane] = sv;
+          }
+          consumer_sync<NW>();
+          if (warp == 0 && lane < 8) {
+            double zz = zsh[0][lane], ss = ssh[0][lane];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) {
+              zz = dadd(zz, zsh[w][lane]);
+              ss = dadd(ss, ssh[w][lane]);
+            }
+            const double z = sqrt(zz);
+            const bool nz = act && z > P.tau;
+            const double d = dsub(z, P.tau);
+            const double scale = !nz ? 0.0 : ddiv(d, dmul(P.gamma, z));
+            scale_sh[lane] = scale;
+            if (act) {
+              const int64_t idx = (int64_t)T.l * P.n + (int64_t)T.c * 32 + 8 * q + lane;
+              A.colpart[idx] = dmul(scale, ss);
+              A.psi[idx] = !nz ? 0.0 : dmul(dmul(d, d), P.half_inv_gamma);
+            }
+          }
+          consumer_sync<NW>();
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int cp = 2 * ((p + rho) & 3);
+            sr[p] = *reinterpret_cast<const double2*>(scale_sh + cp);
+            // beta pair (columns >= n: 0; their scale is 0)
+            const int64_t jc = 32ll * T.c + 8 * q + cp;
+            br[p].x = jc < P.n ? bs[cp] : 0.0;
+            br[p].y = jc + 1 < P.n ? bs[cp + 1] : 0.0;
+          }
+        }
+        if (nseg == 1 || k >= nseg) {  // pass 2: one thread per row
+#pragma unroll
+          for (int ri = 0; ri < 4; ++ri) {
+            const int r = trow + 128 * ri;
+            if (r < rows) {
+              const double* __restrict__ row = buf + r * kRowStride;
+              double acc = nseg == 1 ? racc[ri] : 0.0;
+              const double ar = nseg == 1 ? 0.0 : as[r];
+#pragma unroll
+              for (int p = 0; p < 4; ++p) {
+                const double2 v = *reinterpret_cast<const double2*>(row + 2 * ((p + rho) & 3));
+                if (nseg == 1) {
+                  acc = dfma(sr[p].x, v.x, acc);
+                  acc = dfma(sr[p].y, v.y, acc);
+                } else {
+                  acc = dfma(sr[p].x, relu(residual(ar, br[p].x, v.x)), acc);
+                  acc = dfma(sr[p].y, relu(residual(ar, br[p].y, v.y)), acc);
+                }
+              }
+              if (nseg == 1) {
+                racc[ri] = acc;
+              } else {  // the row's owner adds the quarters in order
+                double* dst = A.rowpart + (int64_t)T.c * P.m + T.o0 + r0 + r;
+                *dst = first_q ? acc : dadd(*dst, acc);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+      first_q = false;
+    }
+    if (nseg == 1) {
+#pragma unroll
+      for (int ri = 0; ri < 4; ++ri) {
+        const int r = trow + 128 * ri;
+        if (r < T.g) A.rowpart[(int64_t)T.c * P.m + T.o0 + r] = racc[ri];
+      }
+    }
+  }
+  TL_EXIT(P.tl, TL_EVAL);
+}
+
+// rows per quarter segment of the quarter pipeline: the tallest group when a
+// slot of that size still leaves three CTAs per SM, else 448
+int eval_qrows_for(int gmax) { return gmax <= 500 ? std::max(gmax, 16) : 448; }
+// the tallest group evaluated as a whole tile: its four padded planes fit the
+// slot of a quarter segment (at least 32,000 bytes)
+int eval_q_short_rows(int qrows) {
+  const int h = std::max(qrows, 500) / 4;  // plane rows incl. padding: (rows + 1) | 1 <= h
+  return std::min(kEvalMaxSeg, (h & 1) ? h - 1 : h - 2);
+}
+
 namespace {
-int g_eval_smem_attr[3] = {0, 0, 0};
+int g_eval_smem_attr[4] = {0, 0, 0, 0};
 }
 
 // Rows per segment: the tallest group when it fits, else kEvalMaxSeg.
 int eval_buf_rows(int gmax) { return std::max(8, std::min(gmax, kEvalMaxSeg)); }
 
-size_t eval_smem_bytes(int seg, int cap) {
-  (void)cap;
-  return sizeof(double) * 2 * ((size_t)seg * 32 + aslot_len(seg) + 34);
+size_t eval_smem_bytes(int seg, int qrows) {
+  if (qrows > 0)  // quarter pipeline: a slot holds a whole short tile or one quarter segment
+    return sizeof(double) * 2 *
+           ((size_t)std::max(4 * plane_len(seg), qrows * kPlaneCols) +
+            aslot_len(std::max(seg, qrows)) + 34);
+  return sizeof(double) * 2 * ((size_t)4 * plane_len(seg) + aslot_len(seg) + 34);
 }
 
 // variant: 0 in place (4 consumer warps), 1 recomputing (4), 2 in place (2)
 static void (*eval_kernel(int variant))(const EvalArgs) {
-  return variant == 1 ? k_eval<true, 4> : variant == 2 ? k_eval<false, 2> : k_eval<false, 4>;
+  return variant == 3   ? k_eval_q
+         : variant == 1 ? k_eval<true, 4>
+         : variant == 2 ? k_eval<false, 2>
+                        : k_eval<false, 4>;
 }
 static int eval_nthreads(int variant) { return eval_threads(variant == 2 ? 2 : 4); }
 
@@ -1112,15 +1585,16 @@ int eval_blocks_per_sm(size_t smem, int variant) {
 
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
-                 double* psi, int seg, int variant, int grid, int* next_task, cudaStream_t s) {
+                 double* psi, int seg, int qrows, int variant, int grid, int* next_task,
+                 cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0)
     throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
   // next_task is EvalScalars::next_task: zero_rows lives in the same block
   EvalScalars* sc = reinterpret_cast<EvalScalars*>(reinterpret_cast<char*>(next_task) -
                                                    offsetof(EvalScalars, next_task));
-  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, next_task, ntasks, ntasks_dev,
-             &sc->zero_rows};
-  const size_t smem = eval_smem_bytes(seg, 0);
+  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, qrows, next_task, ntasks, ntasks_dev,
+             &sc->zero_rows, &sc->read_qrows};
+  const size_t smem = eval_smem_bytes(seg, qrows);
   if ((int)smem > g_eval_smem_attr[variant]) eval_blocks_per_sm(smem, variant);
   launch_pdl(eval_kernel(variant), dim3(grid), dim3(eval_nthreads(variant)), smem, s, A);
 }
@@ -1432,7 +1906,7 @@ __global__ void __launch_bounds__(256) k_plan(DevProblem P, const double* __rest
   }
   const double scale = ddiv(dsub(1.0, ddiv(P.tau, z)), P.gamma);
   for (int r = 0; r < g; ++r) {
-    const double f = residual(__ldg(al + r), bj, cp[32 * r]);
+    const double f = residual(__ldg(al + r), bj, cp[kRowStride * r]);
     o[r] = f > 0.0 ? dmul(scale, f) : 0.0;
   }
 }
@@ -1472,7 +1946,7 @@ __global__ void __launch_bounds__(128) k_plan_diag(DevProblem P, const double* _
   for (int r = 0; r < g; ++r) {
     double t = 0.0;
     if (nz) {
-      const double f = residual(__ldg(x + o0 + r), bj, cp[32 * r]);
+      const double f = residual(__ldg(x + o0 + r), bj, cp[kRowStride * r]);
       t = f > 0.0 ? dmul(scale, f) : 0.0;
     }
     colsum = dadd(colsum, t);
@@ -1507,7 +1981,7 @@ __global__ void __launch_bounds__(128) k_plan_primal(DevProblem P, const double*
     const double* __restrict__ cp = block_ptr(P, o0, g, j);
     double tc = 0.0, tt = 0.0;
     for (int r = 0; r < g; ++r) {
-      const double c = cp[32 * r];
+      const double c = cp[kRowStride * r];
       const double f = residual(__ldg(x + o0 + r), bj, c);
       const double t = f > 0.0 ? dmul(scale, f) : 0.0;
       tc = dadd(tc, dmul(t, c));

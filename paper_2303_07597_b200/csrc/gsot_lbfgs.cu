@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(256) k_publish(DevSync* __restrict__ src, DevS
     sc->ntasks = 0;        // the next screened evaluation starts from zeroed cursors
     sc->next_task = 0;
     sc->zero_rows = 0ull;
+    sc->read_qrows = 0ull;
     sc->ticket = 0u;
     sc->audit_violation = 0;
     sc->audit_where = 0;

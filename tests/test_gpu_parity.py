@@ -675,11 +675,13 @@ def test_tall_blocks_streamed_twice(o):
 
 @pytest.mark.parametrize("sizes", [[100, 28, 5], [300, 129, 7]])
 def test_eval_variants_agree_bitwise(o, sizes, monkeypatch):
-    # k_eval<false> writes [f]+ in place, k_eval<true> (chosen when a block is
-    # taller than a segment) recomputes it in pass 2: the same bits either way.
+    # k_eval<false> writes [f]+ in place, k_eval<true> (the two-pass variant for
+    # blocks taller than a segment, kept behind GSOT_EVAL_TALL_OLD for comparison
+    # with the quarter pipeline) recomputes it in pass 2: the same bits either way.
     p, rng = random_problem(sizes, 70, 0.3, 0.6, 41, weighted=True)
     x = np.concatenate([rng.uniform(-0.1, 1.2, p.m) * 1e-3, rng.uniform(-0.1, 1.2, p.n)])
     out = []
+    monkeypatch.setenv("GSOT_EVAL_TALL_OLD", "1")
     for v in ("0", "1"):
         monkeypatch.setenv("GSOT_EVAL_RECOMPUTE", v)
         monkeypatch.setenv("GSOT_CTX_CACHE", "0")
@@ -692,3 +694,42 @@ def test_eval_variants_agree_bitwise(o, sizes, monkeypatch):
     assert d0[0] == d1[0] and np.array_equal(d0[1], d1[1])
     assert s0[0] == s1[0] and np.array_equal(s0[1], s1[1])
     assert_eval_close(o, p, x, d1[0], d1[1])
+
+
+@pytest.mark.parametrize("sizes,n", [([500, 124, 125, 449, 448, 3], 70),
+                                     ([1100, 460, 200, 64, 9], 45),
+                                     ([129] * 5 + [16, 1], 33)])
+def test_quarter_pipeline(o, sizes, n, monkeypatch):
+    # k_eval_q (instances with a group taller than a whole-tile segment): short
+    # groups as whole tiles, taller ones one 8-column quarter at a time (resident
+    # up to the quarter-segment rows, streamed twice above), quarters without a
+    # possibly-nonzero block never fetched. beta is pushed far down on runs of
+    # columns so that whole quarters are provably zero. Against the oracle;
+    # screened == dense bitwise; repeatable; fast == baseline solve bitwise.
+    monkeypatch.setenv("GSOT_CTX_CACHE", "0")
+    p, rng = random_problem(sizes, n, 0.3, 0.6, 51 + n, weighted=True)
+    ctx = ctx_of(p)
+    x0 = np.zeros(p.m + p.n)
+    beta = rng.uniform(-0.1, 1.2, p.n)
+    for lo, hi in ((3, 14), (16, 24), (40, 41), (n - 9, n - 1)):
+        beta[lo:hi] = -3.0
+    x1 = np.concatenate([rng.uniform(-0.1, 1.2, p.m) * 1e-2, beta])
+    x2 = x1 + 1e-5 * rng.normal(size=x1.size)
+    obj, g, _ = ctx.eval(x1)
+    assert_eval_close(o, p, x1, obj, g)
+    ctx.init_snapshot(x0)
+    ctx.refresh(x1, True)
+    mem_o, _ = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+    obj_s, g_s, st = ctx.eval(x2, screened=True)
+    ga, gb, c_o, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem_o, x2[: p.m], x2[p.m:])
+    assert [st.in_active, st.skipped, st.unskipped, st.upper_bounds] == c_o.tolist()
+    assert_eval_close(o, p, x2, obj_s, g_s, None, np.concatenate([ga, gb]))
+    obj_d, g_d, _ = ctx.eval(x2)
+    assert obj_d == obj_s and np.array_equal(g_d, g_s)
+    for _ in range(3):
+        obj_r, g_r, _ = ctx.eval(x2)
+        assert obj_r == obj_d and np.array_equal(g_r, g_d)
+    rb = ctx.solve(mode=0, max_outer_loops=3, grad_tol=1e-12)
+    rf = ctx.solve(mode=1, max_outer_loops=3, grad_tol=1e-12)
+    assert np.array_equal(rf["x"], rb["x"]) and rf["objective"] == rb["objective"]
+    ctx.close()
