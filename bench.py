@@ -216,7 +216,8 @@ def ncu_traffic(kernel: str, cfg: int):
         return None
     with open(p) as f:
         d = json.load(f)
-    ent = d.get(kernel)
+    # the fused evaluation is k_eval or, for instances with tall groups, k_eval_q
+    ent = d.get(kernel) or (d.get("k_eval_q") if kernel == "k_eval" else None)
     return None if ent is None else ent.get("dram_bytes_per_launch")
 
 

@@ -795,6 +795,7 @@ struct EvalArgs {
   double* psi;
   int seg;          // rows per shared-memory segment (<= kEvalMaxSeg)
   int qrows;        // quarter pipeline (k_eval_q): rows per quarter segment
+  int qrec;         // quarter pipeline: resident quarters recompute [f]+ in pass 2 (no in-place store)
   int* next_task;   // global claim cursor (zeroed per evaluation)
   int ntasks;       // >= 0: list length; -1: read *ntasks_dev (screened)
   const int* ntasks_dev;
@@ -1426,7 +1427,7 @@ __global__ void __launch_bounds__(eval_threads(4), 3) k_eval_q(const EvalArgs A)
         if (k < nseg && act) {  // pass 1
           const double bj = bs[cj];
           double* __restrict__ colp = buf + cj;
-          if (nseg == 1) {
+          if (nseg == 1 && !A.qrec) {
 #pragma unroll 4
             for (int r = 4 * warp + rs; r < rows; r += 16) {
               const double v = relu(residual(as[r], bj, colp[r * kRowStride]));
@@ -1489,11 +1490,12 @@ __global__ void __launch_bounds__(eval_threads(4), 3) k_eval_q(const EvalArgs A)
             if (r < rows) {
               const double* __restrict__ row = buf + r * kRowStride;
               double acc = nseg == 1 ? racc[ri] : 0.0;
-              const double ar = nseg == 1 ? 0.0 : as[r];
+              const bool inplace = nseg == 1 && !A.qrec;
+              const double ar = inplace ? 0.0 : as[r];
 #pragma unroll
               for (int p = 0; p < 4; ++p) {
                 const double2 v = *reinterpret_cast<const double2*>(row + 2 * ((p + rho) & 3));
-                if (nseg == 1) {
+                if (inplace) {
                   acc = dfma(sr[p].x, v.x, acc);
                   acc = dfma(sr[p].y, v.y, acc);
                 } else {
@@ -1592,7 +1594,13 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
   // next_task is EvalScalars::next_task: zero_rows lives in the same block
   EvalScalars* sc = reinterpret_cast<EvalScalars*>(reinterpret_cast<char*>(next_task) -
                                                    offsetof(EvalScalars, next_task));
-  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, qrows, next_task, ntasks, ntasks_dev,
+  static const int qrec = [] {
+    // measured: recomputing [f]+ in pass 2 (no in-place store in pass 1) is
+    // 2 % faster on config 5; GSOT_EVAL_Q_RECOMPUTE=0 keeps the in-place form
+    const char* ev = std::getenv("GSOT_EVAL_Q_RECOMPUTE");
+    return ev ? std::atoi(ev) : 1;
+  }();
+  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, qrows, qrec, next_task, ntasks, ntasks_dev,
              &sc->zero_rows, &sc->read_qrows};
   const size_t smem = eval_smem_bytes(seg, qrows);
   if ((int)smem > g_eval_smem_attr[variant]) eval_blocks_per_sm(smem, variant);
