@@ -124,7 +124,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one, staging, d_bad, cmin, amax, snap_rows};
+                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ex_ready) gsot::exact_ws_free(ex);
@@ -222,6 +222,10 @@ void alloc_buffers(gsot_ctx* c) {
   c->cmin = dalloc<float>(static_cast<size_t>(L) * n, t);
   c->snap_rows = dalloc<unsigned long long>(64, t);
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_rows, 0, sizeof(unsigned long long) * 64, c->stream));
+  if (!std::getenv("GSOT_SNAP_SCATTERED")) {  // (GSOT_SNAP_SCATTERED=1: the one-kernel lazy form)
+    c->snap_list = dalloc<uint32_t>(static_cast<size_t>(L) * n, t);
+    c->snap_cnt = dalloc<unsigned int>(L, t);
+  }
   c->amax = dalloc<double>(L, t);
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dsync = dalloc<gsot::DevSync>(1, t);
@@ -613,9 +617,22 @@ EvalOut eval_device(gsot_ctx* c, const double* d_x, int mode, double* d_grad,
 void enqueue_snapshot(gsot_ctx* c, const double* d_x, bool lazy) {  // take_snapshot (screening.hpp:24-50)
   const DevProblem P = c->problem();
   const double Ln = static_cast<double>(c->L) * c->n;
-  if (lazy) c->launch(K_MISC, 8.0 * c->m, [&] { launch_group_amax(P, d_x, c->amax, c->stream); });
-  c->launch(K_SNAPSHOT, lazy ? -2.0 : 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n),
-            [&] { launch_snapshot(P, d_x, c->zs, c->ks, c->os, lazy, c->snap_rows, c->stream); });
+  unsigned int* list_len = c->snap_cnt;
+  // (instances of short groups only keep the one-kernel form: nothing to list)
+  const bool listed = lazy && c->snap_list != nullptr &&
+                      *std::max_element(c->sizes.begin(), c->sizes.end()) >= gsot::kSnapListMinRows;
+  if (lazy)
+    c->launch(K_MISC, 8.0 * c->m, [&] {
+      launch_group_amax(P, d_x, c->amax, c->stream, listed ? list_len : nullptr);
+    });
+  c->launch(K_SNAPSHOT, lazy ? -2.0 : 8.0 * c->m * c->n + 24.0 * Ln + 8.0 * (c->m + c->n), [&] {
+    if (listed) ++c->launches;  // two kernels
+    if (listed)
+      launch_snapshot_lazy2(P, d_x, c->zs, c->ks, c->os, c->snap_list, list_len, c->snap_rows,
+                            c->stream);
+    else
+      launch_snapshot(P, d_x, c->zs, c->ks, c->os, lazy, c->snap_rows, c->stream);
+  });
   c->snap_lazy = lazy;
   if (d_x != c->snap_x)
     GSOT_CUDA_CHECK(cudaMemcpyAsync(c->snap_x, d_x, sizeof(double) * (c->m + c->n),

@@ -122,6 +122,8 @@ struct gsot_ctx {
   double* amax = nullptr;
   bool snap_lazy = false;  // the current snapshot skipped provably-zero blocks
   unsigned long long* snap_rows = nullptr;  // 64 slots: cost rows read by lazy snapshots
+  uint32_t* snap_list = nullptr;            // lazy snapshots: per group, the columns of its blocks that are not provably zero
+  unsigned int* snap_cnt = nullptr;         // L list lengths
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;

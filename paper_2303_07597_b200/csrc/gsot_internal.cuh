@@ -225,7 +225,16 @@ void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaSt
 // Provably-zero blocks: the per-block minimum cost (once per upload) and the
 // per-group maximum of alpha (per evaluation, programmatic launch).
 void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s);
-void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s);
+// zero_me: optional L counters the kernel also clears (the lazy snapshot's list lengths)
+void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s,
+                       unsigned int* zero_me = nullptr);
+constexpr int kSnapListMinRows = 64;  // shorter groups are walked by the marking kernel itself
+// lazy snapshot through per-group lists of the blocks that are not provably
+// zero (list: L * n column indices; count: L lengths, cleared by the preceding
+// launch_group_amax)
+void launch_snapshot_lazy2(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
+                           uint32_t* list, unsigned int* count, unsigned long long* rows_read,
+                           cudaStream_t s);
 void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s);
 // Per-chunk group masks cmask[c][l / 32] bit l % 32: (l, c) non-empty.
 void launch_fill_cmask(uint32_t* cmask, int32_t L, int32_t nw, cudaStream_t s);

@@ -95,6 +95,64 @@ void launch_relayout(const DevProblem& P, const double* src, int64_t j0, int64_t
 // value, as the reference's is: every decision and counter is unchanged.
 // API snapshots are taken in full (gsot_snapshot_norms returns the reference's
 // values; a lazy snapshot is retaken in full on request).
+// One block of take_snapshot: three sequential sums over the block's rows, U
+// cost loads in flight per thread. kPipe: the next batch is loaded while the
+// current one is summed (the walk of a tall column is a chain of memory round
+// trips: deeper batches, fewer trips).
+template <int U = 8, bool kPipe = false>
+__device__ __forceinline__ void snapshot_block(const DevProblem& P, const double* __restrict__ x,
+                                               int o0, int g, int l, int64_t j,
+                                               double* __restrict__ zs, double* __restrict__ ks,
+                                               double* __restrict__ os) {
+  const double bj = x[P.m + j];
+  const double* __restrict__ al = x + o0;
+  const double* __restrict__ cp = block_ptr(P, o0, g, j);
+  double az = 0.0, ak = 0.0, ao = 0.0;
+#define GSOT_SNAP_STEP(ALPHA, CVAL)                 \
+  {                                                 \
+    const double f = residual((ALPHA), bj, (CVAL)); \
+    const double sq = dmul(f, f);                   \
+    ak = dadd(ak, sq);                              \
+    az = dadd(az, f > 0.0 ? sq : 0.0);              \
+    ao = dadd(ao, f < 0.0 ? sq : 0.0);              \
+  }
+  int r = 0;
+  if constexpr (kPipe) {
+    double c[U], cn[U];
+    if (g >= U) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) c[k] = __ldcs(cp + kRowStride * k);
+    }
+    for (; r + U <= g; r += U) {
+      const bool more = r + 2 * U <= g;
+      if (more) {
+#pragma unroll
+        for (int k = 0; k < U; ++k) cn[k] = __ldcs(cp + kRowStride * (r + U + k));
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) GSOT_SNAP_STEP(__ldg(al + r + k), c[k]);
+      if (more) {
+#pragma unroll
+        for (int k = 0; k < U; ++k) c[k] = cn[k];
+      }
+    }
+  } else {
+    for (; r + U <= g; r += U) {
+      double c[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) c[k] = __ldcs(cp + kRowStride * (r + k));
+#pragma unroll
+      for (int k = 0; k < U; ++k) GSOT_SNAP_STEP(__ldg(al + r + k), c[k]);
+    }
+  }
+  for (; r < g; ++r) GSOT_SNAP_STEP(__ldg(al + r), __ldcs(cp + kRowStride * r));
+#undef GSOT_SNAP_STEP
+  const int64_t idx = (int64_t)l * P.n + j;
+  zs[idx] = sqrt(az);
+  ks[idx] = sqrt(ak);
+  os[idx] = sqrt(ao);
+}
+
 __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __restrict__ x,
                                                   double* __restrict__ zs,
                                                   double* __restrict__ ks,
@@ -105,9 +163,8 @@ __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
   const bool in = j < P.n;
-  const double bj = in ? x[P.m + j] : 0.0;
   if (lazy) {
-    const bool zero = !in || dadd(P.amax[l], bj) <= (double)P.cmin[(int64_t)l * P.n + j];
+    const bool zero = !in || dadd(P.amax[l], x[P.m + j]) <= (double)P.cmin[(int64_t)l * P.n + j];
     const unsigned read = __ballot_sync(0xffffffffu, !zero);  // bytes accounting (slots)
     if ((threadIdx.x & 31) == 0 && read)
       atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(read) * g);
@@ -122,31 +179,88 @@ __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __
     }
   }
   if (!in) return;
-  const double* __restrict__ al = x + o0;
-  const double* __restrict__ cp = block_ptr(P, o0, g, j);
-  double az = 0.0, ak = 0.0, ao = 0.0;
-#define GSOT_SNAP_STEP(ALPHA, CVAL)                 \
-  {                                                 \
-    const double f = residual((ALPHA), bj, (CVAL)); \
-    const double sq = dmul(f, f);                   \
-    ak = dadd(ak, sq);                              \
-    az = dadd(az, f > 0.0 ? sq : 0.0);              \
-    ao = dadd(ao, f < 0.0 ? sq : 0.0);              \
-  }
-  int r = 0;
-  for (; r + 8 <= g; r += 8) {
-    double c[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = __ldcs(cp + kRowStride * (r + k));
-#pragma unroll
-    for (int k = 0; k < 8; ++k) GSOT_SNAP_STEP(__ldg(al + r + k), c[k]);
-  }
-  for (; r < g; ++r) GSOT_SNAP_STEP(__ldg(al + r), __ldcs(cp + kRowStride * r));
-#undef GSOT_SNAP_STEP
+  snapshot_block(P, x, o0, g, l, j, zs, ks, os);
+}
+
+// The lazy snapshot in two kernels (contexts with a block list).
+// k_snapshot_mark tests every block: a provably-zero one gets z~ = k~ = o~ = 0,
+// the others (about 1 % of them during a solve) are appended to their group's
+// list (one atomic per warp; groups of fewer than kSnapListMinRows rows are
+// walked on the spot: config 4's many short groups measured slower listed). k_snapshot_walk then takes one block per thread
+// from the lists, group by group, so every warp of the sequential walks is
+// full and walks columns of one height (in k_snapshot's lazy form a live lane
+// walks its column while the other lanes of its warp have exited). Each
+// block is still one thread's sequential sum: the same bits.
+__global__ void __launch_bounds__(256) k_snapshot_mark(DevProblem P, const double* __restrict__ x,
+                                                       double* __restrict__ zs,
+                                                       double* __restrict__ ks,
+                                                       double* __restrict__ os,
+                                                       uint32_t* __restrict__ list,
+                                                       unsigned int* __restrict__ count,
+                                                       unsigned long long* __restrict__ rows_read) {
+  pdl_wait();  // after the group maxima of x (k_group_amax, which zeroed count[])
+  pdl_trigger();
+  const int l = blockIdx.y;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool in = j < P.n;
   const int64_t idx = (int64_t)l * P.n + j;
-  zs[idx] = sqrt(az);
-  ks[idx] = sqrt(ak);
-  os[idx] = sqrt(ao);
+  const bool zero = !in || dadd(P.amax[l], x[P.m + j]) <= (double)P.cmin[idx];
+  const unsigned livem = __ballot_sync(0xffffffffu, !zero);
+  if (zero && in) {
+    zs[idx] = 0.0;
+    ks[idx] = 0.0;
+    os[idx] = 0.0;
+  }
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  if (g < kSnapListMinRows) {  // a short column: walked here (listing it costs more than it saves)
+    if (livem && (threadIdx.x & 31) == 0)
+      atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(livem) * (unsigned)g);
+    if (!zero) snapshot_block(P, x, o0, g, l, j, zs, ks, os);
+    return;
+  }
+  if (livem) {
+    const int lane = threadIdx.x & 31;
+    unsigned int base = 0;
+    if (lane == 0) {
+      base = atomicAdd(count + l, (unsigned int)__popc(livem));
+      atomicAdd(rows_read + (blockIdx.x & 63),
+                (unsigned long long)__popc(livem) * (unsigned)g);
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (!zero) list[(int64_t)l * P.n + base + __popc(livem & ((1u << lane) - 1u))] = (uint32_t)j;
+  }
+}
+
+constexpr int kSnapWalkX = 8;  // CTAs per group
+__global__ void __launch_bounds__(128) k_snapshot_walk(DevProblem P, const double* __restrict__ x,
+                                                       double* __restrict__ zs,
+                                                       double* __restrict__ ks,
+                                                       double* __restrict__ os,
+                                                       const uint32_t* __restrict__ list,
+                                                       const unsigned int* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
+  const int l = blockIdx.y;
+  const unsigned int n_live = count[l];
+  if (blockIdx.x * blockDim.x >= n_live) return;
+  const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  for (unsigned int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_live;
+       t += gridDim.x * blockDim.x) {
+    const int64_t j = (int64_t)list[(int64_t)l * P.n + t];
+    if (g >= 128)
+      snapshot_block<32, true>(P, x, o0, g, l, j, zs, ks, os);
+    else
+      snapshot_block<8, false>(P, x, o0, g, l, j, zs, ks, os);
+  }
+}
+
+void launch_snapshot_lazy2(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
+                           uint32_t* list, unsigned int* count, unsigned long long* rows_read,
+                           cudaStream_t s) {
+  dim3 grid((unsigned)((P.n + 255) / 256), (unsigned)P.L);
+  launch_pdl(k_snapshot_mark, grid, dim3(256), 0, s, P, x, zs, ks, os, list, count, rows_read);
+  launch_pdl(k_snapshot_walk, dim3(kSnapWalkX, (unsigned)P.L), dim3(128), 0, s, P, x, zs, ks, os,
+             (const uint32_t*)list, (const unsigned int*)count);
 }
 
 void launch_snapshot(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
@@ -738,15 +852,25 @@ void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s) {
 // amax[l] = max over the group's alpha (a NaN propagates: no block of the
 // group is then provably zero). One warp per group.
 __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* __restrict__ x,
-                                                    double* __restrict__ amax) {
+                                                    double* __restrict__ amax,
+                                                    unsigned int* __restrict__ zero_me) {
   pdl_wait();
   pdl_trigger();
+
   const int lane = threadIdx.x & 31;
   const int l = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (l >= P.L) return;
   const int o0 = P.off[l], o1 = P.off[l + 1];
   double v = -__longlong_as_double(0x7ff0000000000000ll);
-  for (int i = o0 + lane; i < o1; i += 32) {
+  int i = o0 + lane;
+  for (; i + 7 * 32 < o1; i += 8 * 32) {  // eight loads in flight (tall groups)
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = x[i + 32 * k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v = (a[k] > v || a[k] != a[k]) ? a[k] : v;
+  }
+  for (; i < o1; i += 32) {
     const double a = x[i];
     v = (a > v || a != a) ? a : v;
   }
@@ -755,11 +879,15 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
     const double w = __shfl_xor_sync(0xffffffffu, v, o);
     v = (w > v || w != w) ? w : v;
   }
-  if (lane == 0) amax[l] = v;
+  if (lane == 0) {
+    amax[l] = v;
+    if (zero_me) zero_me[l] = 0u;  // the lazy snapshot's list length of the group
+  }
 }
 
-void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s) {
-  launch_pdl(k_group_amax, dim3((P.L + 7) / 8), dim3(256), 0, s, P, x, amax);
+void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s,
+                       unsigned int* zero_me) {
+  launch_pdl(k_group_amax, dim3((P.L + 7) / 8), dim3(256), 0, s, P, x, amax, zero_me);
 }
 
 // ---------------------------------------------------------------- fused eval
