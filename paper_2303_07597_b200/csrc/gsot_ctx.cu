@@ -124,7 +124,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt};
+                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt, dpos_fast, cmn, zmm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ex_ready) gsot::exact_ws_free(ex);
@@ -227,6 +227,9 @@ void alloc_buffers(gsot_ctx* c) {
     c->snap_cnt = dalloc<unsigned int>(L, t);
   }
   c->amax = dalloc<double>(L, t);
+  c->dpos_fast = dalloc<double>(L, t);
+  c->cmn = dalloc<float>(static_cast<size_t>(L) * nw, t);
+  c->zmm = dalloc<double2>(static_cast<size_t>(L) * nw, t);
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
   c->dsync = dalloc<gsot::DevSync>(1, t);
   GSOT_CUDA_CHECK(cudaHostAlloc(&c->h_sync, sizeof(gsot::DevSync) + 128, cudaHostAllocMapped));
@@ -541,7 +544,12 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   if (mode != GSOT_EVAL_SCREENED || exact) c->reset_scalars();  // screened: zeroed by k_publish
   // per-group max alpha for the provably-zero block test (k_block_min): read
   // by the screen and the evaluation
-  c->launch(K_MISC, 8.0 * c->m, [&] { launch_group_amax(P, d_x, c->amax, c->stream); });
+  const bool fused = mode == GSOT_EVAL_SCREENED && dbeta_ready && !exact;
+  const bool pre = fused && screen_uses_summaries(P, c->num_sms);  // delta norms once per group
+  c->launch(K_MISC, 8.0 * c->m, [&] {
+    launch_group_amax(P, d_x, c->amax, c->stream, nullptr, pre ? c->snap_x : nullptr,
+                      pre ? c->dpos_fast : nullptr);
+  });
   const uint32_t* words = c->dense_words;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
@@ -549,7 +557,6 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
     // kernel wrote dbeta); every other screened evaluation -- exact mode and
     // the API's gsot_eval -- takes the reference-order norms of k_delta, so
     // its decisions and counters are the reference's bit for bit.
-    const bool fused = dbeta_ready && !exact;
     if (!fused)
       c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
         launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, nullptr,
@@ -559,7 +566,8 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
                     ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
                     c->cmask, fused ? d_x : nullptr, fused ? c->snap_x : nullptr,
-                    fused ? 1 : 0, d_x, c->num_sms, c->stream);
+                    fused ? 1 : 0, d_x, pre ? c->dpos_fast : nullptr, c->zmm, c->num_sms,
+                    c->stream);
     });
     words = c->words;
   }
@@ -633,6 +641,9 @@ void enqueue_snapshot(gsot_ctx* c, const double* d_x, bool lazy) {  // take_snap
     else
       launch_snapshot(P, d_x, c->zs, c->ks, c->os, lazy, c->snap_rows, c->stream);
   });
+  // per-chunk extremes of z~ for the screen's whole-chunk decisions
+  if (screen_uses_summaries(P, c->num_sms))
+    c->launch(K_MISC, 8.0 * Ln, [&] { launch_chunk_minmax(P, c->zs, c->zmm, c->stream); });
   c->snap_lazy = lazy;
   if (d_x != c->snap_x)
     GSOT_CUDA_CHECK(cudaMemcpyAsync(c->snap_x, d_x, sizeof(double) * (c->m + c->n),

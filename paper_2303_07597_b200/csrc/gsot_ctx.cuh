@@ -124,6 +124,9 @@ struct gsot_ctx {
   unsigned long long* snap_rows = nullptr;  // 64 slots: cost rows read by lazy snapshots
   uint32_t* snap_list = nullptr;            // lazy snapshots: per group, the columns of its blocks that are not provably zero
   unsigned int* snap_cnt = nullptr;         // L list lengths
+  double* dpos_fast = nullptr;              // L: fast-mode screen's group delta norms (k_group_amax)
+  float* cmn = nullptr;                     // L * nw: per-chunk minimum of cmin
+  double2* zmm = nullptr;                   // L * nw: per-chunk (min, max) of the snapshot's z~
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;
@@ -189,6 +192,7 @@ struct gsot_ctx {
     P.tl = tl;
     P.cmin = cmin;
     P.amax = amax;
+    P.cmn = cmn;
     return P;
   }
 

@@ -77,6 +77,7 @@ struct DevProblem {
   // (float, rounded down), amax[l] = max_{i in l} alpha_i (NaN if any is NaN)
   const float* cmin;
   const double* amax;
+  const float* cmn;  // per (group, chunk): min of cmin over the chunk's valid columns
 };
 
 // Device scalars written by the reduction kernels and read back with one
@@ -179,7 +180,12 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
-                   const double* xe, int num_sms, cudaStream_t s);
+                   const double* xe, const double* dpre, const double2* zmm, int num_sms,
+                   cudaStream_t s);
+bool screen_uses_summaries(const DevProblem& P, int num_sms);
+// zmm[l * nw + c] = (min, max) of z~ over the chunk's columns: after every snapshot
+void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm, cudaStream_t s);
+// dpre: optional, the fast-mode group delta norms precomputed by launch_group_amax
 // xe: the evaluation state (the provably-zero test; P.amax must hold its
 // group maxima). Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
 int eval_buf_rows(int gmax);
@@ -226,8 +232,10 @@ void launch_fill_words(uint32_t* words, int32_t L, int32_t nw, int64_t n, cudaSt
 // per-group maximum of alpha (per evaluation, programmatic launch).
 void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s);
 // zero_me: optional L counters the kernel also clears (the lazy snapshot's list lengths)
+// xs, dfast: optional; dfast[l] = |[x_l - xs_l]+| (the fast-mode screen's group delta norm)
 void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s,
-                       unsigned int* zero_me = nullptr);
+                       unsigned int* zero_me = nullptr, const double* xs = nullptr,
+                       double* dfast = nullptr);
 constexpr int kSnapListMinRows = 64;  // shorter groups are walked by the marking kernel itself
 // lazy snapshot through per-group lists of the blocks that are not provably
 // zero (list: L * n column indices; count: L lengths, cleared by the preceding

@@ -559,17 +559,16 @@ __global__ void __launch_bounds__(256) k_screen_rows(DevProblem P, const double*
 // z_bar = (z~ + |[dalpha_l]+|) + sqrt(g_l) * [dbeta_j]+ (+ offset) and is
 // skipped iff z_bar <= tau.
 // CTA (kx, ky) covers groups 8 ky .. 8 ky + 7 (one warp each) and the 32
-// chunks of chunk-mask word kx (one lane each), so each lane builds ONE
-// survivor word from its chunk's 32 columns sequentially -- no per-chunk
-// ballots or lane-0 bookkeeping. Bounds and dbeta are transposed through
-// shared memory 16 columns at a time (coalesced global loads, padded rows:
-// no bank conflicts). Per warp: the survivor words, the group's chunk-mask
-// word (one ballot), the group's delta norm (fast mode: fused, fixed tree);
-// per CTA: one atomic reserving the non-empty chunks' work-list slots, the
-// per-chunk group masks (one atomic per chunk), and the GradStats::PerCall
-// counters into one of 64 slots (integers: order-free).
+// chunks of chunk-mask word kx (one lane each). Whole chunks are decided from
+// per-chunk summaries (the extremes of z~, dbeta, beta and cmin; rounding is
+// monotone, so the decisions are the reference's); only mixed chunks are walked
+// column by column (lane = column, one ballot per chunk). Per warp: the
+// survivor words, the group's chunk-mask word (one ballot); per CTA: one atomic
+// reserving the non-empty chunks' work-list slots, the per-chunk group masks
+// (one atomic per chunk), and the GradStats::PerCall counters into one of 64
+// slots (integers: order-free). The group's delta norm comes from
+// k_group_amax (fast mode: fixed tree) or k_delta (reference order).
 constexpr int kScrWarps = 8;   // groups per CTA
-constexpr int kScrHalf = 16;   // columns per transposition round
 
 __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __restrict__ zs,
                                                 const uint32_t* __restrict__ aw,
@@ -582,9 +581,10 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 uint32_t* __restrict__ cmask,
                                                 const double* __restrict__ x,
                                                 const double* __restrict__ xs, int dbeta_ready,
-                                                const double* __restrict__ xe) {
-  __shared__ double zt[kScrWarps][32][kScrHalf + 1];  // [group][chunk][column]
-  __shared__ double dbt[32][kScrHalf + 1];            // [chunk][column]
+                                                const double* __restrict__ xe,
+                                                const double* __restrict__ dpre,
+                                                const double2* __restrict__ zmm) {
+  __shared__ double dbx[32][3];  // per chunk: min / max dbeta, max beta
   __shared__ unsigned long long cnt[kScrWarps][6];
   __shared__ int wn[kScrWarps];                        // non-empty chunks per warp
   __shared__ uint32_t gbits[kScrWarps][32];            // for the per-chunk group masks
@@ -603,7 +603,9 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   const int g = lvalid ? P.off[l + 1] - o0 : 0;
   const uint32_t am = (lvalid && cvalid && aw != nullptr) ? aw[(int64_t)l * P.nw + c] : 0u;
   double dp = 0.0;
-  if (x) {
+  if (x && dpre) {
+    dp = lvalid ? dpre[l] : 0.0;  // fast mode: the same norm, computed once per group (k_group_amax)
+  } else if (x) {
     // fused delta (fast mode): |[alpha_l - alpha~_l]+| over the group's rows,
     // lane-strided chains, then a fixed xor tree
     double acc = 0.0;
@@ -618,71 +620,121 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
     dp = dpos[l];  // k_delta's reference-order norm (exact mode)
   }
   const double sg = lvalid ? P.sqrt_g[l] : 0.0;
+  // Per-chunk summaries first (lane = chunk): with the chunk's extreme z~
+  // (k_chunk_minmax, once per snapshot) and extreme dbeta, monotone rounding
+  // gives the bound of every column between zbar(zmin, dbmin) and zbar(zmax,
+  // dbmax): a chunk whose largest bound is <= tau is skipped whole, one whose
+  // smallest is > tau kept whole -- the reference's decisions, without reading
+  // the 32 z~. Only mixed chunks are walked (lane = column, one ballot each).
+  // dbeta / beta extremes of the CTA's 32 chunks: warp w takes chunks 4w..4w+3.
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int ci = 4 * warp + q;
+    const int64_t j = (int64_t)(c0 + ci) * 32 + lane;
+    const bool ok = c0 + ci < P.nw && j < P.n;
+    double db = 0.0, be = 0.0;
+    if (ok) {
+      db = db_inline ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j];
+      be = xe[P.m + j];
+    }
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    // a NaN makes the chunk mixed (extremes +-inf)
+    double dmx = ok ? (db != db ? inf : db) : -inf, dmn = ok ? (db != db ? -inf : db) : inf;
+    double bmx = ok ? (be != be ? inf : be) : -inf;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+      bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+    }
+    if (lane == 0) {
+      dbx[ci][0] = dmn;
+      dbx[ci][1] = dmx;
+      dbx[ci][2] = bmx;
+    }
+  }
+  __syncthreads();
+  auto zbar_of = [&](double z, double db) {
+    return dadd(dadd(dadd(z, dp), dmul(sg, relu(db))), ub_offset);
+  };
   uint32_t surv = 0u;  // evaluated columns with z_bar > tau
-#pragma unroll 1
-  for (int h = 0; h < 32 / kScrHalf; ++h) {
-    const int cb = h * kScrHalf;  // first column of the round within each chunk
-    __syncthreads();  // the previous round's buffers are consumed
-    // dbeta of the 32 chunks' columns cb..cb+15 (shared by the groups)
-    for (int q = threadIdx.x; q < 32 * kScrHalf; q += blockDim.x) {
-      const int ci = q / kScrHalf, k = q % kScrHalf;
-      const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
-      double v = 0.0;
-      if (c0 + ci < P.nw && j < P.n) v = db_inline ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j];
-      dbt[ci][k] = v;
-    }
-    // this warp's group: z~ of the 32 chunks' columns cb..cb+15, two chunks
-    // per coalesced load (half-warp = 16 consecutive columns), all 16 loads
-    // in flight together
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int ci = 2 * q + (lane >> 4), k = lane & 15;
-      const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
-      zt[warp][ci][k] = (lvalid && c0 + ci < P.nw && j < P.n) ? zs[(int64_t)l * P.n + j] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kScrHalf; ++k) {
-      const double zbar =
-          dadd(dadd(dadd(zt[warp][lane][k], dp), dmul(sg, relu(dbt[lane][k]))), ub_offset);
-      surv |= (zbar <= P.tau ? 0u : 1u) << (cb + k);
-    }
-  }
-  // provably-zero blocks among this lane's chunk's columns:
-  // max alpha + beta_j <= cmin, the same transposed rounds (cmin in zt's
-  // storage as floats, beta in dbt's)
-  uint32_t pz = 0u;  // columns possibly nonzero
   {
-    float(*ct)[32][kScrHalf + 1] = reinterpret_cast<float(*)[32][kScrHalf + 1]>(zt);
-    const double amx = lvalid ? P.amax[l] : 0.0;
-#pragma unroll 1
-    for (int h = 0; h < 32 / kScrHalf; ++h) {
-      const int cb = h * kScrHalf;
-      __syncthreads();
-      for (int q = threadIdx.x; q < 32 * kScrHalf; q += blockDim.x) {
-        const int ci = q / kScrHalf, k = q % kScrHalf;
-        const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
-        dbt[ci][k] = (c0 + ci < P.nw && j < P.n) ? xe[P.m + j] : 0.0;
+    double2 zm = make_double2(0.0, 0.0);
+    if (lvalid && cvalid) zm = zmm[(int64_t)l * P.nw + c];
+    const bool all_skip = zbar_of(zm.y, dbx[lane][1]) <= P.tau;
+    const bool all_keep = !(zbar_of(zm.x, dbx[lane][0]) <= P.tau);
+    surv = all_skip ? 0u : 0xffffffffu;
+    uint32_t need = __ballot_sync(0xffffffffu, lvalid && cvalid && !all_skip && !all_keep);
+    const double* __restrict__ zrow = zs + (int64_t)(lvalid ? l : 0) * P.n;
+    while (need) {  // mixed chunks, four at a time (independent loads)
+      int cis[4];
+      double z[4], db[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cis[u] = need ? __ffs(need) - 1 : -1;
+        need &= need - 1u;
+        z[u] = 0.0;
+        db[u] = 0.0;
+        if (cis[u] >= 0) {
+          const int64_t j = (int64_t)(c0 + cis[u]) * 32 + lane;
+          if (j < P.n) {
+            z[u] = zrow[j];
+            db[u] = db_inline ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j];
+          }
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int ci = 2 * q + (lane >> 4), k = lane & 15;
-        const int64_t j = (int64_t)(c0 + ci) * 32 + cb + k;
-        ct[warp][ci][k] = (lvalid && c0 + ci < P.nw && j < P.n) ? P.cmin[(int64_t)l * P.n + j] : 0.0f;
+      for (int u = 0; u < 4; ++u) {
+        if (cis[u] < 0) break;  // warp-uniform
+        const uint32_t bs = __ballot_sync(0xffffffffu, !(zbar_of(z[u], db[u]) <= P.tau));
+        if (lane == cis[u]) surv = bs;
       }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kScrHalf; ++k)
-        pz |= (dadd(amx, dbt[lane][k]) <= (double)ct[warp][lane][k] ? 0u : 1u) << (cb + k);
     }
   }
-  // masks of this lane's chunk
+  // masks of this lane's chunk (the reference's decisions)
   const int64_t j0 = (int64_t)c * 32;
   const uint32_t vmask = (!lvalid || !cvalid) ? 0u
                          : (P.n - j0 >= 32 ? 0xffffffffu : ((1u << (P.n - j0)) - 1u));
   const uint32_t wa = am & vmask;
   const uint32_t we = vmask & ~wa;
   const uint32_t wd = (surv & we) | wa;  // the reference's decisions (counters)
+  // provably-zero blocks among the chunk's computed columns:
+  // max alpha + beta_j <= cmin. A chunk with nothing to compute needs no test;
+  // one whose largest beta passes against its smallest cmin (k_block_min's
+  // per-chunk minimum) is zero whole; the others are walked.
+  uint32_t pz = 0u;  // columns possibly nonzero
+  {
+    const double amx = lvalid ? P.amax[l] : 0.0;
+    bool detail = false;
+    if (wd != 0u) detail = !(dadd(amx, dbx[lane][2]) <= (double)P.cmn[(int64_t)l * P.nw + c]);
+    uint32_t need = __ballot_sync(0xffffffffu, detail);
+    const float* __restrict__ crow = P.cmin + (int64_t)(lvalid ? l : 0) * P.n;
+    while (need) {
+      int cis[4];
+      double be[4];
+      float cm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cis[u] = need ? __ffs(need) - 1 : -1;
+        need &= need - 1u;
+        be[u] = 0.0;
+        cm[u] = 0.0f;
+        if (cis[u] >= 0) {
+          const int64_t j = (int64_t)(c0 + cis[u]) * 32 + lane;
+          if (j < P.n) {
+            be[u] = xe[P.m + j];
+            cm[u] = crow[j];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (cis[u] < 0) break;
+        const uint32_t bp = __ballot_sync(0xffffffffu, !(dadd(amx, be[u]) <= (double)cm[u]));
+        if (lane == cis[u]) pz = bp;
+      }
+    }
+  }
   const uint32_t ws = wd & pz;           // what the evaluation reads
   if (lvalid && cvalid) words[(int64_t)l * P.nw + c] = ws;
   const unsigned ne = __ballot_sync(0xffffffffu, ws != 0u);
@@ -743,20 +795,29 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   TL_EXIT(P.tl, TL_SCREEN);
 }
 
+// The chunk-summary screen (k_screen) runs when its grid fills the machine;
+// smaller instances take k_screen_rows, which needs neither the per-chunk
+// extremes nor the precomputed group delta norms.
+bool screen_uses_summaries(const DevProblem& P, int num_sms) {
+  const int64_t gx = (P.nw + 31) / 32, gy = (P.L + kScrWarps - 1) / kScrWarps;
+  return gx * gy >= 4ll * num_sms;
+}
+
 void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, const double* dpos,
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
-                   const double* xe, int num_sms, cudaStream_t s) {
+                   const double* xe, const double* dpre, const double2* zmm, int num_sms,
+                   cudaStream_t s) {
   const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)((P.L + kScrWarps - 1) / kScrWarps));
-  if ((int64_t)grid.x * grid.y < 4ll * num_sms) {  // small: one CTA per (group, 2048 columns)
+  if (!screen_uses_summaries(P, num_sms)) {  // small: one CTA per (group, 2048 columns)
     const dim3 g2((unsigned)((P.nw + 63) / 64), (unsigned)P.L);
     launch_pdl(k_screen_rows, g2, dim3(256), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words, tasks,
                sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready);
     return;
   }
   launch_pdl(k_screen, grid, dim3(32 * kScrWarps), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words,
-             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready, xe);
+             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready, xe, dpre, zmm);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
@@ -841,7 +902,45 @@ __global__ void __launch_bounds__(256) k_block_min(DevProblem P, float* __restri
 #pragma unroll 8
   for (int r = 0; r < g; ++r) v = fmin(v, tile[kRowStride * r]);
   const int64_t j = (int64_t)c * 32 + lane;
-  if (j < P.n) cmin[(int64_t)l * P.n + j] = __double2float_rd(v);
+  const float f = __double2float_rd(v);
+  if (j < P.n) cmin[(int64_t)l * P.n + j] = f;
+  // the chunk's smallest (valid columns): the screen's whole-chunk test
+  float fm = j < P.n ? f : __int_as_float(0x7f800000);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) fm = fminf(fm, __shfl_xor_sync(0xffffffffu, fm, o));
+  if (lane == 0) const_cast<float*>(P.cmn)[t] = fm;
+}
+
+// Per (group, chunk): the smallest and largest z~ of the chunk's valid columns
+// (a NaN makes them -inf / +inf: the screen then walks the chunk). Once per
+// snapshot, for the screen's whole-chunk decisions.
+__global__ void __launch_bounds__(256) k_chunk_minmax(DevProblem P, const double* __restrict__ zs,
+                                                      double2* __restrict__ zmm) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // l * nw + c
+  if (t >= (int64_t)P.L * P.nw) return;
+  const int l = (int)(t / P.nw), c = (int)(t % P.nw);
+  const int64_t j = (int64_t)c * 32 + lane;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double mn = inf, mx = -inf;
+  if (j < P.n) {
+    const double z = zs[(int64_t)l * P.n + j];
+    mn = z != z ? -inf : z;
+    mx = z != z ? inf : z;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) zmm[t] = make_double2(mn, mx);
+}
+
+void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm, cudaStream_t s) {
+  const int64_t tiles = (int64_t)P.L * P.nw;
+  launch_pdl(k_chunk_minmax, dim3((unsigned)((tiles + 7) / 8)), dim3(256), 0, s, P, zs, zmm);
 }
 
 void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s) {
@@ -853,7 +952,9 @@ void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s) {
 // group is then provably zero). One warp per group.
 __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* __restrict__ x,
                                                     double* __restrict__ amax,
-                                                    unsigned int* __restrict__ zero_me) {
+                                                    unsigned int* __restrict__ zero_me,
+                                                    const double* __restrict__ xs,
+                                                    double* __restrict__ dfast) {
   pdl_wait();
   pdl_trigger();
 
@@ -862,17 +963,37 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
   if (l >= P.L) return;
   const int o0 = P.off[l], o1 = P.off[l + 1];
   double v = -__longlong_as_double(0x7ff0000000000000ll);
+  // fast solves: the group's |[alpha_l - alpha~_l]+| for the screen (xs: the
+  // snapshot state), lane-strided chains in row order, then a fixed xor tree
+  // -- once per group here instead of once per screen CTA
+  double acc = 0.0;
   int i = o0 + lane;
   for (; i + 7 * 32 < o1; i += 8 * 32) {  // eight loads in flight (tall groups)
-    double a[8];
+    double a[8], b[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = x[i + 32 * k];
+    for (int k = 0; k < 8; ++k) {
+      a[k] = x[i + 32 * k];
+      b[k] = xs ? xs[i + 32 * k] : 0.0;
+    }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v = (a[k] > v || a[k] != a[k]) ? a[k] : v;
+    for (int k = 0; k < 8; ++k) {
+      v = (a[k] > v || a[k] != a[k]) ? a[k] : v;
+      const double d = dsub(a[k], b[k]);
+      if (xs && d > 0.0) acc = dadd(acc, dmul(d, d));
+    }
   }
   for (; i < o1; i += 32) {
     const double a = x[i];
     v = (a > v || a != a) ? a : v;
+    if (xs) {
+      const double d = dsub(a, xs[i]);
+      if (d > 0.0) acc = dadd(acc, dmul(d, d));
+    }
+  }
+  if (xs) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) dfast[l] = sqrt(acc);
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -886,8 +1007,8 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
 }
 
 void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s,
-                       unsigned int* zero_me) {
-  launch_pdl(k_group_amax, dim3((P.L + 7) / 8), dim3(256), 0, s, P, x, amax, zero_me);
+                       unsigned int* zero_me, const double* xs, double* dfast) {
+  launch_pdl(k_group_amax, dim3((P.L + 7) / 8), dim3(256), 0, s, P, x, amax, zero_me, xs, dfast);
 }
 
 // ---------------------------------------------------------------- fused eval
