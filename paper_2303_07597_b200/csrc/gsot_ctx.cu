@@ -585,11 +585,12 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   c->launch(K_EVAL, mode == GSOT_EVAL_DENSE ? dense_bytes : -1.0, [&] {
     if (mode == GSOT_EVAL_SCREENED)
       launch_eval(P, d_x, c->tasks, -1, &c->sc->ntasks, words, c->rowpart, c->colpart, c->psi,
-                  c->eval_buf, c->eval_qrows, c->eval_variant, c->eval_grid, &c->sc->next_task, c->stream);
+                  c->eval_buf, c->eval_qrows, c->eval_variant, c->eval_grid, &c->sc->next_task,
+                  screen_uses_summaries(P, c->num_sms), c->stream);
     else
       launch_eval(P, d_x, c->dense_tasks, c->L * c->nw, nullptr, words, c->rowpart, c->colpart,
                   c->psi, c->eval_buf, c->eval_qrows, c->eval_variant, c->eval_grid, &c->sc->next_task,
-                  c->stream);
+                  false, c->stream);
   });
   c->launch(K_FINALIZE, 16.0 * (c->m + c->n), [&] {
     const bool scr = mode == GSOT_EVAL_SCREENED;

@@ -205,7 +205,9 @@ int eval_blocks_per_sm(size_t smem, int variant);
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
                  double* psi, int seg, int qrows, int variant, int grid, int* next_task,
-                 cudaStream_t s);
+                 bool pz_done, cudaStream_t s);
+// pz_done: the work list comes from the chunk-summary screen, which already
+// dropped the provably-zero columns from the survivor words
 // grad, psi columns, objective and slope (dvec may be null) in one kernel.
 void launch_finalize(const DevProblem& P, const double* x, const uint32_t* words,
                      const uint32_t* gmask, uint32_t* cmask, int clear_cmask,

@@ -1045,6 +1045,7 @@ struct EvalArgs {
   int seg;          // rows per shared-memory segment (<= kEvalMaxSeg)
   int qrows;        // quarter pipeline (k_eval_q): rows per quarter segment
   int qrec;         // quarter pipeline: resident quarters recompute [f]+ in pass 2 (no in-place store)
+  int pz_done;      // the screen already applied the provably-zero test: the words hold only possibly-nonzero columns
   int* next_task;   // global claim cursor (zeroed per evaluation)
   int ntasks;       // >= 0: list length; -1: read *ntasks_dev (screened)
   const int* ntasks_dev;
@@ -1132,7 +1133,8 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
         const int64_t j = 32ll * T.c + lane;
         const bool act = (w >> lane) & 1u;
         const bool maybe =
-            act && !(dadd(P.amax[T.l], A.x[P.m + j]) <= (double)P.cmin[(int64_t)T.l * P.n + j]);
+            act && (A.pz_done ||
+                    !(dadd(P.amax[T.l], A.x[P.m + j]) <= (double)P.cmin[(int64_t)T.l * P.n + j]));
         const uint32_t mb = __ballot_sync(0xffffffffu, maybe);
         T.qm = ((mb & 0xffu) ? 1u : 0u) | ((mb & 0xff00u) ? 2u : 0u) | ((mb & 0xff0000u) ? 4u : 0u) |
                ((mb & 0xff000000u) ? 8u : 0u);
@@ -1442,7 +1444,8 @@ __global__ void __launch_bounds__(eval_threads(4), 3) k_eval_q(const EvalArgs A)
         const int64_t j = 32ll * T.c + lane;
         const bool act = (w >> lane) & 1u;
         const bool maybe =
-            act && !(dadd(P.amax[T.l], A.x[P.m + j]) <= (double)P.cmin[(int64_t)T.l * P.n + j]);
+            act && (A.pz_done ||
+                    !(dadd(P.amax[T.l], A.x[P.m + j]) <= (double)P.cmin[(int64_t)T.l * P.n + j]));
         T.qm = quarter_mask(__ballot_sync(0xffffffffu, maybe));
         T.zero = T.qm == 0u;
       }
@@ -1837,7 +1840,7 @@ int eval_blocks_per_sm(size_t smem, int variant) {
 void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, int ntasks,
                  const int* ntasks_dev, const uint32_t* words, double* rowpart, double* colpart,
                  double* psi, int seg, int qrows, int variant, int grid, int* next_task,
-                 cudaStream_t s) {
+                 bool pz_done, cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0)
     throw Error(GSOT_ERR_INVALID_ARGUMENT, "eval: x must be 16-byte aligned (TMA source)");
   // next_task is EvalScalars::next_task: zero_rows lives in the same block
@@ -1849,7 +1852,7 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
     const char* ev = std::getenv("GSOT_EVAL_Q_RECOMPUTE");
     return ev ? std::atoi(ev) : 1;
   }();
-  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, qrows, qrec, next_task, ntasks, ntasks_dev,
+  EvalArgs A{P, x, tasks, words, rowpart, colpart, psi, seg, qrows, qrec, pz_done ? 1 : 0, next_task, ntasks, ntasks_dev,
              &sc->zero_rows, &sc->read_qrows};
   const size_t smem = eval_smem_bytes(seg, qrows);
   if ((int)smem > g_eval_smem_attr[variant]) eval_blocks_per_sm(smem, variant);
