@@ -1873,16 +1873,23 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
 // (dual.hpp:51) and the line-search slope grad.d; k_publish folds them in
 // block order (and the screen's counter slots) before the host reads them.
 // Block (32, 8): blocks [0, m/32) handle 32 rows, the rest 32 columns.
-constexpr int kFinSlices = 8;
+#ifndef GSOT_FIN_SLICES
+#define GSOT_FIN_SLICES 4
+#endif
+constexpr int kFinSlices = GSOT_FIN_SLICES;  // 8 or 4: threads per row / column (and the sums' slices)
+static_assert(kFinSlices == 8 || kFinSlices == 4, "slices");
+constexpr int kFinUnitT = 32 * kFinSlices;   // threads per unit
+// the bits of a 32-bit mask word whose index is 0 mod kFinSlices
+constexpr uint32_t kFinSel = kFinSlices == 8 ? 0x01010101u : 0x11111111u;
 constexpr int kFinBatch = 8;
 constexpr int kFinMaskCap = 1024;  // mask words staged per row unit
-constexpr int kFinListCap = 256;   // compacted chunks per slice (units within one group)
+constexpr int kFinListCap = 2048 / kFinSlices;  // compacted chunks per slice (units within one group)
 
 // Block = two independent units of (32 rows or columns) x 8 slices. Everything
 // that does not depend on the evaluation (x, d, marginals, the chunk masks and
 // survivor words written by the screen, which completed before the evaluation
 // started) is loaded before the programmatic wait.
-__global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
+__global__ void __launch_bounds__(64 * kFinSlices, kFinSlices == 8 ? 3 : 6) k_finalize(
     DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
     const uint32_t* __restrict__ gmask, uint32_t* __restrict__ cmask, int clear_cmask,
     const double* __restrict__ rowpart, const double* __restrict__ colpart,
@@ -1895,7 +1902,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   // wait instead of every lane scanning the group's chunk mask
   __shared__ int clist[2][kFinSlices][kFinListCap];
   __shared__ int ccount[2][2 * kFinSlices];
-  const int half = threadIdx.x >> 8, t = threadIdx.x & 255;
+  const int half = threadIdx.x / kFinUnitT, t = threadIdx.x % kFinUnitT;
   const int tx = t & 31, ty = t >> 5;
   const int unit = 2 * blockIdx.x + half;
   const bool is_row = unit < row_blocks;
@@ -1924,7 +1931,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     const int per = (P.nw + kFinSlices - 1) / kFinSlices;
     coop = (lf == ll && per <= kFinListCap) || (ll == lf + 1 && per <= kFinListCap / 2);
     if (coop) {
-      const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
+      const uint32_t sel = kFinSel << ty;  // chunks c = ty mod 8 within a mask word
       for (int gi = 0; gi <= ll - lf; ++gi) {
         int* __restrict__ out = clist[half][ty] + gi * (kFinListCap / 2);
         int base = 0;
@@ -1946,7 +1953,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     } else {
       staged = (int64_t)(ll - lf + 1) * nmw <= kFinMaskCap;
       if (staged)
-        for (int k = t; k < (ll - lf + 1) * nmw; k += 256) msk[half][k] = gmask[(int64_t)lf * nmw + k];
+        for (int k = t; k < (ll - lf + 1) * nmw; k += kFinUnitT) msk[half][k] = gmask[(int64_t)lf * nmw + k];
     }
   } else if (live) {
     const int64_t c = unit - row_blocks;
@@ -1959,14 +1966,14 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     }
     staged = nlw <= kFinMaskCap;  // the chunk's group mask (non-empty (l, c))
     if (staged)
-      for (int k = t; k < nlw; k += 256) msk[half][k] = cmask[c * nlw + k];
+      for (int k = t; k < nlw; k += kFinUnitT) msk[half][k] = cmask[c * nlw + k];
   }
   __syncthreads();
   if (live && !is_row && staged && (P.L + kFinSlices - 1) / kFinSlices <= kFinListCap) {
     // column unit: the slice's non-empty groups (l = slice mod 8, ascending)
     // from the staged group mask, compacted by the slice's warp
     coop = true;
-    const uint32_t sel = 0x01010101u << ty;
+    const uint32_t sel = kFinSel << ty;
     int base = 0;
     for (int kb = 0; kb < nlw; kb += 32) {
       const uint32_t w = kb + tx < nlw ? msk[half][kb + tx] & sel : 0u;
@@ -1985,7 +1992,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
     __syncwarp();
   }
   if (clear_cmask && live && !is_row && staged)  // consumed: empty for the next screen
-    for (int k = t; k < nlw; k += 256) cmask[(unit - row_blocks) * (int64_t)nlw + k] = 0u;
+    for (int k = t; k < nlw; k += kFinUnitT) cmask[(unit - row_blocks) * (int64_t)nlw + k] = 0u;
   pdl_wait();
   pdl_trigger();
   TL_ENTER(P.tl, TL_FINALIZE);
@@ -2005,7 +2012,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   } else if (i >= 0) {
     const int l = P.row_group[i];
     const uint32_t* gm = staged ? msk[half] + (int64_t)(l - lf) * nmw : gmask + (int64_t)l * nmw;
-    const uint32_t sel = 0x01010101u << ty;  // chunks c = ty mod 8 within a mask word
+    const uint32_t sel = kFinSel << ty;  // chunks c = ty mod 8 within a mask word
     int k = 0;
     uint32_t cur = nmw > 0 ? gm[0] & sel : 0u;
     for (;;) {  // batches of the slice's non-empty chunks, ascending c
@@ -2057,7 +2064,7 @@ __global__ void __launch_bounds__(64 * kFinSlices, 3) k_finalize(
   } else if (j >= 0) {
     const int64_t c = j >> 5;
     const uint32_t* cm = staged ? msk[half] : cmask + c * nlw;
-    const uint32_t sel = 0x01010101u << ty;  // groups l = ty mod 8 within a mask word
+    const uint32_t sel = kFinSel << ty;  // groups l = ty mod 8 within a mask word
     int k = 0;
     uint32_t cur = nlw > 0 ? cm[0] & sel : 0u;
     for (;;) {  // batches of the slice's non-empty (l, c), ascending l
