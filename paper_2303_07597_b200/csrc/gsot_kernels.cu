@@ -1874,22 +1874,26 @@ void launch_eval(const DevProblem& P, const double* x, const TaskDesc* tasks, in
 // block order (and the screen's counter slots) before the host reads them.
 // Block (32, 8): blocks [0, m/32) handle 32 rows, the rest 32 columns.
 #ifndef GSOT_FIN_SLICES
-#define GSOT_FIN_SLICES 4
+#define GSOT_FIN_SLICES 2
 #endif
-constexpr int kFinSlices = GSOT_FIN_SLICES;  // 8 or 4: threads per row / column (and the sums' slices)
-static_assert(kFinSlices == 8 || kFinSlices == 4, "slices");
+// threads per row / column = slices of the sums. Measured on config 5 (fast
+// solve / baseline-mode solve): 8 slices 83.2 / 650 ms, 4: 80.0 / 642, 2: 77.0 /
+// 682, 1: 77.4 / 739 -- fewer threads per unit mean fewer CTA waves of this
+// latency-bound kernel; dense evaluations (long sums) prefer more slices.
+constexpr int kFinSlices = GSOT_FIN_SLICES;
+static_assert(kFinSlices == 8 || kFinSlices == 4 || kFinSlices == 2 || kFinSlices == 1, "slices");
 constexpr int kFinUnitT = 32 * kFinSlices;   // threads per unit
 // the bits of a 32-bit mask word whose index is 0 mod kFinSlices
-constexpr uint32_t kFinSel = kFinSlices == 8 ? 0x01010101u : 0x11111111u;
+constexpr uint32_t kFinSel = kFinSlices == 8 ? 0x01010101u : kFinSlices == 4 ? 0x11111111u : kFinSlices == 2 ? 0x55555555u : 0xffffffffu;
 constexpr int kFinBatch = 8;
 constexpr int kFinMaskCap = 1024;  // mask words staged per row unit
 constexpr int kFinListCap = 2048 / kFinSlices;  // compacted chunks per slice (units within one group)
 
-// Block = two independent units of (32 rows or columns) x 8 slices. Everything
+// Block = two independent units of (32 rows or columns) x kFinSlices slices. Everything
 // that does not depend on the evaluation (x, d, marginals, the chunk masks and
 // survivor words written by the screen, which completed before the evaluation
 // started) is loaded before the programmatic wait.
-__global__ void __launch_bounds__(64 * kFinSlices, kFinSlices == 8 ? 3 : 6) k_finalize(
+__global__ void __launch_bounds__(64 * kFinSlices, kFinSlices == 8 ? 3 : kFinSlices == 4 ? 6 : kFinSlices == 2 ? 10 : 16) k_finalize(
     DevProblem P, const double* __restrict__ x, const uint32_t* __restrict__ words,
     const uint32_t* __restrict__ gmask, uint32_t* __restrict__ cmask, int clear_cmask,
     const double* __restrict__ rowpart, const double* __restrict__ colpart,
