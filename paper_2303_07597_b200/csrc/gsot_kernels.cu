@@ -1142,17 +1142,14 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
       }
       return T;
     };
-    auto claim = [&]() {  // lane 0 claims, the warp agrees
-      int t = 0;
-      if (lane == 0) t = atomicAdd(A.next_task, 1);
-      return __shfl_sync(0xffffffffu, t, 0);
-    };
-    // CTA b starts with task b; further tasks are claimed from grid onwards
+    // CTA b starts with tasks b and b + grid; further tasks are claimed from
+    // 2 * grid onwards, the claim (one atomic, lane 0) in flight while the
+    // next task's descriptor is fetched
     const int G = (int)gridDim.x;
     const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     uint32_t e = 0;
     EvalTask T = fetch(blockIdx.x);
-    int tn = T.valid ? G + claim() : ntasks;  // claimed one task ahead
+    int tn = T.valid ? G + (int)blockIdx.x : ntasks;  // one task ahead
     for (;;) {
       const double* tile = P.C + 32 * ((int64_t)P.nw * T.o0 + (int64_t)T.c * T.g);
       const int ne = (!T.valid || T.zero) ? 1 : T.nseg == 1 ? 1 : 2 * T.nseg;
@@ -1205,8 +1202,10 @@ __global__ void __launch_bounds__(eval_threads(kEvalWarps), kRecompute ? 3 : (kE
         }
         if (k == 0) {
           // decode the next task and claim the one after while this one loads
+          int tc = 0;
+          if (lane == 0) tc = atomicAdd(A.next_task, 1);
           Tn = fetch(tn);
-          tn = Tn.valid ? G + claim() : ntasks;
+          tn = 2 * G + __shfl_sync(0xffffffffu, tc, 0);
         }
       }
       T = Tn;
@@ -1451,16 +1450,13 @@ __global__ void __launch_bounds__(eval_threads(4), 3) k_eval_q(const EvalArgs A)
       }
       return T;
     };
-    auto claim = [&]() {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(A.next_task, 1);
-      return __shfl_sync(0xffffffffu, t, 0);
-    };
+    // CTA b starts with tasks b and b + grid; further tasks are claimed from
+    // 2 * grid onwards, the claim in flight while the next descriptor is fetched
     const int G = (int)gridDim.x;
     const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     uint32_t e = 0;
     EvalTask T = fetch(blockIdx.x);
-    int tn = T.valid ? G + claim() : ntasks;
+    int tn = T.valid ? G + (int)blockIdx.x : ntasks;
     // one step: wait for the slot, publish the task with its first step
     auto acquire = [&](bool first) {
       const int slot = e & 1u;
@@ -1483,8 +1479,10 @@ __global__ void __launch_bounds__(eval_threads(4), 3) k_eval_q(const EvalArgs A)
       EvalTask Tn{};
       bool first = true;
       auto prefetch_next = [&]() {  // decode the next task while this one loads
+        int tc = 0;
+        if (lane == 0) tc = atomicAdd(A.next_task, 1);
         Tn = fetch(tn);
-        tn = Tn.valid ? G + claim() : ntasks;
+        tn = 2 * G + __shfl_sync(0xffffffffu, tc, 0);
       };
       if (!T.valid) {
         const int slot = acquire(true);
