@@ -127,6 +127,7 @@ struct gsot_ctx {
   double* dpos_fast = nullptr;              // L: fast-mode screen's group delta norms (k_group_amax)
   float* cmn = nullptr;                     // L * nw: per-chunk minimum of cmin
   double2* zmm = nullptr;                   // L * nw: per-chunk (min, max) of the snapshot's z~
+  unsigned char* snap_zero = nullptr;       // L * nw: the chunk's z~ k~ o~ currently hold zeros
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;

@@ -184,7 +184,8 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    cudaStream_t s);
 bool screen_uses_summaries(const DevProblem& P, int num_sms);
 // zmm[l * nw + c] = (min, max) of z~ over the chunk's columns: after every snapshot
-void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm, cudaStream_t s);
+void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm,
+                         const unsigned char* zero_chunk, cudaStream_t s);
 // dpre: optional, the fast-mode group delta norms precomputed by launch_group_amax
 // xe: the evaluation state (the provably-zero test; P.amax must hold its
 // group maxima). Fused evaluation over the non-empty chunks of `words` (gsot_kernels.cu).
@@ -244,7 +245,9 @@ constexpr int kSnapListMinRows = 64;  // shorter groups are walked by the markin
 // launch_group_amax)
 void launch_snapshot_lazy2(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                            uint32_t* list, unsigned int* count, unsigned long long* rows_read,
-                           cudaStream_t s);
+                           unsigned char* zero_chunk, double2* zmm, cudaStream_t s);
+// zero_chunk[l * nw + c] = 1: the chunk's z~ k~ o~ hold zeros (maintained by the
+// listed lazy snapshot; cleared by the caller whenever another form writes them)
 void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s);
 // Per-chunk group masks cmask[c][l / 32] bit l % 32: (l, c) non-empty.
 void launch_fill_cmask(uint32_t* cmask, int32_t L, int32_t nw, cudaStream_t s);

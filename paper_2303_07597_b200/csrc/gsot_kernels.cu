@@ -197,38 +197,67 @@ __global__ void __launch_bounds__(256) k_snapshot_mark(DevProblem P, const doubl
                                                        double* __restrict__ os,
                                                        uint32_t* __restrict__ list,
                                                        unsigned int* __restrict__ count,
-                                                       unsigned long long* __restrict__ rows_read) {
+                                                       unsigned long long* __restrict__ rows_read,
+                                                       unsigned char* __restrict__ zero_chunk,
+                                                       double2* __restrict__ zmm) {
   pdl_wait();  // after the group maxima of x (k_group_amax, which zeroed count[])
   pdl_trigger();
+  // one warp = one 32-column chunk of group l
   const int l = blockIdx.y;
+  const int lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t c = j >> 5;
+  if (c >= P.nw) return;  // whole warp
   const bool in = j < P.n;
   const int64_t idx = (int64_t)l * P.n + j;
-  const bool zero = !in || dadd(P.amax[l], x[P.m + j]) <= (double)P.cmin[idx];
-  const unsigned livem = __ballot_sync(0xffffffffu, !zero);
+  const int64_t t = (int64_t)l * P.nw + c;
+  const double amx = P.amax[l];
+  const double bj = in ? x[P.m + j] : 0.0;
+  // chunk-level test first: the chunk's largest beta against its smallest cmin
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double bmx = in ? (bj != bj ? inf : bj) : -inf;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+  bool zero = true;
+  unsigned livem = 0u;
+  if (!(dadd(amx, bmx) <= (double)P.cmn[t])) {
+    zero = !in || dadd(amx, bj) <= (double)P.cmin[idx];
+    livem = __ballot_sync(0xffffffffu, !zero);
+  }
+  if (livem == 0u) {
+    // the whole chunk is provably zero: its z~ k~ o~ are zeros -- written only
+    // if the chunk does not hold zeros already (zero_chunk: kept by this
+    // kernel, cleared whenever another snapshot form writes the arrays)
+    // (lane 0 reads the flag for the warp: it also writes it)
+    const int was = __shfl_sync(0xffffffffu, lane == 0 ? (int)zero_chunk[t] : 0, 0);
+    if (!was) {
+      if (in) {
+        zs[idx] = 0.0;
+        ks[idx] = 0.0;
+        os[idx] = 0.0;
+      }
+      if (lane == 0) zero_chunk[t] = 1;
+    }
+    if (lane == 0) zmm[t] = make_double2(0.0, 0.0);
+    return;
+  }
+  if (lane == 0) zero_chunk[t] = 0;
   if (zero && in) {
     zs[idx] = 0.0;
     ks[idx] = 0.0;
     os[idx] = 0.0;
   }
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
+  if (lane == 0)
+    atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(livem) * (unsigned)g);
   if (g < kSnapListMinRows) {  // a short column: walked here (listing it costs more than it saves)
-    if (livem && (threadIdx.x & 31) == 0)
-      atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(livem) * (unsigned)g);
     if (!zero) snapshot_block(P, x, o0, g, l, j, zs, ks, os);
     return;
   }
-  if (livem) {
-    const int lane = threadIdx.x & 31;
-    unsigned int base = 0;
-    if (lane == 0) {
-      base = atomicAdd(count + l, (unsigned int)__popc(livem));
-      atomicAdd(rows_read + (blockIdx.x & 63),
-                (unsigned long long)__popc(livem) * (unsigned)g);
-    }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (!zero) list[(int64_t)l * P.n + base + __popc(livem & ((1u << lane) - 1u))] = (uint32_t)j;
-  }
+  unsigned int base = 0;
+  if (lane == 0) base = atomicAdd(count + l, (unsigned int)__popc(livem));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (!zero) list[(int64_t)l * P.n + base + __popc(livem & ((1u << lane) - 1u))] = (uint32_t)j;
 }
 
 constexpr int kSnapWalkX = 8;  // CTAs per group
@@ -256,9 +285,10 @@ __global__ void __launch_bounds__(128) k_snapshot_walk(DevProblem P, const doubl
 
 void launch_snapshot_lazy2(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                            uint32_t* list, unsigned int* count, unsigned long long* rows_read,
-                           cudaStream_t s) {
+                           unsigned char* zero_chunk, double2* zmm, cudaStream_t s) {
   dim3 grid((unsigned)((P.n + 255) / 256), (unsigned)P.L);
-  launch_pdl(k_snapshot_mark, grid, dim3(256), 0, s, P, x, zs, ks, os, list, count, rows_read);
+  launch_pdl(k_snapshot_mark, grid, dim3(256), 0, s, P, x, zs, ks, os, list, count, rows_read,
+             zero_chunk, zmm);
   launch_pdl(k_snapshot_walk, dim3(kSnapWalkX, (unsigned)P.L), dim3(128), 0, s, P, x, zs, ks, os,
              (const uint32_t*)list, (const unsigned int*)count);
 }
@@ -915,12 +945,14 @@ __global__ void __launch_bounds__(256) k_block_min(DevProblem P, float* __restri
 // (a NaN makes them -inf / +inf: the screen then walks the chunk). Once per
 // snapshot, for the screen's whole-chunk decisions.
 __global__ void __launch_bounds__(256) k_chunk_minmax(DevProblem P, const double* __restrict__ zs,
-                                                      double2* __restrict__ zmm) {
+                                                      double2* __restrict__ zmm,
+                                                      const unsigned char* __restrict__ zero_chunk) {
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // l * nw + c
   if (t >= (int64_t)P.L * P.nw) return;
+  if (zero_chunk && zero_chunk[t]) return;  // all zeros: k_snapshot_mark wrote (0, 0)
   const int l = (int)(t / P.nw), c = (int)(t % P.nw);
   const int64_t j = (int64_t)c * 32 + lane;
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -938,9 +970,11 @@ __global__ void __launch_bounds__(256) k_chunk_minmax(DevProblem P, const double
   if (lane == 0) zmm[t] = make_double2(mn, mx);
 }
 
-void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm, cudaStream_t s) {
+void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm,
+                         const unsigned char* zero_chunk, cudaStream_t s) {
   const int64_t tiles = (int64_t)P.L * P.nw;
-  launch_pdl(k_chunk_minmax, dim3((unsigned)((tiles + 7) / 8)), dim3(256), 0, s, P, zs, zmm);
+  launch_pdl(k_chunk_minmax, dim3((unsigned)((tiles + 7) / 8)), dim3(256), 0, s, P, zs, zmm,
+             zero_chunk);
 }
 
 void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s) {
