@@ -829,6 +829,8 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
 // smaller instances take k_screen_rows, which needs neither the per-chunk
 // extremes nor the precomputed group delta norms.
 bool screen_uses_summaries(const DevProblem& P, int num_sms) {
+  // (GSOT_SCREEN_SUMMARIES=1 / 0 forces the choice: tests run k_screen on small instances)
+  if (const char* ev = std::getenv("GSOT_SCREEN_SUMMARIES")) return std::atoi(ev) != 0;
   const int64_t gx = (P.nw + 31) / 32, gy = (P.L + kScrWarps - 1) / kScrWarps;
   return gx * gy >= 4ll * num_sms;
 }

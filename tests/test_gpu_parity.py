@@ -615,6 +615,52 @@ def test_context_cache_reuse_is_clean(o):
     c3.close()
 
 
+@pytest.mark.parametrize("sizes,n", [([70, 100, 64, 9, 130, 33, 65, 80, 77], 200),
+                                     ([300, 64, 5, 90], 97)])
+def test_summary_screen_and_listed_snapshots(o, sizes, n, monkeypatch):
+    # The chunk-summary screen (k_screen: whole chunks decided from the extremes
+    # of z~ / dbeta / beta / cmin, mixed chunks walked) forced on a small instance,
+    # with groups tall enough for the listed lazy snapshot (k_snapshot_mark /
+    # k_snapshot_walk and the zero_chunk flags). Decisions and counters are the
+    # reference's; screened == dense bitwise; fast == baseline solve bitwise; and
+    # a context whose arrays went through lazy snapshots, full API snapshots and
+    # lazy ones again solves exactly as a fresh one.
+    monkeypatch.setenv("GSOT_SCREEN_SUMMARIES", "1")
+    monkeypatch.setenv("GSOT_CTX_CACHE", "0")
+    p, rng = random_problem(sizes, n, 0.3, 0.6, 61 + n, weighted=True)
+    kw = dict(max_outer_loops=4, grad_tol=1e-12)
+    ctx = ctx_of(p)
+    rb = ctx.solve(mode=0, **kw)
+    rf = ctx.solve(mode=1, **kw)  # lazy, listed snapshots
+    assert np.array_equal(rf["x"], rb["x"]) and rf["objective"] == rb["objective"]
+    x0 = np.zeros(p.m + p.n)
+    for scale, spread in ((1e-3, 1e-5), (0.6, 1e-3)):
+        beta = rng.uniform(-0.1, 1.2, p.n) * scale
+        beta[5:40] = -2.0  # whole chunks provably zero
+        x1 = np.concatenate([rng.uniform(-0.1, 1.2, p.m) * scale, beta])
+        x2 = x1 + spread * rng.normal(size=x1.size)
+        ctx.init_snapshot(x0)  # full API snapshots over the lazy ones
+        ctx.refresh(x1, True)
+        mem_o, _ = o.active_set(p, x0[: p.m], x0[p.m:], x1[: p.m], x1[p.m:])
+        obj_s, g_s, st = ctx.eval(x2, screened=True)
+        ga, gb, c_o, _ = o.fast_gradient(p, x1[: p.m], x1[p.m:], mem_o, x2[: p.m], x2[p.m:])
+        assert [st.in_active, st.skipped, st.unskipped, st.upper_bounds] == c_o.tolist()
+        assert_eval_close(o, p, x2, obj_s, g_s, None, np.concatenate([ga, gb]))
+        obj_d, g_d, _ = ctx.eval(x2)
+        assert obj_d == obj_s and np.array_equal(g_d, g_s)
+        z, k, oo = ctx.snapshot_norms()
+        z_o, k_o, oo_o = o.snapshot(p, x1[: p.m], x1[p.m:])
+        assert np.array_equal(z, z_o) and np.array_equal(k, k_o) and np.array_equal(oo, oo_o)
+    again = ctx.solve(mode=1, **kw)  # lazy snapshots over the full ones
+    fresh = ctx_of(p)
+    rf2 = fresh.solve(mode=1, **kw)
+    for r in (again, rf2):
+        assert np.array_equal(r["x"], rf["x"]) and r["objective"] == rf["objective"]
+        assert r["grad_calls"] == rf["grad_calls"] and r["blocks_skipped"] == rf["blocks_skipped"]
+    fresh.close()
+    ctx.close()
+
+
 def test_many_groups_screen_layout(o):
     # L x n large enough (>= 4 CTAs per SM of work) for the transposed screen
     # kernel (lane = chunk, warp = group): decisions and counters still the
