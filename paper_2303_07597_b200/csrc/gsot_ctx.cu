@@ -124,7 +124,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt, dpos_fast, cmn, zmm, snap_zero};
+                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt, dpos_fast, cmn, zmm, snap_zero, bmaxc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ex_ready) gsot::exact_ws_free(ex);
@@ -230,6 +230,7 @@ void alloc_buffers(gsot_ctx* c) {
   c->dpos_fast = dalloc<double>(L, t);
   c->cmn = dalloc<float>(static_cast<size_t>(L) * nw, t);
   c->zmm = dalloc<double2>(static_cast<size_t>(L) * nw, t);
+  c->bmaxc = dalloc<double>(nw, t);
   c->snap_zero = dalloc<unsigned char>(static_cast<size_t>(L) * nw, t);
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_zero, 0, static_cast<size_t>(L) * nw, c->stream));
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
@@ -640,7 +641,8 @@ void enqueue_snapshot(gsot_ctx* c, const double* d_x, bool lazy) {  // take_snap
     if (listed) ++c->launches;  // two kernels
     if (listed)
       launch_snapshot_lazy2(P, d_x, c->zs, c->ks, c->os, c->snap_list, list_len, c->snap_rows,
-                            c->snap_zero, c->zmm, c->stream);
+                            c->snap_zero, c->zmm, c->bmaxc, c->stream);
+    if (listed) ++c->launches;  // k_chunk_bmax
     else
       launch_snapshot(P, d_x, c->zs, c->ks, c->os, lazy, c->snap_rows, c->stream);
   });

@@ -128,6 +128,7 @@ struct gsot_ctx {
   float* cmn = nullptr;                     // L * nw: per-chunk minimum of cmin
   double2* zmm = nullptr;                   // L * nw: per-chunk (min, max) of the snapshot's z~
   unsigned char* snap_zero = nullptr;       // L * nw: the chunk's z~ k~ o~ currently hold zeros
+  double* bmaxc = nullptr;                  // nw: per-chunk maximum of beta (lazy snapshot's chunk test)
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;

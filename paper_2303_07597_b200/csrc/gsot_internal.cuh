@@ -245,7 +245,8 @@ constexpr int kSnapListMinRows = 64;  // shorter groups are walked by the markin
 // launch_group_amax)
 void launch_snapshot_lazy2(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                            uint32_t* list, unsigned int* count, unsigned long long* rows_read,
-                           unsigned char* zero_chunk, double2* zmm, cudaStream_t s);
+                           unsigned char* zero_chunk, double2* zmm, double* bmaxc,
+                           cudaStream_t s);
 // zero_chunk[l * nw + c] = 1: the chunk's z~ k~ o~ hold zeros (maintained by the
 // listed lazy snapshot; cleared by the caller whenever another form writes them)
 void launch_fill_gmask(uint32_t* gmask, int32_t L, int32_t nw, cudaStream_t s);

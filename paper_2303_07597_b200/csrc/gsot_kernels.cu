@@ -199,65 +199,92 @@ __global__ void __launch_bounds__(256) k_snapshot_mark(DevProblem P, const doubl
                                                        unsigned int* __restrict__ count,
                                                        unsigned long long* __restrict__ rows_read,
                                                        unsigned char* __restrict__ zero_chunk,
-                                                       double2* __restrict__ zmm) {
-  pdl_wait();  // after the group maxima of x (k_group_amax, which zeroed count[])
+                                                       double2* __restrict__ zmm,
+                                                       const double* __restrict__ bmaxc) {
+  pdl_wait();  // after k_group_amax: the group maxima of x, the chunk maxima of beta, count[] = 0
   pdl_trigger();
-  // one warp = one 32-column chunk of group l
+  // one warp = 32 consecutive chunks of group l, lane = chunk: a chunk whose
+  // largest beta passes against its smallest cmin is provably zero whole; if
+  // its z~ k~ o~ already hold zeros (zero_chunk: kept here, cleared whenever
+  // another snapshot form writes the arrays) there is nothing to do. The other
+  // chunks are walked one by one (lane = column).
   const int l = blockIdx.y;
   const int lane = threadIdx.x & 31;
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t c = j >> 5;
-  if (c >= P.nw) return;  // whole warp
-  const bool in = j < P.n;
-  const int64_t idx = (int64_t)l * P.n + j;
+  const int64_t c = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32 + lane;
+  const bool cvalid = c < P.nw;
   const int64_t t = (int64_t)l * P.nw + c;
   const double amx = P.amax[l];
-  const double bj = in ? x[P.m + j] : 0.0;
-  // chunk-level test first: the chunk's largest beta against its smallest cmin
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  double bmx = in ? (bj != bj ? inf : bj) : -inf;
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
-  bool zero = true;
-  unsigned livem = 0u;
-  if (!(dadd(amx, bmx) <= (double)P.cmn[t])) {
-    zero = !in || dadd(amx, bj) <= (double)P.cmin[idx];
-    livem = __ballot_sync(0xffffffffu, !zero);
-  }
-  if (livem == 0u) {
-    // the whole chunk is provably zero: its z~ k~ o~ are zeros -- written only
-    // if the chunk does not hold zeros already (zero_chunk: kept by this
-    // kernel, cleared whenever another snapshot form writes the arrays)
-    // (lane 0 reads the flag for the warp: it also writes it)
-    const int was = __shfl_sync(0xffffffffu, lane == 0 ? (int)zero_chunk[t] : 0, 0);
-    if (!was) {
-      if (in) {
-        zs[idx] = 0.0;
-        ks[idx] = 0.0;
-        os[idx] = 0.0;
-      }
-      if (lane == 0) zero_chunk[t] = 1;
-    }
-    if (lane == 0) zmm[t] = make_double2(0.0, 0.0);
-    return;
-  }
-  if (lane == 0) zero_chunk[t] = 0;
-  if (zero && in) {
-    zs[idx] = 0.0;
-    ks[idx] = 0.0;
-    os[idx] = 0.0;
-  }
+  const bool pass = cvalid && dadd(amx, bmaxc[cvalid ? c : 0]) <= (double)P.cmn[cvalid ? t : 0];
+  const bool flagged = cvalid && zero_chunk[cvalid ? t : 0] != 0;
+  uint32_t fill = __ballot_sync(0xffffffffu, pass && !flagged);   // zeros to write
+  uint32_t mixed = __ballot_sync(0xffffffffu, cvalid && !pass);   // column by column
+  const int64_t c0 = c - lane;
   const int o0 = P.off[l], g = P.off[l + 1] - o0;
-  if (lane == 0)
-    atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(livem) * (unsigned)g);
-  if (g < kSnapListMinRows) {  // a short column: walked here (listing it costs more than it saves)
-    if (!zero) snapshot_block(P, x, o0, g, l, j, zs, ks, os);
-    return;
+  while (fill) {
+    const int ci = __ffs(fill) - 1;
+    fill &= fill - 1u;
+    const int64_t j = (c0 + ci) * 32 + lane;
+    if (j < P.n) {
+      const int64_t idx = (int64_t)l * P.n + j;
+      zs[idx] = 0.0;
+      ks[idx] = 0.0;
+      os[idx] = 0.0;
+    }
+    if (lane == 0) {
+      zero_chunk[t + ci] = 1;
+      zmm[t + ci] = make_double2(0.0, 0.0);
+    }
   }
-  unsigned int base = 0;
-  if (lane == 0) base = atomicAdd(count + l, (unsigned int)__popc(livem));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (!zero) list[(int64_t)l * P.n + base + __popc(livem & ((1u << lane) - 1u))] = (uint32_t)j;
+  while (mixed) {
+    const int ci = __ffs(mixed) - 1;
+    mixed &= mixed - 1u;
+    const int64_t j = (c0 + ci) * 32 + lane;
+    const bool in = j < P.n;
+    const int64_t idx = (int64_t)l * P.n + j;
+    const bool zero = !in || dadd(amx, x[P.m + j]) <= (double)P.cmin[idx];
+    const unsigned livem = __ballot_sync(0xffffffffu, !zero);
+    if (zero && in) {
+      zs[idx] = 0.0;
+      ks[idx] = 0.0;
+      os[idx] = 0.0;
+    }
+    if (lane == 0) {
+      zero_chunk[t + ci] = livem == 0u ? 1 : 0;
+      if (livem == 0u) zmm[t + ci] = make_double2(0.0, 0.0);
+    }
+    if (livem == 0u) continue;
+    if (lane == 0)
+      atomicAdd(rows_read + (blockIdx.x & 63), (unsigned long long)__popc(livem) * (unsigned)g);
+    if (g < kSnapListMinRows) {  // a short column: walked here (listing it costs more than it saves)
+      if (!zero) snapshot_block(P, x, o0, g, l, j, zs, ks, os);
+      continue;
+    }
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(count + l, (unsigned int)__popc(livem));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (!zero) list[(int64_t)l * P.n + base + __popc(livem & ((1u << lane) - 1u))] = (uint32_t)j;
+  }
+}
+
+// Per chunk: the largest beta of its valid columns (+inf if one is NaN), for
+// the snapshot's whole-chunk zero test. One warp per chunk.
+__global__ void __launch_bounds__(256) k_chunk_bmax(DevProblem P, const double* __restrict__ x,
+                                                    double* __restrict__ bmaxc) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= P.nw) return;
+  const int64_t j = c * 32 + lane;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double b = -inf;
+  if (j < P.n) {
+    const double v = x[P.m + j];
+    b = v != v ? inf : v;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  if (lane == 0) bmaxc[c] = b;
 }
 
 constexpr int kSnapWalkX = 8;  // CTAs per group
@@ -285,10 +312,12 @@ __global__ void __launch_bounds__(128) k_snapshot_walk(DevProblem P, const doubl
 
 void launch_snapshot_lazy2(const DevProblem& P, const double* x, double* zs, double* ks, double* os,
                            uint32_t* list, unsigned int* count, unsigned long long* rows_read,
-                           unsigned char* zero_chunk, double2* zmm, cudaStream_t s) {
-  dim3 grid((unsigned)((P.n + 255) / 256), (unsigned)P.L);
+                           unsigned char* zero_chunk, double2* zmm, double* bmaxc,
+                           cudaStream_t s) {
+  launch_pdl(k_chunk_bmax, dim3((unsigned)((P.nw + 7) / 8)), dim3(256), 0, s, P, x, bmaxc);
+  dim3 grid((unsigned)((P.nw + 255) / 256), (unsigned)P.L);  // 256 chunks per CTA
   launch_pdl(k_snapshot_mark, grid, dim3(256), 0, s, P, x, zs, ks, os, list, count, rows_read,
-             zero_chunk, zmm);
+             zero_chunk, zmm, (const double*)bmaxc);
   launch_pdl(k_snapshot_walk, dim3(kSnapWalkX, (unsigned)P.L), dim3(128), 0, s, P, x, zs, ks, os,
              (const uint32_t*)list, (const unsigned int*)count);
 }
@@ -951,31 +980,40 @@ __global__ void __launch_bounds__(256) k_chunk_minmax(DevProblem P, const double
                                                       const unsigned char* __restrict__ zero_chunk) {
   pdl_wait();
   pdl_trigger();
+  // one warp = 32 consecutive (group, chunk) pairs, lane = pair: the pairs that
+  // are not known to hold zeros (k_snapshot_mark wrote (0, 0) for those) are
+  // reduced one by one, lane = column
   const int lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // l * nw + c
-  if (t >= (int64_t)P.L * P.nw) return;
-  if (zero_chunk && zero_chunk[t]) return;  // all zeros: k_snapshot_mark wrote (0, 0)
-  const int l = (int)(t / P.nw), c = (int)(t % P.nw);
-  const int64_t j = (int64_t)c * 32 + lane;
+  const int64_t total = (int64_t)P.L * P.nw;
+  const int64_t t0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+  const int64_t tl = t0 + lane;
+  uint32_t todo = __ballot_sync(0xffffffffu, tl < total && !(zero_chunk && zero_chunk[tl]));
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  double mn = inf, mx = -inf;
-  if (j < P.n) {
-    const double z = zs[(int64_t)l * P.n + j];
-    mn = z != z ? -inf : z;
-    mx = z != z ? inf : z;
-  }
+  while (todo) {
+    const int ti = __ffs(todo) - 1;
+    todo &= todo - 1u;
+    const int64_t t = t0 + ti;
+    const int l = (int)(t / P.nw), c = (int)(t % P.nw);
+    const int64_t j = (int64_t)c * 32 + lane;
+    double mn = inf, mx = -inf;
+    if (j < P.n) {
+      const double z = zs[(int64_t)l * P.n + j];
+      mn = z != z ? -inf : z;
+      mx = z != z ? inf : z;
+    }
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o >= 1; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) zmm[t] = make_double2(mn, mx);
   }
-  if (lane == 0) zmm[t] = make_double2(mn, mx);
 }
 
 void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm,
                          const unsigned char* zero_chunk, cudaStream_t s) {
   const int64_t tiles = (int64_t)P.L * P.nw;
-  launch_pdl(k_chunk_minmax, dim3((unsigned)((tiles + 7) / 8)), dim3(256), 0, s, P, zs, zmm,
+  launch_pdl(k_chunk_minmax, dim3((unsigned)((tiles + 255) / 256)), dim3(256), 0, s, P, zs, zmm,
              zero_chunk);
 }
 
