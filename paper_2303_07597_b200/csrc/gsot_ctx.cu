@@ -124,7 +124,7 @@ gsot_ctx::~gsot_ctx() {
                   words,    dense_words, dense_tasks, tasks, snap_x,   zs,      ks,
                   os,       dpos,    dfull,         dneg,        dbeta,    active_words, dsync,
                   cnt_partials, cnt_slots, d_pub_count, gmask, dense_gmask, cmask, dense_cmask, tl,
-                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt, dpos_fast, cmn, zmm, snap_zero, bmaxc};
+                  d_one, staging, d_bad, cmin, amax, snap_rows, snap_list, snap_cnt, dpos_fast, cmn, zmm, snap_zero, bmaxc, dbx3};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ex_ready) gsot::exact_ws_free(ex);
@@ -231,6 +231,7 @@ void alloc_buffers(gsot_ctx* c) {
   c->cmn = dalloc<float>(static_cast<size_t>(L) * nw, t);
   c->zmm = dalloc<double2>(static_cast<size_t>(L) * nw, t);
   c->bmaxc = dalloc<double>(nw, t);
+  c->dbx3 = dalloc<double>(3 * static_cast<size_t>(nw), t);
   c->snap_zero = dalloc<unsigned char>(static_cast<size_t>(L) * nw, t);
   GSOT_CUDA_CHECK(cudaMemsetAsync(c->snap_zero, 0, static_cast<size_t>(L) * nw, c->stream));
   c->active_words = dalloc<uint32_t>(static_cast<size_t>(L) * nw, t);
@@ -548,28 +549,31 @@ void enqueue_eval(gsot_ctx* c, const double* d_x, int mode_flags, double* d_grad
   // per-group max alpha for the provably-zero block test (k_block_min): read
   // by the screen and the evaluation
   const bool fused = mode == GSOT_EVAL_SCREENED && dbeta_ready && !exact;
-  const bool pre = fused && screen_uses_summaries(P, c->num_sms);  // delta norms once per group
+  const bool summ = mode == GSOT_EVAL_SCREENED && screen_uses_summaries(P, c->num_sms);
+  const bool pre = fused && summ;  // delta norms once per group
+  // Fast solves fuse the group delta norms into the screen (the step / trial
+  // kernel wrote dbeta); every other screened evaluation -- exact mode and
+  // the API's gsot_eval -- takes the reference-order norms of k_delta, so
+  // its decisions and counters are the reference's bit for bit.
+  if (mode == GSOT_EVAL_SCREENED && !fused)
+    c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
+      launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, nullptr,
+                   c->stream);
+    });
+  // (after dbeta is final: the chunk role reads it)
   c->launch(K_MISC, 8.0 * c->m, [&] {
     launch_group_amax(P, d_x, c->amax, c->stream, nullptr, pre ? c->snap_x : nullptr,
-                      pre ? c->dpos_fast : nullptr);
+                      pre ? c->dpos_fast : nullptr, summ ? c->dbeta : nullptr,
+                      summ ? c->dbx3 : nullptr);
   });
   const uint32_t* words = c->dense_words;
   const double Ln = static_cast<double>(c->L) * c->n;
   if (mode == GSOT_EVAL_SCREENED) {
-    // Fast solves fuse the group delta norms into the screen (the step / trial
-    // kernel wrote dbeta); every other screened evaluation -- exact mode and
-    // the API's gsot_eval -- takes the reference-order norms of k_delta, so
-    // its decisions and counters are the reference's bit for bit.
-    if (!fused)
-      c->launch(K_DELTA, 16.0 * (c->m + c->n) + 32.0 * c->L + 8.0 * c->n, [&] {
-        launch_delta(P, d_x, c->snap_x, c->dpos, c->dfull, c->dneg, c->dbeta, nullptr, nullptr,
-                     c->stream);
-      });
     c->launch(K_BOUNDS, 8.0 * Ln + 8.0 * c->L * c->nw, [&] {
       launch_screen(P, c->zs, use_active ? c->active_words : nullptr, c->dpos, c->dbeta,
                     ub_offset, c->words, c->tasks, c->sc, c->cnt_slots, c->gmask,
                     c->cmask, fused ? d_x : nullptr, fused ? c->snap_x : nullptr,
-                    fused ? 1 : 0, d_x, pre ? c->dpos_fast : nullptr, c->zmm, c->num_sms,
+                    fused ? 1 : 0, d_x, pre ? c->dpos_fast : nullptr, c->zmm, c->dbx3, c->num_sms,
                     c->stream);
     });
     words = c->words;

@@ -129,6 +129,7 @@ struct gsot_ctx {
   double2* zmm = nullptr;                   // L * nw: per-chunk (min, max) of the snapshot's z~
   unsigned char* snap_zero = nullptr;       // L * nw: the chunk's z~ k~ o~ currently hold zeros
   double* bmaxc = nullptr;                  // nw: per-chunk maximum of beta (lazy snapshot's chunk test)
+  double* dbx3 = nullptr;                   // 3 nw: per-chunk (min dbeta, max dbeta, max beta) for the screen
   uint32_t* active_words = nullptr;
   int64_t active_count = 0;
   bool have_snapshot = false;

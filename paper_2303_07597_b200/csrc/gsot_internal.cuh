@@ -180,8 +180,8 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
-                   const double* xe, const double* dpre, const double2* zmm, int num_sms,
-                   cudaStream_t s);
+                   const double* xe, const double* dpre, const double2* zmm, const double* dbx3,
+                   int num_sms, cudaStream_t s);
 bool screen_uses_summaries(const DevProblem& P, int num_sms);
 // zmm[l * nw + c] = (min, max) of z~ over the chunk's columns: after every snapshot
 void launch_chunk_minmax(const DevProblem& P, const double* zs, double2* zmm,
@@ -238,7 +238,10 @@ void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s);
 // xs, dfast: optional; dfast[l] = |[x_l - xs_l]+| (the fast-mode screen's group delta norm)
 void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s,
                        unsigned int* zero_me = nullptr, const double* xs = nullptr,
-                       double* dfast = nullptr);
+                       double* dfast = nullptr, const double* dbeta = nullptr,
+                       double* dbx3 = nullptr);
+// dbeta, dbx3: optional; dbx3[3 c ..] = (min dbeta, max dbeta, max beta) of chunk c,
+// for the chunk-summary screen
 constexpr int kSnapListMinRows = 64;  // shorter groups are walked by the marking kernel itself
 // lazy snapshot through per-group lists of the blocks that are not provably
 // zero (list: L * n column indices; count: L lengths, cleared by the preceding

@@ -642,8 +642,8 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
                                                 const double* __restrict__ xs, int dbeta_ready,
                                                 const double* __restrict__ xe,
                                                 const double* __restrict__ dpre,
-                                                const double2* __restrict__ zmm) {
-  __shared__ double dbx[32][3];  // per chunk: min / max dbeta, max beta
+                                                const double2* __restrict__ zmm,
+                                                const double* __restrict__ dbx3) {
   __shared__ unsigned long long cnt[kScrWarps][6];
   __shared__ int wn[kScrWarps];                        // non-empty chunks per warp
   __shared__ uint32_t gbits[kScrWarps][32];            // for the per-chunk group masks
@@ -685,34 +685,13 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   // dbmax): a chunk whose largest bound is <= tau is skipped whole, one whose
   // smallest is > tau kept whole -- the reference's decisions, without reading
   // the 32 z~. Only mixed chunks are walked (lane = column, one ballot each).
-  // dbeta / beta extremes of the CTA's 32 chunks: warp w takes chunks 4w..4w+3.
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int ci = 4 * warp + q;
-    const int64_t j = (int64_t)(c0 + ci) * 32 + lane;
-    const bool ok = c0 + ci < P.nw && j < P.n;
-    double db = 0.0, be = 0.0;
-    if (ok) {
-      db = db_inline ? dsub(x[P.m + j], xs[P.m + j]) : dbeta[j];
-      be = xe[P.m + j];
-    }
-    const double inf = __longlong_as_double(0x7ff0000000000000ll);
-    // a NaN makes the chunk mixed (extremes +-inf)
-    double dmx = ok ? (db != db ? inf : db) : -inf, dmn = ok ? (db != db ? -inf : db) : inf;
-    double bmx = ok ? (be != be ? inf : be) : -inf;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
-      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
-      bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
-    }
-    if (lane == 0) {
-      dbx[ci][0] = dmn;
-      dbx[ci][1] = dmx;
-      dbx[ci][2] = bmx;
-    }
+  // (the chunks' dbeta / beta extremes come from k_group_amax's chunk role)
+  double dbmn = 0.0, dbmx = 0.0, bemx = 0.0;
+  if (cvalid) {
+    dbmn = dbx3[3 * (int64_t)c];
+    dbmx = dbx3[3 * (int64_t)c + 1];
+    bemx = dbx3[3 * (int64_t)c + 2];
   }
-  __syncthreads();
   auto zbar_of = [&](double z, double db) {
     return dadd(dadd(dadd(z, dp), dmul(sg, relu(db))), ub_offset);
   };
@@ -720,8 +699,8 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   {
     double2 zm = make_double2(0.0, 0.0);
     if (lvalid && cvalid) zm = zmm[(int64_t)l * P.nw + c];
-    const bool all_skip = zbar_of(zm.y, dbx[lane][1]) <= P.tau;
-    const bool all_keep = !(zbar_of(zm.x, dbx[lane][0]) <= P.tau);
+    const bool all_skip = zbar_of(zm.y, dbmx) <= P.tau;
+    const bool all_keep = !(zbar_of(zm.x, dbmn) <= P.tau);
     surv = all_skip ? 0u : 0xffffffffu;
     uint32_t need = __ballot_sync(0xffffffffu, lvalid && cvalid && !all_skip && !all_keep);
     const double* __restrict__ zrow = zs + (int64_t)(lvalid ? l : 0) * P.n;
@@ -765,7 +744,7 @@ __global__ void __launch_bounds__(256) k_screen(DevProblem P, const double* __re
   {
     const double amx = lvalid ? P.amax[l] : 0.0;
     bool detail = false;
-    if (wd != 0u) detail = !(dadd(amx, dbx[lane][2]) <= (double)P.cmn[(int64_t)l * P.nw + c]);
+    if (wd != 0u) detail = !(dadd(amx, bemx) <= (double)P.cmn[(int64_t)l * P.nw + c]);
     uint32_t need = __ballot_sync(0xffffffffu, detail);
     const float* __restrict__ crow = P.cmin + (int64_t)(lvalid ? l : 0) * P.n;
     while (need) {
@@ -868,8 +847,8 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
                    const double* dbeta, double ub_offset, uint32_t* words, TaskDesc* tasks,
                    EvalScalars* sc, unsigned long long* cnt_slots, uint32_t* gmask,
                    uint32_t* cmask, const double* x, const double* xs, int dbeta_ready,
-                   const double* xe, const double* dpre, const double2* zmm, int num_sms,
-                   cudaStream_t s) {
+                   const double* xe, const double* dpre, const double2* zmm, const double* dbx3,
+                   int num_sms, cudaStream_t s) {
   const dim3 grid((unsigned)((P.nw + 31) / 32), (unsigned)((P.L + kScrWarps - 1) / kScrWarps));
   if (!screen_uses_summaries(P, num_sms)) {  // small: one CTA per (group, 2048 columns)
     const dim3 g2((unsigned)((P.nw + 63) / 64), (unsigned)P.L);
@@ -878,7 +857,7 @@ void launch_screen(const DevProblem& P, const double* zs, const uint32_t* aw, co
     return;
   }
   launch_pdl(k_screen, grid, dim3(32 * kScrWarps), 0, s, P, zs, aw, dpos, dbeta, ub_offset, words,
-             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready, xe, dpre, zmm);
+             tasks, sc, cnt_slots, gmask, cmask, x, xs, dbeta_ready, xe, dpre, zmm, dbx3);
 }
 
 // Dense mode: every word full (bits only for j < n), every chunk a task.
@@ -1028,9 +1007,41 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
                                                     double* __restrict__ amax,
                                                     unsigned int* __restrict__ zero_me,
                                                     const double* __restrict__ xs,
-                                                    double* __restrict__ dfast) {
+                                                    double* __restrict__ dfast,
+                                                    const double* __restrict__ dbeta,
+                                                    double* __restrict__ dbx3) {
   pdl_wait();
   pdl_trigger();
+  const int ga = (P.L + 7) / 8;  // CTAs of the group role; the rest: chunk role
+  if ((int)blockIdx.x >= ga) {
+    // per chunk, for the screen's whole-chunk decisions: the extremes of dbeta
+    // and the largest beta over the chunk's valid columns (a NaN makes them
+    // -inf / +inf: the chunk is then walked). One warp per chunk.
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x - ga) * 8 + (threadIdx.x >> 5);
+    if (c >= P.nw) return;
+    const int64_t j = c * 32 + lane;
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    double dmn = inf, dmx = -inf, bmx = -inf;
+    if (j < P.n) {
+      const double db = dbeta[j], be = x[P.m + j];
+      dmn = db != db ? -inf : db;
+      dmx = db != db ? inf : db;
+      bmx = be != be ? inf : be;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+      bmx = fmax(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+    }
+    if (lane == 0) {
+      dbx3[3 * c] = dmn;
+      dbx3[3 * c + 1] = dmx;
+      dbx3[3 * c + 2] = bmx;
+    }
+    return;
+  }
 
   const int lane = threadIdx.x & 31;
   const int l = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -1081,8 +1092,11 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
 }
 
 void launch_group_amax(const DevProblem& P, const double* x, double* amax, cudaStream_t s,
-                       unsigned int* zero_me, const double* xs, double* dfast) {
-  launch_pdl(k_group_amax, dim3((P.L + 7) / 8), dim3(256), 0, s, P, x, amax, zero_me, xs, dfast);
+                       unsigned int* zero_me, const double* xs, double* dfast,
+                       const double* dbeta, double* dbx3) {
+  const int ga = (P.L + 7) / 8, gc = dbx3 ? (P.nw + 7) / 8 : 0;
+  launch_pdl(k_group_amax, dim3(ga + gc), dim3(256), 0, s, P, x, amax, zero_me, xs, dfast, dbeta,
+             dbx3);
 }
 
 // ---------------------------------------------------------------- fused eval
