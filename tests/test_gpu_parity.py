@@ -252,7 +252,13 @@ def random_problem(sizes, n, gamma, mu, seed, weighted=False):
 
 @pytest.mark.parametrize("struct", sorted(STRUCTURES))
 @pytest.mark.parametrize("gamma,mu", [(1.0, 0.1), (0.3, 0.9)])
-def test_structures_eval_and_screen(o, struct, gamma, mu):
+@pytest.mark.parametrize("summaries", [False, True])
+def test_structures_eval_and_screen(o, struct, gamma, mu, summaries, monkeypatch):
+    # summaries: the chunk-summary screen (k_screen) forced on these small
+    # instances; otherwise they take the small-instance screen (k_screen_rows)
+    if summaries:
+        monkeypatch.setenv("GSOT_SCREEN_SUMMARIES", "1")
+        monkeypatch.setenv("GSOT_CTX_CACHE", "0")
     sizes, n = STRUCTURES[struct]
     p, rng = random_problem(sizes, n, gamma, mu, sum(map(ord, struct)), weighted=True)
     ctx = ctx_of(p)
