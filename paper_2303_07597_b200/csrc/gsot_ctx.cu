@@ -634,9 +634,9 @@ void enqueue_snapshot(gsot_ctx* c, const double* d_x, bool lazy) {  // take_snap
   const DevProblem P = c->problem();
   const double Ln = static_cast<double>(c->L) * c->n;
   unsigned int* list_len = c->snap_cnt;
-  // (instances of short groups only keep the one-kernel form: nothing to list)
-  const bool listed = lazy && c->snap_list != nullptr &&
-                      *std::max_element(c->sizes.begin(), c->sizes.end()) >= gsot::kSnapListMinRows;
+  // (short groups are walked by the marking kernel itself; they still gain its
+  // chunk-level zero test and flags)
+  const bool listed = lazy && c->snap_list != nullptr;
   if (lazy)
     c->launch(K_MISC, 8.0 * c->m, [&] {
       launch_group_amax(P, d_x, c->amax, c->stream, listed ? list_len : nullptr);
