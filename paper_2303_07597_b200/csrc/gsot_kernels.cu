@@ -1006,6 +1006,37 @@ void launch_block_min(const DevProblem& P, float* cmin, cudaStream_t s) {
 
 // amax[l] = max over the group's alpha (a NaN propagates: no block of the
 // group is then provably zero). One warp per group.
+// One stride-S scan of rows [o0, o1) by a thread starting at o0 + first: the
+// maximum of alpha (NaN propagates) and, with xs, the chain of [alpha - alpha~]+^2
+// in row order; eight loads in flight.
+template <int S>
+__device__ __forceinline__ void amax_scan(const double* __restrict__ x, const double* __restrict__ xs,
+                                          int i, int o1, double& v, double& acc) {
+  for (; i + 7 * S < o1; i += 8 * S) {
+    double a[8], b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      a[k] = x[i + S * k];
+      b[k] = xs ? xs[i + S * k] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v = (a[k] > v || a[k] != a[k]) ? a[k] : v;
+      const double d = dsub(a[k], b[k]);
+      if (xs && d > 0.0) acc = dadd(acc, dmul(d, d));
+    }
+  }
+  for (; i < o1; i += S) {
+    const double a = x[i];
+    v = (a > v || a != a) ? a : v;
+    if (xs) {
+      const double d = dsub(a, xs[i]);
+      if (d > 0.0) acc = dadd(acc, dmul(d, d));
+    }
+  }
+}
+
+constexpr int kAmaxTall = 1024;  // taller groups are scanned by the whole CTA
 __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* __restrict__ x,
                                                     double* __restrict__ amax,
                                                     unsigned int* __restrict__ zero_me,
@@ -1013,6 +1044,7 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
                                                     double* __restrict__ dfast,
                                                     const double* __restrict__ dbeta,
                                                     double* __restrict__ dbx3) {
+  __shared__ double sh_v[8], sh_a[8];
   pdl_wait();
   pdl_trigger();
   const int ga = (P.L + 7) / 8;  // CTAs of the group role; the rest: chunk role
@@ -1045,52 +1077,72 @@ __global__ void __launch_bounds__(256) k_group_amax(DevProblem P, const double* 
     }
     return;
   }
-
-  const int lane = threadIdx.x & 31;
-  const int l = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (l >= P.L) return;
-  const int o0 = P.off[l], o1 = P.off[l + 1];
-  double v = -__longlong_as_double(0x7ff0000000000000ll);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double ninf = -__longlong_as_double(0x7ff0000000000000ll);
   // fast solves: the group's |[alpha_l - alpha~_l]+| for the screen (xs: the
-  // snapshot state), lane-strided chains in row order, then a fixed xor tree
-  // -- once per group here instead of once per screen CTA
-  double acc = 0.0;
-  int i = o0 + lane;
-  for (; i + 7 * 32 < o1; i += 8 * 32) {  // eight loads in flight (tall groups)
-    double a[8], b[8];
+  // snapshot state), strided chains in row order, then fixed trees -- once per
+  // group here instead of once per screen CTA. CTA b takes groups b, b + ga,
+  // b + 2 ga, ... (neighbouring groups, often of similar height, go to
+  // different CTAs): a warp per group, but a group taller than kAmaxTall rows
+  // by the CTA's eight warps together (config 4's 4000-row group is otherwise
+  // a 16-round-trip chain for one warp).
+  __shared__ int so0[8], so1[8];
+  if (threadIdx.x < 8) {
+    const int lt = (int)threadIdx.x * ga + (int)blockIdx.x;
+    so0[threadIdx.x] = lt < P.L ? P.off[lt] : 0;
+    so1[threadIdx.x] = lt < P.L ? P.off[lt + 1] : 0;
+  }
+  __syncthreads();
+  {
+    const int l = warp * ga + (int)blockIdx.x;
+    const int o0 = so0[warp], o1 = so1[warp];
+    if (l < P.L && o1 - o0 <= kAmaxTall) {
+      double v = ninf, acc = 0.0;
+      amax_scan<32>(x, xs, o0 + lane, o1, v, acc);
+      if (xs) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      a[k] = x[i + 32 * k];
-      b[k] = xs ? xs[i + 32 * k] : 0.0;
+        for (int o = 16; o >= 1; o >>= 1) acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if (lane == 0) dfast[l] = sqrt(acc);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = (w > v || w != w) ? w : v;
+      }
+      if (lane == 0) {
+        amax[l] = v;
+        if (zero_me) zero_me[l] = 0u;  // the lazy snapshot's list length of the group
+      }
     }
+  }
+  for (int gi = 0; gi < 8; ++gi) {  // the CTA's tall groups, one after the other
+    const int l = gi * ga + (int)blockIdx.x;
+    const int o0 = so0[gi], o1 = so1[gi];
+    if (l >= P.L || o1 - o0 <= kAmaxTall) continue;  // (uniform over the CTA)
+    double v = ninf, acc = 0.0;
+    amax_scan<256>(x, xs, o0 + (int)threadIdx.x, o1, v, acc);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      v = (a[k] > v || a[k] != a[k]) ? a[k] : v;
-      const double d = dsub(a[k], b[k]);
-      if (xs && d > 0.0) acc = dadd(acc, dmul(d, d));
+    for (int o = 16; o >= 1; o >>= 1) {
+      acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      const double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (w > v || w != w) ? w : v;
     }
-  }
-  for (; i < o1; i += 32) {
-    const double a = x[i];
-    v = (a > v || a != a) ? a : v;
-    if (xs) {
-      const double d = dsub(a, xs[i]);
-      if (d > 0.0) acc = dadd(acc, dmul(d, d));
+    if (lane == 0) {
+      sh_v[warp] = v;
+      sh_a[warp] = acc;
     }
-  }
-  if (xs) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc = dadd(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-    if (lane == 0) dfast[l] = sqrt(acc);
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const double w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = (w > v || w != w) ? w : v;
-  }
-  if (lane == 0) {
-    amax[l] = v;
-    if (zero_me) zero_me[l] = 0u;  // the lazy snapshot's list length of the group
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double vv = sh_v[0], aa = sh_a[0];
+      for (int w = 1; w < 8; ++w) {
+        vv = (sh_v[w] > vv || sh_v[w] != sh_v[w]) ? sh_v[w] : vv;
+        aa = dadd(aa, sh_a[w]);
+      }
+      amax[l] = vv;
+      if (xs) dfast[l] = sqrt(aa);
+      if (zero_me) zero_me[l] = 0u;
+    }
+    __syncthreads();
   }
 }
 
