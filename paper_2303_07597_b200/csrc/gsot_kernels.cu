@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) k_snapshot(DevProblem P, const double* __
 // k_snapshot_mark tests every block: a provably-zero one gets z~ = k~ = o~ = 0,
 // the others (about 1 % of them during a solve) are appended to their group's
 // list (one atomic per warp; groups of fewer than kSnapListMinRows rows are
-// walked on the spot: config 4's many short groups measured slower listed). k_snapshot_walk then takes one block per thread
+// walked on the spot). k_snapshot_walk then takes one block per thread
 // from the lists, group by group, so every warp of the sequential walks is
 // full and walks columns of one height (in k_snapshot's lazy form a live lane
 // walks its column while the other lanes of its warp have exited). Each
